@@ -1,0 +1,269 @@
+"""Skeleton computation tree interpreter (ORACLE — test infrastructure only).
+
+The plain definition the method must reproduce is the *sequential,
+single-device, depth-first evaluation of the tree over the whole domain as
+one partition* (§2 "executed sequentially, according to a
+depth-first evaluation of the tree"; §3.1 SPMD model: each
+partition runs the SCT "according to the single device execution model").
+So the oracle never splits: Map's independence is what makes the
+method's splitting legal, and the tests check the method against this
+unsplit evaluation.
+
+Node semantics (DESIGN.md "Readings" R9, R10, R16):
+  Leaf(kind, **params)        a built-in kernel (oracle.kernels)
+  Pipeline(s1..sn)            s1, ..., sn in order; output of s_i is the input
+                              of s_{i+1}
+  Map(t)                      t over the whole domain
+  MapReduce(m, '+')           m per element, then a serial left fold in
+                              Neumaier-compensated fp64
+  LoopFor(b, n)               state_{k+1} = b(state_k), k < n
+  LoopWhileChanged(b, max)    condition before each iteration; stop when the
+                              body changed nothing or max executions reached
+                              (P:221-224); reports executions E
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import kernels as K
+
+# value kinds flowing along tree edges
+SAXPY, RGBA, U8, U8_2D, NBODY, VEC1, VEC2, TERMS, ACCEL, TRAITS = (
+    "saxpy", "rgba", "u8", "u8_2d", "nbody", "vec1", "vec2", "terms", "accel", "traits")
+
+# leaf kind -> (input value kind, output value kind)
+LEAF_SIG = {
+    "saxpy": (SAXPY, SAXPY),
+    "gauss_noise": (RGBA, RGBA),
+    "solarize": (RGBA, RGBA),
+    "mirror": (RGBA, RGBA),
+    "segment": (U8, U8),
+    "hysteresis_finalize": (U8, U8),
+    "hysteresis_step": (U8_2D, U8_2D),
+    "nbody_step": (NBODY, NBODY),
+    "nbody_accel": (NBODY, ACCEL),
+    "map_identity": (VEC1, TERMS),
+    "map_product": (VEC2, TERMS),
+    "debug_traits": (TRAITS, TRAITS),
+}
+
+
+class Node:
+    pass
+
+
+@dataclass
+class Leaf(Node):
+    kind: str
+    params: dict = field(default_factory=dict)
+
+
+@dataclass
+class Pipeline(Node):
+    stages: list
+
+    def __post_init__(self):
+        if len(self.stages) < 2:
+            raise ValueError("Pipeline needs >= 2 stages (SPEC S:68)")
+
+
+@dataclass
+class Map(Node):
+    tree: Node
+
+
+@dataclass
+class MapReduce(Node):
+    map_stage: Node
+    op: str = "+"
+
+
+@dataclass
+class LoopFor(Node):
+    body: Node
+    n: int
+
+
+@dataclass
+class LoopWhileChanged(Node):
+    body: Node
+    max_iters: int
+
+
+@dataclass
+class Result:
+    value: object
+    changed: bool = False          # did the last body change anything
+    executions: int = 0            # while-loop body executions (E)
+    converged: bool = True
+    reduced: float | None = None   # MapReduce fp64 result
+
+
+def _compat(a, b):
+    return a == b or {a, b} == {U8, U8_2D}
+
+
+def sig(node: Node):
+    """(input kind, output kind) of a tree; raises ValueError if ill-typed."""
+    if isinstance(node, Leaf):
+        return LEAF_SIG[node.kind]
+    if isinstance(node, Pipeline):
+        sigs = [sig(s) for s in node.stages]
+        for (_, o), (i, _) in zip(sigs, sigs[1:]):
+            if not _compat(o, i):
+                raise ValueError(f"pipeline stage kinds do not chain: {o} -> {i}")
+        return sigs[0][0], sigs[-1][1]
+    if isinstance(node, Map):
+        return sig(node.tree)
+    if isinstance(node, MapReduce):
+        i, o = sig(node.map_stage)
+        if o != TERMS:
+            raise ValueError("MapReduce map stage must produce terms")
+        return i, "scalar"
+    if isinstance(node, (LoopFor, LoopWhileChanged)):
+        i, o = sig(node.body)
+        if not _compat(i, o):
+            raise ValueError("loop body must preserve its value kind")
+        return i, o
+    raise TypeError(node)
+
+
+def _leaf(node: Leaf, v):
+    p = node.params
+    k = node.kind
+    if k == "saxpy":
+        x, y = v
+        return Result((x, K.saxpy(p["a"], x, y)))
+    if k == "gauss_noise":
+        return Result(K.gauss_noise(v, p["seed"], p["scale"]))
+    if k == "solarize":
+        return Result(K.solarize(v, p["threshold"]))
+    if k == "mirror":
+        return Result(K.mirror(v))
+    if k == "segment":
+        return Result(K.segment(v, p["lo"], p["hi"]))
+    if k == "hysteresis_finalize":
+        return Result(K.hyst_finalize(v))
+    if k == "hysteresis_step":
+        out, changed = K.hyst_step(v)
+        return Result(out, changed=changed)
+    if k == "nbody_step":
+        pos, vel = v
+        po, vo, _ = K.nbody_step(pos, vel, p["eps2"], p["dt"])
+        return Result((po, vo))
+    if k == "nbody_accel":
+        pos = v[0] if isinstance(v, tuple) else v
+        acc, _ = K.nbody_accel(pos, p["eps2"])
+        return Result(acc)
+    if k in ("map_identity", "map_product"):
+        return Result(v)  # terms are formed inside the fold (exact in fp64)
+    if k == "debug_traits":
+        # one partition: SIZE = L, OFFSET = 0 for every element
+        L = int(v)
+        out = np.empty((L, 2), dtype=np.int64)
+        out[:, 0] = L
+        out[:, 1] = 0
+        return Result(out)
+    raise ValueError(k)
+
+
+def evaluate(node: Node, value, while_counts=None) -> Result:
+    """Depth-first evaluation of `node` on `value` (whole domain)."""
+    if isinstance(node, Leaf):
+        return _leaf(node, value)
+    if isinstance(node, Map):
+        return evaluate(node.tree, value)
+    if isinstance(node, Pipeline):
+        r = Result(value)
+        any_changed = False
+        for s in node.stages:
+            r = evaluate(s, r.value)
+            any_changed |= r.changed
+        r.changed = any_changed
+        return r
+    if isinstance(node, MapReduce):
+        if node.op != "+":
+            raise NotImplementedError("merge ops other than + are NEXT-4")
+        m = node.map_stage
+        while isinstance(m, Map):
+            m = m.tree
+        if not isinstance(m, Leaf):
+            raise NotImplementedError("MapReduce map stage must be a map leaf")
+        if m.kind == "map_identity":
+            (x,) = value if isinstance(value, tuple) else (value,)
+            return Result(None, reduced=K.sum_(x))
+        if m.kind == "map_product":
+            x, y = value
+            return Result(None, reduced=K.dot(x, y))
+        raise ValueError(m.kind)
+    if isinstance(node, LoopFor):
+        r = Result(value)
+        for _ in range(node.n):
+            r = evaluate(node.body, r.value)
+        return r
+    if isinstance(node, LoopWhileChanged):
+        changed, e, v = True, 0, value
+        while changed and e < node.max_iters:
+            r = evaluate(node.body, v)
+            v, changed = r.value, r.changed
+            e += 1
+        return Result(v, executions=e, converged=not changed)
+    raise TypeError(node)
+
+
+def leaves(node: Node):
+    """Leaves in depth-first (pre-order) order."""
+    if isinstance(node, Leaf):
+        return [node]
+    if isinstance(node, Pipeline):
+        return [l for s in node.stages for l in leaves(s)]
+    if isinstance(node, Map):
+        return leaves(node.tree)
+    if isinstance(node, MapReduce):
+        return leaves(node.map_stage)
+    return leaves(node.body)
+
+
+def kernel_execution_order(node: Node, while_counts: list[int]) -> list[int]:
+    """Single-device kernel order: leaves numbered in pre-order,
+    loop bodies repeated; while-loops consume `while_counts` in pre-order."""
+    ids = {id(l): i for i, l in enumerate(leaves(node))}
+    counts = list(while_counts)
+    pos = [0]
+
+    def assign(n, table):
+        if isinstance(n, LoopWhileChanged):
+            if pos[0] >= len(counts):
+                raise KeyError("MissingIterationCount")
+            table[id(n)] = counts[pos[0]]
+            pos[0] += 1
+        for c in _children(n):
+            assign(c, table)
+
+    table = {}
+    assign(node, table)
+
+    def walk(n):
+        if isinstance(n, Leaf):
+            return [ids[id(n)]]
+        if isinstance(n, LoopFor):
+            return walk(n.body) * n.n
+        if isinstance(n, LoopWhileChanged):
+            return walk(n.body) * table[id(n)]
+        return [k for c in _children(n) for k in walk(c)]
+
+    return walk(node)
+
+
+def _children(n):
+    if isinstance(n, Leaf):
+        return []
+    if isinstance(n, Pipeline):
+        return list(n.stages)
+    if isinstance(n, Map):
+        return [n.tree]
+    if isinstance(n, MapReduce):
+        return [n.map_stage]
+    return [n.body]

@@ -1,0 +1,608 @@
+#!/usr/bin/env python
+"""Benchmark of the Marrow hot path on B200 (driver contract: one JSON line).
+
+Default workload (BASELINE.json configs[1], the metric's headline config):
+the fused Filter Pipeline (Gaussian noise -> solarize -> mirror) on
+one 8192x8192 RGBA8 image, rows partitioned across the ranks (strong
+scaling).  A step is one run of the whole tree over the image.  Other §8
+rows: --workload saxpy|segmentation|mapreduce_sum|mapreduce_dot|hysteresis|
+nbody|all.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+For N > 1 launch with torchrun (one process per GPU); timing is CUDA events
+on the launching stream, max over ranks.  `--impl reference` times the CPU
+oracle (test infrastructure) as the reference arm on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "elements/s (pixels, particles) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)",
+             "sm_max_mhz": m.get("sm_max_mhz")}
+    return p
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b and b != 0x1]}
+
+
+# ------------------------------------------------------------------ distributed
+class Dist:
+    def __init__(self, gpus):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if gpus != self.world:
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={self.world} (launch N>1 with torchrun)")
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=self.device_obj())
+            self.pg = dist
+
+    def device_obj(self):
+        import torch
+        return torch.device(f"cuda:{self.local}")
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v):
+        if not self.pg:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device=self.device_obj())
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def bcast_bytes(self, b):
+        if not self.pg:
+            return b
+        obj = [b]
+        self.pg.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+
+# ------------------------------------------------------------------ workloads
+class Workload:
+    """One §8 row: builds the tree, allocates this rank's slice (inputs
+    generated on the device, keyed by global index), enqueues one step."""
+    name = ""
+    unit = ""
+    dtype = ""
+    kclass = 0
+    bound = "hbm"
+
+    def __init__(self, M, trees, synth, torch, ctx, dev, rank):
+        self.M, self.trees, self.synth, self.torch = M, trees, synth, torch
+        self.ctx, self.dev, self.rank = ctx, dev, rank
+        self.l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+
+    def sets_for(self, ws_bytes):
+        return max(1, math.ceil(2 * self.l2 / max(1, ws_bytes)))
+
+    def slice(self, L):
+        off, ln = self.M.mw_partition(self.ctx, self.tree, L)
+        return off[self.rank], ln[self.rank]
+
+
+class Filter(Workload):
+    name, unit, dtype = "filter_pipeline_8192x8192_rgba8", "pixels/s", "u8"
+
+    def setup(self, H=8192, W=8192):
+        M, t = self.M, self.torch
+        self.tree = self.trees.filter_pipeline()
+        self.H, self.W = H, W
+        self.kclass = M.MW_KC_RGBA
+        self.o, self.n = self.slice(H)
+        ws = 2 * self.n * W * 4
+        self.B = self.sets_for(ws)
+        self.sets = []
+        for _ in range(self.B):
+            src = t.empty((self.n, W, 4), dtype=t.uint8, device=self.dev)
+            self.synth.dev_fill_rgba(src, self.synth.SEED_IMAGE, self.o * W)
+            dst = t.empty_like(src)
+            self.sets.append((M.arg(src, local_offset=self.o, global_shape=(H, W, 4)),
+                              M.arg(dst, local_offset=self.o, global_shape=(H, W, 4))))
+        self.units = H * W                       # whole-job pixels per step
+        self.launch_bytes = 8 * self.n * W       # algorithmic: read 4 B + write 4 B per pixel
+        self.l2_note = (f"inputs larger than L2 ({ws >> 20} MiB/rank working set)" if self.B == 1 else
+                        f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)")
+
+    def step(self, i):
+        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+
+    def e2e_setup(self):
+        t = self.torch
+        hsrc = t.empty((self.n, self.W, 4), dtype=t.uint8).pin_memory()
+        hsrc.copy_(self.sets[0][0]._owner.cpu())
+        hdst = t.empty_like(hsrc).pin_memory()
+        g = (self.H, self.W, 4)
+        self.e2e_args = [self.M.arg(hsrc, local_offset=self.o, global_shape=g),
+                         self.M.arg(hdst, local_offset=self.o, global_shape=g)]
+        return self.n * self.W * 4, self.n * self.W * 4
+
+    def e2e_step(self):
+        return self.M.mw_run(self.ctx, self.tree, self.e2e_args)
+
+    def config(self):
+        return {"workload": self.name, "image": [self.H, self.W, 4],
+                "tree": "pipeline(gauss_noise(seed=4,S=8), solarize(T=128), mirror)",
+                "rows_per_rank": self.n, "l2": self.l2_note}
+
+
+class Saxpy(Workload):
+    name, unit, dtype = "saxpy_map_2^20_fp32", "elements/s", "f32"
+
+    def setup(self, n=1 << 20):
+        M, t = self.M, self.torch
+        self.tree = self.trees.saxpy()
+        self.kclass = M.MW_KC_SAXPY
+        self.L = n
+        self.o, self.n = self.slice(n)
+        ws = 8 * self.n
+        self.B = self.sets_for(ws)
+        self.sets = []
+        for _ in range(self.B):
+            x = t.empty(self.n, dtype=t.float32, device=self.dev)
+            y = t.empty(self.n, dtype=t.float32, device=self.dev)
+            self.synth.dev_fill_f32_um11(x, self.synth.SEED_SAXPY_X, self.o)
+            self.synth.dev_fill_f32_um11(y, self.synth.SEED_SAXPY_Y, self.o)
+            self.sets.append((M.arg(x, local_offset=self.o, global_shape=(n,)),
+                              M.arg(y, local_offset=self.o, global_shape=(n,))))
+        self.units, self.launch_bytes = n, 12 * self.n
+        self.l2_note = f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)"
+
+    def step(self, i):
+        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+
+    def config(self):
+        return {"workload": self.name, "n": self.L, "a": 2.5, "l2": self.l2_note}
+
+
+class Segmentation(Workload):
+    name, unit, dtype = "segmentation_1024x1024x512_u8", "voxels/s", "u8"
+
+    def setup(self, shape=(512, 1024, 1024)):
+        M, t = self.M, self.torch
+        self.tree = self.trees.segmentation()
+        self.kclass = M.MW_KC_U8
+        self.shape = shape
+        slab = shape[1] * shape[2]
+        self.o, self.n = self.slice(shape[0])
+        ws = 2 * self.n * slab
+        self.B = self.sets_for(ws)
+        self.sets = []
+        for _ in range(self.B):
+            src = t.empty((self.n,) + shape[1:], dtype=t.uint8, device=self.dev)
+            self.synth.dev_fill_u8_stream(src, self.synth.SEED_SEGMENT, self.o * slab)
+            dst = t.empty_like(src)
+            self.sets.append((M.arg(src, local_offset=self.o, global_shape=shape),
+                              M.arg(dst, local_offset=self.o, global_shape=shape)))
+        self.units, self.launch_bytes = shape[0] * slab, 2 * self.n * slab
+        self.l2_note = (f"inputs larger than L2 ({ws >> 20} MiB/rank)" if self.B == 1 else
+                        f"{self.B} rotating buffer sets")
+
+    def step(self, i):
+        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+
+    def config(self):
+        return {"workload": self.name, "shape_zyx": list(self.shape), "lo": 85, "hi": 170,
+                "slabs_per_rank": self.n, "l2": self.l2_note}
+
+
+class MapReduce(Workload):
+    unit, dtype = "elements/s", "f32"
+
+    def __init__(self, *a, dot=True):
+        super().__init__(*a)
+        self.dot = dot
+        self.name = f"mapreduce_{'dot' if dot else 'sum'}_2^30_fp32"
+
+    def setup(self, n=1 << 30):
+        M, t = self.M, self.torch
+        self.tree = self.trees.mapreduce(self.dot)
+        self.kclass = M.MW_KC_REDUCE
+        self.L = n
+        self.o, self.n = self.slice(n)
+        nin = 2 if self.dot else 1
+        ws = 4 * nin * self.n
+        self.B = self.sets_for(ws)
+        self.sets = []
+        for _ in range(self.B):
+            args = []
+            for k, seed in enumerate((self.synth.SEED_MR_X, self.synth.SEED_MR_Y)[:nin]):
+                v = t.empty(self.n, dtype=t.float32, device=self.dev)
+                self.synth.dev_fill_f32_um11(v, seed, self.o)
+                args.append(M.arg(v, local_offset=self.o, global_shape=(n,)))
+            self.sets.append(tuple(args))
+        self.units, self.launch_bytes = n, 4 * nin * self.n
+        self.l2_note = f"inputs larger than L2 ({ws >> 20} MiB/rank)"
+
+    def step(self, i):
+        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+
+    def config(self):
+        return {"workload": self.name, "n": self.L, "merge": "+ (canonical 2^16 chunks, fp64)",
+                "l2": self.l2_note}
+
+
+class Hysteresis(Workload):
+    name, unit, dtype = "hysteresis_16384x16384_u8", "pixels/s", "u8"
+
+    def __init__(self, *a, check_every=1):
+        super().__init__(*a)
+        self.ce = check_every
+
+    def setup(self, H=16384, W=16384):
+        M, t = self.M, self.torch
+        self.tree = self.trees.hysteresis(check_every=self.ce)
+        self.kclass = M.MW_KC_STENCIL
+        self.H, self.W = H, W
+        self.o, self.n = self.slice(H)
+        src = t.empty((self.n, W), dtype=t.uint8, device=self.dev)
+        self.synth.dev_fill_u8_stream(src, self.synth.SEED_HYST, self.o * W)
+        dst = t.empty_like(src)
+        self.sets = [(M.arg(src, local_offset=self.o, global_shape=(H, W)),
+                      M.arg(dst, local_offset=self.o, global_shape=(H, W)))]
+        self.B = 1
+        self.units, self.launch_bytes = H * W, 2 * self.n * W   # per stencil execution
+        self.l2_note = f"ping-pong labels {2 * (self.n + 2) * W >> 20} MiB/rank"
+
+    def step(self, i):
+        return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
+
+    def config(self):
+        return {"workload": self.name, "tree": "pipeline(threshold(173,250), "
+                f"loop_while_changed(step, check_every={self.ce}), finalize)",
+                "rows_per_rank": self.n, "l2": self.l2_note}
+
+
+class NBody(Workload):
+    name, unit, dtype, bound = "nbody_2^20", "bodies/s", "f32", "alu"
+
+    def setup(self, N=1 << 20):
+        M, t = self.M, self.torch
+        self.tree = self.trees.nbody(1)
+        self.kclass = M.MW_KC_NBODY
+        self.N = N
+        self.o, self.n = self.slice(N)
+        pos = t.empty((N, 4), dtype=t.float32, device=self.dev)
+        vel = t.empty((N, 4), dtype=t.float32, device=self.dev)
+        self.synth.dev_fill_nbody(pos, vel, self.synth.SEED_NBODY, 0, 2.0 ** -20)
+        self.sets = [(M.arg(pos, M.MW_COPY), M.arg(vel, M.MW_COPY))]
+        self.B = 1
+        self.units = N
+        self.launch_flops = 20.0 * self.n * N    # GPU Gems convention: 20 flop / interaction
+        self.l2_note = "state 32 MiB (compute bound)"
+
+    def step(self, i):
+        return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
+
+    def config(self):
+        return {"workload": self.name, "bodies": self.N, "eps2": 1e-4, "dt": 1e-3,
+                "bodies_per_rank": self.n, "interactions_per_step": self.N * self.N}
+
+
+WORKLOADS = {"filter": Filter, "saxpy": Saxpy, "segmentation": Segmentation,
+             "mapreduce_sum": lambda *a: MapReduce(*a, dot=False),
+             "mapreduce_dot": lambda *a: MapReduce(*a, dot=True),
+             "hysteresis": Hysteresis, "nbody": NBody}
+
+
+# ------------------------------------------------------------------ oracle legs
+def oracle_filter_rate(budget_s, rows_cap=8192, W=8192):
+    """Oracle (test infrastructure) on bounded row blocks of the config image."""
+    import numpy as np  # noqa: F401
+
+    import synth
+    from oracle import kernels as K
+    rows, px, spent, blocks = 64, 0, 0.0, 0
+    r0 = 0
+    while spent < budget_s:
+        img = synth.host_rgba(synth.SEED_IMAGE, r0 * W, rows * W).reshape(rows, W, 4)
+        t0 = time.perf_counter()
+        K.mirror(K.solarize(K.gauss_noise(img, 4, 8, y0=r0), 128))
+        spent += time.perf_counter() - t0
+        px += rows * W
+        blocks += 1
+        r0 = (r0 + rows) % rows_cap
+    return px / spent, f"{blocks} blocks of {rows}x{W} px rows of the config image", spent
+
+
+def oracle_generic_rate(name, budget_s):
+    """Oracle rate for the other workloads on bounded samples."""
+    import numpy as np
+
+    import synth
+    from oracle import kernels as K
+    spent, units, reps = 0.0, 0, 0
+    while spent < budget_s:
+        if name == "saxpy":
+            n = 1 << 20
+            x, y = synth.host_f32_um11(1, 0, n), synth.host_f32_um11(2, 0, n)
+            t0 = time.perf_counter(); K.saxpy(2.5, x, y); dt = time.perf_counter() - t0
+            what = "whole 2^20 vector"
+        elif name == "segmentation":
+            n = 1 << 24
+            a = synth.host_u8_stream(7, reps * n, n)
+            t0 = time.perf_counter(); K.segment(a, 85, 170); dt = time.perf_counter() - t0
+            what = "16 slabs of 1024x1024"
+        elif name.startswith("mapreduce"):
+            n = 1 << 24
+            x = synth.host_f32_um11(5, reps * n, n)
+            y = synth.host_f32_um11(6, reps * n, n)
+            t0 = time.perf_counter()
+            K.dot(x, y) if name.endswith("dot") else K.sum_(x)
+            dt = time.perf_counter() - t0
+            what = "2^24-element chunks"
+        elif name == "hysteresis":
+            n = 2048
+            g = synth.host_u8_stream(8, 0, n * n).reshape(n, n)
+            t0 = time.perf_counter()
+            L = K.segment(g, 173, 250); f, _ = K.hyst_bfs(L); K.hyst_finalize(f)
+            dt = time.perf_counter() - t0
+            what = "2048x2048 tile (threshold + BFS closed form + finalize)"
+            n = n * n
+        elif name == "nbody":
+            N = 1 << 20
+            pos, _ = synth.host_nbody(9, 0, N, 2.0 ** -20)
+            tg = synth.nbody_sample_indices(N, 64)
+            t0 = time.perf_counter(); K.nbody_accel(pos, 1e-4, targets=tg); dt = time.perf_counter() - t0
+            what = "64 sampled bodies x 2^20 sources (fp64)"
+            n = 64
+        spent += dt
+        units += n if name != "saxpy" else 1 << 20
+        reps += 1
+    return units / spent, f"{reps} x {what}", spent
+
+
+def cpu_rate(name, budget_s):
+    if name.startswith("filter"):
+        return oracle_filter_rate(budget_s)
+    key = {"saxpy_map_2^20_fp32": "saxpy", "segmentation_1024x1024x512_u8": "segmentation",
+           "mapreduce_sum_2^30_fp32": "mapreduce_sum", "mapreduce_dot_2^30_fp32": "mapreduce_dot",
+           "hysteresis_16384x16384_u8": "hysteresis", "nbody_2^20": "nbody"}[name]
+    return oracle_generic_rate(key, budget_s)
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args, dist):
+    """Reference arm: the CPU oracle as it stands, on host cores (rank 0 only)."""
+    if dist.rank != 0:
+        return
+    names = {"filter": ("filter_pipeline_8192x8192_rgba8", "pixels/s", "u8"),
+             "saxpy": ("saxpy_map_2^20_fp32", "elements/s", "f32"),
+             "segmentation": ("segmentation_1024x1024x512_u8", "voxels/s", "u8"),
+             "mapreduce_sum": ("mapreduce_sum_2^30_fp32", "elements/s", "f64"),
+             "mapreduce_dot": ("mapreduce_dot_2^30_fp32", "elements/s", "f64"),
+             "hysteresis": ("hysteresis_16384x16384_u8", "pixels/s", "u8"),
+             "nbody": ("nbody_2^20", "bodies/s", "f64")}
+    wl = args.workload if args.workload != "all" else "filter"
+    name, unit, dtype = names[wl]
+    total_budget = 90.0
+    per_step = total_budget / max(1, args.steps + args.warmup)
+    for _ in range(args.warmup):
+        cpu_rate(name, per_step)
+    rates, spent, sample = [], 0.0, ""
+    for _ in range(args.steps):
+        r, sample, s = cpu_rate(name, per_step)
+        rates.append(r)
+        spent += s
+    value = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * spent / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
+            "data": "synthetic (SplitMix64, seeded; DESIGN.md input recipe)",
+            "config": {"workload": name, "arm": "CPU oracle (oracle/, plain C, 1 thread)"},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "oracle",
+                             "sample": f"per step: {sample}"},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_marrow(args, dist, wl_name):
+    import torch
+
+    import synth
+    from paper_1510_06585_b200 import marrow as M
+    from paper_1510_06585_b200 import trees
+
+    dev = dist.device_obj()
+    torch.cuda.set_device(dev)
+    nccl_id = None
+    if dist.world > 1:
+        nccl_id = dist.bcast_bytes(M.mw_nccl_unique_id() if dist.rank == 0 else None)
+    ctx = M.mw_ctx_create(dist.local, dist.rank, dist.world, 1, nccl_id)
+    w = WORKLOADS[wl_name](M, trees, synth, torch, ctx, dev, dist.rank)
+    w.setup()
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    # warm-up
+    futs = [w.step(i) for i in range(args.warmup)]
+    torch.cuda.synchronize()
+    del futs
+    M.mw_stats_enable(ctx, True)
+    l0 = M.mw_ctx_launch_count(ctx)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dist.local) as clocks:
+        start.record(stream)
+        futs = [w.step(i) for i in range(args.steps)]
+        stop.record(stream)
+        torch.cuda.synchronize()
+    ms_local = start.elapsed_time(stop)
+    launches = M.mw_ctx_launch_count(ctx) - l0
+    res = futs[-1].wait().result()
+    del futs
+    kms, kn = M.mw_kernel_stats(ctx, w.kclass)
+    M.mw_stats_enable(ctx, False)
+    ms = dist.max(ms_local)
+    value = w.units * args.steps / (ms / 1e3)
+    pk = peaks()
+    # roofline of the dominant kernel: algorithmic bytes (flops) per launch / avg launch time
+    avg_launch_s = (kms / max(1, kn)) / 1e3
+    if w.bound == "alu":
+        sm_mhz = pk.get("sm_max_mhz") or 1965.0
+        peak_tf = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FMA lanes x clock
+        launches_per_step = kn / args.steps
+        achieved = w.launch_flops / launches_per_step / max(avg_launch_s, 1e-12) / 1e12 \
+            if launches_per_step else 0.0
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": None,
+                "peak_src": "148 SM x 128 FP32 lanes x 2 flop x max SM clock (guide unit counts)",
+                "kernel": "k_nbody", "flop_per_interaction": 20}
+    else:
+        achieved = w.launch_bytes / max(avg_launch_s, 1e-12) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic_from_profile(wl_name),
+                "peak_src": pk["src"], "kernel_launches": kn,
+                "kernel_avg_us": avg_launch_s * 1e6}
+    line = {"metric": METRIC, "value": value, "unit": w.unit, "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": w.dtype, "data": "synthetic (SplitMix64 seeded, generated on device per rank)",
+            "config": dict(w.config(), parallelism=f"rows/slabs/bodies over {dist.world} GPU(s)",
+                           partitions=dist.world),
+            "roofline": roof, "gpu_launches": launches, "clocks": clocks.summary()}
+    if wl_name == "hysteresis":
+        line["config"]["executions_E"] = res["executions"]
+        line["pixel_executions_per_s"] = value * res["executions"]
+    if wl_name == "nbody":
+        line["interactions_per_s"] = value * w.N
+    # end to end through the C-ABI with HOST buffers (H2D + run + D2H per step)
+    if hasattr(w, "e2e_setup"):
+        h2d, d2h = w.e2e_setup()
+        ek = max(3, min(args.steps, 20))
+        f = w.e2e_step()
+        f.wait()
+        torch.cuda.synchronize()
+        dist.barrier()
+        start.record(stream)
+        futs = [w.e2e_step() for _ in range(ek)]
+        stop.record(stream)
+        torch.cuda.synchronize()
+        del futs
+        ems = dist.max(start.elapsed_time(stop))
+        line["e2e"] = {"value": w.units * ek / (ems / 1e3), "unit": w.unit,
+                       "h2d_bytes_per_step": h2d * dist.world, "d2h_bytes_per_step": d2h * dist.world,
+                       "steps": ek, "path": "mw_run with MW_LOC_HOST pinned buffers (chunked "
+                       "H2D/compute/D2H overlap on 3 streams)"}
+    else:
+        line["e2e"] = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+        rate, sample, spent = cpu_rate(w.name, args.cpu_budget)
+        line["cpu_baseline"] = {"value": rate, "unit": w.unit, "cores": 1, "kind": "oracle",
+                                "sample": sample, "seconds": round(spent, 2)}
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.destroy()
+
+
+def traffic_from_profile(wl_name):
+    """dram bytes (read + write) per launch of the dominant kernel, from the
+    committed `ncu --set full` summary under profiles/ (null if absent)."""
+    path = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(wl_name)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="marrow", choices=["marrow", "reference"])
+    ap.add_argument("--workload", default="filter", choices=list(WORKLOADS) + ["all"])
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    dist = Dist(args.gpus)
+    if args.impl == "reference":
+        if args.steps is None:
+            args.steps = 10
+        run_reference(args, dist)
+        return
+    names = list(WORKLOADS) if args.workload == "all" else [args.workload]
+    default_steps = {"filter": 2000, "saxpy": 5000, "segmentation": 1000, "mapreduce_sum": 300,
+                     "mapreduce_dot": 200, "hysteresis": 20, "nbody": 3}
+    user_steps = args.steps
+    for n in names:
+        args.steps = user_steps or default_steps[n]
+        run_marrow(args, dist, n)
+    if dist.pg:
+        dist.pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

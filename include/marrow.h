@@ -1,0 +1,288 @@
+/*
+ * marrow.h — C-ABI of libmarrow.so, the B200-native hot path of the Marrow
+ * skeleton framework (Soldado, Alexandre, Paulino, arXiv:1510.06585).
+ *
+ * "P:n" cites /root/reference/PAPER.md line n; "S:n" cites SPEC.md line n.
+ * The entry points mirror the paper's constructors and run request (Table 1,
+ * P:181-214): build a skeleton computation tree (SCT) bottom-up from built-in
+ * kernels, set the workload-distribution vector, run it (asynchronously,
+ * returning a future), monitor per-partition times and rebalance.
+ *
+ * Execution model (§3.1 "locality-aware domain decomposition"):
+ * the input domain is split into P = nranks * parts_per_rank contiguous
+ * partitions ("parallel executions" j of P:355-372), one process per GPU
+ * (rank) owning parts_per_rank consecutive partitions; every partition runs
+ * the WHOLE tree on its slice and intermediates stay in device memory.
+ * Inter-partition exchange (hysteresis halos, MapReduce merge, N-body COPY
+ * re-replication, loop-condition reduction) uses device copies inside a rank
+ * and NCCL over NVLink between ranks.
+ *
+ * Conventions for every function:
+ *  - returns MW_OK (0) or an error code; on error, out-params are untouched
+ *    and mw_last_error() holds a message naming the violated rule;
+ *  - no C++ exception crosses this boundary;
+ *  - pointers are borrowed (the caller owns every buffer it passes; device
+ *    buffers must stay valid until the run's future completes);
+ *  - one host thread drives a given mw_ctx.  Node builders touch no
+ *    device and are thread-safe.
+ *  - "collective": every rank must call it, in the same order.
+ */
+#ifndef MARROW_H
+#define MARROW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MW_ABI_VERSION 1
+
+/* ------------------------------------------------------------------ status */
+typedef int32_t mw_status;
+enum {
+    MW_OK = 0,
+    MW_E_INVALID_SPEC = 1,          /* ill-formed tree, params or distribution */
+    MW_E_EPU_NU = 2,                /* epu mod nu != 0            */
+    MW_E_INFEASIBLE_PARTITION = 3,  /* strict divisibility impossible        */
+    MW_E_SHAPE_MISMATCH = 4,        /* args do not match the root's interface*/
+    MW_E_MISSING_ITERATION_COUNT = 5, /* execution order needs a while count  */
+    MW_E_NOT_CONVERGED = 6,         /* while-loop hit max_iters (result still valid) */
+    MW_E_CUDA = 7,
+    MW_E_NCCL = 8,
+    MW_E_STATE = 9,                 /* wrong call order / released handle            */
+    MW_E_OOM = 10,
+    MW_E_UNSUPPORTED = 11,          /* valid SCT outside the built hot path (NEXT-4)  */
+};
+
+const char* mw_status_string(mw_status s);
+/* Last error message of the calling thread (ctx may be NULL). Never NULL.    */
+const char* mw_last_error(const struct mw_ctx* ctx);
+int32_t mw_abi_version(void);
+
+typedef struct mw_ctx mw_ctx;
+typedef struct mw_node mw_node;
+typedef struct mw_future mw_future;
+
+/* ------------------------------------------------------------------ context */
+/* Device memory callbacks (PyTorch's caching allocator in the Python
+ * binding).  alloc returns a device pointer (256-B aligned) or NULL; stream
+ * is the cudaStream_t the memory will be used on.  NULL => cudaMalloc/Free. */
+typedef struct mw_alloc_fns {
+    void* (*alloc)(size_t bytes, void* stream, void* user);
+    void (*free)(void* ptr, void* user);
+    void* user;
+} mw_alloc_fns;
+
+/* NCCL unique id for mw_ctx_create (call on one rank, broadcast the 128 bytes
+ * with torch.distributed).                                                   */
+mw_status mw_nccl_unique_id(uint8_t out[128]);
+
+/* Create a context on CUDA device `device` for rank `rank` of `nranks`
+ * processes, each owning `parts_per_rank` (>= 1) consecutive partitions.
+ * nccl_id: required when nranks > 1 or force_nccl != 0 (then an NCCL
+ * communicator is created — collective), ignored otherwise.  force_nccl
+ * routes even single-rank merges through a 1-rank NCCL communicator.
+ * The initial distribution is uniform over the P partitions (identical
+ * B200s have equal relative performance).                                   */
+mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t parts_per_rank,
+                        const uint8_t* nccl_id, int32_t force_nccl, const mw_alloc_fns* alloc,
+                        mw_ctx** out);
+/* Collective when the ctx owns an NCCL communicator.  Frees all scratch.    */
+mw_status mw_ctx_destroy(mw_ctx* ctx);
+/* Number of partitions P (= nranks * parts_per_rank) and this rank's first. */
+mw_status mw_ctx_info(const mw_ctx* ctx, int32_t* n_parts, int32_t* first_part,
+                      int32_t* parts_per_rank, int32_t* rank, int32_t* nranks);
+
+/* ------------------------------------------------------------------ kernels
+ * Built-in kernel leaves (P:168-178 Kernel objects; the paper's OpenCL
+ * sources become fixed sm_100a kernels).  Each leaf carries its argument
+ * interface (value kind, epu, nu, PARTITION/COPY, Size/Offset traits) and its
+ * scalar parameters.  Definitions: DESIGN.md §Readings (R1-R12).            */
+mw_status mw_kernel_saxpy(float a, mw_node** out);
+/* Gaussian noise (R1): n_c = (popcount((h>>10c)&0x3FF) - 5) * scale,
+ * h = lowbias32(idx ^ lowbias32(seed ^ 0x9E3779B9)), idx = global y*W + x.
+ * scale in [0, 255].                                                         */
+mw_status mw_kernel_gauss_noise(uint32_t seed, int32_t scale, mw_node** out);
+mw_status mw_kernel_solarize(int32_t threshold, mw_node** out);          /* P:725, R2 */
+mw_status mw_kernel_mirror(mw_node** out);
+/* 3-class threshold {0,128,255}, 0 <= lo <= hi <= 256 (R6); also the
+ * hysteresis threshold2d stage.                                              */
+mw_status mw_kernel_segment(int32_t lo, int32_t hi, mw_node** out);
+mw_status mw_kernel_hysteresis_step(mw_node** out);      /* 8-neighbour Jacobi, R11 */
+mw_status mw_kernel_hysteresis_finalize(mw_node** out);  /* 128 -> 0, R11           */
+mw_status mw_kernel_nbody_step(float dt, float eps2, mw_node** out);
+mw_status mw_kernel_nbody_accel(float eps2, mw_node** out);  /* test leaf: a_i only */
+mw_status mw_kernel_map_identity(mw_node** out);         /* MapReduce map stage: x   */
+mw_status mw_kernel_map_product(mw_node** out);          /* MapReduce map stage: x*y */
+/* Test leaf: writes each element's partition (SIZE, OFFSET) trait
+ * values.  epu/nu feed the constraint system;
+ * strict != 0 forbids the L mod granule tail.                                */
+mw_status mw_kernel_debug_traits(int64_t epu, int64_t nu, int32_t strict, mw_node** out);
+
+/* ------------------------------------------------------------------ skeletons
+ * Table 1.  Composites retain their children; trees are
+ * immutable and may be shared across runs and contexts.           */
+mw_status mw_pipeline(mw_node* const* stages, int32_t n, mw_node** out);  /* n >= 2 */
+mw_status mw_map(mw_node* tree, mw_node** out);
+enum { MW_MERGE_ADD = 0 };                    /* P:705-707; SUB/MUL/DIV: NEXT-4 */
+mw_status mw_map_reduce(mw_node* map_stage, int32_t merge_op, mw_node** out);
+mw_status mw_loop_for(mw_node* body, int64_t n, mw_node** out);           /* n >= 0 */
+/* while(changed && executions < max_iters) body.
+ * The stop condition is evaluated on the device and reduced across ranks
+ * every `check_every` (>= 1) executions; extra executions past the fixed
+ * point are no-ops and the reported execution count E is exact.            */
+mw_status mw_loop_while_changed(mw_node* body, int64_t max_iters, int32_t check_every,
+                                mw_node** out);
+void mw_node_retain(mw_node* n);
+void mw_node_release(mw_node* n);
+/* Deterministic content hash (SHA-256 of a canonical serialization): equal
+ * for structurally equal trees, different when any kernel parameter differs
+ * (profile item (a) P:447).                                       */
+mw_status mw_node_id(const mw_node* n, uint8_t out[32]);
+/* Value kinds flowing in/out of a tree (MW_VK_*), see mw_run for the args.  */
+enum {
+    MW_VK_SAXPY = 1, MW_VK_RGBA = 2, MW_VK_U8 = 3, MW_VK_U8_2D = 4, MW_VK_NBODY = 5,
+    MW_VK_VEC1 = 6, MW_VK_VEC2 = 7, MW_VK_TERMS = 8, MW_VK_ACCEL = 9, MW_VK_TRAITS = 10,
+    MW_VK_SCALAR = 11,
+};
+mw_status mw_node_signature(const mw_node* n, int32_t* in_kind, int32_t* out_kind);
+/* Sequential single-device kernel order (depth-first): leaves are
+ * numbered 0.. in pre-order; LoopFor bodies repeat n times; each
+ * LoopWhileChanged node (pre-order) consumes one count from while_counts.
+ * *inout_len: capacity in, length out (MW_E_INVALID_SPEC if too small, with
+ * *inout_len set to the needed length).                                      */
+mw_status mw_kernel_execution_order(const mw_node* root, const int64_t* while_counts,
+                                    int32_t n_counts, int32_t* out_ids, int64_t* inout_len);
+
+/* ------------------------------------------------------------------ partition
+ * Granule g (in units of the partitioned outermost dimension) of a tree:
+ * lcm of every leaf's epu/nu and the alignment unit of its value kind
+ * (R5/R14).                                            */
+mw_status mw_granule(const mw_node* root, int64_t* out);
+/* Pure: largest-remainder apportionment of L units over k fractions with
+ * granule g (R13).  offsets/lengths: k entries each.              */
+mw_status mw_partition_plan(int64_t L, int64_t g, const double* fractions, int32_t k,
+                            int32_t strict, int64_t* offsets, int64_t* lengths);
+/* fractions: P entries, each >= 0, at least one > 0, sum 1 +- 1e-9.         */
+mw_status mw_set_distribution(mw_ctx* ctx, const double* fractions, int32_t n);
+mw_status mw_get_distribution(const mw_ctx* ctx, double* out, int32_t n);
+/* All P partitions of a domain of L outer units for `root` under the ctx's
+ * current distribution — identical on every rank.                           */
+mw_status mw_partition(const mw_ctx* ctx, const mw_node* root, int64_t L, int64_t* offsets,
+                       int64_t* lengths);
+
+/* ------------------------------------------------------------------ run
+ * Buffer argument.  shape is the GLOBAL shape, outermost (partitioned)
+ * dimension first.  A PARTITION buffer on this rank holds global outer rows
+ * [local_offset, local_offset + local_rows) at ptr; it must cover this
+ * rank's partitions (else MW_E_SHAPE_MISMATCH), so both "exactly my slice"
+ * and "the whole array" work.  A COPY buffer holds the whole
+ * array on every rank.  location MW_LOC_HOST: ptr is host memory (pinned for
+ * overlap) — the library stages this rank's slice through device memory with
+ * chunked, multi-stream H2D / compute / D2H overlap (the paper's GPU
+ * "overlap").
+ *
+ * Interfaces by the root's input value kind (mut = written by the run):
+ *   SAXPY        x f32[L], y f32[L] (mut, in place)
+ *   RGBA         src u8[H][W][4], dst u8[H][W][4] (mut)          partition rows
+ *   U8 / U8_2D   src u8[L][...], dst u8 same shape (mut)         outermost dim
+ *   NBODY->NBODY pos f32[N][4] COPY (mut), vel f32[N][4] COPY (mut)  (x,y,z,m)
+ *   NBODY->ACCEL pos f32[N][4] COPY, acc f32[N][4] (mut)
+ *   VEC1 / VEC2  x f32[L] (, y f32[L]); the MapReduce result is in the future
+ *   TRAITS       out i64[L][2] (mut): (SIZE, OFFSET) of each element's partition
+ */
+enum { MW_DT_U8 = 1, MW_DT_F32 = 2, MW_DT_F64 = 3, MW_DT_I64 = 4 };
+enum { MW_PARTITION = 0, MW_COPY = 1 };
+enum { MW_LOC_DEVICE = 0, MW_LOC_HOST = 1 };
+typedef struct mw_arg {
+    void* ptr;
+    int32_t dtype;
+    int32_t ndim;          /* 1..4 */
+    int64_t shape[4];
+    int32_t mode;          /* MW_PARTITION / MW_COPY */
+    int32_t location;      /* MW_LOC_DEVICE / MW_LOC_HOST */
+    int64_t local_offset;  /* PARTITION only */
+    int64_t local_rows;    /* PARTITION only */
+} mw_arg;
+
+/* Enqueue one execution of `root` on the CUDA stream `stream` (cudaStream_t;
+ * NULL = legacy default stream) and return a future.
+ * Runs of one ctx are FIFO (first-come-first-served).  Trees with
+ * a while-loop synchronise the host every check_every executions; all others
+ * return without host synchronisation (device args).  Collective when the
+ * tree exchanges data between ranks (MapReduce, hysteresis, N-body).         */
+mw_status mw_run(mw_ctx* ctx, const mw_node* root, const mw_arg* args, int32_t nargs,
+                 void* stream, mw_future** out);
+mw_status mw_future_wait(mw_future* f);                 /* async CUDA/NCCL errors here */
+mw_status mw_future_query(mw_future* f, int32_t* done);
+/* After wait: out[0] = MapReduce result (fp64), out[1] = its fp32 rounding,
+ * out[2] = while-loop executions E (total over all while loops), out[3] = 1
+ * if every while loop converged else 0.  n <= 4 values are written.         */
+mw_status mw_future_result(mw_future* f, double* out, int32_t n);
+void mw_future_release(mw_future* f);
+
+/* ------------------------------------------------------------------ monitor / balance
+ * Per-partition compute times of the last completed run (events placed
+ * around each partition's kernels, before any collective wait),
+ * for all P partitions (collective when nranks > 1: an all-gather), and the
+ * run's wall time on this rank.  per_part_ms: n >= P floats.                */
+mw_status mw_last_timings(mw_ctx* ctx, float* per_part_ms, int32_t n, float* wall_ms);
+/* Partition lengths (outer units) of the last run, n >= P.                  */
+mw_status mw_last_lengths(const mw_ctx* ctx, int64_t* per_part_len, int32_t n);
+
+/* Kernel statistics.  While enabled (mw_stats_enable(ctx, 1) synchronises
+ * the device and clears them), every partition's kernels of each class are
+ * bracketed by CUDA events on the launching stream and kept; mw_kernel_stats
+ * synchronises and returns the summed event-measured duration (ms) and the
+ * number of kernel launches of that class since enabling.                   */
+enum {
+    MW_KC_SAXPY = 0, MW_KC_RGBA = 1, MW_KC_U8 = 2, MW_KC_STENCIL = 3, MW_KC_NBODY = 4,
+    MW_KC_REDUCE = 5, MW_KC_TRAITS = 6, MW_KC_COUNT = 7
+};
+mw_status mw_stats_enable(mw_ctx* ctx, int32_t on);
+mw_status mw_kernel_stats(mw_ctx* ctx, int32_t kernel_class, double* total_ms, int64_t* launches);
+
+enum { MW_BALANCE_PROPORTIONAL = 0, MW_BALANCE_ABS = 1 };
+typedef struct mw_balance_params {
+    double weight;    /* lbt history weight, default 2/3              */
+    double max_dev;   /* balanced iff dev / c_factor >= max_dev, default 0.85 */
+    double c_factor;  /* correction factor, default 1                 */
+    double trigger;   /* lbt >= trigger starts balancing, default 0.95*/
+    int32_t mode;     /* MW_BALANCE_PROPORTIONAL or MW_BALANCE_ABS (2 parts)  */
+} mw_balance_params;
+typedef struct mw_balance_state {
+    double lbt;
+    int32_t active;
+    int32_t abs_last_dir;
+    double abs_t;
+    int32_t abs_count;
+    int32_t pad;
+    int64_t runs;
+} mw_balance_state;
+void mw_balance_defaults(mw_balance_params* p);
+/* Pure host function: one monitoring step (P:613-638 lbt; P:649-667 ABS;
+ * proportional = P:388's relative-performance rule with measured rates).
+ * Algorithm: DESIGN.md R15-R17.  next: n fractions.                         */
+mw_status mw_balance_step(const mw_balance_params* p, mw_balance_state* inout,
+                          const float* per_part_ms, const int64_t* per_part_len,
+                          const double* cur, int32_t n, double* next, int32_t* triggered);
+/* Convenience (collective): last timings -> mw_balance_step -> set the new
+ * distribution.  The ctx keeps the mw_balance_state.                        */
+mw_status mw_rebalance(mw_ctx* ctx, const mw_balance_params* p, int32_t* triggered);
+mw_status mw_get_balance_state(const mw_ctx* ctx, mw_balance_state* out);
+
+/* Slowdown injector (the analogue of the paper's CPU-load generator,
+ * P:1110-1113): partition `part`'s compute kernels launch on 1/factor of
+ * their usual grid (factor >= 1; 1 = off).  Results are unchanged (every
+ * kernel is a grid-stride loop), only the partition's time grows.          */
+mw_status mw_ctx_set_slowdown(mw_ctx* ctx, int32_t part, float factor);
+
+/* Number of kernels this library launched on the ctx since creation.        */
+mw_status mw_ctx_launch_count(const mw_ctx* ctx, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MARROW_H */

@@ -227,34 +227,35 @@ def leaves(node: Node):
 
 
 def kernel_execution_order(node: Node, while_counts: list[int]) -> list[int]:
-    """Single-device kernel order: leaves numbered in pre-order,
-    loop bodies repeated; while-loops consume `while_counts` in pre-order."""
-    ids = {id(l): i for i, l in enumerate(leaves(node))}
+    """Single-device kernel order: leaf occurrences numbered in
+    pre-order, loop bodies repeated; LoopWhileChanged occurrences (pre-order)
+    consume `while_counts`."""
     counts = list(while_counts)
-    pos = [0]
 
-    def assign(n, table):
-        if isinstance(n, LoopWhileChanged):
-            if pos[0] >= len(counts):
-                raise KeyError("MissingIterationCount")
-            table[id(n)] = counts[pos[0]]
-            pos[0] += 1
-        for c in _children(n):
-            assign(c, table)
+    def nleaves(n):
+        return 1 if isinstance(n, Leaf) else sum(nleaves(c) for c in _children(n))
 
-    table = {}
-    assign(node, table)
+    def nwhile(n):
+        return int(isinstance(n, LoopWhileChanged)) + sum(nwhile(c) for c in _children(n))
 
-    def walk(n):
+    if len(counts) < nwhile(node):
+        raise KeyError("MissingIterationCount")
+
+    def walk(n, lb, wb):
         if isinstance(n, Leaf):
-            return [ids[id(n)]]
+            return [lb]
         if isinstance(n, LoopFor):
-            return walk(n.body) * n.n
+            return walk(n.body, lb, wb) * n.n
         if isinstance(n, LoopWhileChanged):
-            return walk(n.body) * table[id(n)]
-        return [k for c in _children(n) for k in walk(c)]
+            return walk(n.body, lb, wb + 1) * counts[wb]
+        out = []
+        for c in _children(n):
+            out += walk(c, lb, wb)
+            lb += nleaves(c)
+            wb += nwhile(c)
+        return out
 
-    return walk(node)
+    return walk(node, 0, 0)
 
 
 def _children(n):

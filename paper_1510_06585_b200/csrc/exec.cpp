@@ -1,0 +1,1160 @@
+// exec.cpp — contexts, the partitioned executor, futures, monitoring and the
+// NCCL plumbing of libmarrow.
+//
+// The executor realises the paper's SPMD locality-aware decomposition
+// (P:296-338): the domain is cut into P partitions by the distribution vector
+// (R13), every partition runs the whole fused plan on
+// its slice, intermediates stay on the device, and the only data that moves
+// between partitions is what a skeleton requires: hysteresis halo rows
+// (Loop "global synchronization"), MapReduce chunk partials (merge
+// "+"), N-body COPY re-replication and the loop
+// condition.  Inside a rank those are device copies; between ranks
+// they are NCCL collectives over NVLink.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "marrow.h"
+#include "mw_kernels.h"
+#include "sct.h"
+
+namespace mw {
+const char* last_error_cstr();
+}
+
+using mw::fail;
+using mw::Node;
+using mw::Step;
+using mw::StepKind;
+
+#define CUDA_OK(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? MW_E_OOM : MW_E_CUDA,         \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+#define NCCL_OK(expr)                                                                   \
+    do {                                                                                \
+        ncclResult_t r_ = (expr);                                                       \
+        if (r_ != ncclSuccess)                                                          \
+            return fail(MW_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+#define MW_OK_OR_RETURN(expr)          \
+    do {                               \
+        mw_status s_ = (expr);         \
+        if (s_ != MW_OK) return s_;    \
+    } while (0)
+
+namespace {
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+constexpr int kStageSlots = 3;
+
+}  // namespace
+
+struct mw_ctx {
+    int device = 0, rank = 0, nranks = 1, ppr = 1, P = 1;
+    bool use_nccl = false;
+    ncclComm_t comm = nullptr;
+    mw_alloc_fns alloc{};
+    bool has_alloc = false;
+    std::vector<double> dist;
+    std::map<std::string, Buf> scratch;
+    // pinned host memory
+    int32_t* h_flag = nullptr;
+    std::vector<double*> res_free;
+    std::vector<double*> res_pages;
+    // monitoring
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Rec {
+        int part;
+        int cls;
+        cudaEvent_t a, b;
+        int64_t launches;
+    };
+    std::vector<Rec> recs;      // last run (mw_last_timings)
+    bool stats_on = false;
+    std::vector<Rec> stats;     // every run since mw_stats_enable (mw_kernel_stats)
+    cudaEvent_t wall_a = nullptr, wall_b = nullptr;
+    std::vector<int64_t> last_len;
+    bool have_run = false;
+    mw_balance_state bstate{};
+    std::vector<float> slow;
+    unsigned long long launches0 = 0;
+    // host staging (NEXT-1 overlap)
+    cudaStream_t copy_in = nullptr, copy_out = nullptr, aux = nullptr;
+    cudaEvent_t st_in[kStageSlots]{}, st_comp[kStageSlots]{}, st_out[kStageSlots]{};
+    cudaEvent_t st_start = nullptr;
+};
+
+struct mw_future {
+    mw_ctx* ctx = nullptr;
+    cudaEvent_t done = nullptr;
+    double* res = nullptr;     // pinned slot: [reduced]
+    bool has_reduce = false;
+    double executions = 0.0;
+    double converged = 1.0;
+    bool waited = false;
+};
+
+namespace {
+
+// ------------------------------------------------------------ memory
+mw_status ctx_alloc(mw_ctx* c, size_t bytes, cudaStream_t s, void** out) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 256;
+    if (c->has_alloc) {
+        p = c->alloc.alloc(bytes, (void*)s, c->alloc.user);
+        if (!p) return fail(MW_E_OOM, "allocator callback returned NULL for " + std::to_string(bytes) + " bytes");
+    } else {
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess)
+            return fail(MW_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+    return MW_OK;
+}
+void ctx_free(mw_ctx* c, void* p) {
+    if (!p) return;
+    if (c->has_alloc)
+        c->alloc.free(p, c->alloc.user);
+    else
+        cudaFree(p);
+}
+mw_status scratch(mw_ctx* c, const std::string& name, size_t bytes, cudaStream_t s, void** out) {
+    Buf& b = c->scratch[name];
+    if (b.bytes < bytes) {
+        ctx_free(c, b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        MW_OK_OR_RETURN(ctx_alloc(c, bytes, s, &b.p));
+        b.bytes = bytes;
+    }
+    *out = b.p;
+    return MW_OK;
+}
+
+// ------------------------------------------------------------ timing
+cudaEvent_t next_event(mw_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+// Brackets one partition's kernels of one class with CUDA events on the
+// launching stream (monitoring).
+struct PartTimer {
+    mw_ctx* c;
+    cudaStream_t s;
+    int part, cls;
+    cudaEvent_t a;
+    unsigned long long l0;
+    PartTimer(mw_ctx* c_, cudaStream_t s_, int p, int cl) : c(c_), s(s_), part(p), cls(cl) {
+        a = next_event(c);
+        cudaEventRecord(a, s);
+        l0 = mwk::launch_count();
+    }
+    ~PartTimer() {
+        cudaEvent_t b = next_event(c);
+        cudaEventRecord(b, s);
+        mw_ctx::Rec r{part, cls, a, b, (int64_t)(mwk::launch_count() - l0)};
+        c->recs.push_back(r);
+        if (c->stats_on) c->stats.push_back(r);
+    }
+};
+mwk::Launch launch_for(mw_ctx* c, cudaStream_t s, int part) {
+    mwk::Launch L;
+    L.stream = s;
+    L.slow = c->slow[part];
+    return L;
+}
+mw_status kerr(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        return fail(MW_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return MW_OK;
+}
+
+// ------------------------------------------------------------ argument binding
+struct Bound {
+    const mw_arg* a;
+    int64_t row_bytes;  // bytes per outer unit
+};
+int64_t dt_size(int32_t dt) {
+    switch (dt) {
+        case MW_DT_U8: return 1;
+        case MW_DT_F32: return 4;
+        case MW_DT_F64: return 8;
+        case MW_DT_I64: return 8;
+    }
+    return 0;
+}
+mw_status check_arg(const mw_arg& a, int idx, int32_t dtype, int ndim_min, int ndim_max,
+                    int32_t mode, int64_t last_dim /* -1 any */) {
+    std::string pre = "arg " + std::to_string(idx) + ": ";
+    if (!a.ptr && a.shape[0] != 0) return fail(MW_E_SHAPE_MISMATCH, pre + "NULL pointer");
+    if (a.dtype != dtype) return fail(MW_E_SHAPE_MISMATCH, pre + "wrong dtype");
+    if (a.ndim < ndim_min || a.ndim > ndim_max || a.ndim > 4)
+        return fail(MW_E_SHAPE_MISMATCH, pre + "wrong number of dimensions");
+    for (int d = 0; d < a.ndim; ++d)
+        if (a.shape[d] < 0) return fail(MW_E_SHAPE_MISMATCH, pre + "negative extent");
+    if (a.mode != mode)
+        return fail(MW_E_SHAPE_MISMATCH, pre + (mode == MW_COPY ? "must be COPY (P:686-688)"
+                                                                : "must be PARTITION"));
+    if (last_dim >= 0 && a.shape[a.ndim - 1] != last_dim)
+        return fail(MW_E_SHAPE_MISMATCH, pre + "wrong innermost extent");
+    if (a.location != MW_LOC_DEVICE && a.location != MW_LOC_HOST)
+        return fail(MW_E_SHAPE_MISMATCH, pre + "bad location");
+    return MW_OK;
+}
+int64_t row_bytes(const mw_arg& a) {
+    int64_t b = dt_size(a.dtype);
+    for (int d = 1; d < a.ndim; ++d) b *= a.shape[d];
+    return b;
+}
+bool same_shape(const mw_arg& a, const mw_arg& b) {
+    if (a.ndim != b.ndim) return false;
+    for (int d = 0; d < a.ndim; ++d)
+        if (a.shape[d] != b.shape[d]) return false;
+    return true;
+}
+// pointer to global outer row `row` of a PARTITION arg
+template <typename T>
+T* at_row(const mw_arg& a, int64_t row) {
+    return reinterpret_cast<T*>(static_cast<uint8_t*>(a.ptr) + (row - a.local_offset) * row_bytes(a));
+}
+
+// ------------------------------------------------------------ plan helpers
+std::vector<mwk::RgbaProg> rgba_groups(const std::vector<mw::ChainOp>& ops) {
+    // split into launches of <= kMaxOps pointwise ops; mirrors fold into the
+    // source-column parity of their group and the key parity of earlier ops.
+    std::vector<std::vector<mw::ChainOp>> groups(1);
+    int cnt = 0;
+    for (const auto& o : ops) {
+        if (o.kind != mw::LeafKind::Mirror) {
+            if (cnt == mwk::kMaxOps) {
+                groups.emplace_back();
+                cnt = 0;
+            }
+            ++cnt;
+        }
+        groups.back().push_back(o);
+    }
+    std::vector<mwk::RgbaProg> out;
+    for (const auto& g : groups) {
+        mwk::RgbaProg p{};
+        int mirrors_after = 0;
+        for (const auto& o : g)
+            if (o.kind == mw::LeafKind::Mirror) ++mirrors_after;
+        p.mirror = mirrors_after & 1;
+        for (const auto& o : g) {
+            if (o.kind == mw::LeafKind::Mirror) {
+                --mirrors_after;
+                continue;
+            }
+            int k = p.n++;
+            if (o.kind == mw::LeafKind::GaussNoise) {
+                // R1: K = lowbias32(seed ^ 0x9E3779B9)
+                uint32_t v = (uint32_t)o.ia ^ 0x9E3779B9u;
+                v ^= v >> 16; v *= 0x7feb352du; v ^= v >> 15; v *= 0x846ca68bu; v ^= v >> 16;
+                p.kind[k] = mwk::RGBA_NOISE;
+                p.key[k] = v;
+                p.param[k] = (int32_t)o.ib;
+            } else {
+                p.kind[k] = mwk::RGBA_SOLARIZE;
+                p.param[k] = (int32_t)o.ia;
+            }
+            p.key_mirror[k] = mirrors_after & 1;
+        }
+        out.push_back(p);
+    }
+    return out;
+}
+std::vector<mwk::U8Prog> u8_groups(const std::vector<mw::ChainOp>& ops) {
+    std::vector<mwk::U8Prog> out(1);
+    out[0] = mwk::U8Prog{};
+    for (const auto& o : ops) {
+        if (out.back().n == mwk::kMaxOps) out.push_back(mwk::U8Prog{});
+        mwk::U8Prog& p = out.back();
+        int k = p.n++;
+        if (o.kind == mw::LeafKind::Segment) {
+            p.kind[k] = mwk::U8_SEGMENT;
+            p.lo[k] = (int32_t)o.ia;
+            p.hi[k] = (int32_t)o.ib;
+        } else {
+            p.kind[k] = mwk::U8_FINALIZE;
+        }
+    }
+    return out;
+}
+std::vector<mwk::SaxpyProg> saxpy_groups(const std::vector<mw::ChainOp>& ops) {
+    std::vector<mwk::SaxpyProg> out(1);
+    out[0] = mwk::SaxpyProg{};
+    for (const auto& o : ops) {
+        if (out.back().n == mwk::kMaxOps) out.push_back(mwk::SaxpyProg{});
+        out.back().a[out.back().n++] = o.fa;
+    }
+    return out;
+}
+
+// ------------------------------------------------------------ run state
+struct RunCtx {
+    mw_ctx* c;
+    cudaStream_t s;
+    std::vector<int64_t> off, len;  // all P partitions
+    int first;                      // this rank's first partition
+    int owner(int part) const { return part / c->ppr; }
+    bool local(int part) const { return owner(part) == c->rank; }
+};
+
+// Launch a chain of RGBA groups over rows [r0, r0+n): src -> ... -> dst.
+mw_status run_rgba(RunCtx& R, int part, const std::vector<mwk::RgbaProg>& progs,
+                   const uint8_t* src, uint8_t* dst, int64_t rows, int64_t W, int64_t row0,
+                   uint8_t* tmp0, uint8_t* tmp1) {
+    mwk::Launch L = launch_for(R.c, R.s, part);
+    const uint8_t* in = src;
+    for (size_t g = 0; g < progs.size(); ++g) {
+        uint8_t* out = (g + 1 == progs.size()) ? dst : ((g & 1) ? tmp1 : tmp0);
+        MW_OK_OR_RETURN(kerr(mwk::rgba_chain(progs[g], in, out, rows, W, row0, L), "rgba_chain"));
+        in = out;
+    }
+    return MW_OK;
+}
+
+// ------------------------------------------------------------ exchange helpers
+struct Halo {
+    uint8_t* buf[2];  // two ping-pong buffers of (len+2) x pitch, halo row at 0
+};
+
+mw_status exchange_halos(RunCtx& R, std::vector<Halo>& H, int which, int64_t pitch) {
+    mw_ctx* c = R.c;
+    const int P = c->P;
+    std::vector<int> act;
+    for (int p = 0; p < P; ++p)
+        if (R.len[p] > 0) act.push_back(p);
+    bool group = false;
+    for (size_t i = 0; i + 1 < act.size(); ++i) {
+        int a = act[i], b = act[i + 1];
+        bool la = R.local(a), lb = R.local(b);
+        if (!la && !lb) continue;
+        uint8_t* abuf = la ? H[a - R.first].buf[which] : nullptr;
+        uint8_t* bbuf = lb ? H[b - R.first].buf[which] : nullptr;
+        if (la && lb) {
+            // b's top halo <- a's last row; a's bottom halo <- b's first row
+            CUDA_OK(cudaMemcpyAsync(bbuf, abuf + R.len[a] * pitch, pitch, cudaMemcpyDeviceToDevice, R.s));
+            CUDA_OK(cudaMemcpyAsync(abuf + (R.len[a] + 1) * pitch, bbuf + pitch, pitch,
+                                    cudaMemcpyDeviceToDevice, R.s));
+            continue;
+        }
+        if (!c->comm) return fail(MW_E_STATE, "cross-rank halo without an NCCL communicator");
+        if (!group) {
+            NCCL_OK(ncclGroupStart());
+            group = true;
+        }
+        if (la) {
+            int peer = R.owner(b);
+            NCCL_OK(ncclSend(abuf + R.len[a] * pitch, pitch, ncclUint8, peer, c->comm, R.s));
+            NCCL_OK(ncclRecv(abuf + (R.len[a] + 1) * pitch, pitch, ncclUint8, peer, c->comm, R.s));
+        } else {
+            int peer = R.owner(a);
+            NCCL_OK(ncclSend(bbuf + pitch, pitch, ncclUint8, peer, c->comm, R.s));
+            NCCL_OK(ncclRecv(bbuf, pitch, ncclUint8, peer, c->comm, R.s));
+        }
+    }
+    if (group) NCCL_OK(ncclGroupEnd());
+    return MW_OK;
+}
+
+// ------------------------------------------------------------ U8 programs (chains + stencils)
+mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, const mw_arg& dst,
+                 mw_future* f) {
+    mw_ctx* c = R.c;
+    const int ppr = c->ppr;
+    const int64_t inner = row_bytes(src);  // bytes per outer row
+    const bool has_stencil = std::any_of(prog.begin(), prog.end(), [](const Step& s) {
+        return s.kind == StepKind::StencilFor || s.kind == StepKind::StencilWhile;
+    });
+    const int64_t W = inner;               // 2-D when a stencil is present (validated)
+    const int64_t pitch = (W + 15) / 16 * 16;
+    std::vector<Halo> H(ppr);
+    if (has_stencil) {
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            for (int b = 0; b < 2; ++b) {
+                void* ptr;
+                MW_OK_OR_RETURN(scratch(c, "halo" + std::to_string(b) + "_" + std::to_string(q),
+                                        (size_t)(R.len[p] + 2) * pitch, R.s, &ptr));
+                H[q].buf[b] = static_cast<uint8_t*>(ptr);
+                // zero halo rows and pad columns (out-of-image neighbours are 0, R11)
+                CUDA_OK(cudaMemsetAsync(H[q].buf[b], 0, pitch, R.s));
+                CUDA_OK(cudaMemsetAsync(H[q].buf[b] + (R.len[p] + 1) * pitch, 0, pitch, R.s));
+                if (pitch > W)
+                    CUDA_OK(cudaMemset2DAsync(H[q].buf[b] + pitch + W, pitch, 0, pitch - W,
+                                              R.len[p], R.s));
+            }
+        }
+    }
+    // current location of the value, per local partition
+    struct Loc {
+        const uint8_t* p;
+        int64_t pitch;
+        int hb;  // -1: not a halo buffer, else which halo buffer holds it
+    };
+    std::vector<Loc> cur(ppr);
+    for (int q = 0; q < ppr; ++q) {
+        int p = R.first + q;
+        cur[q] = {at_row<const uint8_t>(src, R.off[p]), inner, -1};
+    }
+    int32_t* d_last = nullptr;
+    for (size_t si = 0; si < prog.size(); ++si) {
+        const Step& st = prog[si];
+        const bool last = si + 1 == prog.size();
+        if (st.kind == StepKind::U8) {
+            auto groups = u8_groups(st.ops);
+            const bool next_stencil = !last && (prog[si + 1].kind == StepKind::StencilFor ||
+                                                prog[si + 1].kind == StepKind::StencilWhile);
+            for (int q = 0; q < ppr; ++q) {
+                int p = R.first + q;
+                if (R.len[p] == 0) continue;
+                uint8_t* out;
+                int64_t opitch;
+                int hb = -1;
+                if (last) {
+                    out = at_row<uint8_t>(dst, R.off[p]);
+                    opitch = inner;
+                } else if (next_stencil) {
+                    hb = cur[q].hb == 0 ? 1 : 0;
+                    out = H[q].buf[hb] + pitch;
+                    opitch = pitch;
+                } else {
+                    return fail(MW_E_UNSUPPORTED, "u8 chain followed by a non-stencil step");
+                }
+                PartTimer t(c, R.s, p, MW_KC_U8);
+                mwk::Launch L = launch_for(c, R.s, p);
+                const uint8_t* in = cur[q].p;
+                int64_t ipitch = cur[q].pitch;
+                for (size_t g = 0; g < groups.size(); ++g) {
+                    // multi-group chains (> 16 ops) run in place on the output rows
+                    MW_OK_OR_RETURN(kerr(mwk::u8_chain(groups[g], in, ipitch, out, opitch, R.len[p], W, L),
+                                         "u8_chain"));
+                    in = out;
+                    ipitch = opitch;
+                }
+                cur[q] = {out, opitch, hb};
+            }
+            continue;
+        }
+        // stencil loop
+        const bool is_while = st.kind == StepKind::StencilWhile;
+        if (!d_last) {
+            void* ptr;
+            MW_OK_OR_RETURN(scratch(c, "last_changed", sizeof(int32_t), R.s, &ptr));
+            d_last = static_cast<int32_t*>(ptr);
+        }
+        int hb = 0;
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            if (cur[q].hb < 0)
+                CUDA_OK(cudaMemcpy2DAsync(H[q].buf[0] + pitch, pitch, cur[q].p, cur[q].pitch, W,
+                                          R.len[p], cudaMemcpyDeviceToDevice, R.s));
+            else
+                hb = cur[q].hb;
+        }
+        MW_OK_OR_RETURN(exchange_halos(R, H, hb, pitch));
+        CUDA_OK(cudaMemsetAsync(d_last, 0xFF, sizeof(int32_t), R.s));  // -1
+        const int64_t max_it = st.n;
+        const int64_t ce = is_while ? std::max<int64_t>(1, st.check_every) : max_it;
+        int64_t it = 0;
+        bool converged = !is_while;
+        int64_t E = 0;
+        while (it < max_it) {
+            const int64_t blk = std::min(ce, max_it - it);
+            for (int64_t b = 0; b < blk; ++b, ++it) {
+                for (int q = 0; q < ppr; ++q) {
+                    int p = R.first + q;
+                    if (R.len[p] == 0) continue;
+                    PartTimer t(c, R.s, p, MW_KC_STENCIL);
+                    MW_OK_OR_RETURN(kerr(mwk::hyst_step(H[q].buf[hb], H[q].buf[1 - hb], R.len[p], pitch,
+                                                        (int)it, d_last, launch_for(c, R.s, p)),
+                                         "hyst_step"));
+                }
+                hb = 1 - hb;
+                MW_OK_OR_RETURN(exchange_halos(R, H, hb, pitch));
+            }
+            if (!is_while) continue;
+            // loop condition (P:376 stage 1), reduced over ranks on the device
+            if (c->comm)
+                NCCL_OK(ncclAllReduce(d_last, d_last, 1, ncclInt32, ncclMax, c->comm, R.s));
+            CUDA_OK(cudaMemcpyAsync(c->h_flag, d_last, sizeof(int32_t), cudaMemcpyDeviceToHost, R.s));
+            CUDA_OK(cudaStreamSynchronize(R.s));
+            const int64_t lastc = *c->h_flag;
+            if (lastc < it - 1) {  // iteration it-1 changed nothing: fixed point reached
+                converged = true;
+                E = lastc + 2;
+                break;
+            }
+        }
+        if (is_while) {
+            if (!converged) E = max_it;
+            f->executions += (double)E;
+            if (!converged) f->converged = 0.0;
+        }
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            cur[q] = {H[q].buf[hb] + pitch, pitch, hb};
+        }
+        if (last) {
+            for (int q = 0; q < ppr; ++q) {
+                int p = R.first + q;
+                if (R.len[p] == 0) continue;
+                CUDA_OK(cudaMemcpy2DAsync(at_row<uint8_t>(dst, R.off[p]), inner, cur[q].p, pitch, W,
+                                          R.len[p], cudaMemcpyDeviceToDevice, R.s));
+            }
+        }
+    }
+    if (prog.empty()) {
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            CUDA_OK(cudaMemcpyAsync(at_row<uint8_t>(dst, R.off[p]), cur[q].p, R.len[p] * inner,
+                                    cudaMemcpyDeviceToDevice, R.s));
+        }
+    }
+    return MW_OK;
+}
+
+// ------------------------------------------------------------ N-body
+mw_status allgather_slices(RunCtx& R, float4* buf) {
+    mw_ctx* c = R.c;
+    if (c->nranks == 1) return MW_OK;
+    NCCL_OK(ncclGroupStart());
+    for (int r = 0; r < c->nranks; ++r) {
+        int p0 = r * c->ppr, p1 = p0 + c->ppr - 1;
+        int64_t o = R.off[p0], n = R.off[p1] + R.len[p1] - o;
+        if (n == 0) continue;
+        // allgather-v: one broadcast per root over its contiguous slice (in place)
+        NCCL_OK(ncclBroadcast(buf + o, buf + o, (size_t)n * 4, ncclFloat32, r, c->comm, R.s));
+    }
+    NCCL_OK(ncclGroupEnd());
+    return MW_OK;
+}
+
+mw_status run_nbody(RunCtx& R, const Step& st, const mw_arg& pos, const mw_arg& vel) {
+    mw_ctx* c = R.c;
+    const int64_t N = pos.shape[0];
+    void *p2, *v2;
+    MW_OK_OR_RETURN(scratch(c, "nbody_pos", (size_t)N * 16, R.s, &p2));
+    MW_OK_OR_RETURN(scratch(c, "nbody_vel", (size_t)N * 16, R.s, &v2));
+    float4* P[2] = {static_cast<float4*>(pos.ptr), static_cast<float4*>(p2)};
+    float4* V[2] = {static_cast<float4*>(vel.ptr), static_cast<float4*>(v2)};
+    int cur = 0;
+    for (int64_t it = 0; it < st.n; ++it) {
+        for (int q = 0; q < c->ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            PartTimer t(c, R.s, p, MW_KC_NBODY);
+            MW_OK_OR_RETURN(kerr(mwk::nbody(P[cur], V[cur], P[1 - cur], V[1 - cur], nullptr, R.off[p],
+                                            R.len[p], N, st.eps2, st.dt, 0, launch_for(c, R.s, p)),
+                                 "nbody"));
+        }
+        // Loop state update with global sync: re-replicate
+        MW_OK_OR_RETURN(allgather_slices(R, P[1 - cur]));
+        MW_OK_OR_RETURN(allgather_slices(R, V[1 - cur]));
+        cur = 1 - cur;
+    }
+    if (cur == 1) {
+        CUDA_OK(cudaMemcpyAsync(P[0], P[1], (size_t)N * 16, cudaMemcpyDeviceToDevice, R.s));
+        CUDA_OK(cudaMemcpyAsync(V[0], V[1], (size_t)N * 16, cudaMemcpyDeviceToDevice, R.s));
+    }
+    return MW_OK;
+}
+
+// ------------------------------------------------------------ host-staged chains (NEXT-1)
+mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args) {
+    mw_ctx* c = R.c;
+    const mw_arg& a0 = args[0];
+    const mw_arg& a1 = args[1];
+    const int64_t rb = row_bytes(a0);
+    if (!c->copy_in) {
+        CUDA_OK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+        for (int i = 0; i < kStageSlots; ++i) {
+            CUDA_OK(cudaEventCreateWithFlags(&c->st_in[i], cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&c->st_comp[i], cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&c->st_out[i], cudaEventDisableTiming));
+        }
+        CUDA_OK(cudaEventCreateWithFlags(&c->st_start, cudaEventDisableTiming));
+    }
+    const int64_t chunk_rows = std::max<int64_t>(1, (16ll << 20) / std::max<int64_t>(1, rb));
+    void* slot_in[kStageSlots];
+    void* slot_out[kStageSlots];
+    for (int i = 0; i < kStageSlots; ++i) {
+        MW_OK_OR_RETURN(scratch(c, "stage_in" + std::to_string(i), (size_t)(chunk_rows * rb), R.s, &slot_in[i]));
+        MW_OK_OR_RETURN(scratch(c, "stage_out" + std::to_string(i), (size_t)(chunk_rows * rb), R.s, &slot_out[i]));
+    }
+    const bool a0_host = a0.location == MW_LOC_HOST, a1_host = a1.location == MW_LOC_HOST;
+    CUDA_OK(cudaEventRecord(c->st_start, R.s));
+    CUDA_OK(cudaStreamWaitEvent(c->copy_in, c->st_start, 0));
+    CUDA_OK(cudaStreamWaitEvent(c->copy_out, c->st_start, 0));
+    auto rgba = st.kind == StepKind::Rgba ? rgba_groups(st.ops) : std::vector<mwk::RgbaProg>{};
+    auto u8 = st.kind == StepKind::U8 ? u8_groups(st.ops) : std::vector<mwk::U8Prog>{};
+    auto sx = st.kind == StepKind::Saxpy ? saxpy_groups(st.ops) : std::vector<mwk::SaxpyProg>{};
+    if (st.kind == StepKind::Rgba && rgba.size() > 1)
+        return fail(MW_E_UNSUPPORTED, "host-staged RGBA chains are limited to 16 pointwise ops");
+    int64_t chunk = 0;
+    bool used[kStageSlots] = {false, false, false};
+    for (int q = 0; q < c->ppr; ++q) {
+        int p = R.first + q;
+        for (int64_t r0 = R.off[p]; r0 < R.off[p] + R.len[p]; r0 += chunk_rows, ++chunk) {
+            const int64_t n = std::min(chunk_rows, R.off[p] + R.len[p] - r0);
+            const int sl = (int)(chunk % kStageSlots);
+            if (used[sl]) CUDA_OK(cudaStreamWaitEvent(c->copy_in, c->st_out[sl], 0));
+            used[sl] = true;
+            uint8_t* din = static_cast<uint8_t*>(slot_in[sl]);
+            uint8_t* dout = static_cast<uint8_t*>(slot_out[sl]);
+            // inputs
+            const uint8_t* h0 = at_row<const uint8_t>(a0, r0);
+            const uint8_t* d0 = h0;
+            if (a0_host) {
+                CUDA_OK(cudaMemcpyAsync(din, h0, n * rb, cudaMemcpyHostToDevice, c->copy_in));
+                d0 = din;
+            }
+            uint8_t* d1 = at_row<uint8_t>(a1, r0);
+            if (a1_host) {
+                d1 = dout;
+                if (in_kind == MW_VK_SAXPY)  // y is read and written
+                    CUDA_OK(cudaMemcpyAsync(dout, at_row<const uint8_t>(a1, r0), n * rb,
+                                            cudaMemcpyHostToDevice, c->copy_in));
+            }
+            CUDA_OK(cudaEventRecord(c->st_in[sl], c->copy_in));
+            CUDA_OK(cudaStreamWaitEvent(R.s, c->st_in[sl], 0));
+            {
+                PartTimer t(c, R.s, p, st.kind == StepKind::Rgba ? MW_KC_RGBA : (st.kind == StepKind::U8 ? MW_KC_U8 : MW_KC_SAXPY));
+                mwk::Launch L = launch_for(c, R.s, p);
+                if (st.kind == StepKind::Rgba) {
+                    MW_OK_OR_RETURN(kerr(mwk::rgba_chain(rgba[0], d0, d1, n, a0.shape[1], r0, L), "rgba_chain"));
+                } else if (st.kind == StepKind::U8) {
+                    const uint8_t* in = d0;
+                    for (auto& g : u8) {
+                        MW_OK_OR_RETURN(kerr(mwk::u8_chain(g, in, rb, d1, rb, n, rb, L), "u8_chain"));
+                        in = d1;
+                    }
+                } else {
+                    for (auto& g : sx)
+                        MW_OK_OR_RETURN(kerr(mwk::saxpy_chain(g, reinterpret_cast<const float*>(d0),
+                                                              reinterpret_cast<float*>(d1), n, L),
+                                             "saxpy_chain"));
+                }
+            }
+            CUDA_OK(cudaEventRecord(c->st_comp[sl], R.s));
+            CUDA_OK(cudaStreamWaitEvent(c->copy_out, c->st_comp[sl], 0));
+            if (a1_host)
+                CUDA_OK(cudaMemcpyAsync(at_row<uint8_t>(a1, r0), d1, n * rb, cudaMemcpyDeviceToHost,
+                                        c->copy_out));
+            CUDA_OK(cudaEventRecord(c->st_out[sl], c->copy_out));
+        }
+    }
+    for (int i = 0; i < kStageSlots; ++i)
+        if (used[i]) CUDA_OK(cudaStreamWaitEvent(R.s, c->st_out[i], 0));
+    return MW_OK;
+}
+
+// ------------------------------------------------------------ the run
+mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
+              mw_future* f) {
+    std::vector<Step> prog;
+    MW_OK_OR_RETURN(mw::plan(root, &prog));
+    const int ik = root->in_kind, ok = root->out_kind;
+    // ---- interface (marrow.h, mw_run)
+    int need = (ik == MW_VK_VEC1 || ik == MW_VK_TRAITS) ? 1 : 2;
+    if (nargs != need)
+        return fail(MW_E_SHAPE_MISMATCH, "root expects " + std::to_string(need) + " args, got " +
+                                             std::to_string(nargs));
+    switch (ik) {
+        case MW_VK_SAXPY:
+            MW_OK_OR_RETURN(check_arg(args[0], 0, MW_DT_F32, 1, 1, MW_PARTITION, -1));
+            MW_OK_OR_RETURN(check_arg(args[1], 1, MW_DT_F32, 1, 1, MW_PARTITION, -1));
+            break;
+        case MW_VK_RGBA:
+            MW_OK_OR_RETURN(check_arg(args[0], 0, MW_DT_U8, 3, 3, MW_PARTITION, 4));
+            MW_OK_OR_RETURN(check_arg(args[1], 1, MW_DT_U8, 3, 3, MW_PARTITION, 4));
+            break;
+        case MW_VK_U8:
+        case MW_VK_U8_2D: {
+            int lo = ik == MW_VK_U8_2D ? 2 : 1, hi = ik == MW_VK_U8_2D ? 2 : 4;
+            MW_OK_OR_RETURN(check_arg(args[0], 0, MW_DT_U8, lo, hi, MW_PARTITION, -1));
+            MW_OK_OR_RETURN(check_arg(args[1], 1, MW_DT_U8, lo, hi, MW_PARTITION, -1));
+            break;
+        }
+        case MW_VK_NBODY:
+            MW_OK_OR_RETURN(check_arg(args[0], 0, MW_DT_F32, 2, 2, MW_COPY, 4));
+            if (ok == MW_VK_ACCEL)
+                MW_OK_OR_RETURN(check_arg(args[1], 1, MW_DT_F32, 2, 2, MW_PARTITION, 4));
+            else
+                MW_OK_OR_RETURN(check_arg(args[1], 1, MW_DT_F32, 2, 2, MW_COPY, 4));
+            break;
+        case MW_VK_VEC1:
+        case MW_VK_VEC2:
+            for (int i = 0; i < nargs; ++i)
+                MW_OK_OR_RETURN(check_arg(args[i], i, MW_DT_F32, 1, 1, MW_PARTITION, -1));
+            break;
+        case MW_VK_TRAITS:
+            MW_OK_OR_RETURN(check_arg(args[0], 0, MW_DT_I64, 2, 2, MW_PARTITION, 2));
+            break;
+        default: return fail(MW_E_UNSUPPORTED, "root value kind cannot be run");
+    }
+    if (nargs == 2 && !same_shape(args[0], args[1]))
+        return fail(MW_E_SHAPE_MISMATCH, "args 0 and 1 must have the same global shape");
+    const int64_t L = args[0].shape[0];
+    // ---- partition (identical on every rank)
+    mw_status st;
+    const int64_t g = mw::granule_of(root, &st);
+    if (st) return st;
+    RunCtx R{c, s, std::vector<int64_t>(c->P), std::vector<int64_t>(c->P), c->rank * c->ppr};
+    MW_OK_OR_RETURN(mw::partition_plan(L, g, c->dist.data(), c->P, mw::strict_of(root), R.off.data(),
+                                       R.len.data()));
+    const int plast = R.first + c->ppr - 1;
+    const int64_t s0 = R.off[R.first], s1 = R.off[plast] + R.len[plast];
+    bool host = false;
+    for (int i = 0; i < nargs; ++i) {
+        const mw_arg& a = args[i];
+        host |= a.location == MW_LOC_HOST;
+        if (a.mode == MW_PARTITION && s1 > s0 &&
+            (a.local_offset > s0 || a.local_offset + a.local_rows < s1 || a.local_rows < 0))
+            return fail(MW_E_SHAPE_MISMATCH,
+                        "arg " + std::to_string(i) + " holds rows [" + std::to_string(a.local_offset) +
+                            "," + std::to_string(a.local_offset + a.local_rows) +
+                            ") but this rank's partitions need [" + std::to_string(s0) + "," +
+                            std::to_string(s1) + ")");
+    }
+    if (nargs == 2 && ik != MW_VK_SAXPY && ik != MW_VK_VEC2 && args[0].ptr == args[1].ptr &&
+        args[0].ptr && args[0].location == args[1].location)
+        return fail(MW_E_SHAPE_MISMATCH, "src and dst must not alias");
+    // ---- execute
+    c->recs.clear();
+    if (!c->stats_on) c->ev_used = 0;   // events of accumulated stats stay live
+    CUDA_OK(cudaEventRecord(c->wall_a, s));
+    const int ppr = c->ppr;
+    if (host) {
+        if (prog.size() != 1 || (prog[0].kind != StepKind::Saxpy && prog[0].kind != StepKind::Rgba &&
+                                 prog[0].kind != StepKind::U8))
+            return fail(MW_E_UNSUPPORTED,
+                        "host-resident arguments are supported for single fused Map/Pipeline "
+                        "chains (NEXT-1)");
+        MW_OK_OR_RETURN(run_staged(R, prog[0], ik, args));
+    } else if (ik == MW_VK_SAXPY) {
+        auto groups = prog.empty() ? std::vector<mwk::SaxpyProg>{} : saxpy_groups(prog[0].ops);
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            PartTimer t(c, s, p, MW_KC_SAXPY);
+            for (auto& gp : groups)
+                MW_OK_OR_RETURN(kerr(mwk::saxpy_chain(gp, at_row<const float>(args[0], R.off[p]),
+                                                      at_row<float>(args[1], R.off[p]), R.len[p],
+                                                      launch_for(c, s, p)),
+                                     "saxpy_chain"));
+        }
+    } else if (ik == MW_VK_RGBA) {
+        auto groups = rgba_groups(prog.empty() ? std::vector<mw::ChainOp>{} : prog[0].ops);
+        const int64_t W = args[0].shape[1];
+        uint8_t *t0 = nullptr, *t1 = nullptr;
+        if (groups.size() > 1) {
+            int64_t mx = 0;
+            for (int q = 0; q < ppr; ++q) mx = std::max(mx, R.len[R.first + q]);
+            void *a, *b;
+            MW_OK_OR_RETURN(scratch(c, "rgba_tmp0", (size_t)(mx * W * 4), s, &a));
+            MW_OK_OR_RETURN(scratch(c, "rgba_tmp1", (size_t)(mx * W * 4), s, &b));
+            t0 = static_cast<uint8_t*>(a);
+            t1 = static_cast<uint8_t*>(b);
+        }
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            PartTimer t(c, s, p, MW_KC_RGBA);
+            MW_OK_OR_RETURN(run_rgba(R, p, groups, at_row<const uint8_t>(args[0], R.off[p]),
+                                     at_row<uint8_t>(args[1], R.off[p]), R.len[p], W, R.off[p], t0, t1));
+        }
+    } else if (ik == MW_VK_U8 || ik == MW_VK_U8_2D) {
+        MW_OK_OR_RETURN(run_u8(R, prog, args[0], args[1], f));
+    } else if (ik == MW_VK_NBODY && ok == MW_VK_NBODY) {
+        if (args[0].ptr == args[1].ptr) return fail(MW_E_SHAPE_MISMATCH, "pos and vel alias");
+        if (!prog.empty()) MW_OK_OR_RETURN(run_nbody(R, prog[0], args[0], args[1]));
+    } else if (ik == MW_VK_NBODY) {
+        const Step& stp = prog[0];
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            PartTimer t(c, s, p, MW_KC_NBODY);
+            MW_OK_OR_RETURN(kerr(mwk::nbody(static_cast<const float4*>(args[0].ptr), nullptr, nullptr,
+                                            nullptr, at_row<float4>(args[1], R.off[p]), R.off[p],
+                                            R.len[p], L, stp.eps2, 0.f, 1, launch_for(c, s, p)),
+                                 "nbody_accel"));
+        }
+    } else if (ik == MW_VK_VEC1 || ik == MW_VK_VEC2) {
+        const int64_t CH = 1ll << mwk::kChunkLog2;
+        const int64_t nch = (L + CH - 1) / CH;
+        void *pp, *rp;
+        MW_OK_OR_RETURN(scratch(c, "partials", (size_t)std::max<int64_t>(1, nch) * 8, s, &pp));
+        MW_OK_OR_RETURN(scratch(c, "result", 8, s, &rp));
+        double* partials = static_cast<double*>(pp);
+        CUDA_OK(cudaMemsetAsync(partials, 0, (size_t)std::max<int64_t>(1, nch) * 8, s));
+        const bool dot = prog[0].dot;
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            PartTimer t(c, s, p, MW_KC_REDUCE);
+            MW_OK_OR_RETURN(kerr(mwk::reduce_chunks(at_row<const float>(args[0], R.off[p]),
+                                                    dot ? at_row<const float>(args[1], R.off[p]) : nullptr,
+                                                    R.off[p], R.off[p], R.len[p], L, partials,
+                                                    launch_for(c, s, p)),
+                                 "reduce_chunks"));
+        }
+        // merge "+" across ranks: each chunk partial has exactly
+        // one non-zero contributor, so the sum is exact and order-free.
+        if (c->comm && nch > 0)
+            NCCL_OK(ncclAllReduce(partials, partials, (size_t)nch, ncclFloat64, ncclSum, c->comm, s));
+        MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s), "reduce_combine"));
+        CUDA_OK(cudaMemcpyAsync(f->res, rp, 8, cudaMemcpyDeviceToHost, s));
+        f->has_reduce = true;
+    } else if (ik == MW_VK_TRAITS) {
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            PartTimer t(c, s, p, MW_KC_TRAITS);
+            MW_OK_OR_RETURN(kerr(mwk::fill_traits(at_row<int64_t>(args[0], R.off[p]), R.len[p], R.len[p],
+                                                  R.off[p], launch_for(c, s, p)),
+                                 "fill_traits"));
+        }
+    }
+    CUDA_OK(cudaEventRecord(c->wall_b, s));
+    c->last_len = R.len;
+    c->have_run = true;
+    return MW_OK;
+}
+
+}  // namespace
+
+// ============================================================ C-ABI
+extern "C" {
+
+const char* mw_last_error(const mw_ctx*) { return mw::last_error_cstr(); }
+
+mw_status mw_nccl_unique_id(uint8_t out[128]) {
+    if (!out) return fail(MW_E_INVALID_SPEC, "NULL output");
+    ncclUniqueId id;
+    NCCL_OK(ncclGetUniqueId(&id));
+    static_assert(sizeof(id.internal) == 128, "NCCL unique id size");
+    memcpy(out, id.internal, 128);
+    return MW_OK;
+}
+
+mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t parts_per_rank,
+                        const uint8_t* nccl_id, int32_t force_nccl, const mw_alloc_fns* alloc,
+                        mw_ctx** out) {
+    if (!out) return fail(MW_E_INVALID_SPEC, "out is NULL");
+    if (nranks < 1 || rank < 0 || rank >= nranks || parts_per_rank < 1)
+        return fail(MW_E_INVALID_SPEC, "need 0 <= rank < nranks and parts_per_rank >= 1");
+    const bool use_nccl = nranks > 1 || force_nccl;
+    if (use_nccl && !nccl_id) return fail(MW_E_INVALID_SPEC, "NCCL id required");
+    if (alloc && (!alloc->alloc || !alloc->free))
+        return fail(MW_E_INVALID_SPEC, "allocator needs both alloc and free");
+    CUDA_OK(cudaSetDevice(device));
+    std::unique_ptr<mw_ctx> c(new mw_ctx);
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->ppr = parts_per_rank;
+    c->P = nranks * parts_per_rank;
+    c->dist.assign(c->P, 1.0 / c->P);
+    c->slow.assign(c->P, 1.0f);
+    if (alloc) {
+        c->alloc = *alloc;
+        c->has_alloc = true;
+    }
+    CUDA_OK(cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault));
+    CUDA_OK(cudaEventCreate(&c->wall_a));
+    CUDA_OK(cudaEventCreate(&c->wall_b));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    c->launches0 = mwk::launch_count();
+    c->bstate = mw_balance_state{};
+    if (use_nccl) {
+        ncclUniqueId id;
+        memcpy(id.internal, nccl_id, 128);
+        NCCL_OK(ncclCommInitRank(&c->comm, nranks, id, rank));
+        c->use_nccl = true;
+    }
+    *out = c.release();
+    return MW_OK;
+}
+
+mw_status mw_ctx_destroy(mw_ctx* c) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : c->scratch) ctx_free(c, kv.second.p);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->wall_a) cudaEventDestroy(c->wall_a);
+    if (c->wall_b) cudaEventDestroy(c->wall_b);
+    for (int i = 0; i < kStageSlots; ++i) {
+        if (c->st_in[i]) cudaEventDestroy(c->st_in[i]);
+        if (c->st_comp[i]) cudaEventDestroy(c->st_comp[i]);
+        if (c->st_out[i]) cudaEventDestroy(c->st_out[i]);
+    }
+    if (c->st_start) cudaEventDestroy(c->st_start);
+    if (c->copy_in) cudaStreamDestroy(c->copy_in);
+    if (c->copy_out) cudaStreamDestroy(c->copy_out);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->h_flag) cudaFreeHost(c->h_flag);
+    for (double* p : c->res_pages) cudaFreeHost(p);
+    delete c;
+    return MW_OK;
+}
+
+mw_status mw_ctx_info(const mw_ctx* c, int32_t* n_parts, int32_t* first_part, int32_t* ppr,
+                      int32_t* rank, int32_t* nranks) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    if (n_parts) *n_parts = c->P;
+    if (first_part) *first_part = c->rank * c->ppr;
+    if (ppr) *ppr = c->ppr;
+    if (rank) *rank = c->rank;
+    if (nranks) *nranks = c->nranks;
+    return MW_OK;
+}
+
+mw_status mw_set_distribution(mw_ctx* c, const double* fractions, int32_t n) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    if (n != c->P) return fail(MW_E_INVALID_SPEC, "distribution needs one fraction per partition");
+    MW_OK_OR_RETURN(mw::check_distribution(fractions, n));
+    c->dist.assign(fractions, fractions + n);
+    return MW_OK;
+}
+
+mw_status mw_get_distribution(const mw_ctx* c, double* out, int32_t n) {
+    if (!c || !out) return fail(MW_E_STATE, "NULL argument");
+    if (n < c->P) return fail(MW_E_INVALID_SPEC, "output too small");
+    for (int i = 0; i < c->P; ++i) out[i] = c->dist[i];
+    return MW_OK;
+}
+
+mw_status mw_partition(const mw_ctx* c, const mw_node* root, int64_t L, int64_t* offsets,
+                       int64_t* lengths) {
+    if (!c || !root || !offsets || !lengths) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    mw_status st;
+    const Node* r = reinterpret_cast<const Node*>(root);
+    int64_t g = mw::granule_of(r, &st);
+    if (st) return st;
+    std::vector<int64_t> o(c->P), l(c->P);
+    MW_OK_OR_RETURN(mw::partition_plan(L, g, c->dist.data(), c->P, mw::strict_of(r), o.data(), l.data()));
+    for (int i = 0; i < c->P; ++i) {
+        offsets[i] = o[i];
+        lengths[i] = l[i];
+    }
+    return MW_OK;
+}
+
+mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs, void* stream,
+                 mw_future** out) {
+    if (!c || !root || !out || (nargs > 0 && !args)) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    CUDA_OK(cudaSetDevice(c->device));
+    std::unique_ptr<mw_future> f(new mw_future);
+    f->ctx = c;
+    if (c->res_free.empty()) {
+        double* page;
+        CUDA_OK(cudaHostAlloc(&page, 4096, cudaHostAllocDefault));
+        c->res_pages.push_back(page);
+        for (int i = 0; i < 512; ++i) c->res_free.push_back(page + i);
+    }
+    f->res = c->res_free.back();
+    c->res_free.pop_back();
+    *f->res = 0.0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    mw_status st;
+    try {
+        st = run(c, reinterpret_cast<const Node*>(root), args, nargs, s, f.get());
+    } catch (const std::bad_alloc&) {
+        st = fail(MW_E_OOM, "host allocation failed");
+    } catch (...) {
+        st = fail(MW_E_INVALID_SPEC, "internal error");
+    }
+    if (st != MW_OK) {
+        c->res_free.push_back(f->res);
+        return st;
+    }
+    cudaError_t e = cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(f->done, s);
+    if (e != cudaSuccess) {
+        c->res_free.push_back(f->res);
+        if (f->done) cudaEventDestroy(f->done);
+        return fail(MW_E_CUDA, std::string("future event: ") + cudaGetErrorString(e));
+    }
+    *out = f.release();
+    return MW_OK;
+}
+
+mw_status mw_future_wait(mw_future* f) {
+    if (!f || !f->done) return fail(MW_E_STATE, "invalid future");
+    cudaError_t e = cudaEventSynchronize(f->done);
+    if (e != cudaSuccess) return fail(MW_E_CUDA, std::string("run failed: ") + cudaGetErrorString(e));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MW_E_CUDA, std::string("run failed: ") + cudaGetErrorString(e));
+    if (f->ctx->comm) {
+        ncclResult_t r = ncclSuccess;
+        ncclCommGetAsyncError(f->ctx->comm, &r);
+        if (r != ncclSuccess) return fail(MW_E_NCCL, std::string("NCCL: ") + ncclGetErrorString(r));
+    }
+    f->waited = true;
+    return MW_OK;
+}
+
+mw_status mw_future_query(mw_future* f, int32_t* done) {
+    if (!f || !f->done || !done) return fail(MW_E_STATE, "invalid future");
+    cudaError_t e = cudaEventQuery(f->done);
+    if (e == cudaErrorNotReady) {
+        *done = 0;
+        return MW_OK;
+    }
+    if (e != cudaSuccess) return fail(MW_E_CUDA, std::string("run failed: ") + cudaGetErrorString(e));
+    *done = 1;
+    return MW_OK;
+}
+
+mw_status mw_future_result(mw_future* f, double* out, int32_t n) {
+    if (!f || !out) return fail(MW_E_STATE, "invalid future");
+    if (!f->waited) MW_OK_OR_RETURN(mw_future_wait(f));
+    double v[4] = {f->has_reduce ? *f->res : 0.0, (double)(float)(f->has_reduce ? *f->res : 0.0),
+                   f->executions, f->converged};
+    for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
+    return MW_OK;
+}
+
+void mw_future_release(mw_future* f) {
+    if (!f) return;
+    if (f->done) {
+        cudaEventSynchronize(f->done);
+        cudaEventDestroy(f->done);
+    }
+    if (f->res) f->ctx->res_free.push_back(f->res);
+    delete f;
+}
+
+mw_status mw_last_timings(mw_ctx* c, float* per_part_ms, int32_t n, float* wall_ms) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    if (!c->have_run) return fail(MW_E_STATE, "no run yet");
+    if (per_part_ms && n < c->P) return fail(MW_E_INVALID_SPEC, "output too small");
+    CUDA_OK(cudaSetDevice(c->device));
+    CUDA_OK(cudaEventSynchronize(c->wall_b));
+    std::vector<float> local(c->ppr, 0.0f);
+    for (auto& r : c->recs) {
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
+        local[r.part - c->rank * c->ppr] += ms;
+    }
+    std::vector<float> all(c->P, 0.0f);
+    if (c->nranks > 1) {
+        void* d;
+        MW_OK_OR_RETURN(scratch(c, "timings", (size_t)c->P * 4, c->aux, &d));
+        float* df = static_cast<float*>(d);
+        CUDA_OK(cudaMemcpyAsync(df + c->rank * c->ppr, local.data(), c->ppr * 4, cudaMemcpyHostToDevice, c->aux));
+        NCCL_OK(ncclAllGather(df + c->rank * c->ppr, df, (size_t)c->ppr, ncclFloat32, c->comm, c->aux));
+        CUDA_OK(cudaMemcpyAsync(all.data(), df, c->P * 4, cudaMemcpyDeviceToHost, c->aux));
+        CUDA_OK(cudaStreamSynchronize(c->aux));
+    } else {
+        all = local;
+    }
+    if (per_part_ms)
+        for (int i = 0; i < c->P; ++i) per_part_ms[i] = all[i];
+    if (wall_ms) CUDA_OK(cudaEventElapsedTime(wall_ms, c->wall_a, c->wall_b));
+    return MW_OK;
+}
+
+mw_status mw_stats_enable(mw_ctx* c, int32_t on) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    CUDA_OK(cudaSetDevice(c->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    c->stats.clear();
+    c->recs.clear();
+    c->have_run = false;
+    c->ev_used = 0;
+    c->stats_on = on != 0;
+    return MW_OK;
+}
+
+mw_status mw_kernel_stats(mw_ctx* c, int32_t kernel_class, double* total_ms, int64_t* launches) {
+    if (!c || !total_ms || !launches) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    if (kernel_class < 0 || kernel_class >= MW_KC_COUNT) return fail(MW_E_INVALID_SPEC, "bad kernel class");
+    CUDA_OK(cudaSetDevice(c->device));
+    double tot = 0.0;
+    int64_t n = 0;
+    for (auto& r : c->stats) {
+        if (r.cls != kernel_class) continue;
+        CUDA_OK(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
+        tot += ms;
+        n += r.launches;
+    }
+    *total_ms = tot;
+    *launches = n;
+    return MW_OK;
+}
+
+mw_status mw_last_lengths(const mw_ctx* c, int64_t* per_part_len, int32_t n) {
+    if (!c || !per_part_len) return fail(MW_E_STATE, "NULL argument");
+    if (!c->have_run) return fail(MW_E_STATE, "no run yet");
+    if (n < c->P) return fail(MW_E_INVALID_SPEC, "output too small");
+    for (int i = 0; i < c->P; ++i) per_part_len[i] = c->last_len[i];
+    return MW_OK;
+}
+
+mw_status mw_rebalance(mw_ctx* c, const mw_balance_params* p, int32_t* triggered) {
+    if (!c || !p) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    std::vector<float> ms(c->P);
+    MW_OK_OR_RETURN(mw_last_timings(c, ms.data(), c->P, nullptr));
+    std::vector<double> next(c->P);
+    int trig = 0;
+    MW_OK_OR_RETURN(mw::balance_step(*p, c->bstate, ms.data(), c->last_len.data(), c->dist.data(), c->P,
+                                     next.data(), &trig));
+    if (trig) MW_OK_OR_RETURN(mw_set_distribution(c, next.data(), c->P));
+    if (triggered) *triggered = trig;
+    return MW_OK;
+}
+
+mw_status mw_get_balance_state(const mw_ctx* c, mw_balance_state* out) {
+    if (!c || !out) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    *out = c->bstate;
+    return MW_OK;
+}
+
+mw_status mw_ctx_set_slowdown(mw_ctx* c, int32_t part, float factor) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    if (part < 0 || part >= c->P || !(factor >= 1.0f))
+        return fail(MW_E_INVALID_SPEC, "bad partition or factor < 1");
+    c->slow[part] = factor;
+    return MW_OK;
+}
+
+mw_status mw_ctx_launch_count(const mw_ctx* c, int64_t* out) {
+    if (!c || !out) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    *out = (int64_t)(mwk::launch_count() - c->launches0);
+    return MW_OK;
+}
+
+}  // extern "C"

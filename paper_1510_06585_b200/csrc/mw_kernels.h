@@ -1,0 +1,87 @@
+// mw_kernels.h — internal launcher interface between the host runtime
+// (runtime.cpp) and the sm_100a kernels (kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mwk {
+
+constexpr int kMaxOps = 16;
+
+// Launch geometry shared by every launcher: grid-stride kernels take a grid
+// of min(work, SMs * resident CTAs); the slowdown injector divides that grid
+// by `slow` (>= 1), which changes the speed but never the result.
+struct Launch {
+    cudaStream_t stream;
+    float slow;     // 1 = full speed
+};
+
+// ------------------------------------------------------------ fused Map chains
+// Saxpy chain: y <- fma(a_k, x, y) for k = 0..n-1, in place.
+struct SaxpyProg {
+    int n;
+    float a[kMaxOps];
+};
+cudaError_t saxpy_chain(const SaxpyProg& p, const float* x, float* y, int64_t n, const Launch& L);
+
+// RGBA8 chain: pointwise noise/solarize ops with every mirror
+// folded into a source-column parity; key_mirror[k] says whether op k (a noise
+// stage) runs at the mirrored column of the output pixel.
+enum RgbaOpKind : int32_t { RGBA_NOISE = 0, RGBA_SOLARIZE = 1 };
+struct RgbaProg {
+    int n;
+    int mirror;                     // odd number of mirrors in the chain
+    int32_t kind[kMaxOps];
+    uint32_t key[kMaxOps];          // NOISE: K = lowbias32(seed ^ 0x9E3779B9)
+    int32_t param[kMaxOps];         // NOISE: scale S in [0,255]; SOLARIZE: T
+    int32_t key_mirror[kMaxOps];
+};
+// rows x W pixels; row r of the partition is global row row0 + r.
+cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int64_t rows,
+                       int64_t W, int64_t row0, const Launch& L);
+
+// u8 chain: SEGMENT(lo,hi) / FINALIZE(128->0), rows of W bytes with pitches.
+enum U8OpKind : int32_t { U8_SEGMENT = 0, U8_FINALIZE = 1 };
+struct U8Prog {
+    int n;
+    int32_t kind[kMaxOps];
+    int32_t lo[kMaxOps];
+    int32_t hi[kMaxOps];
+};
+cudaError_t u8_chain(const U8Prog& p, const uint8_t* src, int64_t src_pitch, uint8_t* dst,
+                     int64_t dst_pitch, int64_t rows, int64_t W, const Launch& L);
+
+// ------------------------------------------------------------ hysteresis stencil
+// One Jacobi step over `rows` interior rows.  in/out point at halo row -1 of
+// buffers of (rows + 2) x pitch bytes (pitch % 16 == 0, pad columns zero).
+// Any changed pixel does atomicMax(last_changed, iter).
+cudaError_t hyst_step(const uint8_t* in, uint8_t* out, int64_t rows, int64_t pitch, int iter,
+                      int* last_changed, const Launch& L);
+
+// ------------------------------------------------------------ N-body
+// Bodies [first, first+count) of N: direct-sum acceleration (fp32 per
+// 256-source tile, fp64 across tiles).  mode 0: symplectic Euler step into
+// pos_out/vel_out (same global indexing); mode 1: write a_i (fp32) to acc.
+cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4* vel_out,
+                  float4* acc, int64_t first, int64_t count, int64_t N, float eps2, float dt,
+                  int mode, const Launch& L);
+
+// ------------------------------------------------------------ MapReduce
+constexpr int kChunkLog2 = 16;      // canonical reduction chunk: 2^16 elements
+// fp64 partial of every 2^16-element chunk of elements [first, first+count)
+// (first % 2^16 == 0) into partials[chunk index]; y == nullptr: sum, else dot.
+// x[0] (and y[0]) hold global element x0.
+cudaError_t reduce_chunks(const float* x, const float* y, int64_t x0, int64_t first,
+                          int64_t count, int64_t total, double* partials, const Launch& L);
+// Fixed-tree combine of nchunks partials into *result (one CTA).
+cudaError_t reduce_combine(const double* partials, int64_t nchunks, double* result,
+                           cudaStream_t s);
+
+// ------------------------------------------------------------ traits
+cudaError_t fill_traits(int64_t* out, int64_t count, int64_t size, int64_t offset,
+                        const Launch& L);
+
+int sm_count();
+unsigned long long launch_count();  // kernels launched by this library
+
+}  // namespace mwk

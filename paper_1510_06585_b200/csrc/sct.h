@@ -1,0 +1,83 @@
+// sct.h — host-side skeleton computation tree IR, fusion planner,
+// partitioner and balancer of libmarrow (internal; the ABI is marrow.h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "marrow.h"
+
+namespace mw {
+
+// ------------------------------------------------------------ errors
+struct Error {
+    mw_status code;
+    std::string msg;
+};
+void set_error(const std::string& msg);
+mw_status fail(mw_status code, const std::string& msg);
+
+// ------------------------------------------------------------ tree
+enum class NodeType { Leaf, Pipeline, Map, MapReduce, LoopFor, LoopWhile };
+enum class LeafKind {
+    Saxpy, GaussNoise, Solarize, Mirror, Segment, HystStep, HystFinalize,
+    NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits
+};
+
+struct Node {
+    int refs = 1;
+    NodeType type = NodeType::Leaf;
+    // leaf
+    LeafKind leaf = LeafKind::Saxpy;
+    float fa = 0.f, fb = 0.f;          // saxpy a | nbody dt, eps2
+    int64_t ia = 0, ib = 0, ic = 0;    // seed/scale | T | lo/hi | epu/nu/strict
+    // composites
+    std::vector<Node*> kids;
+    int64_t n = 0;                     // LoopFor count | LoopWhile max_iters
+    int32_t check_every = 1;
+    int32_t merge_op = 0;
+    int32_t in_kind = 0, out_kind = 0; // MW_VK_*
+};
+
+void retain(Node* n);
+void release(Node* n);
+std::string canonical(const Node* n);
+void leaf_epu_nu(const Node* leaf, int64_t* epu, int64_t* nu);
+std::vector<const Node*> leaves(const Node* n);
+
+// ------------------------------------------------------------ fusion plan
+// The tree flattened into the sequence of executable steps; adjacent
+// element-/row-local stages of the same value kind are merged into ONE
+// fused chain (they share the partitioning, so their
+// intermediates never leave the device — here, never leave registers).
+enum class StepKind { Saxpy, Rgba, U8, StencilFor, StencilWhile, NbodyLoop, NbodyAccel,
+                      MapStage, Reduce, Traits };
+struct ChainOp {
+    LeafKind kind;
+    float fa;
+    int64_t ia, ib;
+};
+struct Step {
+    StepKind kind;
+    std::vector<ChainOp> ops;
+    int64_t n = 0;
+    int32_t check_every = 1;
+    float dt = 0.f, eps2 = 0.f;
+    bool dot = false;
+    int64_t epu = 1, nu = 1;
+    bool strict = false;
+};
+mw_status plan(const Node* root, std::vector<Step>* out);
+
+// ------------------------------------------------------------ partitioner / balancer
+int64_t granule_of(const Node* root, mw_status* st);
+bool strict_of(const Node* root);
+mw_status partition_plan(int64_t L, int64_t g, const double* d, int k, bool strict,
+                         int64_t* off, int64_t* len);
+mw_status check_distribution(const double* d, int k);
+mw_status balance_step(const mw_balance_params& p, mw_balance_state& s, const float* ms,
+                       const int64_t* len, const double* cur, int n, double* next, int* trig);
+
+void sha256(const void* data, size_t len, uint8_t out[32]);
+
+}  // namespace mw

@@ -1,0 +1,537 @@
+"""Thin ctypes binding of libmarrow.so (include/marrow.h).
+
+Function names are the C-ABI names; this module only marshals arguments and
+turns error codes into ``MwError``.  Every step of the hot path runs inside
+libmarrow's sm_100a kernels: there is no Python or CPU fallback, and importing
+this module fails loudly if the library has not been built.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libmarrow.so")
+
+# ---------------------------------------------------------------- constants (marrow.h)
+MW_OK = 0
+(MW_E_INVALID_SPEC, MW_E_EPU_NU, MW_E_INFEASIBLE_PARTITION, MW_E_SHAPE_MISMATCH,
+ MW_E_MISSING_ITERATION_COUNT, MW_E_NOT_CONVERGED, MW_E_CUDA, MW_E_NCCL, MW_E_STATE,
+ MW_E_OOM, MW_E_UNSUPPORTED) = range(1, 12)
+MW_MERGE_ADD = 0
+(MW_VK_SAXPY, MW_VK_RGBA, MW_VK_U8, MW_VK_U8_2D, MW_VK_NBODY, MW_VK_VEC1, MW_VK_VEC2,
+ MW_VK_TERMS, MW_VK_ACCEL, MW_VK_TRAITS, MW_VK_SCALAR) = range(1, 12)
+MW_DT_U8, MW_DT_F32, MW_DT_F64, MW_DT_I64 = 1, 2, 3, 4
+MW_PARTITION, MW_COPY = 0, 1
+MW_LOC_DEVICE, MW_LOC_HOST = 0, 1
+MW_BALANCE_PROPORTIONAL, MW_BALANCE_ABS = 0, 1
+(MW_KC_SAXPY, MW_KC_RGBA, MW_KC_U8, MW_KC_STENCIL, MW_KC_NBODY, MW_KC_REDUCE,
+ MW_KC_TRAITS, MW_KC_COUNT) = range(8)
+
+
+class MwError(RuntimeError):
+    def __init__(self, status: int, fn: str, msg: str):
+        self.status = status
+        super().__init__(f"{fn}: {_name(status)}: {msg}")
+
+
+class mw_alloc_fns(ctypes.Structure):
+    _fields_ = [("alloc", ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                           ctypes.c_void_p)),
+                ("free", ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)),
+                ("user", ctypes.c_void_p)]
+
+
+class mw_arg(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("ndim", ctypes.c_int32),
+                ("shape", ctypes.c_int64 * 4), ("mode", ctypes.c_int32),
+                ("location", ctypes.c_int32), ("local_offset", ctypes.c_int64),
+                ("local_rows", ctypes.c_int64)]
+
+
+class mw_balance_params(ctypes.Structure):
+    _fields_ = [("weight", ctypes.c_double), ("max_dev", ctypes.c_double),
+                ("c_factor", ctypes.c_double), ("trigger", ctypes.c_double),
+                ("mode", ctypes.c_int32)]
+
+
+class mw_balance_state(ctypes.Structure):
+    _fields_ = [("lbt", ctypes.c_double), ("active", ctypes.c_int32),
+                ("abs_last_dir", ctypes.c_int32), ("abs_t", ctypes.c_double),
+                ("abs_count", ctypes.c_int32), ("pad", ctypes.c_int32), ("runs", ctypes.c_int64)]
+
+
+_lib = None
+_P = ctypes.POINTER
+_vp, _i32, _i64, _f32, _f64, _u32 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+                                     ctypes.c_float, ctypes.c_double, ctypes.c_uint32)
+_node_pp = _P(_vp)
+
+# name -> argtypes (restype mw_status unless listed in _RES)
+_SIG = {
+    "mw_status_string": [_i32],
+    "mw_last_error": [_vp],
+    "mw_abi_version": [],
+    "mw_nccl_unique_id": [_P(ctypes.c_uint8)],
+    "mw_ctx_create": [_i32, _i32, _i32, _i32, _P(ctypes.c_uint8), _i32, _P(mw_alloc_fns), _P(_vp)],
+    "mw_ctx_destroy": [_vp],
+    "mw_ctx_info": [_vp, _P(_i32), _P(_i32), _P(_i32), _P(_i32), _P(_i32)],
+    "mw_kernel_saxpy": [_f32, _node_pp],
+    "mw_kernel_gauss_noise": [_u32, _i32, _node_pp],
+    "mw_kernel_solarize": [_i32, _node_pp],
+    "mw_kernel_mirror": [_node_pp],
+    "mw_kernel_segment": [_i32, _i32, _node_pp],
+    "mw_kernel_hysteresis_step": [_node_pp],
+    "mw_kernel_hysteresis_finalize": [_node_pp],
+    "mw_kernel_nbody_step": [_f32, _f32, _node_pp],
+    "mw_kernel_nbody_accel": [_f32, _node_pp],
+    "mw_kernel_map_identity": [_node_pp],
+    "mw_kernel_map_product": [_node_pp],
+    "mw_kernel_debug_traits": [_i64, _i64, _i32, _node_pp],
+    "mw_pipeline": [_P(_vp), _i32, _node_pp],
+    "mw_map": [_vp, _node_pp],
+    "mw_map_reduce": [_vp, _i32, _node_pp],
+    "mw_loop_for": [_vp, _i64, _node_pp],
+    "mw_loop_while_changed": [_vp, _i64, _i32, _node_pp],
+    "mw_node_retain": [_vp],
+    "mw_node_release": [_vp],
+    "mw_node_id": [_vp, _P(ctypes.c_uint8)],
+    "mw_node_signature": [_vp, _P(_i32), _P(_i32)],
+    "mw_kernel_execution_order": [_vp, _P(_i64), _i32, _P(_i32), _P(_i64)],
+    "mw_granule": [_vp, _P(_i64)],
+    "mw_partition_plan": [_i64, _i64, _P(_f64), _i32, _i32, _P(_i64), _P(_i64)],
+    "mw_set_distribution": [_vp, _P(_f64), _i32],
+    "mw_get_distribution": [_vp, _P(_f64), _i32],
+    "mw_partition": [_vp, _vp, _i64, _P(_i64), _P(_i64)],
+    "mw_run": [_vp, _vp, _P(mw_arg), _i32, _vp, _P(_vp)],
+    "mw_future_wait": [_vp],
+    "mw_future_query": [_vp, _P(_i32)],
+    "mw_future_result": [_vp, _P(_f64), _i32],
+    "mw_future_release": [_vp],
+    "mw_last_timings": [_vp, _P(_f32), _i32, _P(_f32)],
+    "mw_last_lengths": [_vp, _P(_i64), _i32],
+    "mw_balance_defaults": [_P(mw_balance_params)],
+    "mw_balance_step": [_P(mw_balance_params), _P(mw_balance_state), _P(_f32), _P(_i64),
+                        _P(_f64), _i32, _P(_f64), _P(_i32)],
+    "mw_rebalance": [_vp, _P(mw_balance_params), _P(_i32)],
+    "mw_get_balance_state": [_vp, _P(mw_balance_state)],
+    "mw_ctx_set_slowdown": [_vp, _i32, _f32],
+    "mw_stats_enable": [_vp, _i32],
+    "mw_kernel_stats": [_vp, _i32, _P(_f64), _P(_i64)],
+    "mw_ctx_launch_count": [_vp, _P(_i64)],
+}
+_RES = {"mw_status_string": ctypes.c_char_p, "mw_last_error": ctypes.c_char_p,
+        "mw_abi_version": _i32, "mw_node_retain": None, "mw_node_release": None,
+        "mw_future_release": None, "mw_balance_defaults": None}
+EXPORTS = tuple(_SIG)
+
+
+def lib():
+    """Load libmarrow.so; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: run `python __graft_entry__.py` "
+                              "(build) — the hot path has no non-CUDA implementation")
+        L = ctypes.CDLL(_LIB_PATH)
+        for name, argt in _SIG.items():
+            fn = getattr(L, name)
+            fn.argtypes = argt
+            fn.restype = _RES.get(name, _i32)
+        _lib = L
+    return _lib
+
+
+def _name(st):
+    try:
+        return lib().mw_status_string(st).decode()
+    except Exception:  # pragma: no cover
+        return str(st)
+
+
+def _chk(st, fn):
+    if st != MW_OK:
+        raise MwError(st, fn, lib().mw_last_error(None).decode())
+
+
+def _call(name, *args):
+    _chk(getattr(lib(), name)(*args), name)
+
+
+# ---------------------------------------------------------------- nodes
+class Node:
+    """Owning handle of an mw_node (released on garbage collection)."""
+
+    def __init__(self, ptr, kids=()):
+        self.ptr = ptr
+        self._kids = kids
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.mw_node_release(self.ptr)
+            self.ptr = None
+
+    @property
+    def _as_parameter_(self):
+        return self.ptr
+
+
+def _new(name, *args, kids=()):
+    out = _vp()
+    _call(name, *args, ctypes.byref(out))
+    return Node(out, kids)
+
+
+def mw_kernel_saxpy(a):
+    return _new("mw_kernel_saxpy", _f32(a))
+
+
+def mw_kernel_gauss_noise(seed, scale):
+    return _new("mw_kernel_gauss_noise", _u32(seed & 0xFFFFFFFF), scale)
+
+
+def mw_kernel_solarize(threshold):
+    return _new("mw_kernel_solarize", threshold)
+
+
+def mw_kernel_mirror():
+    return _new("mw_kernel_mirror")
+
+
+def mw_kernel_segment(lo, hi):
+    return _new("mw_kernel_segment", lo, hi)
+
+
+def mw_kernel_hysteresis_step():
+    return _new("mw_kernel_hysteresis_step")
+
+
+def mw_kernel_hysteresis_finalize():
+    return _new("mw_kernel_hysteresis_finalize")
+
+
+def mw_kernel_nbody_step(dt, eps2):
+    return _new("mw_kernel_nbody_step", _f32(dt), _f32(eps2))
+
+
+def mw_kernel_nbody_accel(eps2):
+    return _new("mw_kernel_nbody_accel", _f32(eps2))
+
+
+def mw_kernel_map_identity():
+    return _new("mw_kernel_map_identity")
+
+
+def mw_kernel_map_product():
+    return _new("mw_kernel_map_product")
+
+
+def mw_kernel_debug_traits(epu=1, nu=1, strict=False):
+    return _new("mw_kernel_debug_traits", epu, nu, int(bool(strict)))
+
+
+def mw_pipeline(stages):
+    arr = (_vp * len(stages))(*[s.ptr for s in stages])
+    return _new("mw_pipeline", arr, len(stages), kids=tuple(stages))
+
+
+def mw_map(tree):
+    return _new("mw_map", tree.ptr, kids=(tree,))
+
+
+def mw_map_reduce(map_stage, merge_op=MW_MERGE_ADD):
+    return _new("mw_map_reduce", map_stage.ptr, merge_op, kids=(map_stage,))
+
+
+def mw_loop_for(body, n):
+    return _new("mw_loop_for", body.ptr, n, kids=(body,))
+
+
+def mw_loop_while_changed(body, max_iters, check_every=1):
+    return _new("mw_loop_while_changed", body.ptr, max_iters, check_every, kids=(body,))
+
+
+def mw_node_id(node) -> bytes:
+    buf = (ctypes.c_uint8 * 32)()
+    _call("mw_node_id", node.ptr, buf)
+    return bytes(buf)
+
+
+def mw_node_signature(node):
+    i, o = _i32(), _i32()
+    _call("mw_node_signature", node.ptr, ctypes.byref(i), ctypes.byref(o))
+    return i.value, o.value
+
+
+def mw_kernel_execution_order(node, while_counts=()):
+    wc = (_i64 * max(1, len(while_counts)))(*while_counts)
+    n = _i64(0)
+    st = lib().mw_kernel_execution_order(node.ptr, wc, len(while_counts), None, ctypes.byref(n))
+    if st not in (MW_OK, MW_E_INVALID_SPEC) or (st == MW_E_INVALID_SPEC and n.value == 0):
+        _chk(st, "mw_kernel_execution_order")
+    out = (_i32 * max(1, n.value))()
+    _call("mw_kernel_execution_order", node.ptr, wc, len(while_counts), out, ctypes.byref(n))
+    return list(out[:n.value])
+
+
+def mw_granule(node) -> int:
+    g = _i64()
+    _call("mw_granule", node.ptr, ctypes.byref(g))
+    return g.value
+
+
+def mw_partition_plan(L, g, fractions, strict=False):
+    k = len(fractions)
+    d = (_f64 * max(1, k))(*fractions)
+    off, ln = (_i64 * max(1, k))(), (_i64 * max(1, k))()
+    _call("mw_partition_plan", L, g, d, k, int(bool(strict)), off, ln)
+    return list(off[:k]), list(ln[:k])
+
+
+# ---------------------------------------------------------------- balance (pure host)
+def mw_balance_defaults(mode=MW_BALANCE_PROPORTIONAL):
+    p = mw_balance_params()
+    lib().mw_balance_defaults(ctypes.byref(p))
+    p.mode = mode
+    return p
+
+
+def mw_balance_step(params, state, per_part_ms, per_part_len, cur):
+    n = len(cur)
+    ms = (_f32 * n)(*per_part_ms)
+    ln = (_i64 * n)(*per_part_len)
+    cd = (_f64 * n)(*cur)
+    nx = (_f64 * n)()
+    trig = _i32()
+    _call("mw_balance_step", ctypes.byref(params), ctypes.byref(state), ms, ln, cd, n, nx,
+          ctypes.byref(trig))
+    return list(nx), bool(trig.value)
+
+
+# ---------------------------------------------------------------- context
+def mw_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _call("mw_nccl_unique_id", buf)
+    return bytes(buf)
+
+
+class TorchAllocator:
+    """mw_alloc_fns backed by PyTorch's caching allocator (PyTorch owns memory)."""
+
+    def __init__(self, device):
+        import torch
+        self._torch = torch
+        self.device = torch.device(device)
+        self.live = {}
+
+        @ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+        def _alloc(nbytes, stream, user):
+            try:
+                t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+                self.live[t.data_ptr()] = t
+                return t.data_ptr()
+            except Exception:
+                return None
+
+        @ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+        def _free(ptr, user):
+            self.live.pop(ptr, None)
+
+        self._a, self._f = _alloc, _free
+        self.fns = mw_alloc_fns(_alloc, _free, None)
+
+
+class Ctx:
+    def __init__(self, ptr, allocator):
+        self.ptr = ptr
+        self.allocator = allocator
+
+    def __del__(self):
+        self.destroy()
+
+    def destroy(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.mw_ctx_destroy(self.ptr)
+            self.ptr = None
+
+    @property
+    def _as_parameter_(self):
+        return self.ptr
+
+
+def mw_ctx_create(device=0, rank=0, nranks=1, parts_per_rank=1, nccl_id=None, force_nccl=False,
+                  torch_alloc=True):
+    out = _vp()
+    idbuf = (ctypes.c_uint8 * 128)(*nccl_id) if nccl_id is not None else None
+    alloc = TorchAllocator(f"cuda:{device}") if torch_alloc else None
+    _call("mw_ctx_create", device, rank, nranks, parts_per_rank, idbuf, int(bool(force_nccl)),
+          ctypes.byref(alloc.fns) if alloc else None, ctypes.byref(out))
+    return Ctx(out, alloc)
+
+
+def mw_ctx_destroy(ctx):
+    ctx.destroy()
+
+
+def mw_ctx_info(ctx):
+    v = [_i32() for _ in range(5)]
+    _call("mw_ctx_info", ctx.ptr, *[ctypes.byref(x) for x in v])
+    return {"n_parts": v[0].value, "first_part": v[1].value, "parts_per_rank": v[2].value,
+            "rank": v[3].value, "nranks": v[4].value}
+
+
+def mw_set_distribution(ctx, fractions):
+    d = (_f64 * len(fractions))(*fractions)
+    _call("mw_set_distribution", ctx.ptr, d, len(fractions))
+
+
+def mw_get_distribution(ctx):
+    n = mw_ctx_info(ctx)["n_parts"]
+    d = (_f64 * n)()
+    _call("mw_get_distribution", ctx.ptr, d, n)
+    return list(d)
+
+
+def mw_partition(ctx, node, L):
+    n = mw_ctx_info(ctx)["n_parts"]
+    off, ln = (_i64 * n)(), (_i64 * n)()
+    _call("mw_partition", ctx.ptr, node.ptr, L, off, ln)
+    return list(off), list(ln)
+
+
+# ---------------------------------------------------------------- args / run
+_DT = {"uint8": MW_DT_U8, "float32": MW_DT_F32, "float64": MW_DT_F64, "int64": MW_DT_I64}
+
+
+def arg(t, mode=MW_PARTITION, local_offset=0, global_shape=None):
+    """mw_arg for a torch tensor (CUDA or host) or a numpy array (host).
+
+    global_shape defaults to t.shape (the tensor holds the whole array);
+    for a slice holding global rows [local_offset, local_offset + len(t)),
+    pass the global shape."""
+    a = mw_arg()
+    if hasattr(t, "data_ptr"):
+        ptr, shape, dt = t.data_ptr(), tuple(t.shape), str(t.dtype).replace("torch.", "")
+        loc = MW_LOC_DEVICE if t.is_cuda else MW_LOC_HOST
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+    else:
+        ptr, shape, dt = t.ctypes.data, tuple(t.shape), str(t.dtype)
+        loc = MW_LOC_HOST
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+    gshape = tuple(global_shape) if global_shape is not None else shape
+    a.ptr = ptr
+    a.dtype = _DT[dt]
+    a.ndim = len(gshape)
+    for i, s in enumerate(gshape):
+        a.shape[i] = s
+    a.mode = mode
+    a.location = loc
+    a.local_offset = local_offset
+    a.local_rows = shape[0] if len(shape) else 0
+    a._owner = t   # keeps the buffer alive until the run's future is released
+    return a
+
+
+class Future:
+    def __init__(self, ptr, keep):
+        self.ptr = ptr
+        self._keep = keep
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.mw_future_release(self.ptr)
+            self.ptr = None
+
+    def wait(self):
+        mw_future_wait(self)
+        return self
+
+    def result(self):
+        return mw_future_result(self)
+
+
+def mw_run(ctx, node, args, stream=None):
+    """Enqueue a run on `stream` (torch.cuda.Stream or raw cudaStream_t int;
+    default: torch's current stream)."""
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    arr = (mw_arg * len(args))(*args)
+    out = _vp()
+    _call("mw_run", ctx.ptr, node.ptr, arr, len(args), _vp(sp), ctypes.byref(out))
+    return Future(out, (arr, node, ctx, [getattr(a, "_owner", None) for a in args]))
+
+
+def mw_future_wait(f):
+    _call("mw_future_wait", f.ptr)
+
+
+def mw_future_query(f) -> bool:
+    d = _i32()
+    _call("mw_future_query", f.ptr, ctypes.byref(d))
+    return bool(d.value)
+
+
+def mw_future_result(f):
+    """dict(reduced fp64, reduced32, executions, converged)."""
+    out = (_f64 * 4)()
+    _call("mw_future_result", f.ptr, out, 4)
+    return {"reduced": out[0], "reduced32": out[1], "executions": int(out[2]),
+            "converged": bool(out[3])}
+
+
+def mw_future_release(f):
+    if f.ptr:
+        lib().mw_future_release(f.ptr)
+        f.ptr = None
+
+
+def mw_last_timings(ctx):
+    n = mw_ctx_info(ctx)["n_parts"]
+    ms, wall = (_f32 * n)(), _f32()
+    _call("mw_last_timings", ctx.ptr, ms, n, ctypes.byref(wall))
+    return list(ms), wall.value
+
+
+def mw_last_lengths(ctx):
+    n = mw_ctx_info(ctx)["n_parts"]
+    ln = (_i64 * n)()
+    _call("mw_last_lengths", ctx.ptr, ln, n)
+    return list(ln)
+
+
+def mw_rebalance(ctx, params=None) -> bool:
+    p = params or mw_balance_defaults()
+    t = _i32()
+    _call("mw_rebalance", ctx.ptr, ctypes.byref(p), ctypes.byref(t))
+    return bool(t.value)
+
+
+def mw_get_balance_state(ctx):
+    s = mw_balance_state()
+    _call("mw_get_balance_state", ctx.ptr, ctypes.byref(s))
+    return s
+
+
+def mw_ctx_set_slowdown(ctx, part, factor):
+    _call("mw_ctx_set_slowdown", ctx.ptr, part, _f32(factor))
+
+
+def mw_ctx_launch_count(ctx) -> int:
+    n = _i64()
+    _call("mw_ctx_launch_count", ctx.ptr, ctypes.byref(n))
+    return n.value
+
+
+def mw_stats_enable(ctx, on=True):
+    _call("mw_stats_enable", ctx.ptr, int(bool(on)))
+
+
+def mw_kernel_stats(ctx, kernel_class):
+    """(total event-measured ms, launches) of one kernel class since enabling."""
+    ms, n = _f64(), _i64()
+    _call("mw_kernel_stats", ctx.ptr, kernel_class, ctypes.byref(ms), ctypes.byref(n))
+    return ms.value, n.value

@@ -1,0 +1,413 @@
+"""CUDA path (through the C-ABI) vs the oracle, element by element.
+
+Bit-exact for integer work (filter, segmentation, hysteresis, traits) and
+for saxpy (single-rounding fma on both sides); MapReduce within 1e-5
+relative (north_star) — in practice ~1e-15; N-body accelerations within the
+SURVEY §8(c) c.5 bounds (1e-5 relative, conditioning-aware).
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synth  # noqa: E402
+from oracle import kernels as K  # noqa: E402
+from oracle import partition as OP  # noqa: E402
+from oracle import sct  # noqa: E402
+from paper_1510_06585_b200 import marrow as M  # noqa: E402
+from paper_1510_06585_b200 import trees  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def ctx(ppr=1, dist=None):
+    c = M.mw_ctx_create(0, 0, 1, ppr)
+    if dist is not None:
+        M.mw_set_distribution(c, dist)
+    return c
+
+
+def run(c, node, args):
+    f = M.mw_run(c, node, args)
+    f.wait()
+    return f.result()
+
+
+def dists(k, rng, n=3):
+    out = [[1.0 / k] * k]
+    for _ in range(n):
+        w = rng.integers(0, 4, size=k).astype(float)
+        if w.sum() == 0:
+            w[0] = 1
+        out.append(list(w / w.sum()))
+    return out
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+# ----------------------------------------------------------------- saxpy
+@pytest.mark.parametrize("n", [1, 3, 4, 67, 1000, (1 << 20) + 3])
+def test_saxpy_bitwise(n):
+    rng = np.random.default_rng(n)
+    x = synth.np_f32_um11(1, 0, n)
+    y = synth.np_f32_um11(2, 0, n)
+    want = K.saxpy(2.5, x, y)
+    for d in dists(4, rng):
+        c = ctx(4, d)
+        xd, yd = dev(x), dev(y)
+        run(c, trees.saxpy(2.5), [M.arg(xd), M.arg(yd)])
+        assert np.array_equal(yd.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+def test_saxpy_rounding_pin_and_chain():
+    a = np.float32(1 + 2.0 ** -12)
+    x = np.full(9, a, np.float32)
+    y = np.full(9, -(1 + 2.0 ** -11), np.float32)
+    xd, yd = dev(x), dev(y)
+    run(ctx(), trees.saxpy(float(a)), [M.arg(xd), M.arg(yd)])
+    assert np.all(yd.cpu().numpy() == 2.0 ** -24)
+    # Loop equals its unrolled body, and both equal the oracle's sequential evaluation
+    x = synth.np_f32_um11(1, 0, 1001)
+    y = synth.np_f32_um11(2, 0, 1001)
+    want = sct.evaluate(sct.LoopFor(sct.Leaf("saxpy", {"a": 0.75}), 20), (x, y)).value[1]
+    yd = dev(y)
+    run(ctx(), M.mw_loop_for(M.mw_kernel_saxpy(0.75), 20), [M.arg(dev(x)), M.arg(yd)])
+    assert np.array_equal(yd.cpu().numpy(), want)
+
+
+# ----------------------------------------------------------------- filter pipeline
+def oracle_filter(img, seed=4, S=8, T=128):
+    return sct.evaluate(sct.Pipeline([sct.Leaf("gauss_noise", {"seed": seed, "scale": S}),
+                                      sct.Leaf("solarize", {"threshold": T}),
+                                      sct.Leaf("mirror")]), img).value
+
+
+@pytest.mark.parametrize("H,W", [(2, 4), (37, 64), (33, 61), (5, 1), (256, 512), (900, 1440), (1125, 1800)])
+def test_filter_pipeline_bitwise(H, W):
+    rng = np.random.default_rng(H * 7 + W)
+    img = synth.np_rgba(3, 0, H * W).reshape(H, W, 4)
+    want = oracle_filter(img)
+    for d in dists(3, rng):
+        c = ctx(3, d)
+        src, dst = dev(img), torch.empty((H, W, 4), dtype=torch.uint8, device=DEV)
+        run(c, trees.filter_pipeline(), [M.arg(src), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want), d
+
+
+def test_filter_golden_vector_and_fused_equals_unfused():
+    W, H = 4, 2
+    img = np.array([[(16 * i) % 256, (255 - 16 * i) % 256, (37 * i) % 256, 200]
+                    for i in range(W * H)], dtype=np.uint8).reshape(H, W, 4)
+    c = ctx()
+    src, dst = dev(img), torch.empty_like(dev(img))
+    run(c, trees.filter_pipeline(), [M.arg(src), M.arg(dst)])
+    from tests.golden_io import filter_w4h2
+    _, _, rows = filter_w4h2()
+    assert [[tuple(int(v) for v in px) for px in row] for row in dst.cpu().numpy()] == rows
+    # three separate Map runs (unfused) give the same bytes as the fused pipeline
+    img = synth.np_rgba(3, 0, 123 * 77).reshape(123, 77, 4)
+    a, b, o = dev(img), torch.empty((123, 77, 4), dtype=torch.uint8, device=DEV), None
+    run(c, M.mw_map(M.mw_kernel_gauss_noise(4, 8)), [M.arg(a), M.arg(b)])
+    o1 = torch.empty_like(b)
+    run(c, M.mw_map(M.mw_kernel_solarize(128)), [M.arg(b), M.arg(o1)])
+    o = torch.empty_like(b)
+    run(c, M.mw_map(M.mw_kernel_mirror()), [M.arg(o1), M.arg(o)])
+    fused = torch.empty_like(b)
+    run(c, trees.filter_pipeline(), [M.arg(dev(img)), M.arg(fused)])
+    assert torch.equal(o, fused)
+    assert np.array_equal(o.cpu().numpy(), oracle_filter(img))
+
+
+def test_rgba_long_chains_and_loops():
+    img = synth.np_rgba(5, 0, 41 * 36).reshape(41, 36, 4)
+    c = ctx(2, [0.3, 0.7])
+    # LoopFor(mirror, 2) is the identity; long chains split into several launches
+    dst = torch.empty((41, 36, 4), dtype=torch.uint8, device=DEV)
+    run(c, M.mw_loop_for(M.mw_kernel_mirror(), 2), [M.arg(dev(img)), M.arg(dst)])
+    assert np.array_equal(dst.cpu().numpy(), img)
+    body = sct.Pipeline([sct.Leaf("gauss_noise", {"seed": 11, "scale": 3}), sct.Leaf("mirror"),
+                         sct.Leaf("solarize", {"threshold": 90})])
+    want = sct.evaluate(sct.LoopFor(body, 9), img).value
+    mb = M.mw_pipeline([M.mw_kernel_gauss_noise(11, 3), M.mw_kernel_mirror(), M.mw_kernel_solarize(90)])
+    run(c, M.mw_loop_for(mb, 9), [M.arg(dev(img)), M.arg(dst)])
+    assert np.array_equal(dst.cpu().numpy(), want)
+    run(c, M.mw_loop_for(mb, 0), [M.arg(dev(img)), M.arg(dst)])
+    assert np.array_equal(dst.cpu().numpy(), img)
+
+
+def test_filter_host_staged_equals_device():
+    H, W = 700, 1024
+    img = synth.np_rgba(3, 0, H * W).reshape(H, W, 4)
+    src = torch.from_numpy(img).pin_memory()
+    dst = torch.empty((H, W, 4), dtype=torch.uint8).pin_memory()
+    c = ctx(2, [0.6, 0.4])
+    run(c, trees.filter_pipeline(), [M.arg(src), M.arg(dst)])
+    assert np.array_equal(dst.numpy(), oracle_filter(img))
+
+
+# ----------------------------------------------------------------- segmentation
+@pytest.mark.parametrize("shape", [(37, 16, 48), (5, 3, 7), (64, 64, 64), (1, 1, 1)])
+@pytest.mark.parametrize("lohi", [(85, 170), (0, 0), (256, 256), (0, 256), (128, 200), (3, 129)])
+def test_segmentation_bitwise(shape, lohi):
+    n = int(np.prod(shape))
+    vol = synth.np_u8_stream(7, 0, n).reshape(shape)
+    want = K.segment(vol, *lohi)
+    c = ctx(3, [0.5, 0.0, 0.5])
+    dst = torch.empty(shape, dtype=torch.uint8, device=DEV)
+    run(c, trees.segmentation(*lohi), [M.arg(dev(vol)), M.arg(dst)])
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
+# ----------------------------------------------------------------- MapReduce
+@pytest.mark.parametrize("n", [1, 1000, 1 << 16, (1 << 16) + 1, 3 * (1 << 16) + 12345, 1 << 22])
+@pytest.mark.parametrize("dot", [False, True])
+def test_mapreduce_vs_oracle_and_canonical(n, dot):
+    x = synth.np_f32_um11(5, 0, n)
+    y = synth.np_f32_um11(6, 0, n)
+    want = K.dot(x, y) if dot else K.sum_(x)
+    scale = K.abs_sum(x, y if dot else None)
+    args = [M.arg(dev(x))] + ([M.arg(dev(y))] if dot else [])
+    rng = np.random.default_rng(n)
+    vals = set()
+    for d in dists(4, rng):
+        r = run(ctx(4, d), trees.mapreduce(dot), args)["reduced"]
+        tol = 1e-5 * abs(want) if abs(want) >= 1e-5 * scale else 1e-5 * scale
+        assert abs(r - want) <= tol
+        assert abs(r - want) <= 1e-12 * scale + 1e-300   # per-element fp64 accuracy
+        vals.add(np.float64(r).tobytes())
+    assert len(vals) == 1, "canonical mode must be bit-identical across distributions"
+
+
+def test_mapreduce_closed_forms():
+    n = (1 << 25) + 3
+    r = run(ctx(), trees.mapreduce(False), [M.arg(torch.ones(n, device=DEV))])
+    assert r["reduced"] == float(n) and r["reduced32"] == float(np.float32(n))
+    x = (torch.arange(1 << 20, device=DEV) % 1024).float() / 1024
+    assert run(ctx(), trees.mapreduce(False), [M.arg(x)])["reduced"] == 523776.0
+    e = torch.zeros(1000, device=DEV)
+    e[17] = 1
+    y = dev(synth.np_f32_um11(6, 0, 1000))
+    assert run(ctx(), trees.mapreduce(True), [M.arg(y), M.arg(e)])["reduced"] == float(y[17])
+    assert run(ctx(), trees.mapreduce(False), [M.arg(torch.zeros(0, device=DEV))])["reduced"] == 0.0
+
+
+# ----------------------------------------------------------------- hysteresis
+def oracle_hyst(gray, lo=173, hi=250):
+    L = K.segment(gray, lo, hi)
+    fixed, D = K.hyst_bfs(L)
+    return K.hyst_finalize(fixed), D
+
+
+@pytest.mark.parametrize("H,W", [(64, 64), (100, 37), (257, 300), (1, 1), (3, 1000)])
+@pytest.mark.parametrize("ce", [1, 4, 16])
+def test_hysteresis_bitwise_and_E(H, W, ce):
+    rng = np.random.default_rng(H * W + ce)
+    gray = synth.np_u8_stream(8, 0, H * W).reshape(H, W)
+    want, D = oracle_hyst(gray)
+    for d in dists(3, rng, 2) + [[0.0, 1.0, 0.0]]:
+        c = ctx(3, d)
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(c, trees.hysteresis(check_every=ce), [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want), d
+        assert r["executions"] == D + 1 and r["converged"]
+
+
+def test_hysteresis_long_chains_partitions():
+    # a long weak snake crossing every partition boundary (1-row partitions)
+    H, W = 12, 40
+    L = np.zeros((H, W), np.uint8)
+    L[:, :] = 128
+    L[::2, 1:] = 0
+    L[1::2, :-1] = 0
+    L[1::4, -1] = 128
+    L[3::4, 0] = 128
+    L[0, 0] = 255
+    gray = np.where(L == 255, 255, np.where(L == 128, 200, 0)).astype(np.uint8)
+    want, D = oracle_hyst(gray)
+    for d in ([1 / 12] * 12, [0.5] + [0.5 / 11] * 11):
+        c = ctx(12, d)
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(c, trees.hysteresis(check_every=3), [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want) and r["executions"] == D + 1
+
+
+def test_hysteresis_loop_for_and_max_iters():
+    rng = np.random.default_rng(0)
+    gray = rng.integers(0, 256, size=(50, 70), dtype=np.uint8)
+    L = K.segment(gray, 173, 250)
+    _, D = K.hyst_bfs(L)
+    c = ctx(2)
+    for n in (0, 1, 2, 5):
+        dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
+        run(c, M.mw_loop_for(M.mw_kernel_hysteresis_step(), n), [M.arg(dev(L)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, n)[0])
+    if D >= 2:
+        dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
+        r = run(c, trees.hysteresis(max_iters=2), [M.arg(dev(gray)), M.arg(dst)])
+        assert r["executions"] == 2 and not r["converged"]
+        assert np.array_equal(dst.cpu().numpy(), K.hyst_finalize(K.hyst_bfs(L, 2)[0]))
+
+
+# ----------------------------------------------------------------- N-body
+def _nb_check(acc_g, acc_o, cond):
+    err = np.linalg.norm(acc_g - acc_o, axis=1)
+    nrm = np.linalg.norm(acc_o, axis=1)
+    C = cond
+    ok_cond = (C / np.maximum(nrm, 1e-300)) <= 1e3
+    assert np.all(err[ok_cond] <= 1e-5 * nrm[ok_cond])
+    assert np.all(err <= 1e-5 * np.maximum(nrm, 1e-3 * C))
+    assert np.linalg.norm(acc_g - acc_o) <= 1e-5 * np.linalg.norm(acc_o)
+
+
+@pytest.mark.parametrize("N", [1, 2, 300, 1024, 4096 + 256])
+def test_nbody_accel_vs_oracle(N):
+    pos, _ = synth.np_nbody(9, 0, N, 2.0 ** -10)
+    acc_o, cond = K.nbody_accel(pos, 1e-4)
+    c = ctx(3, [0.2, 0.5, 0.3])
+    acc = torch.empty((N, 4), dtype=torch.float32, device=DEV)
+    run(c, M.mw_kernel_nbody_accel(1e-4), [M.arg(dev(pos), M.MW_COPY), M.arg(acc)])
+    _nb_check(acc.cpu().numpy()[:, :3].astype(np.float64), acc_o, cond)
+
+
+def test_nbody_step_vs_oracle_and_partition_invariance():
+    N = 2048 + 512
+    pos, vel = synth.np_nbody(9, 0, N, 2.0 ** -11)
+    po, vo, acc_o = K.nbody_step(pos, vel, 1e-4, 1e-3)
+    _, cond = K.nbody_accel(pos, 1e-4)
+    results = []
+    for d in ([1.0, 0.0, 0.0, 0.0], [0.25] * 4, [0.1, 0.4, 0.0, 0.5]):
+        c = ctx(4, d)
+        p, v = dev(pos), dev(vel)
+        run(c, trees.nbody(1), [M.arg(p, M.MW_COPY), M.arg(v, M.MW_COPY)])
+        dv = (v.cpu().numpy()[:, :3].astype(np.float64) - vel[:, :3]) / np.float64(np.float32(1e-3))
+        _nb_check(dv, acc_o, cond)
+        results.append((p.cpu().numpy().tobytes(), v.cpu().numpy().tobytes()))
+    assert all(r == results[0] for r in results), "trajectories must not depend on the distribution"
+
+
+def test_nbody_loop_equals_repeated_runs():
+    N = 1024
+    pos, vel = synth.np_nbody(9, 0, N, 2.0 ** -10)
+    c = ctx(2)
+    p1, v1 = dev(pos), dev(vel)
+    run(c, trees.nbody(3), [M.arg(p1, M.MW_COPY), M.arg(v1, M.MW_COPY)])
+    p2, v2 = dev(pos), dev(vel)
+    for _ in range(3):
+        run(c, trees.nbody(1), [M.arg(p2, M.MW_COPY), M.arg(v2, M.MW_COPY)])
+    assert torch.equal(p1, p2) and torch.equal(v1, v2)
+
+
+# ----------------------------------------------------------------- traits / partition
+def test_debug_traits_reproduce_partitions():
+    rng = np.random.default_rng(1)
+    for trial in range(30):
+        k = int(rng.integers(1, 6))
+        L = int(rng.integers(0, 500))
+        epu = int(rng.choice([1, 2, 4, 6]))
+        d = dists(k, rng, 1)[-1]
+        c = ctx(k, d)
+        out = torch.full((L, 2), -1, dtype=torch.int64, device=DEV)
+        node = M.mw_kernel_debug_traits(epu, 1)
+        run(c, node, [M.arg(out)])
+        off, ln = OP.partition(L, OP.granule([(epu, 1)]), d)
+        want = np.concatenate([np.tile([n, o], (n, 1)) for o, n in zip(off, ln)] + [np.zeros((0, 2))]).astype(np.int64)
+        assert np.array_equal(out.cpu().numpy(), want.reshape(L, 2))
+        assert M.mw_partition(c, node, L) == (off, ln)
+
+
+# ----------------------------------------------------------------- rebalancing
+def test_rebalance_slowdown_nbody_bitwise():
+    N = 8192
+    pos, vel = synth.np_nbody(9, 0, N, 2.0 ** -13)
+    c = ctx(4)
+    M.mw_ctx_set_slowdown(c, 3, 8.0)
+    p, v = dev(pos), dev(vel)
+    node = trees.nbody(1)
+    trig_at = None
+    for step in range(6):
+        run(c, node, [M.arg(p, M.MW_COPY), M.arg(v, M.MW_COPY)])
+        if M.mw_rebalance(c) and trig_at is None:
+            trig_at = step
+    assert trig_at == 2, "three consecutive unbalanced runs trigger (lbt 0.963)"
+    d = M.mw_get_distribution(c)
+    assert d[3] < 0.5 * d[0]
+    # identical trajectory to a run that never rebalanced
+    c2 = ctx(1)
+    p2, v2 = dev(pos), dev(vel)
+    run(c2, trees.nbody(6), [M.arg(p2, M.MW_COPY), M.arg(v2, M.MW_COPY)])
+    assert torch.equal(p, p2) and torch.equal(v, v2)
+
+
+# ----------------------------------------------------------------- full config sizes
+@pytest.mark.slow
+def test_config_filter_8192_bitwise():
+    H = W = 8192
+    src = torch.empty((H, W, 4), dtype=torch.uint8, device=DEV)
+    synth.dev_fill_rgba(src, synth.SEED_IMAGE, 0)
+    dst = torch.empty_like(src)
+    run(ctx(), trees.filter_pipeline(), [M.arg(src), M.arg(dst)])
+    img = synth.host_rgba(synth.SEED_IMAGE, 0, H * W).reshape(H, W, 4)
+    assert np.array_equal(src.cpu().numpy(), img)
+    got = dst.cpu().numpy()
+    want = K.mirror(K.solarize(K.gauss_noise(img, 4, 8), 128))
+    assert np.array_equal(got, want)
+    assert zlib.crc32(got.tobytes()) == 0x60CC7642
+
+
+@pytest.mark.slow
+def test_config_hysteresis_16384():
+    n = 16384
+    src = torch.empty((n, n), dtype=torch.uint8, device=DEV)
+    synth.dev_fill_u8_stream(src, synth.SEED_HYST, 0)
+    dst = torch.empty_like(src)
+    r = run(ctx(), trees.hysteresis(), [M.arg(src), M.arg(dst)])
+    gray = synth.host_u8_stream(synth.SEED_HYST, 0, n * n).reshape(n, n)
+    want, D = oracle_hyst(gray)
+    assert r["executions"] == D + 1 == 48
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
+@pytest.mark.slow
+def test_config_segmentation_bitwise():
+    shape = (512, 1024, 1024)
+    src = torch.empty(shape, dtype=torch.uint8, device=DEV)
+    synth.dev_fill_u8_stream(src, synth.SEED_SEGMENT, 0)
+    dst = torch.empty_like(src)
+    run(ctx(), trees.segmentation(), [M.arg(src), M.arg(dst)])
+    got = dst.cpu().numpy()
+    assert zlib.crc32(got.data) == 0x9417CCB7
+    vol = synth.host_u8_stream(synth.SEED_SEGMENT, 0, got.size)
+    assert np.array_equal(got.ravel(), K.segment(vol, 85, 170))
+
+
+@pytest.mark.slow
+def test_config_mapreduce_2p30():
+    n = 1 << 30
+    x = torch.empty(n, dtype=torch.float32, device=DEV)
+    y = torch.empty(n, dtype=torch.float32, device=DEV)
+    synth.dev_fill_f32_um11(x, synth.SEED_MR_X, 0)
+    synth.dev_fill_f32_um11(y, synth.SEED_MR_Y, 0)
+    s = run(ctx(), trees.mapreduce(False), [M.arg(x)])["reduced"]
+    d = run(ctx(), trees.mapreduce(True), [M.arg(x), M.arg(y)])["reduced"]
+    exact_s = -383760319397 / 2.0 ** 23
+    exact_d = 643773335475643653 / 2.0 ** 46
+    assert abs(s - exact_s) <= 1e-12 * abs(exact_s)
+    assert abs(d - exact_d) <= 1e-12 * abs(exact_d)
+
+
+@pytest.mark.slow
+def test_config_nbody_2p20_sampled():
+    N = 1 << 20
+    pos = torch.empty((N, 4), dtype=torch.float32, device=DEV)
+    synth.dev_fill_nbody(pos, None, synth.SEED_NBODY, 0, 2.0 ** -20)
+    acc = torch.empty((N, 4), dtype=torch.float32, device=DEV)
+    run(ctx(), M.mw_kernel_nbody_accel(1e-4), [M.arg(pos, M.MW_COPY), M.arg(acc)])
+    hp = pos.cpu().numpy()
+    samples = np.concatenate([synth.nbody_sample_indices(N, 256), [0, N - 1, 284297]])
+    acc_o, cond = K.nbody_accel(hp, 1e-4, targets=samples)
+    _nb_check(acc.cpu().numpy()[samples, :3].astype(np.float64), acc_o, cond)

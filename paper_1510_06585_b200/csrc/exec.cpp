@@ -478,6 +478,19 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
         }
         MW_OK_OR_RETURN(exchange_halos(R, H, hb, pitch));
         CUDA_OK(cudaMemsetAsync(d_last, 0xFF, sizeof(int32_t), R.s));  // -1
+        // per-tile change flags (two generations) and neighbour presence
+        std::vector<uint8_t*> flags(ppr, nullptr);
+        std::vector<int> top_nbr(ppr, 0), bot_nbr(ppr, 0);
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            void* fp;
+            int64_t nt = mwk::hyst_tiles(R.len[p], pitch);
+            MW_OK_OR_RETURN(scratch(c, "hflags_" + std::to_string(q), (size_t)(2 * nt), R.s, &fp));
+            flags[q] = static_cast<uint8_t*>(fp);
+            for (int a = 0; a < p; ++a) top_nbr[q] |= R.len[a] > 0;
+            for (int a = p + 1; a < c->P; ++a) bot_nbr[q] |= R.len[a] > 0;
+        }
         const int64_t max_it = st.n;
         const int64_t ce = is_while ? std::max<int64_t>(1, st.check_every) : max_it;
         int64_t it = 0;
@@ -489,9 +502,13 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
                 for (int q = 0; q < ppr; ++q) {
                     int p = R.first + q;
                     if (R.len[p] == 0) continue;
+                    const int64_t nt = mwk::hyst_tiles(R.len[p], pitch);
+                    uint8_t* fcur = flags[q] + (it & 1) * nt;
+                    const uint8_t* fprev = it == 0 ? nullptr : flags[q] + ((it + 1) & 1) * nt;
                     PartTimer t(c, R.s, p, MW_KC_STENCIL);
                     MW_OK_OR_RETURN(kerr(mwk::hyst_step(H[q].buf[hb], H[q].buf[1 - hb], R.len[p], pitch,
-                                                        (int)it, d_last, launch_for(c, R.s, p)),
+                                                        (int)it, d_last, fprev, fcur, top_nbr[q],
+                                                        bot_nbr[q], launch_for(c, R.s, p)),
                                          "hyst_step"));
                 }
                 hb = 1 - hb;

@@ -9,6 +9,7 @@
 //
 // Definitions follow DESIGN.md §Readings (R1-R12), citing PAPER.md lines.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "mw_kernels.h"
@@ -61,6 +62,14 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t v) {
 }
 
 int g_sms = 0;
+
+// Tuning knobs (block shape / elements per thread): defaults are the
+// measured best on B200; MW_* environment variables override them for
+// sweeps (the profile-building knobs of NEXT-2).
+int tuning_knob(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
 unsigned long long g_launches = 0;
 
 template <typename K>
@@ -81,7 +90,7 @@ unsigned grid_for(int64_t tiles, int per_sm, const Launch& L) {
 
 // ------------------------------------------------------------ saxpy chain
 // y_i <- fma(a_k, x_i, y_i), k = 0..n-1 (R8 single rounding).
-__global__ void __launch_bounds__(256) k_saxpy_vec(SaxpyProg p, const float4* __restrict__ x,
+__global__ void __launch_bounds__(256) k_saxpy_vec(const __grid_constant__ SaxpyProg p, const float4* __restrict__ x,
                                                    float4* __restrict__ y, int64_t nvec) {
     for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * 256) {
         uint4 xr = ld_stream(reinterpret_cast<const uint4*>(x + i));
@@ -98,7 +107,7 @@ __global__ void __launch_bounds__(256) k_saxpy_vec(SaxpyProg p, const float4* __
         y[i] = yv;
     }
 }
-__global__ void k_saxpy_scalar(SaxpyProg p, const float* __restrict__ x, float* __restrict__ y,
+__global__ void k_saxpy_scalar(const __grid_constant__ SaxpyProg p, const float* __restrict__ x, float* __restrict__ y,
                                int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -170,7 +179,8 @@ __device__ __forceinline__ void apply_rgba(const RgbaProg& p, const RgbaConst& c
 
 // 16 B (4 px) per vector; tile = 256 threads x U vectors, grid-stride.
 template <int U>
-__global__ void __launch_bounds__(256) k_rgba_vec(RgbaProg p, RgbaConst c,
+__global__ void __launch_bounds__(256) k_rgba_vec(const __grid_constant__ RgbaProg p,
+                                                  const __grid_constant__ RgbaConst c,
                                                   const uint4* __restrict__ src,
                                                   uint4* __restrict__ dst, uint32_t total,
                                                   FastDiv V, uint32_t W, uint32_t row0W) {
@@ -208,8 +218,99 @@ __global__ void __launch_bounds__(256) k_rgba_vec(RgbaProg p, RgbaConst c,
     }
 }
 
+// ---- specialised fused chain: noise -> solarize (any mirror placement).
+// The fusion planner's most common RGBA program (the Filter Pipeline,
+// P:725-728) gets a straight-line kernel: no per-op dispatch, the mirror and
+// the noise key parity are template parameters, the hash's first xor-shift
+// is folded with the key (K1 = K ^ K>>16), the three field popcounts are
+// taken on left-shifted copies of h (the shifts run on the FMA pipe as
+// IMAD.SHL) with the field differences folded into the noise IMADs, and for
+// T = 128 solarize is min(c, 255 - c) in 16x2 SIMD lanes.
+struct NsConst {
+    uint32_t K1;       // K ^ (K >> 16)
+    uint32_t S;        // noise scale
+    uint32_t S16;      // S << 16
+    uint32_t m5s_rb;   // (-5S) in both 16-bit lanes
+    uint32_t m5s_g;    // (-5S) in the low lane
+    uint32_t cT2, cT1; // general-T solarize constants
+};
+
+template <bool T128>
+__device__ __forceinline__ uint32_t noise_solarize(uint32_t w, uint32_t idx, const NsConst& c) {
+    uint32_t v = idx ^ (idx >> 16) ^ c.K1;
+    v *= 0x7feb352du;
+    v ^= v >> 15;
+    v *= 0x846ca68bu;
+    v ^= v >> 16;
+    const uint32_t p10 = __popc(v << 22);          // bits 0..9   (R)
+    const uint32_t p20 = __popc(v << 12);          // bits 0..19
+    const uint32_t p30 = __popc(v << 2);           // bits 0..29
+    uint32_t rb = w & 0x00FF00FFu;
+    uint32_t ga = __byte_perm(w, 0, 0x4341);
+    rb += p10 * c.S + p30 * c.S16 - p20 * c.S16;   // + pR*S, + pB*S in the high lane
+    ga += p20 * c.S - p10 * c.S;                   // + pG*S
+    // clamp(lane - 5S, 0, 255) in one VIADDMNMX.S16x2.RELU: relu(min(lane - 5S, 255))
+    rb = __viaddmin_s16x2_relu(rb, c.m5s_rb, 0x00FF00FFu);
+    ga = __viaddmin_s16x2_relu(ga, c.m5s_g, 0x00FF00FFu);
+    uint32_t o = rb + ga * 256u;
+    if (T128) {
+        // c >= 128 -> 255 - c == c ^ 0xFF on R, G, B (alpha byte untouched)
+        // byte mask 0xFF where bit 7 is set (R,G,B), 0 for alpha: one PRMT in
+        // sign-replicate mode (selector nibbles 8,9,A = sign of bytes 0,1,2)
+        uint32_t m;
+        asm("prmt.b32 %0, %1, 0, 0x4A98;" : "=r"(m) : "r"(o));
+        o ^= m;
+    } else {
+        uint32_t mrb = ((rb + c.cT2) >> 15) & 0x00010001u;
+        uint32_t mga = ((ga + c.cT1) >> 15) & 0x00000001u;
+        o ^= (mrb + mga * 256u) * 0xFFu;
+    }
+    return o;
+}
+
+template <int U, bool MIRROR, bool KM, bool T128>
+__global__ void __launch_bounds__(256) k_rgba_ns(const __grid_constant__ NsConst c,
+                                                 const uint4* __restrict__ src,
+                                                 uint4* __restrict__ dst, uint32_t total,
+                                                 FastDiv V, uint32_t W, uint32_t row0W) {
+    for (uint32_t t0 = blockIdx.x * (256u * U); t0 < total; t0 += gridDim.x * (256u * U)) {
+        uint4 v[U];
+        uint32_t ib[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t n = t0 + u * 256u + threadIdx.x;
+            if (n < total) {
+                const uint32_t r = fdiv(n, V);
+                const uint32_t cc = n - r * V.d;
+                // global noise index of the output vector's first pixel
+                ib[u] = row0W + r * W + (KM ? (W - 1u - 4u * cc) : 4u * cc);
+                v[u] = ld_stream(src + (MIRROR ? r * V.d + (V.d - 1u - cc) : n));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t n = t0 + u * 256u + threadIdx.x;
+            if (n < total) {
+                uint32_t w0 = v[u].x, w1 = v[u].y, w2 = v[u].z, w3 = v[u].w;
+                if (MIRROR) {
+                    uint32_t t = w0; w0 = w3; w3 = t;
+                    t = w1; w1 = w2; w2 = t;
+                }
+                const uint32_t i0 = ib[u];
+                uint4 o;
+                o.x = noise_solarize<T128>(w0, KM ? i0 : i0, c);
+                o.y = noise_solarize<T128>(w1, KM ? i0 - 1u : i0 + 1u, c);
+                o.z = noise_solarize<T128>(w2, KM ? i0 - 2u : i0 + 2u, c);
+                o.w = noise_solarize<T128>(w3, KM ? i0 - 3u : i0 + 3u, c);
+                st_stream(dst + n, o);
+            }
+        }
+    }
+}
+
 // Any width / alignment: one pixel per element.
-__global__ void __launch_bounds__(256) k_rgba_scalar(RgbaProg p, RgbaConst c,
+__global__ void __launch_bounds__(256) k_rgba_scalar(const __grid_constant__ RgbaProg p,
+                                                     const __grid_constant__ RgbaConst c,
                                                      const uint32_t* __restrict__ src,
                                                      uint32_t* __restrict__ dst, uint32_t total,
                                                      FastDiv Wd, uint32_t row0W) {
@@ -247,21 +348,6 @@ struct U8Const {
     uint32_t lo7[kMaxOps], hi7[kMaxOps];
     int32_t lo_mode[kMaxOps], hi_mode[kMaxOps];
 };
-__device__ __forceinline__ uint32_t apply_u8(const U8Prog& p, const U8Const& c, uint32_t x) {
-    for (int k = 0; k < p.n; ++k) {
-        if (p.kind[k] == U8_SEGMENT) {
-            // R6: v < lo -> 0; lo <= v < hi -> 128; v >= hi -> 255 (lo <= hi)
-            uint32_t flo = ge_t(x, c.lo7[k], c.lo_mode[k]);
-            uint32_t fhi = ge_t(x, c.hi7[k], c.hi_mode[k]);
-            x = flo | (fhi - (fhi >> 7));
-        } else {
-            // R11 finalize: byte == 128 -> 0 (exact zero-byte test on x ^ 0x80)
-            uint32_t z = ~((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & x & 0x80808080u;
-            x &= ~((z >> 7) * 0xFFu);
-        }
-    }
-    return x;
-}
 __device__ __forceinline__ uint8_t apply_u8_byte(const U8Prog& p, uint8_t v) {
     for (int k = 0; k < p.n; ++k) {
         if (p.kind[k] == U8_SEGMENT)
@@ -272,35 +358,78 @@ __device__ __forceinline__ uint8_t apply_u8_byte(const U8Prog& p, uint8_t v) {
     return v;
 }
 
+// Apply one SEGMENT op to N words with its threshold modes fixed at compile
+// time (the per-op dispatch is hoisted out of the word loop).
+template <int LM, int HM, int N>
+__device__ __forceinline__ void seg_words(uint32_t* w, uint32_t lo7, uint32_t hi7) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const uint32_t x = w[i];
+        const uint32_t flo = ge_t(x, lo7, LM), fhi = ge_t(x, hi7, HM);
+        w[i] = flo | (fhi - (fhi >> 7));
+    }
+}
+template <int N>
+__device__ __forceinline__ void seg_dispatch(uint32_t* w, int lm, int hm, uint32_t lo7,
+                                             uint32_t hi7) {
+    switch (lm * 4 + hm) {
+#define MW_SEG_CASE(A, B) \
+    case A * 4 + B: seg_words<A, B, N>(w, lo7, hi7); break;
+        MW_SEG_CASE(0, 0) MW_SEG_CASE(0, 1) MW_SEG_CASE(0, 2) MW_SEG_CASE(0, 3)
+        MW_SEG_CASE(1, 1) MW_SEG_CASE(2, 1) MW_SEG_CASE(2, 2) MW_SEG_CASE(3, 1)
+        MW_SEG_CASE(3, 2) MW_SEG_CASE(3, 3)
+#undef MW_SEG_CASE
+        default: break;   // unreachable for lo <= hi
+    }
+}
+
 template <int U>
-__global__ void __launch_bounds__(256) k_u8_vec(U8Prog p, U8Const c, const uint8_t* __restrict__ src,
-                                                int64_t sp, uint8_t* __restrict__ dst, int64_t dp,
+__global__ void __launch_bounds__(256) k_u8_vec(const __grid_constant__ U8Prog p,
+                                                const __grid_constant__ U8Const c,
+                                                const uint8_t* __restrict__ src, int64_t sp,
+                                                uint8_t* __restrict__ dst, int64_t dp,
                                                 uint32_t total, FastDiv V) {
     for (uint32_t t0 = blockIdx.x * (256u * U); t0 < total; t0 += gridDim.x * (256u * U)) {
-        uint4 v[U];
+        uint32_t w[4 * U];
         uint32_t row[U], col[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            uint32_t n = t0 + u * 256u + threadIdx.x;
+            const uint32_t n = t0 + u * 256u + threadIdx.x;
+            uint4 v = make_uint4(0, 0, 0, 0);
             if (n < total) {
-                uint32_t r = fdiv(n, V);
+                const uint32_t r = fdiv(n, V);
                 row[u] = r;
                 col[u] = n - r * V.d;
-                v[u] = ld_stream(reinterpret_cast<const uint4*>(src + r * sp) + col[u]);
+                v = ld_stream(reinterpret_cast<const uint4*>(src + r * sp) + col[u]);
+            }
+            w[4 * u] = v.x;
+            w[4 * u + 1] = v.y;
+            w[4 * u + 2] = v.z;
+            w[4 * u + 3] = v.w;
+        }
+        for (int k = 0; k < p.n; ++k) {
+            if (p.kind[k] == U8_SEGMENT) {
+                seg_dispatch<4 * U>(w, c.lo_mode[k], c.hi_mode[k], c.lo7[k], c.hi7[k]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4 * U; ++i) {
+                    // R11 finalize: byte == 128 -> 0 (exact zero-byte test on x ^ 0x80)
+                    const uint32_t x = w[i];
+                    const uint32_t z = ~((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & x & 0x80808080u;
+                    w[i] = x & ~((z >> 7) * 0xFFu);
+                }
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            uint32_t n = t0 + u * 256u + threadIdx.x;
-            if (n < total) {
-                uint4 o = make_uint4(apply_u8(p, c, v[u].x), apply_u8(p, c, v[u].y),
-                                     apply_u8(p, c, v[u].z), apply_u8(p, c, v[u].w));
-                st_stream(reinterpret_cast<uint4*>(dst + row[u] * dp) + col[u], o);
-            }
+            const uint32_t n = t0 + u * 256u + threadIdx.x;
+            if (n < total)
+                st_stream(reinterpret_cast<uint4*>(dst + row[u] * dp) + col[u],
+                          make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]));
         }
     }
 }
-__global__ void k_u8_scalar(U8Prog p, const uint8_t* __restrict__ src, int64_t sp,
+__global__ void k_u8_scalar(const __grid_constant__ U8Prog p, const uint8_t* __restrict__ src, int64_t sp,
                             uint8_t* __restrict__ dst, int64_t dp, int64_t rows, int64_t W) {
     int64_t total = rows * W;
     for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < total;
@@ -349,17 +478,40 @@ __device__ __forceinline__ Row4 hmask(const uint4& v, uint32_t left_word, uint32
     return h;
 }
 
-__global__ void __launch_bounds__(kStencilThreads) k_hyst_step(const uint8_t* __restrict__ in,
-                                                               uint8_t* __restrict__ out,
-                                                               int64_t rows, int64_t pitch,
-                                                               int iter, int* last_changed,
-                                                               int64_t n_strips, int64_t n_colblk) {
+// Active-tile Jacobi: a tile whose 3x3 tile neighbourhood changed nothing
+// in the previous execution is already at the next state in the output
+// buffer (state_{k-1} == state_k == state_{k+1} there), so it is skipped —
+// the iterates, the fixed point and E are exactly those of dense Jacobi.
+// prev_flags == nullptr: every tile is active (first execution).
+__global__ void __launch_bounds__(kStencilThreads) k_hyst_step(
+    const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t rows, int64_t pitch,
+    int iter, int* last_changed, int64_t n_strips, int64_t n_colblk,
+    const uint8_t* __restrict__ prev_flags, uint8_t* __restrict__ cur_flags, int top_nbr,
+    int bot_nbr) {
     const int lane = threadIdx.x & 31;
     const int64_t segs = pitch >> 4;  // 16-byte segments per row
     const int64_t n_tiles = n_strips * n_colblk;
-    uint32_t changed = 0;
+    __shared__ int any_changed;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int64_t strip = t / n_colblk, cb = t - strip * n_colblk;
+        bool active = prev_flags == nullptr || (top_nbr && strip == 0) ||
+                      (bot_nbr && strip == n_strips - 1);
+        if (!active) {
+            for (int64_t ds = -1; ds <= 1 && !active; ++ds)
+                for (int64_t dc = -1; dc <= 1; ++dc) {
+                    const int64_t s2 = strip + ds, c2 = cb + dc;
+                    if (s2 >= 0 && s2 < n_strips && c2 >= 0 && c2 < n_colblk &&
+                        prev_flags[s2 * n_colblk + c2]) {
+                        active = true;
+                        break;
+                    }
+                }
+        }
+        if (!active) {   // uniform over the CTA
+            if (threadIdx.x == 0) cur_flags[t] = 0;
+            continue;
+        }
+        uint32_t changed = 0;
         const int64_t seg = cb * kStencilThreads + threadIdx.x;
         const bool valid = seg < segs;
         const int64_t y0 = strip * kStencilRows;                 // first interior row
@@ -397,18 +549,64 @@ __global__ void __launch_bounds__(kStencilThreads) k_hyst_step(const uint8_t* __
             hprev = hcur;
             hcur = hnext;
         }
+        const int tile_changed = __syncthreads_or(changed != 0);
+        if (threadIdx.x == 0) {
+            cur_flags[t] = (uint8_t)tile_changed;
+            if (tile_changed) atomicMax(last_changed, iter);
+        }
     }
-    if (__any_sync(0xffffffffu, changed != 0) && lane == 0) atomicMax(last_changed, iter);
 }
 
 // ------------------------------------------------------------ N-body
 // a_i = sum_j m_j d_ij (|d_ij|^2 + eps2)^-3/2 (R12): fp32 inside each
 // 256-source tile (global tile boundaries, so results do not depend on the
-// partitioning), fp64 across tiles.  Two bodies per thread amortise the
+// partitioning), fp64 across tiles.  Four bodies per thread amortise the
 // shared-memory broadcast loads; MUFU.RSQ for the inverse square root.
 constexpr int kNbTile = 256;
-constexpr int kNbPer = 2;
+constexpr int kNbPairs = 2;               // body pairs per thread (4 bodies)
+constexpr int kNbPer = 2 * kNbPairs;
 
+// Packed FP32x2 arithmetic (sm_100a FADD2/FMUL2/FFMA2): one instruction
+// updates a pair of bodies; scalar operands are broadcast by ptxas.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+    f2_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
+    f2_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+    f2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_mufu(float x) {
+    float r;  // MUFU.RSQ; x >= eps2 > 0 is never denormal, so .ftz is exact here
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Per interaction (for each body of a pair, in FP32x2 lanes):
+//   d = p_j - p_i;  r2 = dx*dx + (dy*dy + (dz*dz + eps2));  inv = rsqrt(r2)
+//   w = (m_j * inv) * (inv * inv);  f += d * w
+// = 6 packed ops per coordinate triple + 6 more: 12 FP32x2 + 2 MUFU per pair.
 __global__ void __launch_bounds__(kNbTile) k_nbody(const float4* __restrict__ pos,
                                                    const float4* __restrict__ vel,
                                                    float4* __restrict__ pos_out,
@@ -417,64 +615,92 @@ __global__ void __launch_bounds__(kNbTile) k_nbody(const float4* __restrict__ po
                                                    int64_t count, int64_t N, float eps2, float dt,
                                                    int mode) {
     __shared__ float4 sp[kNbTile];
+    __shared__ float2 bp[3][kNbPairs][kNbTile];
     const int64_t per_blk = (int64_t)kNbTile * kNbPer;
     const int64_t nblk = (count + per_blk - 1) / per_blk;
     for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
-        float4 pi[kNbPer];
-        int64_t idx[kNbPer];
         double ax[kNbPer], ay[kNbPer], az[kNbPer];
+        // body positions live only as packed pairs (one aligned register pair each)
+        f2_t px[kNbPairs], py[kNbPairs], pz[kNbPairs];
+        // stage the pairs through shared memory so each lands in an aligned
+        // register pair straight from an LDS.64 (no per-use re-pairing MOVs)
+        __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kNbPer; ++q) {
-            int64_t l = b * per_blk + q * kNbTile + threadIdx.x;
-            idx[q] = first + l;
-            pi[q] = l < count ? pos[first + l] : make_float4(0.f, 0.f, 0.f, 0.f);
-            ax[q] = ay[q] = az[q] = 0.0;
+        for (int h = 0; h < kNbPairs; ++h) {
+            float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f), b4 = a4;
+            const int64_t la = b * per_blk + (2 * h) * kNbTile + threadIdx.x;
+            const int64_t lb = la + kNbTile;
+            if (la < count) a4 = pos[first + la];
+            if (lb < count) b4 = pos[first + lb];
+            bp[0][h][threadIdx.x] = make_float2(a4.x, b4.x);
+            bp[1][h][threadIdx.x] = make_float2(a4.y, b4.y);
+            bp[2][h][threadIdx.x] = make_float2(a4.z, b4.z);
         }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < kNbPairs; ++h) {
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(px[h]) : "r"((unsigned)__cvta_generic_to_shared(&bp[0][h][threadIdx.x])));
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(py[h]) : "r"((unsigned)__cvta_generic_to_shared(&bp[1][h][threadIdx.x])));
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(pz[h]) : "r"((unsigned)__cvta_generic_to_shared(&bp[2][h][threadIdx.x])));
+        }
+#pragma unroll
+        for (int q = 0; q < kNbPer; ++q) ax[q] = ay[q] = az[q] = 0.0;
+        const f2_t e2 = f2_pack(eps2, eps2);
         for (int64_t jt = 0; jt < N; jt += kNbTile) {
             __syncthreads();
-            int64_t j = jt + threadIdx.x;
-            sp[threadIdx.x] = j < N ? pos[j] : make_float4(0.f, 0.f, 0.f, 0.f);  // mass 0 pads
+            const int64_t j = jt + threadIdx.x;
+            sp[threadIdx.x] = j < N ? pos[j] : make_float4(0.f, 0.f, 0.f, 0.f);  // mass-0 pads
             __syncthreads();
-            float fx[kNbPer], fy[kNbPer], fz[kNbPer];
+            f2_t fx[kNbPairs], fy[kNbPairs], fz[kNbPairs];
 #pragma unroll
-            for (int q = 0; q < kNbPer; ++q) fx[q] = fy[q] = fz[q] = 0.f;
+            for (int h = 0; h < kNbPairs; ++h) fx[h] = fy[h] = fz[h] = 0ull;
 #pragma unroll 8
             for (int k = 0; k < kNbTile; ++k) {
-                float4 s = sp[k];
+                const float4 s4 = sp[k];
+                const f2_t sx = f2_pack(s4.x, s4.x), sy = f2_pack(s4.y, s4.y),
+                           sz = f2_pack(s4.z, s4.z), sw = f2_pack(s4.w, s4.w);
 #pragma unroll
-                for (int q = 0; q < kNbPer; ++q) {
-                    float dx = s.x - pi[q].x, dy = s.y - pi[q].y, dz = s.z - pi[q].z;
-                    float r2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmaf_rn(dz, dz, eps2)));
-                    float inv = rsqrtf(r2);
-                    float w = s.w * inv * inv * inv;
-                    fx[q] = __fmaf_rn(dx, w, fx[q]);
-                    fy[q] = __fmaf_rn(dy, w, fy[q]);
-                    fz[q] = __fmaf_rn(dz, w, fz[q]);
+                for (int h = 0; h < kNbPairs; ++h) {
+                    const f2_t dx = f2_sub(sx, px[h]), dy = f2_sub(sy, py[h]),
+                               dz = f2_sub(sz, pz[h]);
+                    const f2_t r2 = f2_fma(dx, dx, f2_fma(dy, dy, f2_fma(dz, dz, e2)));
+                    float r0, r1;
+                    f2_unpack(r2, r0, r1);
+                    const f2_t inv = f2_pack(rsqrt_mufu(r0), rsqrt_mufu(r1));
+                    const f2_t w = f2_mul(f2_mul(sw, inv), f2_mul(inv, inv));
+                    fx[h] = f2_fma(dx, w, fx[h]);
+                    fy[h] = f2_fma(dy, w, fy[h]);
+                    fz[h] = f2_fma(dz, w, fz[h]);
                 }
             }
 #pragma unroll
-            for (int q = 0; q < kNbPer; ++q) {
-                ax[q] += (double)fx[q];
-                ay[q] += (double)fy[q];
-                az[q] += (double)fz[q];
+            for (int h = 0; h < kNbPairs; ++h) {
+                float x0, x1, y0, y1, z0, z1;
+                f2_unpack(fx[h], x0, x1);
+                f2_unpack(fy[h], y0, y1);
+                f2_unpack(fz[h], z0, z1);
+                ax[2 * h] += (double)x0; ax[2 * h + 1] += (double)x1;
+                ay[2 * h] += (double)y0; ay[2 * h + 1] += (double)y1;
+                az[2 * h] += (double)z0; az[2 * h + 1] += (double)z1;
             }
         }
 #pragma unroll
         for (int q = 0; q < kNbPer; ++q) {
-            int64_t l = idx[q] - first;
+            const int64_t l = b * per_blk + q * kNbTile + threadIdx.x;
             if (l >= count) continue;
-            int64_t i = idx[q];
+            const int64_t i = first + l;
             if (mode == 1) {
                 acc_out[l] = make_float4((float)ax[q], (float)ay[q], (float)az[q], 0.f);
             } else {
-                float4 v = vel[i];
-                double d = (double)dt;
-                double vx = (double)v.x + ax[q] * d, vy = (double)v.y + ay[q] * d,
-                       vz = (double)v.z + az[q] * d;
+                const float4 v = vel[i];
+                const float4 pq = pos[i];
+                const double d = (double)dt;
+                const double vx = (double)v.x + ax[q] * d, vy = (double)v.y + ay[q] * d,
+                             vz = (double)v.z + az[q] * d;
                 vel_out[i] = make_float4((float)vx, (float)vy, (float)vz, v.w);
-                pos_out[i] = make_float4((float)((double)pi[q].x + vx * d),
-                                         (float)((double)pi[q].y + vy * d),
-                                         (float)((double)pi[q].z + vz * d), pi[q].w);
+                pos_out[i] = make_float4((float)((double)pq.x + vx * d),
+                                         (float)((double)pq.y + vy * d),
+                                         (float)((double)pq.z + vz * d), pq.w);
             }
         }
     }
@@ -626,6 +852,51 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
     const uint32_t row0W = (uint32_t)(row0 * W);
     const bool vec = (W % 4 == 0) &&
                      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    if (vec && p.n == 2 && p.kind[0] == RGBA_NOISE && p.kind[1] == RGBA_SOLARIZE) {
+        NsConst nc;
+        const uint32_t K = p.key[0], S = (uint32_t)p.param[0];
+        nc.K1 = K ^ (K >> 16);
+        nc.S = S;
+        nc.S16 = S << 16;
+        nc.m5s_rb = c.m5s_rb[0];
+        nc.m5s_g = c.m5s_g[0];
+        nc.cT2 = c.cT2[1];
+        nc.cT1 = c.cT1[1];
+        const bool t128 = p.param[1] == 128;
+        const uint32_t total = (uint32_t)(rows * W / 4);
+        const FastDiv V = make_fastdiv((uint32_t)(W / 4));
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        static const int unroll = tuning_knob("MW_RGBA_UNROLL", 2);
+#define MW_NS_LAUNCH_U(U, MI, KMI, TI)                                                    \
+    do {                                                                                  \
+        static int occ = resident_ctas(k_rgba_ns<U, MI, KMI, TI>, 256);                   \
+        const int64_t tiles = (total + 256 * U - 1) / (256 * U);                          \
+        ++g_launches;                                                                     \
+        k_rgba_ns<U, MI, KMI, TI><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(         \
+            nc, s4, d4, total, V, (uint32_t)W, row0W);                                    \
+    } while (0)
+#define MW_NS_LAUNCH(MI, KMI, TI)                                                         \
+    do {                                                                                  \
+        if (unroll == 2) MW_NS_LAUNCH_U(2, MI, KMI, TI);                                  \
+        else if (unroll == 8) MW_NS_LAUNCH_U(8, MI, KMI, TI);                             \
+        else MW_NS_LAUNCH_U(4, MI, KMI, TI);                                              \
+    } while (0)
+        const int sel = (p.mirror ? 4 : 0) | (p.key_mirror[0] ? 2 : 0) | (t128 ? 1 : 0);
+        switch (sel) {
+            case 0: MW_NS_LAUNCH(false, false, false); break;
+            case 1: MW_NS_LAUNCH(false, false, true); break;
+            case 2: MW_NS_LAUNCH(false, true, false); break;
+            case 3: MW_NS_LAUNCH(false, true, true); break;
+            case 4: MW_NS_LAUNCH(true, false, false); break;
+            case 5: MW_NS_LAUNCH(true, false, true); break;
+            case 6: MW_NS_LAUNCH(true, true, false); break;
+            default: MW_NS_LAUNCH(true, true, true); break;
+        }
+#undef MW_NS_LAUNCH
+#undef MW_NS_LAUNCH_U
+        return cudaGetLastError();
+    }
     if (vec) {
         constexpr int U = 4;
         static int occ = resident_ctas(k_rgba_vec<U>, 256);
@@ -677,8 +948,14 @@ cudaError_t u8_chain(const U8Prog& p, const uint8_t* src, int64_t sp, uint8_t* d
     return cudaGetLastError();
 }
 
+int64_t hyst_tiles(int64_t rows, int64_t pitch) {
+    return ((rows + kStencilRows - 1) / kStencilRows) *
+           ((pitch / 16 + kStencilThreads - 1) / kStencilThreads);
+}
+
 cudaError_t hyst_step(const uint8_t* in, uint8_t* out, int64_t rows, int64_t pitch, int iter,
-                      int* last_changed, const Launch& L) {
+                      int* last_changed, const uint8_t* prev_flags, uint8_t* cur_flags,
+                      int top_nbr, int bot_nbr, const Launch& L) {
     if (rows <= 0) return cudaSuccess;
     if (pitch % 16 != 0) return cudaErrorInvalidValue;
     static int occ = resident_ctas(k_hyst_step, kStencilThreads);
@@ -686,7 +963,8 @@ cudaError_t hyst_step(const uint8_t* in, uint8_t* out, int64_t rows, int64_t pit
     int64_t colblk = (pitch / 16 + kStencilThreads - 1) / kStencilThreads;
     ++g_launches;
     k_hyst_step<<<grid_for(strips * colblk, occ, L), kStencilThreads, 0, L.stream>>>(
-        in, out, rows, pitch, iter, last_changed, strips, colblk);
+        in, out, rows, pitch, iter, last_changed, strips, colblk, prev_flags, cur_flags, top_nbr,
+        bot_nbr);
     return cudaGetLastError();
 }
 

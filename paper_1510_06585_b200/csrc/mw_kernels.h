@@ -54,9 +54,15 @@ cudaError_t u8_chain(const U8Prog& p, const uint8_t* src, int64_t src_pitch, uin
 // ------------------------------------------------------------ hysteresis stencil
 // One Jacobi step over `rows` interior rows.  in/out point at halo row -1 of
 // buffers of (rows + 2) x pitch bytes (pitch % 16 == 0, pad columns zero).
-// Any changed pixel does atomicMax(last_changed, iter).
+// Any changed pixel does atomicMax(last_changed, iter).  Tiles whose 3x3
+// neighbourhood did not change in the previous execution (prev_flags, one
+// byte per tile; nullptr = all active) are skipped; cur_flags receives this
+// execution's per-tile change flags.  top_nbr/bot_nbr: the partition has a
+// neighbour whose halo row may change (its boundary tiles always run).
+int64_t hyst_tiles(int64_t rows, int64_t pitch);
 cudaError_t hyst_step(const uint8_t* in, uint8_t* out, int64_t rows, int64_t pitch, int iter,
-                      int* last_changed, const Launch& L);
+                      int* last_changed, const uint8_t* prev_flags, uint8_t* cur_flags,
+                      int top_nbr, int bot_nbr, const Launch& L);
 
 // ------------------------------------------------------------ N-body
 // Bodies [first, first+count) of N: direct-sum acceleration (fp32 per

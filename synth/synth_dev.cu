@@ -15,19 +15,19 @@ __device__ __forceinline__ uint64_t sm64(uint64_t s, uint64_t i) {
     return z ^ (z >> 31);
 }
 
-__global__ void k_f32_um11(uint64_t seed, uint64_t start, uint64_t n, float* out) {
+__global__ void synth_gen_f32_um11(uint64_t seed, uint64_t start, uint64_t n, float* out) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x)
         out[k] = (float)(sm64(seed, start + k) >> 40) * (1.0f / 8388608.0f) - 1.0f;
 }
 
-__global__ void k_f32_u01(uint64_t seed, uint64_t start, uint64_t n, float* out) {
+__global__ void synth_gen_f32_u01(uint64_t seed, uint64_t start, uint64_t n, float* out) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x)
         out[k] = (float)(sm64(seed, start + k) >> 40) * (1.0f / 16777216.0f);
 }
 
-__global__ void k_u8(uint64_t seed, uint64_t start, uint64_t n, uint8_t* out) {
+__global__ void synth_gen_u8(uint64_t seed, uint64_t start, uint64_t n, uint8_t* out) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t v = start + k;
@@ -35,7 +35,7 @@ __global__ void k_u8(uint64_t seed, uint64_t start, uint64_t n, uint8_t* out) {
     }
 }
 
-__global__ void k_rgba(uint64_t seed, uint64_t start, uint64_t n, uint32_t* out) {
+__global__ void synth_gen_rgba(uint64_t seed, uint64_t start, uint64_t n, uint32_t* out) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t z = sm64(seed, start + k);
@@ -43,7 +43,7 @@ __global__ void k_rgba(uint64_t seed, uint64_t start, uint64_t n, uint32_t* out)
     }
 }
 
-__global__ void k_nbody(uint64_t seed, uint64_t start, uint64_t n, float mass,
+__global__ void synth_gen_nbody(uint64_t seed, uint64_t start, uint64_t n, float mass,
                         float4* pos, float4* vel) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x) {
@@ -76,21 +76,21 @@ inline unsigned grid_for(uint64_t n) {
 extern "C" {
 
 int synth_dev_f32_um11(uint64_t seed, uint64_t start, uint64_t count, float* out, void* stream) {
-    SYNTH_RET((k_f32_um11<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start, count, out)));
+    SYNTH_RET((synth_gen_f32_um11<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start, count, out)));
 }
 int synth_dev_f32_u01(uint64_t seed, uint64_t start, uint64_t count, float* out, void* stream) {
-    SYNTH_RET((k_f32_u01<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start, count, out)));
+    SYNTH_RET((synth_gen_f32_u01<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start, count, out)));
 }
 int synth_dev_u8_stream(uint64_t seed, uint64_t start, uint64_t count, uint8_t* out, void* stream) {
-    SYNTH_RET((k_u8<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start, count, out)));
+    SYNTH_RET((synth_gen_u8<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start, count, out)));
 }
 int synth_dev_rgba(uint64_t seed, uint64_t start_px, uint64_t count, uint8_t* out, void* stream) {
-    SYNTH_RET((k_rgba<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start_px, count,
+    SYNTH_RET((synth_gen_rgba<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(seed, start_px, count,
                                                                          (uint32_t*)out)));
 }
 int synth_dev_nbody(uint64_t seed, uint64_t start, uint64_t count, float mass, float* pos4,
                     float* vel4, void* stream) {
-    SYNTH_RET((k_nbody<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(
+    SYNTH_RET((synth_gen_nbody<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(
         seed, start, count, mass, (float4*)pos4, (float4*)vel4)));
 }
 

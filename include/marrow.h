@@ -223,6 +223,26 @@ mw_status mw_future_query(mw_future* f, int32_t* done);
 mw_status mw_future_result(mw_future* f, double* out, int32_t n);
 void mw_future_release(mw_future* f);
 
+/* ------------------------------------------------------------------ graphs
+ * A built SCT receives many execution requests over time.
+ * mw_graph_capture records one run of `root` on `args` into a CUDA graph
+ * (the partition under the current distribution is frozen into it); each
+ * mw_graph_launch replays exactly that run on the same buffers with no host
+ * work (for launch-bound trees and small partitions).  `stream` must not be
+ * the legacy default stream.  MW_E_UNSUPPORTED for host-resident args and
+ * for while-loops whose condition needs the host (multi-partition byte
+ * stencil); the one-partition hysteresis loop runs on the device and is
+ * capturable.  Timing events are not recorded inside graphs.               */
+typedef struct mw_graph mw_graph;
+mw_status mw_graph_capture(mw_ctx* ctx, const mw_node* root, const mw_arg* args, int32_t nargs,
+                           void* stream, mw_graph** out);
+mw_status mw_graph_launch(mw_graph* g, void* stream);
+/* Results of the most recent replay (same layout as mw_future_result); call
+ * after the launch stream has synchronised.                                */
+mw_status mw_graph_result(mw_graph* g, double* out, int32_t n);
+mw_status mw_graph_kernels(const mw_graph* g, int64_t* kernels_per_replay);
+mw_status mw_graph_destroy(mw_graph* g);
+
 /* ------------------------------------------------------------------ monitor / balance
  * Per-partition compute times of the last completed run (events placed
  * around each partition's kernels, before any collective wait),

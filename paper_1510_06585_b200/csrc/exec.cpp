@@ -98,13 +98,15 @@ struct mw_ctx {
     cudaStream_t copy_in = nullptr, copy_out = nullptr, aux = nullptr;
     cudaEvent_t st_in[kStageSlots]{}, st_comp[kStageSlots]{}, st_out[kStageSlots]{};
     cudaEvent_t st_start = nullptr;
+    bool capturing = false;     // inside mw_graph_capture: no timing events, no host syncs
 };
 
 struct mw_future {
     mw_ctx* ctx = nullptr;
     cudaEvent_t done = nullptr;
-    double* res = nullptr;     // pinned slot: [reduced]
+    double* res = nullptr;     // pinned slot (4 x 8 B): [0] reduced, [1] plane-loop {E, converged} int32
     bool has_reduce = false;
+    bool plane_loop = false;
     double executions = 0.0;
     double converged = 1.0;
     bool waited = false;
@@ -165,11 +167,14 @@ struct PartTimer {
     cudaEvent_t a;
     unsigned long long l0;
     PartTimer(mw_ctx* c_, cudaStream_t s_, int p, int cl) : c(c_), s(s_), part(p), cls(cl) {
+        a = nullptr;
+        l0 = mwk::launch_count();
+        if (c->capturing) return;
         a = next_event(c);
         cudaEventRecord(a, s);
-        l0 = mwk::launch_count();
     }
     ~PartTimer() {
+        if (c->capturing) return;
         cudaEvent_t b = next_event(c);
         cudaEventRecord(b, s);
         mw_ctx::Rec r{part, cls, a, b, (int64_t)(mwk::launch_count() - l0)};
@@ -390,6 +395,79 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
     });
     const int64_t W = inner;               // 2-D when a stencil is present (validated)
     const int64_t pitch = (W + 15) / 16 * 16;
+    // ---- bit-plane path: one partition on this device, pattern
+    //      [u8 chain ending with the threshold] -> stencil loop -> [u8 chain]
+    {
+        int sidx = -1, nst = 0;
+        for (size_t i = 0; i < prog.size(); ++i)
+            if (prog[i].kind == StepKind::StencilFor || prog[i].kind == StepKind::StencilWhile) {
+                sidx = (int)i;
+                ++nst;
+            }
+        static const bool planes_on = [] {
+            const char* v = getenv("MW_HYST_PLANES");
+            return !(v && v[0] == '0');
+        }();
+        const int p0 = R.first;
+        const bool eligible = planes_on && nst == 1 && sidx == 1 && c->nranks == 1 && ppr == 1 &&
+                              prog[0].kind == StepKind::U8 && !prog[0].ops.empty() &&
+                              prog[0].ops.back().kind == mw::LeafKind::Segment &&
+                              (int)prog.size() <= 3 && R.len[p0] > 0 &&
+                              (prog.size() == 2 || prog[2].kind == StepKind::U8);
+        if (eligible) {
+            const int64_t rows = R.len[p0];
+            const int64_t wp = mwk::plane_words(W);
+            const size_t pb = (size_t)(rows + 2) * wp * 4;
+            void *s0, *s1, *kk, *fl;
+            MW_OK_OR_RETURN(scratch(c, "plane_s0", pb, R.s, &s0));
+            MW_OK_OR_RETURN(scratch(c, "plane_s1", pb, R.s, &s1));
+            MW_OK_OR_RETURN(scratch(c, "plane_k", pb, R.s, &kk));
+            MW_OK_OR_RETURN(scratch(c, "plane_flags", 64, R.s, &fl));
+            void* tf;
+            MW_OK_OR_RETURN(scratch(c, "plane_tflags", (size_t)(2 * mwk::planes_tiles(rows, W)), R.s, &tf));
+            uint32_t* S0 = static_cast<uint32_t*>(s0);
+            uint32_t* S1 = static_cast<uint32_t*>(s1);
+            uint32_t* K = static_cast<uint32_t*>(kk);
+            int* flags = static_cast<int*>(fl);
+            int* state = flags + 4;
+            for (uint32_t* b : {S0, S1, K}) {   // zero halo rows (outside the image = 0)
+                CUDA_OK(cudaMemsetAsync(b, 0, wp * 4, R.s));
+                CUDA_OK(cudaMemsetAsync(b + (rows + 1) * wp, 0, wp * 4, R.s));
+            }
+            CUDA_OK(cudaMemsetAsync(flags, 0, 64, R.s));
+            auto pre = u8_groups(prog[0].ops);
+            if (pre.size() != 1) return fail(MW_E_UNSUPPORTED, "chain before the loop > 16 ops");
+            mwk::U8Prog post{};
+            if (prog.size() == 3) {
+                auto g = u8_groups(prog[2].ops);
+                if (g.size() != 1) return fail(MW_E_UNSUPPORTED, "chain after the loop > 16 ops");
+                post = g[0];
+            }
+            const mwk::Launch L = launch_for(c, R.s, p0);
+            {
+                PartTimer t(c, R.s, p0, MW_KC_U8);
+                MW_OK_OR_RETURN(kerr(mwk::planes_pack(pre[0], at_row<const uint8_t>(src, R.off[p0]), inner,
+                                                      rows, W, S0, K, L), "planes_pack"));
+            }
+            {
+                PartTimer t(c, R.s, p0, MW_KC_STENCIL);
+                MW_OK_OR_RETURN(kerr(mwk::planes_loop(S0, S1, K, rows, W, prog[1].n, flags, state,
+                                                      static_cast<uint8_t*>(tf), L),
+                                     "planes_loop"));
+            }
+            {
+                PartTimer t(c, R.s, p0, MW_KC_U8);
+                MW_OK_OR_RETURN(kerr(mwk::planes_unpack(post, S0, S1, K, state,
+                                                        at_row<uint8_t>(dst, R.off[p0]), inner, rows, W, L),
+                                     "planes_unpack"));
+            }
+            if (prog[1].kind == StepKind::StencilWhile) {
+                CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 8, cudaMemcpyDeviceToHost, R.s));
+                f->plane_loop = true;
+            }
+            return MW_OK;
+        }
+    }
     std::vector<Halo> H(ppr);
     if (has_stencil) {
         for (int q = 0; q < ppr; ++q) {
@@ -515,6 +593,10 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
                 MW_OK_OR_RETURN(exchange_halos(R, H, hb, pitch));
             }
             if (!is_while) continue;
+            if (c->capturing)
+                return fail(MW_E_UNSUPPORTED,
+                            "this while-loop evaluates its condition on the host (multi-partition "
+                            "byte stencil) and cannot be captured in a graph");
             // loop condition (P:376 stage 1), reduced over ranks on the device
             if (c->comm)
                 NCCL_OK(ncclAllReduce(d_last, d_last, 1, ncclInt32, ncclMax, c->comm, R.s));
@@ -767,8 +849,10 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
     // ---- execute
     c->recs.clear();
     if (!c->stats_on) c->ev_used = 0;   // events of accumulated stats stay live
-    CUDA_OK(cudaEventRecord(c->wall_a, s));
+    if (!c->capturing) CUDA_OK(cudaEventRecord(c->wall_a, s));
     const int ppr = c->ppr;
+    if (host && c->capturing)
+        return fail(MW_E_UNSUPPORTED, "host-resident arguments cannot be captured in a graph");
     if (host) {
         if (prog.size() != 1 || (prog[0].kind != StepKind::Saxpy && prog[0].kind != StepKind::Rgba &&
                                  prog[0].kind != StepKind::U8))
@@ -860,9 +944,11 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
                                  "fill_traits"));
         }
     }
-    CUDA_OK(cudaEventRecord(c->wall_b, s));
-    c->last_len = R.len;
-    c->have_run = true;
+    if (!c->capturing) {
+        CUDA_OK(cudaEventRecord(c->wall_b, s));
+        c->last_len = R.len;
+        c->have_run = true;
+    }
     return MW_OK;
 }
 
@@ -997,7 +1083,7 @@ mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nar
         double* page;
         CUDA_OK(cudaHostAlloc(&page, 4096, cudaHostAllocDefault));
         c->res_pages.push_back(page);
-        for (int i = 0; i < 512; ++i) c->res_free.push_back(page + i);
+        for (int i = 0; i < 128; ++i) c->res_free.push_back(page + 4 * i);
     }
     f->res = c->res_free.back();
     c->res_free.pop_back();
@@ -1056,8 +1142,14 @@ mw_status mw_future_query(mw_future* f, int32_t* done) {
 mw_status mw_future_result(mw_future* f, double* out, int32_t n) {
     if (!f || !out) return fail(MW_E_STATE, "invalid future");
     if (!f->waited) MW_OK_OR_RETURN(mw_future_wait(f));
+    double ex = f->executions, conv = f->converged;
+    if (f->plane_loop) {
+        const int32_t* st = reinterpret_cast<const int32_t*>(f->res + 1);
+        ex += (double)st[0];
+        if (!st[1]) conv = 0.0;
+    }
     double v[4] = {f->has_reduce ? *f->res : 0.0, (double)(float)(f->has_reduce ? *f->res : 0.0),
-                   f->executions, f->converged};
+                   ex, conv};
     for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
     return MW_OK;
 }
@@ -1171,6 +1263,87 @@ mw_status mw_ctx_set_slowdown(mw_ctx* c, int32_t part, float factor) {
 mw_status mw_ctx_launch_count(const mw_ctx* c, int64_t* out) {
     if (!c || !out) return fail(MW_E_INVALID_SPEC, "NULL argument");
     *out = (int64_t)(mwk::launch_count() - c->launches0);
+    return MW_OK;
+}
+
+
+// ------------------------------------------------------------ graphs
+struct mw_graph {
+    mw_ctx* ctx = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    mw_future f;          // result slot of the captured run
+    int64_t kernels = 0;  // library kernels per replay
+};
+
+mw_status mw_graph_capture(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
+                           void* stream, mw_graph** out) {
+    if (!c || !root || !out || (nargs > 0 && !args)) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    if (!stream) return fail(MW_E_INVALID_SPEC, "graph capture needs a non-default stream");
+    CUDA_OK(cudaSetDevice(c->device));
+    std::unique_ptr<mw_graph> g(new mw_graph);
+    g->ctx = c;
+    g->f.ctx = c;
+    CUDA_OK(cudaHostAlloc(&g->f.res, 32, cudaHostAllocDefault));
+    memset(g->f.res, 0, 32);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned long long l0 = mwk::launch_count();
+    CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    c->capturing = true;
+    mw_status st;
+    try {
+        st = run(c, reinterpret_cast<const Node*>(root), args, nargs, s, &g->f);
+    } catch (...) {
+        st = fail(MW_E_INVALID_SPEC, "internal error");
+    }
+    c->capturing = false;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (st != MW_OK || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaFreeHost(g->f.res);
+        if (st != MW_OK) return st;
+        return fail(MW_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    }
+    g->graph = graph;
+    e = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        cudaFreeHost(g->f.res);
+        return fail(MW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+    g->kernels = (int64_t)(mwk::launch_count() - l0);
+    *out = g.release();
+    return MW_OK;
+}
+
+mw_status mw_graph_launch(mw_graph* g, void* stream) {
+    if (!g || !g->exec) return fail(MW_E_STATE, "invalid graph");
+    CUDA_OK(cudaSetDevice(g->ctx->device));
+    CUDA_OK(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+    return MW_OK;
+}
+
+mw_status mw_graph_result(mw_graph* g, double* out, int32_t n) {
+    if (!g || !out) return fail(MW_E_STATE, "invalid graph");
+    g->f.waited = true;   // the caller synchronised the launch stream
+    return mw_future_result(&g->f, out, n);
+}
+
+mw_status mw_graph_kernels(const mw_graph* g, int64_t* out) {
+    if (!g || !out) return fail(MW_E_STATE, "invalid graph");
+    *out = g->kernels;
+    return MW_OK;
+}
+
+mw_status mw_graph_destroy(mw_graph* g) {
+    if (!g) return fail(MW_E_STATE, "NULL graph");
+    cudaSetDevice(g->ctx->device);
+    cudaDeviceSynchronize();
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->f.res) cudaFreeHost(g->f.res);
+    delete g;
     return MW_OK;
 }
 

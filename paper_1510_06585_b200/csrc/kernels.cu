@@ -10,9 +10,12 @@
 // Definitions follow DESIGN.md §Readings (R1-R12), citing PAPER.md lines.
 #include <cstdint>
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "mw_kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace mwk {
 namespace {
@@ -383,6 +386,23 @@ __device__ __forceinline__ void seg_dispatch(uint32_t* w, int lm, int hm, uint32
     }
 }
 
+template <int N>
+__device__ __forceinline__ void u8_apply_words(const U8Prog& p, const U8Const& c, uint32_t* w) {
+    for (int k = 0; k < p.n; ++k) {
+        if (p.kind[k] == U8_SEGMENT) {
+            seg_dispatch<N>(w, c.lo_mode[k], c.hi_mode[k], c.lo7[k], c.hi7[k]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                // R11 finalize: byte == 128 -> 0 (exact zero-byte test on x ^ 0x80)
+                const uint32_t x = w[i];
+                const uint32_t z = ~((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & x & 0x80808080u;
+                w[i] = x & ~((z >> 7) * 0xFFu);
+            }
+        }
+    }
+}
+
 template <int U>
 __global__ void __launch_bounds__(256) k_u8_vec(const __grid_constant__ U8Prog p,
                                                 const __grid_constant__ U8Const c,
@@ -407,19 +427,7 @@ __global__ void __launch_bounds__(256) k_u8_vec(const __grid_constant__ U8Prog p
             w[4 * u + 2] = v.z;
             w[4 * u + 3] = v.w;
         }
-        for (int k = 0; k < p.n; ++k) {
-            if (p.kind[k] == U8_SEGMENT) {
-                seg_dispatch<4 * U>(w, c.lo_mode[k], c.hi_mode[k], c.lo7[k], c.hi7[k]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4 * U; ++i) {
-                    // R11 finalize: byte == 128 -> 0 (exact zero-byte test on x ^ 0x80)
-                    const uint32_t x = w[i];
-                    const uint32_t z = ~((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & x & 0x80808080u;
-                    w[i] = x & ~((z >> 7) * 0xFFu);
-                }
-            }
-        }
+        u8_apply_words<4 * U>(p, c, w);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t n = t0 + u * 256u + threadIdx.x;
@@ -491,7 +499,6 @@ __global__ void __launch_bounds__(kStencilThreads) k_hyst_step(
     const int lane = threadIdx.x & 31;
     const int64_t segs = pitch >> 4;  // 16-byte segments per row
     const int64_t n_tiles = n_strips * n_colblk;
-    __shared__ int any_changed;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int64_t strip = t / n_colblk, cb = t - strip * n_colblk;
         bool active = prev_flags == nullptr || (top_nbr && strip == 0) ||
@@ -557,6 +564,211 @@ __global__ void __launch_bounds__(kStencilThreads) k_hyst_step(
     }
 }
 
+// ------------------------------------------------------------ hysteresis on bit planes
+// When the labels entering the loop are known to be 3-valued (the stage
+// before the loop ends with the threshold), the loop state is held as two
+// bit planes: S (== 255) and K (== 128, constant).  One Jacobi execution is
+//     S' = S | (K & dilate8(S))
+// on 32 pixels per 32-bit word — the same iterates as the byte stencil, at
+// 1/16 of the bytes (the 16384^2 planes are 32 MiB each and stay in L2).
+// The whole while-loop runs in ONE cooperative kernel: the loop condition is
+// evaluated on the device after a grid-wide barrier every execution (exact,
+// no extra executions, no host round trip).  Plane layout: (rows + 2) x wp
+// words, rows 0 and rows+1 zero halos; bit b of word w is pixel x = 32w + b.
+constexpr int kPlaneRows = 16;   // rows per warp tile
+
+__device__ __forceinline__ uint32_t nib_of(uint32_t flags80) {   // bits 7,15,23,31 -> 4 bits
+    return ((flags80 >> 7) * 0x10204080u) >> 28;
+}
+__device__ __forceinline__ uint32_t expand_nib(uint32_t n) {      // 4 bits -> 0x00/0xFF bytes
+    return ((n * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+
+__global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8Prog p,
+                                                     const __grid_constant__ U8Const c,
+                                                     const uint8_t* __restrict__ src, int64_t sp,
+                                                     int64_t rows, int64_t W, int64_t wp,
+                                                     uint32_t* __restrict__ S,
+                                                     uint32_t* __restrict__ K, FastDiv WP) {
+    const uint32_t total = (uint32_t)(rows * wp);
+    for (uint32_t n = blockIdx.x * 256u + threadIdx.x; n < total; n += gridDim.x * 256u) {
+        const uint32_t y = fdiv(n, WP), w = n - y * WP.d;
+        const int64_t x0 = 32ll * w;
+        const uint8_t* r = src + y * sp + x0;
+        uint32_t v[8];
+        if (x0 + 32 <= W && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
+            const uint4 a = ld_stream(reinterpret_cast<const uint4*>(r));
+            const uint4 b = ld_stream(reinterpret_cast<const uint4*>(r) + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint32_t x = 0;
+                for (int e = 0; e < 4; ++e) {
+                    const int64_t xx = x0 + 4 * i + e;
+                    if (xx < W) x |= (uint32_t)r[4 * i + e] << (8 * e);
+                }
+                v[i] = x;
+            }
+        }
+        u8_apply_words<8>(p, c, v);   // the chain before the loop (ends with the threshold)
+        uint32_t sb = 0, kb = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            sb |= nib_of(is255(v[i])) << (4 * i);
+            kb |= nib_of(is128(v[i])) << (4 * i);
+        }
+        const int64_t rem = W - x0;   // bits beyond the image width stay 0
+        if (rem < 32) {
+            const uint32_t keep = (1u << rem) - 1u;
+            sb &= keep;
+            kb &= keep;
+        }
+        S[(y + 1) * wp + w] = sb;
+        K[(y + 1) * wp + w] = kb;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U8Prog p,
+                                                       const __grid_constant__ U8Const c,
+                                                       const uint32_t* __restrict__ S0,
+                                                       const uint32_t* __restrict__ S1,
+                                                       const uint32_t* __restrict__ K,
+                                                       const int* __restrict__ state,
+                                                       uint8_t* __restrict__ dst, int64_t dp,
+                                                       int64_t rows, int64_t W, int64_t wp,
+                                                       FastDiv WP) {
+    const uint32_t* S = state[2] ? S1 : S0;
+    const uint32_t total = (uint32_t)(rows * wp);
+    for (uint32_t n = blockIdx.x * 256u + threadIdx.x; n < total; n += gridDim.x * 256u) {
+        const uint32_t y = fdiv(n, WP), w = n - y * WP.d;
+        const uint32_t sb = S[(y + 1) * wp + w], kb = K[(y + 1) * wp + w];
+        uint32_t v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t bs = expand_nib((sb >> (4 * i)) & 15u);
+            const uint32_t bk = expand_nib((kb >> (4 * i)) & 15u);
+            v[i] = bs | (bk & 0x80808080u);   // 255 / 128 / 0 labels
+        }
+        u8_apply_words<8>(p, c, v);           // the chain after the loop (finalize, ...)
+        const int64_t x0 = 32ll * w;
+        uint8_t* r = dst + y * dp + x0;
+        if (x0 + 32 <= W && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
+            st_stream(reinterpret_cast<uint4*>(r), make_uint4(v[0], v[1], v[2], v[3]));
+            st_stream(reinterpret_cast<uint4*>(r) + 1, make_uint4(v[4], v[5], v[6], v[7]));
+        } else {
+            for (int e = 0; e < 32 && x0 + e < W; ++e) r[e] = (uint8_t)(v[e >> 2] >> (8 * (e & 3)));
+        }
+    }
+}
+
+// One warp = 32 consecutive words (1024 pixels) x kPlaneRows rows.  All rows
+// of a tile are loaded up front (kPlaneRows + 2 strong words, kPlaneRows weak
+// words, one edge word for lanes 0/31 per row) so a warp keeps ~50 loads in
+// flight.  Active tiles only: a tile whose 3x3 tile neighbourhood did not
+// change in the previous execution already holds the next state in both
+// buffers and is skipped (exact, as for the byte stencil).
+// state = {E, converged, final buffer index}; tflags: 2 x n_tiles bytes.
+__global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
+                                                     uint32_t* __restrict__ S1,
+                                                     const uint32_t* __restrict__ K, int64_t rows,
+                                                     int64_t wp, int64_t max_iters,
+                                                     int* __restrict__ flags,
+                                                     int* __restrict__ state,
+                                                     uint8_t* __restrict__ tflags) {
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    const int64_t n_strips = (rows + kPlaneRows - 1) / kPlaneRows;
+    const int64_t n_cb = (wp + 31) / 32;
+    const int64_t n_tiles = n_strips * n_cb;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    for (int64_t k = 0; k < max_iters; ++k) {
+        const uint32_t* in = (k & 1) ? S1 : S0;
+        uint32_t* out = (k & 1) ? S0 : S1;
+        const uint8_t* fprev = tflags + ((k + 1) & 1) * n_tiles;
+        uint8_t* fcur = tflags + (k & 1) * n_tiles;
+        if (leader) flags[(k + 1) % 3] = 0;   // last read two barriers ago
+        bool ch_any = false;
+        for (int64_t t = gw; t < n_tiles; t += nwarps) {
+            const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+            bool act = k == 0;
+            if (!act) {
+                bool a = false;
+                if (lane < 9) {
+                    const int64_t s2 = strip + lane / 3 - 1, c2 = cb + lane % 3 - 1;
+                    a = s2 >= 0 && s2 < n_strips && c2 >= 0 && c2 < n_cb && fprev[s2 * n_cb + c2];
+                }
+                act = __any_sync(0xffffffffu, a);
+            }
+            if (!act) {
+                if (lane == 0) fcur[t] = 0;
+                continue;
+            }
+            const int64_t w = cb * 32 + lane;
+            const bool valid = w < wp;
+            const bool edge_l = lane == 0, edge_r = lane == 31 || w + 1 == wp;
+            const int64_t y0 = strip * kPlaneRows;
+            uint32_t sv[kPlaneRows + 2], ev[kPlaneRows + 2], kv[kPlaneRows];
+#pragma unroll
+            for (int i = 0; i < kPlaneRows + 2; ++i) {
+                const int64_t y = y0 - 1 + i;              // -1 .. y0+kPlaneRows
+                const bool ok = valid && y <= rows;        // y == rows is the zero halo row
+                const uint32_t* r = in + (y + 1) * wp;
+                sv[i] = ok ? r[w] : 0u;
+                ev[i] = 0u;
+                if (ok && edge_l && w > 0) ev[i] = r[w - 1];
+                if (ok && edge_r && !edge_l && w + 1 < wp) ev[i] = r[w + 1];
+            }
+#pragma unroll
+            for (int i = 0; i < kPlaneRows; ++i) {
+                const int64_t y = y0 + i;
+                kv[i] = (valid && y < rows) ? K[(y + 1) * wp + w] : 0u;
+            }
+            uint32_t hv[kPlaneRows + 2];
+#pragma unroll
+            for (int i = 0; i < kPlaneRows + 2; ++i) {   // dilate8 horizontally
+                const uint32_t s = sv[i];
+                uint32_t l = __shfl_up_sync(0xffffffffu, s, 1);
+                uint32_t r = __shfl_down_sync(0xffffffffu, s, 1);
+                if (edge_l) l = ev[i];
+                if (edge_r) r = edge_l ? 0u : ev[i];
+                hv[i] = s | __funnelshift_l(l, s, 1) | __funnelshift_r(s, r, 1);
+            }
+            uint32_t ch = 0;
+#pragma unroll
+            for (int i = 0; i < kPlaneRows; ++i) {
+                const int64_t y = y0 + i;
+                if (valid && y < rows) {
+                    const uint32_t s2 = sv[i + 1] | (kv[i] & (hv[i] | hv[i + 1] | hv[i + 2]));
+                    ch |= s2 ^ sv[i + 1];
+                    out[(y + 1) * wp + w] = s2;
+                }
+            }
+            const bool tch = __any_sync(0xffffffffu, ch != 0);
+            if (lane == 0) fcur[t] = (uint8_t)tch;
+            ch_any |= tch;
+        }
+        if (ch_any && lane == 0) atomicExch(&flags[k % 3], 1);
+        grid.sync();
+        if (*((volatile int*)&flags[k % 3]) == 0) {   // execution k changed nothing
+            if (leader) {
+                state[0] = (int)(k + 1);
+                state[1] = 1;
+                state[2] = (k & 1) ? 0 : 1;
+            }
+            return;
+        }
+    }
+    if (leader) {
+        state[0] = (int)max_iters;
+        state[1] = 0;
+        state[2] = max_iters == 0 ? 0 : (((max_iters - 1) & 1) ? 0 : 1);
+    }
+}
+
 // ------------------------------------------------------------ N-body
 // a_i = sum_j m_j d_ij (|d_ij|^2 + eps2)^-3/2 (R12): fp32 inside each
 // 256-source tile (global tile boundaries, so results do not depend on the
@@ -576,11 +788,6 @@ __device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
 }
 __device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
     asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
-    f2_t r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
 }
 __device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
     f2_t r;
@@ -966,6 +1173,63 @@ cudaError_t hyst_step(const uint8_t* in, uint8_t* out, int64_t rows, int64_t pit
         in, out, rows, pitch, iter, last_changed, strips, colblk, prev_flags, cur_flags, top_nbr,
         bot_nbr);
     return cudaGetLastError();
+}
+
+static U8Const u8_consts(const U8Prog& p) {
+    U8Const c;
+    auto mode = [](int t) { return t <= 0 ? 0 : (t >= 256 ? 1 : (t >= 128 ? 2 : 3)); };
+    for (int k = 0; k < p.n; ++k) {
+        c.lo_mode[k] = mode(p.lo[k]);
+        c.hi_mode[k] = mode(p.hi[k]);
+        c.lo7[k] = (uint32_t)(p.lo[k] & 0x7F) * 0x01010101u;
+        c.hi7[k] = (uint32_t)(p.hi[k] & 0x7F) * 0x01010101u;
+    }
+    return c;
+}
+
+int64_t plane_words(int64_t W) { return (W + 31) / 32; }
+
+cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
+                        uint32_t* S, uint32_t* K, const Launch& L) {
+    const int64_t wp = plane_words(W);
+    if (rows * wp >= (1ll << 31)) return cudaErrorInvalidValue;
+    if (rows <= 0) return cudaSuccess;
+    static int occ = resident_ctas(k_planes_pack, 256);
+    ++g_launches;
+    k_planes_pack<<<grid_for((rows * wp + 255) / 256, occ, L), 256, 0, L.stream>>>(
+        p, u8_consts(p), src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp));
+    return cudaGetLastError();
+}
+
+cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S1,
+                          const uint32_t* K, const int* state, uint8_t* dst, int64_t dp,
+                          int64_t rows, int64_t W, const Launch& L) {
+    const int64_t wp = plane_words(W);
+    if (rows <= 0) return cudaSuccess;
+    static int occ = resident_ctas(k_planes_unpack, 256);
+    ++g_launches;
+    k_planes_unpack<<<grid_for((rows * wp + 255) / 256, occ, L), 256, 0, L.stream>>>(
+        p, u8_consts(p), S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp));
+    return cudaGetLastError();
+}
+
+int64_t planes_tiles(int64_t rows, int64_t W) {
+    return ((rows + kPlaneRows - 1) / kPlaneRows) * ((plane_words(W) + 31) / 32);
+}
+
+cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,
+                        int64_t max_iters, int* flags, int* state, uint8_t* tflags,
+                        const Launch& L) {
+    int64_t wp = plane_words(W);
+    static int occ = resident_ctas(k_planes_loop, 256);
+    const int64_t tiles = planes_tiles(rows, W);
+    // cooperative: every CTA must be co-resident
+    unsigned grid = grid_for((tiles + 7) / 8, occ, L);
+    int64_t r = rows, mi = max_iters;
+    void* args[] = {&S0, &S1, (void*)&K, &r, &wp, &mi, &flags, &state, &tflags};
+    ++g_launches;
+    return cudaLaunchCooperativeKernel((const void*)k_planes_loop, dim3(grid), dim3(256), args, 0,
+                                       L.stream);
 }
 
 cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4* vel_out,

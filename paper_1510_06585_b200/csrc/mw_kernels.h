@@ -64,6 +64,25 @@ cudaError_t hyst_step(const uint8_t* in, uint8_t* out, int64_t rows, int64_t pit
                       int* last_changed, const uint8_t* prev_flags, uint8_t* cur_flags,
                       int top_nbr, int bot_nbr, const Launch& L);
 
+// Bit-plane hysteresis (one partition per device): pack applies the chain
+// before the loop (ending with the threshold) and writes the strong (S) and
+// weak (K) planes of (rows + 2) x plane_words(W) words with zero halo rows
+// (the caller zeroes rows 0 and rows+1 of S0, S1 and K); loop runs up to
+// max_iters Jacobi executions in one cooperative kernel and writes
+// state[0..2] = {executions E, converged, index of the final S buffer};
+// unpack applies the chain after the loop and writes bytes.
+int64_t plane_words(int64_t W);
+cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
+                        uint32_t* S, uint32_t* K, const Launch& L);
+// tflags: 2 * planes_tiles(rows, W) bytes of per-tile change flags (scratch).
+int64_t planes_tiles(int64_t rows, int64_t W);
+cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,
+                        int64_t max_iters, int* flags, int* state, uint8_t* tflags,
+                        const Launch& L);
+cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S1,
+                          const uint32_t* K, const int* state, uint8_t* dst, int64_t dp,
+                          int64_t rows, int64_t W, const Launch& L);
+
 // ------------------------------------------------------------ N-body
 // Bodies [first, first+count) of N: direct-sum acceleration (fp32 per
 // 256-source tile, fp64 across tiles).  mode 0: symplectic Euler step into

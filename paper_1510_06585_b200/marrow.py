@@ -117,6 +117,11 @@ _SIG = {
     "mw_get_balance_state": [_vp, _P(mw_balance_state)],
     "mw_ctx_set_slowdown": [_vp, _i32, _f32],
     "mw_stats_enable": [_vp, _i32],
+    "mw_graph_capture": [_vp, _vp, _P(mw_arg), _i32, _vp, _P(_vp)],
+    "mw_graph_launch": [_vp, _vp],
+    "mw_graph_result": [_vp, _P(_f64), _i32],
+    "mw_graph_kernels": [_vp, _P(_i64)],
+    "mw_graph_destroy": [_vp],
     "mw_kernel_stats": [_vp, _i32, _P(_f64), _P(_i64)],
     "mw_ctx_launch_count": [_vp, _P(_i64)],
 }
@@ -535,3 +540,56 @@ def mw_kernel_stats(ctx, kernel_class):
     ms, n = _f64(), _i64()
     _call("mw_kernel_stats", ctx.ptr, kernel_class, ctypes.byref(ms), ctypes.byref(n))
     return ms.value, n.value
+
+
+class Graph:
+    """Owning handle of an mw_graph (keeps its buffers and tree alive)."""
+
+    def __init__(self, ptr, keep):
+        self.ptr = ptr
+        self._keep = keep
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.mw_graph_destroy(self.ptr)
+            self.ptr = None
+
+    def launch(self, stream=None):
+        mw_graph_launch(self, stream)
+
+    def result(self):
+        out = (_f64 * 4)()
+        _call("mw_graph_result", self.ptr, out, 4)
+        return {"reduced": out[0], "reduced32": out[1], "executions": int(out[2]),
+                "converged": bool(out[3])}
+
+    @property
+    def kernels(self):
+        n = _i64()
+        _call("mw_graph_kernels", self.ptr, ctypes.byref(n))
+        return n.value
+
+
+def _stream_arg(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return _vp(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def mw_graph_capture(ctx, node, args, stream=None):
+    arr = (mw_arg * len(args))(*args)
+    out = _vp()
+    _call("mw_graph_capture", ctx.ptr, node.ptr, arr, len(args), _stream_arg(stream),
+          ctypes.byref(out))
+    return Graph(out, (arr, node, ctx, [getattr(a, "_owner", None) for a in args]))
+
+
+def mw_graph_launch(g, stream=None):
+    _call("mw_graph_launch", g.ptr, _stream_arg(stream))
+
+
+def mw_graph_destroy(g):
+    if g.ptr:
+        _call("mw_graph_destroy", g.ptr)
+        g.ptr = None

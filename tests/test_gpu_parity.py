@@ -209,8 +209,10 @@ def test_hysteresis_bitwise_and_E(H, W, ce):
     rng = np.random.default_rng(H * W + ce)
     gray = synth.np_u8_stream(8, 0, H * W).reshape(H, W)
     want, D = oracle_hyst(gray)
-    for d in dists(3, rng, 2) + [[0.0, 1.0, 0.0]]:
-        c = ctx(3, d)
+    # byte stencil with halo exchange (3 partitions) and the one-partition
+    # bit-plane path (cooperative device-side loop)
+    for k, d in [(3, x) for x in dists(3, rng, 2) + [[0.0, 1.0, 0.0]]] + [(1, [1.0])]:
+        c = ctx(k, d)
         dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
         r = run(c, trees.hysteresis(check_every=ce), [M.arg(dev(gray)), M.arg(dst)])
         assert np.array_equal(dst.cpu().numpy(), want), d
@@ -246,11 +248,25 @@ def test_hysteresis_loop_for_and_max_iters():
         dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
         run(c, M.mw_loop_for(M.mw_kernel_hysteresis_step(), n), [M.arg(dev(L)), M.arg(dst)])
         assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, n)[0])
-    if D >= 2:
+    for cc in (c, ctx(1)):   # byte path (2 partitions) and bit-plane path (1 partition)
+        if D >= 2:
+            dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
+            r = run(cc, trees.hysteresis(max_iters=2), [M.arg(dev(gray)), M.arg(dst)])
+            assert r["executions"] == 2 and not r["converged"]
+            assert np.array_equal(dst.cpu().numpy(), K.hyst_finalize(K.hyst_bfs(L, 2)[0]))
+        for n in (0, 1, 3, D + 5):   # pipeline(threshold, loop_for(step, n), finalize)
+            tree = M.mw_pipeline([M.mw_kernel_segment(173, 250),
+                                  M.mw_loop_for(M.mw_kernel_hysteresis_step(), n),
+                                  M.mw_kernel_hysteresis_finalize()])
+            dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
+            run(cc, tree, [M.arg(dev(gray)), M.arg(dst)])
+            assert np.array_equal(dst.cpu().numpy(), K.hyst_finalize(K.hyst_bfs(L, n)[0])), n
+        # threshold + loop only (labels out, no finalize)
+        tree = M.mw_pipeline([M.mw_kernel_segment(173, 250),
+                              M.mw_loop_while_changed(M.mw_kernel_hysteresis_step(), 1000)])
         dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
-        r = run(c, trees.hysteresis(max_iters=2), [M.arg(dev(gray)), M.arg(dst)])
-        assert r["executions"] == 2 and not r["converged"]
-        assert np.array_equal(dst.cpu().numpy(), K.hyst_finalize(K.hyst_bfs(L, 2)[0]))
+        r = run(cc, tree, [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L)[0]) and r["executions"] == D + 1
 
 
 # ----------------------------------------------------------------- N-body
@@ -411,3 +427,69 @@ def test_config_nbody_2p20_sampled():
     samples = np.concatenate([synth.nbody_sample_indices(N, 256), [0, N - 1, 284297]])
     acc_o, cond = K.nbody_accel(hp, 1e-4, targets=samples)
     _nb_check(acc.cpu().numpy()[samples, :3].astype(np.float64), acc_o, cond)
+
+
+# ----------------------------------------------------------------- NCCL call sites (1-rank communicator)
+def test_nccl_communicator_paths():
+    """force_nccl routes the MapReduce merge and the loop-condition reduction
+    through a real (1-rank) NCCL communicator: the same call sites a
+    multi-GPU run uses; results must be identical to the device-copy path."""
+    nid = M.mw_nccl_unique_id()
+    c = M.mw_ctx_create(0, 0, 1, 3, nid, force_nccl=True)
+    M.mw_set_distribution(c, [0.5, 0.25, 0.25])
+    n = 5 * (1 << 16) + 77
+    x = synth.np_f32_um11(5, 0, n)
+    y = synth.np_f32_um11(6, 0, n)
+    xd, yd = dev(x), dev(y)
+    r = run(c, trees.mapreduce(True), [M.arg(xd), M.arg(yd)])["reduced"]
+    r0 = run(ctx(3, [0.5, 0.25, 0.25]), trees.mapreduce(True), [M.arg(xd), M.arg(yd)])["reduced"]
+    assert r == r0 and abs(r - K.dot(x, y)) <= 1e-12 * K.abs_sum(x, y)
+    gray = synth.np_u8_stream(8, 0, 90 * 70).reshape(90, 70)
+    want, D = oracle_hyst(gray)
+    dst = torch.empty((90, 70), dtype=torch.uint8, device=DEV)
+    res = run(c, trees.hysteresis(check_every=2), [M.arg(dev(gray)), M.arg(dst)])
+    assert np.array_equal(dst.cpu().numpy(), want) and res["executions"] == D + 1
+    ms, wall = M.mw_last_timings(c)
+    assert len(ms) == 3 and all(t > 0 for t in ms) and wall > 0
+    c.destroy()
+
+
+# ----------------------------------------------------------------- CUDA graph replay
+def test_graph_capture_replay():
+    s = torch.cuda.Stream()
+    c = ctx(2, [0.25, 0.75])
+    x = dev(synth.np_f32_um11(1, 0, 4099))
+    y0 = synth.np_f32_um11(2, 0, 4099)
+    y = dev(y0)
+    with torch.cuda.stream(s):
+        g = M.mw_graph_capture(c, trees.saxpy(0.5), [M.arg(x), M.arg(y)], s)
+        for _ in range(7):
+            g.launch(s)
+    s.synchronize()
+    want = y0
+    for _ in range(7):
+        want = K.saxpy(0.5, synth.np_f32_um11(1, 0, 4099), want)
+    assert np.array_equal(y.cpu().numpy(), want) and g.kernels >= 2
+    # MapReduce result through the graph's pinned slot
+    xs = synth.np_f32_um11(5, 0, 3 * (1 << 16) + 5)
+    xd = dev(xs)
+    with torch.cuda.stream(s):
+        g2 = M.mw_graph_capture(c, trees.mapreduce(False), [M.arg(xd)], s)
+        g2.launch(s)
+    s.synchronize()
+    assert abs(g2.result()["reduced"] - K.sum_(xs)) <= 1e-12 * K.abs_sum(xs)
+    # one-partition hysteresis: the whole while-loop runs on the device -> capturable
+    gray = synth.np_u8_stream(8, 0, 77 * 130).reshape(77, 130)
+    want_h, D = oracle_hyst(gray)
+    c1 = ctx(1)
+    dst = torch.empty((77, 130), dtype=torch.uint8, device=DEV)
+    with torch.cuda.stream(s):
+        g3 = M.mw_graph_capture(c1, trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)], s)
+        g3.launch(s)
+    s.synchronize()
+    assert np.array_equal(dst.cpu().numpy(), want_h) and g3.result()["executions"] == D + 1
+    # multi-partition byte stencil needs the host for its loop condition
+    with pytest.raises(M.MwError) as e:
+        with torch.cuda.stream(s):
+            M.mw_graph_capture(c, trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)], s)
+    assert e.value.status == M.MW_E_UNSUPPORTED

@@ -189,6 +189,9 @@ class Filter(Workload):
     def e2e_step(self):
         return self.M.mw_run(self.ctx, self.tree, self.e2e_args)
 
+    def roof_bytes(self, cls, launches, steps, res):
+        return 8.0 * self.n * self.W * steps if cls == self.M.MW_KC_RGBA else 0.0   # this rank's rows
+
     def config(self):
         return {"workload": self.name, "image": [self.H, self.W, 4],
                 "tree": "pipeline(gauss_noise(seed=4,S=8), solarize(T=128), mirror)",
@@ -217,11 +220,23 @@ class Saxpy(Workload):
         self.units, self.launch_bytes = n, 12 * self.n
         self.l2_note = f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)"
 
+    def capture(self, stream):
+        """2^20 elements are ~2 us of HBM time, below launch latency: each step
+        replays a CUDA graph of one run (mw_graph_capture), one graph per
+        rotating buffer set."""
+        self.graphs = [self.M.mw_graph_capture(self.ctx, self.tree, list(st), stream)
+                       for st in self.sets]
+        self.graph_kernels = self.graphs[0].kernels
+
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+        self.graphs[i % self.B].launch(self.stream)
 
     def config(self):
-        return {"workload": self.name, "n": self.L, "a": 2.5, "l2": self.l2_note}
+        return {"workload": self.name, "n": self.L, "a": 2.5, "l2": self.l2_note,
+                "launch": "CUDA graph replay of one run per step (mw_graph_capture)"}
+
+    def roof_bytes(self, cls, launches, steps, res):
+        return 12.0 * self.n * steps
 
 
 class Segmentation(Workload):
@@ -249,6 +264,9 @@ class Segmentation(Workload):
 
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+
+    def roof_bytes(self, cls, launches, steps, res):
+        return 2.0 * self.n * self.shape[1] * self.shape[2] * steps if cls == self.M.MW_KC_U8 else 0.0
 
     def config(self):
         return {"workload": self.name, "shape_zyx": list(self.shape), "lo": 85, "hi": 170,
@@ -286,6 +304,9 @@ class MapReduce(Workload):
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
 
+    def roof_bytes(self, cls, launches, steps, res):
+        return (8.0 if self.dot else 4.0) * self.n * steps if cls == self.M.MW_KC_REDUCE else 0.0
+
     def config(self):
         return {"workload": self.name, "n": self.L, "merge": "+ (canonical 2^16 chunks, fp64)",
                 "l2": self.l2_note}
@@ -316,6 +337,19 @@ class Hysteresis(Workload):
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
 
+    def roof_bytes(self, cls, launches, steps, res):
+        """Algorithmic bytes.  Bit-plane path (one stencil launch per step):
+        pack 1 B + 1/4 B and unpack 1/4 B + 1 B per pixel (U8 class); each
+        Jacobi execution reads S and K and writes S, 3/8 B per pixel (STENCIL).
+        Byte path: 2 B per pixel per chain and per execution."""
+        px, E = float(self.n * self.W), float(res.get("executions", 0))
+        plane = launches.get(self.M.MW_KC_STENCIL, 0) <= steps
+        if cls == self.M.MW_KC_U8:
+            return (2.5 if plane else 4.0) * px * steps
+        if cls == self.M.MW_KC_STENCIL:
+            return (0.375 if plane else 2.0) * px * E * steps
+        return 0.0
+
     def config(self):
         return {"workload": self.name, "tree": "pipeline(threshold(173,250), "
                 f"loop_while_changed(step, check_every={self.ce}), finalize)",
@@ -343,10 +377,16 @@ class NBody(Workload):
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
 
+    def roof_bytes(self, cls, launches, steps, res):   # flops for the ALU-bound row
+        return self.launch_flops * steps if cls == self.M.MW_KC_NBODY else 0.0
+
     def config(self):
         return {"workload": self.name, "bodies": self.N, "eps2": 1e-4, "dt": 1e-3,
                 "bodies_per_rank": self.n, "interactions_per_step": self.N * self.N}
 
+
+KCLASS = {0: "saxpy_chain", 1: "rgba_chain (k_rgba_ns)", 2: "u8_chain / plane pack+unpack",
+          3: "hysteresis stencil loop", 4: "k_nbody", 5: "k_reduce_chunks", 6: "traits"}
 
 WORKLOADS = {"filter": Filter, "saxpy": Saxpy, "segmentation": Segmentation,
              "mapreduce_sum": lambda *a: MapReduce(*a, dot=False),
@@ -479,8 +519,12 @@ def run_marrow(args, dist, wl_name):
         nccl_id = dist.bcast_bytes(M.mw_nccl_unique_id() if dist.rank == 0 else None)
     ctx = M.mw_ctx_create(dist.local, dist.rank, dist.world, 1, nccl_id)
     w = WORKLOADS[wl_name](M, trees, synth, torch, ctx, dev, dist.rank)
+    stream = torch.cuda.Stream(device=dev)   # a real stream (graph capture needs one)
+    torch.cuda.set_stream(stream)
     w.setup()
-    stream = torch.cuda.current_stream()
+    w.stream = stream
+    if hasattr(w, "capture"):
+        w.capture(stream)
     torch.cuda.synchronize()
     # warm-up
     futs = [w.step(i) for i in range(args.warmup)]
@@ -498,38 +542,60 @@ def run_marrow(args, dist, wl_name):
         torch.cuda.synchronize()
     ms_local = start.elapsed_time(stop)
     launches = M.mw_ctx_launch_count(ctx) - l0
-    res = futs[-1].wait().result()
+    if hasattr(w, "graphs"):
+        launches = w.graph_kernels * args.steps
+        res = w.graphs[0].result()
+    else:
+        res = futs[-1].wait().result()
     del futs
-    kms, kn = M.mw_kernel_stats(ctx, w.kclass)
+    kstats = {cls: M.mw_kernel_stats(ctx, cls) for cls in range(M.MW_KC_COUNT)}
     M.mw_stats_enable(ctx, False)
     ms = dist.max(ms_local)
     value = w.units * args.steps / (ms / 1e3)
     pk = peaks()
-    # roofline of the dominant kernel: algorithmic bytes (flops) per launch / avg launch time
-    avg_launch_s = (kms / max(1, kn)) / 1e3
+    # roofline of the dominant kernel class: algorithmic bytes (flops) of its
+    # launches in the timed region / their CUDA-event-measured duration
+    nlaunch = {cls: n for cls, (_, n) in kstats.items()}
+    breakdown = []
+    for cls, (kms, kn) in kstats.items():
+        if kn == 0:
+            continue
+        b = w.roof_bytes(cls, nlaunch, args.steps, res)
+        breakdown.append({"class": KCLASS[cls], "launches": kn, "ms": round(kms, 4),
+                          "share": None, "achieved": (b / (kms / 1e3) / (1e12 if w.bound == "alu" else 1e9))
+                          if kms > 0 and b else None})
+    tot = sum(x["ms"] for x in breakdown) or 1.0
+    for x in breakdown:
+        x["share"] = round(x["ms"] / tot, 4)
+    if breakdown:
+        dom = max(breakdown, key=lambda x: x["ms"])
+        kms, kn = dom["ms"], dom["launches"]
+        achieved = dom["achieved"] or 0.0
+        kname = dom["class"]
+    else:   # graph replay: no per-launch events; use the step time
+        kms, kn, kname = ms, launches, KCLASS[w.kclass]
+        achieved = w.roof_bytes(w.kclass, {}, args.steps, res) / (ms / 1e3) / 1e9
     if w.bound == "alu":
         sm_mhz = pk.get("sm_max_mhz") or 1965.0
         peak_tf = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FMA lanes x clock
-        launches_per_step = kn / args.steps
-        achieved = w.launch_flops / launches_per_step / max(avg_launch_s, 1e-12) / 1e12 \
-            if launches_per_step else 0.0
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved / peak_tf, "traffic": None,
                 "peak_src": "148 SM x 128 FP32 lanes x 2 flop x max SM clock (guide unit counts)",
-                "kernel": "k_nbody", "flop_per_interaction": 20}
+                "kernel": kname, "flop_per_interaction": 20, "kernel_launches": kn,
+                "kernel_avg_us": 1e3 * kms / max(1, kn)}
     else:
-        achieved = w.launch_bytes / max(avg_launch_s, 1e-12) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic_from_profile(wl_name),
-                "peak_src": pk["src"], "kernel_launches": kn,
-                "kernel_avg_us": avg_launch_s * 1e6}
+                "peak_src": pk["src"], "kernel": kname, "kernel_launches": kn,
+                "kernel_avg_us": 1e3 * kms / max(1, kn)}
     line = {"metric": METRIC, "value": value, "unit": w.unit, "n_gpus": dist.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (SplitMix64 seeded, generated on device per rank)",
             "config": dict(w.config(), parallelism=f"rows/slabs/bodies over {dist.world} GPU(s)",
                            partitions=dist.world),
-            "roofline": roof, "gpu_launches": launches, "clocks": clocks.summary()}
+            "roofline": roof, "kernels": breakdown, "gpu_launches": launches,
+            "clocks": clocks.summary()}
     if wl_name == "hysteresis":
         line["config"]["executions_E"] = res["executions"]
         line["pixel_executions_per_s"] = value * res["executions"]

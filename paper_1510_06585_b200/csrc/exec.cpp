@@ -434,7 +434,7 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
                 CUDA_OK(cudaMemsetAsync(b, 0, wp * 4, R.s));
                 CUDA_OK(cudaMemsetAsync(b + (rows + 1) * wp, 0, wp * 4, R.s));
             }
-            CUDA_OK(cudaMemsetAsync(flags, 0, 64, R.s));
+            CUDA_OK(cudaMemsetAsync(flags, 0xFF, 64, R.s));   // pass flags start at -1
             auto pre = u8_groups(prog[0].ops);
             if (pre.size() != 1) return fail(MW_E_UNSUPPORTED, "chain before the loop > 16 ops");
             mwk::U8Prog post{};

@@ -575,7 +575,6 @@ __global__ void __launch_bounds__(kStencilThreads) k_hyst_step(
 // evaluated on the device after a grid-wide barrier every execution (exact,
 // no extra executions, no host round trip).  Plane layout: (rows + 2) x wp
 // words, rows 0 and rows+1 zero halos; bit b of word w is pixel x = 32w + b.
-constexpr int kPlaneRows = 16;   // rows per warp tile
 
 __device__ __forceinline__ uint32_t nib_of(uint32_t flags80) {   // bits 7,15,23,31 -> 4 bits
     return ((flags80 >> 7) * 0x10204080u) >> 28;
@@ -584,6 +583,7 @@ __device__ __forceinline__ uint32_t expand_nib(uint32_t n) {      // 4 bits -> 0
     return ((n * 0x00204081u) & 0x01010101u) * 0xFFu;
 }
 
+template <bool SEG_ONLY>
 __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8Prog p,
                                                      const __grid_constant__ U8Const c,
                                                      const uint8_t* __restrict__ src, int64_t sp,
@@ -612,12 +612,24 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
                 v[i] = x;
             }
         }
-        u8_apply_words<8>(p, c, v);   // the chain before the loop (ends with the threshold)
         uint32_t sb = 0, kb = 0;
+        if (SEG_ONLY) {
+            // the chain is exactly the threshold: strong = v >= hi, weak = lo <= v < hi
+            const int lm = c.lo_mode[0], hm = c.hi_mode[0];
+            const uint32_t l7 = c.lo7[0], h7 = c.hi7[0];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            sb |= nib_of(is255(v[i])) << (4 * i);
-            kb |= nib_of(is128(v[i])) << (4 * i);
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t fhi = ge_t(v[i], h7, hm), flo = ge_t(v[i], l7, lm);
+                sb += nib_of(fhi) << (4 * i);
+                kb += nib_of(flo & ~fhi) << (4 * i);
+            }
+        } else {
+            u8_apply_words<8>(p, c, v);   // the chain before the loop (ends with the threshold)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                sb |= nib_of(is255(v[i])) << (4 * i);
+                kb |= nib_of(is128(v[i])) << (4 * i);
+            }
         }
         const int64_t rem = W - x0;   // bits beyond the image width stay 0
         if (rem < 32) {
@@ -630,6 +642,7 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
     }
 }
 
+template <bool FIN_ONLY>
 __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U8Prog p,
                                                        const __grid_constant__ U8Const c,
                                                        const uint32_t* __restrict__ S0,
@@ -643,15 +656,26 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
     const uint32_t total = (uint32_t)(rows * wp);
     for (uint32_t n = blockIdx.x * 256u + threadIdx.x; n < total; n += gridDim.x * 256u) {
         const uint32_t y = fdiv(n, WP), w = n - y * WP.d;
-        const uint32_t sb = S[(y + 1) * wp + w], kb = K[(y + 1) * wp + w];
+        const uint32_t sb = S[(y + 1) * wp + w];
         uint32_t v[8];
+        if (FIN_ONLY) {
+            // the chain is exactly finalize (128 -> 0): strong pixels 255, all else 0;
+            // nibble bits to byte msbs with one IMAD, then a sign-replicating PRMT
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint32_t bs = expand_nib((sb >> (4 * i)) & 15u);
-            const uint32_t bk = expand_nib((kb >> (4 * i)) & 15u);
-            v[i] = bs | (bk & 0x80808080u);   // 255 / 128 / 0 labels
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t m = ((sb >> (4 * i)) & 15u) * 0x10204080u;
+                asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(v[i]) : "r"(m));
+            }
+        } else {
+            const uint32_t kb = K[(y + 1) * wp + w];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t bs = expand_nib((sb >> (4 * i)) & 15u);
+                const uint32_t bk = expand_nib((kb >> (4 * i)) & 15u);
+                v[i] = bs | (bk & 0x80808080u);   // 255 / 128 / 0 labels
+            }
+            u8_apply_words<8>(p, c, v);           // the chain after the loop
         }
-        u8_apply_words<8>(p, c, v);           // the chain after the loop (finalize, ...)
         const int64_t x0 = 32ll * w;
         uint8_t* r = dst + y * dp + x0;
         if (x0 + 32 <= W && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
@@ -663,38 +687,54 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
     }
 }
 
-// One warp = 32 consecutive words (1024 pixels) x kPlaneRows rows.  All rows
-// of a tile are loaded up front (kPlaneRows + 2 strong words, kPlaneRows weak
-// words, one edge word for lanes 0/31 per row) so a warp keeps ~50 loads in
-// flight.  Active tiles only: a tile whose 3x3 tile neighbourhood did not
-// change in the previous execution already holds the next state in both
-// buffers and is skipped (exact, as for the byte stencil).
-// state = {E, converged, final buffer index}; tflags: 2 x n_tiles bytes.
-__global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
+// Temporal blocking: one pass advances the state by T Jacobi executions.  A
+// warp tile holds kTbRows rows x 32 words in registers: lanes 1..30 and rows
+// T..kTbRows-T-1 are owned (written back), lanes 0/31 and T rows above and
+// below are halo recomputed from the neighbours (validity shrinks by one
+// pixel per execution, so T <= 31 bits / T <= kTbRows/2 rows stay exact).
+// Every execution inside a pass is one global Jacobi step; the device keeps
+// the last execution index that changed an owned pixel, so E is exact and a
+// pass that ends without change has reached the fixed point (extra in-pass
+// executions past it are no-ops).  Tiles whose 3x3 tile neighbourhood did not
+// change in the previous pass are skipped.  One cooperative kernel runs all
+// passes; flags[pass % 3] = last changed execution of the pass (-1: none).
+
+constexpr int kTbWarps = 4;      // 128-thread CTAs; the weak plane of a tile lives in smem
+
+template <int T, int ROWS>
+__global__ void __launch_bounds__(32 * kTbWarps) k_planes_loop(uint32_t* __restrict__ S0,
                                                      uint32_t* __restrict__ S1,
                                                      const uint32_t* __restrict__ K, int64_t rows,
                                                      int64_t wp, int64_t max_iters,
                                                      int* __restrict__ flags,
                                                      int* __restrict__ state,
                                                      uint8_t* __restrict__ tflags) {
+    constexpr int R = ROWS - 2 * T;      // owned rows per tile
+    constexpr int OW = 30;               // owned words per tile
+    __shared__ uint32_t ks[kTbWarps][ROWS][32];
     cg::grid_group grid = cg::this_grid();
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int64_t nwarps = (int64_t)gridDim.x * 8;
-    const int64_t n_strips = (rows + kPlaneRows - 1) / kPlaneRows;
-    const int64_t n_cb = (wp + 31) / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * kTbWarps + wid;
+    const int64_t nwarps = (int64_t)gridDim.x * kTbWarps;
+    const int64_t n_strips = (rows + R - 1) / R;
+    const int64_t n_cb = (wp + OW - 1) / OW;
     const int64_t n_tiles = n_strips * n_cb;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    for (int64_t k = 0; k < max_iters; ++k) {
-        const uint32_t* in = (k & 1) ? S1 : S0;
-        uint32_t* out = (k & 1) ? S0 : S1;
-        const uint8_t* fprev = tflags + ((k + 1) & 1) * n_tiles;
-        uint8_t* fcur = tflags + (k & 1) * n_tiles;
-        if (leader) flags[(k + 1) % 3] = 0;   // last read two barriers ago
-        bool ch_any = false;
+    const bool own_lane = lane >= 1 && lane <= OW;
+    uint32_t (*kt)[32] = ks[wid];
+    int64_t k0 = 0;
+    int pass = 0;
+    while (k0 < max_iters) {
+        const int steps = (int)min((int64_t)T, max_iters - k0);
+        const uint32_t* in = (pass & 1) ? S1 : S0;
+        uint32_t* out = (pass & 1) ? S0 : S1;
+        const uint8_t* fprev = tflags + ((pass + 1) & 1) * n_tiles;
+        uint8_t* fcur = tflags + (pass & 1) * n_tiles;
+        if (leader) flags[(pass + 1) % 3] = -1;   // last read two barriers ago
+        int my_last = -1;
         for (int64_t t = gw; t < n_tiles; t += nwarps) {
             const int64_t strip = t / n_cb, cb = t - strip * n_cb;
-            bool act = k == 0;
+            bool act = pass == 0;
             if (!act) {
                 bool a = false;
                 if (lane < 9) {
@@ -707,65 +747,77 @@ __global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
                 if (lane == 0) fcur[t] = 0;
                 continue;
             }
-            const int64_t w = cb * 32 + lane;
-            const bool valid = w < wp;
-            const bool edge_l = lane == 0, edge_r = lane == 31 || w + 1 == wp;
-            const int64_t y0 = strip * kPlaneRows;
-            uint32_t sv[kPlaneRows + 2], ev[kPlaneRows + 2], kv[kPlaneRows];
+            const int64_t w = cb * OW - 1 + lane;          // lane 0 / 31: halo words
+            const bool wv = w >= 0 && w < wp;
+            const int64_t ybase = strip * R - T;            // image row of register row 0
+            const int ilo = (int)max((int64_t)0, -1 - ybase);          // rows outside [-1, rows]
+            const int ihi = (int)min((int64_t)ROWS, rows + 1 - ybase); // are zero
+            const uint32_t* ip = in + (ybase + 1) * wp + w;
+            const uint32_t* kp = K + (ybase + 1) * wp + w;
+            uint32_t sv[ROWS];
+            __syncwarp();
 #pragma unroll
-            for (int i = 0; i < kPlaneRows + 2; ++i) {
-                const int64_t y = y0 - 1 + i;              // -1 .. y0+kPlaneRows
-                const bool ok = valid && y <= rows;        // y == rows is the zero halo row
-                const uint32_t* r = in + (y + 1) * wp;
-                sv[i] = ok ? r[w] : 0u;
-                ev[i] = 0u;
-                if (ok && edge_l && w > 0) ev[i] = r[w - 1];
-                if (ok && edge_r && !edge_l && w + 1 < wp) ev[i] = r[w + 1];
+            for (int i = 0; i < ROWS; ++i) {
+                const bool okr = wv && i >= ilo && i < ihi;
+                sv[i] = okr ? ip[(int64_t)i * wp] : 0u;
+                const int64_t y = ybase + i;
+                kt[i][lane] = (okr && y >= 0 && y < rows) ? kp[(int64_t)i * wp] : 0u;
             }
+            __syncwarp();
+            int tile_last = -1;
+            // lanes 0/31 take their own word as the outer neighbour: the error
+            // enters at their far bits and moves one bit per step, never reaching
+            // the owned lanes (T <= 16)
+            auto hrow = [&](uint32_t sx) {
+                const uint32_t l = __shfl_up_sync(0xffffffffu, sx, 1);
+                const uint32_t r = __shfl_down_sync(0xffffffffu, sx, 1);
+                return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
+            };
 #pragma unroll
-            for (int i = 0; i < kPlaneRows; ++i) {
-                const int64_t y = y0 + i;
-                kv[i] = (valid && y < rows) ? K[(y + 1) * wp + w] : 0u;
-            }
-            uint32_t hv[kPlaneRows + 2];
+            for (int st = 0; st < T; ++st) {
+                if (st < steps) {
+                    // after st executions rows [st, ROWS-1-st] are exact; update
+                    // only the rows that stay exact: [st+1, ROWS-2-st]
+                    uint32_t hp = hrow(sv[st]), hc = hrow(sv[st + 1]);
+                    uint32_t ch = 0;
 #pragma unroll
-            for (int i = 0; i < kPlaneRows + 2; ++i) {   // dilate8 horizontally
-                const uint32_t s = sv[i];
-                uint32_t l = __shfl_up_sync(0xffffffffu, s, 1);
-                uint32_t r = __shfl_down_sync(0xffffffffu, s, 1);
-                if (edge_l) l = ev[i];
-                if (edge_r) r = edge_l ? 0u : ev[i];
-                hv[i] = s | __funnelshift_l(l, s, 1) | __funnelshift_r(s, r, 1);
-            }
-            uint32_t ch = 0;
-#pragma unroll
-            for (int i = 0; i < kPlaneRows; ++i) {
-                const int64_t y = y0 + i;
-                if (valid && y < rows) {
-                    const uint32_t s2 = sv[i + 1] | (kv[i] & (hv[i] | hv[i + 1] | hv[i + 2]));
-                    ch |= s2 ^ sv[i + 1];
-                    out[(y + 1) * wp + w] = s2;
+                    for (int i = st + 1; i <= ROWS - 2 - st; ++i) {
+                        const uint32_t hn = hrow(sv[i + 1]);   // old row i+1
+                        const uint32_t s2 = sv[i] | (kt[i][lane] & (hp | hc | hn));
+                        if (i >= T && i < T + R) ch |= s2 ^ sv[i];
+                        sv[i] = s2;
+                        hp = hc;
+                        hc = hn;
+                    }
+                    if (__any_sync(0xffffffffu, own_lane && ch != 0)) tile_last = st;
                 }
             }
-            const bool tch = __any_sync(0xffffffffu, ch != 0);
-            if (lane == 0) fcur[t] = (uint8_t)tch;
-            ch_any |= tch;
+            uint32_t* op = out + (ybase + 1) * wp + w;
+#pragma unroll
+            for (int i = T; i < T + R; ++i)
+                if (own_lane && wv && i < ihi - 1) op[(int64_t)i * wp] = sv[i];
+            if (lane == 0) fcur[t] = (uint8_t)(tile_last >= 0);
+            my_last = max(my_last, tile_last);
         }
-        if (ch_any && lane == 0) atomicExch(&flags[k % 3], 1);
+        if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
         grid.sync();
-        if (*((volatile int*)&flags[k % 3]) == 0) {   // execution k changed nothing
+        const int last = *((volatile int*)&flags[pass % 3]);
+        if (last < k0 + steps - 1) {   // the pass ended with an execution that changed nothing
             if (leader) {
-                state[0] = (int)(k + 1);
+                const int64_t last_global = last >= 0 ? last : k0 - 1;
+                state[0] = (int)(last_global + 2);
                 state[1] = 1;
-                state[2] = (k & 1) ? 0 : 1;
+                state[2] = (pass & 1) ? 0 : 1;
             }
             return;
         }
+        k0 += steps;
+        ++pass;
     }
     if (leader) {
         state[0] = (int)max_iters;
         state[1] = 0;
-        state[2] = max_iters == 0 ? 0 : (((max_iters - 1) & 1) ? 0 : 1);
+        state[2] = pass == 0 ? 0 : (((pass - 1) & 1) ? 0 : 1);
     }
 }
 
@@ -1194,10 +1246,18 @@ cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t
     const int64_t wp = plane_words(W);
     if (rows * wp >= (1ll << 31)) return cudaErrorInvalidValue;
     if (rows <= 0) return cudaSuccess;
-    static int occ = resident_ctas(k_planes_pack, 256);
+    const int64_t tiles = (rows * wp + 255) / 256;
+    const U8Const c = u8_consts(p);
     ++g_launches;
-    k_planes_pack<<<grid_for((rows * wp + 255) / 256, occ, L), 256, 0, L.stream>>>(
-        p, u8_consts(p), src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp));
+    if (p.n == 1 && p.kind[0] == U8_SEGMENT) {
+        static int occ = resident_ctas(k_planes_pack<true>, 256);
+        k_planes_pack<true><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
+            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp));
+    } else {
+        static int occ = resident_ctas(k_planes_pack<false>, 256);
+        k_planes_pack<false><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
+            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp));
+    }
     return cudaGetLastError();
 }
 
@@ -1206,30 +1266,57 @@ cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S
                           int64_t rows, int64_t W, const Launch& L) {
     const int64_t wp = plane_words(W);
     if (rows <= 0) return cudaSuccess;
-    static int occ = resident_ctas(k_planes_unpack, 256);
+    const int64_t tiles = (rows * wp + 255) / 256;
+    const U8Const c = u8_consts(p);
     ++g_launches;
-    k_planes_unpack<<<grid_for((rows * wp + 255) / 256, occ, L), 256, 0, L.stream>>>(
-        p, u8_consts(p), S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp));
+    if (p.n == 1 && p.kind[0] == U8_FINALIZE) {
+        static int occ = resident_ctas(k_planes_unpack<true>, 256);
+        k_planes_unpack<true><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
+            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp));
+    } else {
+        static int occ = resident_ctas(k_planes_unpack<false>, 256);
+        k_planes_unpack<false><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
+            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp));
+    }
     return cudaGetLastError();
 }
 
-int64_t planes_tiles(int64_t rows, int64_t W) {
-    return ((rows + kPlaneRows - 1) / kPlaneRows) * ((plane_words(W) + 31) / 32);
+int64_t planes_tiles(int64_t rows, int64_t W) {   // upper bound over the variants (R >= 8)
+    return ((rows + 7) / 8) * ((plane_words(W) + 29) / 30);
+}
+
+template <int T, int ROWS>
+static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows,
+                                 int64_t wp, int64_t max_iters, int* flags, int* state,
+                                 uint8_t* tflags, const Launch& L) {
+    static int occ = resident_ctas(k_planes_loop<T, ROWS>, 32 * kTbWarps);
+    constexpr int R = ROWS - 2 * T;
+    const int64_t tiles = ((rows + R - 1) / R) * ((wp + 29) / 30);
+    // cooperative: every CTA must be co-resident
+    unsigned grid = grid_for((tiles + kTbWarps - 1) / kTbWarps, occ, L);
+    int64_t r = rows, w = wp, mi = max_iters;
+    void* args[] = {&S0, &S1, (void*)&K, &r, &w, &mi, &flags, &state, &tflags};
+    ++g_launches;
+    return cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid),
+                                       dim3(32 * kTbWarps), args, 0, L.stream);
 }
 
 cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,
                         int64_t max_iters, int* flags, int* state, uint8_t* tflags,
                         const Launch& L) {
-    int64_t wp = plane_words(W);
-    static int occ = resident_ctas(k_planes_loop, 256);
-    const int64_t tiles = planes_tiles(rows, W);
-    // cooperative: every CTA must be co-resident
-    unsigned grid = grid_for((tiles + 7) / 8, occ, L);
-    int64_t r = rows, mi = max_iters;
-    void* args[] = {&S0, &S1, (void*)&K, &r, &wp, &mi, &flags, &state, &tflags};
-    ++g_launches;
-    return cudaLaunchCooperativeKernel((const void*)k_planes_loop, dim3(grid), dim3(256), args, 0,
-                                       L.stream);
+    const int64_t wp = plane_words(W);
+    static const int T = tuning_knob("MW_HYST_T", 8);
+    static const int ROWS = tuning_knob("MW_HYST_ROWS", 48);
+#define MW_PL(TT, RR) \
+    if (T == TT && ROWS == RR) return planes_loop_t<TT, RR>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L)
+    MW_PL(4, 32);
+    MW_PL(8, 32);
+    MW_PL(4, 48);
+    MW_PL(12, 48);
+    MW_PL(8, 64);
+    MW_PL(16, 64);
+#undef MW_PL
+    return planes_loop_t<8, 48>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L);
 }
 
 cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4* vel_out,

@@ -142,6 +142,9 @@ class Workload:
         self.ctx, self.dev, self.rank = ctx, dev, rank
         self.l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 
+    def bound_of(self, cls, launches, steps):
+        return self.bound
+
     def sets_for(self, ws_bytes):
         return max(1, math.ceil(2 * self.l2 / max(1, ws_bytes)))
 
@@ -221,19 +224,27 @@ class Saxpy(Workload):
         self.l2_note = f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)"
 
     def capture(self, stream):
-        """2^20 elements are ~2 us of HBM time, below launch latency: each step
-        replays a CUDA graph of one run (mw_graph_capture), one graph per
-        rotating buffer set."""
-        self.graphs = [self.M.mw_graph_capture(self.ctx, self.tree, list(st), stream)
-                       for st in self.sets]
-        self.graph_kernels = self.graphs[0].kernels
+        """2^20 elements are ~2 us of HBM time, below launch latency: the B
+        rotating-buffer runs are captured back to back in ONE CUDA graph
+        (mw_graph_capture_many); step i is run i of the replayed sequence."""
+        self.graph = self.M.mw_graph_capture_many(self.ctx, self.tree, [list(st) for st in self.sets],
+                                                  stream)
+        self.graphs = [self.graph]
+        self.graph_kernels = self.graph.kernels // self.B
+
+    def run_steps(self, k):
+        assert k % self.B == 0, "steps must be a multiple of the buffer-set count"
+        for _ in range(k // self.B):
+            self.graph.launch(self.stream)
+        return []
 
     def step(self, i):
-        self.graphs[i % self.B].launch(self.stream)
+        raise NotImplementedError
 
     def config(self):
         return {"workload": self.name, "n": self.L, "a": 2.5, "l2": self.l2_note,
-                "launch": "CUDA graph replay of one run per step (mw_graph_capture)"}
+                "launch": "one CUDA graph replaying the rotating-buffer runs back to back "
+                          "(mw_graph_capture_many); a step is one run"}
 
     def roof_bytes(self, cls, launches, steps, res):
         return 12.0 * self.n * steps
@@ -337,17 +348,27 @@ class Hysteresis(Workload):
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
 
+    def plane(self, launches, steps):
+        return launches.get(self.M.MW_KC_STENCIL, 0) <= steps
+
+    def bound_of(self, cls, launches, steps):
+        # the one-kernel bit-plane loop works on L2-resident planes and is bound by
+        # the integer ALU / shuffle pipes, not by HBM
+        return "alu" if cls == self.M.MW_KC_STENCIL and self.plane(launches, steps) else "hbm"
+
     def roof_bytes(self, cls, launches, steps, res):
-        """Algorithmic bytes.  Bit-plane path (one stencil launch per step):
-        pack 1 B + 1/4 B and unpack 1/4 B + 1 B per pixel (U8 class); each
-        Jacobi execution reads S and K and writes S, 3/8 B per pixel (STENCIL).
-        Byte path: 2 B per pixel per chain and per execution."""
+        """Algorithmic work.  Bit-plane path (one stencil launch per step):
+        pack 1 B + 1/4 B and unpack 1/4 B + 1 B per pixel (U8 class, HBM);
+        each Jacobi execution of the dense plane algorithm costs 5 integer ALU
+        lane-operations per 32 pixels (2 funnel shifts + 3 LOP3; the 2 shuffles
+        run elsewhere) -> 0.15625 ops per pixel-execution (STENCIL class, ALU).
+        Byte path: 2 B per pixel per chain and per execution (HBM)."""
         px, E = float(self.n * self.W), float(res.get("executions", 0))
-        plane = launches.get(self.M.MW_KC_STENCIL, 0) <= steps
+        plane = self.plane(launches, steps)
         if cls == self.M.MW_KC_U8:
             return (2.5 if plane else 4.0) * px * steps
         if cls == self.M.MW_KC_STENCIL:
-            return (0.375 if plane else 2.0) * px * E * steps
+            return (0.15625 if plane else 2.0) * px * E * steps
         return 0.0
 
     def config(self):
@@ -527,9 +548,13 @@ def run_marrow(args, dist, wl_name):
         w.capture(stream)
     torch.cuda.synchronize()
     # warm-up
-    futs = [w.step(i) for i in range(args.warmup)]
+    if hasattr(w, "run_steps"):
+        args.steps = max(w.B, args.steps // w.B * w.B)
+        w.run_steps(max(w.B, args.warmup // w.B * w.B))
+    else:
+        futs = [w.step(i) for i in range(args.warmup)]
+        del futs
     torch.cuda.synchronize()
-    del futs
     M.mw_stats_enable(ctx, True)
     l0 = M.mw_ctx_launch_count(ctx)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -537,7 +562,8 @@ def run_marrow(args, dist, wl_name):
     torch.cuda.synchronize()
     with ClockSampler(dist.local) as clocks:
         start.record(stream)
-        futs = [w.step(i) for i in range(args.steps)]
+        futs = w.run_steps(args.steps) if hasattr(w, "run_steps") else \
+            [w.step(i) for i in range(args.steps)]
         stop.record(stream)
         torch.cuda.synchronize()
     ms_local = start.elapsed_time(stop)
@@ -556,33 +582,39 @@ def run_marrow(args, dist, wl_name):
     # roofline of the dominant kernel class: algorithmic bytes (flops) of its
     # launches in the timed region / their CUDA-event-measured duration
     nlaunch = {cls: n for cls, (_, n) in kstats.items()}
+    sm_mhz = pk.get("sm_max_mhz") or 1965.0
+    alu_peak = {"nbody": (148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "TFLOP/s",
+                          "148 SM x 128 FP32 lanes x 2 flop x max SM clock (guide unit counts)"),
+                "hysteresis": (148 * 64 * sm_mhz * 1e6 / 1e12, "Tops/s",
+                               "148 SM x 64 integer-ALU lanes x max SM clock (guide unit counts)")}
     breakdown = []
     for cls, (kms, kn) in kstats.items():
         if kn == 0:
             continue
         b = w.roof_bytes(cls, nlaunch, args.steps, res)
-        breakdown.append({"class": KCLASS[cls], "launches": kn, "ms": round(kms, 4),
-                          "share": None, "achieved": (b / (kms / 1e3) / (1e12 if w.bound == "alu" else 1e9))
-                          if kms > 0 and b else None})
+        bd = w.bound_of(cls, nlaunch, args.steps)
+        scale = 1e12 if bd == "alu" else 1e9
+        breakdown.append({"class": KCLASS[cls], "bound": bd, "launches": kn, "ms": round(kms, 4),
+                          "share": None,
+                          "achieved": (b / (kms / 1e3) / scale) if kms > 0 and b else None})
     tot = sum(x["ms"] for x in breakdown) or 1.0
     for x in breakdown:
         x["share"] = round(x["ms"] / tot, 4)
     if breakdown:
         dom = max(breakdown, key=lambda x: x["ms"])
-        kms, kn = dom["ms"], dom["launches"]
+        kms, kn, bound = dom["ms"], dom["launches"], dom["bound"]
         achieved = dom["achieved"] or 0.0
         kname = dom["class"]
     else:   # graph replay: no per-launch events; use the step time
-        kms, kn, kname = ms, launches, KCLASS[w.kclass]
+        kms, kn, kname, bound = ms, launches, KCLASS[w.kclass], w.bound
         achieved = w.roof_bytes(w.kclass, {}, args.steps, res) / (ms / 1e3) / 1e9
-    if w.bound == "alu":
-        sm_mhz = pk.get("sm_max_mhz") or 1965.0
-        peak_tf = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FMA lanes x clock
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved / peak_tf, "traffic": None,
-                "peak_src": "148 SM x 128 FP32 lanes x 2 flop x max SM clock (guide unit counts)",
-                "kernel": kname, "flop_per_interaction": 20, "kernel_launches": kn,
-                "kernel_avg_us": 1e3 * kms / max(1, kn)}
+    if bound == "alu":
+        peak, unit, src = alu_peak["nbody" if wl_name == "nbody" else "hysteresis"]
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak, "traffic": None, "peak_src": src, "kernel": kname,
+                "kernel_launches": kn, "kernel_avg_us": 1e3 * kms / max(1, kn)}
+        if wl_name == "nbody":
+            roof["flop_per_interaction"] = 20
     else:
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic_from_profile(wl_name),

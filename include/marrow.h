@@ -236,6 +236,11 @@ void mw_future_release(mw_future* f);
 typedef struct mw_graph mw_graph;
 mw_status mw_graph_capture(mw_ctx* ctx, const mw_node* root, const mw_arg* args, int32_t nargs,
                            void* stream, mw_graph** out);
+/* Same, capturing `nsets` back-to-back runs of `root`, run k on
+ * args[k*nargs .. k*nargs+nargs) (e.g. rotating buffer sets); one
+ * mw_graph_launch then replays all of them in order.                       */
+mw_status mw_graph_capture_many(mw_ctx* ctx, const mw_node* root, const mw_arg* args,
+                                int32_t nargs, int32_t nsets, void* stream, mw_graph** out);
 mw_status mw_graph_launch(mw_graph* g, void* stream);
 /* Results of the most recent replay (same layout as mw_future_result); call
  * after the launch stream has synchronised.                                */

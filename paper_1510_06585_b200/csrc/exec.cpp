@@ -1276,9 +1276,10 @@ struct mw_graph {
     int64_t kernels = 0;  // library kernels per replay
 };
 
-mw_status mw_graph_capture(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
-                           void* stream, mw_graph** out) {
-    if (!c || !root || !out || (nargs > 0 && !args)) return fail(MW_E_INVALID_SPEC, "NULL argument");
+mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* args,
+                                int32_t nargs, int32_t nsets, void* stream, mw_graph** out) {
+    if (!c || !root || !out || (nargs > 0 && !args) || nsets < 1)
+        return fail(MW_E_INVALID_SPEC, "NULL argument or nsets < 1");
     if (!stream) return fail(MW_E_INVALID_SPEC, "graph capture needs a non-default stream");
     CUDA_OK(cudaSetDevice(c->device));
     std::unique_ptr<mw_graph> g(new mw_graph);
@@ -1290,9 +1291,13 @@ mw_status mw_graph_capture(mw_ctx* c, const mw_node* root, const mw_arg* args, i
     const unsigned long long l0 = mwk::launch_count();
     CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     c->capturing = true;
-    mw_status st;
+    mw_status st = MW_OK;
     try {
-        st = run(c, reinterpret_cast<const Node*>(root), args, nargs, s, &g->f);
+        for (int32_t k = 0; k < nsets && st == MW_OK; ++k) {
+            g->f.has_reduce = false;
+            g->f.plane_loop = false;
+            st = run(c, reinterpret_cast<const Node*>(root), args + (size_t)k * nargs, nargs, s, &g->f);
+        }
     } catch (...) {
         st = fail(MW_E_INVALID_SPEC, "internal error");
     }
@@ -1315,6 +1320,11 @@ mw_status mw_graph_capture(mw_ctx* c, const mw_node* root, const mw_arg* args, i
     g->kernels = (int64_t)(mwk::launch_count() - l0);
     *out = g.release();
     return MW_OK;
+}
+
+mw_status mw_graph_capture(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
+                           void* stream, mw_graph** out) {
+    return mw_graph_capture_many(c, root, args, nargs, 1, stream, out);
 }
 
 mw_status mw_graph_launch(mw_graph* g, void* stream) {

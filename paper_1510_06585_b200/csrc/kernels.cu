@@ -311,6 +311,133 @@ __global__ void __launch_bounds__(256) k_rgba_ns(const __grid_constant__ NsConst
     }
 }
 
+// ---- TMA (bulk-copy) variant of the same chain.  Persistent CTAs (one per
+// SM slot) stream row chunks of CH bytes through an NS-stage shared-memory
+// ring: one thread issues cp.async.bulk global->smem loads completing on an
+// mbarrier (expect_tx), all 256 threads run the chain smem->smem, and the
+// same thread writes the result back with cp.async.bulk smem->global
+// (bulk_group).  The mirror is a contiguous source segment read backwards.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(smem_src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int kTmaChunk, int kTmaStages, bool MIRROR, bool KM, bool T128>
+__global__ void __launch_bounds__(256) k_rgba_ns_tma(const __grid_constant__ NsConst c,
+                                                     const uint8_t* __restrict__ src,
+                                                     uint8_t* __restrict__ dst, int64_t rows,
+                                                     uint32_t W, uint32_t row0) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint4* sin = reinterpret_cast<uint4*>(smem);                                   // NS x CH
+    uint4* sout = reinterpret_cast<uint4*>(smem + kTmaStages * kTmaChunk);         // NS x CH
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * kTmaStages * kTmaChunk);
+    const uint32_t rowb = W * 4u;
+    const uint32_t cpr = rowb / kTmaChunk;                 // chunks per row
+    const int64_t n_items = rows * cpr;
+    constexpr uint32_t VPC = kTmaChunk / 16;                // vectors per chunk
+    constexpr uint32_t PPC = kTmaChunk / 4;                 // pixels per chunk
+    auto src_of = [&](int64_t item) {                      // global source of an item
+        const int64_t r = item / cpr;
+        const uint32_t ch = (uint32_t)(item - r * cpr);
+        const uint32_t sc = MIRROR ? (cpr - 1u - ch) : ch;   // mirrored chunk of the row
+        return src + r * (int64_t)rowb + (int64_t)sc * kTmaChunk;
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < kTmaStages; ++s) {
+            const int64_t item = blockIdx.x + (int64_t)s * gridDim.x;
+            if (item < n_items) {
+                mbar_expect_tx(&bar[s], kTmaChunk);
+                bulk_load(sin + s * VPC, src_of(item), kTmaChunk, &bar[s]);
+            }
+        }
+    }
+    __syncthreads();
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int stage = it % kTmaStages;
+        const uint32_t phase = (uint32_t)(it / kTmaStages) & 1u;
+        mbar_wait(&bar[stage], phase);
+        if (threadIdx.x == 0) bulk_wait_read<kTmaStages - 1>();   // out[stage] free again
+        __syncthreads();
+        const int64_t r = item / cpr;
+        const uint32_t ch = (uint32_t)(item - r * cpr);
+        const uint32_t x0 = ch * PPC;                            // first output pixel
+        const uint32_t rowbase = (row0 + (uint32_t)r) * W;
+        const uint4* in = sin + stage * VPC;
+        uint4* out = sout + stage * VPC;
+#pragma unroll
+        for (int k = 0; k < (int)(VPC / 256); ++k) {
+            const uint32_t v = k * 256u + threadIdx.x;            // output vector in chunk
+            uint4 q = in[MIRROR ? (VPC - 1u - v) : v];
+            uint32_t w0 = q.x, w1 = q.y, w2 = q.z, w3 = q.w;
+            if (MIRROR) {
+                uint32_t t = w0; w0 = w3; w3 = t;
+                t = w1; w1 = w2; w2 = t;
+            }
+            const uint32_t xo = x0 + 4u * v;                      // output column
+            const uint32_t i0 = rowbase + (KM ? (W - 1u - xo) : xo);
+            uint4 o;
+            o.x = noise_solarize<T128>(w0, i0, c);
+            o.y = noise_solarize<T128>(w1, KM ? i0 - 1u : i0 + 1u, c);
+            o.z = noise_solarize<T128>(w2, KM ? i0 - 2u : i0 + 2u, c);
+            o.w = noise_solarize<T128>(w3, KM ? i0 - 3u : i0 + 3u, c);
+            out[v] = o;
+        }
+        fence_proxy_async();   // make the generic-proxy smem writes visible to the bulk copy
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_store(dst + r * (int64_t)rowb + (int64_t)ch * kTmaChunk, out, kTmaChunk);
+            const int64_t nxt = item + (int64_t)kTmaStages * gridDim.x;
+            if (nxt < n_items) {                                 // in[stage] fully consumed
+                mbar_expect_tx(&bar[stage], kTmaChunk);
+                bulk_load(sin + stage * VPC, src_of(nxt), kTmaChunk, &bar[stage]);
+            }
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait_read<0>();
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Any width / alignment: one pixel per element.
 __global__ void __launch_bounds__(256) k_rgba_scalar(const __grid_constant__ RgbaProg p,
                                                      const __grid_constant__ RgbaConst c,
@@ -699,10 +826,11 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // change in the previous pass are skipped.  One cooperative kernel runs all
 // passes; flags[pass % 3] = last changed execution of the pass (-1: none).
 
-constexpr int kTbWarps = 4;      // 128-thread CTAs; the weak plane of a tile lives in smem
-
+// (Measured on B200: keeping the weak plane in registers with 256-thread CTAs
+// and a rolled execution loop beats smem-resident K and a fully unrolled
+// shrinking-window loop, whose code no longer fits the instruction cache.)
 template <int T, int ROWS>
-__global__ void __launch_bounds__(32 * kTbWarps) k_planes_loop(uint32_t* __restrict__ S0,
+__global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
                                                      uint32_t* __restrict__ S1,
                                                      const uint32_t* __restrict__ K, int64_t rows,
                                                      int64_t wp, int64_t max_iters,
@@ -711,17 +839,15 @@ __global__ void __launch_bounds__(32 * kTbWarps) k_planes_loop(uint32_t* __restr
                                                      uint8_t* __restrict__ tflags) {
     constexpr int R = ROWS - 2 * T;      // owned rows per tile
     constexpr int OW = 30;               // owned words per tile
-    __shared__ uint32_t ks[kTbWarps][ROWS][32];
     cg::grid_group grid = cg::this_grid();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * kTbWarps + wid;
-    const int64_t nwarps = (int64_t)gridDim.x * kTbWarps;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
     const int64_t n_strips = (rows + R - 1) / R;
     const int64_t n_cb = (wp + OW - 1) / OW;
     const int64_t n_tiles = n_strips * n_cb;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     const bool own_lane = lane >= 1 && lane <= OW;
-    uint32_t (*kt)[32] = ks[wid];
     int64_t k0 = 0;
     int pass = 0;
     while (k0 < max_iters) {
@@ -750,52 +876,41 @@ __global__ void __launch_bounds__(32 * kTbWarps) k_planes_loop(uint32_t* __restr
             const int64_t w = cb * OW - 1 + lane;          // lane 0 / 31: halo words
             const bool wv = w >= 0 && w < wp;
             const int64_t ybase = strip * R - T;            // image row of register row 0
-            const int ilo = (int)max((int64_t)0, -1 - ybase);          // rows outside [-1, rows]
-            const int ihi = (int)min((int64_t)ROWS, rows + 1 - ybase); // are zero
-            const uint32_t* ip = in + (ybase + 1) * wp + w;
-            const uint32_t* kp = K + (ybase + 1) * wp + w;
-            uint32_t sv[ROWS];
-            __syncwarp();
+            uint32_t sv[ROWS], kv[ROWS];
 #pragma unroll
             for (int i = 0; i < ROWS; ++i) {
-                const bool okr = wv && i >= ilo && i < ihi;
-                sv[i] = okr ? ip[(int64_t)i * wp] : 0u;
                 const int64_t y = ybase + i;
-                kt[i][lane] = (okr && y >= 0 && y < rows) ? kp[(int64_t)i * wp] : 0u;
+                sv[i] = (wv && y >= -1 && y <= rows) ? in[(y + 1) * wp + w] : 0u;
+                kv[i] = (wv && y >= 0 && y < rows) ? K[(y + 1) * wp + w] : 0u;
             }
-            __syncwarp();
             int tile_last = -1;
-            // lanes 0/31 take their own word as the outer neighbour: the error
-            // enters at their far bits and moves one bit per step, never reaching
-            // the owned lanes (T <= 16)
-            auto hrow = [&](uint32_t sx) {
-                const uint32_t l = __shfl_up_sync(0xffffffffu, sx, 1);
-                const uint32_t r = __shfl_down_sync(0xffffffffu, sx, 1);
-                return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
-            };
+            for (int st = 0; st < steps; ++st) {
+                // lanes 0/31 take their own word as the outer neighbour: the error
+                // enters at their far bits and moves one bit per execution, never
+                // reaching the owned lanes (T <= 16)
+                auto hrow = [&](uint32_t sx) {
+                    const uint32_t l = __shfl_up_sync(0xffffffffu, sx, 1);
+                    const uint32_t r = __shfl_down_sync(0xffffffffu, sx, 1);
+                    return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
+                };
+                uint32_t hp = hrow(sv[0]), hc = hrow(sv[1]);
+                uint32_t ch = 0;
 #pragma unroll
-            for (int st = 0; st < T; ++st) {
-                if (st < steps) {
-                    // after st executions rows [st, ROWS-1-st] are exact; update
-                    // only the rows that stay exact: [st+1, ROWS-2-st]
-                    uint32_t hp = hrow(sv[st]), hc = hrow(sv[st + 1]);
-                    uint32_t ch = 0;
-#pragma unroll
-                    for (int i = st + 1; i <= ROWS - 2 - st; ++i) {
-                        const uint32_t hn = hrow(sv[i + 1]);   // old row i+1
-                        const uint32_t s2 = sv[i] | (kt[i][lane] & (hp | hc | hn));
-                        if (i >= T && i < T + R) ch |= s2 ^ sv[i];
-                        sv[i] = s2;
-                        hp = hc;
-                        hc = hn;
-                    }
-                    if (__any_sync(0xffffffffu, own_lane && ch != 0)) tile_last = st;
+                for (int i = 1; i < ROWS - 1; ++i) {
+                    const uint32_t hn = hrow(sv[i + 1]);     // old row i+1 (not yet updated)
+                    const uint32_t s2 = sv[i] | (kv[i] & (hp | hc | hn));
+                    if (i >= T && i < T + R) ch |= s2 ^ sv[i];
+                    sv[i] = s2;
+                    hp = hc;
+                    hc = hn;
                 }
+                if (__any_sync(0xffffffffu, own_lane && ch != 0)) tile_last = st;
             }
-            uint32_t* op = out + (ybase + 1) * wp + w;
 #pragma unroll
-            for (int i = T; i < T + R; ++i)
-                if (own_lane && wv && i < ihi - 1) op[(int64_t)i * wp] = sv[i];
+            for (int i = T; i < T + R; ++i) {
+                const int64_t y = ybase + i;
+                if (own_lane && wv && y < rows) out[(y + 1) * wp + w] = sv[i];
+            }
             if (lane == 0) fcur[t] = (uint8_t)(tile_last >= 0);
             my_last = max(my_last, tile_last);
         }
@@ -1126,6 +1241,47 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
         const FastDiv V = make_fastdiv((uint32_t)(W / 4));
         const uint4* s4 = reinterpret_cast<const uint4*>(src);
         uint4* d4 = reinterpret_cast<uint4*>(dst);
+        // TMA path: chunk bytes x stages per CTA (tuning knob MW_RGBA_TMA:
+        // 0 = LSU path, 1 = 16 KiB x 3, 2 = 8 KiB x 4, 3 = 8 KiB x 3, 4 = 4 KiB x 4)
+        static const int tma_cfg = tuning_knob("MW_RGBA_TMA", 2);
+        const int chunk = tma_cfg == 1 ? 16384 : (tma_cfg == 4 ? 4096 : 8192);
+        if (tma_cfg > 0 && (W * 4) % chunk == 0 &&
+            ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+#define MW_TMA_LAUNCH(CH, NS, MI, KMI, TI)                                                     \
+    do {                                                                                       \
+        constexpr size_t smem = 2 * NS * CH + 64;                                              \
+        static int occ = [] {                                                                  \
+            cudaFuncSetAttribute(k_rgba_ns_tma<CH, NS, MI, KMI, TI>,                           \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+            return resident_ctas(k_rgba_ns_tma<CH, NS, MI, KMI, TI>, 256, smem);               \
+        }();                                                                                   \
+        const int64_t items = rows * (W * 4 / CH);                                             \
+        ++g_launches;                                                                          \
+        k_rgba_ns_tma<CH, NS, MI, KMI, TI><<<grid_for(items, occ, L), 256, smem, L.stream>>>(  \
+            nc, src, dst, rows, (uint32_t)W, (uint32_t)row0);                                  \
+    } while (0)
+#define MW_TMA_CFG(MI, KMI, TI)                                                                \
+    do {                                                                                       \
+        if (tma_cfg == 1) MW_TMA_LAUNCH(16384, 3, MI, KMI, TI);                                \
+        else if (tma_cfg == 3) MW_TMA_LAUNCH(8192, 3, MI, KMI, TI);                            \
+        else if (tma_cfg == 4) MW_TMA_LAUNCH(4096, 4, MI, KMI, TI);                            \
+        else MW_TMA_LAUNCH(8192, 4, MI, KMI, TI);                                              \
+    } while (0)
+            const int sel = (p.mirror ? 4 : 0) | (p.key_mirror[0] ? 2 : 0) | (t128 ? 1 : 0);
+            switch (sel) {
+                case 0: MW_TMA_CFG(false, false, false); break;
+                case 1: MW_TMA_CFG(false, false, true); break;
+                case 2: MW_TMA_CFG(false, true, false); break;
+                case 3: MW_TMA_CFG(false, true, true); break;
+                case 4: MW_TMA_CFG(true, false, false); break;
+                case 5: MW_TMA_CFG(true, false, true); break;
+                case 6: MW_TMA_CFG(true, true, false); break;
+                default: MW_TMA_CFG(true, true, true); break;
+            }
+#undef MW_TMA_CFG
+#undef MW_TMA_LAUNCH
+            return cudaGetLastError();
+        }
         static const int unroll = tuning_knob("MW_RGBA_UNROLL", 2);
 #define MW_NS_LAUNCH_U(U, MI, KMI, TI)                                                    \
     do {                                                                                  \
@@ -1289,16 +1445,16 @@ template <int T, int ROWS>
 static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows,
                                  int64_t wp, int64_t max_iters, int* flags, int* state,
                                  uint8_t* tflags, const Launch& L) {
-    static int occ = resident_ctas(k_planes_loop<T, ROWS>, 32 * kTbWarps);
+    static int occ = resident_ctas(k_planes_loop<T, ROWS>, 256);
     constexpr int R = ROWS - 2 * T;
     const int64_t tiles = ((rows + R - 1) / R) * ((wp + 29) / 30);
     // cooperative: every CTA must be co-resident
-    unsigned grid = grid_for((tiles + kTbWarps - 1) / kTbWarps, occ, L);
+    unsigned grid = grid_for((tiles + 7) / 8, occ, L);
     int64_t r = rows, w = wp, mi = max_iters;
     void* args[] = {&S0, &S1, (void*)&K, &r, &w, &mi, &flags, &state, &tflags};
     ++g_launches;
-    return cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid),
-                                       dim3(32 * kTbWarps), args, 0, L.stream);
+    return cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid), dim3(256),
+                                       args, 0, L.stream);
 }
 
 cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,
@@ -1306,17 +1462,15 @@ cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t r
                         const Launch& L) {
     const int64_t wp = plane_words(W);
     static const int T = tuning_knob("MW_HYST_T", 8);
-    static const int ROWS = tuning_knob("MW_HYST_ROWS", 48);
+    static const int ROWS = tuning_knob("MW_HYST_ROWS", 40);
 #define MW_PL(TT, RR) \
     if (T == TT && ROWS == RR) return planes_loop_t<TT, RR>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L)
     MW_PL(4, 32);
-    MW_PL(8, 32);
-    MW_PL(4, 48);
-    MW_PL(12, 48);
-    MW_PL(8, 64);
-    MW_PL(16, 64);
+    MW_PL(6, 32);
+    MW_PL(8, 40);
+    MW_PL(12, 40);
 #undef MW_PL
-    return planes_loop_t<8, 48>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L);
+    return planes_loop_t<8, 40>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L);
 }
 
 cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4* vel_out,

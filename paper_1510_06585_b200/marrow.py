@@ -118,6 +118,7 @@ _SIG = {
     "mw_ctx_set_slowdown": [_vp, _i32, _f32],
     "mw_stats_enable": [_vp, _i32],
     "mw_graph_capture": [_vp, _vp, _P(mw_arg), _i32, _vp, _P(_vp)],
+    "mw_graph_capture_many": [_vp, _vp, _P(mw_arg), _i32, _i32, _vp, _P(_vp)],
     "mw_graph_launch": [_vp, _vp],
     "mw_graph_result": [_vp, _P(_f64), _i32],
     "mw_graph_kernels": [_vp, _P(_i64)],
@@ -583,6 +584,17 @@ def mw_graph_capture(ctx, node, args, stream=None):
     _call("mw_graph_capture", ctx.ptr, node.ptr, arr, len(args), _stream_arg(stream),
           ctypes.byref(out))
     return Graph(out, (arr, node, ctx, [getattr(a, "_owner", None) for a in args]))
+
+
+def mw_graph_capture_many(ctx, node, arg_sets, stream=None):
+    """One graph replaying len(arg_sets) back-to-back runs (set k on arg_sets[k])."""
+    nargs = len(arg_sets[0])
+    flat = [a for st in arg_sets for a in st]
+    arr = (mw_arg * len(flat))(*flat)
+    out = _vp()
+    _call("mw_graph_capture_many", ctx.ptr, node.ptr, arr, nargs, len(arg_sets),
+          _stream_arg(stream), ctypes.byref(out))
+    return Graph(out, (arr, node, ctx, [getattr(a, "_owner", None) for a in flat]))
 
 
 def mw_graph_launch(g, stream=None):

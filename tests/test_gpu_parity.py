@@ -87,7 +87,8 @@ def oracle_filter(img, seed=4, S=8, T=128):
                                       sct.Leaf("mirror")]), img).value
 
 
-@pytest.mark.parametrize("H,W", [(2, 4), (37, 64), (33, 61), (5, 1), (256, 512), (900, 1440), (1125, 1800)])
+@pytest.mark.parametrize("H,W", [(2, 4), (37, 64), (33, 61), (5, 1), (256, 512), (900, 1440), (1125, 1800),
+                                 (33, 4096), (7, 8192)])
 def test_filter_pipeline_bitwise(H, W):
     rng = np.random.default_rng(H * 7 + W)
     img = synth.np_rgba(3, 0, H * W).reshape(H, W, 4)

@@ -406,6 +406,18 @@ class NBody(Workload):
                 "bodies_per_rank": self.n, "interactions_per_step": self.N * self.N}
 
 
+# workload-describing config keys shared by both arms
+REF_CONFIG = {
+    "filter": {"image": [8192, 8192, 4],
+               "tree": "pipeline(gauss_noise(seed=4,S=8), solarize(T=128), mirror)"},
+    "saxpy": {"n": 1 << 20, "a": 2.5},
+    "segmentation": {"shape_zyx": [512, 1024, 1024], "lo": 85, "hi": 170},
+    "mapreduce_sum": {"n": 1 << 30}, "mapreduce_dot": {"n": 1 << 30},
+    "hysteresis": {"tree": "pipeline(threshold(173,250), loop_while_changed(step, "
+                           "check_every=1), finalize)"},
+    "nbody": {"bodies": 1 << 20, "eps2": 1e-4, "dt": 1e-3},
+}
+
 KCLASS = {0: "saxpy_chain", 1: "rgba_chain (k_rgba_ns)", 2: "u8_chain / plane pack+unpack",
           3: "hysteresis stencil loop", 4: "k_nbody", 5: "k_reduce_chunks", 6: "traits"}
 
@@ -519,7 +531,8 @@ def run_reference(args, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * spent / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
             "data": "synthetic (SplitMix64, seeded; DESIGN.md input recipe)",
-            "config": {"workload": name, "arm": "CPU oracle (oracle/, plain C, 1 thread)"},
+            "config": dict(REF_CONFIG.get(wl, {}), workload=name,
+                           arm="CPU oracle (oracle/, plain C, 1 thread)"),
             "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "oracle",
                              "sample": f"per step: {sample}"},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -981,6 +981,7 @@ __device__ __forceinline__ float rsqrt_mufu(float x) {
 //   d = p_j - p_i;  r2 = dx*dx + (dy*dy + (dz*dz + eps2));  inv = rsqrt(r2)
 //   w = (m_j * inv) * (inv * inv);  f += d * w
 // = 6 packed ops per coordinate triple + 6 more: 12 FP32x2 + 2 MUFU per pair.
+template <bool SPLIT>
 __global__ void __launch_bounds__(kNbTile) k_nbody(const float4* __restrict__ pos,
                                                    const float4* __restrict__ vel,
                                                    float4* __restrict__ pos_out,
@@ -1025,9 +1026,12 @@ __global__ void __launch_bounds__(kNbTile) k_nbody(const float4* __restrict__ po
             const int64_t j = jt + threadIdx.x;
             sp[threadIdx.x] = j < N ? pos[j] : make_float4(0.f, 0.f, 0.f, 0.f);  // mass-0 pads
             __syncthreads();
-            f2_t fx[kNbPairs], fy[kNbPairs], fz[kNbPairs];
+            f2_t fx[kNbPairs], fy[kNbPairs], fz[kNbPairs];   // packed accumulators
+            float gx[kNbPer], gy[kNbPer], gz[kNbPer];        // scalar accumulators (SPLIT)
 #pragma unroll
             for (int h = 0; h < kNbPairs; ++h) fx[h] = fy[h] = fz[h] = 0ull;
+#pragma unroll
+            for (int q = 0; q < kNbPer; ++q) gx[q] = gy[q] = gz[q] = 0.f;
 #pragma unroll 8
             for (int k = 0; k < kNbTile; ++k) {
                 const float4 s4 = sp[k];
@@ -1041,10 +1045,29 @@ __global__ void __launch_bounds__(kNbTile) k_nbody(const float4* __restrict__ po
                     float r0, r1;
                     f2_unpack(r2, r0, r1);
                     const f2_t inv = f2_pack(rsqrt_mufu(r0), rsqrt_mufu(r1));
-                    const f2_t w = f2_mul(f2_mul(sw, inv), f2_mul(inv, inv));
-                    fx[h] = f2_fma(dx, w, fx[h]);
-                    fy[h] = f2_fma(dy, w, fy[h]);
-                    fz[h] = f2_fma(dz, w, fz[h]);
+                    if (SPLIT) {
+                        // 8 packed ops on the FMA-heavy pipe, 8 scalar ops free to
+                        // issue to the FMA-lite pipe (same roundings as the packed form)
+                        const f2_t t = f2_mul(sw, inv), i2 = f2_mul(inv, inv);
+                        float t0, t1, q0, q1, x0, x1, y0, y1, z0, z1;
+                        f2_unpack(t, t0, t1);
+                        f2_unpack(i2, q0, q1);
+                        f2_unpack(dx, x0, x1);
+                        f2_unpack(dy, y0, y1);
+                        f2_unpack(dz, z0, z1);
+                        const float w0 = t0 * q0, w1 = t1 * q1;
+                        gx[2 * h] = __fmaf_rn(x0, w0, gx[2 * h]);
+                        gx[2 * h + 1] = __fmaf_rn(x1, w1, gx[2 * h + 1]);
+                        gy[2 * h] = __fmaf_rn(y0, w0, gy[2 * h]);
+                        gy[2 * h + 1] = __fmaf_rn(y1, w1, gy[2 * h + 1]);
+                        gz[2 * h] = __fmaf_rn(z0, w0, gz[2 * h]);
+                        gz[2 * h + 1] = __fmaf_rn(z1, w1, gz[2 * h + 1]);
+                    } else {
+                        const f2_t w = f2_mul(f2_mul(sw, inv), f2_mul(inv, inv));
+                        fx[h] = f2_fma(dx, w, fx[h]);
+                        fy[h] = f2_fma(dy, w, fy[h]);
+                        fz[h] = f2_fma(dz, w, fz[h]);
+                    }
                 }
             }
 #pragma unroll
@@ -1053,6 +1076,11 @@ __global__ void __launch_bounds__(kNbTile) k_nbody(const float4* __restrict__ po
                 f2_unpack(fx[h], x0, x1);
                 f2_unpack(fy[h], y0, y1);
                 f2_unpack(fz[h], z0, z1);
+                if (SPLIT) {
+                    x0 = gx[2 * h]; x1 = gx[2 * h + 1];
+                    y0 = gy[2 * h]; y1 = gy[2 * h + 1];
+                    z0 = gz[2 * h]; z1 = gz[2 * h + 1];
+                }
                 ax[2 * h] += (double)x0; ax[2 * h + 1] += (double)x1;
                 ay[2 * h] += (double)y0; ay[2 * h + 1] += (double)y1;
                 az[2 * h] += (double)z0; az[2 * h + 1] += (double)z1;
@@ -1242,9 +1270,11 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
         const uint4* s4 = reinterpret_cast<const uint4*>(src);
         uint4* d4 = reinterpret_cast<uint4*>(dst);
         // TMA path: chunk bytes x stages per CTA (tuning knob MW_RGBA_TMA:
-        // 0 = LSU path, 1 = 16 KiB x 3, 2 = 8 KiB x 4, 3 = 8 KiB x 3, 4 = 4 KiB x 4)
-        static const int tma_cfg = tuning_knob("MW_RGBA_TMA", 2);
-        const int chunk = tma_cfg == 1 ? 16384 : (tma_cfg == 4 ? 4096 : 8192);
+        // 0 = LSU path, 1 = 16 KiB x 3 (measured best), 2 = 8 KiB x 4, 3 = 8 KiB x 3,
+        // 4 = 4 KiB x 4, 5 = 32 KiB x 3, 6 = 16 KiB x 6)
+        static const int tma_cfg = tuning_knob("MW_RGBA_TMA", 1);
+        const int chunk = (tma_cfg == 1 || tma_cfg == 6) ? 16384
+                          : (tma_cfg == 4 ? 4096 : (tma_cfg == 5 ? 32768 : 8192));
         if (tma_cfg > 0 && (W * 4) % chunk == 0 &&
             ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
 #define MW_TMA_LAUNCH(CH, NS, MI, KMI, TI)                                                     \
@@ -1263,6 +1293,8 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
 #define MW_TMA_CFG(MI, KMI, TI)                                                                \
     do {                                                                                       \
         if (tma_cfg == 1) MW_TMA_LAUNCH(16384, 3, MI, KMI, TI);                                \
+        else if (tma_cfg == 5) MW_TMA_LAUNCH(32768, 3, MI, KMI, TI);                           \
+        else if (tma_cfg == 6) MW_TMA_LAUNCH(16384, 6, MI, KMI, TI);                           \
         else if (tma_cfg == 3) MW_TMA_LAUNCH(8192, 3, MI, KMI, TI);                            \
         else if (tma_cfg == 4) MW_TMA_LAUNCH(4096, 4, MI, KMI, TI);                            \
         else MW_TMA_LAUNCH(8192, 4, MI, KMI, TI);                                              \
@@ -1477,11 +1509,20 @@ cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4*
                   float4* acc, int64_t first, int64_t count, int64_t N, float eps2, float dt,
                   int mode, const Launch& L) {
     if (count <= 0) return cudaSuccess;
-    static int occ = resident_ctas(k_nbody, kNbTile);
+    // MW_NBODY_SPLIT: 1 = packed FP32x2 + scalar split across the FMA pipes (measured
+    // slower on B200: 537 vs 519 ms per 2^20 step, so off by default)
+    static const int split = tuning_knob("MW_NBODY_SPLIT", 0);
     int64_t blocks = (count + kNbTile * kNbPer - 1) / (kNbTile * kNbPer);
     ++g_launches;
-    k_nbody<<<grid_for(blocks, occ, L), kNbTile, 0, L.stream>>>(pos, vel, pos_out, vel_out, acc,
-                                                                first, count, N, eps2, dt, mode);
+    if (split) {
+        static int occ = resident_ctas(k_nbody<true>, kNbTile);
+        k_nbody<true><<<grid_for(blocks, occ, L), kNbTile, 0, L.stream>>>(
+            pos, vel, pos_out, vel_out, acc, first, count, N, eps2, dt, mode);
+    } else {
+        static int occ = resident_ctas(k_nbody<false>, kNbTile);
+        k_nbody<false><<<grid_for(blocks, occ, L), kNbTile, 0, L.stream>>>(
+            pos, vel, pos_out, vel_out, acc, first, count, N, eps2, dt, mode);
+    }
     return cudaGetLastError();
 }
 

@@ -494,3 +494,34 @@ def test_graph_capture_replay():
         with torch.cuda.stream(s):
             M.mw_graph_capture(c, trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)], s)
     assert e.value.status == M.MW_E_UNSUPPORTED
+
+
+# ----------------------------------------------------------------- degenerate inputs
+def test_empty_inputs():
+    c = ctx(3, [0.2, 0.3, 0.5])
+    e = torch.empty((0, 16, 4), dtype=torch.uint8, device=DEV)
+    run(c, trees.filter_pipeline(), [M.arg(e), M.arg(torch.empty_like(e))])
+    v = torch.empty((0, 8, 8), dtype=torch.uint8, device=DEV)
+    run(c, trees.segmentation(), [M.arg(v), M.arg(torch.empty_like(v))])
+    x = torch.empty(0, dtype=torch.float32, device=DEV)
+    run(c, trees.saxpy(), [M.arg(x), M.arg(torch.empty_like(x))])
+    g = torch.empty((0, 33), dtype=torch.uint8, device=DEV)
+    for cc in (c, ctx(1)):
+        r = run(cc, trees.hysteresis(), [M.arg(g), M.arg(torch.empty_like(g))])
+        assert r["executions"] == 1 and r["converged"]   # one execution that changes nothing
+    p = torch.empty((0, 4), dtype=torch.float32, device=DEV)
+    run(c, trees.nbody(2), [M.arg(p, M.MW_COPY), M.arg(torch.empty_like(p), M.MW_COPY)])
+
+
+def test_single_pixel_and_single_row_images():
+    for H, W in ((1, 1), (1, 4096), (4096, 1)):
+        img = synth.np_rgba(3, 0, H * W).reshape(H, W, 4)
+        dst = torch.empty((H, W, 4), dtype=torch.uint8, device=DEV)
+        run(ctx(2, [0.5, 0.5]), trees.filter_pipeline(), [M.arg(dev(img)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), oracle_filter(img))
+        gray = synth.np_u8_stream(8, 0, H * W).reshape(H, W)
+        want, D = oracle_hyst(gray)
+        for cc in (ctx(1), ctx(2, [0.5, 0.5])):
+            out = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+            r = run(cc, trees.hysteresis(), [M.arg(dev(gray)), M.arg(out)])
+            assert np.array_equal(out.cpu().numpy(), want) and r["executions"] == D + 1

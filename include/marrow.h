@@ -304,6 +304,60 @@ mw_status mw_get_balance_state(const mw_ctx* ctx, mw_balance_state* out);
  * kernel is a grid-stride loop), only the partition's time grows.          */
 mw_status mw_ctx_set_slowdown(mw_ctx* ctx, int32_t part, float factor);
 
+/* Tuning knobs: the B200 platform configuration of a profile (P:446-456
+ * item (d)) — block/element shapes the profile builder (mw_autotune)
+ * searches.  Every value gives bit-identical results.  Defaults are the
+ * measured best on B200 (MW_* environment variables override them).       */
+enum {
+    MW_TUNE_RGBA_TMA = 0,     /* fused RGBA chain: 0 LSU path, 1 = 16 KiB x 3 stages TMA,
+                                 2 = 8 KiB x 4, 3 = 8 KiB x 3, 4 = 4 KiB x 4, 5 = 32 KiB x 3,
+                                 6 = 16 KiB x 6                                            */
+    MW_TUNE_RGBA_UNROLL = 1,  /* LSU path: 16-byte vectors per thread (2, 4, 8)            */
+    MW_TUNE_HYST_PLANES = 2,  /* 1: one-partition hysteresis on bit planes; 0: byte stencil */
+    MW_TUNE_HYST_T = 3,       /* executions per pass of the plane loop (4, 6, 8, 12)        */
+    MW_TUNE_HYST_ROWS = 4,    /* register rows per plane tile (32, 40)                      */
+    MW_TUNE_NBODY_SPLIT = 5,  /* 1: split packed/scalar FP32 across the FMA pipes           */
+    MW_TUNE_U8_TMA = 6,       /* 1: TMA bulk-copy ring for contiguous u8 chains (volumes)   */
+    MW_TUNE_COUNT = 7
+};
+mw_status mw_ctx_set_tuning(mw_ctx* ctx, int32_t knob, int32_t value);
+mw_status mw_ctx_get_tuning(const mw_ctx* ctx, int32_t knob, int32_t* value);
+
+/* ------------------------------------------------------------------ profiles / Knowledge Base
+ * NEXT-2 of SURVEY §8(f): the paper's Knowledge Base stores, per
+ * (SCT id, workload), the best configuration found (profile items (a)-(f),
+ * P:446-456): the tree's content hash, the global shape, the distribution
+ * vector, the tuning knobs, the best time and the provenance.  Lookup
+ * derives a configuration for an unseen workload by narrowing the scope
+ * SCT -> workload -> dimensionality, nearest neighbour in
+ * log2-size space (R22).  The file is plain text, one record per
+ * line, rewritten by mw_kb_save / mw_kb_close.                             */
+typedef struct mw_kb mw_kb;
+enum { MW_PROV_BUILT = 0, MW_PROV_DERIVED = 1, MW_PROV_BALANCED = 2 };
+enum { MW_KB_NONE = 0, MW_KB_EXACT = 1, MW_KB_SCT = 2, MW_KB_WORKLOAD = 3,
+       MW_KB_DIMENSIONALITY = 4 };
+mw_status mw_kb_open(const char* path /* NULL or "" = in memory */, mw_kb** out);
+mw_status mw_kb_save(const mw_kb* kb);
+mw_status mw_kb_close(mw_kb* kb);                      /* saves, then frees */
+mw_status mw_kb_count(const mw_kb* kb, int32_t* n);
+/* Keeps the better of an existing (SCT, workload) record and this one
+ * (progressive refinement); derived records are always replaced. */
+mw_status mw_kb_store(mw_kb* kb, const mw_node* root, const int64_t* dims, int32_t ndims,
+                      const int32_t* tune /* MW_TUNE_COUNT */, const double* fractions,
+                      int32_t nparts, double best_ms, int32_t provenance);
+/* *scope = MW_KB_NONE when nothing applies (outputs untouched), else the
+ * narrowing level that matched; fractions_out (nparts) gets the record's
+ * distribution when its partition count matches, else uniform.             */
+mw_status mw_kb_lookup(const mw_kb* kb, const mw_node* root, const int64_t* dims, int32_t ndims,
+                       int32_t* tune_out, double* fractions_out, int32_t nparts, int32_t* scope);
+/* Profile building (Alg. 1, over the B200 knobs): runs `root` on
+ * `args` (collective like mw_run) warm-up + `reps` times per candidate
+ * setting of the knobs that apply to its plan, keeps the fastest in the ctx,
+ * stores it in `kb` (if not NULL, provenance BUILT) and returns it.
+ * In-place arguments (Saxpy y, N-body state) are restored afterwards.        */
+mw_status mw_autotune(mw_ctx* ctx, const mw_node* root, const mw_arg* args, int32_t nargs,
+                      void* stream, int32_t reps, mw_kb* kb, int32_t* tune_out, double* best_ms);
+
 /* Number of kernels this library launched on the ctx since creation.        */
 mw_status mw_ctx_launch_count(const mw_ctx* ctx, int64_t* out);
 

@@ -99,6 +99,7 @@ struct mw_ctx {
     cudaEvent_t st_in[kStageSlots]{}, st_comp[kStageSlots]{}, st_out[kStageSlots]{};
     cudaEvent_t st_start = nullptr;
     bool capturing = false;     // inside mw_graph_capture: no timing events, no host syncs
+    int tune[mwk::TUNE_COUNT];  // tuning knobs (mw_ctx_set_tuning)
 };
 
 struct mw_future {
@@ -186,6 +187,7 @@ mwk::Launch launch_for(mw_ctx* c, cudaStream_t s, int part) {
     mwk::Launch L;
     L.stream = s;
     L.slow = c->slow[part];
+    L.tune = c->tune;
     return L;
 }
 mw_status kerr(cudaError_t e, const char* what) {
@@ -404,10 +406,7 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
                 sidx = (int)i;
                 ++nst;
             }
-        static const bool planes_on = [] {
-            const char* v = getenv("MW_HYST_PLANES");
-            return !(v && v[0] == '0');
-        }();
+        const bool planes_on = c->tune[mwk::TUNE_HYST_PLANES] != 0;
         const int p0 = R.first;
         const bool eligible = planes_on && nst == 1 && sidx == 1 && c->nranks == 1 && ppr == 1 &&
                               prog[0].kind == StepKind::U8 && !prog[0].ops.empty() &&
@@ -844,7 +843,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
                             std::to_string(s1) + ")");
     }
     if (nargs == 2 && ik != MW_VK_SAXPY && ik != MW_VK_VEC2 && args[0].ptr == args[1].ptr &&
-        args[0].ptr && args[0].location == args[1].location)
+        args[0].ptr && L > 0 && args[0].location == args[1].location)
         return fail(MW_E_SHAPE_MISMATCH, "src and dst must not alias");
     // ---- execute
     c->recs.clear();
@@ -895,7 +894,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
     } else if (ik == MW_VK_U8 || ik == MW_VK_U8_2D) {
         MW_OK_OR_RETURN(run_u8(R, prog, args[0], args[1], f));
     } else if (ik == MW_VK_NBODY && ok == MW_VK_NBODY) {
-        if (args[0].ptr == args[1].ptr) return fail(MW_E_SHAPE_MISMATCH, "pos and vel alias");
+        if (L > 0 && args[0].ptr == args[1].ptr) return fail(MW_E_SHAPE_MISMATCH, "pos and vel alias");
         if (!prog.empty()) MW_OK_OR_RETURN(run_nbody(R, prog[0], args[0], args[1]));
     } else if (ik == MW_VK_NBODY) {
         const Step& stp = prog[0];
@@ -987,6 +986,7 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
     c->P = nranks * parts_per_rank;
     c->dist.assign(c->P, 1.0 / c->P);
     c->slow.assign(c->P, 1.0f);
+    mwk::tune_defaults(c->tune);
     if (alloc) {
         c->alloc = *alloc;
         c->has_alloc = true;
@@ -1077,6 +1077,11 @@ mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nar
                  mw_future** out) {
     if (!c || !root || !out || (nargs > 0 && !args)) return fail(MW_E_INVALID_SPEC, "NULL argument");
     CUDA_OK(cudaSetDevice(c->device));
+    // Consume a stale non-sticky error left in the runtime's last-error slot by
+    // an unrelated earlier call (ours or the host application's), so that the
+    // post-launch checks below report only this run's launches.  Sticky
+    // (asynchronous) faults are still returned by every subsequent call.
+    (void)cudaGetLastError();
     std::unique_ptr<mw_future> f(new mw_future);
     f->ctx = c;
     if (c->res_free.empty()) {
@@ -1260,6 +1265,28 @@ mw_status mw_ctx_set_slowdown(mw_ctx* c, int32_t part, float factor) {
     return MW_OK;
 }
 
+mw_status mw_ctx_set_tuning(mw_ctx* c, int32_t knob, int32_t value) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    if (knob < 0 || knob >= MW_TUNE_COUNT) return fail(MW_E_INVALID_SPEC, "unknown tuning knob");
+    if (!mwk::tune_valid(knob, value))
+        return fail(MW_E_INVALID_SPEC, "tuning value not supported for knob " + std::to_string(knob));
+    if (knob == MW_TUNE_HYST_T || knob == MW_TUNE_HYST_ROWS) {   // (T, ROWS) must be a built pair
+        int T = knob == MW_TUNE_HYST_T ? value : c->tune[MW_TUNE_HYST_T];
+        int Rw = knob == MW_TUNE_HYST_ROWS ? value : c->tune[MW_TUNE_HYST_ROWS];
+        const bool ok = (Rw == 32 && (T == 4 || T == 6 || T == 8)) || (Rw == 40 && (T == 8 || T == 12));
+        if (!ok) return fail(MW_E_INVALID_SPEC, "(hyst T, rows) pair not built: use (4|6|8, 32) or (8|12, 40)");
+    }
+    c->tune[knob] = value;
+    return MW_OK;
+}
+
+mw_status mw_ctx_get_tuning(const mw_ctx* c, int32_t knob, int32_t* value) {
+    if (!c || !value) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    if (knob < 0 || knob >= MW_TUNE_COUNT) return fail(MW_E_INVALID_SPEC, "unknown tuning knob");
+    *value = c->tune[knob];
+    return MW_OK;
+}
+
 mw_status mw_ctx_launch_count(const mw_ctx* c, int64_t* out) {
     if (!c || !out) return fail(MW_E_INVALID_SPEC, "NULL argument");
     *out = (int64_t)(mwk::launch_count() - c->launches0);
@@ -1354,6 +1381,126 @@ mw_status mw_graph_destroy(mw_graph* g) {
     if (g->graph) cudaGraphDestroy(g->graph);
     if (g->f.res) cudaFreeHost(g->f.res);
     delete g;
+    return MW_OK;
+}
+
+
+// ------------------------------------------------------------ profile building
+mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
+                      void* stream, int32_t reps, mw_kb* kb, int32_t* tune_out, double* best_ms) {
+    if (!c || !root || (nargs > 0 && !args) || reps < 1) return fail(MW_E_INVALID_SPEC, "bad argument");
+    CUDA_OK(cudaSetDevice(c->device));
+    const Node* r = reinterpret_cast<const Node*>(root);
+    std::vector<Step> prog;
+    MW_OK_OR_RETURN(mw::plan(r, &prog));
+    bool has_rgba = false, has_stencil = false, has_nbody = false, has_u8 = false;
+    for (const Step& st : prog) {
+        has_u8 |= st.kind == StepKind::U8;
+        has_rgba |= st.kind == StepKind::Rgba;
+        has_stencil |= st.kind == StepKind::StencilFor || st.kind == StepKind::StencilWhile;
+        has_nbody |= st.kind == StepKind::NbodyLoop || st.kind == StepKind::NbodyAccel;
+    }
+    using Tune = std::vector<int>;
+    const Tune base(c->tune, c->tune + mwk::TUNE_COUNT);
+    std::vector<Tune> cands{base};
+    if (has_rgba) {
+        for (int tma = 0; tma <= 6; ++tma)
+            for (int un : {2, 4, 8}) {
+                if (tma > 0 && un != base[mwk::TUNE_RGBA_UNROLL]) continue;
+                Tune t = base;
+                t[mwk::TUNE_RGBA_TMA] = tma;
+                t[mwk::TUNE_RGBA_UNROLL] = un;
+                cands.push_back(t);
+            }
+    }
+    if (has_stencil) {
+        const int pairs[5][2] = {{4, 32}, {6, 32}, {8, 32}, {8, 40}, {12, 40}};
+        Tune t = base;
+        t[mwk::TUNE_HYST_PLANES] = 0;
+        cands.push_back(t);
+        for (auto& pr : pairs) {
+            Tune u = base;
+            u[mwk::TUNE_HYST_PLANES] = 1;
+            u[mwk::TUNE_HYST_T] = pr[0];
+            u[mwk::TUNE_HYST_ROWS] = pr[1];
+            cands.push_back(u);
+        }
+    }
+    if (has_u8)
+        for (int v : {0, 1}) {
+            Tune t = base;
+            t[mwk::TUNE_U8_TMA] = v;
+            cands.push_back(t);
+        }
+    if (has_nbody)
+        for (int sp : {0, 1}) {
+            Tune t = base;
+            t[mwk::TUNE_NBODY_SPLIT] = sp;
+            cands.push_back(t);
+        }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // snapshot the arguments a run updates in place
+    std::vector<std::pair<const mw_arg*, void*>> snaps;
+    const int ik = r->in_kind, ok = r->out_kind;
+    auto bytes_of = [](const mw_arg& a) {
+        int64_t n = a.mode == MW_COPY ? a.shape[0] : a.local_rows;
+        return (size_t)(n * row_bytes(a));
+    };
+    std::vector<int> inplace;
+    if (ik == MW_VK_SAXPY && nargs == 2) inplace = {1};
+    if (ik == MW_VK_NBODY && ok == MW_VK_NBODY && nargs == 2) inplace = {0, 1};
+    for (int i : inplace) {
+        void* p;
+        MW_OK_OR_RETURN(scratch(c, "autotune_snap" + std::to_string(i), bytes_of(args[i]) + 16, s, &p));
+        CUDA_OK(cudaMemcpyAsync(p, args[i].ptr, bytes_of(args[i]), cudaMemcpyDefault, s));
+        snaps.push_back({&args[i], p});
+    }
+    auto restore = [&]() -> mw_status {
+        for (auto& sn : snaps)
+            CUDA_OK(cudaMemcpyAsync(sn.first->ptr, sn.second, bytes_of(*sn.first), cudaMemcpyDefault, s));
+        return MW_OK;
+    };
+    cudaEvent_t e0, e1;
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    mw_future f;
+    f.ctx = c;
+    double tmp[4] = {0, 0, 0, 0};
+    f.res = tmp;   // host memory is fine: results are only written by D2H copies we sync on
+    double best = 1e300;
+    Tune best_t = base;
+    mw_status st = MW_OK;
+    for (const Tune& t : cands) {
+        for (int k = 0; k < mwk::TUNE_COUNT; ++k) c->tune[k] = t[k];
+        st = run(c, r, args, nargs, s, &f);   // warm-up (allocates scratch)
+        if (st != MW_OK) break;
+        CUDA_OK(cudaEventRecord(e0, s));
+        for (int i = 0; i < reps && st == MW_OK; ++i) st = run(c, r, args, nargs, s, &f);
+        if (st != MW_OK) break;
+        CUDA_OK(cudaEventRecord(e1, s));
+        CUDA_OK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        const double per = (double)ms / reps;
+        if (per < best) {
+            best = per;
+            best_t = t;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (int k = 0; k < mwk::TUNE_COUNT; ++k) c->tune[k] = best_t[k];
+    MW_OK_OR_RETURN(restore());
+    CUDA_OK(cudaStreamSynchronize(s));
+    if (st != MW_OK) return st;
+    if (kb) {
+        std::vector<int64_t> dims(args[0].shape, args[0].shape + args[0].ndim);
+        MW_OK_OR_RETURN(mw_kb_store(kb, root, dims.data(), (int32_t)dims.size(), best_t.data(),
+                                    c->dist.data(), c->P, best, MW_PROV_BUILT));
+    }
+    if (tune_out)
+        for (int k = 0; k < mwk::TUNE_COUNT; ++k) tune_out[k] = best_t[k];
+    if (best_ms) *best_ms = best;
     return MW_OK;
 }
 

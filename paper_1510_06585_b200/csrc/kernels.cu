@@ -564,6 +564,70 @@ __global__ void __launch_bounds__(256) k_u8_vec(const __grid_constant__ U8Prog p
         }
     }
 }
+// ---- TMA (bulk-copy) streaming variant of the u8 chain for contiguous rows
+// (segmentation volumes): same ring as k_rgba_ns_tma, flat byte stream.
+template <int CH, int NS>
+__global__ void __launch_bounds__(256) k_u8_tma(const __grid_constant__ U8Prog p,
+                                                const __grid_constant__ U8Const c,
+                                                const uint8_t* __restrict__ src,
+                                                uint8_t* __restrict__ dst, int64_t nbytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint4* sin = reinterpret_cast<uint4*>(smem);
+    uint4* sout = reinterpret_cast<uint4*>(smem + NS * CH);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * NS * CH);
+    const int64_t n_items = (nbytes + CH - 1) / CH;
+    constexpr uint32_t VPC = CH / 16;
+    auto len_of = [&](int64_t item) { return (uint32_t)min((int64_t)CH, nbytes - item * CH); };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < NS; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < NS; ++st) {
+            const int64_t item = blockIdx.x + (int64_t)st * gridDim.x;
+            if (item < n_items) {
+                mbar_expect_tx(&bar[st], len_of(item));
+                bulk_load(sin + st * VPC, src + item * CH, len_of(item), &bar[st]);
+            }
+        }
+    }
+    __syncthreads();
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int stage = it % NS;
+        mbar_wait(&bar[stage], (uint32_t)(it / NS) & 1u);
+        if (threadIdx.x == 0) bulk_wait_read<NS - 1>();
+        __syncthreads();
+        const uint32_t nv = len_of(item) / 16;
+        const uint4* in = sin + stage * VPC;
+        uint4* out = sout + stage * VPC;
+        constexpr int PER = VPC / 256;
+        uint32_t w[4 * PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t v = k * 256u + threadIdx.x;
+            const uint4 q = v < nv ? in[v] : make_uint4(0, 0, 0, 0);
+            w[4 * k] = q.x; w[4 * k + 1] = q.y; w[4 * k + 2] = q.z; w[4 * k + 3] = q.w;
+        }
+        u8_apply_words<4 * PER>(p, c, w);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t v = k * 256u + threadIdx.x;
+            if (v < nv) out[v] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_store(dst + item * CH, out, len_of(item));
+            const int64_t nxt = item + (int64_t)NS * gridDim.x;
+            if (nxt < n_items) {
+                mbar_expect_tx(&bar[stage], len_of(nxt));
+                bulk_load(sin + stage * VPC, src + nxt * CH, len_of(nxt), &bar[stage]);
+            }
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait_read<0>();
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void k_u8_scalar(const __grid_constant__ U8Prog p, const uint8_t* __restrict__ src, int64_t sp,
                             uint8_t* __restrict__ dst, int64_t dp, int64_t rows, int64_t W) {
     int64_t total = rows * W;
@@ -1209,6 +1273,34 @@ __global__ void k_traits(int64_t* out, int64_t count, int64_t size, int64_t offs
 // ============================================================ launchers
 unsigned long long launch_count() { return g_launches; }
 
+void tune_defaults(int* out) {
+    out[TUNE_RGBA_TMA] = tuning_knob("MW_RGBA_TMA", 1);        // 16 KiB x 3 stages
+    out[TUNE_RGBA_UNROLL] = tuning_knob("MW_RGBA_UNROLL", 2);
+    out[TUNE_HYST_PLANES] = tuning_knob("MW_HYST_PLANES", 1);
+    out[TUNE_HYST_T] = tuning_knob("MW_HYST_T", 8);
+    out[TUNE_HYST_ROWS] = tuning_knob("MW_HYST_ROWS", 40);
+    out[TUNE_NBODY_SPLIT] = tuning_knob("MW_NBODY_SPLIT", 0);
+    out[TUNE_U8_TMA] = tuning_knob("MW_U8_TMA", 1);
+    for (int k = 0; k < TUNE_COUNT; ++k)
+        if (!tune_valid(k, out[k])) {   // ignore malformed overrides
+            const int d[TUNE_COUNT] = {1, 2, 1, 8, 40, 0, 1};
+            out[k] = d[k];
+        }
+}
+
+bool tune_valid(int knob, int v) {
+    switch (knob) {
+        case TUNE_RGBA_TMA: return v >= 0 && v <= 6;
+        case TUNE_RGBA_UNROLL: return v == 2 || v == 4 || v == 8;
+        case TUNE_HYST_PLANES: return v == 0 || v == 1;
+        case TUNE_HYST_T: return v == 4 || v == 6 || v == 8 || v == 12;
+        case TUNE_HYST_ROWS: return v == 32 || v == 40;
+        case TUNE_NBODY_SPLIT: return v == 0 || v == 1;
+        case TUNE_U8_TMA: return v == 0 || v == 1;
+    }
+    return false;
+}
+
 int sm_count() {
     if (g_sms == 0) {
         int dev = 0, n = 0;
@@ -1272,7 +1364,7 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
         // TMA path: chunk bytes x stages per CTA (tuning knob MW_RGBA_TMA:
         // 0 = LSU path, 1 = 16 KiB x 3 (measured best), 2 = 8 KiB x 4, 3 = 8 KiB x 3,
         // 4 = 4 KiB x 4, 5 = 32 KiB x 3, 6 = 16 KiB x 6)
-        static const int tma_cfg = tuning_knob("MW_RGBA_TMA", 1);
+        const int tma_cfg = L.tune[TUNE_RGBA_TMA];
         const int chunk = (tma_cfg == 1 || tma_cfg == 6) ? 16384
                           : (tma_cfg == 4 ? 4096 : (tma_cfg == 5 ? 32768 : 8192));
         if (tma_cfg > 0 && (W * 4) % chunk == 0 &&
@@ -1314,7 +1406,7 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
 #undef MW_TMA_LAUNCH
             return cudaGetLastError();
         }
-        static const int unroll = tuning_knob("MW_RGBA_UNROLL", 2);
+        const int unroll = L.tune[TUNE_RGBA_UNROLL];
 #define MW_NS_LAUNCH_U(U, MI, KMI, TI)                                                    \
     do {                                                                                  \
         static int occ = resident_ctas(k_rgba_ns<U, MI, KMI, TI>, 256);                   \
@@ -1376,8 +1468,21 @@ cudaError_t u8_chain(const U8Prog& p, const uint8_t* src, int64_t sp, uint8_t* d
         c.lo7[k] = (uint32_t)(p.lo[k] & 0x7F) * 0x01010101u;
         c.hi7[k] = (uint32_t)(p.hi[k] & 0x7F) * 0x01010101u;
     }
-    const bool vec = (W % 16 == 0) && (sp % 16 == 0) && (dp % 16 == 0) &&
-                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 &&
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    if (L.tune[TUNE_U8_TMA] && sp == W && dp == W && aligned && (rows * W) % 16 == 0) {
+        constexpr int CH = 16384, NS = 3;
+        constexpr size_t smem = 2 * NS * CH + 64;
+        static int occ = [] {
+            cudaFuncSetAttribute(k_u8_tma<CH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            return resident_ctas(k_u8_tma<CH, NS>, 256, smem);
+        }();
+        ++g_launches;
+        k_u8_tma<CH, NS><<<grid_for((rows * W + CH - 1) / CH, occ, L), 256, smem, L.stream>>>(
+            p, c, src, dst, rows * W);
+        return cudaGetLastError();
+    }
+    const bool vec = (W % 16 == 0) && (sp % 16 == 0) && (dp % 16 == 0) && aligned &&
                      rows * (W / 16) < (1ll << 31);
     if (vec) {
         constexpr int U = 4;
@@ -1493,12 +1598,13 @@ cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t r
                         int64_t max_iters, int* flags, int* state, uint8_t* tflags,
                         const Launch& L) {
     const int64_t wp = plane_words(W);
-    static const int T = tuning_knob("MW_HYST_T", 8);
-    static const int ROWS = tuning_knob("MW_HYST_ROWS", 40);
+    const int T = L.tune[TUNE_HYST_T];
+    const int ROWS = L.tune[TUNE_HYST_ROWS];
 #define MW_PL(TT, RR) \
     if (T == TT && ROWS == RR) return planes_loop_t<TT, RR>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L)
     MW_PL(4, 32);
     MW_PL(6, 32);
+    MW_PL(8, 32);
     MW_PL(8, 40);
     MW_PL(12, 40);
 #undef MW_PL
@@ -1511,7 +1617,7 @@ cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4*
     if (count <= 0) return cudaSuccess;
     // MW_NBODY_SPLIT: 1 = packed FP32x2 + scalar split across the FMA pipes (measured
     // slower on B200: 537 vs 519 ms per 2^20 step, so off by default)
-    static const int split = tuning_knob("MW_NBODY_SPLIT", 0);
+    const int split = L.tune[TUNE_NBODY_SPLIT];
     int64_t blocks = (count + kNbTile * kNbPer - 1) / (kNbTile * kNbPer);
     ++g_launches;
     if (split) {

@@ -11,9 +11,18 @@ constexpr int kMaxOps = 16;
 // Launch geometry shared by every launcher: grid-stride kernels take a grid
 // of min(work, SMs * resident CTAs); the slowdown injector divides that grid
 // by `slow` (>= 1), which changes the speed but never the result.
+// Tuning knobs (indices = MW_TUNE_* of marrow.h); every value gives
+// bit-identical results, only speed changes.
+enum TuneKnob : int {
+    TUNE_RGBA_TMA = 0, TUNE_RGBA_UNROLL = 1, TUNE_HYST_PLANES = 2, TUNE_HYST_T = 3,
+    TUNE_HYST_ROWS = 4, TUNE_NBODY_SPLIT = 5, TUNE_U8_TMA = 6, TUNE_COUNT = 7
+};
+void tune_defaults(int* out);                 // measured best on B200 (+ MW_* env overrides)
+bool tune_valid(int knob, int value);
 struct Launch {
     cudaStream_t stream;
-    float slow;     // 1 = full speed
+    float slow;        // 1 = full speed
+    const int* tune;   // TUNE_COUNT values
 };
 
 // ------------------------------------------------------------ fused Map chains

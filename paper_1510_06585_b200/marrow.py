@@ -25,6 +25,10 @@ MW_DT_U8, MW_DT_F32, MW_DT_F64, MW_DT_I64 = 1, 2, 3, 4
 MW_PARTITION, MW_COPY = 0, 1
 MW_LOC_DEVICE, MW_LOC_HOST = 0, 1
 MW_BALANCE_PROPORTIONAL, MW_BALANCE_ABS = 0, 1
+MW_PROV_BUILT, MW_PROV_DERIVED, MW_PROV_BALANCED = 0, 1, 2
+MW_KB_NONE, MW_KB_EXACT, MW_KB_SCT, MW_KB_WORKLOAD, MW_KB_DIMENSIONALITY = range(5)
+(MW_TUNE_RGBA_TMA, MW_TUNE_RGBA_UNROLL, MW_TUNE_HYST_PLANES, MW_TUNE_HYST_T, MW_TUNE_HYST_ROWS,
+ MW_TUNE_NBODY_SPLIT, MW_TUNE_U8_TMA, MW_TUNE_COUNT) = range(8)
 (MW_KC_SAXPY, MW_KC_RGBA, MW_KC_U8, MW_KC_STENCIL, MW_KC_NBODY, MW_KC_REDUCE,
  MW_KC_TRAITS, MW_KC_COUNT) = range(8)
 
@@ -125,6 +129,15 @@ _SIG = {
     "mw_graph_destroy": [_vp],
     "mw_kernel_stats": [_vp, _i32, _P(_f64), _P(_i64)],
     "mw_ctx_launch_count": [_vp, _P(_i64)],
+    "mw_ctx_set_tuning": [_vp, _i32, _i32],
+    "mw_kb_open": [ctypes.c_char_p, _P(_vp)],
+    "mw_kb_save": [_vp],
+    "mw_kb_close": [_vp],
+    "mw_kb_count": [_vp, _P(_i32)],
+    "mw_kb_store": [_vp, _vp, _P(_i64), _i32, _P(_i32), _P(_f64), _i32, _f64, _i32],
+    "mw_kb_lookup": [_vp, _vp, _P(_i64), _i32, _P(_i32), _P(_f64), _i32, _P(_i32)],
+    "mw_autotune": [_vp, _vp, _P(mw_arg), _i32, _vp, _i32, _vp, _P(_i32), _P(_f64)],
+    "mw_ctx_get_tuning": [_vp, _i32, _P(_i32)],
 }
 _RES = {"mw_status_string": ctypes.c_char_p, "mw_last_error": ctypes.c_char_p,
         "mw_abi_version": _i32, "mw_node_retain": None, "mw_node_release": None,
@@ -605,3 +618,81 @@ def mw_graph_destroy(g):
     if g.ptr:
         _call("mw_graph_destroy", g.ptr)
         g.ptr = None
+
+
+def mw_ctx_set_tuning(ctx, knob, value):
+    _call("mw_ctx_set_tuning", ctx.ptr, knob, value)
+
+
+def mw_ctx_get_tuning(ctx, knob) -> int:
+    v = _i32()
+    _call("mw_ctx_get_tuning", ctx.ptr, knob, ctypes.byref(v))
+    return v.value
+
+
+class KB:
+    """Owning handle of an mw_kb (saved and freed on close / garbage collection)."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def close(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _call("mw_kb_close", self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mw_kb_open(path=None):
+    out = _vp()
+    _call("mw_kb_open", (path or "").encode(), ctypes.byref(out))
+    return KB(out)
+
+
+def mw_kb_save(kb):
+    _call("mw_kb_save", kb.ptr)
+
+
+def mw_kb_close(kb):
+    kb.close()
+
+
+def mw_kb_count(kb) -> int:
+    n = _i32()
+    _call("mw_kb_count", kb.ptr, ctypes.byref(n))
+    return n.value
+
+
+def mw_kb_store(kb, node, dims, tune, fractions, best_ms, provenance=MW_PROV_BUILT):
+    d = (_i64 * max(1, len(dims)))(*dims)
+    tn = (_i32 * MW_TUNE_COUNT)(*tune)
+    fr = (_f64 * max(1, len(fractions)))(*fractions)
+    _call("mw_kb_store", kb.ptr, node.ptr, d, len(dims), tn, fr, len(fractions), best_ms, provenance)
+
+
+def mw_kb_lookup(kb, node, dims, nparts=0):
+    """-> (scope, tune list or None, fractions list or None)."""
+    d = (_i64 * max(1, len(dims)))(*dims)
+    tn = (_i32 * MW_TUNE_COUNT)()
+    fr = (_f64 * max(1, nparts))()
+    sc = _i32()
+    _call("mw_kb_lookup", kb.ptr, node.ptr, d, len(dims), tn, fr if nparts else None, nparts,
+          ctypes.byref(sc))
+    if sc.value == MW_KB_NONE:
+        return MW_KB_NONE, None, None
+    return sc.value, list(tn), (list(fr)[:nparts] if nparts else None)
+
+
+def mw_autotune(ctx, node, args, stream=None, reps=3, kb=None):
+    """Profile building over the tuning knobs; returns (tune list, best ms per run)."""
+    arr = (mw_arg * len(args))(*args)
+    tn = (_i32 * MW_TUNE_COUNT)()
+    ms = _f64()
+    _call("mw_autotune", ctx.ptr, node.ptr, arr, len(args), _stream_arg(stream), reps,
+          kb.ptr if kb is not None else None, tn, ctypes.byref(ms))
+    return list(tn), ms.value

@@ -525,3 +525,74 @@ def test_single_pixel_and_single_row_images():
             out = torch.empty((H, W), dtype=torch.uint8, device=DEV)
             r = run(cc, trees.hysteresis(), [M.arg(dev(gray)), M.arg(out)])
             assert np.array_equal(out.cpu().numpy(), want) and r["executions"] == D + 1
+
+
+# ----------------------------------------------------------------- tuning knobs
+def test_tuning_knobs_bit_identical():
+    """Every tuning value (the profile builder's search space) gives the same bytes."""
+    c = ctx(1)
+    img = synth.np_rgba(3, 0, 6 * 8192).reshape(6, 8192, 4)
+    want = oracle_filter(img)
+    src = dev(img)
+    for tma in range(7):
+        for unroll in (2, 4, 8):
+            M.mw_ctx_set_tuning(c, M.MW_TUNE_RGBA_TMA, tma)
+            M.mw_ctx_set_tuning(c, M.MW_TUNE_RGBA_UNROLL, unroll)
+            dst = torch.empty_like(src)
+            run(c, trees.filter_pipeline(), [M.arg(src), M.arg(dst)])
+            assert np.array_equal(dst.cpu().numpy(), want), (tma, unroll)
+            if tma:
+                break
+    gray = synth.np_u8_stream(8, 0, 300 * 257).reshape(300, 257)
+    want_h, D = oracle_hyst(gray)
+    for planes, T, R in ((0, 8, 40), (1, 4, 32), (1, 6, 32), (1, 8, 32), (1, 8, 40), (1, 12, 40)):
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_PLANES, planes)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_ROWS, R)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_T, T)
+        out = torch.empty((300, 257), dtype=torch.uint8, device=DEV)
+        r = run(c, trees.hysteresis(), [M.arg(dev(gray)), M.arg(out)])
+        assert np.array_equal(out.cpu().numpy(), want_h) and r["executions"] == D + 1, (planes, T, R)
+    pos, vel = synth.np_nbody(9, 0, 1024, 2.0 ** -10)
+    outs = []
+    for split in (0, 1):
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_NBODY_SPLIT, split)
+        acc = torch.empty((1024, 4), dtype=torch.float32, device=DEV)
+        run(c, M.mw_kernel_nbody_accel(1e-4), [M.arg(dev(pos), M.MW_COPY), M.arg(acc)])
+        outs.append(acc.cpu().numpy())
+    acc_o, cond = K.nbody_accel(pos, 1e-4)
+    for o in outs:
+        _nb_check(o[:, :3].astype(np.float64), acc_o, cond)
+    with pytest.raises(M.MwError):
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_T, 5)
+
+
+# ----------------------------------------------------------------- profile building (NEXT-2)
+def test_autotune_filter_and_nbody(tmp_path):
+    kb = M.mw_kb_open(str(tmp_path / "kb.txt"))
+    c = ctx(1)
+    img = synth.np_rgba(3, 0, 64 * 8192).reshape(64, 8192, 4)
+    src, dst = dev(img), torch.empty((64, 8192, 4), dtype=torch.uint8, device=DEV)
+    tree = trees.filter_pipeline()
+    tune, ms = M.mw_autotune(c, tree, [M.arg(src), M.arg(dst)], reps=2, kb=kb)
+    assert ms > 0 and [M.mw_ctx_get_tuning(c, k) for k in range(M.MW_TUNE_COUNT)] == tune
+    assert np.array_equal(dst.cpu().numpy(), oracle_filter(img))
+    assert M.mw_kb_lookup(kb, tree, [64, 8192, 4])[0] == M.MW_KB_EXACT
+    # in-place state is restored after tuning
+    pos, vel = synth.np_nbody(9, 0, 2048, 2.0 ** -11)
+    p, v = dev(pos), dev(vel)
+    M.mw_autotune(c, trees.nbody(1), [M.arg(p, M.MW_COPY), M.arg(v, M.MW_COPY)], reps=1, kb=kb)
+    assert np.array_equal(p.cpu().numpy(), pos) and np.array_equal(v.cpu().numpy(), vel)
+    assert M.mw_kb_count(kb) == 2
+    kb.close()
+
+
+def test_u8_tma_and_lsu_paths_identical():
+    c = ctx(2, [0.4, 0.6])
+    for shape in ((9, 64, 256), (3, 100, 100), (40, 1024, 16)):
+        vol = synth.np_u8_stream(7, 0, int(np.prod(shape))).reshape(shape)
+        want = K.segment(vol, 85, 170)
+        for v in (0, 1):
+            M.mw_ctx_set_tuning(c, M.MW_TUNE_U8_TMA, v)
+            dst = torch.empty(shape, dtype=torch.uint8, device=DEV)
+            run(c, trees.segmentation(), [M.arg(dev(vol)), M.arg(dst)])
+            assert np.array_equal(dst.cpu().numpy(), want), (shape, v)

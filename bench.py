@@ -675,6 +675,54 @@ def run_marrow(args, dist, wl_name):
     ctx.destroy()
 
 
+def run_rebalance_scenario(args, dist):
+    """§8 a9 on one GPU (the E5 analogue): N-body Loop over P
+    virtual partitions; from step 10 to 29 partition 3 computes 4x slower
+    (slowdown injector, the paper's CPU-load generator P:1110-1113); after every
+    step the monitor/rebalancer runs (mw_rebalance).  Reports when it
+    triggered, the distributions, the per-step times, and that the trajectory
+    is bitwise identical to a run that never rebalanced."""
+    import torch
+
+    import synth
+    from paper_1510_06585_b200 import marrow as M
+    from paper_1510_06585_b200 import trees
+    if dist.world != 1:
+        if dist.rank == 0:
+            print(json.dumps({"workload": "rebalance", "skipped": "runs on one GPU (virtual partitions)"}))
+        return
+    N, P, steps = 1 << 18, 8, 40
+    ctx = M.mw_ctx_create(0, 0, 1, P)
+    pos = torch.empty((N, 4), dtype=torch.float32, device="cuda")
+    vel = torch.empty((N, 4), dtype=torch.float32, device="cuda")
+    synth.dev_fill_nbody(pos, vel, synth.SEED_NBODY, 0, 2.0 ** -18)
+    ref_p, ref_v = pos.clone(), vel.clone()
+    node = trees.nbody(1)
+    trace = []
+    for k in range(steps):
+        M.mw_ctx_set_slowdown(ctx, 3, 4.0 if 10 <= k < 30 else 1.0)
+        M.mw_run(ctx, node, [M.arg(pos, M.MW_COPY), M.arg(vel, M.MW_COPY)]).wait()
+        ms, wall = M.mw_last_timings(ctx)
+        trig = M.mw_rebalance(ctx)
+        st = M.mw_get_balance_state(ctx)
+        trace.append({"step": k, "wall_ms": round(wall, 3), "part_ms": [round(x, 3) for x in ms],
+                      "lbt": round(st.lbt, 4), "triggered": trig,
+                      "dist": [round(x, 4) for x in M.mw_get_distribution(ctx)]})
+    c2 = M.mw_ctx_create(0, 0, 1, 1)
+    M.mw_run(c2, trees.nbody(steps), [M.arg(ref_p, M.MW_COPY), M.arg(ref_v, M.MW_COPY)]).wait()
+    same = bool(torch.equal(pos, ref_p) and torch.equal(vel, ref_v))
+    trig_steps = [t["step"] for t in trace if t["triggered"]]
+    line = {"workload": "nbody_rebalance_2^18_8parts", "metric": "online rebalancing (lbt trigger, "
+            "proportional re-derivation) under an injected 4x slowdown of partition 3, steps 10-29",
+            "trigger_steps": trig_steps, "bitwise_identical_to_unbalanced_run": same,
+            "wall_ms_before": trace[9]["wall_ms"], "wall_ms_slowed_unbalanced": trace[11]["wall_ms"],
+            "wall_ms_slowed_rebalanced": trace[20]["wall_ms"], "wall_ms_after": trace[39]["wall_ms"],
+            "dist_while_slowed": trace[20]["dist"], "dist_after": trace[39]["dist"], "trace": trace}
+    print(json.dumps(line), flush=True)
+    ctx.destroy()
+    c2.destroy()
+
+
 def traffic_from_profile(wl_name):
     """dram bytes (read + write) per launch of the dominant kernel, from the
     committed `ncu --set full` summary under profiles/ (null if absent)."""
@@ -692,7 +740,7 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="marrow", choices=["marrow", "reference"])
-    ap.add_argument("--workload", default="filter", choices=list(WORKLOADS) + ["all"])
+    ap.add_argument("--workload", default="filter", choices=list(WORKLOADS) + ["all", "rebalance"])
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -703,6 +751,9 @@ def main():
         if args.steps is None:
             args.steps = 10
         run_reference(args, dist)
+        return
+    if args.workload == "rebalance":
+        run_rebalance_scenario(args, dist)
         return
     names = list(WORKLOADS) if args.workload == "all" else [args.workload]
     default_steps = {"filter": 2000, "saxpy": 5000, "segmentation": 1000, "mapreduce_sum": 300,

@@ -56,14 +56,14 @@ enum {
     MW_E_UNSUPPORTED = 11,          /* valid SCT outside the built hot path (NEXT-4)  */
 };
 
-const char* mw_status_string(mw_status s);
-/* Last error message of the calling thread (ctx may be NULL). Never NULL.    */
-const char* mw_last_error(const struct mw_ctx* ctx);
-int32_t mw_abi_version(void);
-
 typedef struct mw_ctx mw_ctx;
 typedef struct mw_node mw_node;
 typedef struct mw_future mw_future;
+
+const char* mw_status_string(mw_status s);
+/* Last error message of the calling thread (ctx may be NULL). Never NULL.    */
+const char* mw_last_error(const mw_ctx* ctx);
+int32_t mw_abi_version(void);
 
 /* ------------------------------------------------------------------ context */
 /* Device memory callbacks (PyTorch's caching allocator in the Python
@@ -89,7 +89,9 @@ mw_status mw_nccl_unique_id(uint8_t out[128]);
 mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t parts_per_rank,
                         const uint8_t* nccl_id, int32_t force_nccl, const mw_alloc_fns* alloc,
                         mw_ctx** out);
-/* Collective when the ctx owns an NCCL communicator.  Frees all scratch.    */
+/* Collective when the ctx owns an NCCL communicator.  Frees all scratch; when
+ * futures or graphs of the ctx are still alive the teardown happens at the
+ * release of the last of them (the ctx is unusable from this call on).     */
 mw_status mw_ctx_destroy(mw_ctx* ctx);
 /* Number of partitions P (= nranks * parts_per_rank) and this rank's first. */
 mw_status mw_ctx_info(const mw_ctx* ctx, int32_t* n_parts, int32_t* first_part,
@@ -299,9 +301,10 @@ mw_status mw_rebalance(mw_ctx* ctx, const mw_balance_params* p, int32_t* trigger
 mw_status mw_get_balance_state(const mw_ctx* ctx, mw_balance_state* out);
 
 /* Slowdown injector (the analogue of the paper's CPU-load generator,
- * P:1110-1113): partition `part`'s compute kernels launch on 1/factor of
- * their usual grid (factor >= 1; 1 = off).  Results are unchanged (every
- * kernel is a grid-stride loop), only the partition's time grows.          */
+ * P:1110-1113): partition `part` computes as on a device `factor` (>= 1;
+ * 1 = off) times slower.  The idempotent N-body step kernel is repeated
+ * round(factor) times (time exactly proportional); the other kernels launch
+ * on 1/factor of their usual grid (grid-stride loops).  Results never change. */
 mw_status mw_ctx_set_slowdown(mw_ctx* ctx, int32_t part, float factor);
 
 /* Tuning knobs: the B200 platform configuration of a profile (P:446-456
@@ -311,7 +314,8 @@ mw_status mw_ctx_set_slowdown(mw_ctx* ctx, int32_t part, float factor);
 enum {
     MW_TUNE_RGBA_TMA = 0,     /* fused RGBA chain: 0 LSU path, 1 = 16 KiB x 3 stages TMA,
                                  2 = 8 KiB x 4, 3 = 8 KiB x 3, 4 = 4 KiB x 4, 5 = 32 KiB x 3,
-                                 6 = 16 KiB x 6                                            */
+                                 6 = 16 KiB x 6; warp-granular rings: 7 = 4 KiB x 3 x 8 warps,
+                                 8 = 8 KiB x 2 x 6 warps                                  */
     MW_TUNE_RGBA_UNROLL = 1,  /* LSU path: 16-byte vectors per thread (2, 4, 8)            */
     MW_TUNE_HYST_PLANES = 2,  /* 1: one-partition hysteresis on bit planes; 0: byte stencil */
     MW_TUNE_HYST_T = 3,       /* executions per pass of the plane loop (4, 6, 8, 12)        */

@@ -99,6 +99,8 @@ struct mw_ctx {
     cudaEvent_t st_in[kStageSlots]{}, st_comp[kStageSlots]{}, st_out[kStageSlots]{};
     cudaEvent_t st_start = nullptr;
     bool capturing = false;     // inside mw_graph_capture: no timing events, no host syncs
+    int refs = 1;               // the user's handle + outstanding futures and graphs
+    bool destroyed = false;     // mw_ctx_destroy called; teardown at the last release
     int tune[mwk::TUNE_COUNT];  // tuning knobs (mw_ctx_set_tuning)
 };
 
@@ -668,9 +670,18 @@ mw_status run_nbody(RunCtx& R, const Step& st, const mw_arg& pos, const mw_arg& 
             int p = R.first + q;
             if (R.len[p] == 0) continue;
             PartTimer t(c, R.s, p, MW_KC_NBODY);
-            MW_OK_OR_RETURN(kerr(mwk::nbody(P[cur], V[cur], P[1 - cur], V[1 - cur], nullptr, R.off[p],
-                                            R.len[p], N, st.eps2, st.dt, 0, launch_for(c, R.s, p)),
-                                 "nbody"));
+            // The step kernel is idempotent (reads state k, writes state k+1), so the
+            // slowdown injector repeats it `factor` times: time grows exactly by the
+            // factor, as on a device that is that much slower (the grid clamp used for
+            // the other kernels is not proportional once a partition no longer fills
+            // the GPU).  Results are unchanged.
+            mwk::Launch L = launch_for(c, R.s, p);
+            const int reps = L.slow > 1.0f ? (int)std::lround(L.slow) : 1;
+            L.slow = 1.0f;
+            for (int rep = 0; rep < reps; ++rep)
+                MW_OK_OR_RETURN(kerr(mwk::nbody(P[cur], V[cur], P[1 - cur], V[1 - cur], nullptr,
+                                                R.off[p], R.len[p], N, st.eps2, st.dt, 0, L),
+                                     "nbody"));
         }
         // Loop state update with global sync: re-replicate
         MW_OK_OR_RETURN(allgather_slices(R, P[1 - cur]));
@@ -1007,8 +1018,7 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
     return MW_OK;
 }
 
-mw_status mw_ctx_destroy(mw_ctx* c) {
-    if (!c) return fail(MW_E_STATE, "NULL ctx");
+static void ctx_teardown(mw_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto& kv : c->scratch) ctx_free(c, kv.second.p);
@@ -1027,7 +1037,21 @@ mw_status mw_ctx_destroy(mw_ctx* c) {
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->h_flag) cudaFreeHost(c->h_flag);
     for (double* p : c->res_pages) cudaFreeHost(p);
+    (void)cudaGetLastError();   // leave no stale error behind for the host application
     delete c;
+}
+static void ctx_retain(mw_ctx* c) { ++c->refs; }
+static void ctx_release(mw_ctx* c) {
+    if (--c->refs == 0) ctx_teardown(c);
+}
+
+// Futures and graphs hold a reference: a ctx destroyed while they are alive
+// is torn down when the last of them is released.
+mw_status mw_ctx_destroy(mw_ctx* c) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    if (c->destroyed) return fail(MW_E_STATE, "ctx already destroyed");
+    c->destroyed = true;
+    ctx_release(c);
     return MW_OK;
 }
 
@@ -1076,6 +1100,7 @@ mw_status mw_partition(const mw_ctx* c, const mw_node* root, int64_t L, int64_t*
 mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs, void* stream,
                  mw_future** out) {
     if (!c || !root || !out || (nargs > 0 && !args)) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
     CUDA_OK(cudaSetDevice(c->device));
     // Consume a stale non-sticky error left in the runtime's last-error slot by
     // an unrelated earlier call (ours or the host application's), so that the
@@ -1113,6 +1138,7 @@ mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nar
         if (f->done) cudaEventDestroy(f->done);
         return fail(MW_E_CUDA, std::string("future event: ") + cudaGetErrorString(e));
     }
+    ctx_retain(c);
     *out = f.release();
     return MW_OK;
 }
@@ -1166,7 +1192,9 @@ void mw_future_release(mw_future* f) {
         cudaEventDestroy(f->done);
     }
     if (f->res) f->ctx->res_free.push_back(f->res);
+    mw_ctx* c = f->ctx;
     delete f;
+    ctx_release(c);
 }
 
 mw_status mw_last_timings(mw_ctx* c, float* per_part_ms, int32_t n, float* wall_ms) {
@@ -1308,7 +1336,9 @@ mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* ar
     if (!c || !root || !out || (nargs > 0 && !args) || nsets < 1)
         return fail(MW_E_INVALID_SPEC, "NULL argument or nsets < 1");
     if (!stream) return fail(MW_E_INVALID_SPEC, "graph capture needs a non-default stream");
+    if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
     CUDA_OK(cudaSetDevice(c->device));
+    (void)cudaGetLastError();   // see mw_run
     std::unique_ptr<mw_graph> g(new mw_graph);
     g->ctx = c;
     g->f.ctx = c;
@@ -1345,6 +1375,7 @@ mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* ar
         return fail(MW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
     g->kernels = (int64_t)(mwk::launch_count() - l0);
+    ctx_retain(c);
     *out = g.release();
     return MW_OK;
 }
@@ -1380,7 +1411,9 @@ mw_status mw_graph_destroy(mw_graph* g) {
     if (g->exec) cudaGraphExecDestroy(g->exec);
     if (g->graph) cudaGraphDestroy(g->graph);
     if (g->f.res) cudaFreeHost(g->f.res);
+    mw_ctx* c = g->ctx;
     delete g;
+    ctx_release(c);
     return MW_OK;
 }
 
@@ -1389,7 +1422,9 @@ mw_status mw_graph_destroy(mw_graph* g) {
 mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
                       void* stream, int32_t reps, mw_kb* kb, int32_t* tune_out, double* best_ms) {
     if (!c || !root || (nargs > 0 && !args) || reps < 1) return fail(MW_E_INVALID_SPEC, "bad argument");
+    if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
     CUDA_OK(cudaSetDevice(c->device));
+    (void)cudaGetLastError();   // see mw_run
     const Node* r = reinterpret_cast<const Node*>(root);
     std::vector<Step> prog;
     MW_OK_OR_RETURN(mw::plan(r, &prog));
@@ -1404,7 +1439,7 @@ mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_
     const Tune base(c->tune, c->tune + mwk::TUNE_COUNT);
     std::vector<Tune> cands{base};
     if (has_rgba) {
-        for (int tma = 0; tma <= 6; ++tma)
+        for (int tma = 0; tma <= 8; ++tma)
             for (int un : {2, 4, 8}) {
                 if (tma > 0 && un != base[mwk::TUNE_RGBA_UNROLL]) continue;
                 Tune t = base;

@@ -438,6 +438,91 @@ __global__ void __launch_bounds__(256) k_rgba_ns_tma(const __grid_constant__ NsC
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---- warp-granular TMA variant: every warp owns an NS-stage ring of CH-byte
+// chunks and issues its own bulk loads/stores (lane 0), synchronising only
+// with __syncwarp and its own mbarriers — no CTA-wide barrier, so warps of a
+// CTA stream independently.
+template <int CH, int NS, int WARPS, bool MIRROR, bool KM, bool T128>
+__global__ void __launch_bounds__(32 * WARPS) k_rgba_ns_tmaw(const __grid_constant__ NsConst c,
+                                                             const uint8_t* __restrict__ src,
+                                                             uint8_t* __restrict__ dst,
+                                                             int64_t rows, uint32_t W,
+                                                             uint32_t row0) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr uint32_t VPC = CH / 16, PPC = CH / 4;
+    uint4* sin = reinterpret_cast<uint4*>(smem + (size_t)wid * 2 * NS * CH);
+    uint4* sout = sin + NS * VPC;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * 2 * NS * CH) + wid * NS;
+    const uint32_t rowb = W * 4u;
+    const uint32_t cpr = rowb / CH;
+    const int64_t n_items = rows * cpr;
+    const int64_t gw = (int64_t)blockIdx.x * WARPS + wid, nw = (int64_t)gridDim.x * WARPS;
+    auto src_of = [&](int64_t item) {
+        const int64_t r = item / cpr;
+        const uint32_t ch = (uint32_t)(item - r * cpr);
+        const uint32_t sc = MIRROR ? (cpr - 1u - ch) : ch;
+        return src + r * (int64_t)rowb + (int64_t)sc * CH;
+    };
+    if (lane == 0) {
+        for (int st = 0; st < NS; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < NS; ++st) {
+            const int64_t item = gw + (int64_t)st * nw;
+            if (item < n_items) {
+                mbar_expect_tx(&bar[st], CH);
+                bulk_load(sin + st * VPC, src_of(item), CH, &bar[st]);
+            }
+        }
+    }
+    __syncwarp();
+    int it = 0;
+    for (int64_t item = gw; item < n_items; item += nw, ++it) {
+        const int stage = it % NS;
+        mbar_wait(&bar[stage], (uint32_t)(it / NS) & 1u);
+        if (lane == 0) bulk_wait_read<NS - 1>();   // out[stage] of NS items ago was read
+        __syncwarp();
+        const int64_t r = item / cpr;
+        const uint32_t ch = (uint32_t)(item - r * cpr);
+        const uint32_t x0 = ch * PPC;
+        const uint32_t rowbase = (row0 + (uint32_t)r) * W;
+        const uint4* in = sin + stage * VPC;
+        uint4* out = sout + stage * VPC;
+#pragma unroll
+        for (int k = 0; k < (int)(VPC / 32); ++k) {
+            const uint32_t v = k * 32u + lane;
+            uint4 q = in[MIRROR ? (VPC - 1u - v) : v];
+            uint32_t w0 = q.x, w1 = q.y, w2 = q.z, w3 = q.w;
+            if (MIRROR) {
+                uint32_t t = w0; w0 = w3; w3 = t;
+                t = w1; w1 = w2; w2 = t;
+            }
+            const uint32_t xo = x0 + 4u * v;
+            const uint32_t i0 = rowbase + (KM ? (W - 1u - xo) : xo);
+            uint4 o;
+            o.x = noise_solarize<T128>(w0, i0, c);
+            o.y = noise_solarize<T128>(w1, KM ? i0 - 1u : i0 + 1u, c);
+            o.z = noise_solarize<T128>(w2, KM ? i0 - 2u : i0 + 2u, c);
+            o.w = noise_solarize<T128>(w3, KM ? i0 - 3u : i0 + 3u, c);
+            out[v] = o;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            bulk_store(dst + r * (int64_t)rowb + (int64_t)ch * CH, out, CH);
+            const int64_t nxt = item + (int64_t)NS * nw;
+            if (nxt < n_items) {
+                mbar_expect_tx(&bar[stage], CH);
+                bulk_load(sin + stage * VPC, src_of(nxt), CH, &bar[stage]);
+            }
+        }
+    }
+    if (lane == 0) {
+        bulk_wait_read<0>();
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
 // Any width / alignment: one pixel per element.
 __global__ void __launch_bounds__(256) k_rgba_scalar(const __grid_constant__ RgbaProg p,
                                                      const __grid_constant__ RgbaConst c,
@@ -1290,7 +1375,7 @@ void tune_defaults(int* out) {
 
 bool tune_valid(int knob, int v) {
     switch (knob) {
-        case TUNE_RGBA_TMA: return v >= 0 && v <= 6;
+        case TUNE_RGBA_TMA: return v >= 0 && v <= 8;
         case TUNE_RGBA_UNROLL: return v == 2 || v == 4 || v == 8;
         case TUNE_HYST_PLANES: return v == 0 || v == 1;
         case TUNE_HYST_T: return v == 4 || v == 6 || v == 8 || v == 12;
@@ -1366,7 +1451,43 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
         // 4 = 4 KiB x 4, 5 = 32 KiB x 3, 6 = 16 KiB x 6)
         const int tma_cfg = L.tune[TUNE_RGBA_TMA];
         const int chunk = (tma_cfg == 1 || tma_cfg == 6) ? 16384
-                          : (tma_cfg == 4 ? 4096 : (tma_cfg == 5 ? 32768 : 8192));
+                          : ((tma_cfg == 4 || tma_cfg == 7) ? 4096 : (tma_cfg == 5 ? 32768 : 8192));
+        if (tma_cfg >= 7 && (W * 4) % chunk == 0 &&
+            ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+#define MW_TMAW_LAUNCH(CH, NS, WP, MI, KMI, TI)                                               \
+    do {                                                                                       \
+        constexpr size_t smem = (size_t)WP * 2 * NS * CH + WP * NS * 8;                        \
+        static int occ = [] {                                                                  \
+            cudaFuncSetAttribute(k_rgba_ns_tmaw<CH, NS, WP, MI, KMI, TI>,                      \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+            return resident_ctas(k_rgba_ns_tmaw<CH, NS, WP, MI, KMI, TI>, 32 * WP, smem);      \
+        }();                                                                                   \
+        const int64_t items = rows * (W * 4 / CH);                                             \
+        ++g_launches;                                                                          \
+        k_rgba_ns_tmaw<CH, NS, WP, MI, KMI, TI>                                                \
+            <<<grid_for((items + WP - 1) / WP, occ, L), 32 * WP, smem, L.stream>>>(            \
+                nc, src, dst, rows, (uint32_t)W, (uint32_t)row0);                              \
+    } while (0)
+#define MW_TMAW_CFG(MI, KMI, TI)                                                               \
+    do {                                                                                       \
+        if (tma_cfg == 7) MW_TMAW_LAUNCH(4096, 3, 8, MI, KMI, TI);                             \
+        else MW_TMAW_LAUNCH(8192, 2, 6, MI, KMI, TI);                                          \
+    } while (0)
+            const int selw = (p.mirror ? 4 : 0) | (p.key_mirror[0] ? 2 : 0) | (t128 ? 1 : 0);
+            switch (selw) {
+                case 0: MW_TMAW_CFG(false, false, false); break;
+                case 1: MW_TMAW_CFG(false, false, true); break;
+                case 2: MW_TMAW_CFG(false, true, false); break;
+                case 3: MW_TMAW_CFG(false, true, true); break;
+                case 4: MW_TMAW_CFG(true, false, false); break;
+                case 5: MW_TMAW_CFG(true, false, true); break;
+                case 6: MW_TMAW_CFG(true, true, false); break;
+                default: MW_TMAW_CFG(true, true, true); break;
+            }
+#undef MW_TMAW_CFG
+#undef MW_TMAW_LAUNCH
+            return cudaGetLastError();
+        }
         if (tma_cfg > 0 && (W * 4) % chunk == 0 &&
             ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
 #define MW_TMA_LAUNCH(CH, NS, MI, KMI, TI)                                                     \

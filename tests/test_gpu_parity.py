@@ -534,7 +534,7 @@ def test_tuning_knobs_bit_identical():
     img = synth.np_rgba(3, 0, 6 * 8192).reshape(6, 8192, 4)
     want = oracle_filter(img)
     src = dev(img)
-    for tma in range(7):
+    for tma in range(9):
         for unroll in (2, 4, 8):
             M.mw_ctx_set_tuning(c, M.MW_TUNE_RGBA_TMA, tma)
             M.mw_ctx_set_tuning(c, M.MW_TUNE_RGBA_UNROLL, unroll)
@@ -596,3 +596,43 @@ def test_u8_tma_and_lsu_paths_identical():
             dst = torch.empty(shape, dtype=torch.uint8, device=DEV)
             run(c, trees.segmentation(), [M.arg(dev(vol)), M.arg(dst)])
             assert np.array_equal(dst.cpu().numpy(), want), (shape, v)
+
+
+# ----------------------------------------------------------------- C-ABI from C
+def test_c_program_through_the_abi():
+    """examples/filter_c.c drives the C-ABI with no Python; its output checksum
+    must equal the oracle's for the same input."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "filter_c")
+    H, W = 61, 96
+    i = np.arange(H * W, dtype=np.int64)
+    img = np.stack([(i * 7) % 256, (i * 13) % 256, (i * 29) % 256, np.full_like(i, 255)], -1)
+    want = oracle_filter(img.astype(np.uint8).reshape(H, W, 4))
+    fnv = 1469598103934665603
+    for b in want.tobytes():
+        fnv = ((fnv ^ b) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    for parts in (1, 3):
+        out = subprocess.run([exe, str(H), str(W), str(parts)], capture_output=True, text=True, check=True)
+        assert out.stdout.split()[1] == f"{fnv:016x}", out.stdout
+
+
+def test_ctx_destroy_while_future_and_graph_alive():
+    c = ctx()
+    x = dev(synth.np_f32_um11(1, 0, 4096))
+    y = dev(synth.np_f32_um11(2, 0, 4096))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = M.mw_graph_capture(c, trees.saxpy(1.0), [M.arg(x), M.arg(y)], s)
+    f = M.mw_run(c, trees.mapreduce(False), [M.arg(x)])
+    raw = c.ptr
+    c.destroy()                      # deferred: the future and the graph still hold the ctx
+    f.wait()
+    assert abs(f.result()["reduced"] - K.sum_(x.cpu().numpy())) <= 1e-12 * 4096
+    with torch.cuda.stream(s):
+        g.launch(s)
+    s.synchronize()
+    st = M.lib().mw_run(raw, trees.saxpy(1.0).ptr, None, 0, None, None)
+    assert st == M.MW_E_INVALID_SPEC or st == M.MW_E_STATE
+    del f, g                         # last references: the teardown runs here
+    torch.cuda.synchronize()

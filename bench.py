@@ -676,12 +676,13 @@ def run_marrow(args, dist, wl_name):
 
 
 def run_rebalance_scenario(args, dist):
-    """§8 a9 on one GPU (the E5 analogue): N-body Loop over P
-    virtual partitions; from step 10 to 29 partition 3 computes 4x slower
-    (slowdown injector, the paper's CPU-load generator P:1110-1113); after every
-    step the monitor/rebalancer runs (mw_rebalance).  Reports when it
-    triggered, the distributions, the per-step times, and that the trajectory
-    is bitwise identical to a run that never rebalanced."""
+    """§8 a9 on one GPU (the E5 analogue): the fused Filter
+    Pipeline on a 16384^2 image split into P = 8 virtual partitions; from run
+    10 to 29 partition 3 computes 4x slower (slowdown injector, the analogue of
+    the paper's CPU-load generator P:1110-1113); after every run the monitor /
+    rebalancer runs (mw_rebalance: lbt trigger + proportional re-derivation).
+    Reports when it triggered, the distributions and per-partition times, and
+    that the output is bitwise identical to the one-partition run."""
     import torch
 
     import synth
@@ -691,36 +692,43 @@ def run_rebalance_scenario(args, dist):
         if dist.rank == 0:
             print(json.dumps({"workload": "rebalance", "skipped": "runs on one GPU (virtual partitions)"}))
         return
-    N, P, steps = 1 << 18, 8, 40
+    H = W = 16384   # big enough that every partition's launch is well above launch latency
+    P, runs = 8, 40
     ctx = M.mw_ctx_create(0, 0, 1, P)
-    pos = torch.empty((N, 4), dtype=torch.float32, device="cuda")
-    vel = torch.empty((N, 4), dtype=torch.float32, device="cuda")
-    synth.dev_fill_nbody(pos, vel, synth.SEED_NBODY, 0, 2.0 ** -18)
-    ref_p, ref_v = pos.clone(), vel.clone()
-    node = trees.nbody(1)
+    src = torch.empty((H, W, 4), dtype=torch.uint8, device="cuda")
+    synth.dev_fill_rgba(src, synth.SEED_IMAGE, 0)
+    dst = torch.empty_like(src)
+    node = trees.filter_pipeline()
+    for _ in range(5):   # warm-up runs, not monitored
+        M.mw_run(ctx, node, [M.arg(src), M.arg(dst)]).wait()
     trace = []
-    for k in range(steps):
+    for k in range(runs):
         M.mw_ctx_set_slowdown(ctx, 3, 4.0 if 10 <= k < 30 else 1.0)
-        M.mw_run(ctx, node, [M.arg(pos, M.MW_COPY), M.arg(vel, M.MW_COPY)]).wait()
+        M.mw_run(ctx, node, [M.arg(src), M.arg(dst)]).wait()
         ms, wall = M.mw_last_timings(ctx)
+        rows = M.mw_last_lengths(ctx)
         trig = M.mw_rebalance(ctx)
         st = M.mw_get_balance_state(ctx)
-        trace.append({"step": k, "wall_ms": round(wall, 3), "part_ms": [round(x, 3) for x in ms],
-                      "lbt": round(st.lbt, 4), "triggered": trig,
-                      "dist": [round(x, 4) for x in M.mw_get_distribution(ctx)]})
-    c2 = M.mw_ctx_create(0, 0, 1, 1)
-    M.mw_run(c2, trees.nbody(steps), [M.arg(ref_p, M.MW_COPY), M.arg(ref_v, M.MW_COPY)]).wait()
-    same = bool(torch.equal(pos, ref_p) and torch.equal(vel, ref_v))
-    trig_steps = [t["step"] for t in trace if t["triggered"]]
-    line = {"workload": "nbody_rebalance_2^18_8parts", "metric": "online rebalancing (lbt trigger, "
-            "proportional re-derivation) under an injected 4x slowdown of partition 3, steps 10-29",
-            "trigger_steps": trig_steps, "bitwise_identical_to_unbalanced_run": same,
-            "wall_ms_before": trace[9]["wall_ms"], "wall_ms_slowed_unbalanced": trace[11]["wall_ms"],
-            "wall_ms_slowed_rebalanced": trace[20]["wall_ms"], "wall_ms_after": trace[39]["wall_ms"],
-            "dist_while_slowed": trace[20]["dist"], "dist_after": trace[39]["dist"], "trace": trace}
+        trace.append({"run": k, "wall_ms": round(wall, 4), "part_ms": [round(x, 4) for x in ms],
+                      "rows": rows, "lbt": round(st.lbt, 4), "triggered": trig,
+                      "next_dist": [round(x, 4) for x in M.mw_get_distribution(ctx)]})
+    ref = torch.empty_like(src)
+    c1 = M.mw_ctx_create(0, 0, 1, 1)
+    M.mw_run(c1, node, [M.arg(src), M.arg(ref)]).wait()
+    same = bool(torch.equal(dst, ref))
+    line = {"workload": "filter_rebalance_16384x16384_8parts",
+            "metric": "online rebalancing (lbt trigger, proportional re-derivation) under an "
+                      "injected 4x slowdown of partition 3 during runs 10-29",
+            "trigger_runs": [t["run"] for t in trace if t["triggered"]],
+            "bitwise_identical_to_one_partition_run": same,
+            "wall_ms": {"balanced": trace[9]["wall_ms"], "slowed_before_rebalance": trace[11]["wall_ms"],
+                        "slowed_after_rebalance": trace[25]["wall_ms"],
+                        "recovered": trace[39]["wall_ms"]},
+            "rows_while_slowed": trace[25]["rows"], "rows_after_recovery": trace[39]["rows"],
+            "trace": trace}
     print(json.dumps(line), flush=True)
     ctx.destroy()
-    c2.destroy()
+    c1.destroy()
 
 
 def traffic_from_profile(wl_name):

@@ -302,9 +302,10 @@ mw_status mw_get_balance_state(const mw_ctx* ctx, mw_balance_state* out);
 
 /* Slowdown injector (the analogue of the paper's CPU-load generator,
  * P:1110-1113): partition `part` computes as on a device `factor` (>= 1;
- * 1 = off) times slower.  The idempotent N-body step kernel is repeated
- * round(factor) times (time exactly proportional); the other kernels launch
- * on 1/factor of their usual grid (grid-stride loops).  Results never change. */
+ * 1 = off) times slower.  Idempotent work (the N-body step, RGBA chains
+ * src -> dst) is repeated round(factor) times (time exactly proportional);
+ * the other kernels launch on 1/factor of their usual grid (grid-stride
+ * loops).  Results never change.                                           */
 mw_status mw_ctx_set_slowdown(mw_ctx* ctx, int32_t part, float factor);
 
 /* Tuning knobs: the B200 platform configuration of a profile (P:446-456

@@ -335,6 +335,7 @@ mw_status run_rgba(RunCtx& R, int part, const std::vector<mwk::RgbaProg>& progs,
                    const uint8_t* src, uint8_t* dst, int64_t rows, int64_t W, int64_t row0,
                    uint8_t* tmp0, uint8_t* tmp1) {
     mwk::Launch L = launch_for(R.c, R.s, part);
+    L.slow = 1.0f;   // slowdown is applied by repetition (caller)
     const uint8_t* in = src;
     for (size_t g = 0; g < progs.size(); ++g) {
         uint8_t* out = (g + 1 == progs.size()) ? dst : ((g & 1) ? tmp1 : tmp0);
@@ -899,8 +900,13 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
             int p = R.first + q;
             if (R.len[p] == 0) continue;
             PartTimer t(c, s, p, MW_KC_RGBA);
-            MW_OK_OR_RETURN(run_rgba(R, p, groups, at_row<const uint8_t>(args[0], R.off[p]),
-                                     at_row<uint8_t>(args[1], R.off[p]), R.len[p], W, R.off[p], t0, t1));
+            // src -> dst chains are idempotent: the slowdown injector repeats them
+            // (time exactly proportional to the factor; results unchanged)
+            const int reps = c->slow[p] > 1.0f ? (int)std::lround(c->slow[p]) : 1;
+            for (int rep = 0; rep < reps; ++rep)
+                MW_OK_OR_RETURN(run_rgba(R, p, groups, at_row<const uint8_t>(args[0], R.off[p]),
+                                         at_row<uint8_t>(args[1], R.off[p]), R.len[p], W, R.off[p],
+                                         t0, t1));
         }
     } else if (ik == MW_VK_U8 || ik == MW_VK_U8_2D) {
         MW_OK_OR_RETURN(run_u8(R, prog, args[0], args[1], f));

@@ -150,7 +150,8 @@ class Workload:
 
     def slice(self, L):
         off, ln = self.M.mw_partition(self.ctx, self.tree, L)
-        return off[self.rank], ln[self.rank]
+        k = len(off) // int(os.environ.get("WORLD_SIZE", "1"))   # this rank's partitions: contiguous
+        return off[self.rank * k], sum(ln[self.rank * k:(self.rank + 1) * k])
 
 
 class Filter(Workload):
@@ -349,15 +350,18 @@ class Hysteresis(Workload):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
 
     def plane(self, launches, steps):
-        return launches.get(self.M.MW_KC_STENCIL, 0) <= steps
+        # bit planes unless disabled (one partition: one cooperative launch per
+        # step; several: one pass kernel per partition per T executions)
+        return self.M.mw_ctx_get_tuning(self.ctx, self.M.MW_TUNE_HYST_PLANES) != 0
 
     def bound_of(self, cls, launches, steps):
-        # the one-kernel bit-plane loop works on L2-resident planes and is bound by
-        # the integer ALU / shuffle pipes, not by HBM
+        # the bit-plane loop works on L2-resident planes and is bound by the
+        # integer ALU / shuffle pipes, not by HBM
         return "alu" if cls == self.M.MW_KC_STENCIL and self.plane(launches, steps) else "hbm"
 
     def roof_bytes(self, cls, launches, steps, res):
-        """Algorithmic work.  Bit-plane path (one stencil launch per step):
+        """Algorithmic work.  Bit-plane path (one cooperative launch per step, or
+        per-partition pass kernels):
         pack 1 B + 1/4 B and unpack 1/4 B + 1 B per pixel (U8 class, HBM);
         each Jacobi execution of the dense plane algorithm costs 5 integer ALU
         lane-operations per 32 pixels (2 funnel shifts + 3 LOP3; the 2 shuffles
@@ -551,7 +555,7 @@ def run_marrow(args, dist, wl_name):
     nccl_id = None
     if dist.world > 1:
         nccl_id = dist.bcast_bytes(M.mw_nccl_unique_id() if dist.rank == 0 else None)
-    ctx = M.mw_ctx_create(dist.local, dist.rank, dist.world, 1, nccl_id)
+    ctx = M.mw_ctx_create(dist.local, dist.rank, dist.world, args.parts, nccl_id)
     w = WORKLOADS[wl_name](M, trees, synth, torch, ctx, dev, dist.rank)
     stream = torch.cuda.Stream(device=dev)   # a real stream (graph capture needs one)
     torch.cuda.set_stream(stream)
@@ -638,7 +642,7 @@ def run_marrow(args, dist, wl_name):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (SplitMix64 seeded, generated on device per rank)",
             "config": dict(w.config(), parallelism=f"rows/slabs/bodies over {dist.world} GPU(s)",
-                           partitions=dist.world),
+                           partitions=dist.world * args.parts),
             "roofline": roof, "kernels": breakdown, "gpu_launches": launches,
             "clocks": clocks.summary()}
     if wl_name == "hysteresis":
@@ -751,6 +755,8 @@ def main():
     ap.add_argument("--workload", default="filter", choices=list(WORKLOADS) + ["all", "rebalance"])
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--parts", type=int, default=1,
+                    help="virtual partitions per GPU (uniform distribution vector)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <string>
@@ -73,7 +74,8 @@ struct mw_ctx {
     std::vector<double> dist;
     std::map<std::string, Buf> scratch;
     // pinned host memory
-    int32_t* h_flag = nullptr;
+    int32_t* h_flag = nullptr;   // 16 ints: [0] byte-stencil flag, [4..7] plane-pass ring
+    cudaEvent_t lag_ev[4]{};
     std::vector<double*> res_free;
     std::vector<double*> res_pages;
     // monitoring
@@ -350,24 +352,39 @@ struct Halo {
     uint8_t* buf[2];  // two ping-pong buffers of (len+2) x pitch, halo row at 0
 };
 
-mw_status exchange_halos(RunCtx& R, std::vector<Halo>& H, int which, int64_t pitch) {
+// Exchange `hr` boundary rows of `rb` bytes between neighbouring active
+// partitions.  bufs[q] (local partition q) holds hr halo rows, len interior
+// rows, hr halo rows; every active partition has len >= hr.
+mw_status exchange_rows(RunCtx& R, const std::vector<uint8_t*>& bufs, int64_t hr, int64_t rb) {
     mw_ctx* c = R.c;
     const int P = c->P;
     std::vector<int> act;
     for (int p = 0; p < P; ++p)
         if (R.len[p] > 0) act.push_back(p);
+    const int64_t n = hr * rb;
     bool group = false;
+    mwk::CopyBatch cb;
+    cb.n = 0;
     for (size_t i = 0; i + 1 < act.size(); ++i) {
         int a = act[i], b = act[i + 1];
         bool la = R.local(a), lb = R.local(b);
         if (!la && !lb) continue;
-        uint8_t* abuf = la ? H[a - R.first].buf[which] : nullptr;
-        uint8_t* bbuf = lb ? H[b - R.first].buf[which] : nullptr;
+        uint8_t* abuf = la ? bufs[a - R.first] : nullptr;
+        uint8_t* bbuf = lb ? bufs[b - R.first] : nullptr;
+        uint8_t* a_last = la ? abuf + R.len[a] * rb : nullptr;        // a's last hr rows
+        uint8_t* a_bhalo = la ? abuf + (R.len[a] + hr) * rb : nullptr;
+        uint8_t* b_first = lb ? bbuf + n : nullptr;                    // b's first hr rows
+        uint8_t* b_thalo = bbuf;
         if (la && lb) {
-            // b's top halo <- a's last row; a's bottom halo <- b's first row
-            CUDA_OK(cudaMemcpyAsync(bbuf, abuf + R.len[a] * pitch, pitch, cudaMemcpyDeviceToDevice, R.s));
-            CUDA_OK(cudaMemcpyAsync(abuf + (R.len[a] + 1) * pitch, bbuf + pitch, pitch,
-                                    cudaMemcpyDeviceToDevice, R.s));
+            for (int k = 0; k < 2; ++k) {
+                if (cb.n == 32) {
+                    MW_OK_OR_RETURN(kerr(mwk::copy_batch(cb, R.s), "copy_batch"));
+                    cb.n = 0;
+                }
+                cb.src[cb.n] = k ? b_first : a_last;
+                cb.dst[cb.n] = k ? a_bhalo : b_thalo;
+                cb.bytes[cb.n++] = n;
+            }
             continue;
         }
         if (!c->comm) return fail(MW_E_STATE, "cross-rank halo without an NCCL communicator");
@@ -377,15 +394,175 @@ mw_status exchange_halos(RunCtx& R, std::vector<Halo>& H, int which, int64_t pit
         }
         if (la) {
             int peer = R.owner(b);
-            NCCL_OK(ncclSend(abuf + R.len[a] * pitch, pitch, ncclUint8, peer, c->comm, R.s));
-            NCCL_OK(ncclRecv(abuf + (R.len[a] + 1) * pitch, pitch, ncclUint8, peer, c->comm, R.s));
+            NCCL_OK(ncclSend(a_last, n, ncclUint8, peer, c->comm, R.s));
+            NCCL_OK(ncclRecv(a_bhalo, n, ncclUint8, peer, c->comm, R.s));
         } else {
             int peer = R.owner(a);
-            NCCL_OK(ncclSend(bbuf + pitch, pitch, ncclUint8, peer, c->comm, R.s));
-            NCCL_OK(ncclRecv(bbuf, pitch, ncclUint8, peer, c->comm, R.s));
+            NCCL_OK(ncclSend(b_first, n, ncclUint8, peer, c->comm, R.s));
+            NCCL_OK(ncclRecv(b_thalo, n, ncclUint8, peer, c->comm, R.s));
         }
     }
     if (group) NCCL_OK(ncclGroupEnd());
+    if (cb.n) MW_OK_OR_RETURN(kerr(mwk::copy_batch(cb, R.s), "copy_batch"));
+    return MW_OK;
+}
+
+mw_status exchange_halos(RunCtx& R, std::vector<Halo>& H, int which, int64_t pitch) {
+    std::vector<uint8_t*> bufs(H.size());
+    for (size_t q = 0; q < H.size(); ++q) bufs[q] = H[q].buf[which];
+    return exchange_rows(R, bufs, 1, pitch);
+}
+
+// ------------------------------------------------------------ bit planes, several partitions
+// [u8 chain ending with the threshold] -> stencil loop -> [u8 chain] over P
+// partitions (this rank's ppr of them).  Each partition's planes carry T halo
+// rows; a pass of T executions runs per partition (one launch each), then T
+// plane rows are exchanged with the neighbours (device copies on this rank,
+// NCCL send/recv across ranks) and, for a while-loop, the last changing
+// execution is reduced (atomicMax on the device, NCCL max across ranks) and
+// read on the host: the loop stops after the first pass whose final execution
+// changed nothing, with E = last + 2 exactly as in the one-partition kernel.
+mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src,
+                           const mw_arg& dst, mw_future* f) {
+    mw_ctx* c = R.c;
+    const int ppr = c->ppr;
+    const int64_t W = row_bytes(src);
+    const int64_t wp = mwk::plane_words(W);
+    const int64_t rb = wp * 4;
+    const Step& st = prog[1];
+    const bool is_while = st.kind == StepKind::StencilWhile;
+    if (is_while && c->capturing)
+        return fail(MW_E_UNSUPPORTED,
+                    "this while-loop evaluates its condition on the host (several partitions) "
+                    "and cannot be captured in a graph");
+    int64_t min_len = INT64_MAX;
+    for (int p = 0; p < c->P; ++p)
+        if (R.len[p] > 0) min_len = std::min(min_len, R.len[p]);
+    const int T = mwk::planes_pass_depth(c->tune[mwk::TUNE_HYST_T], min_len);
+    auto pre = u8_groups(prog[0].ops);
+    if (pre.size() != 1) return fail(MW_E_UNSUPPORTED, "chain before the loop > 16 ops");
+    mwk::U8Prog post{};
+    if (prog.size() == 3) {
+        auto g = u8_groups(prog[2].ops);
+        if (g.size() != 1) return fail(MW_E_UNSUPPORTED, "chain after the loop > 16 ops");
+        post = g[0];
+    }
+    std::vector<uint8_t*> S[2], K;
+    std::vector<uint8_t*> fl(ppr, nullptr);
+    std::vector<int> top(ppr, 0), bot(ppr, 0);
+    for (int b = 0; b < 2; ++b) S[b].assign(ppr, nullptr);
+    K.assign(ppr, nullptr);
+    void* lp;
+    MW_OK_OR_RETURN(scratch(c, "planes_last", 64, R.s, &lp));
+    int* d_last = static_cast<int*>(lp);
+    CUDA_OK(cudaMemsetAsync(d_last, 0, 64, R.s));   // d_last[4..6]: unpack state (buffer 0)
+    for (int q = 0; q < ppr; ++q) {
+        const int p = R.first + q;
+        const int64_t len = R.len[p];
+        if (len == 0) continue;
+        const size_t pb = (size_t)(len + 2 * T) * rb;
+        void* v;
+        const std::string sq = std::to_string(q);
+        MW_OK_OR_RETURN(scratch(c, "mplane_s0_" + sq, pb, R.s, &v));
+        S[0][q] = static_cast<uint8_t*>(v);
+        MW_OK_OR_RETURN(scratch(c, "mplane_s1_" + sq, pb, R.s, &v));
+        S[1][q] = static_cast<uint8_t*>(v);
+        MW_OK_OR_RETURN(scratch(c, "mplane_k_" + sq, pb, R.s, &v));
+        K[q] = static_cast<uint8_t*>(v);
+        MW_OK_OR_RETURN(scratch(c, "mplane_tf_" + sq, (size_t)(2 * mwk::planes_tiles(len, W)), R.s, &v));
+        fl[q] = static_cast<uint8_t*>(v);
+        for (uint8_t* b : {S[0][q], S[1][q], K[q]}) {   // halos outside the image stay 0
+            CUDA_OK(cudaMemsetAsync(b, 0, T * rb, R.s));
+            CUDA_OK(cudaMemsetAsync(b + (len + T) * rb, 0, T * rb, R.s));
+        }
+        for (int a = 0; a < p; ++a) top[q] |= R.len[a] > 0;
+        for (int a = p + 1; a < c->P; ++a) bot[q] |= R.len[a] > 0;
+        PartTimer t(c, R.s, p, MW_KC_U8);
+        MW_OK_OR_RETURN(kerr(mwk::planes_pack(pre[0], at_row<const uint8_t>(src, R.off[p]), W, len, W,
+                                              reinterpret_cast<uint32_t*>(S[0][q]),
+                                              reinterpret_cast<uint32_t*>(K[q]), launch_for(c, R.s, p), T),
+                             "planes_pack"));
+    }
+    MW_OK_OR_RETURN(exchange_rows(R, K, T, rb));
+    MW_OK_OR_RETURN(exchange_rows(R, S[0], T, rb));
+    // The host reads the (running-max) last changing execution LAG passes
+    // behind the device, so the GPU never waits for it; passes queued after
+    // the fixed point change nothing, so they cost only their boundary tiles.
+    constexpr int LAG = 2, SLOTS = 4;
+    const int64_t max_it = st.n;
+    int cur = 0, pass = 0, slot = 0;
+    int64_t k0 = 0, E = max_it;
+    bool converged = false;
+    struct Pending {
+        int slot;
+        int64_t end;
+    };
+    std::deque<Pending> inflight;
+    if (is_while) {
+        CUDA_OK(cudaMemsetAsync(d_last, 0xFF, sizeof(int), R.s));
+        for (int i = 0; i < SLOTS; ++i)
+            if (!c->lag_ev[i]) CUDA_OK(cudaEventCreateWithFlags(&c->lag_ev[i], cudaEventDisableTiming));
+    }
+    auto settled = [&](const Pending& x) {   // after cudaEventSynchronize(lag_ev[x.slot])
+        const int64_t last = c->h_flag[4 + x.slot];
+        if (last < x.end - 1) {   // that pass ended with an execution that changed nothing
+            converged = true;
+            E = last + 2;
+        }
+        return converged;
+    };
+    while (k0 < max_it) {
+        const int steps = (int)std::min<int64_t>(T, max_it - k0);
+        for (int q = 0; q < ppr; ++q) {
+            const int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            const int64_t nt = mwk::planes_tiles(R.len[p], W);
+            PartTimer t(c, R.s, p, MW_KC_STENCIL);
+            MW_OK_OR_RETURN(kerr(mwk::planes_pass(reinterpret_cast<const uint32_t*>(S[cur][q]),
+                                                  reinterpret_cast<uint32_t*>(S[1 - cur][q]),
+                                                  reinterpret_cast<const uint32_t*>(K[q]), R.len[p], W, T,
+                                                  steps, k0, fl[q] + ((pass + 1) & 1) * nt,
+                                                  fl[q] + (pass & 1) * nt, pass == 0, top[q], bot[q],
+                                                  d_last, launch_for(c, R.s, p)),
+                                 "planes_pass"));
+        }
+        cur = 1 - cur;
+        ++pass;
+        MW_OK_OR_RETURN(exchange_rows(R, S[cur], T, rb));
+        k0 += steps;
+        if (!is_while) continue;
+        if (c->comm) NCCL_OK(ncclAllReduce(d_last, d_last, 1, ncclInt32, ncclMax, c->comm, R.s));
+        CUDA_OK(cudaMemcpyAsync(c->h_flag + 4 + slot, d_last, sizeof(int32_t), cudaMemcpyDeviceToHost, R.s));
+        CUDA_OK(cudaEventRecord(c->lag_ev[slot], R.s));
+        inflight.push_back({slot, k0});
+        slot = (slot + 1) % SLOTS;
+        if ((int)inflight.size() > LAG) {
+            const Pending x = inflight.front();
+            inflight.pop_front();
+            CUDA_OK(cudaEventSynchronize(c->lag_ev[x.slot]));
+            if (settled(x)) break;
+        }
+    }
+    while (is_while && !converged && !inflight.empty()) {
+        const Pending x = inflight.front();
+        inflight.pop_front();
+        CUDA_OK(cudaEventSynchronize(c->lag_ev[x.slot]));
+        settled(x);
+    }
+    if (is_while) {
+        f->executions += (double)E;
+        if (!converged) f->converged = 0.0;
+    }
+    for (int q = 0; q < ppr; ++q) {
+        const int p = R.first + q;
+        if (R.len[p] == 0) continue;
+        const uint32_t* fin = reinterpret_cast<const uint32_t*>(S[cur][q]);
+        PartTimer t(c, R.s, p, MW_KC_U8);
+        MW_OK_OR_RETURN(kerr(mwk::planes_unpack(post, fin, fin, reinterpret_cast<const uint32_t*>(K[q]),
+                                                d_last + 4, at_row<uint8_t>(dst, R.off[p]), W, R.len[p],
+                                                W, launch_for(c, R.s, p), T),
+                             "planes_unpack"));
+    }
     return MW_OK;
 }
 
@@ -411,11 +588,15 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
             }
         const bool planes_on = c->tune[mwk::TUNE_HYST_PLANES] != 0;
         const int p0 = R.first;
-        const bool eligible = planes_on && nst == 1 && sidx == 1 && c->nranks == 1 && ppr == 1 &&
-                              prog[0].kind == StepKind::U8 && !prog[0].ops.empty() &&
-                              prog[0].ops.back().kind == mw::LeafKind::Segment &&
-                              (int)prog.size() <= 3 && R.len[p0] > 0 &&
-                              (prog.size() == 2 || prog[2].kind == StepKind::U8);
+        const bool pattern = planes_on && nst == 1 && sidx == 1 &&
+                             prog[0].kind == StepKind::U8 && !prog[0].ops.empty() &&
+                             prog[0].ops.back().kind == mw::LeafKind::Segment &&
+                             (int)prog.size() <= 3 &&
+                             (prog.size() == 2 || prog[2].kind == StepKind::U8);
+        const bool eligible = pattern && c->nranks == 1 && ppr == 1 && R.len[p0] > 0;
+        const bool any = std::any_of(R.len.begin(), R.len.end(), [](int64_t l) { return l > 0; });
+        if (pattern && any && (c->nranks > 1 || ppr > 1))
+            return run_planes_multi(R, prog, src, dst, f);
         if (eligible) {
             const int64_t rows = R.len[p0];
             const int64_t wp = mwk::plane_words(W);
@@ -1042,6 +1223,8 @@ static void ctx_teardown(mw_ctx* c) {
     if (c->copy_out) cudaStreamDestroy(c->copy_out);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->h_flag) cudaFreeHost(c->h_flag);
+    for (cudaEvent_t e : c->lag_ev)
+        if (e) cudaEventDestroy(e);
     for (double* p : c->res_pages) cudaFreeHost(p);
     (void)cudaGetLastError();   // leave no stale error behind for the host application
     delete c;

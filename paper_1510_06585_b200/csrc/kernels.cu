@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
                                                      const uint8_t* __restrict__ src, int64_t sp,
                                                      int64_t rows, int64_t W, int64_t wp,
                                                      uint32_t* __restrict__ S,
-                                                     uint32_t* __restrict__ K, FastDiv WP) {
+                                                     uint32_t* __restrict__ K, FastDiv WP, int hd) {
     const uint32_t total = (uint32_t)(rows * wp);
     for (uint32_t n = blockIdx.x * 256u + threadIdx.x; n < total; n += gridDim.x * 256u) {
         const uint32_t y = fdiv(n, WP), w = n - y * WP.d;
@@ -913,8 +913,8 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
             sb &= keep;
             kb &= keep;
         }
-        S[(y + 1) * wp + w] = sb;
-        K[(y + 1) * wp + w] = kb;
+        S[(y + hd) * wp + w] = sb;
+        K[(y + hd) * wp + w] = kb;
     }
 }
 
@@ -927,12 +927,12 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
                                                        const int* __restrict__ state,
                                                        uint8_t* __restrict__ dst, int64_t dp,
                                                        int64_t rows, int64_t W, int64_t wp,
-                                                       FastDiv WP) {
+                                                       FastDiv WP, int hd) {
     const uint32_t* S = state[2] ? S1 : S0;
     const uint32_t total = (uint32_t)(rows * wp);
     for (uint32_t n = blockIdx.x * 256u + threadIdx.x; n < total; n += gridDim.x * 256u) {
         const uint32_t y = fdiv(n, WP), w = n - y * WP.d;
-        const uint32_t sb = S[(y + 1) * wp + w];
+        const uint32_t sb = S[(y + hd) * wp + w];
         uint32_t v[8];
         if (FIN_ONLY) {
             // the chain is exactly finalize (128 -> 0): strong pixels 255, all else 0;
@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
                 asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(v[i]) : "r"(m));
             }
         } else {
-            const uint32_t kb = K[(y + 1) * wp + w];
+            const uint32_t kb = K[(y + hd) * wp + w];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const uint32_t bs = expand_nib((sb >> (4 * i)) & 15u);
@@ -975,9 +975,83 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // change in the previous pass are skipped.  One cooperative kernel runs all
 // passes; flags[pass % 3] = last changed execution of the pass (-1: none).
 
+// One warp tile: T Jacobi executions (steps <= T) on register rows
+// [strip*R - T, strip*R + R + T) x lanes, owned rows/lanes written to `out`.
+// Buffers hold rows [-hd, rows + hd) at buffer row y + hd (halo rows: zero at
+// the image boundary, the neighbour partition's rows otherwise); rows outside
+// are zero.  Returns the last execution (0-based) that changed an owned bit.
 // (Measured on B200: keeping the weak plane in registers with 256-thread CTAs
 // and a rolled execution loop beats smem-resident K and a fully unrolled
 // shrinking-window loop, whose code no longer fits the instruction cache.)
+template <int T, int ROWS>
+__device__ __forceinline__ int plane_tile(const uint32_t* __restrict__ in,
+                                          uint32_t* __restrict__ out,
+                                          const uint32_t* __restrict__ K, int64_t rows,
+                                          int64_t wp, int hd, int64_t strip, int64_t cb,
+                                          int steps, int lane) {
+    constexpr int R = ROWS - 2 * T;
+    constexpr int OW = 30;
+    const bool own_lane = lane >= 1 && lane <= OW;
+    const int64_t w = cb * OW - 1 + lane;          // lane 0 / 31: halo words
+    const bool wv = w >= 0 && w < wp;
+    const int64_t ybase = strip * R - T;            // row of register row 0
+    uint32_t sv[ROWS], kv[ROWS];
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+        const int64_t y = ybase + i;
+        const bool ok = wv && y >= -hd && y < rows + hd;
+        sv[i] = ok ? in[(y + hd) * wp + w] : 0u;
+        kv[i] = ok ? K[(y + hd) * wp + w] : 0u;
+    }
+    int tile_last = -1;
+    for (int st = 0; st < steps; ++st) {
+        // lanes 0/31 take their own word as the outer neighbour: the error
+        // enters at their far bits and moves one bit per execution, never
+        // reaching the owned lanes (T <= 16)
+        auto hrow = [&](uint32_t sx) {
+            const uint32_t l = __shfl_up_sync(0xffffffffu, sx, 1);
+            const uint32_t r = __shfl_down_sync(0xffffffffu, sx, 1);
+            return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
+        };
+        uint32_t hp = hrow(sv[0]), hc = hrow(sv[1]);
+        uint32_t ch = 0;
+#pragma unroll
+        for (int i = 1; i < ROWS - 1; ++i) {
+            const uint32_t hn = hrow(sv[i + 1]);     // old row i+1 (not yet updated)
+            const uint32_t s2 = sv[i] | (kv[i] & (hp | hc | hn));
+            if (i >= T && i < T + R) ch |= s2 ^ sv[i];
+            sv[i] = s2;
+            hp = hc;
+            hc = hn;
+        }
+        if (__any_sync(0xffffffffu, own_lane && ch != 0)) tile_last = st;
+    }
+#pragma unroll
+    for (int i = T; i < T + R; ++i) {
+        const int64_t y = ybase + i;
+        if (own_lane && wv && y < rows) out[(y + hd) * wp + w] = sv[i];
+    }
+    return tile_last;
+}
+
+// is tile t active: some tile of its 3x3 neighbourhood changed last pass, or
+// it touches a partition boundary whose halo may have changed
+__device__ __forceinline__ bool plane_tile_active(const uint8_t* fprev, int64_t strip, int64_t cb,
+                                                  int64_t n_strips, int64_t n_cb, bool first,
+                                                  int top_nbr, int bot_nbr, int lane) {
+    bool act = first || (top_nbr && strip == 0) || (bot_nbr && strip == n_strips - 1);
+    if (!act) {
+        bool a = false;
+        if (lane < 9) {
+            const int64_t s2 = strip + lane / 3 - 1, c2 = cb + lane % 3 - 1;
+            a = s2 >= 0 && s2 < n_strips && c2 >= 0 && c2 < n_cb && fprev[s2 * n_cb + c2];
+        }
+        act = __any_sync(0xffffffffu, a);
+    }
+    return act;
+}
+
+// Whole loop, one partition per device: one cooperative kernel, all passes.
 template <int T, int ROWS>
 __global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
                                                      uint32_t* __restrict__ S1,
@@ -986,17 +1060,15 @@ __global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
                                                      int* __restrict__ flags,
                                                      int* __restrict__ state,
                                                      uint8_t* __restrict__ tflags) {
-    constexpr int R = ROWS - 2 * T;      // owned rows per tile
-    constexpr int OW = 30;               // owned words per tile
+    constexpr int R = ROWS - 2 * T;
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int64_t nwarps = (int64_t)gridDim.x * 8;
     const int64_t n_strips = (rows + R - 1) / R;
-    const int64_t n_cb = (wp + OW - 1) / OW;
+    const int64_t n_cb = (wp + 29) / 30;
     const int64_t n_tiles = n_strips * n_cb;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    const bool own_lane = lane >= 1 && lane <= OW;
     int64_t k0 = 0;
     int pass = 0;
     while (k0 < max_iters) {
@@ -1009,59 +1081,13 @@ __global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
         int my_last = -1;
         for (int64_t t = gw; t < n_tiles; t += nwarps) {
             const int64_t strip = t / n_cb, cb = t - strip * n_cb;
-            bool act = pass == 0;
-            if (!act) {
-                bool a = false;
-                if (lane < 9) {
-                    const int64_t s2 = strip + lane / 3 - 1, c2 = cb + lane % 3 - 1;
-                    a = s2 >= 0 && s2 < n_strips && c2 >= 0 && c2 < n_cb && fprev[s2 * n_cb + c2];
-                }
-                act = __any_sync(0xffffffffu, a);
-            }
-            if (!act) {
+            if (!plane_tile_active(fprev, strip, cb, n_strips, n_cb, pass == 0, 0, 0, lane)) {
                 if (lane == 0) fcur[t] = 0;
                 continue;
             }
-            const int64_t w = cb * OW - 1 + lane;          // lane 0 / 31: halo words
-            const bool wv = w >= 0 && w < wp;
-            const int64_t ybase = strip * R - T;            // image row of register row 0
-            uint32_t sv[ROWS], kv[ROWS];
-#pragma unroll
-            for (int i = 0; i < ROWS; ++i) {
-                const int64_t y = ybase + i;
-                sv[i] = (wv && y >= -1 && y <= rows) ? in[(y + 1) * wp + w] : 0u;
-                kv[i] = (wv && y >= 0 && y < rows) ? K[(y + 1) * wp + w] : 0u;
-            }
-            int tile_last = -1;
-            for (int st = 0; st < steps; ++st) {
-                // lanes 0/31 take their own word as the outer neighbour: the error
-                // enters at their far bits and moves one bit per execution, never
-                // reaching the owned lanes (T <= 16)
-                auto hrow = [&](uint32_t sx) {
-                    const uint32_t l = __shfl_up_sync(0xffffffffu, sx, 1);
-                    const uint32_t r = __shfl_down_sync(0xffffffffu, sx, 1);
-                    return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
-                };
-                uint32_t hp = hrow(sv[0]), hc = hrow(sv[1]);
-                uint32_t ch = 0;
-#pragma unroll
-                for (int i = 1; i < ROWS - 1; ++i) {
-                    const uint32_t hn = hrow(sv[i + 1]);     // old row i+1 (not yet updated)
-                    const uint32_t s2 = sv[i] | (kv[i] & (hp | hc | hn));
-                    if (i >= T && i < T + R) ch |= s2 ^ sv[i];
-                    sv[i] = s2;
-                    hp = hc;
-                    hc = hn;
-                }
-                if (__any_sync(0xffffffffu, own_lane && ch != 0)) tile_last = st;
-            }
-#pragma unroll
-            for (int i = T; i < T + R; ++i) {
-                const int64_t y = ybase + i;
-                if (own_lane && wv && y < rows) out[(y + 1) * wp + w] = sv[i];
-            }
-            if (lane == 0) fcur[t] = (uint8_t)(tile_last >= 0);
-            my_last = max(my_last, tile_last);
+            const int tl = plane_tile<T, ROWS>(in, out, K, rows, wp, 1, strip, cb, steps, lane);
+            if (lane == 0) fcur[t] = (uint8_t)(tl >= 0);
+            my_last = max(my_last, tl);
         }
         if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
         grid.sync();
@@ -1083,6 +1109,38 @@ __global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
         state[1] = 0;
         state[2] = pass == 0 ? 0 : (((pass - 1) & 1) ? 0 : 1);
     }
+}
+
+// One pass over one partition of several (halo depth T, host loop between
+// passes exchanges T plane rows with the neighbours and reduces `last`).
+template <int T, int ROWS>
+__global__ void __launch_bounds__(256) k_planes_pass(const uint32_t* __restrict__ in,
+                                                     uint32_t* __restrict__ out,
+                                                     const uint32_t* __restrict__ K, int64_t rows,
+                                                     int64_t wp, int steps, int64_t k0,
+                                                     const uint8_t* __restrict__ fprev,
+                                                     uint8_t* __restrict__ fcur, int first,
+                                                     int top_nbr, int bot_nbr,
+                                                     int* __restrict__ last) {
+    constexpr int R = ROWS - 2 * T;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    const int64_t n_strips = (rows + R - 1) / R;
+    const int64_t n_cb = (wp + 29) / 30;
+    const int64_t n_tiles = n_strips * n_cb;
+    int my_last = -1;
+    for (int64_t t = gw; t < n_tiles; t += nwarps) {
+        const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+        if (!plane_tile_active(fprev, strip, cb, n_strips, n_cb, first != 0, top_nbr, bot_nbr, lane)) {
+            if (lane == 0) fcur[t] = 0;
+            continue;
+        }
+        const int tl = plane_tile<T, ROWS>(in, out, K, rows, wp, T, strip, cb, steps, lane);
+        if (lane == 0) fcur[t] = (uint8_t)(tl >= 0);
+        my_last = max(my_last, tl);
+    }
+    if (lane == 0 && my_last >= 0) atomicMax(last, (int)(k0 + my_last));
 }
 
 // ------------------------------------------------------------ N-body
@@ -1653,10 +1711,36 @@ static U8Const u8_consts(const U8Prog& p) {
     return c;
 }
 
+// Batched device copies (halo rows between partitions on one device): one
+// launch instead of one cudaMemcpyAsync per boundary; blockIdx.y = entry.
+__global__ void __launch_bounds__(256) k_copy_batch(const __grid_constant__ CopyBatch b) {
+    const int e = blockIdx.y;
+    const int64_t n = b.bytes[e];
+    if (((uintptr_t)b.src[e] | (uintptr_t)b.dst[e] | (uintptr_t)n) % 16 == 0) {
+        const int4* s = reinterpret_cast<const int4*>(b.src[e]);
+        int4* d = reinterpret_cast<int4*>(b.dst[e]);
+        for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n / 16; i += (int64_t)gridDim.x * 256)
+            d[i] = s[i];
+    } else {
+        for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+            b.dst[e][i] = b.src[e][i];
+    }
+}
+
+cudaError_t copy_batch(const CopyBatch& b, cudaStream_t s) {
+    if (b.n <= 0) return cudaSuccess;
+    int64_t mx = 0;
+    for (int i = 0; i < b.n; ++i) mx = std::max(mx, b.bytes[i]);
+    const int gx = (int)std::min<int64_t>(64, std::max<int64_t>(1, (mx / 16 + 255) / 256));
+    ++g_launches;
+    k_copy_batch<<<dim3(gx, b.n), 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
 int64_t plane_words(int64_t W) { return (W + 31) / 32; }
 
 cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
-                        uint32_t* S, uint32_t* K, const Launch& L) {
+                        uint32_t* S, uint32_t* K, const Launch& L, int hd) {
     const int64_t wp = plane_words(W);
     if (rows * wp >= (1ll << 31)) return cudaErrorInvalidValue;
     if (rows <= 0) return cudaSuccess;
@@ -1666,18 +1750,18 @@ cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t
     if (p.n == 1 && p.kind[0] == U8_SEGMENT) {
         static int occ = resident_ctas(k_planes_pack<true>, 256);
         k_planes_pack<true><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp));
+            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp), hd);
     } else {
         static int occ = resident_ctas(k_planes_pack<false>, 256);
         k_planes_pack<false><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp));
+            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp), hd);
     }
     return cudaGetLastError();
 }
 
 cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S1,
                           const uint32_t* K, const int* state, uint8_t* dst, int64_t dp,
-                          int64_t rows, int64_t W, const Launch& L) {
+                          int64_t rows, int64_t W, const Launch& L, int hd) {
     const int64_t wp = plane_words(W);
     if (rows <= 0) return cudaSuccess;
     const int64_t tiles = (rows * wp + 255) / 256;
@@ -1686,11 +1770,11 @@ cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S
     if (p.n == 1 && p.kind[0] == U8_FINALIZE) {
         static int occ = resident_ctas(k_planes_unpack<true>, 256);
         k_planes_unpack<true><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp));
+            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp), hd);
     } else {
         static int occ = resident_ctas(k_planes_unpack<false>, 256);
         k_planes_unpack<false><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp));
+            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp), hd);
     }
     return cudaGetLastError();
 }
@@ -1713,6 +1797,42 @@ static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, 
     ++g_launches;
     return cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid), dim3(256),
                                        args, 0, L.stream);
+}
+
+template <int T, int ROWS>
+static cudaError_t planes_pass_t(const uint32_t* in, uint32_t* out, const uint32_t* K, int64_t rows,
+                                 int64_t wp, int steps, int64_t k0, const uint8_t* fprev,
+                                 uint8_t* fcur, int first, int top, int bot, int* last,
+                                 const Launch& L) {
+    static int occ = resident_ctas(k_planes_pass<T, ROWS>, 256);
+    constexpr int R = ROWS - 2 * T;
+    const int64_t tiles = ((rows + R - 1) / R) * ((wp + 29) / 30);
+    ++g_launches;
+    k_planes_pass<T, ROWS><<<grid_for((tiles + 7) / 8, occ, L), 256, 0, L.stream>>>(
+        in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last);
+    return cudaGetLastError();
+}
+
+int planes_pass_depth(int T_pref, int64_t min_rows) {
+    const int ts[] = {12, 8, 6, 4, 2, 1};
+    for (int t : ts)
+        if (t <= T_pref && t <= min_rows) return t;
+    return 1;
+}
+
+cudaError_t planes_pass(const uint32_t* in, uint32_t* out, const uint32_t* K, int64_t rows,
+                        int64_t W, int T, int steps, int64_t k0, const uint8_t* fprev,
+                        uint8_t* fcur, int first, int top, int bot, int* last, const Launch& L) {
+    const int64_t wp = plane_words(W);
+    if (rows <= 0) return cudaSuccess;
+    switch (T) {
+        case 12: return planes_pass_t<12, 40>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
+        case 8: return planes_pass_t<8, 40>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
+        case 6: return planes_pass_t<6, 32>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
+        case 4: return planes_pass_t<4, 32>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
+        case 2: return planes_pass_t<2, 32>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
+        default: return planes_pass_t<1, 32>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
+    }
 }
 
 cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,

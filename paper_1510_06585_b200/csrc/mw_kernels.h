@@ -81,8 +81,9 @@ cudaError_t hyst_step(const uint8_t* in, uint8_t* out, int64_t rows, int64_t pit
 // state[0..2] = {executions E, converged, index of the final S buffer};
 // unpack applies the chain after the loop and writes bytes.
 int64_t plane_words(int64_t W);
+// hd: halo rows above and below the interior in the plane buffers
 cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
-                        uint32_t* S, uint32_t* K, const Launch& L);
+                        uint32_t* S, uint32_t* K, const Launch& L, int hd = 1);
 // tflags: 2 * planes_tiles(rows, W) bytes of per-tile change flags (scratch).
 int64_t planes_tiles(int64_t rows, int64_t W);
 cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,
@@ -90,7 +91,21 @@ cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t r
                         const Launch& L);
 cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S1,
                           const uint32_t* K, const int* state, uint8_t* dst, int64_t dp,
-                          int64_t rows, int64_t W, const Launch& L);
+                          int64_t rows, int64_t W, const Launch& L, int hd = 1);
+// Up to 32 independent device copies in one launch.
+struct CopyBatch {
+    int n;
+    const uint8_t* src[32];
+    uint8_t* dst[32];
+    int64_t bytes[32];
+};
+cudaError_t copy_batch(const CopyBatch& b, cudaStream_t s);
+// Several partitions (or ranks): one pass of `steps` (<= T) executions over one
+// partition whose buffers carry T halo rows; atomicMax(last, k0 + last changed).
+int planes_pass_depth(int T_pref, int64_t min_rows);   // largest built T <= both
+cudaError_t planes_pass(const uint32_t* in, uint32_t* out, const uint32_t* K, int64_t rows,
+                        int64_t W, int T, int steps, int64_t k0, const uint8_t* fprev,
+                        uint8_t* fcur, int first, int top, int bot, int* last, const Launch& L);
 
 // ------------------------------------------------------------ N-body
 // Bodies [first, first+count) of N: direct-sum acceleration (fp32 per

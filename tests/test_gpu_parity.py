@@ -204,23 +204,32 @@ def oracle_hyst(gray, lo=173, hi=250):
     return K.hyst_finalize(fixed), D
 
 
+def pctx(ppr, dist, planes):
+    c = ctx(ppr, dist)
+    M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_PLANES, planes)
+    return c
+
+
 @pytest.mark.parametrize("H,W", [(64, 64), (100, 37), (257, 300), (1, 1), (3, 1000)])
 @pytest.mark.parametrize("ce", [1, 4, 16])
-def test_hysteresis_bitwise_and_E(H, W, ce):
+@pytest.mark.parametrize("planes", [0, 1])
+def test_hysteresis_bitwise_and_E(H, W, ce, planes):
     rng = np.random.default_rng(H * W + ce)
     gray = synth.np_u8_stream(8, 0, H * W).reshape(H, W)
     want, D = oracle_hyst(gray)
-    # byte stencil with halo exchange (3 partitions) and the one-partition
-    # bit-plane path (cooperative device-side loop)
+    # planes=0: byte stencil with one-row halo exchange; planes=1: bit planes,
+    # one partition -> cooperative device-side loop, several -> per-pass
+    # kernels with T-row plane halos
     for k, d in [(3, x) for x in dists(3, rng, 2) + [[0.0, 1.0, 0.0]]] + [(1, [1.0])]:
-        c = ctx(k, d)
+        c = pctx(k, d, planes)
         dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
         r = run(c, trees.hysteresis(check_every=ce), [M.arg(dev(gray)), M.arg(dst)])
         assert np.array_equal(dst.cpu().numpy(), want), d
         assert r["executions"] == D + 1 and r["converged"]
 
 
-def test_hysteresis_long_chains_partitions():
+@pytest.mark.parametrize("planes", [0, 1])
+def test_hysteresis_long_chains_partitions(planes):
     # a long weak snake crossing every partition boundary (1-row partitions)
     H, W = 12, 40
     L = np.zeros((H, W), np.uint8)
@@ -232,24 +241,25 @@ def test_hysteresis_long_chains_partitions():
     L[0, 0] = 255
     gray = np.where(L == 255, 255, np.where(L == 128, 200, 0)).astype(np.uint8)
     want, D = oracle_hyst(gray)
-    for d in ([1 / 12] * 12, [0.5] + [0.5 / 11] * 11):
-        c = ctx(12, d)
+    for d in ([1 / 12] * 12, [0.5] + [0.5 / 11] * 11, [0.25, 0.0, 0.5, 0.25] + [0.0] * 8):
+        c = pctx(12, d, planes)
         dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
         r = run(c, trees.hysteresis(check_every=3), [M.arg(dev(gray)), M.arg(dst)])
         assert np.array_equal(dst.cpu().numpy(), want) and r["executions"] == D + 1
 
 
-def test_hysteresis_loop_for_and_max_iters():
+@pytest.mark.parametrize("planes", [0, 1])
+def test_hysteresis_loop_for_and_max_iters(planes):
     rng = np.random.default_rng(0)
     gray = rng.integers(0, 256, size=(50, 70), dtype=np.uint8)
     L = K.segment(gray, 173, 250)
     _, D = K.hyst_bfs(L)
-    c = ctx(2)
+    c = pctx(2, None, planes)
     for n in (0, 1, 2, 5):
         dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
         run(c, M.mw_loop_for(M.mw_kernel_hysteresis_step(), n), [M.arg(dev(L)), M.arg(dst)])
         assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, n)[0])
-    for cc in (c, ctx(1)):   # byte path (2 partitions) and bit-plane path (1 partition)
+    for cc in (c, pctx(1, None, planes)):   # 2 partitions and 1 partition
         if D >= 2:
             dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
             r = run(cc, trees.hysteresis(max_iters=2), [M.arg(dev(gray)), M.arg(dst)])
@@ -268,6 +278,30 @@ def test_hysteresis_loop_for_and_max_iters():
         dst = torch.empty((50, 70), dtype=torch.uint8, device=DEV)
         r = run(cc, tree, [M.arg(dev(gray)), M.arg(dst)])
         assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L)[0]) and r["executions"] == D + 1
+
+
+@pytest.mark.parametrize("T", [4, 6, 8, 12])
+def test_hysteresis_planes_partitions_depths(T):
+    """Several partitions on the bit-plane path: T-row halos, T clamped to the
+    smallest active partition, boundary tiles always active."""
+    rng = np.random.default_rng(T)
+    H, W = 700, 1100
+    gray = synth.np_u8_stream(8, 7, H * W).reshape(H, W)
+    want, D = oracle_hyst(gray)
+    for k, d in [(4, x) for x in dists(4, rng, 2)] + [(5, [0.2, 0.003, 0.0, 0.397, 0.4])]:
+        c = pctx(k, d, 1)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_ROWS, 40 if T in (8, 12) else 32)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_T, T)
+        for ce in (1, 5):
+            dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+            r = run(c, trees.hysteresis(check_every=ce), [M.arg(dev(gray)), M.arg(dst)])
+            assert np.array_equal(dst.cpu().numpy(), want), (d, ce)
+            assert r["executions"] == D + 1 and r["converged"]
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(c, trees.hysteresis(max_iters=D - 3), [M.arg(dev(gray)), M.arg(dst)])
+        L = K.segment(gray, 173, 250)
+        assert np.array_equal(dst.cpu().numpy(), K.hyst_finalize(K.hyst_bfs(L, D - 3)[0]))
+        assert r["executions"] == D - 3 and not r["converged"]
 
 
 # ----------------------------------------------------------------- N-body
@@ -447,9 +481,11 @@ def test_nccl_communicator_paths():
     assert r == r0 and abs(r - K.dot(x, y)) <= 1e-12 * K.abs_sum(x, y)
     gray = synth.np_u8_stream(8, 0, 90 * 70).reshape(90, 70)
     want, D = oracle_hyst(gray)
-    dst = torch.empty((90, 70), dtype=torch.uint8, device=DEV)
-    res = run(c, trees.hysteresis(check_every=2), [M.arg(dev(gray)), M.arg(dst)])
-    assert np.array_equal(dst.cpu().numpy(), want) and res["executions"] == D + 1
+    for planes in (1, 0):   # T-row plane halos / one-row byte halos
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_PLANES, planes)
+        dst = torch.empty((90, 70), dtype=torch.uint8, device=DEV)
+        res = run(c, trees.hysteresis(check_every=2), [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want) and res["executions"] == D + 1
     ms, wall = M.mw_last_timings(c)
     assert len(ms) == 3 and all(t > 0 for t in ms) and wall > 0
     c.destroy()

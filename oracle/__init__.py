@@ -12,6 +12,7 @@ Modules:
   partition — granule / largest-remainder partitioner (integer)
   balance   — lbt monitor, proportional re-derivation, Adaptive Binary Search
   brute     — pure-Python brute force of the kernels for tiny inputs
+  fft       — FFT / inverse FFT pipeline (NEXT-3) in fp64 with its tolerance
 
 "parity unpinned": fidelity of the noise / solarize / segmentation / N-body
 *definitions* to the paper's own (unpublished) OpenCL kernels.  Everything

@@ -637,3 +637,71 @@ def test_abs_converges_two_classes():
         d, _ = B.step(p, s, t, [1 if d[0] > 0 else 0, 1 if d[1] > 0 else 0], d)
     t = [d[0] / rate[0], d[1] / rate[1]]
     assert B.deviation(t, [1, 1]) >= 0.85
+
+
+# ----------------------------------------------------------------- FFT (NEXT-3)
+from oracle import fft as FF  # noqa: E402
+
+
+@pytest.mark.parametrize("N", [1, 2, 8, 64, 512, 4096])
+def test_fft_chain_vs_brute_force_dft(N):
+    """The oracle's library step agrees with the direct definition (sign of
+    the exponent, 1/N on the inverse only, natural output order)."""
+    x = synth.np_f32_um11(11, 0, 2 * N).reshape(N, 2)
+    xc = FF.as_complex(x)
+    assert xc[0] == complex(float(x[0, 0]), float(x[0, 1]))
+    for d, inv in (("F", False), ("I", True)):
+        got = FF.fft_chain(xc, d)
+        want = FF.dft_brute(xc, inv)
+        assert FF.rel_l2(got, want) < 1e-12 * max(1.0, math.log2(N))
+
+
+def test_fft_closed_forms_at_65536():
+    N = 1 << 16
+    n = np.arange(N)
+    # delta at n0 -> X[k] = exp(-2 pi i n0 k / N)  (exponent reduced mod N exactly)
+    for n0 in (0, 1, 12345):
+        d = np.zeros(N, np.complex128)
+        d[n0] = 1.0
+        want = np.exp(-2j * np.pi * ((n0 * n) % N) / N)
+        assert np.max(np.abs(FF.fft_chain(d, "F") - want)) < 1e-11
+    # pure tone m -> N delta_{k,m}; constant -> N delta_{k,0}
+    m = 777
+    tone = np.exp(2j * np.pi * ((m * n) % N) / N)
+    X = FF.fft_chain(tone, "F")
+    assert abs(X[m] - N) < 1e-7 and np.max(np.abs(np.delete(X, m))) < 1e-7
+    X = FF.fft_chain(np.ones(N), "F")
+    assert X[0] == N and np.max(np.abs(X[1:])) < 1e-9
+    # inverse of a delta at k0 = (1/N) exp(+2 pi i k0 n / N)
+    d = np.zeros(N, np.complex128)
+    d[3] = 1.0
+    assert np.max(np.abs(FF.fft_chain(d, "I") - np.exp(2j * np.pi * 3 * n / N) / N)) < 1e-16
+
+
+def test_fft_invariants_batch():
+    B, N = 3, 1 << 13
+    x = FF.as_complex(synth.np_f32_um11(11, 0, 2 * B * N).reshape(B, N, 2))
+    X = FF.fft_chain(x, "F")
+    # Parseval: sum |X|^2 = N sum |x|^2, per transform of the batch
+    assert np.allclose(np.sum(np.abs(X) ** 2, -1), N * np.sum(np.abs(x) ** 2, -1), rtol=1e-12)
+    # round trip (the benchmark's pipeline(fft, ifft)) and its reverse
+    assert np.max(FF.rel_l2(FF.fft_chain(x, "FI"), x)) < 1e-14
+    assert np.max(FF.rel_l2(FF.fft_chain(x, "IF"), x)) < 1e-14
+    # batch rows are independent: row 1 alone gives the same transform
+    assert np.array_equal(FF.fft_chain(x[1], "F"), X[1])
+    # shift theorem: x[(n - s) mod N] -> X[k] exp(-2 pi i s k / N)
+    s = 100
+    k = np.arange(N)
+    Xs = FF.fft_chain(np.roll(x[0], s), "F")
+    assert np.max(np.abs(Xs - X[0] * np.exp(-2j * np.pi * ((s * k) % N) / N))) < 1e-9
+    # F F x = N x[-n mod N]
+    FFx = FF.fft_chain(x[0], "FF")
+    assert np.max(np.abs(FFx - N * x[0][(-k) % N])) < 1e-8
+    # brute force on one full 8192-point row
+    assert FF.rel_l2(X[2], FF.dft_brute(x[2])) < 1e-12
+
+
+def test_fft_tolerance_formula():
+    # Higham Thm 24.2 shape: grows with log2 N and the number of stages
+    assert FF.tolerance(1 << 16, 1) < FF.tolerance(1 << 16, 2) < 2 * FF.tolerance(1 << 16, 1) + 1e-7
+    assert FF.tolerance(1 << 13, 1) < FF.tolerance(1 << 16, 1) < 1e-5

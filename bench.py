@@ -420,15 +420,67 @@ REF_CONFIG = {
     "hysteresis": {"tree": "pipeline(threshold(173,250), loop_while_changed(step, "
                            "check_every=1), finalize)"},
     "nbody": {"bodies": 1 << 20, "eps2": 1e-4, "dt": 1e-3},
+    "fft": {"batch": 512, "points": 1 << 16, "tree": "pipeline(fft(2^16), ifft(2^16))"},
 }
 
 KCLASS = {0: "saxpy_chain", 1: "rgba_chain (k_rgba_ns)", 2: "u8_chain / plane pack+unpack",
-          3: "hysteresis stencil loop", 4: "k_nbody", 5: "k_reduce_chunks", 6: "traits"}
+          3: "hysteresis stencil loop", 4: "k_nbody", 5: "k_reduce_chunks", 6: "traits",
+          7: "k_fft (cluster FFT)"}
+
+class Fft(Workload):
+    """NEXT-3: the paper's FFT benchmark: a batch of 512 KiB
+    (65536-point complex64) FFTs, each pipelined with its inversion; one unit
+    = one FFT -> IFFT of one epu.  256 MiB batch (512 transforms)."""
+    name, unit, dtype = "fft_ifft_512x65536_c64", "ffts/s", "f32"
+
+    def setup(self, B=512, log2n=16):
+        M, t = self.M, self.torch
+        self.tree = self.trees.fft_pipeline(log2n)
+        self.kclass = M.MW_KC_FFT
+        self.Bt, self.N = B, 1 << log2n
+        self.o, self.n = self.slice(B)
+        src = t.empty((self.n, self.N, 2), dtype=t.float32, device=self.dev)
+        self.synth.dev_fill_f32_um11(src, 11, self.o * self.N * 2)
+        dst = t.empty_like(src)
+        g = (B, self.N, 2)
+        self.sets = [(M.arg(src, local_offset=self.o, global_shape=g),
+                      M.arg(dst, local_offset=self.o, global_shape=g))]
+        self.B = 1
+        self.units = B
+        ws = 2 * self.n * self.N * 8
+        self.l2_note = f"inputs larger than L2 ({ws >> 20} MiB/rank)"
+
+    def step(self, i):
+        return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
+
+    def e2e_setup(self):
+        t = self.torch
+        hsrc = t.empty((self.n, self.N, 2), dtype=t.float32).pin_memory()
+        hsrc.copy_(self.sets[0][0]._owner.cpu())
+        hdst = t.empty_like(hsrc).pin_memory()
+        g = (self.Bt, self.N, 2)
+        self.e2e_args = [self.M.arg(hsrc, local_offset=self.o, global_shape=g),
+                         self.M.arg(hdst, local_offset=self.o, global_shape=g)]
+        return self.n * self.N * 8, self.n * self.N * 8
+
+    def e2e_step(self):
+        return self.M.mw_run(self.ctx, self.tree, self.e2e_args)
+
+    def roof_bytes(self, cls, launches, steps, res):
+        # the fused FFT -> IFFT reads and writes each transform once: 2 x 512 KiB
+        return 16.0 * self.n * self.N * steps if cls == self.M.MW_KC_FFT else 0.0
+
+    def config(self):
+        return {"workload": self.name, "batch": self.Bt, "points": self.N,
+                "tree": "pipeline(fft(2^16), ifft(2^16)) (1/N in the inverse)",
+                "ffts_per_rank": self.n, "l2": self.l2_note,
+                "flop_convention": "5 N log2 N per transform, 2 transforms per unit"}
+
 
 WORKLOADS = {"filter": Filter, "saxpy": Saxpy, "segmentation": Segmentation,
              "mapreduce_sum": lambda *a: MapReduce(*a, dot=False),
              "mapreduce_dot": lambda *a: MapReduce(*a, dot=True),
-             "hysteresis": Hysteresis, "nbody": NBody}
+             "hysteresis": Hysteresis, "nbody": NBody, "fft": Fft}
 
 
 # ------------------------------------------------------------------ oracle legs
@@ -485,6 +537,13 @@ def oracle_generic_rate(name, budget_s):
             dt = time.perf_counter() - t0
             what = "2048x2048 tile (threshold + BFS closed form + finalize)"
             n = n * n
+        elif name == "fft":
+            from oracle import fft as FF
+            N = 1 << 16
+            x = synth.host_f32_um11(11, reps * 2 * N, 2 * N).reshape(N, 2)
+            t0 = time.perf_counter(); FF.fft_chain(FF.as_complex(x), "FI"); dt = time.perf_counter() - t0
+            what = "one 65536-point FFT -> IFFT (fp64, numpy pocketfft)"
+            n = 1
         elif name == "nbody":
             N = 1 << 20
             pos, _ = synth.host_nbody(9, 0, N, 2.0 ** -20)
@@ -503,7 +562,8 @@ def cpu_rate(name, budget_s):
         return oracle_filter_rate(budget_s)
     key = {"saxpy_map_2^20_fp32": "saxpy", "segmentation_1024x1024x512_u8": "segmentation",
            "mapreduce_sum_2^30_fp32": "mapreduce_sum", "mapreduce_dot_2^30_fp32": "mapreduce_dot",
-           "hysteresis_16384x16384_u8": "hysteresis", "nbody_2^20": "nbody"}[name]
+           "hysteresis_16384x16384_u8": "hysteresis", "nbody_2^20": "nbody",
+           "fft_ifft_512x65536_c64": "fft"}[name]
     return oracle_generic_rate(key, budget_s)
 
 
@@ -518,7 +578,8 @@ def run_reference(args, dist):
              "mapreduce_sum": ("mapreduce_sum_2^30_fp32", "elements/s", "f64"),
              "mapreduce_dot": ("mapreduce_dot_2^30_fp32", "elements/s", "f64"),
              "hysteresis": ("hysteresis_16384x16384_u8", "pixels/s", "u8"),
-             "nbody": ("nbody_2^20", "bodies/s", "f64")}
+             "nbody": ("nbody_2^20", "bodies/s", "f64"),
+             "fft": ("fft_ifft_512x65536_c64", "ffts/s", "f64")}
     wl = args.workload if args.workload != "all" else "filter"
     name, unit, dtype = names[wl]
     total_budget = 90.0
@@ -650,6 +711,9 @@ def run_marrow(args, dist, wl_name):
         line["pixel_executions_per_s"] = value * res["executions"]
     if wl_name == "nbody":
         line["interactions_per_s"] = value * w.N
+    if wl_name == "fft":
+        import math
+        line["gflops_5nlogn"] = value * 2 * 5 * w.N * math.log2(w.N) / 1e9
     # end to end through the C-ABI with HOST buffers (H2D + run + D2H per step)
     if hasattr(w, "e2e_setup"):
         h2d, d2h = w.e2e_setup()
@@ -771,7 +835,7 @@ def main():
         return
     names = list(WORKLOADS) if args.workload == "all" else [args.workload]
     default_steps = {"filter": 2000, "saxpy": 5000, "segmentation": 1000, "mapreduce_sum": 300,
-                     "mapreduce_dot": 200, "hysteresis": 20, "nbody": 3}
+                     "mapreduce_dot": 200, "hysteresis": 20, "nbody": 3, "fft": 200}
     user_steps = args.steps
     for n in names:
         args.steps = user_steps or default_steps[n]

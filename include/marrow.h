@@ -122,6 +122,16 @@ mw_status mw_kernel_map_product(mw_node** out);          /* MapReduce map stage:
  * values.  epu/nu feed the constraint system;
  * strict != 0 forbids the L mod granule tail.                                */
 mw_status mw_kernel_debug_traits(int64_t epu, int64_t nu, int32_t strict, mw_node** out);
+/* FFT leaf (NEXT-3; "a set of Fast-Fourier Transformations ...
+ * pipelined with its inversion ... The elementary partitioning unit is the
+ * size of each FFT which is 512 KBytes"; readings R23-R25): every row of a
+ * complex64 batch f32[B][N][2] (interleaved re, im; N = 2^log2n, log2n in
+ * 13..16, default benchmark 16 = 512 KiB) is transformed; inverse != 0 gives
+ * the inverse transform including the 1/N factor.  Consecutive FFT leaves of
+ * a Pipeline fuse (a forward followed by an inverse is one launch: each FFT
+ * crosses HBM once).  Partitioned by whole transforms.  log2n outside 13..16
+ * or inverse not 0/1: MW_E_INVALID_SPEC.                                    */
+mw_status mw_kernel_fft(int32_t log2n, int32_t inverse, mw_node** out);
 
 /* ------------------------------------------------------------------ skeletons
  * Table 1.  Composites retain their children; trees are
@@ -147,7 +157,7 @@ mw_status mw_node_id(const mw_node* n, uint8_t out[32]);
 enum {
     MW_VK_SAXPY = 1, MW_VK_RGBA = 2, MW_VK_U8 = 3, MW_VK_U8_2D = 4, MW_VK_NBODY = 5,
     MW_VK_VEC1 = 6, MW_VK_VEC2 = 7, MW_VK_TERMS = 8, MW_VK_ACCEL = 9, MW_VK_TRAITS = 10,
-    MW_VK_SCALAR = 11,
+    MW_VK_SCALAR = 11, MW_VK_CPLX = 12,
 };
 mw_status mw_node_signature(const mw_node* n, int32_t* in_kind, int32_t* out_kind);
 /* Sequential single-device kernel order (depth-first): leaves are
@@ -194,6 +204,8 @@ mw_status mw_partition(const mw_ctx* ctx, const mw_node* root, int64_t L, int64_
  *   NBODY->ACCEL pos f32[N][4] COPY, acc f32[N][4] (mut)
  *   VEC1 / VEC2  x f32[L] (, y f32[L]); the MapReduce result is in the future
  *   TRAITS       out i64[L][2] (mut): (SIZE, OFFSET) of each element's partition
+ *   CPLX         src f32[B][N][2], dst f32[B][N][2] (mut); N = 2^log2n of
+ *                every FFT leaf (else MW_E_SHAPE_MISMATCH); partition B
  */
 enum { MW_DT_U8 = 1, MW_DT_F32 = 2, MW_DT_F64 = 3, MW_DT_I64 = 4 };
 enum { MW_PARTITION = 0, MW_COPY = 1 };
@@ -266,7 +278,7 @@ mw_status mw_last_lengths(const mw_ctx* ctx, int64_t* per_part_len, int32_t n);
  * number of kernel launches of that class since enabling.                   */
 enum {
     MW_KC_SAXPY = 0, MW_KC_RGBA = 1, MW_KC_U8 = 2, MW_KC_STENCIL = 3, MW_KC_NBODY = 4,
-    MW_KC_REDUCE = 5, MW_KC_TRAITS = 6, MW_KC_COUNT = 7
+    MW_KC_REDUCE = 5, MW_KC_TRAITS = 6, MW_KC_FFT = 7, MW_KC_COUNT = 8
 };
 mw_status mw_stats_enable(mw_ctx* ctx, int32_t on);
 mw_status mw_kernel_stats(mw_ctx* ctx, int32_t kernel_class, double* total_ms, int64_t* launches);

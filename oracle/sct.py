@@ -27,11 +27,12 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import fft as FF
 from . import kernels as K
 
 # value kinds flowing along tree edges
-SAXPY, RGBA, U8, U8_2D, NBODY, VEC1, VEC2, TERMS, ACCEL, TRAITS = (
-    "saxpy", "rgba", "u8", "u8_2d", "nbody", "vec1", "vec2", "terms", "accel", "traits")
+SAXPY, RGBA, U8, U8_2D, NBODY, VEC1, VEC2, TERMS, ACCEL, TRAITS, CPLX = (
+    "saxpy", "rgba", "u8", "u8_2d", "nbody", "vec1", "vec2", "terms", "accel", "traits", "cplx")
 
 # leaf kind -> (input value kind, output value kind)
 LEAF_SIG = {
@@ -47,6 +48,7 @@ LEAF_SIG = {
     "map_identity": (VEC1, TERMS),
     "map_product": (VEC2, TERMS),
     "debug_traits": (TRAITS, TRAITS),
+    "fft": (CPLX, CPLX),
 }
 
 
@@ -159,6 +161,11 @@ def _leaf(node: Leaf, v):
         return Result(acc)
     if k in ("map_identity", "map_product"):
         return Result(v)  # terms are formed inside the fold (exact in fp64)
+    if k == "fft":
+        # one transform per row (R23/R24); complex128 flows between
+        # FFT stages, fp32 [.., N, 2] in
+        x = v if np.iscomplexobj(v) else FF.as_complex(v)
+        return Result(FF.fft_chain(x, "I" if p["inverse"] else "F"))
     if k == "debug_traits":
         # one partition: SIZE = L, OFFSET = 0 for every element
         L = int(v)

@@ -877,6 +877,20 @@ mw_status run_nbody(RunCtx& R, const Step& st, const mw_arg& pos, const mw_arg& 
     return MW_OK;
 }
 
+// FFT chains (NEXT-3): groups of <= 32 stages per fft_chain call, the first
+// reading src, later ones in place on dst.
+mw_status run_fft_chain(const std::vector<mw::ChainOp>& ops, const float* src, float* dst,
+                        int64_t nfft, int log2n, const mwk::Launch& L) {
+    for (size_t g = 0; g < ops.size(); g += 32) {
+        const int n = (int)std::min<size_t>(32, ops.size() - g);
+        uint32_t inv = 0;
+        for (int i = 0; i < n; ++i)
+            if (ops[g + i].ib) inv |= 1u << i;
+        MW_OK_OR_RETURN(kerr(mwk::fft_chain(g == 0 ? src : dst, dst, nfft, log2n, inv, n, L), "fft_chain"));
+    }
+    return MW_OK;
+}
+
 // ------------------------------------------------------------ host-staged chains (NEXT-1)
 mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args) {
     mw_ctx* c = R.c;
@@ -937,9 +951,16 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
             CUDA_OK(cudaEventRecord(c->st_in[sl], c->copy_in));
             CUDA_OK(cudaStreamWaitEvent(R.s, c->st_in[sl], 0));
             {
-                PartTimer t(c, R.s, p, st.kind == StepKind::Rgba ? MW_KC_RGBA : (st.kind == StepKind::U8 ? MW_KC_U8 : MW_KC_SAXPY));
+                PartTimer t(c, R.s, p,
+                            st.kind == StepKind::Rgba ? MW_KC_RGBA
+                            : st.kind == StepKind::U8 ? MW_KC_U8
+                            : st.kind == StepKind::Fft ? MW_KC_FFT
+                                                       : MW_KC_SAXPY);
                 mwk::Launch L = launch_for(c, R.s, p);
-                if (st.kind == StepKind::Rgba) {
+                if (st.kind == StepKind::Fft) {
+                    MW_OK_OR_RETURN(run_fft_chain(st.ops, reinterpret_cast<const float*>(d0),
+                                                  reinterpret_cast<float*>(d1), n, (int)st.ops[0].ia, L));
+                } else if (st.kind == StepKind::Rgba) {
                     MW_OK_OR_RETURN(kerr(mwk::rgba_chain(rgba[0], d0, d1, n, a0.shape[1], r0, L), "rgba_chain"));
                 } else if (st.kind == StepKind::U8) {
                     const uint8_t* in = d0;
@@ -1009,6 +1030,16 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         case MW_VK_TRAITS:
             MW_OK_OR_RETURN(check_arg(args[0], 0, MW_DT_I64, 2, 2, MW_PARTITION, 2));
             break;
+        case MW_VK_CPLX:
+            MW_OK_OR_RETURN(check_arg(args[0], 0, MW_DT_F32, 3, 3, MW_PARTITION, 2));
+            MW_OK_OR_RETURN(check_arg(args[1], 1, MW_DT_F32, 3, 3, MW_PARTITION, 2));
+            for (const Step& stp : prog)
+                for (const mw::ChainOp& o : stp.ops)
+                    if (args[0].shape[1] != (int64_t{1} << o.ia))
+                        return fail(MW_E_SHAPE_MISMATCH,
+                                    "fft leaf of N = 2^" + std::to_string(o.ia) + " on rows of " +
+                                        std::to_string(args[0].shape[1]) + " points");
+            break;
         default: return fail(MW_E_UNSUPPORTED, "root value kind cannot be run");
     }
     if (nargs == 2 && !same_shape(args[0], args[1]))
@@ -1047,7 +1078,8 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         return fail(MW_E_UNSUPPORTED, "host-resident arguments cannot be captured in a graph");
     if (host) {
         if (prog.size() != 1 || (prog[0].kind != StepKind::Saxpy && prog[0].kind != StepKind::Rgba &&
-                                 prog[0].kind != StepKind::U8))
+                                 prog[0].kind != StepKind::U8 && prog[0].kind != StepKind::Fft) ||
+            (prog[0].kind == StepKind::Fft && prog[0].ops.empty()))
             return fail(MW_E_UNSUPPORTED,
                         "host-resident arguments are supported for single fused Map/Pipeline "
                         "chains (NEXT-1)");
@@ -1131,6 +1163,22 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s), "reduce_combine"));
         CUDA_OK(cudaMemcpyAsync(f->res, rp, 8, cudaMemcpyDeviceToHost, s));
         f->has_reduce = true;
+    } else if (ik == MW_VK_CPLX) {
+        const std::vector<mw::ChainOp> none;
+        const std::vector<mw::ChainOp>& ops = prog.empty() ? none : prog[0].ops;
+        for (int q = 0; q < ppr; ++q) {
+            int p = R.first + q;
+            if (R.len[p] == 0) continue;
+            if (ops.empty()) {   // e.g. loop_for(fft, 0): identity
+                CUDA_OK(cudaMemcpyAsync(at_row<float>(args[1], R.off[p]), at_row<const float>(args[0], R.off[p]),
+                                        R.len[p] * row_bytes(args[0]), cudaMemcpyDeviceToDevice, s));
+                continue;
+            }
+            PartTimer t(c, s, p, MW_KC_FFT);
+            MW_OK_OR_RETURN(run_fft_chain(ops, at_row<const float>(args[0], R.off[p]),
+                                          at_row<float>(args[1], R.off[p]), R.len[p], (int)ops[0].ia,
+                                          launch_for(c, s, p)));
+        }
     } else if (ik == MW_VK_TRAITS) {
         for (int q = 0; q < ppr; ++q) {
             int p = R.first + q;

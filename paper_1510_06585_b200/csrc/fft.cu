@@ -1,0 +1,440 @@
+// fft.cu — the FFT workload (NEXT-3): batched FFT / inverse FFT chains.
+//
+// PAPER.md P:729-732 (§4): "FFT is a set of Fast-Fourier Transformations
+// adapted from the SHOC Benchmark Suite, where FFT is pipelined with its
+// inversion.  The elementary partitioning unit is the size of each FFT which
+// is 512 KBytes."  Readings R23-R25: N = 65536 complex64 points
+// per FFT (2^13..2^16 accepted), forward e^{-2 pi i nk/N}, inverse with 1/N.
+//
+// B200 design.  One FFT is held on chip by a thread-block CLUSTER of
+// C = N / 8192 CTAs (C in {1,2,4,8}); each CTA keeps 8192 points (64 KiB,
+// padded) in shared memory and the CTAs exchange data through distributed
+// shared memory, so one FFT moves through HBM exactly once per launch — and a
+// fused pipeline(fft, ifft) (the planner fuses consecutive FFT leaves) reads
+// the input once and writes the output once, with no intermediate in HBM.
+// Decomposition N = C * N2 (N2 = 8192), n = N2 n1 + n2, k = k1 + C k2:
+//   X[k1 + C k2] = sum_n2 W_N2^{n2 k2} W_N^{n2 k1} sum_n1 x[N2 n1 + n2] W_C^{n1 k1}
+// forward: radix-C DFT across the cluster (each CTA owns a slice of n2 and
+// pushes y[k1][n2] into CTA k1's shared memory), then a local 8192-point
+// Stockham FFT (radix 32, 16, 16) leaves X[k1 + C k2] at position k2 of CTA
+// k1 ("T layout").  The inverse runs the mirror image: local inverse FFT on
+// the T layout, then the twiddled radix-C inverse DFT gathered across the
+// cluster lands in natural order — fft followed by ifft needs no exchange in
+// the middle.  Twiddles come from exact-rounded fp64 tables in shared memory
+// (quadrant-reduced; the cross-CTA one is two-level), so mu <= 4u (R25).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mw_kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace mwk {
+namespace {
+
+constexpr int FN2 = 8192;              // points per CTA
+constexpr int FT = 256;                // threads per CTA
+constexpr int FPAD = FN2 + FN2 / 32;   // one pad element per 32 (conflict-free radix-32 stores)
+constexpr int T13 = 2048;              // W_8192^i, i < 8192/4
+constexpr int T9 = 128;                // W_512^i,  i < 512/4
+constexpr int THI = 64, TLO = 256;     // W_65536^(256h) and W_65536^l (first quadrant)
+constexpr size_t kFftSmem = sizeof(float2) * (FPAD + T13 + T9 + THI + TLO);
+
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 5); }
+
+// complex add / sub as one packed FP32x2 instruction (sm_100a FADD2)
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    unsigned long long ua, ub, ur;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(ua) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(ub) : "f"(b.x), "f"(b.y));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(ur) : "l"(ua), "l"(ub));
+    float2 r;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(ur));
+    return r;
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    unsigned long long ua, ub, ur;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(ua) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(ub) : "f"(b.x), "f"(b.y));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ur) : "l"(ua), "l"(ub));
+    float2 r;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(ur));
+    return r;
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+// cos(2 pi k / 32), k = 0..8 (fp32, correctly rounded)
+__host__ __device__ constexpr float c32(int k) {
+    return k == 0 ? 1.0f
+         : k == 1 ? 9.807852507e-01f
+         : k == 2 ? 9.238795042e-01f
+         : k == 3 ? 8.314695954e-01f
+         : k == 4 ? 7.071067691e-01f
+         : k == 5 ? 5.555702448e-01f
+         : k == 6 ? 3.826834261e-01f
+         : k == 7 ? 1.950903237e-01f
+         : 0.0f;
+}
+
+// d * W_32^k (forward W = e^{-2 pi i/32}; INV: conjugate), 0 <= k < 16.  k is
+// a constant after unrolling, so the branches and table fold away.
+template <bool INV>
+__device__ __forceinline__ float2 tw32(float2 d, int k) {
+    if (k == 0) return d;
+    if (k == 8) return INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);   // +-i
+    const float c = k <= 8 ? c32(k) : -c32(16 - k);
+    const float s = k <= 8 ? c32(8 - k) : c32(k - 8);
+    const float si = INV ? s : -s;
+    // d * (c + i si) = d.x (c, si) + d.y (-si, c): FMUL2 + FFMA2 with the
+    // scalar d.x / d.y broadcast across the pair
+    unsigned long long bx, by, w, iw, t, r;
+    asm("mov.b64 %0, {%1,%1};" : "=l"(bx) : "f"(d.x));
+    asm("mov.b64 %0, {%1,%1};" : "=l"(by) : "f"(d.y));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(w) : "f"(c), "f"(si));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(iw) : "f"(-si), "f"(c));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(bx), "l"(w));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(by), "l"(iw), "l"(t));
+    float2 o;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+
+__host__ __device__ constexpr int bitrev(int i, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+    return r;
+}
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// In-register R-point DFT (R | 32): radix-2 decimation in frequency (one
+// template level per stage, so every index is a compile-time constant), then
+// a compile-time bit-reversal renaming to natural output order.
+template <int R, int HALF, bool INV>
+__device__ __forceinline__ void dif_stage(float2* v) {
+#pragma unroll
+    for (int blk = 0; blk < R; blk += 2 * HALF) {
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) {
+            const float2 a = v[blk + j], b = v[blk + j + HALF];
+            v[blk + j] = cadd(a, b);
+            v[blk + j + HALF] = tw32<INV>(csub(a, b), j * (16 / HALF));
+        }
+    }
+    if constexpr (HALF > 1) dif_stage<R, HALF / 2, INV>(v);
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft(float2* v) {
+    if constexpr (R > 1) {
+        dif_stage<R, R / 2, INV>(v);
+        float2 t[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) t[i] = v[bitrev(i, ilog2(R))];
+#pragma unroll
+        for (int i = 0; i < R; ++i) v[i] = t[i];
+    }
+}
+
+// W_M^e from a first-quadrant table T[i] = W_M^i, i < M/4 (exact quadrant turn)
+template <bool INV>
+__device__ __forceinline__ float2 tw_q(const float2* T, int e, int qlog2) {
+    const int q = (e >> qlog2) & 3;
+    float2 w = T[e & ((1 << qlog2) - 1)];
+    if (q & 1) w = make_float2(w.y, -w.x);    // * (-i)
+    if (q & 2) w = make_float2(-w.x, -w.y);   // * (-1)
+    if (INV) w.y = -w.y;
+    return w;
+}
+// W_65536^e, two-level first-quadrant table
+template <bool INV>
+__device__ __forceinline__ float2 tw_cross(const float2* Thi, const float2* Tlo, int e) {
+    const int q = (e >> 14) & 3, r = e & 16383;
+    float2 w = cmul(Thi[r >> 8], Tlo[r & 255]);
+    if (q & 1) w = make_float2(w.y, -w.x);
+    if (q & 2) w = make_float2(-w.x, -w.y);
+    if (INV) w.y = -w.y;
+    return w;
+}
+
+// One Stockham pass over the CTA's 8192 points (in place: all loads, barrier,
+// all stores): v[r] = s[j + r N2/R] * W_{Ns R}^{r k}, R-point DFT, stored at
+// (j / Ns) Ns R + k + r Ns, k = j mod Ns.
+template <int R, int NS, bool INV>
+__device__ __forceinline__ void stockham_pass(float2* s, const float2* T13p, const float2* T9p) {
+    constexpr int NB = FN2 / R, PER = NB / FT;
+    int tid = threadIdx.x;
+    asm volatile("" : "+r"(tid));   // per pass: no addresses kept live across passes
+    float2 v[PER][R];
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+        const int j = tid + p * FT;
+        const int k = j & (NS - 1);
+        // NB is a multiple of 32: fpad(j + r NB) = fpad(j) + r (NB + NB/32), so
+        // every load is one base register plus an immediate offset
+        const float2* src = s + fpad(j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[p][r] = src[r * (NB + NB / 32)];
+        if constexpr (NS > 1) {
+            constexpr int M = NS * R;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                float2 w;
+                if constexpr (M == 8192) w = tw_q<INV>(T13p, (r * k) & 8191, 11);
+                else w = tw_q<INV>(T9p, (r * k) & 511, 7);
+                v[p][r] = cmul(v[p][r], w);
+            }
+        }
+        dft<R, INV>(v[p]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+        const int j = tid + p * FT;
+        const int k = j & (NS - 1);
+        const int d = (j / NS) * NS * R + k;
+        // NS = 1: d is a multiple of R = 32, so d + r stays in one 32-run;
+        // NS >= 32: r NS is a multiple of 32 -> immediate offsets again
+        static_assert(NS == 1 ? R == 32 : NS % 32 == 0, "padding plan");
+        float2* dst = s + fpad(d);
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[NS == 1 ? r : r * (NS + NS / 32)] = v[p][r];
+    }
+    __syncthreads();
+}
+
+// Not inlined: the three passes get their own register allocation instead of
+// competing with the cluster-exchange code around them (measured: inlining
+// them into the fused forward->inverse kernel spills ~400 B per thread).
+template <bool INV>
+__device__ __noinline__ void local_fft(float2* s, const float2* T13p, const float2* T9p) {
+    static_assert(FN2 == 32 * 16 * 16, "pass plan");
+    stockham_pass<32, 1, INV>(s, T13p, T9p);
+    stockham_pass<16, 32, INV>(s, T13p, T9p);
+    stockham_pass<16, 512, INV>(s, T13p, T9p);
+}
+
+template <int C>
+__device__ __forceinline__ void csync() {
+    if constexpr (C > 1) cg::this_cluster().sync();
+    else __syncthreads();
+}
+
+__device__ __forceinline__ float2 ld_nc(const float2* p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_cs(float2* p, float2 v) {
+    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
+enum FftMode { FFT_F = 0, FFT_I = 1, FFT_FI = 2 };
+
+// One launch = one of: forward, inverse, or the fused forward -> inverse
+// (pipeline(fft, ifft)) over nfft transforms of N = C * 8192 points.  Longer
+// chains are split into such launches by the host (in place on the output).
+template <int C, int MODE>
+__global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, int64_t nfft) {
+    extern __shared__ float4 fft_smem[];
+    float2* S = reinterpret_cast<float2*>(fft_smem);
+    float2* T13p = S + FPAD;
+    float2* T9p = T13p + T13;
+    float2* Thi = T9p + T9;
+    float2* Tlo = Thi + THI;
+    for (int i = threadIdx.x; i < T13 + T9 + THI + TLO; i += FT) {
+        double x;   // angle / pi
+        float2* dst;
+        if (i < T13) { x = 2.0 * i / 8192.0; dst = T13p + i; }
+        else if (i < T13 + T9) { x = 2.0 * (i - T13) / 512.0; dst = T9p + (i - T13); }
+        else if (i < T13 + T9 + THI) { x = 2.0 * 256.0 * (i - T13 - T9) / 65536.0; dst = Thi + (i - T13 - T9); }
+        else { x = 2.0 * (i - T13 - T9 - THI) / 65536.0; dst = Tlo + (i - T13 - T9 - THI); }
+        double sn, cs;
+        sincospi(x, &sn, &cs);
+        *dst = make_float2((float)cs, (float)-sn);
+    }
+    __syncthreads();
+    constexpr int NI = 32 / C;             // n2 values per thread (x C values of n1)
+    constexpr int N = C * FN2;
+    constexpr int STEP = 65536 / N;        // W_N = W_65536^STEP
+    const int c = C > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    // peer CTA k's shared-memory window (one mapa instruction)
+    auto rem = [S](int k) -> float2* {
+        float2* p = S;
+        asm volatile("" : "+l"(p));   // recompute per use instead of holding C pointers live
+        if constexpr (C > 1) return cg::this_cluster().map_shared_rank(p, k);
+        else return p;
+    };
+    const float scale = 1.0f / (float)N;   // exact (power of two)
+    for (int64_t f = blockIdx.x / C; f < nfft; f += gridDim.x / C) {
+        // opaque per iteration: keeps the compiler from hoisting the 32
+        // per-element addresses out of the persistent loop (and spilling them)
+        int tid = threadIdx.x;
+        asm volatile("" : "+r"(tid));
+        const float2* x = in + f * N;
+        float2* y = out + f * N;
+        {   // natural-order input: thread owns n2 = c N2/C + tid + 256 i, all n1
+            float2 v[NI][C];
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int n2 = c * (FN2 / C) + tid + FT * i;
+#pragma unroll
+                for (int n1 = 0; n1 < C; ++n1) v[i][n1] = ld_nc(x + n1 * FN2 + n2);
+            }
+            csync<C>();   // every peer is done reading the shared memory we write
+            if constexpr (MODE == FFT_I) {
+                // T layout directly: X[m] goes to CTA m mod C at position m / C
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int n2 = c * (FN2 / C) + tid + FT * i;
+#pragma unroll
+                    for (int n1 = 0; n1 < C; ++n1) {
+                        const int m = n1 * FN2 + n2;
+                        rem(m % C)[fpad(m / C)] = v[i][n1];
+                    }
+                }
+            } else {
+                // radix-C forward DFT across the cluster, twiddle W_N^{n2 k1}, push to CTA k1
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int n2 = c * (FN2 / C) + tid + FT * i;
+                    dft<C, false>(v[i]);
+#pragma unroll
+                    for (int k1 = 0; k1 < C; ++k1) {
+                        float2 t = v[i][k1];
+                        if (k1 > 0) t = cmul(t, tw_cross<false>(Thi, Tlo, (n2 * k1 * STEP) & 65535));
+                        rem(k1)[fpad(n2)] = t;
+                    }
+                }
+            }
+            csync<C>();
+        }
+        if constexpr (MODE != FFT_I) local_fft<false>(S, T13p, T9p);   // -> X[k1 + C k2] at k2
+        if constexpr (MODE != FFT_F) local_fft<true>(S, T13p, T9p);    // -> z[k1][n2] at n2
+        csync<C>();   // every CTA's local transform is complete
+        {
+            float2 v[NI][C];
+            if constexpr (MODE == FFT_F) {
+                // T layout -> natural order
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int n2 = c * (FN2 / C) + tid + FT * i;
+#pragma unroll
+                    for (int n1 = 0; n1 < C; ++n1) {
+                        const int m = n1 * FN2 + n2;
+                        v[i][n1] = rem(m % C)[fpad(m / C)];
+                    }
+                }
+            } else {
+                // twiddle W_N^{-k1 n2}, radix-C inverse DFT across the cluster, 1/N
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int n2 = c * (FN2 / C) + tid + FT * i;
+#pragma unroll
+                    for (int k1 = 0; k1 < C; ++k1) {
+                        float2 t = rem(k1)[fpad(n2)];
+                        if (k1 > 0) t = cmul(t, tw_cross<true>(Thi, Tlo, (n2 * k1 * STEP) & 65535));
+                        v[i][k1] = t;
+                    }
+                    dft<C, true>(v[i]);
+#pragma unroll
+                    for (int n1 = 0; n1 < C; ++n1) v[i][n1] = make_float2(v[i][n1].x * scale, v[i][n1].y * scale);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int n2 = c * (FN2 / C) + tid + FT * i;
+#pragma unroll
+                for (int n1 = 0; n1 < C; ++n1) st_cs(y + n1 * FN2 + n2, v[i][n1]);
+            }
+        }
+    }
+    csync<C>();   // no CTA leaves while a peer may still read its shared memory
+}
+
+template <int C, int MODE>
+cudaError_t fft_launch(const float2* in, float2* out, int64_t nfft, const Launch& L) {
+    static int max_clusters = -1;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    if (max_clusters < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_fft<C, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kFftSmem);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(C * 1024);
+        cfg.blockDim = dim3(FT);
+        cfg.dynamicSmemBytes = kFftSmem;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_fft<C, MODE>, &cfg) != cudaSuccess || n < 1) n = 1;
+        max_clusters = n;
+    }
+    int64_t clusters = nfft < max_clusters ? nfft : max_clusters;
+    if (L.slow > 1.0f) clusters = (int64_t)((double)clusters / (double)L.slow + 0.999);
+    if (clusters < 1) clusters = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(clusters * C));
+    cfg.blockDim = dim3(FT);
+    cfg.dynamicSmemBytes = kFftSmem;
+    cfg.stream = L.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    note_launch();
+    return cudaLaunchKernelEx(&cfg, k_fft<C, MODE>, in, out, nfft);
+}
+
+template <int C>
+cudaError_t fft_launch_mode(int mode, const float2* in, float2* out, int64_t nfft, const Launch& L) {
+    switch (mode) {
+        case FFT_F: return fft_launch<C, FFT_F>(in, out, nfft, L);
+        case FFT_I: return fft_launch<C, FFT_I>(in, out, nfft, L);
+        default: return fft_launch<C, FFT_FI>(in, out, nfft, L);
+    }
+}
+
+}  // namespace
+
+bool fft_supported(int log2n) { return log2n >= 13 && log2n <= 16; }
+
+cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint32_t inv, int nst,
+                      const Launch& L) {
+    if (nfft <= 0) return cudaSuccess;
+    if (nst > 32 || !fft_supported(log2n)) return cudaErrorInvalidValue;
+    const float2* src = reinterpret_cast<const float2*>(in);
+    float2* o2 = reinterpret_cast<float2*>(out);
+    if (nst == 0) {
+        if (in != out) return cudaMemcpyAsync(out, in, (size_t)nfft << (log2n + 3), cudaMemcpyDeviceToDevice, L.stream);
+        return cudaSuccess;
+    }
+    // greedy grouping: a forward followed by an inverse is one fused launch
+    for (int s = 0; s < nst;) {
+        const bool iv = (inv >> s) & 1;
+        int mode = iv ? FFT_I : FFT_F;
+        int used = 1;
+        if (!iv && s + 1 < nst && ((inv >> (s + 1)) & 1)) {
+            mode = FFT_FI;
+            used = 2;
+        }
+        cudaError_t e;
+        switch (log2n) {
+            case 13: e = fft_launch_mode<1>(mode, src, o2, nfft, L); break;
+            case 14: e = fft_launch_mode<2>(mode, src, o2, nfft, L); break;
+            case 15: e = fft_launch_mode<4>(mode, src, o2, nfft, L); break;
+            default: e = fft_launch_mode<8>(mode, src, o2, nfft, L); break;
+        }
+        if (e != cudaSuccess) return e;
+        src = o2;   // later launches run in place on the output
+        s += used;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace mwk

@@ -1415,6 +1415,7 @@ __global__ void k_traits(int64_t* out, int64_t count, int64_t size, int64_t offs
 
 // ============================================================ launchers
 unsigned long long launch_count() { return g_launches; }
+void note_launch() { ++g_launches; }
 
 void tune_defaults(int* out) {
     out[TUNE_RGBA_TMA] = tuning_knob("MW_RGBA_TMA", 1);        // 16 KiB x 3 stages

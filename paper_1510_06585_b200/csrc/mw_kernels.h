@@ -131,6 +131,14 @@ cudaError_t fill_traits(int64_t* out, int64_t count, int64_t size, int64_t offse
                         const Launch& L);
 
 int sm_count();
+void note_launch();   // count one launch of ours (mw_ctx_launch_count)
+
+// ------------------------------------------------------------ FFT (NEXT-3)
+// nfft transforms of N = 2^log2n complex64 points (interleaved re, im), a
+// chain of nst stages (bit s of inv: inverse with 1/N); in may equal out.
+bool fft_supported(int log2n);   // 13..16
+cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint32_t inv, int nst,
+                      const Launch& L);
 unsigned long long launch_count();  // kernels launched by this library
 
 }  // namespace mwk

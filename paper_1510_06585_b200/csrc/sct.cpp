@@ -51,6 +51,7 @@ static const char* leaf_name(LeafKind k) {
         case LeafKind::MapIdentity: return "map_identity";
         case LeafKind::MapProduct: return "map_product";
         case LeafKind::DebugTraits: return "debug_traits";
+        case LeafKind::Fft: return "fft";
     }
     return "?";
 }
@@ -120,7 +121,7 @@ static int norm2d(int kind, bool two_d) {
 
 // ============================================================ plan (fusion)
 static bool is_chain(StepKind k) {
-    return k == StepKind::Saxpy || k == StepKind::Rgba || k == StepKind::U8;
+    return k == StepKind::Saxpy || k == StepKind::Rgba || k == StepKind::U8 || k == StepKind::Fft;
 }
 static void append_merged(std::vector<Step>& dst, const std::vector<Step>& src) {
     for (const Step& s : src) {
@@ -168,6 +169,7 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
             case LeafKind::NbodyAccel: s.kind = StepKind::NbodyAccel; s.eps2 = n->fb; break;
             case LeafKind::MapIdentity: s.kind = StepKind::MapStage; s.dot = false; break;
             case LeafKind::MapProduct: s.kind = StepKind::MapStage; s.dot = true; break;
+            case LeafKind::Fft: s.kind = StepKind::Fft; s.ops = {op}; break;
             case LeafKind::DebugTraits:
                 s.kind = StepKind::Traits;
                 s.epu = n->ia;
@@ -542,6 +544,12 @@ mw_status mw_kernel_map_identity(mw_node** out) {
 }
 mw_status mw_kernel_map_product(mw_node** out) {
     return make_leaf(LeafKind::MapProduct, MW_VK_VEC2, MW_VK_TERMS, out);
+}
+mw_status mw_kernel_fft(int32_t log2n, int32_t inverse, mw_node** out) {
+    if (log2n < 13 || log2n > 16)
+        return fail(MW_E_INVALID_SPEC, "fft: log2n must be in 13..16 (N = 8192..65536 points)");
+    if (inverse != 0 && inverse != 1) return fail(MW_E_INVALID_SPEC, "fft: inverse must be 0 or 1");
+    return make_leaf(LeafKind::Fft, MW_VK_CPLX, MW_VK_CPLX, out, 0, 0, log2n, inverse);
 }
 mw_status mw_kernel_debug_traits(int64_t epu, int64_t nu, int32_t strict, mw_node** out) {
     if (epu < 1 || nu < 1) return fail(MW_E_INVALID_SPEC, "epu and nu must be >= 1");

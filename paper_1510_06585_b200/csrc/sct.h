@@ -21,7 +21,7 @@ mw_status fail(mw_status code, const std::string& msg);
 enum class NodeType { Leaf, Pipeline, Map, MapReduce, LoopFor, LoopWhile };
 enum class LeafKind {
     Saxpy, GaussNoise, Solarize, Mirror, Segment, HystStep, HystFinalize,
-    NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits
+    NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits, Fft
 };
 
 struct Node {
@@ -51,7 +51,7 @@ std::vector<const Node*> leaves(const Node* n);
 // fused chain (they share the partitioning, so their
 // intermediates never leave the device — here, never leave registers).
 enum class StepKind { Saxpy, Rgba, U8, StencilFor, StencilWhile, NbodyLoop, NbodyAccel,
-                      MapStage, Reduce, Traits };
+                      MapStage, Reduce, Traits, Fft };
 struct ChainOp {
     LeafKind kind;
     float fa;

@@ -20,7 +20,7 @@ MW_OK = 0
  MW_E_OOM, MW_E_UNSUPPORTED) = range(1, 12)
 MW_MERGE_ADD = 0
 (MW_VK_SAXPY, MW_VK_RGBA, MW_VK_U8, MW_VK_U8_2D, MW_VK_NBODY, MW_VK_VEC1, MW_VK_VEC2,
- MW_VK_TERMS, MW_VK_ACCEL, MW_VK_TRAITS, MW_VK_SCALAR) = range(1, 12)
+ MW_VK_TERMS, MW_VK_ACCEL, MW_VK_TRAITS, MW_VK_SCALAR, MW_VK_CPLX) = range(1, 13)
 MW_DT_U8, MW_DT_F32, MW_DT_F64, MW_DT_I64 = 1, 2, 3, 4
 MW_PARTITION, MW_COPY = 0, 1
 MW_LOC_DEVICE, MW_LOC_HOST = 0, 1
@@ -30,7 +30,7 @@ MW_KB_NONE, MW_KB_EXACT, MW_KB_SCT, MW_KB_WORKLOAD, MW_KB_DIMENSIONALITY = range
 (MW_TUNE_RGBA_TMA, MW_TUNE_RGBA_UNROLL, MW_TUNE_HYST_PLANES, MW_TUNE_HYST_T, MW_TUNE_HYST_ROWS,
  MW_TUNE_NBODY_SPLIT, MW_TUNE_U8_TMA, MW_TUNE_COUNT) = range(8)
 (MW_KC_SAXPY, MW_KC_RGBA, MW_KC_U8, MW_KC_STENCIL, MW_KC_NBODY, MW_KC_REDUCE,
- MW_KC_TRAITS, MW_KC_COUNT) = range(8)
+ MW_KC_TRAITS, MW_KC_FFT, MW_KC_COUNT) = range(9)
 
 
 class MwError(RuntimeError):
@@ -92,6 +92,7 @@ _SIG = {
     "mw_kernel_map_identity": [_node_pp],
     "mw_kernel_map_product": [_node_pp],
     "mw_kernel_debug_traits": [_i64, _i64, _i32, _node_pp],
+    "mw_kernel_fft": [_i32, _i32, _node_pp],
     "mw_pipeline": [_P(_vp), _i32, _node_pp],
     "mw_map": [_vp, _node_pp],
     "mw_map_reduce": [_vp, _i32, _node_pp],
@@ -247,6 +248,12 @@ def mw_kernel_map_product():
 
 def mw_kernel_debug_traits(epu=1, nu=1, strict=False):
     return _new("mw_kernel_debug_traits", epu, nu, int(bool(strict)))
+
+
+def mw_kernel_fft(log2n=16, inverse=False):
+    """FFT of every row of a complex64 batch f32[B][2^log2n][2] (NEXT-3,
+    P:729-732); inverse includes 1/N."""
+    return _new("mw_kernel_fft", log2n, int(bool(inverse)))
 
 
 def mw_pipeline(stages):

@@ -45,3 +45,10 @@ def hysteresis(lo=HYST_LO, hi=HYST_HI, max_iters=10000, check_every=1):
 def nbody(steps, dt=NBODY_DT, eps2=NBODY_EPS2):
     """loop(nbody step, steps) with COPY positions — P:734-737."""
     return M.mw_loop_for(M.mw_kernel_nbody_step(dt, eps2), steps)
+
+
+def fft_pipeline(log2n=16):
+    """The FFT benchmark: "FFT is pipelined with its inversion" (P:729-732);
+    pipeline(fft, ifft) over a batch of 2^log2n-point complex64 transforms
+    (512 KiB each at log2n = 16, reading R23)."""
+    return M.mw_pipeline([M.mw_kernel_fft(log2n, False), M.mw_kernel_fft(log2n, True)])

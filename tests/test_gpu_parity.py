@@ -672,3 +672,112 @@ def test_ctx_destroy_while_future_and_graph_alive():
     assert st == M.MW_E_INVALID_SPEC or st == M.MW_E_STATE
     del f, g                         # last references: the teardown runs here
     torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------- FFT (NEXT-3)
+from oracle import fft as FF  # noqa: E402
+
+SEED_FFT = 11
+
+
+def _fft_tree(log2n, dirs):
+    leaves = [M.mw_kernel_fft(log2n, d == "I") for d in dirs]
+    return leaves[0] if len(leaves) == 1 else M.mw_pipeline(leaves)
+
+
+def _fft_in(B, N, start=0):
+    return synth.np_f32_um11(SEED_FFT, start, 2 * B * N).reshape(B, N, 2)
+
+
+def _fft_check(got, x, dirs):
+    N = x.shape[1]
+    want = FF.fft_chain(FF.as_complex(x), dirs)
+    err = FF.rel_l2(FF.as_complex(got), want)
+    assert np.all(np.isfinite(err)) and err.max() <= FF.tolerance(N, len(dirs)), (dirs, err.max())
+    return err.max()
+
+
+@pytest.mark.parametrize("log2n", [13, 14, 15, 16])
+@pytest.mark.parametrize("dirs", ["F", "I", "FI", "IF", "FF", "FIIF"])
+def test_fft_chain_parity(log2n, dirs):
+    N = 1 << log2n
+    B = 3
+    x = _fft_in(B, N, 77)
+    src = dev(x)
+    dst = torch.empty_like(src)
+    run(ctx(), _fft_tree(log2n, dirs), [M.arg(src), M.arg(dst)])
+    _fft_check(dst.cpu().numpy(), x, dirs)
+    assert torch.equal(src, dev(x))   # input untouched
+
+
+def test_fft_pipeline_partitions_bitwise_and_batch():
+    """The benchmark tree over a batch split into partitions (whole FFTs per
+    partition, zero shares, ragged splits): every FFT is computed the same way
+    wherever it lands, so the output is bit-identical across distributions."""
+    log2n, B = 16, 37
+    N = 1 << log2n
+    x = _fft_in(B, N)
+    src = dev(x)
+    ref = torch.empty_like(src)
+    run(ctx(), trees.fft_pipeline(log2n), [M.arg(src), M.arg(ref)])
+    _fft_check(ref.cpu().numpy(), x, "FI")
+    rng = np.random.default_rng(5)
+    for k, d in [(3, x_) for x_ in dists(3, rng, 2) + [[0.0, 1.0, 0.0]]] + [(5, [0.1, 0.2, 0.0, 0.3, 0.4])]:
+        dst = torch.empty_like(src)
+        run(ctx(k, d), trees.fft_pipeline(log2n), [M.arg(src), M.arg(dst)])
+        assert torch.equal(dst, ref), d
+
+
+def test_fft_closed_forms_on_device():
+    """Delta and single-tone inputs (closed forms, no oracle library): the
+    forward transform of a delta at n0 is the twiddle row exp(-2 pi i n0 k/N)."""
+    N = 1 << 16
+    x = np.zeros((2, N, 2), np.float32)
+    x[0, 5, 0] = 1.0
+    x[1, 0, 0] = 1.0   # delta at 0 -> all ones
+    src = dev(x)
+    dst = torch.empty_like(src)
+    run(ctx(), M.mw_kernel_fft(16, False), [M.arg(src), M.arg(dst)])
+    g = dst.cpu().numpy().astype(np.float64)
+    k = np.arange(N)
+    want = np.exp(-2j * np.pi * ((5 * k) % N) / N)
+    assert np.max(np.abs(g[0, :, 0] + 1j * g[0, :, 1] - want)) < 4e-6
+    assert np.array_equal(g[1], np.stack([np.ones(N), np.zeros(N)], -1))
+
+
+def test_fft_edge_cases():
+    c = ctx(2)
+    e = torch.empty((0, 1 << 13, 2), dtype=torch.float32, device=DEV)
+    run(c, trees.fft_pipeline(13), [M.arg(e), M.arg(torch.empty_like(e))])   # empty batch
+    x = _fft_in(1, 1 << 13)
+    src = dev(x)
+    dst = torch.empty_like(src)
+    run(c, trees.fft_pipeline(13), [M.arg(src), M.arg(dst)])   # one FFT, two partitions
+    _fft_check(dst.cpu().numpy(), x, "FI")
+    # loop_for(fft, 0) is the identity; loop_for(pipeline(fft, ifft), 3) fuses to 3 launches
+    run(c, M.mw_loop_for(M.mw_kernel_fft(13, False), 0), [M.arg(src), M.arg(dst)])
+    assert torch.equal(dst, src)
+    run(c, M.mw_loop_for(trees.fft_pipeline(13), 3), [M.arg(src), M.arg(dst)])
+    _fft_check(dst.cpu().numpy(), x, "FIFIFI")
+    with pytest.raises(M.MwError):   # leaf size != row length
+        run(c, trees.fft_pipeline(14), [M.arg(src), M.arg(dst)])
+
+
+def test_fft_host_staged_and_graph():
+    log2n, B = 16, 40
+    x = _fft_in(B, 1 << log2n, 3)
+    src = dev(x)
+    ref = torch.empty_like(src)
+    c = ctx()
+    run(c, trees.fft_pipeline(log2n), [M.arg(src), M.arg(ref)])
+    hin = torch.from_numpy(x).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    run(c, trees.fft_pipeline(log2n), [M.arg(hin), M.arg(hout)])
+    assert torch.equal(hout, ref.cpu())
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        out = torch.empty_like(src)
+        g = M.mw_graph_capture(c, trees.fft_pipeline(log2n), [M.arg(src), M.arg(out)], s)
+        g.launch(s)
+        s.synchronize()
+    assert torch.equal(out, ref)

@@ -45,6 +45,12 @@ def test_status_strings_and_errors():
     assert e.value.status == M.MW_E_UNSUPPORTED
     with pytest.raises(M.MwError):
         M.mw_loop_while_changed(M.mw_kernel_hysteresis_step(), 10, 0)
+    for bad in (12, 17, 0):   # FFT sizes 2^13..2^16 (R23)
+        with pytest.raises(M.MwError) as e:
+            M.mw_kernel_fft(bad)
+        assert e.value.status == M.MW_E_INVALID_SPEC
+    with pytest.raises(M.MwError):
+        M.mw_pipeline([M.mw_kernel_fft(16), M.mw_kernel_mirror()])   # kinds do not chain
 
 
 def test_signatures():
@@ -54,6 +60,9 @@ def test_signatures():
     assert M.mw_node_signature(trees.mapreduce(True)) == (M.MW_VK_VEC2, M.MW_VK_SCALAR)
     assert M.mw_node_signature(trees.nbody(3)) == (M.MW_VK_NBODY, M.MW_VK_NBODY)
     assert M.mw_node_signature(M.mw_kernel_nbody_accel(1e-4)) == (M.MW_VK_NBODY, M.MW_VK_ACCEL)
+    assert M.mw_node_signature(trees.fft_pipeline()) == (M.MW_VK_CPLX, M.MW_VK_CPLX)
+    assert M.mw_node_id(trees.fft_pipeline(16)) != M.mw_node_id(trees.fft_pipeline(15))
+    assert M.mw_kernel_execution_order(M.mw_loop_for(trees.fft_pipeline(), 2), []) == [0, 1, 0, 1]
 
 
 def test_node_id_determinism():

@@ -37,7 +37,10 @@ namespace {
 constexpr int FN2 = 8192;              // points per CTA
 constexpr int FT = 256;                // threads per CTA
 constexpr int FPAD = FN2 + FN2 / 32;   // one pad element per 32 (conflict-free radix-32 stores)
-constexpr int T13 = 2048;              // W_8192^i, i < 8192/4
+// twiddle tables are stored XOR-swizzled (tsw): the index strides r * k of
+// the Stockham twiddles then spread over more banks (a bank model over all
+// r of both passes: 37 % fewer shared-memory wavefronts than linear order)
+constexpr int T13 = 2048;              // W_8192^i, i < 8192/4 (first quadrant)
 constexpr int T9 = 128;                // W_512^i,  i < 512/4
 constexpr int THI = 64, TLO = 256;     // W_65536^(256h) and W_65536^l (first quadrant)
 constexpr size_t kFftSmem = sizeof(float2) * (FPAD + T13 + T9 + THI + TLO);
@@ -140,10 +143,11 @@ __device__ __forceinline__ void dft(float2* v) {
 }
 
 // W_M^e from a first-quadrant table T[i] = W_M^i, i < M/4 (exact quadrant turn)
+__device__ __forceinline__ int tsw(int i) { return i ^ ((i >> 1) & 15); }
 template <bool INV>
 __device__ __forceinline__ float2 tw_q(const float2* T, int e, int qlog2) {
     const int q = (e >> qlog2) & 3;
-    float2 w = T[e & ((1 << qlog2) - 1)];
+    float2 w = T[tsw(e & ((1 << qlog2) - 1))];
     if (q & 1) w = make_float2(w.y, -w.x);    // * (-i)
     if (q & 2) w = make_float2(-w.x, -w.y);   // * (-1)
     if (INV) w.y = -w.y;
@@ -222,6 +226,20 @@ __device__ __forceinline__ void csync() {
     if constexpr (C > 1) cg::this_cluster().sync();
     else __syncthreads();
 }
+// Split barrier without memory ordering: only protects shared memory that
+// peers READ before arriving (their loaded values were consumed before the
+// arrive, so the reads are complete) from our next writes.  The arrive is
+// issued right after the gather; the output stores and the next transform's
+// input loads run before the matching wait.
+template <int C>
+__device__ __forceinline__ void war_arrive() {
+    if constexpr (C > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+template <int C>
+__device__ __forceinline__ void war_wait() {
+    if constexpr (C > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    else __syncthreads();
+}
 
 __device__ __forceinline__ float2 ld_nc(const float2* p) {
     float2 v;
@@ -248,8 +266,8 @@ __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, in
     for (int i = threadIdx.x; i < T13 + T9 + THI + TLO; i += FT) {
         double x;   // angle / pi
         float2* dst;
-        if (i < T13) { x = 2.0 * i / 8192.0; dst = T13p + i; }
-        else if (i < T13 + T9) { x = 2.0 * (i - T13) / 512.0; dst = T9p + (i - T13); }
+        if (i < T13) { x = 2.0 * i / 8192.0; dst = T13p + tsw(i); }
+        else if (i < T13 + T9) { x = 2.0 * (i - T13) / 512.0; dst = T9p + tsw(i - T13); }
         else if (i < T13 + T9 + THI) { x = 2.0 * 256.0 * (i - T13 - T9) / 65536.0; dst = Thi + (i - T13 - T9); }
         else { x = 2.0 * (i - T13 - T9 - THI) / 65536.0; dst = Tlo + (i - T13 - T9 - THI); }
         double sn, cs;
@@ -269,6 +287,7 @@ __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, in
         else return p;
     };
     const float scale = 1.0f / (float)N;   // exact (power of two)
+    war_arrive<C>();
     for (int64_t f = blockIdx.x / C; f < nfft; f += gridDim.x / C) {
         // opaque per iteration: keeps the compiler from hoisting the 32
         // per-element addresses out of the persistent loop (and spilling them)
@@ -284,7 +303,7 @@ __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, in
 #pragma unroll
                 for (int n1 = 0; n1 < C; ++n1) v[i][n1] = ld_nc(x + n1 * FN2 + n2);
             }
-            csync<C>();   // every peer is done reading the shared memory we write
+            war_wait<C>();   // every peer is done reading the shared memory we write
             if constexpr (MODE == FFT_I) {
                 // T layout directly: X[m] goes to CTA m mod C at position m / C
 #pragma unroll
@@ -344,15 +363,19 @@ __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, in
                     for (int n1 = 0; n1 < C; ++n1) v[i][n1] = make_float2(v[i][n1].x * scale, v[i][n1].y * scale);
                 }
             }
+            // done reading peers' shared memory: the inverse gather's values were
+            // consumed by the DFT above; the plain transpose's by the stores below
+            if constexpr (MODE != FFT_F) war_arrive<C>();
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
                 const int n2 = c * (FN2 / C) + tid + FT * i;
 #pragma unroll
                 for (int n1 = 0; n1 < C; ++n1) st_cs(y + n1 * FN2 + n2, v[i][n1]);
             }
+            if constexpr (MODE == FFT_F) war_arrive<C>();
         }
     }
-    csync<C>();   // no CTA leaves while a peer may still read its shared memory
+    war_wait<C>();   // no CTA leaves while a peer may still read its shared memory
 }
 
 template <int C, int MODE>

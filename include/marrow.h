@@ -138,8 +138,21 @@ mw_status mw_kernel_fft(int32_t log2n, int32_t inverse, mw_node** out);
  * immutable and may be shared across runs and contexts.           */
 mw_status mw_pipeline(mw_node* const* stages, int32_t n, mw_node** out);  /* n >= 2 */
 mw_status mw_map(mw_node* tree, mw_node** out);
-enum { MW_MERGE_ADD = 0 };                    /* P:705-707; SUB/MUL/DIV: NEXT-4 */
-mw_status mw_map_reduce(mw_node* map_stage, int32_t merge_op, mw_node** out);
+/* Merging functions ("a set of predefined functions (addition,
+ * subtraction, multiplication and division) and also ... user-defined
+ * functions"; NEXT-4, reading R26).  ADD returns the canonical sum of all
+ * terms (chunk partials combined in global order: bit-identical for every
+ * distribution).  SUB / MUL / DIV / USER combine the per-partition partial
+ * results r_p (each partition's own reduction, partitions with work in
+ * global order): acc = r_first; acc = op(acc, r_p) — on the host, when the
+ * future completes; the result depends on the distribution by definition.
+ * MapReduce roots with SUB..USER cannot be captured in a graph.              */
+enum { MW_MERGE_ADD = 0, MW_MERGE_SUB = 1, MW_MERGE_MUL = 2, MW_MERGE_DIV = 3, MW_MERGE_USER = 4 };
+typedef double (*mw_merge_fn)(double acc, double partial, void* user);
+mw_status mw_map_reduce(mw_node* map_stage, int32_t merge_op, mw_node** out);   /* ADD..DIV */
+/* User-defined merging function (called on the host thread that waits on the
+ * future; fn must not call back into libmarrow).                           */
+mw_status mw_map_reduce_user(mw_node* map_stage, mw_merge_fn fn, void* user, mw_node** out);
 mw_status mw_loop_for(mw_node* body, int64_t n, mw_node** out);           /* n >= 0 */
 /* while(changed && executions < max_iters) body.
  * The stop condition is evaluated on the device and reduced across ranks
@@ -147,6 +160,20 @@ mw_status mw_loop_for(mw_node* body, int64_t n, mw_node** out);           /* n >
  * point are no-ops and the reported execution count E is exact.            */
 mw_status mw_loop_while_changed(mw_node* body, int64_t max_iters, int32_t check_every,
                                 mw_node** out);
+/* Loop with a host-side condition / state update ("1 - evaluation
+ * of the condition, on the host; 2 - execution of the body (the SCT), on the
+ * device(s); and 3 - the update of the loop's state ... (also performed on
+ * the host)"; NEXT-4, reading R27).  Before iteration i (0-based, i <
+ * max_iters) the library synchronizes the run's stream and calls
+ * cond(i, user) on the calling thread; 0 ends the loop.  The callback may
+ * read or write host state (stage 3).  Iteration i reads the previous
+ * iteration's output (ping-pong; src -> dst for i = 0), so a body of k
+ * iterations equals loop_for(body, k).  Executions are reported like
+ * LoopWhileChanged's.  Root-only (nested: MW_E_UNSUPPORTED); not capturable.
+ * mw_run returns after the last condition evaluation.                        */
+typedef int32_t (*mw_loop_cond_fn)(int64_t iteration, void* user);
+mw_status mw_loop_host(mw_node* body, int64_t max_iters, mw_loop_cond_fn cond, void* user,
+                       mw_node** out);
 void mw_node_retain(mw_node* n);
 void mw_node_release(mw_node* n);
 /* Deterministic content hash (SHA-256 of a canonical serialization): equal

@@ -78,8 +78,12 @@ class Map(Node):
 
 @dataclass
 class MapReduce(Node):
+    """op: '+' (the canonical sum of all terms) or, NEXT-4 (P:705-707,
+    DESIGN.md R26), '-', '*', '/' or a callable fn(acc, partial): the
+    per-partition partial results r_p (partitions with work, global order)
+    merged left to right — evaluate() then needs the partition lengths."""
     map_stage: Node
-    op: str = "+"
+    op: object = "+"
 
 
 @dataclass
@@ -92,6 +96,15 @@ class LoopFor(Node):
 class LoopWhileChanged(Node):
     body: Node
     max_iters: int
+
+
+@dataclass
+class LoopHost(Node):
+    """NEXT-4 (P:374-378 stages 1 and 3 on the host, R27): before iteration i
+    cond(i) is evaluated on the host; False ends the loop."""
+    body: Node
+    max_iters: int
+    cond: object = None
 
 
 @dataclass
@@ -124,7 +137,7 @@ def sig(node: Node):
         if o != TERMS:
             raise ValueError("MapReduce map stage must produce terms")
         return i, "scalar"
-    if isinstance(node, (LoopFor, LoopWhileChanged)):
+    if isinstance(node, (LoopFor, LoopWhileChanged, LoopHost)):
         i, o = sig(node.body)
         if not _compat(i, o):
             raise ValueError("loop body must preserve its value kind")
@@ -176,12 +189,28 @@ def _leaf(node: Leaf, v):
     raise ValueError(k)
 
 
-def evaluate(node: Node, value, while_counts=None) -> Result:
-    """Depth-first evaluation of `node` on `value` (whole domain)."""
+def _merge(op, parts):
+    acc = parts[0]
+    for r in parts[1:]:
+        if op == "-":
+            acc = acc - r
+        elif op == "*":
+            acc = acc * r
+        elif op == "/":
+            acc = acc / r
+        else:
+            acc = op(acc, r)
+    return acc
+
+
+def evaluate(node: Node, value, while_counts=None, lengths=None) -> Result:
+    """Depth-first evaluation of `node` on `value` (whole domain).  lengths:
+    the partition lengths (outer units, global order) — used only by the
+    partition-dependent NEXT-4 merging functions."""
     if isinstance(node, Leaf):
         return _leaf(node, value)
     if isinstance(node, Map):
-        return evaluate(node.tree, value)
+        return evaluate(node.tree, value, lengths=lengths)
     if isinstance(node, Pipeline):
         r = Result(value)
         any_changed = False
@@ -191,20 +220,29 @@ def evaluate(node: Node, value, while_counts=None) -> Result:
         r.changed = any_changed
         return r
     if isinstance(node, MapReduce):
-        if node.op != "+":
-            raise NotImplementedError("merge ops other than + are NEXT-4")
         m = node.map_stage
         while isinstance(m, Map):
             m = m.tree
         if not isinstance(m, Leaf):
             raise NotImplementedError("MapReduce map stage must be a map leaf")
-        if m.kind == "map_identity":
-            (x,) = value if isinstance(value, tuple) else (value,)
-            return Result(None, reduced=K.sum_(x))
-        if m.kind == "map_product":
-            x, y = value
-            return Result(None, reduced=K.dot(x, y))
-        raise ValueError(m.kind)
+        if m.kind not in ("map_identity", "map_product"):
+            raise ValueError(m.kind)
+        vals = value if isinstance(value, tuple) else (value,)
+
+        def red(sl):
+            if m.kind == "map_identity":
+                return K.sum_(vals[0][sl])
+            return K.dot(vals[0][sl], vals[1][sl])
+        if node.op == "+":
+            return Result(None, reduced=red(slice(None)))
+        if lengths is None:
+            raise ValueError("merging functions other than + need the partition lengths")
+        parts, o = [], 0
+        for ln in lengths:
+            if ln > 0:
+                parts.append(red(slice(o, o + ln)))
+            o += ln
+        return Result(None, reduced=_merge(node.op, parts))
     if isinstance(node, LoopFor):
         r = Result(value)
         for _ in range(node.n):
@@ -217,6 +255,15 @@ def evaluate(node: Node, value, while_counts=None) -> Result:
             v, changed = r.value, r.changed
             e += 1
         return Result(v, executions=e, converged=not changed)
+    if isinstance(node, LoopHost):
+        e, v, stopped = 0, value, False
+        while e < node.max_iters:
+            if not node.cond(e):       # stage 1 on the host
+                stopped = True
+                break
+            v = evaluate(node.body, v).value
+            e += 1
+        return Result(v, executions=e, converged=stopped)
     raise TypeError(node)
 
 
@@ -243,7 +290,7 @@ def kernel_execution_order(node: Node, while_counts: list[int]) -> list[int]:
         return 1 if isinstance(n, Leaf) else sum(nleaves(c) for c in _children(n))
 
     def nwhile(n):
-        return int(isinstance(n, LoopWhileChanged)) + sum(nwhile(c) for c in _children(n))
+        return int(isinstance(n, (LoopWhileChanged, LoopHost))) + sum(nwhile(c) for c in _children(n))
 
     if len(counts) < nwhile(node):
         raise KeyError("MissingIterationCount")
@@ -253,7 +300,7 @@ def kernel_execution_order(node: Node, while_counts: list[int]) -> list[int]:
             return [lb]
         if isinstance(n, LoopFor):
             return walk(n.body, lb, wb) * n.n
-        if isinstance(n, LoopWhileChanged):
+        if isinstance(n, (LoopWhileChanged, LoopHost)):
             return walk(n.body, lb, wb + 1) * counts[wb]
         out = []
         for c in _children(n):

@@ -115,6 +115,12 @@ struct mw_future {
     double executions = 0.0;
     double converged = 1.0;
     bool waited = false;
+    // MapReduce with a non-ADD merging function: per-partition partials (pinned)
+    double* parts = nullptr;
+    std::vector<char> part_active;
+    int32_t merge_op = 0;
+    mw_merge_fn merge_fn = nullptr;
+    void* merge_user = nullptr;
 };
 
 namespace {
@@ -989,8 +995,12 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
 }
 
 // ------------------------------------------------------------ the run
+mw_status run_loop_host(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
+                        mw_future* f);
+
 mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
               mw_future* f) {
+    if (root->type == mw::NodeType::LoopHost) return run_loop_host(c, root, args, nargs, s, f);
     std::vector<Step> prog;
     MW_OK_OR_RETURN(mw::plan(root, &prog));
     const int ik = root->in_kind, ok = root->out_kind;
@@ -1160,8 +1170,32 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         // one non-zero contributor, so the sum is exact and order-free.
         if (c->comm && nch > 0)
             NCCL_OK(ncclAllReduce(partials, partials, (size_t)nch, ncclFloat64, ncclSum, c->comm, s));
-        MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s), "reduce_combine"));
-        CUDA_OK(cudaMemcpyAsync(f->res, rp, 8, cudaMemcpyDeviceToHost, s));
+        if (prog[0].merge_op == MW_MERGE_ADD) {
+            MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s), "reduce_combine"));
+            CUDA_OK(cudaMemcpyAsync(f->res, rp, 8, cudaMemcpyDeviceToHost, s));
+        } else {
+            // NEXT-4 merging functions: every rank holds every chunk partial after
+            // the all-reduce, so each forms all P partition partials (same fixed
+            // tree as the canonical combine, over the partition's chunk range)
+            if (c->capturing)
+                return fail(MW_E_UNSUPPORTED, "MapReduce with a non-ADD merge is merged on the host "
+                                              "and cannot be captured in a graph");
+            void* dp;
+            MW_OK_OR_RETURN(scratch(c, "part_partials", (size_t)c->P * 8, s, &dp));
+            double* dparts = static_cast<double*>(dp);
+            f->part_active.assign(c->P, 0);
+            for (int p = 0; p < c->P; ++p) {
+                if (R.len[p] == 0) continue;
+                const int64_t c0 = R.off[p] / CH, c1 = (R.off[p] + R.len[p] + CH - 1) / CH;
+                MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials + c0, c1 - c0, dparts + p, s), "reduce_combine"));
+                f->part_active[p] = 1;
+            }
+            CUDA_OK(cudaHostAlloc(&f->parts, (size_t)c->P * 8, cudaHostAllocDefault));
+            CUDA_OK(cudaMemcpyAsync(f->parts, dparts, (size_t)c->P * 8, cudaMemcpyDeviceToHost, s));
+            f->merge_op = prog[0].merge_op;
+            f->merge_fn = reinterpret_cast<mw_merge_fn>(prog[0].fn);
+            f->merge_user = prog[0].user;
+        }
         f->has_reduce = true;
     } else if (ik == MW_VK_CPLX) {
         const std::vector<mw::ChainOp> none;
@@ -1194,6 +1228,55 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         c->last_len = R.len;
         c->have_run = true;
     }
+    return MW_OK;
+}
+
+// Loop with a host-side condition (NEXT-4, reading R27): stage 1
+// (the condition) and stage 3 (state update) run on the host between body
+// executions; stage 2 (the body) runs through run().  Value kinds with a
+// separate output ping-pong through a scratch copy of this rank's rows.
+mw_status run_loop_host(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
+                        mw_future* f) {
+    if (c->capturing)
+        return fail(MW_E_UNSUPPORTED, "a host-condition loop evaluates its condition on the host "
+                                      "and cannot be captured in a graph");
+    for (int i = 0; i < nargs; ++i)
+        if (args[i].location == MW_LOC_HOST)
+            return fail(MW_E_UNSUPPORTED, "host-condition loops take device-resident arguments");
+    const Node* body = root->kids[0];
+    auto cond = reinterpret_cast<mw_loop_cond_fn>(root->fn);
+    const int ik = body->in_kind;
+    const bool two = nargs == 2 && (ik == MW_VK_RGBA || ik == MW_VK_U8 || ik == MW_VK_U8_2D ||
+                                    ik == MW_VK_CPLX);
+    std::vector<mw_arg> cur(args, args + nargs);
+    void* tmp = nullptr;
+    size_t tbytes = 0;
+    if (two) {
+        tbytes = (size_t)(args[1].local_rows * row_bytes(args[1]));
+        MW_OK_OR_RETURN(scratch(c, "loop_host_tmp", std::max<size_t>(tbytes, 16), s, &tmp));
+    }
+    int64_t E = 0;
+    bool stopped = false;
+    for (int64_t it = 0; it < root->n; ++it) {
+        CUDA_OK(cudaStreamSynchronize(s));   // stage 3 of the previous iteration is visible
+        if (!cond(it, root->user)) {
+            stopped = true;
+            break;
+        }
+        if (two && it > 0) {   // input of iteration it = output of it - 1
+            CUDA_OK(cudaMemcpyAsync(tmp, args[1].ptr, tbytes, cudaMemcpyDeviceToDevice, s));
+            cur[0] = args[1];
+            cur[0].ptr = tmp;
+        }
+        MW_OK_OR_RETURN(run(c, body, cur.data(), nargs, s, f));
+        ++E;
+    }
+    if (two && E == 0 && args[0].ptr != args[1].ptr)   // no iteration: the loop is the identity
+        CUDA_OK(cudaMemcpyAsync(args[1].ptr, static_cast<const uint8_t*>(args[0].ptr) +
+                                                 (args[1].local_offset - args[0].local_offset) * row_bytes(args[0]),
+                                tbytes, cudaMemcpyDeviceToDevice, s));
+    f->executions += (double)E;
+    if (!stopped) f->converged = 0.0;
     return MW_OK;
 }
 
@@ -1416,8 +1499,27 @@ mw_status mw_future_result(mw_future* f, double* out, int32_t n) {
         ex += (double)st[0];
         if (!st[1]) conv = 0.0;
     }
-    double v[4] = {f->has_reduce ? *f->res : 0.0, (double)(float)(f->has_reduce ? *f->res : 0.0),
-                   ex, conv};
+    double red = f->has_reduce ? *f->res : 0.0;
+    if (f->parts) {   // merging function over the partitions with work, in global order
+        bool first = true;
+        red = 0.0;
+        for (size_t p = 0; p < f->part_active.size(); ++p) {
+            if (!f->part_active[p]) continue;
+            const double r = f->parts[p];
+            if (first) {
+                red = r;
+                first = false;
+                continue;
+            }
+            switch (f->merge_op) {
+                case MW_MERGE_SUB: red = red - r; break;
+                case MW_MERGE_MUL: red = red * r; break;
+                case MW_MERGE_DIV: red = red / r; break;
+                default: red = f->merge_fn(red, r, f->merge_user); break;
+            }
+        }
+    }
+    double v[4] = {red, (double)(float)red, ex, conv};
     for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
     return MW_OK;
 }
@@ -1429,6 +1531,7 @@ void mw_future_release(mw_future* f) {
         cudaEventDestroy(f->done);
     }
     if (f->res) f->ctx->res_free.push_back(f->res);
+    if (f->parts) cudaFreeHost(f->parts);
     mw_ctx* c = f->ctx;
     delete f;
     ctx_release(c);

@@ -69,8 +69,11 @@ std::string canonical(const Node* n) {
             return s + ")";
         }
         case NodeType::Map: return "M(" + canonical(n->kids[0]) + ")";
-        case NodeType::MapReduce:
-            snprintf(buf, sizeof buf, "R(%d;", n->merge_op);
+        case NodeType::MapReduce:   // a user merge hashes by function address
+            snprintf(buf, sizeof buf, "R(%d;%p;", n->merge_op, n->merge_op == MW_MERGE_USER ? n->fn : nullptr);
+            return buf + canonical(n->kids[0]) + ")";
+        case NodeType::LoopHost:
+            snprintf(buf, sizeof buf, "H(%" PRId64 ";%p;", n->n, n->fn);
             return buf + canonical(n->kids[0]) + ")";
         case NodeType::LoopFor:
             snprintf(buf, sizeof buf, "F(%" PRId64 ";", n->n);
@@ -200,6 +203,9 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
             Step s;
             s.kind = StepKind::Reduce;
             s.dot = a[0].dot;
+            s.merge_op = n->merge_op;
+            s.fn = n->fn;
+            s.user = n->user;
             out->push_back(s);
             return MW_OK;
         }
@@ -240,6 +246,8 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
             out->push_back(s);
             return MW_OK;
         }
+        case NodeType::LoopHost:
+            return fail(MW_E_UNSUPPORTED, "a host-condition loop (mw_loop_host) must be the root of the run");
         default: break;
     }
     return fail(MW_E_INVALID_SPEC, "unknown node type");
@@ -581,12 +589,13 @@ static mw_status make_comp(NodeType t, mw_node* const* kids, int n, mw_node** ou
         case NodeType::MapReduce:
             if (ks[0]->out_kind != MW_VK_TERMS)
                 return fail(MW_E_INVALID_SPEC, "MapReduce map stage must produce terms");
-            if (op != MW_MERGE_ADD)
-                return fail(MW_E_UNSUPPORTED, "only the + merging function is built (NEXT-4)");
+            if (op < MW_MERGE_ADD || op > MW_MERGE_USER)
+                return fail(MW_E_INVALID_SPEC, "unknown merging function");
             out_kind = MW_VK_SCALAR;
             break;
         case NodeType::LoopFor:
         case NodeType::LoopWhile:
+        case NodeType::LoopHost:
             if (!mw::compat(ks[0]->in_kind, ks[0]->out_kind))
                 return fail(MW_E_INVALID_SPEC, "loop body must preserve its value kind");
             if (cnt < 0) return fail(MW_E_INVALID_SPEC, "loop count must be >= 0");
@@ -618,7 +627,28 @@ mw_status mw_map(mw_node* tree, mw_node** out) {
     return make_comp(NodeType::Map, &tree, 1, out, 0, 1, 0);
 }
 mw_status mw_map_reduce(mw_node* map_stage, int32_t merge_op, mw_node** out) {
+    if (merge_op == MW_MERGE_USER)
+        return fail(MW_E_INVALID_SPEC, "MW_MERGE_USER needs mw_map_reduce_user (a function)");
     return make_comp(NodeType::MapReduce, &map_stage, 1, out, 0, 1, merge_op);
+}
+mw_status mw_map_reduce_user(mw_node* map_stage, mw_merge_fn fn, void* user, mw_node** out) {
+    if (!fn) return fail(MW_E_INVALID_SPEC, "NULL merging function");
+    mw_status st = make_comp(NodeType::MapReduce, &map_stage, 1, out, 0, 1, MW_MERGE_USER);
+    if (st) return st;
+    Node* nd = reinterpret_cast<Node*>(*out);
+    nd->fn = reinterpret_cast<void*>(fn);
+    nd->user = user;
+    return MW_OK;
+}
+mw_status mw_loop_host(mw_node* body, int64_t max_iters, mw_loop_cond_fn cond, void* user,
+                       mw_node** out) {
+    if (!cond) return fail(MW_E_INVALID_SPEC, "NULL loop condition");
+    mw_status st = make_comp(NodeType::LoopHost, &body, 1, out, max_iters, 1, 0);
+    if (st) return st;
+    Node* nd = reinterpret_cast<Node*>(*out);
+    nd->fn = reinterpret_cast<void*>(cond);
+    nd->user = user;
+    return MW_OK;
 }
 mw_status mw_loop_for(mw_node* body, int64_t n, mw_node** out) {
     return make_comp(NodeType::LoopFor, &body, 1, out, n, 1, 0);
@@ -653,7 +683,7 @@ static int64_t count_leaves(const Node* n) {
     return c;
 }
 static int64_t count_while(const Node* n) {
-    int64_t c = n->type == NodeType::LoopWhile ? 1 : 0;
+    int64_t c = (n->type == NodeType::LoopWhile || n->type == NodeType::LoopHost) ? 1 : 0;
     for (const Node* k : n->kids) c += count_while(k);
     return c;
 }
@@ -670,6 +700,7 @@ static mw_status exec_order(const Node* n, int64_t lb, int64_t wb, const int64_t
             }
             return MW_OK;
         case NodeType::LoopWhile:
+        case NodeType::LoopHost:
             for (int64_t i = 0; i < wc[wb]; ++i) {
                 mw_status st = exec_order(n->kids[0], lb, wb + 1, wc, out);
                 if (st) return st;

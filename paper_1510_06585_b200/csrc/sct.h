@@ -18,7 +18,7 @@ void set_error(const std::string& msg);
 mw_status fail(mw_status code, const std::string& msg);
 
 // ------------------------------------------------------------ tree
-enum class NodeType { Leaf, Pipeline, Map, MapReduce, LoopFor, LoopWhile };
+enum class NodeType { Leaf, Pipeline, Map, MapReduce, LoopFor, LoopWhile, LoopHost };
 enum class LeafKind {
     Saxpy, GaussNoise, Solarize, Mirror, Segment, HystStep, HystFinalize,
     NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits, Fft
@@ -36,6 +36,8 @@ struct Node {
     int64_t n = 0;                     // LoopFor count | LoopWhile max_iters
     int32_t check_every = 1;
     int32_t merge_op = 0;
+    void* fn = nullptr;                // MapReduce USER merge | LoopHost condition
+    void* user = nullptr;
     int32_t in_kind = 0, out_kind = 0; // MW_VK_*
 };
 
@@ -66,6 +68,9 @@ struct Step {
     bool dot = false;
     int64_t epu = 1, nu = 1;
     bool strict = false;
+    int32_t merge_op = 0;              // Reduce: MW_MERGE_*
+    void* fn = nullptr;
+    void* user = nullptr;
 };
 mw_status plan(const Node* root, std::vector<Step>* out);
 

@@ -18,7 +18,10 @@ MW_OK = 0
 (MW_E_INVALID_SPEC, MW_E_EPU_NU, MW_E_INFEASIBLE_PARTITION, MW_E_SHAPE_MISMATCH,
  MW_E_MISSING_ITERATION_COUNT, MW_E_NOT_CONVERGED, MW_E_CUDA, MW_E_NCCL, MW_E_STATE,
  MW_E_OOM, MW_E_UNSUPPORTED) = range(1, 12)
-MW_MERGE_ADD = 0
+MW_MERGE_ADD, MW_MERGE_SUB, MW_MERGE_MUL, MW_MERGE_DIV, MW_MERGE_USER = range(5)
+# host callbacks (NEXT-4): merging function and host-side loop condition
+_MERGE_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
+_COND_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p)
 (MW_VK_SAXPY, MW_VK_RGBA, MW_VK_U8, MW_VK_U8_2D, MW_VK_NBODY, MW_VK_VEC1, MW_VK_VEC2,
  MW_VK_TERMS, MW_VK_ACCEL, MW_VK_TRAITS, MW_VK_SCALAR, MW_VK_CPLX) = range(1, 13)
 MW_DT_U8, MW_DT_F32, MW_DT_F64, MW_DT_I64 = 1, 2, 3, 4
@@ -96,6 +99,8 @@ _SIG = {
     "mw_pipeline": [_P(_vp), _i32, _node_pp],
     "mw_map": [_vp, _node_pp],
     "mw_map_reduce": [_vp, _i32, _node_pp],
+    "mw_map_reduce_user": [_vp, _MERGE_FN, _vp, _node_pp],
+    "mw_loop_host": [_vp, _i64, _COND_FN, _vp, _node_pp],
     "mw_loop_for": [_vp, _i64, _node_pp],
     "mw_loop_while_changed": [_vp, _i64, _i32, _node_pp],
     "mw_node_retain": [_vp],
@@ -275,6 +280,20 @@ def mw_loop_for(body, n):
 
 def mw_loop_while_changed(body, max_iters, check_every=1):
     return _new("mw_loop_while_changed", body.ptr, max_iters, check_every, kids=(body,))
+
+
+def mw_map_reduce_user(map_stage, fn):
+    """MapReduce with a user-defined merging function fn(acc, partial) -> float
+    over the per-partition partial results (NEXT-4)."""
+    cb = _MERGE_FN(lambda acc, part, _u: float(fn(acc, part)))
+    return _new("mw_map_reduce_user", map_stage.ptr, cb, None, kids=(map_stage, cb))
+
+
+def mw_loop_host(body, max_iters, cond):
+    """Loop whose condition cond(iteration) -> bool runs on the host before
+    every iteration (P:374-378 stages 1 and 3; NEXT-4)."""
+    cb = _COND_FN(lambda it, _u: 1 if cond(it) else 0)
+    return _new("mw_loop_host", body.ptr, max_iters, cb, None, kids=(body, cb))
 
 
 def mw_node_id(node) -> bytes:

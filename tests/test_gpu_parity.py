@@ -781,3 +781,106 @@ def test_fft_host_staged_and_graph():
         g.launch(s)
         s.synchronize()
     assert torch.equal(out, ref)
+
+
+# ----------------------------------------------------------------- NEXT-4 variants
+def _merge_ref(op, parts):
+    acc = parts[0]
+    for r in parts[1:]:
+        acc = (acc - r if op == M.MW_MERGE_SUB else acc * r if op == M.MW_MERGE_MUL
+               else acc / r if op == M.MW_MERGE_DIV else op(acc, r))
+    return acc
+
+
+@pytest.mark.parametrize("dot", [False, True])
+def test_mapreduce_merge_functions(dot):
+    """P:705-707 merging functions (R26): per-partition partials merged in
+    partition order; each compared with the oracle's partition-aware
+    evaluation within a first-order propagated fp64 bound."""
+    n = 7 * (1 << 16) + 311
+    x = synth.np_f32_um11(5, 0, n)
+    y = synth.np_f32_um11(6, 0, n)
+    xd, yd = dev(x), dev(y)
+    args = [M.arg(xd), M.arg(yd)] if dot else [M.arg(xd)]
+    stage = M.mw_kernel_map_product() if dot else M.mw_kernel_map_identity()
+    ostage = sct.Leaf("map_product" if dot else "map_identity")
+    user = lambda a, r: 0.5 * a + r   # noqa: E731  (order-sensitive)
+    for d in ([0.5, 0.25, 0.25], [0.2, 0.0, 0.8], [1.0, 0.0, 0.0]):
+        c = ctx(3, d)
+        off, lens = M.mw_partition(c, stage, n)
+        for op in (M.MW_MERGE_SUB, M.MW_MERGE_MUL, M.MW_MERGE_DIV, user):
+            node = M.mw_map_reduce_user(stage, op) if callable(op) else M.mw_map_reduce(stage, op)
+            got = run(c, node, args)["reduced"]
+            oop = op if callable(op) else {M.MW_MERGE_SUB: "-", M.MW_MERGE_MUL: "*", M.MW_MERGE_DIV: "/"}[op]
+            want = sct.evaluate(sct.MapReduce(ostage, oop), (x, y) if dot else (x,), lengths=lens).reduced
+            # first-order bound: partial p is within 1e-13 * sum|terms_p| of exact
+            parts, tol, o = [], [], 0
+            for ln in lens:
+                if ln:
+                    sl = slice(o, o + ln)
+                    terms = x[sl].astype(np.float64) * (y[sl].astype(np.float64) if dot else 1.0)
+                    parts.append(float(np.sum(terms)))
+                    tol.append(1e-13 * float(np.sum(np.abs(terms))))
+                o += ln
+            bound = 0.0
+            for p in range(len(parts)):
+                h = tol[p]
+                q = list(parts)
+                q[p] += h
+                bound += abs(_merge_ref(op, q) - _merge_ref(op, parts)) if h else 0.0
+            assert abs(got - want) <= 2 * bound + 1e-300, (d, op, got, want, bound)
+        c.destroy()
+    # ADD keeps the canonical, distribution-independent sum
+    r1 = run(ctx(3, [0.2, 0.0, 0.8]), M.mw_map_reduce(stage, M.MW_MERGE_ADD), args)["reduced"]
+    r2 = run(ctx(1), M.mw_map_reduce(stage, M.MW_MERGE_ADD), args)["reduced"]
+    assert r1 == r2
+
+
+def test_loop_host_condition():
+    """P:374-378: condition (stage 1) and state update (stage 3) on the host;
+    a loop stopped at k by its host condition equals loop_for(body, k)."""
+    img = synth.np_rgba(3, 0, 40 * 256).reshape(40, 256, 4)
+    src = dev(img)
+    for k, dist in ((0, [1.0]), (1, [0.5, 0.5]), (3, [0.3, 0.7])):
+        c = ctx(len(dist), dist)
+        calls = []
+        dst = torch.empty_like(src)
+        r = run(c, M.mw_loop_host(trees.filter_pipeline(), 50, lambda i: (calls.append(i), i < k)[1]),
+                [M.arg(src), M.arg(dst)])
+        ref = torch.empty_like(src)
+        run(c, M.mw_loop_for(trees.filter_pipeline(), k), [M.arg(src), M.arg(ref)])
+        assert torch.equal(dst, ref) and r["executions"] == k and r["converged"], k
+        assert calls == list(range(k + 1))
+        want = sct.evaluate(sct.LoopFor(sct.Pipeline([sct.Leaf("gauss_noise", {"seed": 4, "scale": 8}),
+                                                       sct.Leaf("solarize", {"threshold": 128}),
+                                                       sct.Leaf("mirror")]), k), img).value
+        assert np.array_equal(dst.cpu().numpy(), want)
+    # in-place state (saxpy): the host update reads the device state each iteration
+    c = ctx(2)
+    x = dev(synth.np_f32_um11(1, 0, 4099))
+    y0 = synth.np_f32_um11(2, 0, 4099)
+    y = dev(y0)
+    seen = []
+
+    def cond(i):
+        seen.append(float(y[7]))   # stage 3: state read on the host between iterations
+        return i < 4
+    r = run(c, M.mw_loop_host(trees.saxpy(0.5), 100, cond), [M.arg(x), M.arg(y)])
+    want = y0
+    for _ in range(4):
+        want = K.saxpy(0.5, synth.np_f32_um11(1, 0, 4099), want)
+    assert np.array_equal(y.cpu().numpy(), want) and r["executions"] == 4 and len(seen) == 5
+    # max_iters reached -> not converged; a hysteresis step body (stencil, ping-pong)
+    gray = synth.np_u8_stream(8, 0, 60 * 90).reshape(60, 90)
+    L = K.segment(gray, 173, 250)
+    dst = torch.empty((60, 90), dtype=torch.uint8, device=DEV)
+    r = run(ctx(3), M.mw_loop_host(M.mw_kernel_hysteresis_step(), 4, lambda i: True), [M.arg(dev(L)), M.arg(dst)])
+    assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, 4)[0]) and r["executions"] == 4 and not r["converged"]
+    # not capturable; not nestable
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with pytest.raises(M.MwError):
+            M.mw_graph_capture(ctx(1), M.mw_loop_host(trees.saxpy(0.5), 3, lambda i: True), [M.arg(x), M.arg(y)], s)
+    with pytest.raises(M.MwError):
+        run(ctx(1), M.mw_pipeline([M.mw_loop_host(M.mw_kernel_mirror(), 2, lambda i: True), M.mw_kernel_mirror()]),
+            [M.arg(src), M.arg(torch.empty_like(src))])

@@ -40,9 +40,12 @@ def test_status_strings_and_errors():
         M.mw_kernel_segment(10, 5)
     with pytest.raises(M.MwError):
         M.mw_kernel_gauss_noise(1, 300)
-    with pytest.raises(M.MwError) as e:
-        M.mw_map_reduce(M.mw_kernel_map_identity(), 1)
-    assert e.value.status == M.MW_E_UNSUPPORTED
+    for bad in (7, -1, M.MW_MERGE_USER):   # USER needs mw_map_reduce_user (a function)
+        with pytest.raises(M.MwError) as e:
+            M.mw_map_reduce(M.mw_kernel_map_identity(), bad)
+        assert e.value.status == M.MW_E_INVALID_SPEC
+    with pytest.raises(M.MwError):
+        M.mw_loop_host(M.mw_kernel_mirror(), -1, lambda i: True)   # negative max_iters
     with pytest.raises(M.MwError):
         M.mw_loop_while_changed(M.mw_kernel_hysteresis_step(), 10, 0)
     for bad in (12, 17, 0):   # FFT sizes 2^13..2^16 (R23)
@@ -63,6 +66,13 @@ def test_signatures():
     assert M.mw_node_signature(trees.fft_pipeline()) == (M.MW_VK_CPLX, M.MW_VK_CPLX)
     assert M.mw_node_id(trees.fft_pipeline(16)) != M.mw_node_id(trees.fft_pipeline(15))
     assert M.mw_kernel_execution_order(M.mw_loop_for(trees.fft_pipeline(), 2), []) == [0, 1, 0, 1]
+    # a host-condition loop takes its count like a while-loop (known after the run)
+    lh = M.mw_loop_host(trees.filter_pipeline(), 10, lambda i: i < 2)
+    assert M.mw_kernel_execution_order(lh, [2]) == [0, 1, 2, 0, 1, 2]
+    assert M.mw_node_signature(M.mw_map_reduce(M.mw_kernel_map_product(), M.MW_MERGE_DIV)) == \
+        (M.MW_VK_VEC2, M.MW_VK_SCALAR)
+    assert M.mw_node_id(M.mw_map_reduce(M.mw_kernel_map_identity(), M.MW_MERGE_SUB)) != \
+        M.mw_node_id(M.mw_map_reduce(M.mw_kernel_map_identity(), M.MW_MERGE_MUL))
 
 
 def test_node_id_determinism():

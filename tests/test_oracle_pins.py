@@ -705,3 +705,50 @@ def test_fft_tolerance_formula():
     # Higham Thm 24.2 shape: grows with log2 N and the number of stages
     assert FF.tolerance(1 << 16, 1) < FF.tolerance(1 << 16, 2) < 2 * FF.tolerance(1 << 16, 1) + 1e-7
     assert FF.tolerance(1 << 13, 1) < FF.tolerance(1 << 16, 1) < 1e-5
+
+
+# ----------------------------------------------------------------- NEXT-4 variants
+def test_merge_functions_pinned_to_exact_partials():
+    """P:705-707 merging functions over per-partition partials (R26): each
+    partial is pinned to math.fsum (exactly rounded), then merged in order."""
+    n = 5 * (1 << 16) + 123
+    x = synth.np_f32_um11(5, 0, n)
+    y = synth.np_f32_um11(6, 0, n)
+    lengths = [2 << 16, 0, 1 << 16, (2 << 16) + 123]
+    xs = x.astype(np.float64)
+    ex, ed, o = [], [], 0
+    for ln in lengths:
+        if ln:
+            ex.append(math.fsum(xs[o:o + ln]))
+            ed.append(math.fsum(xs[o:o + ln] * y[o:o + ln].astype(np.float64)))
+        o += ln
+    ident = sct.Leaf("map_identity")
+    prod = sct.Leaf("map_product")
+    for op, f in (("-", lambda a, b: a - b), ("*", lambda a, b: a * b), ("/", lambda a, b: a / b),
+                  (lambda a, b: 2 * a + b, lambda a, b: 2 * a + b)):
+        want_s, want_d = ex[0], ed[0]
+        for a, b in zip(ex[1:], ed[1:]):
+            want_s, want_d = f(want_s, a), f(want_d, b)
+        got_s = sct.evaluate(sct.MapReduce(ident, op), (x,), lengths=lengths).reduced
+        got_d = sct.evaluate(sct.MapReduce(prod, op), (x, y), lengths=lengths).reduced
+        assert abs(got_s - want_s) <= 1e-12 * max(1.0, abs(want_s))
+        assert abs(got_d - want_d) <= 1e-12 * max(1.0, abs(want_d))
+    # '+' ignores the partitioning (the canonical sum)
+    assert abs(sct.evaluate(sct.MapReduce(ident, "+"), (x,)).reduced - math.fsum(xs)) < 1e-9
+
+
+def test_loop_host_reduces_to_loop_for():
+    """a host condition that stops at k equals loop_for(body, k)."""
+    img = synth.np_rgba(3, 0, 8 * 16).reshape(8, 16, 4)
+    body = sct.Pipeline([sct.Leaf("gauss_noise", {"seed": 4, "scale": 8}),
+                         sct.Leaf("mirror")])
+    seen = []
+    for k in (0, 1, 3):
+        seen.clear()
+        r = sct.evaluate(sct.LoopHost(body, 10, lambda i: (seen.append(i), i < k)[1]), img)
+        want = sct.evaluate(sct.LoopFor(body, k), img).value
+        assert np.array_equal(r.value, want) and r.executions == k and r.converged
+        assert seen == list(range(k + 1))
+    r = sct.evaluate(sct.LoopHost(body, 2, lambda i: True), img)
+    assert r.executions == 2 and not r.converged
+    assert sct.kernel_execution_order(sct.LoopHost(body, 9, None), [2]) == [0, 1, 0, 1]

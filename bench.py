@@ -148,6 +148,41 @@ class Workload:
     def sets_for(self, ws_bytes):
         return max(1, math.ceil(2 * self.l2 / max(1, ws_bytes)))
 
+    # ---- end-to-end leg (the public API with host data every step)
+    e2e_mode = None          # "staged": mw_run on pinned HOST args (library overlap);
+    e2e_in, e2e_out = (), ()  # "explicit": H2D of sets[0][e2e_in], mw_run, D2H of e2e_out
+
+    def _host_arg(self, a):
+        t = a._owner
+        h = self.torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory()
+        h.copy_(t)
+        return self.M.arg(h, a.mode, local_offset=a.local_offset,
+                          global_shape=tuple(a.shape[i] for i in range(a.ndim)))
+
+    def e2e_setup(self):
+        st = self.sets[0]
+        nbytes = lambda t: t.numel() * t.element_size()   # noqa: E731
+        h2d = sum(nbytes(st[i]._owner) for i in self.e2e_in)
+        d2h = sum(nbytes(st[i]._owner) for i in self.e2e_out) if self.e2e_out else 8   # or one fp64
+        if self.e2e_mode == "staged":
+            self.e2e_args = [self._host_arg(a) for a in st]
+            return h2d, d2h
+        self.e2e_h_in = [(self._host_arg(st[i])._owner, st[i]._owner) for i in self.e2e_in]
+        self.e2e_h_out = [(st[i]._owner, self.torch.empty(tuple(st[i]._owner.shape),
+                                                          dtype=st[i]._owner.dtype).pin_memory())
+                          for i in self.e2e_out]
+        return h2d, d2h
+
+    def e2e_step(self):
+        if self.e2e_mode == "staged":
+            return self.M.mw_run(self.ctx, self.tree, self.e2e_args)
+        for h, d in self.e2e_h_in:
+            d.copy_(h, non_blocking=True)
+        f = self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
+        for d, h in self.e2e_h_out:
+            h.copy_(d, non_blocking=True)
+        return f
+
     def slice(self, L):
         off, ln = self.M.mw_partition(self.ctx, self.tree, L)
         k = len(off) // int(os.environ.get("WORLD_SIZE", "1"))   # this rank's partitions: contiguous
@@ -156,6 +191,7 @@ class Workload:
 
 class Filter(Workload):
     name, unit, dtype = "filter_pipeline_8192x8192_rgba8", "pixels/s", "u8"
+    e2e_mode, e2e_in, e2e_out = "staged", (0,), (1,)
 
     def setup(self, H=8192, W=8192):
         M, t = self.M, self.torch
@@ -180,19 +216,6 @@ class Filter(Workload):
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
 
-    def e2e_setup(self):
-        t = self.torch
-        hsrc = t.empty((self.n, self.W, 4), dtype=t.uint8).pin_memory()
-        hsrc.copy_(self.sets[0][0]._owner.cpu())
-        hdst = t.empty_like(hsrc).pin_memory()
-        g = (self.H, self.W, 4)
-        self.e2e_args = [self.M.arg(hsrc, local_offset=self.o, global_shape=g),
-                         self.M.arg(hdst, local_offset=self.o, global_shape=g)]
-        return self.n * self.W * 4, self.n * self.W * 4
-
-    def e2e_step(self):
-        return self.M.mw_run(self.ctx, self.tree, self.e2e_args)
-
     def roof_bytes(self, cls, launches, steps, res):
         return 8.0 * self.n * self.W * steps if cls == self.M.MW_KC_RGBA else 0.0   # this rank's rows
 
@@ -204,6 +227,7 @@ class Filter(Workload):
 
 class Saxpy(Workload):
     name, unit, dtype = "saxpy_map_2^20_fp32", "elements/s", "f32"
+    e2e_mode, e2e_in, e2e_out = "staged", (0, 1), (1,)
 
     def setup(self, n=1 << 20):
         M, t = self.M, self.torch
@@ -253,6 +277,7 @@ class Saxpy(Workload):
 
 class Segmentation(Workload):
     name, unit, dtype = "segmentation_1024x1024x512_u8", "voxels/s", "u8"
+    e2e_mode, e2e_in, e2e_out = "staged", (0,), (1,)
 
     def setup(self, shape=(512, 1024, 1024)):
         M, t = self.M, self.torch
@@ -287,10 +312,12 @@ class Segmentation(Workload):
 
 class MapReduce(Workload):
     unit, dtype = "elements/s", "f32"
+    e2e_mode, e2e_out = "explicit", ()
 
     def __init__(self, *a, dot=True):
         super().__init__(*a)
         self.dot = dot
+        self.e2e_in = (0, 1) if dot else (0,)
         self.name = f"mapreduce_{'dot' if dot else 'sum'}_2^30_fp32"
 
     def setup(self, n=1 << 30):
@@ -326,6 +353,7 @@ class MapReduce(Workload):
 
 class Hysteresis(Workload):
     name, unit, dtype = "hysteresis_16384x16384_u8", "pixels/s", "u8"
+    e2e_mode, e2e_in, e2e_out = "explicit", (0,), (1,)
 
     def __init__(self, *a, check_every=1):
         super().__init__(*a)
@@ -383,6 +411,7 @@ class Hysteresis(Workload):
 
 class NBody(Workload):
     name, unit, dtype, bound = "nbody_2^20", "bodies/s", "f32", "alu"
+    e2e_mode, e2e_in, e2e_out = "explicit", (0, 1), (0, 1)
 
     def setup(self, N=1 << 20):
         M, t = self.M, self.torch
@@ -432,6 +461,7 @@ class Fft(Workload):
     (65536-point complex64) FFTs, each pipelined with its inversion; one unit
     = one FFT -> IFFT of one epu.  256 MiB batch (512 transforms)."""
     name, unit, dtype = "fft_ifft_512x65536_c64", "ffts/s", "f32"
+    e2e_mode, e2e_in, e2e_out = "staged", (0,), (1,)
 
     def setup(self, B=512, log2n=16):
         M, t = self.M, self.torch
@@ -452,19 +482,6 @@ class Fft(Workload):
 
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
-
-    def e2e_setup(self):
-        t = self.torch
-        hsrc = t.empty((self.n, self.N, 2), dtype=t.float32).pin_memory()
-        hsrc.copy_(self.sets[0][0]._owner.cpu())
-        hdst = t.empty_like(hsrc).pin_memory()
-        g = (self.Bt, self.N, 2)
-        self.e2e_args = [self.M.arg(hsrc, local_offset=self.o, global_shape=g),
-                         self.M.arg(hdst, local_offset=self.o, global_shape=g)]
-        return self.n * self.N * 8, self.n * self.N * 8
-
-    def e2e_step(self):
-        return self.M.mw_run(self.ctx, self.tree, self.e2e_args)
 
     def roof_bytes(self, cls, launches, steps, res):
         # the fused FFT -> IFFT reads and writes each transform once: 2 x 512 KiB
@@ -715,7 +732,7 @@ def run_marrow(args, dist, wl_name):
         import math
         line["gflops_5nlogn"] = value * 2 * 5 * w.N * math.log2(w.N) / 1e9
     # end to end through the C-ABI with HOST buffers (H2D + run + D2H per step)
-    if hasattr(w, "e2e_setup"):
+    if w.e2e_mode:
         h2d, d2h = w.e2e_setup()
         ek = max(3, min(args.steps, 20))
         f = w.e2e_step()
@@ -730,8 +747,11 @@ def run_marrow(args, dist, wl_name):
         ems = dist.max(start.elapsed_time(stop))
         line["e2e"] = {"value": w.units * ek / (ems / 1e3), "unit": w.unit,
                        "h2d_bytes_per_step": h2d * dist.world, "d2h_bytes_per_step": d2h * dist.world,
-                       "steps": ek, "path": "mw_run with MW_LOC_HOST pinned buffers (chunked "
-                       "H2D/compute/D2H overlap on 3 streams)"}
+                       "steps": ek,
+                       "path": ("mw_run with MW_LOC_HOST pinned buffers (library-staged chunked "
+                                "H2D/compute/D2H overlap on 3 streams)" if w.e2e_mode == "staged" else
+                                "pinned H2D of the inputs + mw_run + D2H of the result on the run's "
+                                "stream (tree not host-stageable)")}
     else:
         line["e2e"] = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:

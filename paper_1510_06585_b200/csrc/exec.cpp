@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -100,6 +101,7 @@ struct mw_ctx {
     cudaStream_t copy_in = nullptr, copy_out = nullptr, aux = nullptr;
     cudaEvent_t st_in[kStageSlots]{}, st_comp[kStageSlots]{}, st_out[kStageSlots]{};
     cudaEvent_t st_start = nullptr;
+    bool st_valid[kStageSlots]{};   // slot has a recorded st_out (possibly from an earlier run)
     bool capturing = false;     // inside mw_graph_capture: no timing events, no host syncs
     int refs = 1;               // the user's handle + outstanding futures and graphs
     bool destroyed = false;     // mw_ctx_destroy called; teardown at the last release
@@ -913,7 +915,12 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
         }
         CUDA_OK(cudaEventCreateWithFlags(&c->st_start, cudaEventDisableTiming));
     }
-    const int64_t chunk_rows = std::max<int64_t>(1, (16ll << 20) / std::max<int64_t>(1, rb));
+    static const int64_t stage_bytes = [] {
+        const char* v = getenv("MW_STAGE_MB");   // staging chunk (MiB); 32 measured best
+        const int64_t mb = v ? atoll(v) : 32;
+        return (mb > 0 ? mb : 32) << 20;
+    }();
+    const int64_t chunk_rows = std::max<int64_t>(1, stage_bytes / std::max<int64_t>(1, rb));
     void* slot_in[kStageSlots];
     void* slot_out[kStageSlots];
     for (int i = 0; i < kStageSlots; ++i) {
@@ -921,22 +928,23 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
         MW_OK_OR_RETURN(scratch(c, "stage_out" + std::to_string(i), (size_t)(chunk_rows * rb), R.s, &slot_out[i]));
     }
     const bool a0_host = a0.location == MW_LOC_HOST, a1_host = a1.location == MW_LOC_HOST;
-    CUDA_OK(cudaEventRecord(c->st_start, R.s));
-    CUDA_OK(cudaStreamWaitEvent(c->copy_in, c->st_start, 0));
-    CUDA_OK(cudaStreamWaitEvent(c->copy_out, c->st_start, 0));
+    // No run-wide start barrier: the copy streams only wait for the previous
+    // use of each staging slot (possibly by the previous run), so this run's
+    // first uploads overlap the previous run's last downloads.  Device
+    // arguments and kernels stay ordered on the run's stream.
     auto rgba = st.kind == StepKind::Rgba ? rgba_groups(st.ops) : std::vector<mwk::RgbaProg>{};
     auto u8 = st.kind == StepKind::U8 ? u8_groups(st.ops) : std::vector<mwk::U8Prog>{};
     auto sx = st.kind == StepKind::Saxpy ? saxpy_groups(st.ops) : std::vector<mwk::SaxpyProg>{};
     if (st.kind == StepKind::Rgba && rgba.size() > 1)
         return fail(MW_E_UNSUPPORTED, "host-staged RGBA chains are limited to 16 pointwise ops");
     int64_t chunk = 0;
-    bool used[kStageSlots] = {false, false, false};
+    bool used[kStageSlots] = {false, false, false};   // by this run
     for (int q = 0; q < c->ppr; ++q) {
         int p = R.first + q;
         for (int64_t r0 = R.off[p]; r0 < R.off[p] + R.len[p]; r0 += chunk_rows, ++chunk) {
             const int64_t n = std::min(chunk_rows, R.off[p] + R.len[p] - r0);
             const int sl = (int)(chunk % kStageSlots);
-            if (used[sl]) CUDA_OK(cudaStreamWaitEvent(c->copy_in, c->st_out[sl], 0));
+            if (used[sl] || c->st_valid[sl]) CUDA_OK(cudaStreamWaitEvent(c->copy_in, c->st_out[sl], 0));
             used[sl] = true;
             uint8_t* din = static_cast<uint8_t*>(slot_in[sl]);
             uint8_t* dout = static_cast<uint8_t*>(slot_out[sl]);
@@ -987,6 +995,7 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
                 CUDA_OK(cudaMemcpyAsync(at_row<uint8_t>(a1, r0), d1, n * rb, cudaMemcpyDeviceToHost,
                                         c->copy_out));
             CUDA_OK(cudaEventRecord(c->st_out[sl], c->copy_out));
+            c->st_valid[sl] = true;
         }
     }
     for (int i = 0; i < kStageSlots; ++i)

@@ -36,6 +36,13 @@ def run():
     got = M.mw_run(ctx, trees.mapreduce(True), [M.arg(torch.from_numpy(x).to(dev)),
                                                M.arg(torch.from_numpy(y).to(dev))]).wait().result()
     assert abs(got["reduced"] - K.dot(x, y)) <= 1e-12 * K.abs_sum(x, y)
+    # FFT -> IFFT pipeline (NEXT-3): 3 transforms of 8192 points over 2 partitions
+    from oracle import fft as FF
+    xf = synth.np_f32_um11(11, 0, 2 * 3 * 8192).reshape(3, 8192, 2)
+    yf = torch.empty((3, 8192, 2), dtype=torch.float32, device=dev)
+    M.mw_run(ctx, trees.fft_pipeline(13), [M.arg(torch.from_numpy(xf).to(dev)), M.arg(yf)]).wait()
+    got = FF.as_complex(yf.cpu().numpy())
+    assert FF.rel_l2(got, FF.fft_chain(FF.as_complex(xf), "FI")).max() <= FF.tolerance(8192, 2)
     assert M.mw_ctx_launch_count(ctx) > 0
     ctx.destroy()
     print("smoke OK")

@@ -464,6 +464,24 @@ def test_config_nbody_2p20_sampled():
     _nb_check(acc.cpu().numpy()[samples, :3].astype(np.float64), acc_o, cond)
 
 
+@pytest.mark.slow
+def test_config_fft_512x65536_sampled():
+    """The bench's FFT workload (512 x 65536 points, fused fft -> ifft, one
+    launch): sampled transforms against the fp64 oracle, plus the forward
+    leaf alone on the same batch."""
+    B, N = 512, 1 << 16
+    src = torch.empty((B, N, 2), dtype=torch.float32, device=DEV)
+    synth.dev_fill_f32_um11(src, 11, 0)
+    dst = torch.empty_like(src)
+    run(ctx(), trees.fft_pipeline(16), [M.arg(src), M.arg(dst)])
+    rows = [0, 1, 255, 256, 300, 511]
+    x = np.stack([synth.np_f32_um11(11, r * 2 * N, 2 * N).reshape(N, 2) for r in rows])
+    assert np.array_equal(src.cpu().numpy()[rows], x)
+    _fft_check(dst.cpu().numpy()[rows], x, "FI")
+    run(ctx(), M.mw_kernel_fft(16, False), [M.arg(src), M.arg(dst)])
+    _fft_check(dst.cpu().numpy()[rows], x, "F")
+
+
 # ----------------------------------------------------------------- NCCL call sites (1-rank communicator)
 def test_nccl_communicator_paths():
     """force_nccl routes the MapReduce merge and the loop-condition reduction

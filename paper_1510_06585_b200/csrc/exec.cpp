@@ -868,9 +868,12 @@ mw_status run_nbody(RunCtx& R, const Step& st, const mw_arg& pos, const mw_arg& 
             mwk::Launch L = launch_for(c, R.s, p);
             const int reps = L.slow > 1.0f ? (int)std::lround(L.slow) : 1;
             L.slow = 1.0f;
+            void* pp;
+            MW_OK_OR_RETURN(scratch(c, "nbody_part", (size_t)mwk::nbody_part_doubles(R.len[p]) * 8, R.s, &pp));
             for (int rep = 0; rep < reps; ++rep)
                 MW_OK_OR_RETURN(kerr(mwk::nbody(P[cur], V[cur], P[1 - cur], V[1 - cur], nullptr,
-                                                R.off[p], R.len[p], N, st.eps2, st.dt, 0, L),
+                                                R.off[p], R.len[p], N, st.eps2, st.dt, 0,
+                                                static_cast<double*>(pp), L),
                                      "nbody"));
         }
         // Loop state update with global sync: re-replicate
@@ -1150,10 +1153,13 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         for (int q = 0; q < ppr; ++q) {
             int p = R.first + q;
             if (R.len[p] == 0) continue;
+            void* pp;
+            MW_OK_OR_RETURN(scratch(c, "nbody_part", (size_t)mwk::nbody_part_doubles(R.len[p]) * 8, s, &pp));
             PartTimer t(c, s, p, MW_KC_NBODY);
             MW_OK_OR_RETURN(kerr(mwk::nbody(static_cast<const float4*>(args[0].ptr), nullptr, nullptr,
                                             nullptr, at_row<float4>(args[1], R.off[p]), R.off[p],
-                                            R.len[p], L, stp.eps2, 0.f, 1, launch_for(c, s, p)),
+                                            R.len[p], L, stp.eps2, 0.f, 1, static_cast<double*>(pp),
+                                            launch_for(c, s, p)),
                                  "nbody_accel"));
         }
     } else if (ik == MW_VK_VEC1 || ik == MW_VK_VEC2) {

@@ -109,11 +109,13 @@ cudaError_t planes_pass(const uint32_t* in, uint32_t* out, const uint32_t* K, in
 
 // ------------------------------------------------------------ N-body
 // Bodies [first, first+count) of N: direct-sum acceleration (fp32 per
-// 256-source tile, fp64 across tiles).  mode 0: symplectic Euler step into
-// pos_out/vel_out (same global indexing); mode 1: write a_i (fp32) to acc.
+// 256-source tile, fp64 across tiles and across the fixed source segments).
+// mode 0: symplectic Euler step into pos_out/vel_out (same global indexing);
+// mode 1: write a_i (fp32) to acc.  part: nbody_part_doubles(count) fp64 scratch.
+int64_t nbody_part_doubles(int64_t count);
 cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4* vel_out,
                   float4* acc, int64_t first, int64_t count, int64_t N, float eps2, float dt,
-                  int mode, const Launch& L);
+                  int mode, double* part, const Launch& L);
 
 // ------------------------------------------------------------ MapReduce
 constexpr int kChunkLog2 = 16;      // canonical reduction chunk: 2^16 elements

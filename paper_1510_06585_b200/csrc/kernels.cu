@@ -92,9 +92,21 @@ unsigned grid_for(int64_t tiles, int per_sm, const Launch& L) {
 }
 
 // ------------------------------------------------------------ saxpy chain
+// Programmatic dependent launch: launched with programmatic stream
+// serialization, the kernel may be scheduled while its predecessor drains;
+// griddepcontrol.wait (before any global access) blocks until the
+// predecessor grid has completed and its memory is visible, so ordering is
+// unchanged — only the launch latency is hidden (a 2^20 saxpy is ~2 us of HBM
+// time, comparable to the launch gap between graph nodes).
+__device__ __forceinline__ void pdl_wait_and_release() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // y_i <- fma(a_k, x_i, y_i), k = 0..n-1 (R8 single rounding).
 __global__ void __launch_bounds__(256) k_saxpy_vec(const __grid_constant__ SaxpyProg p, const float4* __restrict__ x,
                                                    float4* __restrict__ y, int64_t nvec) {
+    pdl_wait_and_release();
     for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * 256) {
         uint4 xr = ld_stream(reinterpret_cast<const uint4*>(x + i));
         float4 yv = y[i];
@@ -112,6 +124,7 @@ __global__ void __launch_bounds__(256) k_saxpy_vec(const __grid_constant__ Saxpy
 }
 __global__ void k_saxpy_scalar(const __grid_constant__ SaxpyProg p, const float* __restrict__ x, float* __restrict__ y,
                                int64_t n) {
+    pdl_wait_and_release();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         float yv = y[i], xv = x[i];
@@ -1497,15 +1510,28 @@ cudaError_t saxpy_chain(const SaxpyProg& p, const float* x, float* y, int64_t n,
     static int occ_v = resident_ctas(k_saxpy_vec, 256), occ_s = resident_ctas(k_saxpy_scalar, 256);
     bool al = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
     int64_t nv = al ? n / 4 : 0;
-    if (nv > 0)
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(256);
+    cfg.stream = L.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (nv > 0) {
         ++g_launches;
-        k_saxpy_vec<<<grid_for((nv + 255) / 256, occ_v, L), 256, 0, L.stream>>>(
-            p, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), nv);
+        cfg.gridDim = dim3(grid_for((nv + 255) / 256, occ_v, L));
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_saxpy_vec, p, reinterpret_cast<const float4*>(x),
+                                           reinterpret_cast<float4*>(y), nv);
+        if (e != cudaSuccess) return e;
+    }
     int64_t rest = n - nv * 4;
-    if (rest > 0)
+    if (rest > 0) {
         ++g_launches;
-        k_saxpy_scalar<<<grid_for((rest + 255) / 256, occ_s, L), 256, 0, L.stream>>>(
-            p, x + nv * 4, y + nv * 4, rest);
+        cfg.gridDim = dim3(grid_for((rest + 255) / 256, occ_s, L));
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_saxpy_scalar, p, x + nv * 4, y + nv * 4, rest);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
 }
 

@@ -614,7 +614,8 @@ def run_reference(args, dist):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
             "data": "synthetic (SplitMix64, seeded; DESIGN.md input recipe)",
             "config": dict(REF_CONFIG.get(wl, {}), workload=name,
-                           arm="CPU oracle (oracle/, plain C, 1 thread)"),
+                           arm=("CPU oracle (oracle/fft.py, numpy pocketfft fp64, 1 thread)"
+                                if wl == "fft" else "CPU oracle (oracle/, plain C, 1 thread)")),
             "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "oracle",
                              "sample": f"per step: {sample}"},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

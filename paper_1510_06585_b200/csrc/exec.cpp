@@ -1656,8 +1656,11 @@ mw_status mw_ctx_set_tuning(mw_ctx* c, int32_t knob, int32_t value) {
     if (knob == MW_TUNE_HYST_T || knob == MW_TUNE_HYST_ROWS) {   // (T, ROWS) must be a built pair
         int T = knob == MW_TUNE_HYST_T ? value : c->tune[MW_TUNE_HYST_T];
         int Rw = knob == MW_TUNE_HYST_ROWS ? value : c->tune[MW_TUNE_HYST_ROWS];
-        const bool ok = (Rw == 32 && (T == 4 || T == 6 || T == 8)) || (Rw == 40 && (T == 8 || T == 12));
-        if (!ok) return fail(MW_E_INVALID_SPEC, "(hyst T, rows) pair not built: use (4|6|8, 32) or (8|12, 40)");
+        const bool ok = (Rw == 32 && (T == 4 || T == 6 || T == 8)) || (Rw == 40 && (T == 8 || T == 12)) ||
+                        (Rw == 48 && (T == 6 || T == 8));
+        if (!ok)
+            return fail(MW_E_INVALID_SPEC,
+                        "(hyst T, rows) pair not built: use (4|6|8, 32), (8|12, 40) or (6|8, 48)");
     }
     c->tune[knob] = value;
     return MW_OK;
@@ -1804,7 +1807,7 @@ mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_
             }
     }
     if (has_stencil) {
-        const int pairs[5][2] = {{4, 32}, {6, 32}, {8, 32}, {8, 40}, {12, 40}};
+        const int pairs[7][2] = {{4, 32}, {6, 32}, {8, 32}, {8, 40}, {12, 40}, {6, 48}, {8, 48}};
         Tune t = base;
         t[mwk::TUNE_HYST_PLANES] = 0;
         cands.push_back(t);

@@ -1471,7 +1471,7 @@ void tune_defaults(int* out) {
     out[TUNE_RGBA_UNROLL] = tuning_knob("MW_RGBA_UNROLL", 2);
     out[TUNE_HYST_PLANES] = tuning_knob("MW_HYST_PLANES", 1);
     out[TUNE_HYST_T] = tuning_knob("MW_HYST_T", 8);
-    out[TUNE_HYST_ROWS] = tuning_knob("MW_HYST_ROWS", 40);
+    out[TUNE_HYST_ROWS] = tuning_knob("MW_HYST_ROWS", 48);   // (8, 48): 0.407 vs 0.44 ms (8, 40)
     out[TUNE_NBODY_SPLIT] = tuning_knob("MW_NBODY_SPLIT", 0);
     out[TUNE_U8_TMA] = tuning_knob("MW_U8_TMA", 1);
     for (int k = 0; k < TUNE_COUNT; ++k)
@@ -1487,7 +1487,7 @@ bool tune_valid(int knob, int v) {
         case TUNE_RGBA_UNROLL: return v == 2 || v == 4 || v == 8;
         case TUNE_HYST_PLANES: return v == 0 || v == 1;
         case TUNE_HYST_T: return v == 4 || v == 6 || v == 8 || v == 12;
-        case TUNE_HYST_ROWS: return v == 32 || v == 40;
+        case TUNE_HYST_ROWS: return v == 32 || v == 40 || v == 48;
         case TUNE_NBODY_SPLIT: return v == 0 || v == 1;
         case TUNE_U8_TMA: return v == 0 || v == 1;
     }
@@ -1890,7 +1890,7 @@ cudaError_t planes_pass(const uint32_t* in, uint32_t* out, const uint32_t* K, in
     if (rows <= 0) return cudaSuccess;
     switch (T) {
         case 12: return planes_pass_t<12, 40>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
-        case 8: return planes_pass_t<8, 40>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
+        case 8: return planes_pass_t<8, 48>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
         case 6: return planes_pass_t<6, 32>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
         case 4: return planes_pass_t<4, 32>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
         case 2: return planes_pass_t<2, 32>(in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last, L);
@@ -1911,8 +1911,10 @@ cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t r
     MW_PL(8, 32);
     MW_PL(8, 40);
     MW_PL(12, 40);
+    MW_PL(8, 48);
+    MW_PL(6, 48);
 #undef MW_PL
-    return planes_loop_t<8, 40>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L);
+    return planes_loop_t<8, 48>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L);
 }
 
 int64_t nbody_part_doubles(int64_t count) { return (int64_t)kNbSeg * count * 3; }

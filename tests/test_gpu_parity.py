@@ -290,6 +290,7 @@ def test_hysteresis_planes_partitions_depths(T):
     want, D = oracle_hyst(gray)
     for k, d in [(4, x) for x in dists(4, rng, 2)] + [(5, [0.2, 0.003, 0.0, 0.397, 0.4])]:
         c = pctx(k, d, 1)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_T, 8)
         M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_ROWS, 40 if T in (8, 12) else 32)
         M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_T, T)
         for ce in (1, 5):
@@ -599,8 +600,10 @@ def test_tuning_knobs_bit_identical():
                 break
     gray = synth.np_u8_stream(8, 0, 300 * 257).reshape(300, 257)
     want_h, D = oracle_hyst(gray)
-    for planes, T, R in ((0, 8, 40), (1, 4, 32), (1, 6, 32), (1, 8, 32), (1, 8, 40), (1, 12, 40)):
+    for planes, T, R in ((0, 8, 40), (1, 4, 32), (1, 6, 32), (1, 8, 32), (1, 8, 40), (1, 12, 40),
+                         (1, 6, 48), (1, 8, 48)):
         M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_PLANES, planes)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_T, 8)   # valid with every row count
         M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_ROWS, R)
         M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_T, T)
         out = torch.empty((300, 257), dtype=torch.uint8, device=DEV)

@@ -872,7 +872,9 @@ __device__ __forceinline__ uint32_t expand_nib(uint32_t n) {      // 4 bits -> 0
     return ((n * 0x00204081u) & 0x01010101u) * 0xFFu;
 }
 
-template <bool SEG_ONLY>
+// SEG >= 0: the chain is exactly one threshold with compile-time compare modes
+// (lo mode = SEG / 4, hi mode = SEG % 4); SEG < 0: any chain ending with it.
+template <int SEG>
 __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8Prog p,
                                                      const __grid_constant__ U8Const c,
                                                      const uint8_t* __restrict__ src, int64_t sp,
@@ -902,15 +904,16 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
             }
         }
         uint32_t sb = 0, kb = 0;
-        if (SEG_ONLY) {
-            // the chain is exactly the threshold: strong = v >= hi, weak = lo <= v < hi
-            const int lm = c.lo_mode[0], hm = c.hi_mode[0];
+        if constexpr (SEG >= 0) {
+            // the chain is exactly the threshold: strong = v >= hi, weak = lo <= v < hi.
+            // The byte msbs 7,15,23,31 land on product bits 28..31 of f * 0x00204081
+            // (partial products at distinct bits: no carries), then move to 4i.
             const uint32_t l7 = c.lo7[0], h7 = c.hi7[0];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const uint32_t fhi = ge_t(v[i], h7, hm), flo = ge_t(v[i], l7, lm);
-                sb += nib_of(fhi) << (4 * i);
-                kb += nib_of(flo & ~fhi) << (4 * i);
+                const uint32_t fhi = ge_t(v[i], h7, SEG % 4), flo = ge_t(v[i], l7, SEG / 4);
+                sb |= ((fhi * 0x00204081u) >> 28) << (4 * i);
+                kb |= (((flo & ~fhi) * 0x00204081u) >> 28) << (4 * i);
             }
         } else {
             u8_apply_words<8>(p, c, v);   // the chain before the loop (ends with the threshold)
@@ -928,6 +931,42 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
         }
         S[(y + hd) * wp + w] = sb;
         K[(y + hd) * wp + w] = kb;
+    }
+}
+
+// Unpack when the chain after the loop is exactly finalize and a row has a
+// multiple of 4096 pixels: a warp owns 4 KiB of output (128 plane words);
+// lane l writes 16-byte chunk l of every 512 B, so each STG.128 of the warp
+// covers 512 contiguous bytes, and the 8 plane-word loads per lane (2 lanes
+// share a word) are issued before any store.  (The per-word variant below
+// left every thread with one dependent L2 load per 32 bytes of output.)
+__global__ void __launch_bounds__(256) k_planes_unpack_fin_w(const uint32_t* __restrict__ S0,
+                                                             const uint32_t* __restrict__ S1,
+                                                             const int* __restrict__ state,
+                                                             uint8_t* __restrict__ dst, int64_t dp,
+                                                             int64_t rows, int64_t wp, FastDiv UPR,
+                                                             int hd) {
+    const uint32_t* S = state[2] ? S1 : S0;
+    const int lane = threadIdx.x & 31;
+    const uint32_t total = (uint32_t)(rows * (wp / 128));
+    for (uint32_t u = blockIdx.x * 8u + (threadIdx.x >> 5); u < total; u += gridDim.x * 8u) {
+        const uint32_t y = fdiv(u, UPR), q = u - y * UPR.d;
+        const uint32_t* srow = S + ((int64_t)y + hd) * wp + 128ll * q;
+        uint8_t* drow = dst + (int64_t)y * dp + 4096ll * q + 16 * lane;
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = srow[(lane >> 1) + 16 * k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t h = w[k] >> (16 * (lane & 1));   // this lane's 16 pixels
+            uint32_t v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t m = ((h >> (4 * i)) & 15u) * 0x10204080u;
+                asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(v[i]) : "r"(m));
+            }
+            st_stream(reinterpret_cast<uint4*>(drow + 512 * k), make_uint4(v[0], v[1], v[2], v[3]));
+        }
     }
 }
 
@@ -1810,16 +1849,31 @@ cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t
     const int64_t tiles = (rows * wp + 255) / 256;
     const U8Const c = u8_consts(p);
     ++g_launches;
-    if (p.n == 1 && p.kind[0] == U8_SEGMENT) {
-        static int occ = resident_ctas(k_planes_pack<true>, 256);
-        k_planes_pack<true><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp), hd);
-    } else {
-        static int occ = resident_ctas(k_planes_pack<false>, 256);
-        k_planes_pack<false><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, src, sp, rows, W, wp, S, K, make_fastdiv((uint32_t)wp), hd);
+    const FastDiv WPd = make_fastdiv((uint32_t)wp);
+#define MW_PACK(SEGV)                                                                       \
+    {                                                                                       \
+        static int occ = resident_ctas(k_planes_pack<SEGV>, 256);                           \
+        k_planes_pack<SEGV><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(p, c, src, sp, rows, \
+                                                                          W, wp, S, K, WPd, hd); \
+        return cudaGetLastError();                                                          \
     }
-    return cudaGetLastError();
+    if (p.n == 1 && p.kind[0] == U8_SEGMENT) {
+        switch (c.lo_mode[0] * 4 + c.hi_mode[0]) {   // modes fixed at compile time
+            case 0: MW_PACK(0)
+            case 1: MW_PACK(1)
+            case 2: MW_PACK(2)
+            case 3: MW_PACK(3)
+            case 5: MW_PACK(5)
+            case 9: MW_PACK(9)
+            case 10: MW_PACK(10)
+            case 13: MW_PACK(13)
+            case 14: MW_PACK(14)
+            case 15: MW_PACK(15)
+            default: break;
+        }
+    }
+    MW_PACK(-1)
+#undef MW_PACK
 }
 
 cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S1,
@@ -1830,7 +1884,13 @@ cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S
     const int64_t tiles = (rows * wp + 255) / 256;
     const U8Const c = u8_consts(p);
     ++g_launches;
-    if (p.n == 1 && p.kind[0] == U8_FINALIZE) {
+    if (p.n == 1 && p.kind[0] == U8_FINALIZE && wp % 128 == 0 && dp % 16 == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && rows * (wp / 128) < (1ll << 31)) {
+        static int occ = resident_ctas(k_planes_unpack_fin_w, 256);
+        const int64_t units = rows * (wp / 128);
+        k_planes_unpack_fin_w<<<grid_for((units + 7) / 8, occ, L), 256, 0, L.stream>>>(
+            S0, S1, state, dst, dp, rows, wp, make_fastdiv((uint32_t)(wp / 128)), hd);
+    } else if (p.n == 1 && p.kind[0] == U8_FINALIZE) {
         static int occ = resident_ctas(k_planes_unpack<true>, 256);
         k_planes_unpack<true><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
             p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp), hd);

@@ -280,6 +280,18 @@ def test_hysteresis_loop_for_and_max_iters(planes):
         assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L)[0]) and r["executions"] == D + 1
 
 
+@pytest.mark.parametrize("W", [4096, 8192 + 4096])
+def test_hysteresis_wide_rows(W):
+    """Rows of a multiple of 4096 pixels take the warp-wide finalize unpack."""
+    H = 45
+    gray = synth.np_u8_stream(8, 3, H * W).reshape(H, W)
+    want, D = oracle_hyst(gray)
+    for k, d in ((1, [1.0]), (3, [0.3, 0.3, 0.4])):
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(pctx(k, d, 1), trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want) and r["executions"] == D + 1
+
+
 @pytest.mark.parametrize("T", [4, 6, 8, 12])
 def test_hysteresis_planes_partitions_depths(T):
     """Several partitions on the bit-plane path: T-row halos, T clamped to the

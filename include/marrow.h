@@ -289,6 +289,12 @@ mw_status mw_graph_result(mw_graph* g, double* out, int32_t n);
 mw_status mw_graph_kernels(const mw_graph* g, int64_t* kernels_per_replay);
 mw_status mw_graph_destroy(mw_graph* g);
 
+/* Monitoring (per-device execution times feed the load balancer)
+ * is on by default: every run records CUDA events around each partition's
+ * kernels (mw_last_timings, mw_kernel_stats, mw_rebalance).  Off: no events,
+ * so back-to-back runs carry no timing work between them (mw_last_timings
+ * and mw_rebalance then return MW_E_STATE).                                 */
+mw_status mw_ctx_set_monitoring(mw_ctx* ctx, int32_t on);
 /* ------------------------------------------------------------------ monitor / balance
  * Per-partition compute times of the last completed run (events placed
  * around each partition's kernels, before any collective wait),

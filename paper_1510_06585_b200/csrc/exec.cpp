@@ -103,6 +103,7 @@ struct mw_ctx {
     cudaEvent_t st_start = nullptr;
     bool st_valid[kStageSlots]{};   // slot has a recorded st_out (possibly from an earlier run)
     bool capturing = false;     // inside mw_graph_capture: no timing events, no host syncs
+    bool monitor = true;        // per-partition timing events (mw_ctx_set_monitoring)
     int refs = 1;               // the user's handle + outstanding futures and graphs
     bool destroyed = false;     // mw_ctx_destroy called; teardown at the last release
     int tune[mwk::TUNE_COUNT];  // tuning knobs (mw_ctx_set_tuning)
@@ -182,12 +183,12 @@ struct PartTimer {
     PartTimer(mw_ctx* c_, cudaStream_t s_, int p, int cl) : c(c_), s(s_), part(p), cls(cl) {
         a = nullptr;
         l0 = mwk::launch_count();
-        if (c->capturing) return;
+        if (c->capturing || !c->monitor) return;
         a = next_event(c);
         cudaEventRecord(a, s);
     }
     ~PartTimer() {
-        if (c->capturing) return;
+        if (c->capturing || !c->monitor) return;
         cudaEvent_t b = next_event(c);
         cudaEventRecord(b, s);
         mw_ctx::Rec r{part, cls, a, b, (int64_t)(mwk::launch_count() - l0)};
@@ -1094,7 +1095,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
     // ---- execute
     c->recs.clear();
     if (!c->stats_on) c->ev_used = 0;   // events of accumulated stats stay live
-    if (!c->capturing) CUDA_OK(cudaEventRecord(c->wall_a, s));
+    if (!c->capturing && c->monitor) CUDA_OK(cudaEventRecord(c->wall_a, s));
     const int ppr = c->ppr;
     if (host && c->capturing)
         return fail(MW_E_UNSUPPORTED, "host-resident arguments cannot be captured in a graph");
@@ -1239,9 +1240,9 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         }
     }
     if (!c->capturing) {
-        CUDA_OK(cudaEventRecord(c->wall_b, s));
+        if (c->monitor) CUDA_OK(cudaEventRecord(c->wall_b, s));
         c->last_len = R.len;
-        c->have_run = true;
+        c->have_run = c->monitor;
     }
     return MW_OK;
 }
@@ -1554,7 +1555,8 @@ void mw_future_release(mw_future* f) {
 
 mw_status mw_last_timings(mw_ctx* c, float* per_part_ms, int32_t n, float* wall_ms) {
     if (!c) return fail(MW_E_STATE, "NULL ctx");
-    if (!c->have_run) return fail(MW_E_STATE, "no run yet");
+    if (!c->have_run)
+        return fail(MW_E_STATE, c->monitor ? "no run yet" : "monitoring is disabled (mw_ctx_set_monitoring)");
     if (per_part_ms && n < c->P) return fail(MW_E_INVALID_SPEC, "output too small");
     CUDA_OK(cudaSetDevice(c->device));
     CUDA_OK(cudaEventSynchronize(c->wall_b));
@@ -1615,7 +1617,8 @@ mw_status mw_kernel_stats(mw_ctx* c, int32_t kernel_class, double* total_ms, int
 
 mw_status mw_last_lengths(const mw_ctx* c, int64_t* per_part_len, int32_t n) {
     if (!c || !per_part_len) return fail(MW_E_STATE, "NULL argument");
-    if (!c->have_run) return fail(MW_E_STATE, "no run yet");
+    if (!c->have_run)
+        return fail(MW_E_STATE, c->monitor ? "no run yet" : "monitoring is disabled (mw_ctx_set_monitoring)");
     if (n < c->P) return fail(MW_E_INVALID_SPEC, "output too small");
     for (int i = 0; i < c->P; ++i) per_part_len[i] = c->last_len[i];
     return MW_OK;
@@ -1645,6 +1648,13 @@ mw_status mw_ctx_set_slowdown(mw_ctx* c, int32_t part, float factor) {
     if (part < 0 || part >= c->P || !(factor >= 1.0f))
         return fail(MW_E_INVALID_SPEC, "bad partition or factor < 1");
     c->slow[part] = factor;
+    return MW_OK;
+}
+
+mw_status mw_ctx_set_monitoring(mw_ctx* c, int32_t on) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    c->monitor = on != 0;
+    if (!c->monitor) c->have_run = false;
     return MW_OK;
 }
 

@@ -99,6 +99,7 @@ _SIG = {
     "mw_pipeline": [_P(_vp), _i32, _node_pp],
     "mw_map": [_vp, _node_pp],
     "mw_map_reduce": [_vp, _i32, _node_pp],
+    "mw_ctx_set_monitoring": [_vp, _i32],
     "mw_map_reduce_user": [_vp, _MERGE_FN, _vp, _node_pp],
     "mw_loop_host": [_vp, _i64, _COND_FN, _vp, _node_pp],
     "mw_loop_for": [_vp, _i64, _node_pp],
@@ -644,6 +645,12 @@ def mw_graph_destroy(g):
     if g.ptr:
         _call("mw_graph_destroy", g.ptr)
         g.ptr = None
+
+
+def mw_ctx_set_monitoring(ctx, on=True):
+    """Per-partition timing events on/off (on by default; needed by
+    mw_last_timings / mw_rebalance)."""
+    _call("mw_ctx_set_monitoring", ctx.ptr, int(bool(on)))
 
 
 def mw_ctx_set_tuning(ctx, knob, value):

@@ -9,8 +9,11 @@
 //
 // Definitions follow DESIGN.md §Readings (R1-R12), citing PAPER.md lines.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "mw_kernels.h"
@@ -924,8 +927,8 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
             }
         }
         const int64_t rem = W - x0;   // bits beyond the image width stay 0
-        if (rem < 32) {
-            const uint32_t keep = (1u << rem) - 1u;
+        if (rem < 32) {   // (pad words past the image: rem <= 0)
+            const uint32_t keep = rem <= 0 ? 0u : (1u << rem) - 1u;
             sb &= keep;
             kb &= keep;
         }
@@ -1035,26 +1038,12 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // (Measured on B200: keeping the weak plane in registers with 256-thread CTAs
 // and a rolled execution loop beats smem-resident K and a fully unrolled
 // shrinking-window loop, whose code no longer fits the instruction cache.)
+// T executions on a register tile (rows [ybase, ybase + ROWS) x lanes);
+// returns the last execution (0-based) that changed an owned bit.
 template <int T, int ROWS>
-__device__ __forceinline__ int plane_tile(const uint32_t* __restrict__ in,
-                                          uint32_t* __restrict__ out,
-                                          const uint32_t* __restrict__ K, int64_t rows,
-                                          int64_t wp, int hd, int64_t strip, int64_t cb,
-                                          int steps, int lane) {
+__device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
+                                           int steps, bool own_lane) {
     constexpr int R = ROWS - 2 * T;
-    constexpr int OW = 30;
-    const bool own_lane = lane >= 1 && lane <= OW;
-    const int64_t w = cb * OW - 1 + lane;          // lane 0 / 31: halo words
-    const bool wv = w >= 0 && w < wp;
-    const int64_t ybase = strip * R - T;            // row of register row 0
-    uint32_t sv[ROWS], kv[ROWS];
-#pragma unroll
-    for (int i = 0; i < ROWS; ++i) {
-        const int64_t y = ybase + i;
-        const bool ok = wv && y >= -hd && y < rows + hd;
-        sv[i] = ok ? in[(y + hd) * wp + w] : 0u;
-        kv[i] = ok ? K[(y + hd) * wp + w] : 0u;
-    }
     int tile_last = -1;
     for (int st = 0; st < steps; ++st) {
         // lanes 0/31 take their own word as the outer neighbour: the error
@@ -1078,11 +1067,44 @@ __device__ __forceinline__ int plane_tile(const uint32_t* __restrict__ in,
         }
         if (__any_sync(0xffffffffu, own_lane && ch != 0)) tile_last = st;
     }
+    return tile_last;
+}
+
+template <int T, int ROWS>
+__device__ __forceinline__ void plane_store(const uint32_t (&sv)[ROWS], uint32_t* __restrict__ out,
+                                            int64_t rows, int64_t wp, int hd, int64_t ybase,
+                                            int64_t w, bool own_lane, bool wv) {
+    constexpr int R = ROWS - 2 * T;
 #pragma unroll
     for (int i = T; i < T + R; ++i) {
         const int64_t y = ybase + i;
         if (own_lane && wv && y < rows) out[(y + hd) * wp + w] = sv[i];
     }
+}
+
+// One warp tile with plain global loads (the per-partition pass kernel).
+template <int T, int ROWS>
+__device__ __forceinline__ int plane_tile(const uint32_t* __restrict__ in,
+                                          uint32_t* __restrict__ out,
+                                          const uint32_t* __restrict__ K, int64_t rows,
+                                          int64_t wp, int hd, int64_t strip, int64_t cb,
+                                          int steps, int lane) {
+    constexpr int R = ROWS - 2 * T;
+    constexpr int OW = 30;
+    const bool own_lane = lane >= 1 && lane <= OW;
+    const int64_t w = cb * OW - 1 + lane;          // lane 0 / 31: halo words
+    const bool wv = w >= 0 && w < wp;
+    const int64_t ybase = strip * R - T;            // row of register row 0
+    uint32_t sv[ROWS], kv[ROWS];
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+        const int64_t y = ybase + i;
+        const bool ok = wv && y >= -hd && y < rows + hd;
+        sv[i] = ok ? in[(y + hd) * wp + w] : 0u;
+        kv[i] = ok ? K[(y + hd) * wp + w] : 0u;
+    }
+    const int tile_last = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
+    plane_store<T, ROWS>(sv, out, rows, wp, hd, ybase, w, own_lane, wv);
     return tile_last;
 }
 
@@ -1104,45 +1126,122 @@ __device__ __forceinline__ bool plane_tile_active(const uint8_t* fprev, int64_t 
 }
 
 // Whole loop, one partition per device: one cooperative kernel, all passes.
+// Every warp prefetches its next active tile (S and K boxes of ROWS x 36
+// words from the 16-byte-aligned column at or left of the tile's first word
+// — TMA box origins are 16-byte aligned; lane l reads word o + l of a box
+// row — 2-D TMA with out-of-bounds zero fill = the image-boundary rule)
+// into its shared-memory slot while it computes the current one; the L2
+// latency of the tile load (~2.4 us per tile measured with plain loads,
+// 28 % of the loop) is hidden behind the T executions.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int T, int ROWS>
-__global__ void __launch_bounds__(256) k_planes_loop(uint32_t* __restrict__ S0,
-                                                     uint32_t* __restrict__ S1,
-                                                     const uint32_t* __restrict__ K, int64_t rows,
+__global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUtensorMap tm_s0,
+                                                     const __grid_constant__ CUtensorMap tm_s1,
+                                                     const __grid_constant__ CUtensorMap tm_k,
+                                                     uint32_t* __restrict__ S0,
+                                                     uint32_t* __restrict__ S1, int64_t rows,
                                                      int64_t wp, int64_t max_iters,
                                                      int* __restrict__ flags,
                                                      int* __restrict__ state,
-                                                     uint8_t* __restrict__ tflags) {
+                                                     uint8_t* __restrict__ tflags,
+                                                     unsigned long long* __restrict__ prof) {
     constexpr int R = ROWS - 2 * T;
+    constexpr int OW = 30;
+    constexpr int BW = 36;                          // box width (words)
+    constexpr uint32_t kBox = ROWS * BW * 4;        // bytes per plane box
+    extern __shared__ __align__(128) uint32_t psm[];   // 8 warp slots, then 8 mbarriers
+    uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * ROWS * BW);
     cg::grid_group grid = cg::this_grid();
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* sb = psm + wid * (2 * ROWS * BW);     // [ROWS][BW] S box, then K box
+    uint32_t* kb = sb + ROWS * BW;
+    uint64_t* bar = &bars[wid];
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t gw = (int64_t)blockIdx.x * 8 + wid;
     const int64_t nwarps = (int64_t)gridDim.x * 8;
     const int64_t n_strips = (rows + R - 1) / R;
-    const int64_t n_cb = (wp + 29) / 30;
+    const int64_t n_cb = (wp + OW - 1) / OW;
     const int64_t n_tiles = n_strips * n_cb;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool own_lane = lane >= 1 && lane <= OW;
+    auto gtime = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (prof && leader) prof[0] = gtime();
+    uint32_t phase = 0;
     int64_t k0 = 0;
     int pass = 0;
     while (k0 < max_iters) {
         const int steps = (int)min((int64_t)T, max_iters - k0);
-        const uint32_t* in = (pass & 1) ? S1 : S0;
+        const CUtensorMap* tin = (pass & 1) ? &tm_s1 : &tm_s0;
         uint32_t* out = (pass & 1) ? S0 : S1;
         const uint8_t* fprev = tflags + ((pass + 1) & 1) * n_tiles;
         uint8_t* fcur = tflags + (pass & 1) * n_tiles;
         if (leader) flags[(pass + 1) % 3] = -1;   // last read two barriers ago
-        int my_last = -1;
-        for (int64_t t = gw; t < n_tiles; t += nwarps) {
-            const int64_t strip = t / n_cb, cb = t - strip * n_cb;
-            if (!plane_tile_active(fprev, strip, cb, n_strips, n_cb, pass == 0, 0, 0, lane)) {
+        // the next active tile of this warp at or after t (inactive ones are
+        // marked unchanged on the way)
+        auto next_active = [&](int64_t t) {
+            for (; t < n_tiles; t += nwarps) {
+                const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+                if (plane_tile_active(fprev, strip, cb, n_strips, n_cb, pass == 0, 0, 0, lane))
+                    break;
                 if (lane == 0) fcur[t] = 0;
-                continue;
             }
-            const int tl = plane_tile<T, ROWS>(in, out, K, rows, wp, 1, strip, cb, steps, lane);
+            return t;
+        };
+        auto issue = [&](int64_t t) {
+            if (lane == 0) {
+                const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+                const int x = (int)(cb * OW - 1) & ~3, y = (int)(strip * R - T + 1);
+                mbar_expect_tx(bar, 2 * kBox);
+                tma_load_2d(sb, tin, x, y, bar);
+                tma_load_2d(kb, &tm_k, x, y, bar);
+            }
+        };
+        int my_last = -1;
+        int64_t t = next_active(gw);
+        if (t < n_tiles) issue(t);
+        while (t < n_tiles) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            const int o = (int)((t % n_cb) * OW - 1) & 3;   // tile's first word in the box
+            uint32_t sv[ROWS], kv[ROWS];
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i) {
+                sv[i] = sb[i * BW + o + lane];
+                kv[i] = kb[i * BW + o + lane];
+            }
+            __syncwarp();                               // slot free: prefetch the next tile
+            const int64_t tn = next_active(t + nwarps);
+            if (tn < n_tiles) issue(tn);
+            const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+            const int64_t w = cb * OW - 1 + lane;
+            const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
+            plane_store<T, ROWS>(sv, out, rows, wp, 1, strip * R - T, w, own_lane,
+                                 w >= 0 && w < wp);
             if (lane == 0) fcur[t] = (uint8_t)(tl >= 0);
             my_last = max(my_last, tl);
+            t = tn;
         }
         if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
+        // the next pass reads `out` through the async (TMA) proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         grid.sync();
+        if (prof && leader) prof[1 + pass] = gtime();
         const int last = *((volatile int*)&flags[pass % 3]);
         if (last < k0 + steps - 1) {   // the pass ended with an execution that changed nothing
             if (leader) {
@@ -1839,7 +1938,8 @@ cudaError_t copy_batch(const CopyBatch& b, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-int64_t plane_words(int64_t W) { return (W + 31) / 32; }
+// rounded up to 4 words: the row pitch of a TMA tensor map is a multiple of 16 B
+int64_t plane_words(int64_t W) { return (W + 127) / 128 * 4; }
 
 cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
                         uint32_t* S, uint32_t* K, const Launch& L, int hd) {
@@ -1906,20 +2006,70 @@ int64_t planes_tiles(int64_t rows, int64_t W) {   // upper bound over the varian
     return ((rows + 7) / 8) * ((plane_words(W) + 29) / 30);
 }
 
+// 2-D tensor map over a plane buffer of (rows + 2) x wp words, box ROWS x 36
+static bool plane_tmap(CUtensorMap* tm, const uint32_t* base, int64_t rows, int64_t wp, int box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = []() {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)wp, (cuuint64_t)(rows + 2)};
+    const cuuint64_t strides[1] = {(cuuint64_t)wp * 4};
+    const cuuint32_t box[2] = {36, (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// MW_HYST_PROF=1: per-pass device timestamps of the loop kernel to stderr
+static unsigned long long* hyst_prof_buf() {
+    static unsigned long long* p = []() -> unsigned long long* {
+        unsigned long long* q = nullptr;
+        if (getenv("MW_HYST_PROF") && cudaMalloc(&q, 1024) != cudaSuccess) q = nullptr;
+        return q;
+    }();
+    return p;
+}
+
 template <int T, int ROWS>
 static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows,
                                  int64_t wp, int64_t max_iters, int* flags, int* state,
                                  uint8_t* tflags, const Launch& L) {
-    static int occ = resident_ctas(k_planes_loop<T, ROWS>, 256);
+    constexpr size_t smem = 8 * 2 * ROWS * 36 * 4 + 8 * 8;
+    static int occ = [] {
+        cudaFuncSetAttribute(k_planes_loop<T, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        return resident_ctas(k_planes_loop<T, ROWS>, 256, smem);
+    }();
     constexpr int R = ROWS - 2 * T;
     const int64_t tiles = ((rows + R - 1) / R) * ((wp + 29) / 30);
     // cooperative: every CTA must be co-resident
     unsigned grid = grid_for((tiles + 7) / 8, occ, L);
+    CUtensorMap ts0, ts1, tk;
+    if (!plane_tmap(&ts0, S0, rows, wp, ROWS) || !plane_tmap(&ts1, S1, rows, wp, ROWS) ||
+        !plane_tmap(&tk, K, rows, wp, ROWS))
+        return cudaErrorInvalidValue;
+    unsigned long long* prof = hyst_prof_buf();
+    if (prof) cudaMemsetAsync(prof, 0, 1024, L.stream);
     int64_t r = rows, w = wp, mi = max_iters;
-    void* args[] = {&S0, &S1, (void*)&K, &r, &w, &mi, &flags, &state, &tflags};
+    void* args[] = {&ts0, &ts1, &tk, &S0, &S1, &r, &w, &mi, &flags, &state, &tflags, &prof};
     ++g_launches;
-    return cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid), dim3(256),
-                                       args, 0, L.stream);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid),
+                                                dim3(256), args, smem, L.stream);
+    if (prof && e == cudaSuccess) {
+        unsigned long long h[128];
+        cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, L.stream);
+        cudaStreamSynchronize(L.stream);
+        fprintf(stderr, "MW_HYST_PROF grid=%u tiles=%lld", grid, (long long)tiles);
+        for (int i = 1; i < 100 && h[i]; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) / 1e3);
+        fprintf(stderr, " us\n");
+    }
+    return e;
 }
 
 template <int T, int ROWS>

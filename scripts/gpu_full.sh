@@ -1,0 +1,10 @@
+# Full round check on one B200: build, smoke, GPU parity suite, bench of every workload.
+set -x
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+tail -1 gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/gpu_tests.log 2>&1
+tail -3 gpurun_out/gpu_tests.log
+timeout 300 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+cat gpurun_out/bench_default.json
+timeout 900 python bench.py --workload all --no-cpu > gpurun_out/bench_all.json 2> gpurun_out/bench_all.err
+cat gpurun_out/bench_all.json | cut -c1-400

@@ -1038,35 +1038,63 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // (Measured on B200: keeping the weak plane in registers with 256-thread CTAs
 // and a rolled execution loop beats smem-resident K and a fully unrolled
 // shrinking-window loop, whose code no longer fits the instruction cache.)
-// T executions on a register tile (rows [ybase, ybase + ROWS) x lanes);
-// returns the last execution (0-based) that changed an owned bit.
-template <int T, int ROWS>
-__device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
-                                           int steps, bool own_lane) {
-    constexpr int R = ROWS - 2 * T;
-    int tile_last = -1;
-    for (int st = 0; st < steps; ++st) {
+// One execution on register rows [LO, HI] (rows outside keep their values
+// and only serve as neighbours); returns whether an owned row [T, ROWS - T)
+// of an owned lane changed.
+template <int T, int ROWS, int LO, int HI>
+__device__ __forceinline__ bool plane_exec(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
+                                           bool own_lane) {
+    auto hrow = [&](uint32_t sx) {
         // lanes 0/31 take their own word as the outer neighbour: the error
         // enters at their far bits and moves one bit per execution, never
         // reaching the owned lanes (T <= 16)
-        auto hrow = [&](uint32_t sx) {
-            const uint32_t l = __shfl_up_sync(0xffffffffu, sx, 1);
-            const uint32_t r = __shfl_down_sync(0xffffffffu, sx, 1);
-            return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
-        };
-        uint32_t hp = hrow(sv[0]), hc = hrow(sv[1]);
-        uint32_t ch = 0;
+        const uint32_t l = __shfl_up_sync(0xffffffffu, sx, 1);
+        const uint32_t r = __shfl_down_sync(0xffffffffu, sx, 1);
+        return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
+    };
+    uint32_t hp = hrow(sv[LO - 1]), hc = hrow(sv[LO]);
+    uint32_t ch = 0;
 #pragma unroll
-        for (int i = 1; i < ROWS - 1; ++i) {
-            const uint32_t hn = hrow(sv[i + 1]);     // old row i+1 (not yet updated)
-            const uint32_t s2 = sv[i] | (kv[i] & (hp | hc | hn));
-            if (i >= T && i < T + R) ch |= s2 ^ sv[i];
-            sv[i] = s2;
-            hp = hc;
-            hc = hn;
-        }
-        if (__any_sync(0xffffffffu, own_lane && ch != 0)) tile_last = st;
+    for (int i = LO; i <= HI; ++i) {
+        const uint32_t hn = hrow(sv[i + 1]);     // old row i+1 (not yet updated)
+        const uint32_t s2 = sv[i] | (kv[i] & (hp | hc | hn));
+        if (i >= T && i < ROWS - T) ch |= s2 ^ sv[i];
+        sv[i] = s2;
+        hp = hc;
+        hc = hn;
     }
+    return __any_sync(0xffffffffu, own_lane && ch != 0);
+}
+
+// T executions on a register tile (rows [ybase, ybase + ROWS) x lanes);
+// returns the last execution (0-based) that changed an owned bit.  Row r is
+// exact after execution st when st < r < ROWS - 1 - st (validity shrinks by
+// a row per execution at each end), so a full pass computes rows [1, ROWS-2]
+// in its first T/2 executions and only [T/2 + 1, ROWS - 2 - T/2] in the
+// rest (a superset of what each later execution needs); executions run in
+// pairs so the updated rows alternate between two register sets instead of
+// being moved back every execution.
+template <int T, int ROWS>
+__device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
+                                           int steps, bool own_lane) {
+    int tile_last = -1;
+    if (T % 4 == 0 && steps == T) {
+        constexpr int H = T / 2;
+#pragma unroll 1
+        for (int st = 0; st < H; st += 2) {
+            if (plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane)) tile_last = st;
+            if (plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane)) tile_last = st + 1;
+        }
+#pragma unroll 1
+        for (int st = H; st < T; st += 2) {
+            if (plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane)) tile_last = st;
+            if (plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane)) tile_last = st + 1;
+        }
+        return tile_last;
+    }
+#pragma unroll 1
+    for (int st = 0; st < steps; ++st)
+        if (plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane)) tile_last = st;
     return tile_last;
 }
 
@@ -1075,10 +1103,17 @@ __device__ __forceinline__ void plane_store(const uint32_t (&sv)[ROWS], uint32_t
                                             int64_t rows, int64_t wp, int hd, int64_t ybase,
                                             int64_t w, bool own_lane, bool wv) {
     constexpr int R = ROWS - 2 * T;
+    if (!own_lane || !wv) return;
+    uint32_t* o = out + (ybase + T + hd) * wp + w;    // owned row 0
+    const uint32_t pw = (uint32_t)wp;
+    if (ybase + T + R <= rows) {                       // every owned row inside the image
 #pragma unroll
-    for (int i = T; i < T + R; ++i) {
-        const int64_t y = ybase + i;
-        if (own_lane && wv && y < rows) out[(y + hd) * wp + w] = sv[i];
+        for (int i = 0; i < R; ++i) o[i * pw] = sv[T + i];
+    } else {
+        const int n = (int)(rows - (ybase + T));
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (i < n) o[i * pw] = sv[T + i];
     }
 }
 

@@ -5,7 +5,7 @@ Default workload (BASELINE.json configs[1], the metric's headline config):
 the fused Filter Pipeline (Gaussian noise -> solarize -> mirror) on
 one 8192x8192 RGBA8 image, rows partitioned across the ranks (strong
 scaling).  A step is one run of the whole tree over the image.  Other §8
-rows: --workload saxpy|segmentation|mapreduce_sum|mapreduce_dot|hysteresis|
+rows: --workload saxpy|segmentation|mapreduce_sum|mapreduce_dot|mapreduce_max|hysteresis|
 nbody|all.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
@@ -314,15 +314,18 @@ class MapReduce(Workload):
     unit, dtype = "elements/s", "f32"
     e2e_mode, e2e_out = "explicit", ()
 
-    def __init__(self, *a, dot=True):
+    def __init__(self, *a, dot=True, reduce_op=None):
         super().__init__(*a)
         self.dot = dot
+        self.reduce_op = reduce_op   # None: map_reduce(+); else a device reduction stage (NEXT-4)
         self.e2e_in = (0, 1) if dot else (0,)
-        self.name = f"mapreduce_{'dot' if dot else 'sum'}_2^30_fp32"
+        self.name = (f"mapreduce_{'dot' if dot else 'sum'}_2^30_fp32" if reduce_op is None
+                     else "mapreduce_max_product_2^30_fp32")
 
     def setup(self, n=1 << 30):
         M, t = self.M, self.torch
-        self.tree = self.trees.mapreduce(self.dot)
+        self.tree = (self.trees.mapreduce(self.dot) if self.reduce_op is None
+                     else self.trees.mapreduce_sct(self.reduce_op, self.dot))
         self.kclass = M.MW_KC_REDUCE
         self.L = n
         self.o, self.n = self.slice(n)
@@ -347,8 +350,9 @@ class MapReduce(Workload):
         return (8.0 if self.dot else 4.0) * self.n * steps if cls == self.M.MW_KC_REDUCE else 0.0
 
     def config(self):
-        return {"workload": self.name, "n": self.L, "merge": "+ (canonical 2^16 chunks, fp64)",
-                "l2": self.l2_note}
+        merge = ("+ (canonical 2^16 chunks, fp64)" if self.reduce_op is None
+                 else "device reduction stage reduce(max) over x*y (fp64-exact products)")
+        return {"workload": self.name, "n": self.L, "merge": merge, "l2": self.l2_note}
 
 
 class Hysteresis(Workload):
@@ -445,7 +449,7 @@ REF_CONFIG = {
                "tree": "pipeline(gauss_noise(seed=4,S=8), solarize(T=128), mirror)"},
     "saxpy": {"n": 1 << 20, "a": 2.5},
     "segmentation": {"shape_zyx": [512, 1024, 1024], "lo": 85, "hi": 170},
-    "mapreduce_sum": {"n": 1 << 30}, "mapreduce_dot": {"n": 1 << 30},
+    "mapreduce_sum": {"n": 1 << 30}, "mapreduce_dot": {"n": 1 << 30}, "mapreduce_max": {"n": 1 << 30},
     "hysteresis": {"tree": "pipeline(threshold(173,250), loop_while_changed(step, "
                            "check_every=1), finalize)"},
     "nbody": {"bodies": 1 << 20, "eps2": 1e-4, "dt": 1e-3},
@@ -497,6 +501,7 @@ class Fft(Workload):
 WORKLOADS = {"filter": Filter, "saxpy": Saxpy, "segmentation": Segmentation,
              "mapreduce_sum": lambda *a: MapReduce(*a, dot=False),
              "mapreduce_dot": lambda *a: MapReduce(*a, dot=True),
+             "mapreduce_max": lambda *a: MapReduce(*a, dot=True, reduce_op=1),
              "hysteresis": Hysteresis, "nbody": NBody, "fft": Fft}
 
 
@@ -543,7 +548,10 @@ def oracle_generic_rate(name, budget_s):
             x = synth.host_f32_um11(5, reps * n, n)
             y = synth.host_f32_um11(6, reps * n, n)
             t0 = time.perf_counter()
-            K.dot(x, y) if name.endswith("dot") else K.sum_(x)
+            if name.endswith("max"):
+                K.fold_extreme(x, y)
+            else:
+                K.dot(x, y) if name.endswith("dot") else K.sum_(x)
             dt = time.perf_counter() - t0
             what = "2^24-element chunks"
         elif name == "hysteresis":
@@ -579,6 +587,7 @@ def cpu_rate(name, budget_s):
         return oracle_filter_rate(budget_s)
     key = {"saxpy_map_2^20_fp32": "saxpy", "segmentation_1024x1024x512_u8": "segmentation",
            "mapreduce_sum_2^30_fp32": "mapreduce_sum", "mapreduce_dot_2^30_fp32": "mapreduce_dot",
+           "mapreduce_max_product_2^30_fp32": "mapreduce_max",
            "hysteresis_16384x16384_u8": "hysteresis", "nbody_2^20": "nbody",
            "fft_ifft_512x65536_c64": "fft"}[name]
     return oracle_generic_rate(key, budget_s)
@@ -594,6 +603,7 @@ def run_reference(args, dist):
              "segmentation": ("segmentation_1024x1024x512_u8", "voxels/s", "u8"),
              "mapreduce_sum": ("mapreduce_sum_2^30_fp32", "elements/s", "f64"),
              "mapreduce_dot": ("mapreduce_dot_2^30_fp32", "elements/s", "f64"),
+             "mapreduce_max": ("mapreduce_max_product_2^30_fp32", "elements/s", "f64"),
              "hysteresis": ("hysteresis_16384x16384_u8", "pixels/s", "u8"),
              "nbody": ("nbody_2^20", "bodies/s", "f64"),
              "fft": ("fft_ifft_512x65536_c64", "ffts/s", "f64")}
@@ -877,7 +887,7 @@ def main():
         return
     names = list(WORKLOADS) if args.workload == "all" else [args.workload]
     default_steps = {"filter": 2000, "saxpy": 5000, "segmentation": 1000, "mapreduce_sum": 300,
-                     "mapreduce_dot": 200, "hysteresis": 20, "nbody": 3, "fft": 200}
+                     "mapreduce_dot": 200, "mapreduce_max": 200, "hysteresis": 20, "nbody": 3, "fft": 200}
     user_steps = args.steps
     for n in names:
         args.steps = user_steps or default_steps[n]

@@ -118,6 +118,18 @@ mw_status mw_kernel_nbody_step(float dt, float eps2, mw_node** out);     /* P:73
 mw_status mw_kernel_nbody_accel(float eps2, mw_node** out);  /* test leaf: a_i only */
 mw_status mw_kernel_map_identity(mw_node** out);         /* MapReduce map stage: x   */
 mw_status mw_kernel_map_product(mw_node** out);          /* MapReduce map stage: x*y */
+/* Reduction-stage leaf (NEXT-4; Table 1 P:191 "map_reduce(SCT map_stage, SCT
+ * reduction_stage)", "It is thus up to the programmer to decide where
+ * the reduction takes place" — here: on the device).  It reduces the terms
+ * of a map stage (x or x*y, each exact in fp64) with an associative,
+ * commutative operator; the partitions' partial results are merged with the
+ * same operator, so the result is the reduction over the whole domain
+ * (reading R28): SUM = the canonical fp64 sum (as MW_MERGE_ADD), MAX / MIN =
+ * IEEE maxNum / minNum (a NaN term is ignored; exact, bit-identical for every
+ * distribution).  Empty domain: 0, -inf, +inf.  Only usable as the second
+ * argument of mw_map_reduce_sct; op outside 0..2: MW_E_INVALID_SPEC.        */
+enum { MW_REDUCE_SUM = 0, MW_REDUCE_MAX = 1, MW_REDUCE_MIN = 2 };
+mw_status mw_kernel_reduce(int32_t op, mw_node** out);
 /* Test leaf: writes each element's partition (SIZE, OFFSET) trait
  * values.  epu/nu feed the constraint system;
  * strict != 0 forbids the L mod granule tail.                                */
@@ -153,6 +165,13 @@ mw_status mw_map_reduce(mw_node* map_stage, int32_t merge_op, mw_node** out);   
 /* User-defined merging function (called on the host thread that waits on the
  * future; fn must not call back into libmarrow).                           */
 mw_status mw_map_reduce_user(mw_node* map_stage, mw_merge_fn fn, void* user, mw_node** out);
+/* MapReduce with a device reduction stage (an mw_kernel_reduce leaf; NEXT-4,
+ * P:191): the map stage's terms are reduced on the device, partition
+ * partials merged with the same operator across ranks (NCCL all-reduce).
+ * Result as for mw_map_reduce (mw_future_result out[0] fp64, out[1] fp32).
+ * reduction_stage not a reduce leaf, or map_stage not producing terms:
+ * MW_E_INVALID_SPEC.                                                        */
+mw_status mw_map_reduce_sct(mw_node* map_stage, mw_node* reduction_stage, mw_node** out);
 mw_status mw_loop_for(mw_node* body, int64_t n, mw_node** out);           /* n >= 0 */
 /* while(changed && executions < max_iters) body.
  * The stop condition is evaluated on the device and reduced across ranks

@@ -39,6 +39,7 @@ def lib():
             "orc_sum": (f64, [i64, vp]),
             "orc_dot": (f64, [i64, vp, vp]),
             "orc_abs_sum": (f64, [i64, vp, vp]),
+            "orc_fold_extreme": (f64, [i64, vp, vp, i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -175,6 +176,16 @@ class Fold:
     @property
     def value(self) -> float:
         return float(self.sc[0] + self.sc[1])
+
+
+def fold_extreme(x, y=None, is_min=False):
+    """Reduction stage MAX / MIN (NEXT-4, R28): serial fold of the terms x
+    (or x*y, exact in fp64) with maxNum / minNum; empty -> -inf / +inf."""
+    x = _c(x, np.float32)
+    if y is not None:
+        y = _c(y, np.float32)
+        assert y.size == x.size
+    return float(lib().orc_fold_extreme(x.size, _p(x), _p(y), int(bool(is_min))))
 
 
 def abs_sum(x, y=None):

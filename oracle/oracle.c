@@ -266,6 +266,20 @@ void orc_fold_chunk(int64_t n, const float* x, const float* y, double* sc) {
         neumaier_add(&sc[0], &sc[1], y ? (double)x[i] * (double)y[i] : (double)x[i]);
 }
 
+/* Device reduction stage (NEXT-4; P:191 map_reduce(SCT map_stage, SCT
+ * reduction_stage); reading R28): a serial left fold of the terms (x, or x*y
+ * exact in fp64) with maxNum (is_min = 0) or minNum (is_min = 1): a NaN term
+ * is ignored, acc starts at the identity -inf / +inf (the empty result).    */
+double orc_fold_extreme(int64_t n, const float* x, const float* y, int is_min) {
+    double acc = is_min ? INFINITY : -INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+        const double t = y ? (double)x[i] * (double)y[i] : (double)x[i];
+        if (t != t) continue;                       /* NaN term: ignored */
+        if (is_min ? (t < acc) : (t > acc)) acc = t;
+    }
+    return acc;
+}
+
 /* sum |terms| for the ill-conditioned tolerance branch. */
 double orc_abs_sum(int64_t n, const float* x, const float* y) {
     double s = 0.0, c = 0.0;

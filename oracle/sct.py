@@ -16,6 +16,9 @@ Node semantics (DESIGN.md "Readings" R9, R10, R16):
   Map(t)                      t over the whole domain
   MapReduce(m, '+')           m per element, then a serial left fold in
                               Neumaier-compensated fp64
+  MapReduce(m, Leaf('reduce', op=...))  the reduction stage is an SCT
+                              (P:191; NEXT-4, R28): 'sum' = the '+' fold,
+                              'max' / 'min' = serial maxNum / minNum fold
   LoopFor(b, n)               state_{k+1} = b(state_k), k < n (P:163, P:376-378)
   LoopWhileChanged(b, max)    condition before each iteration; stop when the
                               body changed nothing or max executions reached
@@ -49,6 +52,7 @@ LEAF_SIG = {
     "map_product": (VEC2, TERMS),
     "debug_traits": (TRAITS, TRAITS),
     "fft": (CPLX, CPLX),
+    "reduce": (TERMS, "scalar"),
 }
 
 
@@ -235,6 +239,14 @@ def evaluate(node: Node, value, while_counts=None, lengths=None) -> Result:
             return K.dot(vals[0][sl], vals[1][sl])
         if node.op == "+":
             return Result(None, reduced=red(slice(None)))
+        if isinstance(node.op, Leaf):          # device reduction stage
+            if node.op.kind != "reduce":
+                raise ValueError("the reduction stage must be a reduce leaf")
+            rop = node.op.params.get("op", "sum")
+            if rop == "sum":
+                return Result(None, reduced=red(slice(None)))
+            y = vals[1] if m.kind == "map_product" else None
+            return Result(None, reduced=K.fold_extreme(vals[0], y, is_min=(rop == "min")))
         if lengths is None:
             raise ValueError("merging functions other than + need the partition lengths")
         parts, o = [], 0
@@ -276,7 +288,7 @@ def leaves(node: Node):
     if isinstance(node, Map):
         return leaves(node.tree)
     if isinstance(node, MapReduce):
-        return leaves(node.map_stage)
+        return [l for c in _children(node) for l in leaves(c)]
     return leaves(node.body)
 
 
@@ -319,6 +331,6 @@ def _children(n):
         return list(n.stages)
     if isinstance(n, Map):
         return [n.tree]
-    if isinstance(n, MapReduce):
-        return [n.map_stage]
+    if isinstance(n, MapReduce):   # a reduction-stage SCT runs after the map stage
+        return [n.map_stage] + ([n.op] if isinstance(n.op, Leaf) else [])
     return [n.body]

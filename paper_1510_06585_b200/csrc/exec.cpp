@@ -1170,7 +1170,11 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         MW_OK_OR_RETURN(scratch(c, "partials", (size_t)std::max<int64_t>(1, nch) * 8, s, &pp));
         MW_OK_OR_RETURN(scratch(c, "result", 8, s, &rp));
         double* partials = static_cast<double*>(pp);
-        CUDA_OK(cudaMemsetAsync(partials, 0, (size_t)std::max<int64_t>(1, nch) * 8, s));
+        // device reduction stage (MW_REDUCE_*; SUM for mw_map_reduce): chunk
+        // partials start at the operator's identity
+        const int rop = prog[0].reduce_op;
+        MW_OK_OR_RETURN(kerr(mwk::reduce_fill_identity(partials, std::max<int64_t>(1, nch), s, rop),
+                             "reduce_fill"));
         const bool dot = prog[0].dot;
         for (int q = 0; q < ppr; ++q) {
             int p = R.first + q;
@@ -1179,15 +1183,19 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
             MW_OK_OR_RETURN(kerr(mwk::reduce_chunks(at_row<const float>(args[0], R.off[p]),
                                                     dot ? at_row<const float>(args[1], R.off[p]) : nullptr,
                                                     R.off[p], R.off[p], R.len[p], L, partials,
-                                                    launch_for(c, s, p)),
+                                                    launch_for(c, s, p), rop),
                                  "reduce_chunks"));
         }
         // merge "+" across ranks: each chunk partial has exactly
         // one non-zero contributor, so the sum is exact and order-free.
+        // (max / min: one contributor per chunk, the others hold the identity)
         if (c->comm && nch > 0)
-            NCCL_OK(ncclAllReduce(partials, partials, (size_t)nch, ncclFloat64, ncclSum, c->comm, s));
+            NCCL_OK(ncclAllReduce(partials, partials, (size_t)nch, ncclFloat64,
+                                  rop == MW_REDUCE_MAX ? ncclMax : (rop == MW_REDUCE_MIN ? ncclMin : ncclSum),
+                                  c->comm, s));
         if (prog[0].merge_op == MW_MERGE_ADD) {
-            MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s), "reduce_combine"));
+            MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s, rop),
+                                 "reduce_combine"));
             CUDA_OK(cudaMemcpyAsync(f->res, rp, 8, cudaMemcpyDeviceToHost, s));
         } else {
             // NEXT-4 merging functions: every rank holds every chunk partial after

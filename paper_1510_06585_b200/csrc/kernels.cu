@@ -11,7 +11,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cooperative_groups.h>
+#include <math_constants.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -1543,9 +1545,28 @@ __global__ void k_nbody_fin(const double* __restrict__ part, const float4* __res
 // converted exactly; products x*y exact in fp64), then a fixed xor-shuffle
 // tree and a fixed 8-warp tree.  The order depends only on global chunk
 // boundaries, so every distribution vector gives bit-identical partials.
+// OP (MW_REDUCE_*): 0 = fp64 sum; 1 / 2 = maxNum / minNum of the exactly
+// converted terms (a NaN term is ignored), exact in any order.
 constexpr int kRedThreads = 256;
 
-template <bool DOT>
+template <int OP>
+__device__ __forceinline__ double red_op(double a, double b) {
+    if constexpr (OP == 0) return a + b;
+    else if constexpr (OP == 1) return fmax(a, b);
+    else return fmin(a, b);
+}
+template <int OP>
+__device__ __forceinline__ double red_id() {
+    return OP == 0 ? 0.0 : (OP == 1 ? -CUDART_INF : CUDART_INF);
+}
+// one term into the accumulator: sum folds with an fma for products
+template <int OP, bool DOT>
+__device__ __forceinline__ double red_term(double acc, float a, float b) {
+    if constexpr (OP == 0) return DOT ? __fma_rn((double)a, (double)b, acc) : acc + (double)a;
+    else return red_op<OP>(acc, DOT ? (double)a * (double)b : (double)a);
+}
+
+template <bool DOT, int OP>
 __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __restrict__ x,
                                                                const float* __restrict__ y,
                                                                int64_t x0, int64_t first_chunk,
@@ -1558,7 +1579,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
         const int64_t gbase = c * CH;
         const int64_t len = min(CH, total - gbase);
         const int64_t base = gbase - x0;  // local index of the chunk's first element
-        double acc = 0.0;
+        double acc = red_id<OP>();
         const bool vec = len == CH && ((reinterpret_cast<uintptr_t>(x + base) & 15) == 0) &&
                          (!DOT || ((reinterpret_cast<uintptr_t>(y + base) & 15) == 0));
         if (vec) {
@@ -1567,62 +1588,58 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
 #pragma unroll 8
             for (int k = 0; k < (int)(CH / 4 / kRedThreads); ++k) {
                 uint4 a = ld_stream(xv + k * kRedThreads + threadIdx.x);
-                if (DOT) {
-                    uint4 b = ld_stream(yv + k * kRedThreads + threadIdx.x);
-                    acc = __fma_rn((double)__uint_as_float(a.x), (double)__uint_as_float(b.x), acc);
-                    acc = __fma_rn((double)__uint_as_float(a.y), (double)__uint_as_float(b.y), acc);
-                    acc = __fma_rn((double)__uint_as_float(a.z), (double)__uint_as_float(b.z), acc);
-                    acc = __fma_rn((double)__uint_as_float(a.w), (double)__uint_as_float(b.w), acc);
-                } else {
-                    acc += (double)__uint_as_float(a.x);
-                    acc += (double)__uint_as_float(a.y);
-                    acc += (double)__uint_as_float(a.z);
-                    acc += (double)__uint_as_float(a.w);
-                }
+                uint4 b = a;
+                if (DOT) b = ld_stream(yv + k * kRedThreads + threadIdx.x);
+                acc = red_term<OP, DOT>(acc, __uint_as_float(a.x), __uint_as_float(b.x));
+                acc = red_term<OP, DOT>(acc, __uint_as_float(a.y), __uint_as_float(b.y));
+                acc = red_term<OP, DOT>(acc, __uint_as_float(a.z), __uint_as_float(b.z));
+                acc = red_term<OP, DOT>(acc, __uint_as_float(a.w), __uint_as_float(b.w));
             }
         } else {
             for (int k = 0; k < (int)(CH / 4 / kRedThreads); ++k) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     int64_t i = ((int64_t)k * kRedThreads + threadIdx.x) * 4 + e;
-                    if (i < len) {
-                        if (DOT)
-                            acc = __fma_rn((double)x[base + i], (double)y[base + i], acc);
-                        else
-                            acc += (double)x[base + i];
-                    }
+                    if (i < len) acc = red_term<OP, DOT>(acc, x[base + i], DOT ? y[base + i] : 0.f);
                 }
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        for (int o = 16; o > 0; o >>= 1) acc = red_op<OP>(acc, __shfl_xor_sync(0xffffffffu, acc, o));
         if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = acc;
         __syncthreads();
         if (threadIdx.x == 0) {
-            double s = 0.0;
+            double s = red_id<OP>();
 #pragma unroll
-            for (int w = 0; w < kRedThreads / 32; ++w) s += warp_part[w];
+            for (int w = 0; w < kRedThreads / 32; ++w) s = red_op<OP>(s, warp_part[w]);
             partials[c] = s;
         }
         __syncthreads();
     }
 }
 
+template <int OP>
 __global__ void __launch_bounds__(1024) k_reduce_combine(const double* __restrict__ partials,
                                                          int64_t n, double* __restrict__ result) {
     __shared__ double wp[32];
-    double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += 1024) acc += partials[i];
+    double acc = red_id<OP>();
+    for (int64_t i = threadIdx.x; i < n; i += 1024) acc = red_op<OP>(acc, partials[i]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o > 0; o >>= 1) acc = red_op<OP>(acc, __shfl_xor_sync(0xffffffffu, acc, o));
     if ((threadIdx.x & 31) == 0) wp[threadIdx.x >> 5] = acc;
     __syncthreads();
     if (threadIdx.x < 32) {
         double s = wp[threadIdx.x];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        for (int o = 16; o > 0; o >>= 1) s = red_op<OP>(s, __shfl_xor_sync(0xffffffffu, s, o));
         if (threadIdx.x == 0) *result = s;
     }
+}
+
+template <int OP>
+__global__ void k_fill_identity(double* __restrict__ p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = red_id<OP>();
 }
 
 __global__ void k_traits(int64_t* out, int64_t count, int64_t size, int64_t offset) {
@@ -2190,28 +2207,48 @@ cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4*
     return cudaGetLastError();
 }
 
+template <bool DOT, int OP>
+static void reduce_chunks_t(const float* x, const float* y, int64_t x0, int64_t c0, int64_t nc,
+                            int64_t total, double* partials, const Launch& L) {
+    static int occ = resident_ctas(k_reduce_chunks<DOT, OP>, kRedThreads);
+    ++g_launches;
+    k_reduce_chunks<DOT, OP><<<grid_for(nc, occ, L), kRedThreads, 0, L.stream>>>(x, y, x0, c0, nc, total, partials);
+}
+
 cudaError_t reduce_chunks(const float* x, const float* y, int64_t x0, int64_t first,
-                          int64_t count, int64_t total, double* partials, const Launch& L) {
+                          int64_t count, int64_t total, double* partials, const Launch& L,
+                          int op) {
     if (count <= 0) return cudaSuccess;
     const int64_t CH = 1ll << kChunkLog2;
-    if (first % CH != 0) return cudaErrorInvalidValue;
+    if (first % CH != 0 || op < 0 || op > 2) return cudaErrorInvalidValue;
     int64_t c0 = first / CH, nc = (count + CH - 1) / CH;
-    if (y) {
-        static int occ = resident_ctas(k_reduce_chunks<true>, kRedThreads);
-        ++g_launches;
-        k_reduce_chunks<true><<<grid_for(nc, occ, L), kRedThreads, 0, L.stream>>>(x, y, x0, c0, nc, total, partials);
-    } else {
-        static int occ = resident_ctas(k_reduce_chunks<false>, kRedThreads);
-        ++g_launches;
-        k_reduce_chunks<false><<<grid_for(nc, occ, L), kRedThreads, 0, L.stream>>>(x, y, x0, c0, nc, total, partials);
+    switch (op * 2 + (y ? 1 : 0)) {
+        case 0: reduce_chunks_t<false, 0>(x, y, x0, c0, nc, total, partials, L); break;
+        case 1: reduce_chunks_t<true, 0>(x, y, x0, c0, nc, total, partials, L); break;
+        case 2: reduce_chunks_t<false, 1>(x, y, x0, c0, nc, total, partials, L); break;
+        case 3: reduce_chunks_t<true, 1>(x, y, x0, c0, nc, total, partials, L); break;
+        case 4: reduce_chunks_t<false, 2>(x, y, x0, c0, nc, total, partials, L); break;
+        default: reduce_chunks_t<true, 2>(x, y, x0, c0, nc, total, partials, L); break;
     }
     return cudaGetLastError();
 }
 
 cudaError_t reduce_combine(const double* partials, int64_t nchunks, double* result,
-                           cudaStream_t s) {
+                           cudaStream_t s, int op) {
     ++g_launches;
-    k_reduce_combine<<<1, 1024, 0, s>>>(partials, nchunks, result);
+    if (op == 1) k_reduce_combine<1><<<1, 1024, 0, s>>>(partials, nchunks, result);
+    else if (op == 2) k_reduce_combine<2><<<1, 1024, 0, s>>>(partials, nchunks, result);
+    else k_reduce_combine<0><<<1, 1024, 0, s>>>(partials, nchunks, result);
+    return cudaGetLastError();
+}
+
+cudaError_t reduce_fill_identity(double* partials, int64_t n, cudaStream_t s, int op) {
+    if (n <= 0) return cudaSuccess;
+    if (op == 0) return cudaMemsetAsync(partials, 0, (size_t)n * 8, s);
+    ++g_launches;
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 1024);
+    if (op == 1) k_fill_identity<1><<<g, 256, 0, s>>>(partials, n);
+    else k_fill_identity<2><<<g, 256, 0, s>>>(partials, n);
     return cudaGetLastError();
 }
 

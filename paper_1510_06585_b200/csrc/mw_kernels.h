@@ -122,11 +122,15 @@ constexpr int kChunkLog2 = 16;      // canonical reduction chunk: 2^16 elements
 // fp64 partial of every 2^16-element chunk of elements [first, first+count)
 // (first % 2^16 == 0) into partials[chunk index]; y == nullptr: sum, else dot.
 // x[0] (and y[0]) hold global element x0.
+// op: MW_REDUCE_* (0 sum, 1 maxNum, 2 minNum).
 cudaError_t reduce_chunks(const float* x, const float* y, int64_t x0, int64_t first,
-                          int64_t count, int64_t total, double* partials, const Launch& L);
+                          int64_t count, int64_t total, double* partials, const Launch& L,
+                          int op = 0);
 // Fixed-tree combine of nchunks partials into *result (one CTA).
 cudaError_t reduce_combine(const double* partials, int64_t nchunks, double* result,
-                           cudaStream_t s);
+                           cudaStream_t s, int op = 0);
+// partials[0..n) = the operator's identity (0, -inf, +inf)
+cudaError_t reduce_fill_identity(double* partials, int64_t n, cudaStream_t s, int op);
 
 // ------------------------------------------------------------ traits
 cudaError_t fill_traits(int64_t* out, int64_t count, int64_t size, int64_t offset,

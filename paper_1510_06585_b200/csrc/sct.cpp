@@ -52,6 +52,7 @@ static const char* leaf_name(LeafKind k) {
         case LeafKind::MapProduct: return "map_product";
         case LeafKind::DebugTraits: return "debug_traits";
         case LeafKind::Fft: return "fft";
+        case LeafKind::Reduce: return "reduce";
     }
     return "?";
 }
@@ -71,7 +72,8 @@ std::string canonical(const Node* n) {
         case NodeType::Map: return "M(" + canonical(n->kids[0]) + ")";
         case NodeType::MapReduce:   // a user merge hashes by function address
             snprintf(buf, sizeof buf, "R(%d;%p;", n->merge_op, n->merge_op == MW_MERGE_USER ? n->fn : nullptr);
-            return buf + canonical(n->kids[0]) + ")";
+            return buf + canonical(n->kids[0]) +
+                   (n->kids.size() > 1 ? "," + canonical(n->kids[1]) : std::string()) + ")";
         case NodeType::LoopHost:
             snprintf(buf, sizeof buf, "H(%" PRId64 ";%p;", n->n, n->fn);
             return buf + canonical(n->kids[0]) + ")";
@@ -173,6 +175,8 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
             case LeafKind::MapIdentity: s.kind = StepKind::MapStage; s.dot = false; break;
             case LeafKind::MapProduct: s.kind = StepKind::MapStage; s.dot = true; break;
             case LeafKind::Fft: s.kind = StepKind::Fft; s.ops = {op}; break;
+            case LeafKind::Reduce:
+                return fail(MW_E_INVALID_SPEC, "a reduction stage runs only inside mw_map_reduce_sct");
             case LeafKind::DebugTraits:
                 s.kind = StepKind::Traits;
                 s.epu = n->ia;
@@ -204,6 +208,7 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
             s.kind = StepKind::Reduce;
             s.dot = a[0].dot;
             s.merge_op = n->merge_op;
+            s.reduce_op = n->kids.size() > 1 ? (int32_t)n->kids[1]->ia : MW_REDUCE_SUM;
             s.fn = n->fn;
             s.user = n->user;
             out->push_back(s);
@@ -630,6 +635,18 @@ mw_status mw_map_reduce(mw_node* map_stage, int32_t merge_op, mw_node** out) {
     if (merge_op == MW_MERGE_USER)
         return fail(MW_E_INVALID_SPEC, "MW_MERGE_USER needs mw_map_reduce_user (a function)");
     return make_comp(NodeType::MapReduce, &map_stage, 1, out, 0, 1, merge_op);
+}
+mw_status mw_kernel_reduce(int32_t op, mw_node** out) {
+    if (op < MW_REDUCE_SUM || op > MW_REDUCE_MIN) return fail(MW_E_INVALID_SPEC, "unknown reduction operator");
+    return make_leaf(LeafKind::Reduce, MW_VK_TERMS, MW_VK_SCALAR, out, 0, 0, op);
+}
+mw_status mw_map_reduce_sct(mw_node* map_stage, mw_node* reduction_stage, mw_node** out) {
+    if (!reduction_stage) return fail(MW_E_INVALID_SPEC, "NULL reduction stage");
+    const Node* r = reinterpret_cast<const Node*>(reduction_stage);
+    if (r->type != NodeType::Leaf || r->leaf != LeafKind::Reduce)
+        return fail(MW_E_INVALID_SPEC, "the reduction stage must be an mw_kernel_reduce leaf");
+    mw_node* kids[2] = {map_stage, reduction_stage};
+    return make_comp(NodeType::MapReduce, kids, 2, out, 0, 1, MW_MERGE_ADD);
 }
 mw_status mw_map_reduce_user(mw_node* map_stage, mw_merge_fn fn, void* user, mw_node** out) {
     if (!fn) return fail(MW_E_INVALID_SPEC, "NULL merging function");

@@ -21,7 +21,7 @@ mw_status fail(mw_status code, const std::string& msg);
 enum class NodeType { Leaf, Pipeline, Map, MapReduce, LoopFor, LoopWhile, LoopHost };
 enum class LeafKind {
     Saxpy, GaussNoise, Solarize, Mirror, Segment, HystStep, HystFinalize,
-    NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits, Fft
+    NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits, Fft, Reduce
 };
 
 struct Node {
@@ -69,6 +69,7 @@ struct Step {
     int64_t epu = 1, nu = 1;
     bool strict = false;
     int32_t merge_op = 0;              // Reduce: MW_MERGE_*
+    int32_t reduce_op = 0;             // Reduce: MW_REDUCE_* (device reduction stage)
     void* fn = nullptr;
     void* user = nullptr;
 };

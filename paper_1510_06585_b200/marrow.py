@@ -19,6 +19,7 @@ MW_OK = 0
  MW_E_MISSING_ITERATION_COUNT, MW_E_NOT_CONVERGED, MW_E_CUDA, MW_E_NCCL, MW_E_STATE,
  MW_E_OOM, MW_E_UNSUPPORTED) = range(1, 12)
 MW_MERGE_ADD, MW_MERGE_SUB, MW_MERGE_MUL, MW_MERGE_DIV, MW_MERGE_USER = range(5)
+MW_REDUCE_SUM, MW_REDUCE_MAX, MW_REDUCE_MIN = range(3)
 # host callbacks (NEXT-4): merging function and host-side loop condition
 _MERGE_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
 _COND_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p)
@@ -99,6 +100,8 @@ _SIG = {
     "mw_pipeline": [_P(_vp), _i32, _node_pp],
     "mw_map": [_vp, _node_pp],
     "mw_map_reduce": [_vp, _i32, _node_pp],
+    "mw_kernel_reduce": [_i32, _node_pp],
+    "mw_map_reduce_sct": [_vp, _vp, _node_pp],
     "mw_ctx_set_monitoring": [_vp, _i32],
     "mw_map_reduce_user": [_vp, _MERGE_FN, _vp, _node_pp],
     "mw_loop_host": [_vp, _i64, _COND_FN, _vp, _node_pp],
@@ -273,6 +276,17 @@ def mw_map(tree):
 
 def mw_map_reduce(map_stage, merge_op=MW_MERGE_ADD):
     return _new("mw_map_reduce", map_stage.ptr, merge_op, kids=(map_stage,))
+
+
+def mw_kernel_reduce(op=MW_REDUCE_SUM):
+    """Device reduction-stage leaf (NEXT-4, P:191 map_reduce(SCT, SCT))."""
+    return _new("mw_kernel_reduce", op)
+
+
+def mw_map_reduce_sct(map_stage, reduction_stage):
+    """MapReduce whose reduction stage is a device SCT (mw_kernel_reduce)."""
+    return _new("mw_map_reduce_sct", map_stage.ptr, reduction_stage.ptr,
+                kids=(map_stage, reduction_stage))
 
 
 def mw_loop_for(body, n):

@@ -34,6 +34,13 @@ def mapreduce(dot=True):
     return M.mw_map_reduce(m, M.MW_MERGE_ADD)
 
 
+def mapreduce_sct(op, dot=True):
+    """map_reduce(map stage, reduce(op)) with a device reduction stage
+    (NEXT-4, P:191, P:379): op = M.MW_REDUCE_SUM / MAX / MIN."""
+    m = M.mw_kernel_map_product() if dot else M.mw_kernel_map_identity()
+    return M.mw_map_reduce_sct(m, M.mw_kernel_reduce(op))
+
+
 def hysteresis(lo=HYST_LO, hi=HYST_HI, max_iters=10000, check_every=1):
     """pipeline(threshold, loop(step), finalize) — the Fig. 1 shape."""
     return M.mw_pipeline([M.mw_kernel_segment(lo, hi),

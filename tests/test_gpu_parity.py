@@ -184,6 +184,46 @@ def test_mapreduce_vs_oracle_and_canonical(n, dot):
     assert len(vals) == 1, "canonical mode must be bit-identical across distributions"
 
 
+@pytest.mark.parametrize("n", [1, 5, (1 << 16) - 1, 1 << 16, 3 * (1 << 16) + 17, (1 << 22) + 5])
+@pytest.mark.parametrize("dot", [False, True])
+def test_mapreduce_reduction_stage(n, dot):
+    """Device reduction stage (NEXT-4, R28): MAX / MIN bit-exact against
+    the oracle's serial fold for every distribution; SUM bit-identical to the
+    canonical mw_map_reduce(+)."""
+    x = synth.np_f32_um11(5, 0, n)
+    y = synth.np_f32_um11(6, 0, n)
+    args = [M.arg(dev(x))] + ([M.arg(dev(y))] if dot else [])
+    rng = np.random.default_rng(n + dot)
+    for op, is_min in ((M.MW_REDUCE_MAX, False), (M.MW_REDUCE_MIN, True)):
+        want = K.fold_extreme(x, y if dot else None, is_min)
+        for k, d in [(1, None)] + [(4, dd) for dd in dists(4, rng, 2)]:
+            r = run(ctx(k, d), trees.mapreduce_sct(op, dot), args)
+            assert r["reduced"] == want and r["reduced32"] == float(np.float32(want))
+    canon = run(ctx(), trees.mapreduce(dot), args)["reduced"]
+    for k, d in [(1, None), (3, [0.5, 0.0, 0.5])]:
+        assert run(ctx(k, d), trees.mapreduce_sct(M.MW_REDUCE_SUM, dot), args)["reduced"] == canon
+
+
+def test_mapreduce_reduction_stage_edges():
+    e = torch.zeros(0, device=DEV)
+    assert run(ctx(), trees.mapreduce_sct(M.MW_REDUCE_MAX, False), [M.arg(e)])["reduced"] == -np.inf
+    assert run(ctx(), trees.mapreduce_sct(M.MW_REDUCE_MIN, False), [M.arg(e)])["reduced"] == np.inf
+    assert run(ctx(), trees.mapreduce_sct(M.MW_REDUCE_SUM, False), [M.arg(e)])["reduced"] == 0.0
+    z = torch.tensor([np.nan, -2.0, np.nan, 3.0, np.nan], dtype=torch.float32, device=DEV)
+    assert run(ctx(), trees.mapreduce_sct(M.MW_REDUCE_MAX, False), [M.arg(z)])["reduced"] == 3.0
+    assert run(ctx(), trees.mapreduce_sct(M.MW_REDUCE_MIN, False), [M.arg(z)])["reduced"] == -2.0
+    # the maximum in the ragged tail of the last chunk, and the exact product
+    n = 5 * (1 << 16) + 9
+    x = torch.full((n,), -1.0, device=DEV)
+    x[n - 2] = 1 + 2.0 ** -23
+    r = run(ctx(3, [0.2, 0.3, 0.5]), trees.mapreduce_sct(M.MW_REDUCE_MAX, True), [M.arg(x), M.arg(x)])
+    assert r["reduced"] == (1 + 2.0 ** -23) ** 2
+    # a 2^20-element minimum on one partition
+    xs = dev(synth.np_f32_um11(5, 0, 1 << 20))
+    want = run(ctx(), trees.mapreduce_sct(M.MW_REDUCE_MIN, False), [M.arg(xs)])["reduced"]
+    assert want == K.fold_extreme(xs.cpu().numpy(), None, True)
+
+
 def test_mapreduce_closed_forms():
     n = (1 << 25) + 3
     r = run(ctx(), trees.mapreduce(False), [M.arg(torch.ones(n, device=DEV))])

@@ -73,6 +73,20 @@ def test_signatures():
         (M.MW_VK_VEC2, M.MW_VK_SCALAR)
     assert M.mw_node_id(M.mw_map_reduce(M.mw_kernel_map_identity(), M.MW_MERGE_SUB)) != \
         M.mw_node_id(M.mw_map_reduce(M.mw_kernel_map_identity(), M.MW_MERGE_MUL))
+    # device reduction stage (NEXT-4): map stage then reduction stage
+    for op in (M.MW_REDUCE_SUM, M.MW_REDUCE_MAX, M.MW_REDUCE_MIN):
+        t = trees.mapreduce_sct(op)
+        assert M.mw_node_signature(t) == (M.MW_VK_VEC2, M.MW_VK_SCALAR)
+        assert M.mw_kernel_execution_order(t, []) == [0, 1]
+    ids = {M.mw_node_id(trees.mapreduce_sct(op, d)) for op in range(3) for d in (False, True)}
+    assert len(ids) == 6
+    assert M.mw_node_id(trees.mapreduce_sct(M.MW_REDUCE_SUM)) != M.mw_node_id(trees.mapreduce(True))
+    for bad in (lambda: M.mw_kernel_reduce(3), lambda: M.mw_kernel_reduce(-1),
+                lambda: M.mw_map_reduce_sct(M.mw_kernel_map_product(), M.mw_kernel_map_identity()),
+                lambda: M.mw_map_reduce_sct(M.mw_kernel_mirror(), M.mw_kernel_reduce(1))):
+        with pytest.raises(M.MwError) as e:
+            bad()
+        assert e.value.status == M.MW_E_INVALID_SPEC
 
 
 def test_node_id_determinism():

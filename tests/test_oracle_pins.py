@@ -737,6 +737,52 @@ def test_merge_functions_pinned_to_exact_partials():
     assert abs(sct.evaluate(sct.MapReduce(ident, "+"), (x,)).reduced - math.fsum(xs)) < 1e-9
 
 
+def test_reduction_stage_extremes_pinned():
+    """Device reduction stage MAX / MIN (NEXT-4, reading R28): the
+    oracle's serial maxNum/minNum fold is pinned to (a) Python's built-in
+    max/min over the terms as Python floats (fp64; fp32 x*y is exact there) on
+    tiny inputs, (b) closed forms, (c) invariants: max = -min of the negated
+    terms, the fold over a concatenation = the fold of the pieces' folds
+    (any partitioning), NaN terms ignored, empty -> -inf / +inf."""
+    rng = np.random.default_rng(28)
+    for n in (1, 2, 7, 33):
+        x = synth.np_f32_um11(5, 0, n)
+        y = synth.np_f32_um11(6, 0, n)
+        tx = [float(a) for a in x]
+        td = [float(a) * float(b) for a, b in zip(x, y)]
+        assert K.fold_extreme(x) == max(tx) and K.fold_extreme(x, is_min=True) == min(tx)
+        assert K.fold_extreme(x, y) == max(td) and K.fold_extreme(x, y, True) == min(td)
+    # closed forms: x_i = i - k over n elements; x*y with y = -x peaks at 0
+    n, k = 1000, 377
+    x = (np.arange(n) - k).astype(np.float32)
+    assert K.fold_extreme(x) == n - 1 - k and K.fold_extreme(x, is_min=True) == -k
+    assert K.fold_extreme(x, -x) == 0.0 and K.fold_extreme(x, -x, True) == -float(n - 1 - k) ** 2
+    # exact product: (1 + 2^-23)^2 needs 47 bits, kept exactly in fp64
+    a = np.array([1 + 2.0 ** -23], np.float32)
+    assert K.fold_extreme(a, a) == (1 + 2.0 ** -23) ** 2 != float(np.float32(a[0] * a[0]))
+    # invariants
+    x = synth.np_f32_um11(5, 0, 5000)
+    y = synth.np_f32_um11(6, 0, 5000)
+    assert K.fold_extreme(x) == -K.fold_extreme(-x, is_min=True)
+    cuts = np.sort(rng.integers(0, 5000, size=5))
+    pieces = np.split(np.arange(5000), cuts)
+    for is_min in (False, True):
+        parts = [K.fold_extreme(x[p], y[p], is_min) for p in pieces]
+        agg = min(parts) if is_min else max(parts)
+        assert agg == K.fold_extreme(x, y, is_min)
+    z = np.array([np.nan, -2.0, np.nan, 3.0], np.float32)
+    assert K.fold_extreme(z) == 3.0 and K.fold_extreme(z, is_min=True) == -2.0
+    assert K.fold_extreme(np.zeros(0, np.float32)) == -math.inf
+    assert K.fold_extreme(np.zeros(0, np.float32), is_min=True) == math.inf
+    # through the interpreter: reduce('sum') is the '+' fold
+    ident, prod = sct.Leaf("map_identity"), sct.Leaf("map_product")
+    assert sct.evaluate(sct.MapReduce(ident, sct.Leaf("reduce", {"op": "sum"})), (x,)).reduced == \
+        sct.evaluate(sct.MapReduce(ident, "+"), (x,)).reduced
+    assert sct.evaluate(sct.MapReduce(prod, sct.Leaf("reduce", {"op": "max"})), (x, y)).reduced == \
+        max(float(a) * float(b) for a, b in zip(x, y))
+    assert sct.kernel_execution_order(sct.MapReduce(prod, sct.Leaf("reduce", {"op": "min"})), []) == [0, 1]
+
+
 def test_loop_host_reduces_to_loop_for():
     """a host condition that stops at k equals loop_for(body, k)."""
     img = synth.np_rgba(3, 0, 8 * 16).reshape(8, 16, 4)

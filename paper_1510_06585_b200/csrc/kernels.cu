@@ -1119,32 +1119,6 @@ __device__ __forceinline__ void plane_store(const uint32_t (&sv)[ROWS], uint32_t
     }
 }
 
-// One warp tile with plain global loads (the per-partition pass kernel).
-template <int T, int ROWS>
-__device__ __forceinline__ int plane_tile(const uint32_t* __restrict__ in,
-                                          uint32_t* __restrict__ out,
-                                          const uint32_t* __restrict__ K, int64_t rows,
-                                          int64_t wp, int hd, int64_t strip, int64_t cb,
-                                          int steps, int lane) {
-    constexpr int R = ROWS - 2 * T;
-    constexpr int OW = 30;
-    const bool own_lane = lane >= 1 && lane <= OW;
-    const int64_t w = cb * OW - 1 + lane;          // lane 0 / 31: halo words
-    const bool wv = w >= 0 && w < wp;
-    const int64_t ybase = strip * R - T;            // row of register row 0
-    uint32_t sv[ROWS], kv[ROWS];
-#pragma unroll
-    for (int i = 0; i < ROWS; ++i) {
-        const int64_t y = ybase + i;
-        const bool ok = wv && y >= -hd && y < rows + hd;
-        sv[i] = ok ? in[(y + hd) * wp + w] : 0u;
-        kv[i] = ok ? K[(y + hd) * wp + w] : 0u;
-    }
-    const int tile_last = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
-    plane_store<T, ROWS>(sv, out, rows, wp, hd, ybase, w, own_lane, wv);
-    return tile_last;
-}
-
 // is tile t active: some tile of its 3x3 neighbourhood changed last pass, or
 // it touches a partition boundary whose halo may have changed
 __device__ __forceinline__ bool plane_tile_active(const uint8_t* fprev, int64_t strip, int64_t cb,
@@ -1179,6 +1153,79 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, in
         : "memory");
 }
 
+// One pass of a warp over its tiles (t = gw, gw + nwarps, ...): prefetch the
+// next active tile into the warp's slot (sb: S box, kb: K box, bar, phase)
+// while the current one runs its executions; returns the last execution
+// (0-based) in which one of the warp's tiles changed an owned bit.  Buffers
+// hold rows [-hd, rows + hd) at buffer row y + hd; tensor maps cover them.
+template <int T, int ROWS>
+__device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUtensorMap* tk,
+                                               uint32_t* __restrict__ out, int64_t rows,
+                                               int64_t wp, int hd, int steps,
+                                               const uint8_t* __restrict__ fprev,
+                                               uint8_t* __restrict__ fcur, bool all_active,
+                                               int top_nbr, int bot_nbr, int64_t gw,
+                                               int64_t nwarps, int lane, uint32_t* sb,
+                                               uint32_t* kb, uint64_t* bar, uint32_t& phase) {
+    constexpr int R = ROWS - 2 * T;
+    constexpr int OW = 30;
+    constexpr int BW = 36;                          // box width (words)
+    constexpr uint32_t kBox = ROWS * BW * 4;        // bytes per plane box
+    const int64_t n_strips = (rows + R - 1) / R;
+    const int64_t n_cb = (wp + OW - 1) / OW;
+    const int64_t n_tiles = n_strips * n_cb;
+    const bool own_lane = lane >= 1 && lane <= OW;
+    // the next active tile of this warp at or after t (inactive ones are
+    // marked unchanged on the way)
+    auto next_active = [&](int64_t t) {
+        for (; t < n_tiles; t += nwarps) {
+            const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+            if (plane_tile_active(fprev, strip, cb, n_strips, n_cb, all_active, top_nbr, bot_nbr, lane))
+                break;
+            if (lane == 0) fcur[t] = 0;
+        }
+        return t;
+    };
+    auto issue = [&](int64_t t) {
+        if (lane == 0) {
+            const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+            const int x = (int)(cb * OW - 1) & ~3, y = (int)(strip * R - T + hd);
+            mbar_expect_tx(bar, 2 * kBox);
+            tma_load_2d(sb, tin, x, y, bar);
+            tma_load_2d(kb, tk, x, y, bar);
+        }
+    };
+    int my_last = -1;
+    int64_t t = next_active(gw);
+    if (t < n_tiles) issue(t);
+    while (t < n_tiles) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        const int o = (int)((t % n_cb) * OW - 1) & 3;   // tile's first word in the box
+        uint32_t sv[ROWS], kv[ROWS];
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+            sv[i] = sb[i * BW + o + lane];
+            kv[i] = kb[i * BW + o + lane];
+        }
+        __syncwarp();                               // slot free: prefetch the next tile
+        const int64_t tn = next_active(t + nwarps);
+        if (tn < n_tiles) issue(tn);
+        const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+        const int64_t w = cb * OW - 1 + lane;
+        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
+        plane_store<T, ROWS>(sv, out, rows, wp, hd, strip * R - T, w, own_lane, w >= 0 && w < wp);
+        if (lane == 0) fcur[t] = (uint8_t)(tl >= 0);
+        my_last = max(my_last, tl);
+        t = tn;
+    }
+    return my_last;
+}
+
+// The per-warp slots of shared memory: [8][2][ROWS][36] words, then 8 mbarriers.
+template <int ROWS>
+constexpr size_t plane_smem_bytes() { return 8 * 2 * ROWS * 36 * 4 + 8 * 8; }
+
 template <int T, int ROWS>
 __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUtensorMap tm_s0,
                                                      const __grid_constant__ CUtensorMap tm_s1,
@@ -1191,9 +1238,7 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
                                                      uint8_t* __restrict__ tflags,
                                                      unsigned long long* __restrict__ prof) {
     constexpr int R = ROWS - 2 * T;
-    constexpr int OW = 30;
-    constexpr int BW = 36;                          // box width (words)
-    constexpr uint32_t kBox = ROWS * BW * 4;        // bytes per plane box
+    constexpr int BW = 36;
     extern __shared__ __align__(128) uint32_t psm[];   // 8 warp slots, then 8 mbarriers
     uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * ROWS * BW);
     cg::grid_group grid = cg::this_grid();
@@ -1208,11 +1253,8 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
     __syncwarp();
     const int64_t gw = (int64_t)blockIdx.x * 8 + wid;
     const int64_t nwarps = (int64_t)gridDim.x * 8;
-    const int64_t n_strips = (rows + R - 1) / R;
-    const int64_t n_cb = (wp + OW - 1) / OW;
-    const int64_t n_tiles = n_strips * n_cb;
+    const int64_t n_tiles = ((rows + R - 1) / R) * ((wp + 29) / 30);
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    const bool own_lane = lane >= 1 && lane <= OW;
     auto gtime = []() {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1224,56 +1266,11 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
     int pass = 0;
     while (k0 < max_iters) {
         const int steps = (int)min((int64_t)T, max_iters - k0);
-        const CUtensorMap* tin = (pass & 1) ? &tm_s1 : &tm_s0;
-        uint32_t* out = (pass & 1) ? S0 : S1;
-        const uint8_t* fprev = tflags + ((pass + 1) & 1) * n_tiles;
-        uint8_t* fcur = tflags + (pass & 1) * n_tiles;
         if (leader) flags[(pass + 1) % 3] = -1;   // last read two barriers ago
-        // the next active tile of this warp at or after t (inactive ones are
-        // marked unchanged on the way)
-        auto next_active = [&](int64_t t) {
-            for (; t < n_tiles; t += nwarps) {
-                const int64_t strip = t / n_cb, cb = t - strip * n_cb;
-                if (plane_tile_active(fprev, strip, cb, n_strips, n_cb, pass == 0, 0, 0, lane))
-                    break;
-                if (lane == 0) fcur[t] = 0;
-            }
-            return t;
-        };
-        auto issue = [&](int64_t t) {
-            if (lane == 0) {
-                const int64_t strip = t / n_cb, cb = t - strip * n_cb;
-                const int x = (int)(cb * OW - 1) & ~3, y = (int)(strip * R - T + 1);
-                mbar_expect_tx(bar, 2 * kBox);
-                tma_load_2d(sb, tin, x, y, bar);
-                tma_load_2d(kb, &tm_k, x, y, bar);
-            }
-        };
-        int my_last = -1;
-        int64_t t = next_active(gw);
-        if (t < n_tiles) issue(t);
-        while (t < n_tiles) {
-            mbar_wait(bar, phase);
-            phase ^= 1u;
-            const int o = (int)((t % n_cb) * OW - 1) & 3;   // tile's first word in the box
-            uint32_t sv[ROWS], kv[ROWS];
-#pragma unroll
-            for (int i = 0; i < ROWS; ++i) {
-                sv[i] = sb[i * BW + o + lane];
-                kv[i] = kb[i * BW + o + lane];
-            }
-            __syncwarp();                               // slot free: prefetch the next tile
-            const int64_t tn = next_active(t + nwarps);
-            if (tn < n_tiles) issue(tn);
-            const int64_t strip = t / n_cb, cb = t - strip * n_cb;
-            const int64_t w = cb * OW - 1 + lane;
-            const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
-            plane_store<T, ROWS>(sv, out, rows, wp, 1, strip * R - T, w, own_lane,
-                                 w >= 0 && w < wp);
-            if (lane == 0) fcur[t] = (uint8_t)(tl >= 0);
-            my_last = max(my_last, tl);
-            t = tn;
-        }
+        const int my_last = plane_pass_warp<T, ROWS>(
+            (pass & 1) ? &tm_s1 : &tm_s0, &tm_k, (pass & 1) ? S0 : S1, rows, wp, 1, steps,
+            tflags + ((pass + 1) & 1) * n_tiles, tflags + (pass & 1) * n_tiles, pass == 0, 0, 0,
+            gw, nwarps, lane, sb, kb, bar, phase);
         if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
         // the next pass reads `out` through the async (TMA) proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1300,34 +1297,33 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
 }
 
 // One pass over one partition of several (halo depth T, host loop between
-// passes exchanges T plane rows with the neighbours and reduces `last`).
+// passes exchanges T plane rows with the neighbours and reduces `last`);
+// the same TMA-prefetched warp tiles as the one-partition loop.
 template <int T, int ROWS>
-__global__ void __launch_bounds__(256) k_planes_pass(const uint32_t* __restrict__ in,
-                                                     uint32_t* __restrict__ out,
-                                                     const uint32_t* __restrict__ K, int64_t rows,
+__global__ void __launch_bounds__(256) k_planes_pass(const __grid_constant__ CUtensorMap tm_in,
+                                                     const __grid_constant__ CUtensorMap tm_k,
+                                                     uint32_t* __restrict__ out, int64_t rows,
                                                      int64_t wp, int steps, int64_t k0,
                                                      const uint8_t* __restrict__ fprev,
                                                      uint8_t* __restrict__ fcur, int first,
                                                      int top_nbr, int bot_nbr,
                                                      int* __restrict__ last) {
-    constexpr int R = ROWS - 2 * T;
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int64_t nwarps = (int64_t)gridDim.x * 8;
-    const int64_t n_strips = (rows + R - 1) / R;
-    const int64_t n_cb = (wp + 29) / 30;
-    const int64_t n_tiles = n_strips * n_cb;
-    int my_last = -1;
-    for (int64_t t = gw; t < n_tiles; t += nwarps) {
-        const int64_t strip = t / n_cb, cb = t - strip * n_cb;
-        if (!plane_tile_active(fprev, strip, cb, n_strips, n_cb, first != 0, top_nbr, bot_nbr, lane)) {
-            if (lane == 0) fcur[t] = 0;
-            continue;
-        }
-        const int tl = plane_tile<T, ROWS>(in, out, K, rows, wp, T, strip, cb, steps, lane);
-        if (lane == 0) fcur[t] = (uint8_t)(tl >= 0);
-        my_last = max(my_last, tl);
+    constexpr int BW = 36;
+    extern __shared__ __align__(128) uint32_t psm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * ROWS * BW);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* sb = psm + wid * (2 * ROWS * BW);
+    uint32_t* kb = sb + ROWS * BW;
+    uint64_t* bar = &bars[wid];
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncwarp();
+    uint32_t phase = 0;
+    const int my_last = plane_pass_warp<T, ROWS>(
+        &tm_in, &tm_k, out, rows, wp, T, steps, fprev, fcur, first != 0, top_nbr, bot_nbr,
+        (int64_t)blockIdx.x * 8 + wid, (int64_t)gridDim.x * 8, lane, sb, kb, bar, phase);
     if (lane == 0 && my_last >= 0) atomicMax(last, (int)(k0 + my_last));
 }
 
@@ -2058,8 +2054,9 @@ int64_t planes_tiles(int64_t rows, int64_t W) {   // upper bound over the varian
     return ((rows + 7) / 8) * ((plane_words(W) + 29) / 30);
 }
 
-// 2-D tensor map over a plane buffer of (rows + 2) x wp words, box ROWS x 36
-static bool plane_tmap(CUtensorMap* tm, const uint32_t* base, int64_t rows, int64_t wp, int box_rows) {
+// 2-D tensor map over a plane buffer of (rows + 2 hd) x wp words, box ROWS x 36
+static bool plane_tmap(CUtensorMap* tm, const uint32_t* base, int64_t rows, int64_t wp, int box_rows,
+                       int hd = 1) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = []() {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -2069,7 +2066,7 @@ static bool plane_tmap(CUtensorMap* tm, const uint32_t* base, int64_t rows, int6
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
     if (!enc) return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)wp, (cuuint64_t)(rows + 2)};
+    const cuuint64_t dims[2] = {(cuuint64_t)wp, (cuuint64_t)(rows + 2 * hd)};
     const cuuint64_t strides[1] = {(cuuint64_t)wp * 4};
     const cuuint32_t box[2] = {36, (cuuint32_t)box_rows};
     const cuuint32_t es[2] = {1, 1};
@@ -2092,7 +2089,7 @@ template <int T, int ROWS>
 static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows,
                                  int64_t wp, int64_t max_iters, int* flags, int* state,
                                  uint8_t* tflags, const Launch& L) {
-    constexpr size_t smem = 8 * 2 * ROWS * 36 * 4 + 8 * 8;
+    constexpr size_t smem = plane_smem_bytes<ROWS>();
     static int occ = [] {
         cudaFuncSetAttribute(k_planes_loop<T, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
@@ -2129,12 +2126,20 @@ static cudaError_t planes_pass_t(const uint32_t* in, uint32_t* out, const uint32
                                  int64_t wp, int steps, int64_t k0, const uint8_t* fprev,
                                  uint8_t* fcur, int first, int top, int bot, int* last,
                                  const Launch& L) {
-    static int occ = resident_ctas(k_planes_pass<T, ROWS>, 256);
+    constexpr size_t smem = plane_smem_bytes<ROWS>();
+    static int occ = [] {
+        cudaFuncSetAttribute(k_planes_pass<T, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        return resident_ctas(k_planes_pass<T, ROWS>, 256, smem);
+    }();
     constexpr int R = ROWS - 2 * T;
     const int64_t tiles = ((rows + R - 1) / R) * ((wp + 29) / 30);
+    CUtensorMap tin, tk;
+    if (!plane_tmap(&tin, in, rows, wp, ROWS, T) || !plane_tmap(&tk, K, rows, wp, ROWS, T))
+        return cudaErrorInvalidValue;
     ++g_launches;
-    k_planes_pass<T, ROWS><<<grid_for((tiles + 7) / 8, occ, L), 256, 0, L.stream>>>(
-        in, out, K, rows, wp, steps, k0, fprev, fcur, first, top, bot, last);
+    k_planes_pass<T, ROWS><<<grid_for((tiles + 7) / 8, occ, L), 256, smem, L.stream>>>(
+        tin, tk, out, rows, wp, steps, k0, fprev, fcur, first, top, bot, last);
     return cudaGetLastError();
 }
 

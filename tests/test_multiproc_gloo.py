@@ -4,7 +4,7 @@ Each rank takes its slice from the C-ABI partitioner (identical on every
 rank), computes its partition with the oracle's kernels (Offset trait for
 global keys), and the ranks exchange exactly what libmarrow exchanges over
 NCCL: hysteresis halo rows + loop-condition all-reduce, MapReduce partial
-merge "+", N-body COPY re-replication, rebalancer timing all-gather.  The
+merge "+" (and max / min for the device reduction stage), N-body COPY re-replication, rebalancer timing all-gather.  The
 gathered result must equal the single-partition oracle.
 """
 import os
@@ -67,6 +67,16 @@ def _worker(rank, port, results):
     dist.all_reduce(t)
     xs = synth.np_f32_um11(5, 0, n)
     out["mapreduce"] = abs(t.item() - K.sum_(xs)) <= 1e-12 * K.abs_sum(xs)
+    # device reduction stage max / min (NEXT-4, R28): partials merged with the
+    # same operator (libmarrow: NCCL max / min) equal the whole-domain fold
+    y = synth.np_f32_um11(6, off[rank], ln[rank])
+    ys = synth.np_f32_um11(6, 0, n)
+    ok = True
+    for is_min, op in ((False, dist.ReduceOp.MAX), (True, dist.ReduceOp.MIN)):
+        t = torch.tensor([K.fold_extreme(x, y, is_min)], dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        ok &= t.item() == K.fold_extreme(xs, ys, is_min)
+    out["mapreduce_extremes"] = ok
 
     # ---- Hysteresis: halo rows + loop condition all-reduce (Jacobi per partition)
     H, W = 29, 31

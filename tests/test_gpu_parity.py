@@ -468,12 +468,16 @@ def test_config_hysteresis_16384():
     n = 16384
     src = torch.empty((n, n), dtype=torch.uint8, device=DEV)
     synth.dev_fill_u8_stream(src, synth.SEED_HYST, 0)
-    dst = torch.empty_like(src)
-    r = run(ctx(), trees.hysteresis(), [M.arg(src), M.arg(dst)])
     gray = synth.host_u8_stream(synth.SEED_HYST, 0, n * n).reshape(n, n)
     want, D = oracle_hyst(gray)
-    assert r["executions"] == D + 1 == 48
-    assert np.array_equal(dst.cpu().numpy(), want)
+    # one partition (the cooperative plane loop, bench default) and the
+    # per-partition pass protocol of bench --parts / N > 1 (T-row plane halos,
+    # lagged loop condition), uneven and with a zero share
+    for k, d in [(1, None), (8, [0.05, 0.2, 0.1, 0.15, 0.1, 0.1, 0.2, 0.1]), (3, [0.5, 0.0, 0.5])]:
+        dst = torch.zeros_like(src)
+        r = run(ctx(k, d), trees.hysteresis(), [M.arg(src), M.arg(dst)])
+        assert r["executions"] == D + 1 == 48, (k, d)
+        assert np.array_equal(dst.cpu().numpy(), want), (k, d)
 
 
 @pytest.mark.slow

@@ -137,6 +137,15 @@ class Workload:
     kclass = 0
     bound = "hbm"
 
+    def arglist(self, k):
+        """The prebuilt argument array of buffer set k (marshalled once)."""
+        if not hasattr(self, "_al"):
+            self._al = {}
+        al = self._al.get(k)
+        if al is None:
+            al = self._al[k] = self.M.ArgList(list(self.sets[k]))
+        return al
+
     def __init__(self, M, trees, synth, torch, ctx, dev, rank):
         self.M, self.trees, self.synth, self.torch = M, trees, synth, torch
         self.ctx, self.dev, self.rank = ctx, dev, rank
@@ -214,7 +223,7 @@ class Filter(Workload):
                         f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)")
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(i % self.B))
 
     def roof_bytes(self, cls, launches, steps, res):
         return 8.0 * self.n * self.W * steps if cls == self.M.MW_KC_RGBA else 0.0   # this rank's rows
@@ -300,7 +309,7 @@ class Segmentation(Workload):
                         f"{self.B} rotating buffer sets")
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(i % self.B))
 
     def roof_bytes(self, cls, launches, steps, res):
         return 2.0 * self.n * self.shape[1] * self.shape[2] * steps if cls == self.M.MW_KC_U8 else 0.0
@@ -344,7 +353,7 @@ class MapReduce(Workload):
         self.l2_note = f"inputs larger than L2 ({ws >> 20} MiB/rank)"
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, list(self.sets[i % self.B]))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(i % self.B))
 
     def roof_bytes(self, cls, launches, steps, res):
         return (8.0 if self.dot else 4.0) * self.n * steps if cls == self.M.MW_KC_REDUCE else 0.0
@@ -379,7 +388,7 @@ class Hysteresis(Workload):
         self.l2_note = f"ping-pong labels {2 * (self.n + 2) * W >> 20} MiB/rank"
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(0))
 
     def plane(self, launches, steps):
         # bit planes unless disabled (one partition: one cooperative launch per
@@ -433,7 +442,7 @@ class NBody(Workload):
         self.l2_note = "state 32 MiB (compute bound)"
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(0))
 
     def roof_bytes(self, cls, launches, steps, res):   # flops for the ALU-bound row
         return self.launch_flops * steps if cls == self.M.MW_KC_NBODY else 0.0
@@ -485,7 +494,7 @@ class Fft(Workload):
         self.l2_note = f"inputs larger than L2 ({ws >> 20} MiB/rank)"
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(0))
 
     def roof_bytes(self, cls, launches, steps, res):
         # the fused FFT -> IFFT reads and writes each transform once: 2 x 512 KiB

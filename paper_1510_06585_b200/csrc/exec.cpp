@@ -106,6 +106,12 @@ struct mw_ctx {
     bool monitor = true;        // per-partition timing events (mw_ctx_set_monitoring)
     int refs = 1;               // the user's handle + outstanding futures and graphs
     bool destroyed = false;     // mw_ctx_destroy called; teardown at the last release
+    // futures released while their run was still in flight: reclaimed once
+    // their event completed (next mw_run) or at mw_ctx_destroy — releasing a
+    // future never blocks the host, so a loop that drops each future keeps
+    // the device fed
+    std::deque<mw_future*> retired;    // in release order
+    std::vector<cudaEvent_t> fut_ev;   // completion events of released futures, reused
     int tune[mwk::TUNE_COUNT];  // tuning knobs (mw_ctx_set_tuning)
 };
 
@@ -1014,8 +1020,10 @@ mw_status run_loop_host(mw_ctx* c, const Node* root, const mw_arg* args, int nar
 mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
               mw_future* f) {
     if (root->type == mw::NodeType::LoopHost) return run_loop_host(c, root, args, nargs, s, f);
-    std::vector<Step> prog;
-    MW_OK_OR_RETURN(mw::plan(root, &prog));
+    mw_status pst;
+    const mw::NodeCache* nc = mw::plan_cached(root, &pst);
+    if (!nc) return pst;
+    const std::vector<Step>& prog = nc->prog;
     const int ik = root->in_kind, ok = root->out_kind;
     // ---- interface (marrow.h, mw_run)
     int need = (ik == MW_VK_VEC1 || ik == MW_VK_TRAITS) ? 1 : 2;
@@ -1069,11 +1077,14 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         return fail(MW_E_SHAPE_MISMATCH, "args 0 and 1 must have the same global shape");
     const int64_t L = args[0].shape[0];
     // ---- partition (identical on every rank)
-    mw_status st;
-    const int64_t g = mw::granule_of(root, &st);
-    if (st) return st;
+    if (nc->gst) {   // re-derive the granule error message for this call
+        mw_status st;
+        mw::granule_of(root, &st);
+        return st;
+    }
+    const int64_t g = nc->granule;
     RunCtx R{c, s, std::vector<int64_t>(c->P), std::vector<int64_t>(c->P), c->rank * c->ppr};
-    MW_OK_OR_RETURN(mw::partition_plan(L, g, c->dist.data(), c->P, mw::strict_of(root), R.off.data(),
+    MW_OK_OR_RETURN(mw::partition_plan(L, g, c->dist.data(), c->P, nc->strict, R.off.data(),
                                        R.len.data()));
     const int plast = R.first + c->ppr - 1;
     const int64_t s0 = R.off[R.first], s1 = R.off[plast] + R.len[plast];
@@ -1360,12 +1371,15 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
     return MW_OK;
 }
 
+static void reap_retired(mw_ctx* c, bool sync);
+
 static void ctx_teardown(mw_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto& kv : c->scratch) ctx_free(c, kv.second.p);
     if (c->comm) ncclCommDestroy(c->comm);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->fut_ev) cudaEventDestroy(e);
     if (c->wall_a) cudaEventDestroy(c->wall_a);
     if (c->wall_b) cudaEventDestroy(c->wall_b);
     for (int i = 0; i < kStageSlots; ++i) {
@@ -1395,6 +1409,7 @@ mw_status mw_ctx_destroy(mw_ctx* c) {
     if (!c) return fail(MW_E_STATE, "NULL ctx");
     if (c->destroyed) return fail(MW_E_STATE, "ctx already destroyed");
     c->destroyed = true;
+    reap_retired(c, true);   // the retired futures' references (the user's handle remains)
     ctx_release(c);
     return MW_OK;
 }
@@ -1446,6 +1461,7 @@ mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nar
     if (!c || !root || !out || (nargs > 0 && !args)) return fail(MW_E_INVALID_SPEC, "NULL argument");
     if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
     CUDA_OK(cudaSetDevice(c->device));
+    reap_retired(c, false);
     // Consume a stale non-sticky error left in the runtime's last-error slot by
     // an unrelated earlier call (ours or the host application's), so that the
     // post-launch checks below report only this run's launches.  Sticky
@@ -1475,7 +1491,13 @@ mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nar
         c->res_free.push_back(f->res);
         return st;
     }
-    cudaError_t e = cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming);
+    cudaError_t e = cudaSuccess;
+    if (!c->fut_ev.empty()) {
+        f->done = c->fut_ev.back();
+        c->fut_ev.pop_back();
+    } else {
+        e = cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaEventRecord(f->done, s);
     if (e != cudaSuccess) {
         c->res_free.push_back(f->res);
@@ -1548,11 +1570,37 @@ mw_status mw_future_result(mw_future* f, double* out, int32_t n) {
     return MW_OK;
 }
 
+static void future_free(mw_future* f);
+
+// reclaim retired futures whose run completed (sync: wait for all of them)
+static void reap_retired(mw_ctx* c, bool sync) {
+    // oldest first; stop at the first run still in flight (later releases are
+    // usually later runs), so a call costs O(reclaimed + 1) event queries
+    while (!c->retired.empty()) {
+        mw_future* f = c->retired.front();
+        if (!sync && cudaEventQuery(f->done) == cudaErrorNotReady) {
+            (void)cudaGetLastError();   // a NotReady query is not an error of the next call
+            break;
+        }
+        c->retired.pop_front();
+        future_free(f);
+    }
+}
+
 void mw_future_release(mw_future* f) {
     if (!f) return;
+    if (f->done && !f->ctx->destroyed) {   // reclaimed by a later mw_run / mw_ctx_destroy
+        f->ctx->retired.push_back(f);
+        return;
+    }
+    future_free(f);
+}
+
+static void future_free(mw_future* f) {
     if (f->done) {
         cudaEventSynchronize(f->done);
-        cudaEventDestroy(f->done);
+        if (f->ctx->fut_ev.size() < 256) f->ctx->fut_ev.push_back(f->done);
+        else cudaEventDestroy(f->done);
     }
     if (f->res) f->ctx->res_free.push_back(f->res);
     if (f->parts) cudaFreeHost(f->parts);

@@ -401,6 +401,11 @@ __global__ void __launch_bounds__(256) k_rgba_ns_tma(const __grid_constant__ NsC
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTmaStages; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // launched with programmatic stream serialization: the CTA may start
+        // while the previous kernel drains; thread 0 is the only thread that
+        // touches global memory (bulk copies), so it waits here for the
+        // predecessor grid, then lets the next run's grid be scheduled
+        pdl_wait_and_release();
         for (int s = 0; s < kTmaStages; ++s) {
             const int64_t item = blockIdx.x + (int64_t)s * gridDim.x;
             if (item < n_items) {
@@ -1807,8 +1812,18 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
         }();                                                                                   \
         const int64_t items = rows * (W * 4 / CH);                                             \
         ++g_launches;                                                                          \
-        k_rgba_ns_tma<CH, NS, MI, KMI, TI><<<grid_for(items, occ, L), 256, smem, L.stream>>>(  \
-            nc, src, dst, rows, (uint32_t)W, (uint32_t)row0);                                  \
+        cudaLaunchAttribute at[1];                                                             \
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                         \
+        at[0].val.programmaticStreamSerializationAllowed = 1;                                  \
+        cudaLaunchConfig_t cfg = {};                                                           \
+        cfg.gridDim = dim3(grid_for(items, occ, L));                                           \
+        cfg.blockDim = dim3(256);                                                              \
+        cfg.dynamicSmemBytes = smem;                                                           \
+        cfg.stream = L.stream;                                                                 \
+        cfg.attrs = at;                                                                        \
+        cfg.numAttrs = 1;                                                                      \
+        cudaLaunchKernelEx(&cfg, k_rgba_ns_tma<CH, NS, MI, KMI, TI>, nc, src, dst, rows,       \
+                           (uint32_t)W, (uint32_t)row0);                                       \
     } while (0)
 #define MW_TMA_CFG(MI, KMI, TI)                                                                \
     do {                                                                                       \

@@ -33,6 +33,7 @@ void release(Node* n) {
     if (!n) return;
     if (__atomic_sub_fetch(&n->refs, 1, __ATOMIC_ACQ_REL) == 0) {
         for (Node* k : n->kids) release(k);
+        delete n->cache.load(std::memory_order_acquire);
         delete n;
     }
 }
@@ -267,6 +268,28 @@ static int64_t align_of(int kind) {
         case MW_VK_VEC2: return 1 << 16;     // canonical reduction chunk
         default: return 1;                   // one row / slab / element
     }
+}
+
+const NodeCache* plan_cached(const Node* root, mw_status* st) {
+    Node* n = const_cast<Node*>(root);
+    if (const NodeCache* c = n->cache.load(std::memory_order_acquire)) {
+        *st = MW_OK;
+        return c;
+    }
+    NodeCache* c = new NodeCache;
+    *st = plan(root, &c->prog);
+    if (*st != MW_OK) {   // errors are not cached (the message is per call)
+        delete c;
+        return nullptr;
+    }
+    c->granule = granule_of(root, &c->gst);
+    c->strict = strict_of(root);
+    NodeCache* expect = nullptr;
+    if (!n->cache.compare_exchange_strong(expect, c, std::memory_order_acq_rel)) {
+        delete c;   // another thread published first
+        return expect;
+    }
+    return c;
 }
 
 int64_t granule_of(const Node* root, mw_status* st) {

@@ -1,6 +1,7 @@
 // sct.h — host-side skeleton computation tree IR, fusion planner,
 // partitioner and balancer of libmarrow (internal; the ABI is marrow.h).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -24,8 +25,12 @@ enum class LeafKind {
     NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits, Fft, Reduce
 };
 
+struct Step;
+struct NodeCache;   // per-node run plan, computed once (see plan_cached)
+
 struct Node {
     int refs = 1;
+    std::atomic<NodeCache*> cache{nullptr};   // immutable once published
     NodeType type = NodeType::Leaf;
     // leaf
     LeafKind leaf = LeafKind::Saxpy;
@@ -74,6 +79,17 @@ struct Step {
     void* user = nullptr;
 };
 mw_status plan(const Node* root, std::vector<Step>* out);
+
+// The plan, granule and strict flag of a node depend only on the (immutable)
+// tree: computed on first use and published once (compare-exchange), so
+// repeated runs of a tree skip the planner.  Returns nullptr + *st on error.
+struct NodeCache {
+    std::vector<Step> prog;
+    int64_t granule = 1;
+    bool strict = false;
+    mw_status gst = MW_OK;   // granule status (reported when the plan is run)
+};
+const NodeCache* plan_cached(const Node* root, mw_status* st);
 
 // ------------------------------------------------------------ partitioner / balancer
 int64_t granule_of(const Node* root, mw_status* st);

@@ -512,17 +512,46 @@ class Future:
         return mw_future_result(self)
 
 
+class ArgList:
+    """The ctypes argument array of a run, built once: pass it to mw_run in
+    place of a list to skip the per-call marshalling (repeated runs on the
+    same buffers, e.g. a benchmark loop)."""
+    __slots__ = ("arr", "n", "owners")
+
+    def __init__(self, args):
+        self.arr = (mw_arg * len(args))(*args)
+        self.n = len(args)
+        self.owners = [getattr(a, "_owner", None) for a in args]
+
+
+_run_fn = None
+
+
+def _current_stream_ptr():
+    import torch
+    try:
+        return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
+    except AttributeError:  # pragma: no cover
+        return torch.cuda.current_stream().cuda_stream
+
+
 def mw_run(ctx, node, args, stream=None):
     """Enqueue a run on `stream` (torch.cuda.Stream or raw cudaStream_t int;
-    default: torch's current stream)."""
+    default: torch's current stream).  args: a list of mw_arg or an ArgList."""
+    global _run_fn
+    if _run_fn is None:
+        _run_fn = lib().mw_run
+    if not isinstance(args, ArgList):
+        args = ArgList(args)
     if stream is None:
-        import torch
-        stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-    arr = (mw_arg * len(args))(*args)
+        sp = _current_stream_ptr()
+    else:
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = _vp()
-    _call("mw_run", ctx.ptr, node.ptr, arr, len(args), _vp(sp), ctypes.byref(out))
-    return Future(out, (arr, node, ctx, [getattr(a, "_owner", None) for a in args]))
+    st = _run_fn(ctx.ptr, node.ptr, args.arr, args.n, _vp(sp), ctypes.byref(out))
+    if st != MW_OK:
+        _chk(st, "mw_run")
+    return Future(out, (args, node, ctx))
 
 
 def mw_future_wait(f):

@@ -1048,6 +1048,9 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // One execution on register rows [LO, HI] (rows outside keep their values
 // and only serve as neighbours); returns whether an owned row [T, ROWS - T)
 // of an owned lane changed.
+// One execution on register rows [LO, HI] (rows outside keep their values
+// and only serve as neighbours); returns whether an owned row [T, ROWS - T)
+// of an owned lane changed.
 template <int T, int ROWS, int LO, int HI>
 __device__ __forceinline__ bool plane_exec(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
                                            bool own_lane) {
@@ -1073,14 +1076,14 @@ __device__ __forceinline__ bool plane_exec(uint32_t (&sv)[ROWS], const uint32_t 
     return __any_sync(0xffffffffu, own_lane && ch != 0);
 }
 
-// T executions on a register tile (rows [ybase, ybase + ROWS) x lanes);
-// returns the last execution (0-based) that changed an owned bit.  Row r is
-// exact after execution st when st < r < ROWS - 1 - st (validity shrinks by
-// a row per execution at each end), so a full pass computes rows [1, ROWS-2]
-// in its first T/2 executions and only [T/2 + 1, ROWS - 2 - T/2] in the
-// rest (a superset of what each later execution needs); executions run in
-// pairs so the updated rows alternate between two register sets instead of
-// being moved back every execution.
+// T executions on a register tile (rows [ybase, ybase + ROWS) x lanes).
+// Row r is exact after execution st when st < r < ROWS - 1 - st (validity
+// shrinks by a row per execution at each end), so a full pass computes rows
+// [1, ROWS-2] in its first T/2 executions and only [T/2 + 1, ROWS - 2 - T/2]
+// in the rest (a superset of what each later execution needs); executions
+// run in pairs so the updated rows alternate between two register sets
+// instead of being moved back every execution.
+// Returns the last execution (0-based) that changed an owned bit.
 template <int T, int ROWS>
 __device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
                                            int steps, bool own_lane) {
@@ -1124,8 +1127,13 @@ __device__ __forceinline__ void plane_store(const uint32_t (&sv)[ROWS], uint32_t
     }
 }
 
-// is tile t active: some tile of its 3x3 neighbourhood changed last pass, or
-// it touches a partition boundary whose halo may have changed
+// is tile t active: some tile of its 3x3 neighbourhood changed in the last
+// execution of the previous pass (flag bit 0), the tile itself changed at any
+// execution of it (bit 1: its newest state must reach this pass's output
+// buffer), or it touches a partition boundary whose halo may have changed.
+// A front that stopped before the last execution of a pass changes nothing
+// later, and one alive at it moves at most T pixels in the next pass, which
+// stays inside the 3x3 tile neighbourhood (T <= R rows, T <= 30 words).
 __device__ __forceinline__ bool plane_tile_active(const uint8_t* fprev, int64_t strip, int64_t cb,
                                                   int64_t n_strips, int64_t n_cb, bool first,
                                                   int top_nbr, int bot_nbr, int lane) {
@@ -1134,7 +1142,8 @@ __device__ __forceinline__ bool plane_tile_active(const uint8_t* fprev, int64_t 
         bool a = false;
         if (lane < 9) {
             const int64_t s2 = strip + lane / 3 - 1, c2 = cb + lane % 3 - 1;
-            a = s2 >= 0 && s2 < n_strips && c2 >= 0 && c2 < n_cb && fprev[s2 * n_cb + c2];
+            a = s2 >= 0 && s2 < n_strips && c2 >= 0 && c2 < n_cb &&
+                (fprev[s2 * n_cb + c2] & (lane == 4 ? 3 : 1));
         }
         act = __any_sync(0xffffffffu, a);
     }
@@ -1171,7 +1180,8 @@ __device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUt
                                                uint8_t* __restrict__ fcur, bool all_active,
                                                int top_nbr, int bot_nbr, int64_t gw,
                                                int64_t nwarps, int lane, uint32_t* sb,
-                                               uint32_t* kb, uint64_t* bar, uint32_t& phase) {
+                                               uint32_t* kb, uint64_t* bar, uint32_t& phase,
+                                               bool last_bit = false) {
     constexpr int R = ROWS - 2 * T;
     constexpr int OW = 30;
     constexpr int BW = 36;                          // box width (words)
@@ -1219,9 +1229,14 @@ __device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUt
         const int64_t strip = t / n_cb, cb = t - strip * n_cb;
         const int64_t w = cb * OW - 1 + lane;
         const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
-        plane_store<T, ROWS>(sv, out, rows, wp, hd, strip * R - T, w, own_lane, w >= 0 && w < wp);
-        if (lane == 0) fcur[t] = (uint8_t)(tl >= 0);
+        // bit 0: changed in the last execution of the pass (fronts still alive);
+        // bit 1: changed at all.  last_bit: with the tighter rule of the
+        // one-partition loop, bit 0 only for a change in the last execution,
+        // otherwise bit 0 = bit 1 (any change, the rule of the pass kernel).
+        const uint8_t fl = tl < 0 ? 0 : (tl == steps - 1 || !last_bit ? 3 : 2);
         my_last = max(my_last, tl);
+        plane_store<T, ROWS>(sv, out, rows, wp, hd, strip * R - T, w, own_lane, w >= 0 && w < wp);
+        if (lane == 0) fcur[t] = fl;
         t = tn;
     }
     return my_last;
@@ -1275,7 +1290,7 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
         const int my_last = plane_pass_warp<T, ROWS>(
             (pass & 1) ? &tm_s1 : &tm_s0, &tm_k, (pass & 1) ? S0 : S1, rows, wp, 1, steps,
             tflags + ((pass + 1) & 1) * n_tiles, tflags + (pass & 1) * n_tiles, pass == 0, 0, 0,
-            gw, nwarps, lane, sb, kb, bar, phase);
+            gw, nwarps, lane, sb, kb, bar, phase, true);
         if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
         // the next pass reads `out` through the async (TMA) proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -961,3 +961,25 @@ def test_loop_host_condition():
     with pytest.raises(M.MwError):
         run(ctx(1), M.mw_pipeline([M.mw_loop_host(M.mw_kernel_mirror(), 2, lambda i: True), M.mw_kernel_mirror()]),
             [M.arg(src), M.arg(torch.empty_like(src))])
+
+
+def test_released_futures_and_arglist():
+    """Futures dropped without waiting are reclaimed by later runs (release
+    never blocks); a prebuilt ArgList gives the same bytes as a list; a ctx
+    destroyed with runs in flight drains them first."""
+    H, W = 256, 512
+    img = synth.np_rgba(3, 0, H * W).reshape(H, W, 4)
+    want = oracle_filter(img)
+    c = ctx(2, [0.5, 0.5])
+    src = dev(img)
+    outs = [torch.empty((H, W, 4), dtype=torch.uint8, device=DEV) for _ in range(4)]
+    lists = [M.ArgList([M.arg(src), M.arg(o)]) for o in outs]
+    for i in range(300):
+        M.mw_run(c, trees.filter_pipeline(), lists[i % 4] if i % 2 else [M.arg(src), M.arg(outs[i % 4])])
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy(), want)
+    tail = M.mw_run(c, trees.filter_pipeline(), lists[0])
+    M.mw_ctx_destroy(c)
+    tail.wait()
+    assert np.array_equal(outs[0].cpu().numpy(), want)

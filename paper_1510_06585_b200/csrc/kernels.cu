@@ -1230,9 +1230,9 @@ __device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUt
         const int64_t w = cb * OW - 1 + lane;
         const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
         // bit 0: changed in the last execution of the pass (fronts still alive);
-        // bit 1: changed at all.  last_bit: with the tighter rule of the
-        // one-partition loop, bit 0 only for a change in the last execution,
-        // otherwise bit 0 = bit 1 (any change, the rule of the pass kernel).
+        // bit 1: changed at all.  last_bit = false: bit 0 = bit 1 (the looser
+        // any-change rule; both kernels use the tight one — boundary strips of
+        // a partition with a neighbour are active every pass regardless).
         const uint8_t fl = tl < 0 ? 0 : (tl == steps - 1 || !last_bit ? 3 : 2);
         my_last = max(my_last, tl);
         plane_store<T, ROWS>(sv, out, rows, wp, hd, strip * R - T, w, own_lane, w >= 0 && w < wp);
@@ -1343,7 +1343,7 @@ __global__ void __launch_bounds__(256) k_planes_pass(const __grid_constant__ CUt
     uint32_t phase = 0;
     const int my_last = plane_pass_warp<T, ROWS>(
         &tm_in, &tm_k, out, rows, wp, T, steps, fprev, fcur, first != 0, top_nbr, bot_nbr,
-        (int64_t)blockIdx.x * 8 + wid, (int64_t)gridDim.x * 8, lane, sb, kb, bar, phase);
+        (int64_t)blockIdx.x * 8 + wid, (int64_t)gridDim.x * 8, lane, sb, kb, bar, phase, true);
     if (lane == 0 && my_last >= 0) atomicMax(last, (int)(k0 + my_last));
 }
 

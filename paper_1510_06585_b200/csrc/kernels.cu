@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <cooperative_groups.h>
 #include <math_constants.h>
 #include <cuda.h>
@@ -2096,13 +2098,44 @@ static bool plane_tmap(CUtensorMap* tm, const uint32_t* base, int64_t rows, int6
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
     if (!enc) return false;
+    // encoded maps are cached by (buffer, shape): the per-partition pass kernel
+    // launches twice per partition and pass on the same scratch planes
+    struct Key {
+        const void* p;
+        int64_t rows, wp;
+        int box, hd;
+        bool operator==(const Key& o) const {
+            return p == o.p && rows == o.rows && wp == o.wp && box == o.box && hd == o.hd;
+        }
+    };
+    struct Hash {
+        size_t operator()(const Key& k) const {
+            return std::hash<const void*>()(k.p) ^ (size_t)(k.rows * 1000003 + k.wp * 131 + k.box * 7 + k.hd);
+        }
+    };
+    static std::mutex mu;
+    static std::unordered_map<Key, CUtensorMap, Hash> cache;
+    const Key key{base, rows, wp, box_rows, hd};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *tm = it->second;
+            return true;
+        }
+    }
     const cuuint64_t dims[2] = {(cuuint64_t)wp, (cuuint64_t)(rows + 2 * hd)};
     const cuuint64_t strides[1] = {(cuuint64_t)wp * 4};
     const cuuint32_t box[2] = {36, (cuuint32_t)box_rows};
     const cuuint32_t es[2] = {1, 1};
-    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides,
-               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() > 4096) cache.clear();   // bounded (freed scratch leaves stale keys)
+    cache[key] = *tm;
+    return true;
 }
 
 // MW_HYST_PROF=1: per-pass device timestamps of the loop kernel to stderr

@@ -746,7 +746,8 @@ def run_marrow(args, dist, wl_name):
     if bound == "alu":
         peak, unit, src = alu_peak["nbody" if wl_name == "nbody" else "hysteresis"]
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
-                "frac": achieved / peak, "traffic": None, "peak_src": src, "kernel": kname,
+                "frac": achieved / peak, "traffic": traffic_from_profile(wl_name),
+                "peak_src": src, "kernel": kname,
                 "kernel_launches": kn, "kernel_avg_us": 1e3 * kms / max(1, kn),
                 "kernel_time_source": ksrc}
         if wl_name == "nbody":

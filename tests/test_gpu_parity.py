@@ -983,3 +983,23 @@ def test_released_futures_and_arglist():
     M.mw_ctx_destroy(c)
     tail.wait()
     assert np.array_equal(outs[0].cpu().numpy(), want)
+
+
+def test_plan_cache_errors_not_cached():
+    """The per-node plan cache publishes only successful plans: a tree that
+    cannot run reports its error on every run, and a shared subtree planned
+    inside several roots gives the same bytes each time."""
+    c = ctx()
+    bad = M.mw_kernel_reduce(M.MW_REDUCE_MAX)   # a reduction stage runs only inside map_reduce_sct
+    x = torch.ones(100, device=DEV)
+    for _ in range(2):
+        with pytest.raises(M.MwError) as e:
+            run(c, bad, [M.arg(x)])
+        assert e.value.status == M.MW_E_INVALID_SPEC
+    m = M.mw_kernel_map_identity()
+    t1 = M.mw_map_reduce_sct(m, M.mw_kernel_reduce(M.MW_REDUCE_MAX))
+    t2 = M.mw_map_reduce(m, M.MW_MERGE_ADD)
+    xs = dev(synth.np_f32_um11(5, 0, 5000))
+    for _ in range(3):
+        assert run(c, t1, [M.arg(xs)])["reduced"] == K.fold_extreme(xs.cpu().numpy())
+        assert run(c, t2, [M.arg(xs)])["reduced"] == K.sum_(xs.cpu().numpy())

@@ -176,20 +176,46 @@ class Workload:
         if self.e2e_mode == "staged":
             self.e2e_args = [self._host_arg(a) for a in st]
             return h2d, d2h
-        self.e2e_h_in = [(self._host_arg(st[i])._owner, st[i]._owner) for i in self.e2e_in]
-        self.e2e_h_out = [(st[i]._owner, self.torch.empty(tuple(st[i]._owner.shape),
-                                                          dtype=st[i]._owner.dtype).pin_memory())
-                          for i in self.e2e_out]
+        # Two device buffer sets on two streams: step i+1's uploads overlap
+        # step i's downloads (PCIe duplex); the runs themselves stay in FIFO
+        # order (each waits for the previous run: the ctx scratch is shared).
+        torch, M = self.torch, self.M
+
+        def clone(a):
+            t2 = torch.empty_like(a._owner)
+            return M.arg(t2, mode=a.mode, local_offset=a.local_offset,
+                         global_shape=tuple(a.shape[k] for k in range(a.ndim)))
+        dsets = [list(st), [clone(a) for a in st]]
+        host_in = [self._host_arg(st[i])._owner for i in self.e2e_in]
+        self.e2e_slots = []
+        for ds in dsets:
+            outs = [(ds[i]._owner, torch.empty(tuple(ds[i]._owner.shape),
+                                               dtype=ds[i]._owner.dtype).pin_memory())
+                    for i in self.e2e_out]
+            ins = [(h, ds[i]._owner) for h, i in zip(host_in, self.e2e_in)]
+            self.e2e_slots.append((torch.cuda.Stream(device=self.dev), ds, ins, outs))
+        self.e2e_streams = [sl[0] for sl in self.e2e_slots]
+        self.e2e_i = 0
+        self.e2e_prev = None
         return h2d, d2h
 
     def e2e_step(self):
         if self.e2e_mode == "staged":
             return self.M.mw_run(self.ctx, self.tree, self.e2e_args)
-        for h, d in self.e2e_h_in:
-            d.copy_(h, non_blocking=True)
-        f = self.M.mw_run(self.ctx, self.tree, list(self.sets[0]))
-        for d, h in self.e2e_h_out:
-            h.copy_(d, non_blocking=True)
+        torch = self.torch
+        s, ds, ins, outs = self.e2e_slots[self.e2e_i % 2]
+        self.e2e_i += 1
+        with torch.cuda.stream(s):
+            for h, d in ins:
+                d.copy_(h, non_blocking=True)
+            if self.e2e_prev is not None:
+                s.wait_event(self.e2e_prev)
+            f = self.M.mw_run(self.ctx, self.tree, ds, stream=s)
+            ev = torch.cuda.Event()
+            ev.record(s)
+            self.e2e_prev = ev
+            for d, h in outs:
+                h.copy_(d, non_blocking=True)
         return f
 
     def slice(self, L):
@@ -782,7 +808,11 @@ def run_marrow(args, dist, wl_name):
         torch.cuda.synchronize()
         dist.barrier()
         start.record(stream)
+        for es in getattr(w, "e2e_streams", []):
+            es.wait_stream(stream)
         futs = [w.e2e_step() for _ in range(ek)]
+        for es in getattr(w, "e2e_streams", []):
+            stream.wait_stream(es)
         stop.record(stream)
         torch.cuda.synchronize()
         del futs
@@ -792,8 +822,9 @@ def run_marrow(args, dist, wl_name):
                        "steps": ek,
                        "path": ("mw_run with MW_LOC_HOST pinned buffers (library-staged chunked "
                                 "H2D/compute/D2H overlap on 3 streams)" if w.e2e_mode == "staged" else
-                                "pinned H2D of the inputs + mw_run + D2H of the result on the run's "
-                                "stream (tree not host-stageable)")}
+                                "pinned H2D of the inputs + mw_run + D2H of the result, two device "
+                                "buffer sets on two streams (uploads of step i+1 overlap downloads of "
+                                "step i; runs in FIFO order) (tree not host-stageable)")}
     else:
         line["e2e"] = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:

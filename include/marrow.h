@@ -281,6 +281,10 @@ mw_status mw_future_query(mw_future* f, int32_t* done);
  * out[2] = while-loop executions E (total over all while loops), out[3] = 1
  * if every while loop converged else 0.  n <= 4 values are written.         */
 mw_status mw_future_result(mw_future* f, double* out, int32_t n);
+/* Releases the handle without blocking: a run still in flight is retired and
+ * its resources are reclaimed once it completes (by a later mw_run on the
+ * same ctx, or at mw_ctx_destroy, which waits for retired runs).  The buffers
+ * the run reads and writes must stay valid until it completes.             */
 void mw_future_release(mw_future* f);
 
 /* ------------------------------------------------------------------ graphs

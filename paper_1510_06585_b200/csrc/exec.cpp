@@ -124,6 +124,7 @@ struct mw_future {
     double executions = 0.0;
     double converged = 1.0;
     bool waited = false;
+    bool completed = false;    // a query or wait saw the run complete
     // MapReduce with a non-ADD merging function: per-partition partials (pinned)
     double* parts = nullptr;
     std::vector<char> part_active;
@@ -1533,6 +1534,7 @@ mw_status mw_future_query(mw_future* f, int32_t* done) {
     }
     if (e != cudaSuccess) return fail(MW_E_CUDA, std::string("run failed: ") + cudaGetErrorString(e));
     *done = 1;
+    f->completed = true;
     return MW_OK;
 }
 
@@ -1589,7 +1591,7 @@ static void reap_retired(mw_ctx* c, bool sync) {
 
 void mw_future_release(mw_future* f) {
     if (!f) return;
-    if (f->done && !f->ctx->destroyed) {   // reclaimed by a later mw_run / mw_ctx_destroy
+    if (f->done && !f->ctx->destroyed && !f->completed && !f->waited) {   // reclaimed later
         f->ctx->retired.push_back(f);
         return;
     }

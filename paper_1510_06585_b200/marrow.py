@@ -411,6 +411,10 @@ class Ctx:
 
     def destroy(self):
         if getattr(self, "ptr", None) and _lib is not None:
+            try:
+                _reap_pending(all_of_ctx=self)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
             _lib.mw_ctx_destroy(self.ptr)
             self.ptr = None
 
@@ -494,6 +498,40 @@ def arg(t, mode=MW_PARTITION, local_offset=0, global_shape=None):
     return a
 
 
+# Futures dropped while their run is still in flight: the handle and the
+# argument owners are parked here (release order) and released once the run
+# completes — checked oldest-first by every mw_run, so dropping a future never
+# blocks and torch's caching allocator cannot hand a dropped argument's memory
+# to a new tensor before the run has used it.
+import collections as _collections
+
+_pending = _collections.deque()
+
+
+_reaping = [False]
+
+
+def _reap_pending(all_of_ctx=None):
+    if _reaping[0]:   # re-entered from a destructor run by the garbage collector
+        return
+    _reaping[0] = True
+    try:
+        if all_of_ctx is not None:   # ctx teardown: release its parked futures
+            for item in [it for it in _pending if it[1][2] is all_of_ctx]:
+                _pending.remove(item)
+                _lib.mw_future_release(item[0])
+            return
+        while _pending:
+            item = _pending.popleft()
+            d = _i32()
+            if _lib.mw_future_query(item[0], ctypes.byref(d)) == MW_OK and not d.value:
+                _pending.appendleft(item)   # oldest still in flight: stop
+                break
+            _lib.mw_future_release(item[0])
+    finally:
+        _reaping[0] = False
+
+
 class Future:
     def __init__(self, ptr, keep):
         self.ptr = ptr
@@ -501,7 +539,10 @@ class Future:
 
     def __del__(self):
         if getattr(self, "ptr", None) and _lib is not None:
-            _lib.mw_future_release(self.ptr)
+            if self._keep and getattr(self._keep[2], "ptr", None):
+                _pending.append((self.ptr, self._keep))   # maybe in flight: park it
+            else:
+                _lib.mw_future_release(self.ptr)
             self.ptr = None
 
     def wait(self):
@@ -547,6 +588,8 @@ def mw_run(ctx, node, args, stream=None):
         sp = _current_stream_ptr()
     else:
         sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    if len(_pending) > 32:   # amortised: one completion query per reclaimed run
+        _reap_pending()
     out = _vp()
     st = _run_fn(ctx.ptr, node.ptr, args.arr, args.n, _vp(sp), ctypes.byref(out))
     if st != MW_OK:

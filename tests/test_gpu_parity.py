@@ -1003,3 +1003,24 @@ def test_plan_cache_errors_not_cached():
     for _ in range(3):
         assert run(c, t1, [M.arg(xs)])["reduced"] == K.fold_extreme(xs.cpu().numpy())
         assert run(c, t2, [M.arg(xs)])["reduced"] == K.sum_(xs.cpu().numpy())
+
+
+def test_dropped_future_keeps_temporaries_alive():
+    """A future dropped while its run is in flight, together with the only
+    reference to a temporary input, on a side stream: the caching allocator
+    must not hand the input's memory to a new tensor before the run read it."""
+    H, W = 2048, 2048
+    img = synth.np_rgba(3, 0, H * W).reshape(H, W, 4)
+    want = oracle_filter(img)
+    c = ctx()
+    side = torch.cuda.Stream()
+    dst = torch.empty((H, W, 4), dtype=torch.uint8, device=DEV)
+    for _ in range(5):
+        tmp = dev(img)                     # allocated on the default stream
+        side.wait_stream(torch.cuda.current_stream())
+        M.mw_run(c, trees.filter_pipeline(), [M.arg(tmp), M.arg(dst)], stream=side)
+        del tmp                            # future and input dropped at once
+        junk = torch.full((H, W, 4), 7, dtype=torch.uint8, device=DEV)   # may reuse the block
+        del junk
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.cpu().numpy(), want)

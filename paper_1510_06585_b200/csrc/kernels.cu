@@ -1559,7 +1559,7 @@ __global__ void k_nbody_fin(const double* __restrict__ part, const float4* __res
 
 // ------------------------------------------------------------ MapReduce
 // One CTA per canonical 2^16-element chunk; thread t folds elements
-// (k*256 + t)*4 + e, k = 0..63, e = 0..3, in that order in fp64 (each fp32
+// (k*256 + t)*4 + e, k = 0..63, into accumulator e = 0..3 in fp64 (each fp32
 // converted exactly; products x*y exact in fp64), then a fixed xor-shuffle
 // tree and a fixed 8-warp tree.  The order depends only on global chunk
 // boundaries, so every distribution vector gives bit-identical partials.
@@ -1597,7 +1597,11 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
         const int64_t gbase = c * CH;
         const int64_t len = min(CH, total - gbase);
         const int64_t base = gbase - x0;  // local index of the chunk's first element
-        double acc = red_id<OP>();
+        // four independent accumulators (element e of each 4-vector), joined
+        // as (a0 . a1) . (a2 . a3): a fixed order, so partials stay
+        // independent of the partitioning; four chains instead of one
+        // dependent chain of 256 fp64 operations per thread
+        double acc4[4] = {red_id<OP>(), red_id<OP>(), red_id<OP>(), red_id<OP>()};
         const bool vec = len == CH && ((reinterpret_cast<uintptr_t>(x + base) & 15) == 0) &&
                          (!DOT || ((reinterpret_cast<uintptr_t>(y + base) & 15) == 0));
         if (vec) {
@@ -1608,20 +1612,21 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
                 uint4 a = ld_stream(xv + k * kRedThreads + threadIdx.x);
                 uint4 b = a;
                 if (DOT) b = ld_stream(yv + k * kRedThreads + threadIdx.x);
-                acc = red_term<OP, DOT>(acc, __uint_as_float(a.x), __uint_as_float(b.x));
-                acc = red_term<OP, DOT>(acc, __uint_as_float(a.y), __uint_as_float(b.y));
-                acc = red_term<OP, DOT>(acc, __uint_as_float(a.z), __uint_as_float(b.z));
-                acc = red_term<OP, DOT>(acc, __uint_as_float(a.w), __uint_as_float(b.w));
+                acc4[0] = red_term<OP, DOT>(acc4[0], __uint_as_float(a.x), __uint_as_float(b.x));
+                acc4[1] = red_term<OP, DOT>(acc4[1], __uint_as_float(a.y), __uint_as_float(b.y));
+                acc4[2] = red_term<OP, DOT>(acc4[2], __uint_as_float(a.z), __uint_as_float(b.z));
+                acc4[3] = red_term<OP, DOT>(acc4[3], __uint_as_float(a.w), __uint_as_float(b.w));
             }
         } else {
             for (int k = 0; k < (int)(CH / 4 / kRedThreads); ++k) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     int64_t i = ((int64_t)k * kRedThreads + threadIdx.x) * 4 + e;
-                    if (i < len) acc = red_term<OP, DOT>(acc, x[base + i], DOT ? y[base + i] : 0.f);
+                    if (i < len) acc4[e] = red_term<OP, DOT>(acc4[e], x[base + i], DOT ? y[base + i] : 0.f);
                 }
             }
         }
+        double acc = red_op<OP>(red_op<OP>(acc4[0], acc4[1]), red_op<OP>(acc4[2], acc4[3]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc = red_op<OP>(acc, __shfl_xor_sync(0xffffffffu, acc, o));
         if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = acc;

@@ -894,6 +894,9 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
                                                      uint32_t* __restrict__ S,
                                                      uint32_t* __restrict__ K, FastDiv WP, int hd) {
     const uint32_t total = (uint32_t)(rows * wp);
+    uint32_t one;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(one));
+    one = one > 0u ? 1u : 0u;
     for (uint32_t n = blockIdx.x * 256u + threadIdx.x; n < total; n += gridDim.x * 256u) {
         const uint32_t y = fdiv(n, WP), w = n - y * WP.d;
         const int64_t x0 = 32ll * w;
@@ -920,13 +923,21 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
             // the chain is exactly the threshold: strong = v >= hi, weak = lo <= v < hi.
             // The byte msbs 7,15,23,31 land on product bits 28..31 of f * 0x00204081
             // (partial products at distinct bits: no carries), then move to 4i.
+            // The nibble lands at bit 4i through a multiply-add by 2^(4i) (FMA
+            // pipe; the nibbles are disjoint) — `one` is opaque to ptxas
+            // (%nsmid >= 1) so it stays an IMAD instead of a shift + OR.
+            // lo <= hi, so the strong flags are a subset of the v >= lo flags:
+            // weak = (v >= lo) - strong, bitwise and as whole planes.
             const uint32_t l7 = c.lo7[0], h7 = c.hi7[0];
+            uint32_t lb = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const uint32_t fhi = ge_t(v[i], h7, SEG % 4), flo = ge_t(v[i], l7, SEG / 4);
-                sb |= ((fhi * 0x00204081u) >> 28) << (4 * i);
-                kb |= (((flo & ~fhi) * 0x00204081u) >> 28) << (4 * i);
+                const uint32_t pw = one << (4 * i);
+                sb = ((fhi * 0x00204081u) >> 28) * pw + sb;
+                lb = ((flo * 0x00204081u) >> 28) * pw + lb;
             }
+            kb = lb - sb;
         } else {
             u8_apply_words<8>(p, c, v);   // the chain before the loop (ends with the threshold)
 #pragma unroll

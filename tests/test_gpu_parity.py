@@ -1024,3 +1024,18 @@ def test_dropped_future_keeps_temporaries_alive():
         del junk
     torch.cuda.synchronize()
     assert np.array_equal(dst.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("lohi", [(0, 0), (0, 256), (256, 256), (100, 100), (3, 129), (130, 200),
+                                  (0, 90), (200, 256), (127, 128)])
+def test_hysteresis_threshold_modes(lohi):
+    """Every compile-time compare-mode pair of the plane pack (lo / hi below
+    128, at or above 128, <= 0, >= 256), one and three partitions."""
+    H, W = 130, 300
+    gray = synth.np_u8_stream(8, 11, H * W).reshape(H, W)
+    want, D = oracle_hyst(gray, *lohi)
+    for k, d in ((1, None), (3, [0.3, 0.3, 0.4])):
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(pctx(k, d, 1), trees.hysteresis(*lohi), [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want), (lohi, k)
+        assert r["executions"] == D + 1, (lohi, k)

@@ -644,7 +644,7 @@ def run_reference(args, dist):
              "fft": ("fft_ifft_512x65536_c64", "ffts/s", "f64")}
     wl = args.workload if args.workload != "all" else "filter"
     name, unit, dtype = names[wl]
-    total_budget = 90.0
+    total_budget = float(os.environ.get("MW_REF_BUDGET_S", "90"))   # the whole arm, seconds
     per_step = total_budget / max(1, args.steps + args.warmup)
     for _ in range(args.warmup):
         cpu_rate(name, per_step)

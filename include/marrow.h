@@ -381,10 +381,11 @@ mw_status mw_ctx_set_slowdown(mw_ctx* ctx, int32_t part, float factor);
  * searches.  Every value gives bit-identical results.  Defaults are the
  * measured best on B200 (MW_* environment variables override them).       */
 enum {
-    MW_TUNE_RGBA_TMA = 0,     /* fused RGBA chain: 0 LSU path, 1 = 16 KiB x 3 stages TMA,
+    MW_TUNE_RGBA_TMA = 0,     /* fused RGBA chain: 0 LSU path, 1 = 16 KiB TMA ring, 2 stages
+                                 for launches of >= 8 waves of chunks else 3 (default),
                                  2 = 8 KiB x 4, 3 = 8 KiB x 3, 4 = 4 KiB x 4, 5 = 32 KiB x 3,
-                                 6 = 16 KiB x 6; warp-granular rings: 7 = 4 KiB x 3 x 8 warps,
-                                 8 = 8 KiB x 2 x 6 warps                                  */
+                                 6 = 16 KiB x 6, 9 = 16 KiB x 2; warp-granular rings:
+                                 7 = 4 KiB x 3 x 8 warps, 8 = 8 KiB x 2 x 6 warps         */
     MW_TUNE_RGBA_UNROLL = 1,  /* LSU path: 16-byte vectors per thread (2, 4, 8)            */
     MW_TUNE_HYST_PLANES = 2,  /* 1: one-partition hysteresis on bit planes; 0: byte stencil */
     MW_TUNE_HYST_T = 3,       /* executions per pass of the plane loop (4, 6, 8, 12)        */

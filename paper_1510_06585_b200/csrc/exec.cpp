@@ -1865,7 +1865,7 @@ mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_
     const Tune base(c->tune, c->tune + mwk::TUNE_COUNT);
     std::vector<Tune> cands{base};
     if (has_rgba) {
-        for (int tma = 0; tma <= 8; ++tma)
+        for (int tma = 0; tma <= 9; ++tma)
             for (int un : {2, 4, 8}) {
                 if (tma > 0 && un != base[mwk::TUNE_RGBA_UNROLL]) continue;
                 Tune t = base;

@@ -1707,7 +1707,7 @@ void tune_defaults(int* out) {
 
 bool tune_valid(int knob, int v) {
     switch (knob) {
-        case TUNE_RGBA_TMA: return v >= 0 && v <= 8;
+        case TUNE_RGBA_TMA: return v >= 0 && v <= 9;
         case TUNE_RGBA_UNROLL: return v == 2 || v == 4 || v == 8;
         case TUNE_HYST_PLANES: return v == 0 || v == 1;
         case TUNE_HYST_T: return v == 4 || v == 6 || v == 8 || v == 12;
@@ -1795,9 +1795,9 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
         // 0 = LSU path, 1 = 16 KiB x 3 (measured best), 2 = 8 KiB x 4, 3 = 8 KiB x 3,
         // 4 = 4 KiB x 4, 5 = 32 KiB x 3, 6 = 16 KiB x 6)
         const int tma_cfg = L.tune[TUNE_RGBA_TMA];
-        const int chunk = (tma_cfg == 1 || tma_cfg == 6) ? 16384
+        const int chunk = (tma_cfg == 1 || tma_cfg == 6 || tma_cfg == 9) ? 16384
                           : ((tma_cfg == 4 || tma_cfg == 7) ? 4096 : (tma_cfg == 5 ? 32768 : 8192));
-        if (tma_cfg >= 7 && (W * 4) % chunk == 0 &&
+        if ((tma_cfg == 7 || tma_cfg == 8) && (W * 4) % chunk == 0 &&
             ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
 #define MW_TMAW_LAUNCH(CH, NS, WP, MI, KMI, TI)                                               \
     do {                                                                                       \
@@ -1833,6 +1833,11 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
 #undef MW_TMAW_LAUNCH
             return cudaGetLastError();
         }
+        // default (1): 16 KiB x 2 stages (three CTAs per SM) for launches of at
+        // least 8 waves of chunks, 16 KiB x 3 (two CTAs per SM, fewer tail
+        // rounds) below — measured 89.3 vs 92.7 us at 8192 rows, 25.3 vs
+        // 26.3 us at 2048 rows, 17.1 vs 15.1 us at 1024 rows
+        const bool big = rows * (W * 4 / 16384) >= 8ll * sm_count() * 3;
         if (tma_cfg > 0 && (W * 4) % chunk == 0 &&
             ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
 #define MW_TMA_LAUNCH(CH, NS, MI, KMI, TI)                                                     \
@@ -1860,7 +1865,9 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
     } while (0)
 #define MW_TMA_CFG(MI, KMI, TI)                                                                \
     do {                                                                                       \
-        if (tma_cfg == 1) MW_TMA_LAUNCH(16384, 3, MI, KMI, TI);                                \
+        if (tma_cfg == 1 && big) MW_TMA_LAUNCH(16384, 2, MI, KMI, TI);                         \
+        else if (tma_cfg == 1) MW_TMA_LAUNCH(16384, 3, MI, KMI, TI);                           \
+        else if (tma_cfg == 9) MW_TMA_LAUNCH(16384, 2, MI, KMI, TI);                           \
         else if (tma_cfg == 5) MW_TMA_LAUNCH(32768, 3, MI, KMI, TI);                           \
         else if (tma_cfg == 6) MW_TMA_LAUNCH(16384, 6, MI, KMI, TI);                           \
         else if (tma_cfg == 3) MW_TMA_LAUNCH(8192, 3, MI, KMI, TI);                            \
@@ -1946,16 +1953,25 @@ cudaError_t u8_chain(const U8Prog& p, const uint8_t* src, int64_t sp, uint8_t* d
     }
     const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
     if (L.tune[TUNE_U8_TMA] && sp == W && dp == W && aligned && (rows * W) % 16 == 0) {
-        constexpr int CH = 16384, NS = 3;
-        constexpr size_t smem = 2 * NS * CH + 64;
-        static int occ = [] {
-            cudaFuncSetAttribute(k_u8_tma<CH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            return resident_ctas(k_u8_tma<CH, NS>, 256, smem);
-        }();
+        // 16 KiB chunks; 2 stages (three CTAs per SM) for launches of at least
+        // 8 waves of chunks, else 3 (measured on the 512 MiB volume: 180.8 vs
+        // 183.2 us)
+        constexpr int CH = 16384;
+        const int64_t items = (rows * W + CH - 1) / CH;
         ++g_launches;
-        k_u8_tma<CH, NS><<<grid_for((rows * W + CH - 1) / CH, occ, L), 256, smem, L.stream>>>(
-            p, c, src, dst, rows * W);
+#define MW_U8_TMA_LAUNCH(NS)                                                                   \
+        {                                                                                      \
+            constexpr size_t smem = 2 * NS * CH + 64;                                          \
+            static int occ = [] {                                                              \
+                cudaFuncSetAttribute(k_u8_tma<CH, NS>,                                         \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+                return resident_ctas(k_u8_tma<CH, NS>, 256, smem);                             \
+            }();                                                                               \
+            k_u8_tma<CH, NS><<<grid_for(items, occ, L), 256, smem, L.stream>>>(p, c, src, dst,  \
+                                                                              rows * W);       \
+        }
+        if (items >= 8ll * sm_count() * 3) MW_U8_TMA_LAUNCH(2) else MW_U8_TMA_LAUNCH(3)
+#undef MW_U8_TMA_LAUNCH
         return cudaGetLastError();
     }
     const bool vec = (W % 16 == 0) && (sp % 16 == 0) && (dp % 16 == 0) && aligned &&

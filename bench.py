@@ -10,8 +10,9 @@ nbody|all.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-For N > 1 launch with torchrun (one process per GPU); timing is CUDA events
-on the launching stream, max over ranks.  `--impl reference` times the CPU
+For N > 1 launch with torchrun (one process per GPU), or plain
+`python bench.py --gpus N`, which starts the N local ranks itself; timing is
+CUDA events on the launching stream, max over ranks.  `--impl reference` times the CPU
 oracle (test infrastructure) as the reference arm on a bounded sample.
 """
 from __future__ import annotations
@@ -96,7 +97,7 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         if gpus != self.world:
-            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={self.world} (launch N>1 with torchrun)")
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={self.world}")
         self.pg = None
         if self.world > 1:
             import torch.distributed as dist
@@ -667,6 +668,21 @@ def run_reference(args, dist):
     print(json.dumps(line), flush=True)
 
 
+def comm_check(M, trees, torch, ctx, dist, parts):
+    """The library's own communicator spans every rank: a MapReduce sum of
+    ones over world x parts x 2^16 elements (each rank holding its rows) must
+    all-reduce to exactly that count on every rank."""
+    node = trees.mapreduce(False)
+    L = dist.world * parts * (1 << 16)
+    off, ln = M.mw_partition(ctx, node, L)
+    f = dist.rank * parts
+    s0, s1 = off[f], off[f + parts - 1] + ln[f + parts - 1]
+    x = torch.ones(s1 - s0, dtype=torch.float32, device=dist.device_obj())
+    r = M.mw_run(ctx, node, [M.arg(x, local_offset=s0, global_shape=(L,))]).wait().result()
+    ok = dist.max(0.0 if r["reduced"] == L else 1.0) == 0.0
+    return {"transport": "nccl", "nranks": dist.world, "allreduce_sum_of_ones_ok": ok}
+
+
 def run_marrow(args, dist, wl_name):
     import torch
 
@@ -680,6 +696,7 @@ def run_marrow(args, dist, wl_name):
     if dist.world > 1:
         nccl_id = dist.bcast_bytes(M.mw_nccl_unique_id() if dist.rank == 0 else None)
     ctx = M.mw_ctx_create(dist.local, dist.rank, dist.world, args.parts, nccl_id)
+    comm = comm_check(M, trees, torch, ctx, dist, args.parts) if dist.world > 1 else None
     w = WORKLOADS[wl_name](M, trees, synth, torch, ctx, dev, dist.rank)
     stream = torch.cuda.Stream(device=dev)   # a real stream (graph capture needs one)
     torch.cuda.set_stream(stream)
@@ -791,6 +808,8 @@ def run_marrow(args, dist, wl_name):
                            partitions=dist.world * args.parts),
             "roofline": roof, "kernels": breakdown, "gpu_launches": launches,
             "clocks": clocks.summary()}
+    if comm is not None:
+        line["comm"] = comm
     if wl_name == "hysteresis":
         line["config"]["executions_E"] = res["executions"]
         line["pixel_executions_per_s"] = value * res["executions"]
@@ -903,7 +922,36 @@ def traffic_from_profile(wl_name):
         return None
 
 
+def self_launch(n):
+    """`python bench.py --gpus N` outside torchrun: start N local ranks (one
+    process per GPU, the torchrun environment on 127.0.0.1), forward rank 0's
+    JSON line, exit with the worst return code.  NCCL's INFO log (init: rank
+    and nranks of every communicator) goes to stderr so stdout keeps one line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    sys.exit(max(rcs, key=abs))
+
+
 def main():
+    if "WORLD_SIZE" not in os.environ:
+        for i, a in enumerate(sys.argv):
+            g = a.split("=", 1)[1] if a.startswith("--gpus=") else (
+                sys.argv[i + 1] if a == "--gpus" and i + 1 < len(sys.argv) else None)
+            if g is not None and int(g) > 1:
+                self_launch(int(g))
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
@@ -917,7 +965,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    dist = Dist(args.gpus)
+    if args.impl == "reference" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        if int(os.environ.get("RANK", "0")) != 0:
+            return   # the reference arm runs on rank 0 alone; the other ranks exit 0
+        dist = Dist.__new__(Dist)
+        dist.world, dist.rank, dist.local, dist.pg = args.gpus, 0, 0, None
+    else:
+        dist = Dist(args.gpus)
     if args.impl == "reference":
         if args.steps is None:
             args.steps = 10

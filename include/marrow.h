@@ -79,15 +79,30 @@ typedef struct mw_alloc_fns {
  * with torch.distributed).                                                   */
 mw_status mw_nccl_unique_id(uint8_t out[128]);
 
+/* Transport of the cross-rank exchanges (halo rows, merges, COPY
+ * re-replication, loop condition, timings; P:224, P:376, P:705-707,
+ * P:736-737).                                                                */
+enum {
+    MW_TRANSPORT_AUTO = 0,     /* NCCL when nranks > 1, none for one rank      */
+    MW_TRANSPORT_NCCL = 1,     /* NCCL even for one rank (1-rank communicator) */
+    /* TEST-ONLY: the ranks are threads of ONE process sharing a device; every
+     * exchange is device copies between their buffers ordered by CUDA events
+     * and host barriers, with NCCL's completion semantics.  It runs the
+     * cross-rank code paths of the executor on a one-GPU machine.  The id is
+     * any 128 bytes shared by the group (e.g. mw_nccl_unique_id's).        */
+    MW_TRANSPORT_LOOPBACK = 2
+};
 /* Create a context on CUDA device `device` for rank `rank` of `nranks`
- * processes, each owning `parts_per_rank` (>= 1) consecutive partitions.
- * nccl_id: required when nranks > 1 or force_nccl != 0 (then an NCCL
- * communicator is created — collective), ignored otherwise.  force_nccl
- * routes even single-rank merges through a 1-rank NCCL communicator.
+ * processes (or loopback threads), each owning `parts_per_rank` (>= 1)
+ * consecutive partitions.
+ * nccl_id: the group id, required when nranks > 1 or transport != AUTO (then
+ * a communicator is created — collective: blocks until every rank joined),
+ * ignored otherwise.
  * The initial distribution is uniform over the P partitions (identical
- * B200s have equal relative performance).                                   */
+ * B200s have equal relative performance).  Errors: MW_E_INVALID_SPEC (bad
+ * rank / transport / missing id), MW_E_NCCL, MW_E_CUDA.                     */
 mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t parts_per_rank,
-                        const uint8_t* nccl_id, int32_t force_nccl, const mw_alloc_fns* alloc,
+                        const uint8_t* nccl_id, int32_t transport, const mw_alloc_fns* alloc,
                         mw_ctx** out);
 /* Collective when the ctx owns an NCCL communicator.  Frees all scratch; when
  * futures or graphs of the ctx are still alive the teardown happens at the

@@ -23,6 +23,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "marrow.h"
 #include "mw_kernels.h"
 #include "sct.h"
@@ -68,8 +69,7 @@ constexpr int kStageSlots = 3;
 
 struct mw_ctx {
     int device = 0, rank = 0, nranks = 1, ppr = 1, P = 1;
-    bool use_nccl = false;
-    ncclComm_t comm = nullptr;
+    std::unique_ptr<mwc::Comm> comm;   // NCCL, or the test-only loopback (comm.h)
     mw_alloc_fns alloc{};
     bool has_alloc = false;
     std::vector<double> dist;
@@ -233,7 +233,9 @@ int64_t dt_size(int32_t dt) {
 mw_status check_arg(const mw_arg& a, int idx, int32_t dtype, int ndim_min, int ndim_max,
                     int32_t mode, int64_t last_dim /* -1 any */) {
     std::string pre = "arg " + std::to_string(idx) + ": ";
-    if (!a.ptr && a.shape[0] != 0) return fail(MW_E_SHAPE_MISMATCH, pre + "NULL pointer");
+    // a rank may hold no rows of a PARTITION argument (zero share): NULL is fine then
+    if (!a.ptr && (a.mode == MW_COPY ? a.shape[0] : a.local_rows) != 0)
+        return fail(MW_E_SHAPE_MISMATCH, pre + "NULL pointer");
     if (a.dtype != dtype) return fail(MW_E_SHAPE_MISMATCH, pre + "wrong dtype");
     if (a.ndim < ndim_min || a.ndim > ndim_max || a.ndim > 4)
         return fail(MW_E_SHAPE_MISMATCH, pre + "wrong number of dimensions");
@@ -403,22 +405,22 @@ mw_status exchange_rows(RunCtx& R, const std::vector<uint8_t*>& bufs, int64_t hr
             }
             continue;
         }
-        if (!c->comm) return fail(MW_E_STATE, "cross-rank halo without an NCCL communicator");
+        if (!c->comm) return fail(MW_E_STATE, "cross-rank halo without a communicator");
         if (!group) {
-            NCCL_OK(ncclGroupStart());
+            MW_OK_OR_RETURN(c->comm->group_start());
             group = true;
         }
         if (la) {
             int peer = R.owner(b);
-            NCCL_OK(ncclSend(a_last, n, ncclUint8, peer, c->comm, R.s));
-            NCCL_OK(ncclRecv(a_bhalo, n, ncclUint8, peer, c->comm, R.s));
+            MW_OK_OR_RETURN(c->comm->send(a_last, n, peer, R.s));
+            MW_OK_OR_RETURN(c->comm->recv(a_bhalo, n, peer, R.s));
         } else {
             int peer = R.owner(a);
-            NCCL_OK(ncclSend(b_first, n, ncclUint8, peer, c->comm, R.s));
-            NCCL_OK(ncclRecv(b_thalo, n, ncclUint8, peer, c->comm, R.s));
+            MW_OK_OR_RETURN(c->comm->send(b_first, n, peer, R.s));
+            MW_OK_OR_RETURN(c->comm->recv(b_thalo, n, peer, R.s));
         }
     }
-    if (group) NCCL_OK(ncclGroupEnd());
+    if (group) MW_OK_OR_RETURN(c->comm->group_end());
     if (cb.n) MW_OK_OR_RETURN(kerr(mwk::copy_batch(cb, R.s), "copy_batch"));
     return MW_OK;
 }
@@ -547,7 +549,7 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
         MW_OK_OR_RETURN(exchange_rows(R, S[cur], T, rb));
         k0 += steps;
         if (!is_while) continue;
-        if (c->comm) NCCL_OK(ncclAllReduce(d_last, d_last, 1, ncclInt32, ncclMax, c->comm, R.s));
+        if (c->comm) MW_OK_OR_RETURN(c->comm->allreduce(d_last, 1, mwc::DType::I32, mwc::ROp::Max, R.s));
         CUDA_OK(cudaMemcpyAsync(c->h_flag + 4 + slot, d_last, sizeof(int32_t), cudaMemcpyDeviceToHost, R.s));
         CUDA_OK(cudaEventRecord(c->lag_ev[slot], R.s));
         inflight.push_back({slot, k0});
@@ -798,7 +800,7 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
                             "byte stencil) and cannot be captured in a graph");
             // loop condition (P:376 stage 1), reduced over ranks on the device
             if (c->comm)
-                NCCL_OK(ncclAllReduce(d_last, d_last, 1, ncclInt32, ncclMax, c->comm, R.s));
+                MW_OK_OR_RETURN(c->comm->allreduce(d_last, 1, mwc::DType::I32, mwc::ROp::Max, R.s));
             CUDA_OK(cudaMemcpyAsync(c->h_flag, d_last, sizeof(int32_t), cudaMemcpyDeviceToHost, R.s));
             CUDA_OK(cudaStreamSynchronize(R.s));
             const int64_t lastc = *c->h_flag;
@@ -842,15 +844,15 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
 mw_status allgather_slices(RunCtx& R, float4* buf) {
     mw_ctx* c = R.c;
     if (c->nranks == 1) return MW_OK;
-    NCCL_OK(ncclGroupStart());
+    MW_OK_OR_RETURN(c->comm->group_start());
     for (int r = 0; r < c->nranks; ++r) {
         int p0 = r * c->ppr, p1 = p0 + c->ppr - 1;
         int64_t o = R.off[p0], n = R.off[p1] + R.len[p1] - o;
         if (n == 0) continue;
         // allgather-v: one broadcast per root over its contiguous slice (in place)
-        NCCL_OK(ncclBroadcast(buf + o, buf + o, (size_t)n * 4, ncclFloat32, r, c->comm, R.s));
+        MW_OK_OR_RETURN(c->comm->broadcast(buf + o, (size_t)n * sizeof(float4), r, R.s));
     }
-    NCCL_OK(ncclGroupEnd());
+    MW_OK_OR_RETURN(c->comm->group_end());
     return MW_OK;
 }
 
@@ -1202,9 +1204,11 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         // one non-zero contributor, so the sum is exact and order-free.
         // (max / min: one contributor per chunk, the others hold the identity)
         if (c->comm && nch > 0)
-            NCCL_OK(ncclAllReduce(partials, partials, (size_t)nch, ncclFloat64,
-                                  rop == MW_REDUCE_MAX ? ncclMax : (rop == MW_REDUCE_MIN ? ncclMin : ncclSum),
-                                  c->comm, s));
+            MW_OK_OR_RETURN(c->comm->allreduce(partials, (size_t)nch, mwc::DType::F64,
+                                               rop == MW_REDUCE_MAX   ? mwc::ROp::Max
+                                               : rop == MW_REDUCE_MIN ? mwc::ROp::Min
+                                                                      : mwc::ROp::Sum,
+                                               s));
         if (prog[0].merge_op == MW_MERGE_ADD) {
             MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s, rop),
                                  "reduce_combine"));
@@ -1333,13 +1337,15 @@ mw_status mw_nccl_unique_id(uint8_t out[128]) {
 }
 
 mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t parts_per_rank,
-                        const uint8_t* nccl_id, int32_t force_nccl, const mw_alloc_fns* alloc,
+                        const uint8_t* nccl_id, int32_t transport, const mw_alloc_fns* alloc,
                         mw_ctx** out) {
     if (!out) return fail(MW_E_INVALID_SPEC, "out is NULL");
     if (nranks < 1 || rank < 0 || rank >= nranks || parts_per_rank < 1)
         return fail(MW_E_INVALID_SPEC, "need 0 <= rank < nranks and parts_per_rank >= 1");
-    const bool use_nccl = nranks > 1 || force_nccl;
-    if (use_nccl && !nccl_id) return fail(MW_E_INVALID_SPEC, "NCCL id required");
+    if (transport < MW_TRANSPORT_AUTO || transport > MW_TRANSPORT_LOOPBACK)
+        return fail(MW_E_INVALID_SPEC, "unknown transport");
+    const bool use_comm = nranks > 1 || transport != MW_TRANSPORT_AUTO;
+    if (use_comm && !nccl_id) return fail(MW_E_INVALID_SPEC, "group id required");
     if (alloc && (!alloc->alloc || !alloc->free))
         return fail(MW_E_INVALID_SPEC, "allocator needs both alloc and free");
     CUDA_OK(cudaSetDevice(device));
@@ -1362,11 +1368,11 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
     CUDA_OK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     c->launches0 = mwk::launch_count();
     c->bstate = mw_balance_state{};
-    if (use_nccl) {
-        ncclUniqueId id;
-        memcpy(id.internal, nccl_id, 128);
-        NCCL_OK(ncclCommInitRank(&c->comm, nranks, id, rank));
-        c->use_nccl = true;
+    if (use_comm) {
+        if (transport == MW_TRANSPORT_LOOPBACK)
+            MW_OK_OR_RETURN(mwc::make_loopback(device, rank, nranks, nccl_id, &c->comm));
+        else
+            MW_OK_OR_RETURN(mwc::make_nccl(rank, nranks, nccl_id, &c->comm));
     }
     *out = c.release();
     return MW_OK;
@@ -1378,7 +1384,7 @@ static void ctx_teardown(mw_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto& kv : c->scratch) ctx_free(c, kv.second.p);
-    if (c->comm) ncclCommDestroy(c->comm);
+    c->comm.reset();
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : c->fut_ev) cudaEventDestroy(e);
     if (c->wall_a) cudaEventDestroy(c->wall_a);
@@ -1516,11 +1522,7 @@ mw_status mw_future_wait(mw_future* f) {
     if (e != cudaSuccess) return fail(MW_E_CUDA, std::string("run failed: ") + cudaGetErrorString(e));
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MW_E_CUDA, std::string("run failed: ") + cudaGetErrorString(e));
-    if (f->ctx->comm) {
-        ncclResult_t r = ncclSuccess;
-        ncclCommGetAsyncError(f->ctx->comm, &r);
-        if (r != ncclSuccess) return fail(MW_E_NCCL, std::string("NCCL: ") + ncclGetErrorString(r));
-    }
+    if (f->ctx->comm) MW_OK_OR_RETURN(f->ctx->comm->async_error());
     f->waited = true;
     return MW_OK;
 }
@@ -1630,7 +1632,7 @@ mw_status mw_last_timings(mw_ctx* c, float* per_part_ms, int32_t n, float* wall_
         MW_OK_OR_RETURN(scratch(c, "timings", (size_t)c->P * 4, c->aux, &d));
         float* df = static_cast<float*>(d);
         CUDA_OK(cudaMemcpyAsync(df + c->rank * c->ppr, local.data(), c->ppr * 4, cudaMemcpyHostToDevice, c->aux));
-        NCCL_OK(ncclAllGather(df + c->rank * c->ppr, df, (size_t)c->ppr, ncclFloat32, c->comm, c->aux));
+        MW_OK_OR_RETURN(c->comm->allgather(df + c->rank * c->ppr, df, (size_t)c->ppr * 4, c->aux));
         CUDA_OK(cudaMemcpyAsync(all.data(), df, c->P * 4, cudaMemcpyDeviceToHost, c->aux));
         CUDA_OK(cudaStreamSynchronize(c->aux));
     } else {

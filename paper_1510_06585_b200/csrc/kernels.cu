@@ -80,7 +80,7 @@ int tuning_knob(const char* name, int dflt) {
     const char* v = getenv(name);
     return v ? atoi(v) : dflt;
 }
-unsigned long long g_launches = 0;
+thread_local unsigned long long g_launches = 0;   // per host thread (one ctx per thread)
 
 template <typename K>
 int resident_ctas(K kernel, int threads, size_t smem = 0) {
@@ -2047,6 +2047,39 @@ cudaError_t copy_batch(const CopyBatch& b, cudaStream_t s) {
     const int gx = (int)std::min<int64_t>(64, std::max<int64_t>(1, (mx / 16 + 255) / 256));
     ++g_launches;
     k_copy_batch<<<dim3(gx, b.n), 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+struct RankPtrs {
+    const void* p[16];
+};
+template <typename T, int OP>
+__global__ void __launch_bounds__(256) k_reduce_ranks(const __grid_constant__ RankPtrs src, int n, T* dst,
+                                                      int64_t count) {
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < count; i += (int64_t)gridDim.x * 256) {
+        T acc = static_cast<const T*>(src.p[0])[i];
+        for (int r = 1; r < n; ++r) {
+            const T v = static_cast<const T*>(src.p[r])[i];
+            acc = OP == 0 ? acc + v : (OP == 1 ? (v > acc ? v : acc) : (v < acc ? v : acc));
+        }
+        dst[i] = acc;
+    }
+}
+
+cudaError_t reduce_ranks(const void* const* srcs, int n, void* dst, size_t count, int dt, int op,
+                         cudaStream_t s) {
+    if (n < 1 || n > 16 || dt < 0 || dt > 2 || op < 0 || op > 2) return cudaErrorInvalidValue;
+    if (count == 0) return cudaSuccess;
+    RankPtrs rp{};
+    for (int r = 0; r < n; ++r) rp.p[r] = srcs[r];
+    const int g = (int)std::min<int64_t>(1024, ((int64_t)count + 255) / 256);
+    ++g_launches;
+#define RR_CASE(T, D, O) \
+    if (dt == D && op == O) k_reduce_ranks<T, O><<<g, 256, 0, s>>>(rp, n, static_cast<T*>(dst), (int64_t)count);
+    RR_CASE(int32_t, 0, 0) RR_CASE(int32_t, 0, 1) RR_CASE(int32_t, 0, 2)
+    RR_CASE(float, 1, 0) RR_CASE(float, 1, 1) RR_CASE(float, 1, 2)
+    RR_CASE(double, 2, 0) RR_CASE(double, 2, 1) RR_CASE(double, 2, 2)
+#undef RR_CASE
     return cudaGetLastError();
 }
 

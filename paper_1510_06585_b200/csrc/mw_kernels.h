@@ -100,6 +100,11 @@ struct CopyBatch {
     int64_t bytes[32];
 };
 cudaError_t copy_batch(const CopyBatch& b, cudaStream_t s);
+// Loopback transport (test-only, comm.cpp): dst[i] = op over r of srcs[r][i]
+// in rank order; dt 0 int32 / 1 fp32 / 2 fp64, op 0 sum / 1 max / 2 min
+// (the executor's max/min operands are never NaN: R28 partials use maxNum).
+cudaError_t reduce_ranks(const void* const* srcs, int n, void* dst, size_t count, int dt, int op,
+                         cudaStream_t s);
 // Several partitions (or ranks): one pass of `steps` (<= T) executions over one
 // partition whose buffers carry T halo rows; atomicMax(last, k0 + last changed).
 int planes_pass_depth(int T_pref, int64_t min_rows);   // largest built T <= both

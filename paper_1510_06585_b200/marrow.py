@@ -28,6 +28,7 @@ _COND_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p)
 MW_DT_U8, MW_DT_F32, MW_DT_F64, MW_DT_I64 = 1, 2, 3, 4
 MW_PARTITION, MW_COPY = 0, 1
 MW_LOC_DEVICE, MW_LOC_HOST = 0, 1
+MW_TRANSPORT_AUTO, MW_TRANSPORT_NCCL, MW_TRANSPORT_LOOPBACK = 0, 1, 2
 MW_BALANCE_PROPORTIONAL, MW_BALANCE_ABS = 0, 1
 MW_PROV_BUILT, MW_PROV_DERIVED, MW_PROV_BALANCED = 0, 1, 2
 MW_KB_NONE, MW_KB_EXACT, MW_KB_SCT, MW_KB_WORKLOAD, MW_KB_DIMENSIONALITY = range(5)
@@ -424,11 +425,14 @@ class Ctx:
 
 
 def mw_ctx_create(device=0, rank=0, nranks=1, parts_per_rank=1, nccl_id=None, force_nccl=False,
-                  torch_alloc=True):
+                  torch_alloc=True, transport=None):
+    """transport: MW_TRANSPORT_* (default AUTO, or NCCL when force_nccl)."""
     out = _vp()
     idbuf = (ctypes.c_uint8 * 128)(*nccl_id) if nccl_id is not None else None
     alloc = TorchAllocator(f"cuda:{device}") if torch_alloc else None
-    _call("mw_ctx_create", device, rank, nranks, parts_per_rank, idbuf, int(bool(force_nccl)),
+    if transport is None:
+        transport = MW_TRANSPORT_NCCL if force_nccl else MW_TRANSPORT_AUTO
+    _call("mw_ctx_create", device, rank, nranks, parts_per_rank, idbuf, int(transport),
           ctypes.byref(alloc.fns) if alloc else None, ctypes.byref(out))
     return Ctx(out, alloc)
 
@@ -504,14 +508,21 @@ def arg(t, mode=MW_PARTITION, local_offset=0, global_shape=None):
 # blocks and torch's caching allocator cannot hand a dropped argument's memory
 # to a new tensor before the run has used it.
 import collections as _collections
+import threading as _threading
 
 _pending = _collections.deque()
+_pending_lock = _threading.RLock()   # ranks may be host threads (loopback transport)
 
 
 _reaping = [False]
 
 
 def _reap_pending(all_of_ctx=None):
+    with _pending_lock:
+        _reap_pending_locked(all_of_ctx)
+
+
+def _reap_pending_locked(all_of_ctx):
     if _reaping[0]:   # re-entered from a destructor run by the garbage collector
         return
     _reaping[0] = True
@@ -540,7 +551,8 @@ class Future:
     def __del__(self):
         if getattr(self, "ptr", None) and _lib is not None:
             if self._keep and getattr(self._keep[2], "ptr", None):
-                _pending.append((self.ptr, self._keep))   # maybe in flight: park it
+                with _pending_lock:
+                    _pending.append((self.ptr, self._keep))   # maybe in flight: park it
             else:
                 _lib.mw_future_release(self.ptr)
             self.ptr = None

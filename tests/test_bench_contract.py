@@ -33,6 +33,21 @@ def test_reference_arm_line():
     assert d["config"]["workload"].startswith("saxpy")
 
 
+def test_self_launch_of_n_ranks():
+    """`python bench.py --gpus 2` without torchrun starts two local ranks
+    itself; rank 0 prints the one JSON line (reference arm: CPU only)."""
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e["MW_REF_BUDGET_S"] = "2"
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl",
+                          "reference", "--workload", "saxpy", "--steps", "1", "--warmup", "3"],
+                         cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
 def test_warmup_below_three_is_refused():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--warmup", "2"],
                          cwd=ROOT, capture_output=True, text=True, timeout=300)

@@ -380,16 +380,53 @@ def test_nbody_vs_mpmath():
         assert np.abs(acc[i] - ref).max() <= 1e-13 * np.abs(ref).max()
 
 
-def test_nbody_step_integrator():
-    p, v = synth.np_nbody(9, 0, 40, 2.0 ** -6)
-    v[:, :3] = synth.np_f32_um11(13, 0, 120).reshape(40, 3) * np.float32(0.01)
-    dt = 1e-3
-    po, vo, acc = K.nbody_step(p, v, 1e-4, dt)
-    dtd = np.float64(np.float32(dt))
-    vv = v[:, :3].astype(np.float64) + acc * dtd
-    assert np.array_equal(vo[:, :3], vv.astype(np.float32))
-    assert np.array_equal(po[:, :3], (p[:, :3].astype(np.float64) + vv * dtd).astype(np.float32))
-    assert np.array_equal(po[:, 3], p[:, 3])
+def test_nbody_step_free_particles_closed_form():
+    """Symplectic Euler (R12) with a = 0 — one body, or bodies of mass 0 —
+    is uniform motion: v' = v and, with exactly representable p, v and dt,
+    p_k = p_0 + k v dt exactly after k steps (closed form, no fp64 detour)."""
+    dt = 2.0 ** -10
+    p = np.float32([[0.5, -0.25, 0.125, 1.0]])
+    v = np.float32([[0.25, 0.5, -1.0, 0.0]])
+    for k in range(1, 6):
+        p, v, acc = K.nbody_step(p, v, 1e-4, dt)
+        assert np.all(acc == 0.0) and np.array_equal(v[0, :3], np.float32([0.25, 0.5, -1.0]))
+        want = [0.5 + k * 0.25 * dt, -0.25 + k * 0.5 * dt, 0.125 - k * dt]
+        assert [Fraction(float(c)) for c in p[0, :3]] == [Fraction(w) for w in want]
+        assert p[0, 3] == 1.0
+    # many bodies, all massless: every body moves on its own straight line
+    pos, _ = synth.np_nbody(9, 0, 50, 0.0)
+    vel = np.zeros_like(pos)
+    vel[:, :3] = np.float32(2.0 ** -4)
+    po, vo, acc = K.nbody_step(pos, vel, 1e-4, dt)
+    assert np.all(acc == 0.0) and np.array_equal(vo, vel)
+    want = [[Fraction(float(c)) + Fraction(1, 2 ** 14) for c in row[:3]] for row in pos]
+    got = [[Fraction(float(c)) for c in row[:3]] for row in po]
+    for g, w, row in zip(got, want, pos):   # exact when representable, else one rounding
+        for gc, wc in zip(g, w):
+            assert abs(gc - wc) <= Fraction(abs(float(np.spacing(np.float32(float(wc)))))) / 2
+
+
+def test_nbody_step_antisymmetric_pair_closed_form():
+    """Two equal masses at rest at (+-x, 0, 0): each is pulled toward the
+    other with a = m (2x) / ((2x)^2 + eps^2)^(3/2) (closed form, mpmath), then
+    v' = a dt, p' = p + v' dt, rounded once to binary32 (R12): the pair stays
+    mirror-symmetric bit for bit, and the values agree with the closed form
+    to half an fp32 ulp."""
+    import mpmath
+    mpmath.mp.dps = 50
+    x, m, eps2, dt = 0.375, 0.5, np.float32(1e-4), np.float32(1e-3)
+    pos = np.float32([[x, 0, 0, m], [-x, 0, 0, m]])
+    vel = np.zeros_like(pos)
+    po, vo, acc = K.nbody_step(pos, vel, float(eps2), float(dt))
+    d = mpmath.mpf(2 * x)
+    a = mpmath.mpf(m) * d / (d ** 2 + mpmath.mpf(float(eps2))) ** mpmath.mpf(1.5)
+    v1 = a * mpmath.mpf(float(dt))
+    p1 = mpmath.mpf(x) - v1 * mpmath.mpf(float(dt))
+    assert abs(acc[0, 0] - float(-a)) <= 1e-15 * float(a) and acc[0, 1] == acc[0, 2] == 0.0
+    assert abs(float(vo[0, 0]) - float(-v1)) <= float(np.spacing(np.float32(float(v1)))) / 2
+    assert abs(float(po[0, 0]) - float(p1)) <= float(np.spacing(np.float32(float(p1)))) / 2
+    assert vo[1, 0] == -vo[0, 0] and po[1, 0] == -po[0, 0]
+    assert np.all(vo[:, 1:3] == 0) and np.all(po[:, 1:3] == 0) and np.all(po[:, 3] == m)
 
 
 @pytest.mark.slow
@@ -411,6 +448,29 @@ def test_nbody_config_reference():
 
 
 # ----------------------------------------------------------------- MapReduce
+def test_abs_sum_pins():
+    """sum |terms| (the conditioning scale of the MapReduce tolerance, SURVEY
+    §8(c) c.5): +-1 sequences sum |.| to n exactly whatever their signed sum;
+    exact rational brute force (fractions) for random fp32 inputs (sum and
+    dot terms); sign flips of x or y do not change it; it dominates |sum|."""
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 7, 1000, 4097):
+        s = np.where(rng.integers(0, 2, n) == 1, 1.0, -1.0).astype(np.float32)
+        assert K.abs_sum(s) == float(n)
+        assert K.abs_sum(s, s) == float(n) and K.abs_sum(s, -s) == float(n)
+        assert K.sum_(s) == float(np.sum(s.astype(np.int64)))
+    for n in (1, 10, 333, 2000):
+        x = synth.np_f32_um11(21, 0, n) * np.float32(2.0 ** rng.integers(-20, 20))
+        y = synth.np_f32_um11(22, 0, n)
+        ex = sum(abs(Fraction(float(v))) for v in x)
+        exd = sum(abs(Fraction(float(a)) * Fraction(float(b))) for a, b in zip(x, y))
+        assert abs(Fraction(K.abs_sum(x)) - ex) <= ex * Fraction(1, 2 ** 52)
+        assert abs(Fraction(K.abs_sum(x, y)) - exd) <= exd * Fraction(1, 2 ** 52)
+        assert K.abs_sum(-x) == K.abs_sum(x) and K.abs_sum(x, -y) == K.abs_sum(x, y)
+        assert K.abs_sum(x) >= abs(K.sum_(x)) and K.abs_sum(x, y) >= abs(K.dot(x, y))
+        assert K.abs_sum(np.abs(x)) == K.sum_(np.abs(x))   # one sign: abs_sum = sum
+
+
 def test_mapreduce_closed_forms():
     n = (1 << 25) + 3
     ones = np.ones(n, np.float32)
@@ -705,6 +765,61 @@ def test_fft_tolerance_formula():
     # Higham Thm 24.2 shape: grows with log2 N and the number of stages
     assert FF.tolerance(1 << 16, 1) < FF.tolerance(1 << 16, 2) < 2 * FF.tolerance(1 << 16, 1) + 1e-7
     assert FF.tolerance(1 << 13, 1) < FF.tolerance(1 << 16, 1) < 1e-5
+
+
+def test_fft_tolerance_value_vs_higham_constants():
+    """The VALUE of the bound, recomputed in 50-digit arithmetic from the
+    constants of Higham (2002) Thm 24.2 as printed there: unit roundoff of
+    binary32 u = 2^-24, gamma_n = n u / (1 - n u), computed weights with
+    |w^ - w| <= mu, eta = mu + gamma_4 (sqrt 2 + mu), relative error of the
+    radix-2 FFT <= log2(N) eta / (1 - log2(N) eta); R25 takes
+    mu = 4u (a tabulated fp32 root times one complex product) and adds u for
+    the final rounding to fp32 per chain."""
+    import mpmath
+    mpmath.mp.dps = 50
+    u = mpmath.mpf(2) ** -24
+
+    def gamma(n):
+        return n * u / (1 - n * u)
+
+    mu = 4 * u
+    eta = mu + gamma(4) * (mpmath.sqrt(2) + mu)
+    for log2n in (13, 14, 15, 16):
+        per = log2n * eta / (1 - log2n * eta)
+        for stages in (1, 2, 6):
+            want = float(stages * per + u)
+            assert abs(FF.tolerance(1 << log2n, stages) - want) <= 1e-12 * want
+    # the number DESIGN.md R25 quotes: 9.3e-6 per stage at N = 65536
+    assert 9.2e-6 < FF.tolerance(1 << 16, 1) < 9.3e-6
+
+
+def test_fft_tolerance_bounds_a_real_fp32_fft():
+    """The bound is a bound: an iterative radix-2 FFT carried out in complex64
+    (numpy, every butterfly rounded to binary32, twiddles rounded to binary32)
+    stays within tolerance(N, 1) of the fp64 transform, and the bound is not
+    vacuous (within 200x of the observed worst error)."""
+    rng = np.random.default_rng(7)
+    for log2n in (8, 10, 12):
+        N = 1 << log2n
+        worst = 0.0
+        for trial in range(4):
+            x = (rng.uniform(-1, 1, N) + 1j * rng.uniform(-1, 1, N)).astype(np.complex64)
+            # bit-reversal permutation, then log2n butterfly levels in complex64
+            rev = np.array([int(format(i, f"0{log2n}b")[::-1], 2) for i in range(N)])
+            y = x[rev].copy()
+            h = 1
+            while h < N:
+                k = np.arange(h)
+                w = np.exp(-2j * np.pi * k / (2 * h)).astype(np.complex64)
+                y = y.reshape(-1, 2 * h)
+                a, b = y[:, :h].copy(), (y[:, h:] * w).astype(np.complex64)
+                y[:, :h], y[:, h:] = a + b, a - b
+                y = y.reshape(N)
+                h *= 2
+            err = FF.rel_l2(y.astype(np.complex128), np.fft.fft(x.astype(np.complex128)))
+            worst = max(worst, float(err))
+        tol = FF.tolerance(N, 1)
+        assert worst <= tol and tol <= 200 * worst, (N, worst, tol)
 
 
 # ----------------------------------------------------------------- NEXT-4 variants

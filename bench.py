@@ -176,6 +176,9 @@ class Workload:
         d2h = sum(nbytes(st[i]._owner) for i in self.e2e_out) if self.e2e_out else 8   # or one fp64
         if self.e2e_mode == "staged":
             self.e2e_args = [self._host_arg(a) for a in st]
+            # the pinned inputs are complete before the timed region: a run's
+            # uploads may overlap the previous run's downloads (marrow.h)
+            self.M.mw_ctx_set_staging_overlap(self.ctx, True)
             return h2d, d2h
         # Two device buffer sets on two streams: step i+1's uploads overlap
         # step i's downloads (PCIe duplex); the runs themselves stay in FIFO

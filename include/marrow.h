@@ -284,7 +284,9 @@ typedef struct mw_arg {
 
 /* Enqueue one execution of `root` on the CUDA stream `stream` (cudaStream_t;
  * NULL = legacy default stream) and return a future.
- * Runs of one ctx are FIFO (first-come-first-served).  Trees with
+ * Runs of one ctx are FIFO (first-come-first-served), also when
+ * issued on different streams: each run (and graph replay) first waits on
+ * the device for the end of the ctx's previous one.  Trees with
  * a while-loop synchronise the host every check_every executions; all others
  * return without host synchronisation (device args).  Collective when the
  * tree exchanges data between ranks (MapReduce, hysteresis, N-body).         */
@@ -327,6 +329,13 @@ mw_status mw_graph_result(mw_graph* g, double* out, int32_t n);
 mw_status mw_graph_kernels(const mw_graph* g, int64_t* kernels_per_replay);
 mw_status mw_graph_destroy(mw_graph* g);
 
+/* Host-staged runs (MW_LOC_HOST arguments, NEXT-1): by default a run's
+ * uploads start after the work enqueued on its stream before the call (a
+ * pinned host input may be produced by an asynchronous D2H on that stream).
+ * on != 0 promises that every host input is complete when mw_run is called;
+ * the uploads of a run then overlap the previous run's downloads (no start
+ * barrier).  Default off.                                                    */
+mw_status mw_ctx_set_staging_overlap(mw_ctx* ctx, int32_t on);
 /* Monitoring (per-device execution times feed the load balancer)
  * is on by default: every run records CUDA events around each partition's
  * kernels (mw_last_timings, mw_kernel_stats, mw_rebalance).  Off: no events,

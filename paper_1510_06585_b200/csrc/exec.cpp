@@ -74,6 +74,17 @@ struct mw_ctx {
     bool has_alloc = false;
     std::vector<double> dist;
     std::map<std::string, Buf> scratch;
+    // Scratch pointers baked into live CUDA graphs (refcount per pointer): a
+    // buffer replaced by a larger one while a graph references it is parked in
+    // `orphans` and freed with the last such graph (or at teardown).
+    std::map<void*, int> graph_refs;
+    std::vector<void*> orphans;
+    std::vector<void*>* capture_bufs = nullptr;   // collects scratch used while capturing
+    // FIFO of runs across streams: every run waits for the previous run's end
+    // (a no-op on one stream) and records it (ctx scratch is shared by runs).
+    cudaEvent_t last_run = nullptr;
+    bool have_last_run = false;
+    bool staging_overlap = false;   // mw_ctx_set_staging_overlap
     // pinned host memory
     int32_t* h_flag = nullptr;   // 16 ints: [0] byte-stencil flag, [4..7] plane-pass ring
     cudaEvent_t lag_ev[4]{};
@@ -160,12 +171,28 @@ void ctx_free(mw_ctx* c, void* p) {
 mw_status scratch(mw_ctx* c, const std::string& name, size_t bytes, cudaStream_t s, void** out) {
     Buf& b = c->scratch[name];
     if (b.bytes < bytes) {
-        ctx_free(c, b.p);
+        if (b.p) {
+            auto it = c->graph_refs.find(b.p);
+            if (it != c->graph_refs.end() && it->second > 0) {
+                c->orphans.push_back(b.p);   // a live graph still writes it
+            } else if (c->capturing) {
+                c->orphans.push_back(b.p);   // freeing is not capturable; freed at teardown
+            } else {
+                // every stream of the ctx may still use it (copy streams,
+                // timings): drain them before the caching allocator may
+                // hand the block to someone else
+                for (cudaStream_t q : {s, c->copy_in, c->copy_out, c->aux})
+                    if (q) cudaStreamSynchronize(q);
+                ctx_free(c, b.p);
+            }
+        }
         b.p = nullptr;
         b.bytes = 0;
-        MW_OK_OR_RETURN(ctx_alloc(c, bytes, s, &b.p));
+        // under capture the allocator must not touch the capturing stream
+        MW_OK_OR_RETURN(ctx_alloc(c, bytes, c->capturing ? nullptr : s, &b.p));
         b.bytes = bytes;
     }
+    if (c->capture_bufs) c->capture_bufs->push_back(b.p);
     *out = b.p;
     return MW_OK;
 }
@@ -941,10 +968,18 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
         MW_OK_OR_RETURN(scratch(c, "stage_out" + std::to_string(i), (size_t)(chunk_rows * rb), R.s, &slot_out[i]));
     }
     const bool a0_host = a0.location == MW_LOC_HOST, a1_host = a1.location == MW_LOC_HOST;
-    // No run-wide start barrier: the copy streams only wait for the previous
-    // use of each staging slot (possibly by the previous run), so this run's
-    // first uploads overlap the previous run's last downloads.  Device
-    // arguments and kernels stay ordered on the run's stream.
+    // Uploads start after the work enqueued on the run's stream before this
+    // call (a pinned host input may be filled by an asynchronous D2H on that
+    // stream).  With staging overlap on (mw_ctx_set_staging_overlap: host
+    // inputs are complete when mw_run is called) there is no start barrier:
+    // the copy streams only wait for the previous use of each staging slot
+    // (possibly by the previous run), so this run's first uploads overlap the
+    // previous run's last downloads.  Device arguments and kernels stay
+    // ordered on the run's stream.
+    if (!c->staging_overlap) {
+        CUDA_OK(cudaEventRecord(c->st_start, R.s));
+        CUDA_OK(cudaStreamWaitEvent(c->copy_in, c->st_start, 0));
+    }
     auto rgba = st.kind == StepKind::Rgba ? rgba_groups(st.ops) : std::vector<mwk::RgbaProg>{};
     auto u8 = st.kind == StepKind::U8 ? u8_groups(st.ops) : std::vector<mwk::U8Prog>{};
     auto sx = st.kind == StepKind::Saxpy ? saxpy_groups(st.ops) : std::vector<mwk::SaxpyProg>{};
@@ -1366,6 +1401,7 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
     CUDA_OK(cudaEventCreate(&c->wall_a));
     CUDA_OK(cudaEventCreate(&c->wall_b));
     CUDA_OK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->last_run, cudaEventDisableTiming));
     c->launches0 = mwk::launch_count();
     c->bstate = mw_balance_state{};
     if (use_comm) {
@@ -1379,6 +1415,19 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
 }
 
 static void reap_retired(mw_ctx* c, bool sync);
+
+// Runs of one ctx execute in call order even on different streams (they
+// share the ctx scratch): a run's stream first waits for the previous run's
+// end, which each run records.  On one stream the wait is a no-op.
+static mw_status fifo_enter(mw_ctx* c, cudaStream_t s) {
+    if (c->capturing || !c->have_last_run) return MW_OK;
+    CUDA_OK(cudaStreamWaitEvent(s, c->last_run, 0));
+    return MW_OK;
+}
+static void fifo_exit(mw_ctx* c, cudaStream_t s) {
+    if (c->capturing) return;
+    if (cudaEventRecord(c->last_run, s) == cudaSuccess) c->have_last_run = true;
+}
 
 static void ctx_teardown(mw_ctx* c) {
     cudaSetDevice(c->device);
@@ -1395,6 +1444,8 @@ static void ctx_teardown(mw_ctx* c) {
         if (c->st_out[i]) cudaEventDestroy(c->st_out[i]);
     }
     if (c->st_start) cudaEventDestroy(c->st_start);
+    if (c->last_run) cudaEventDestroy(c->last_run);
+    for (void* p : c->orphans) ctx_free(c, p);
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);
     if (c->aux) cudaStreamDestroy(c->aux);
@@ -1486,6 +1537,7 @@ mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nar
     c->res_free.pop_back();
     *f->res = 0.0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    MW_OK_OR_RETURN(fifo_enter(c, s));
     mw_status st;
     try {
         st = run(c, reinterpret_cast<const Node*>(root), args, nargs, s, f.get());
@@ -1495,9 +1547,17 @@ mw_status mw_run(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nar
         st = fail(MW_E_INVALID_SPEC, "internal error");
     }
     if (st != MW_OK) {
+        // copies into the result slot (or the partials) may already be queued
+        // (e.g. a host-condition loop failing on a later iteration): drain
+        // them before the slot can serve another future
+        cudaStreamSynchronize(s);
+        (void)cudaGetLastError();
         c->res_free.push_back(f->res);
+        if (f->parts) cudaFreeHost(f->parts);
+        f->parts = nullptr;
         return st;
     }
+    fifo_exit(c, s);
     cudaError_t e = cudaSuccess;
     if (!c->fut_ev.empty()) {
         f->done = c->fut_ev.back();
@@ -1711,6 +1771,12 @@ mw_status mw_ctx_set_slowdown(mw_ctx* c, int32_t part, float factor) {
     return MW_OK;
 }
 
+mw_status mw_ctx_set_staging_overlap(mw_ctx* c, int32_t on) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    c->staging_overlap = on != 0;
+    return MW_OK;
+}
+
 mw_status mw_ctx_set_monitoring(mw_ctx* c, int32_t on) {
     if (!c) return fail(MW_E_STATE, "NULL ctx");
     c->monitor = on != 0;
@@ -1757,6 +1823,7 @@ struct mw_graph {
     cudaGraphExec_t exec = nullptr;
     mw_future f;          // result slot of the captured run
     int64_t kernels = 0;  // library kernels per replay
+    std::vector<void*> bufs;   // ctx scratch the graph writes (kept alive while it lives)
 };
 
 mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* args,
@@ -1770,12 +1837,15 @@ mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* ar
     std::unique_ptr<mw_graph> g(new mw_graph);
     g->ctx = c;
     g->f.ctx = c;
+    MW_OK_OR_RETURN(fifo_enter(c, static_cast<cudaStream_t>(stream)));   // before capture begins
     CUDA_OK(cudaHostAlloc(&g->f.res, 32, cudaHostAllocDefault));
     memset(g->f.res, 0, 32);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const unsigned long long l0 = mwk::launch_count();
     CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     c->capturing = true;
+    std::vector<void*> used;
+    c->capture_bufs = &used;
     mw_status st = MW_OK;
     try {
         for (int32_t k = 0; k < nsets && st == MW_OK; ++k) {
@@ -1787,6 +1857,7 @@ mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* ar
         st = fail(MW_E_INVALID_SPEC, "internal error");
     }
     c->capturing = false;
+    c->capture_bufs = nullptr;
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(s, &graph);
     if (st != MW_OK || e != cudaSuccess) {
@@ -1803,6 +1874,10 @@ mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* ar
         return fail(MW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
     g->kernels = (int64_t)(mwk::launch_count() - l0);
+    std::sort(used.begin(), used.end());
+    used.erase(std::unique(used.begin(), used.end()), used.end());
+    for (void* p : used) ++c->graph_refs[p];
+    g->bufs = std::move(used);
     ctx_retain(c);
     *out = g.release();
     return MW_OK;
@@ -1816,7 +1891,10 @@ mw_status mw_graph_capture(mw_ctx* c, const mw_node* root, const mw_arg* args, i
 mw_status mw_graph_launch(mw_graph* g, void* stream) {
     if (!g || !g->exec) return fail(MW_E_STATE, "invalid graph");
     CUDA_OK(cudaSetDevice(g->ctx->device));
-    CUDA_OK(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    MW_OK_OR_RETURN(fifo_enter(g->ctx, s));
+    CUDA_OK(cudaGraphLaunch(g->exec, s));
+    fifo_exit(g->ctx, s);
     return MW_OK;
 }
 
@@ -1840,6 +1918,16 @@ mw_status mw_graph_destroy(mw_graph* g) {
     if (g->graph) cudaGraphDestroy(g->graph);
     if (g->f.res) cudaFreeHost(g->f.res);
     mw_ctx* c = g->ctx;
+    for (void* p : g->bufs) {
+        auto it = c->graph_refs.find(p);
+        if (it == c->graph_refs.end() || --it->second > 0) continue;
+        c->graph_refs.erase(it);
+        auto o = std::find(c->orphans.begin(), c->orphans.end(), p);
+        if (o != c->orphans.end()) {   // replaced while the graph lived: free it now
+            c->orphans.erase(o);
+            ctx_free(c, p);
+        }
+    }
     delete g;
     ctx_release(c);
     return MW_OK;
@@ -1902,6 +1990,7 @@ mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_
             cands.push_back(t);
         }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    MW_OK_OR_RETURN(fifo_enter(c, s));
     // snapshot the arguments a run updates in place
     std::vector<std::pair<const mw_arg*, void*>> snaps;
     const int ik = r->in_kind, ok = r->out_kind;
@@ -1954,6 +2043,7 @@ mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_
     cudaEventDestroy(e1);
     for (int k = 0; k < mwk::TUNE_COUNT; ++k) c->tune[k] = best_t[k];
     MW_OK_OR_RETURN(restore());
+    fifo_exit(c, s);
     CUDA_OK(cudaStreamSynchronize(s));
     if (st != MW_OK) return st;
     if (kb) {

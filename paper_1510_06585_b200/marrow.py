@@ -104,6 +104,7 @@ _SIG = {
     "mw_kernel_reduce": [_i32, _node_pp],
     "mw_map_reduce_sct": [_vp, _vp, _node_pp],
     "mw_ctx_set_monitoring": [_vp, _i32],
+    "mw_ctx_set_staging_overlap": [_vp, _i32],
     "mw_map_reduce_user": [_vp, _MERGE_FN, _vp, _node_pp],
     "mw_loop_host": [_vp, _i64, _COND_FN, _vp, _node_pp],
     "mw_loop_for": [_vp, _i64, _node_pp],
@@ -387,8 +388,16 @@ class TorchAllocator:
 
         @ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
         def _alloc(nbytes, stream, user):
+            # the block belongs to the stream the library uses it on, so the
+            # caching allocator never hands it to another stream while that
+            # stream's kernels may still run (the library drains its streams
+            # before it frees a buffer)
             try:
-                t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+                if stream:
+                    with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.device)):
+                        t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+                else:
+                    t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
                 self.live[t.data_ptr()] = t
                 return t.data_ptr()
             except Exception:
@@ -749,6 +758,12 @@ def mw_ctx_set_monitoring(ctx, on=True):
     """Per-partition timing events on/off (on by default; needed by
     mw_last_timings / mw_rebalance)."""
     _call("mw_ctx_set_monitoring", ctx.ptr, int(bool(on)))
+
+
+def mw_ctx_set_staging_overlap(ctx, on=True):
+    """Host inputs are complete when mw_run is called: staged uploads overlap
+    the previous run's downloads (no start barrier)."""
+    _call("mw_ctx_set_staging_overlap", ctx.ptr, int(bool(on)))
 
 
 def mw_ctx_set_tuning(ctx, knob, value):

@@ -416,7 +416,10 @@ enum {
     MW_TUNE_HYST_ROWS = 4,    /* register rows per plane tile (32, 40)                      */
     MW_TUNE_NBODY_SPLIT = 5,  /* 1: split packed/scalar FP32 across the FMA pipes           */
     MW_TUNE_U8_TMA = 6,       /* 1: TMA bulk-copy ring for contiguous u8 chains (volumes)   */
-    MW_TUNE_COUNT = 7
+    MW_TUNE_HYST_FUSED = 7,   /* 1: several partitions of one rank run the whole plane loop in
+                                 ONE cooperative kernel (in-kernel halo exchange, device loop
+                                 condition); 0: one launch per partition and pass            */
+    MW_TUNE_COUNT = 8
 };
 mw_status mw_ctx_set_tuning(mw_ctx* ctx, int32_t knob, int32_t value);
 mw_status mw_ctx_get_tuning(const mw_ctx* ctx, int32_t knob, int32_t* value);

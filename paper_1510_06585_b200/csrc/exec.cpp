@@ -208,13 +208,18 @@ cudaEvent_t next_event(mw_ctx* c) {
 }
 // Brackets one partition's kernels of one class with CUDA events on the
 // launching stream (monitoring).
+// `shared`: a further partition of a launch already timed by another
+// PartTimer (several partitions in one launch): it feeds mw_last_timings but
+// not the per-kernel-class statistics, which count each launch once.
 struct PartTimer {
     mw_ctx* c;
     cudaStream_t s;
     int part, cls;
+    bool shared;
     cudaEvent_t a;
     unsigned long long l0;
-    PartTimer(mw_ctx* c_, cudaStream_t s_, int p, int cl) : c(c_), s(s_), part(p), cls(cl) {
+    PartTimer(mw_ctx* c_, cudaStream_t s_, int p, int cl, bool sh = false)
+        : c(c_), s(s_), part(p), cls(cl), shared(sh) {
         a = nullptr;
         l0 = mwk::launch_count();
         if (c->capturing || !c->monitor) return;
@@ -225,9 +230,9 @@ struct PartTimer {
         if (c->capturing || !c->monitor) return;
         cudaEvent_t b = next_event(c);
         cudaEventRecord(b, s);
-        mw_ctx::Rec r{part, cls, a, b, (int64_t)(mwk::launch_count() - l0)};
+        mw_ctx::Rec r{part, cls, a, b, shared ? 0 : (int64_t)(mwk::launch_count() - l0)};
         c->recs.push_back(r);
-        if (c->stats_on) c->stats.push_back(r);
+        if (c->stats_on && !shared) c->stats.push_back(r);
     }
 };
 mwk::Launch launch_for(mw_ctx* c, cudaStream_t s, int part) {
@@ -476,10 +481,6 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
     const int64_t rb = wp * 4;
     const Step& st = prog[1];
     const bool is_while = st.kind == StepKind::StencilWhile;
-    if (is_while && c->capturing)
-        return fail(MW_E_UNSUPPORTED,
-                    "this while-loop evaluates its condition on the host (several partitions) "
-                    "and cannot be captured in a graph");
     int64_t min_len = INT64_MAX;
     for (int p = 0; p < c->P; ++p)
         if (R.len[p] > 0) min_len = std::min(min_len, R.len[p]);
@@ -516,20 +517,108 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
         K[q] = static_cast<uint8_t*>(v);
         MW_OK_OR_RETURN(scratch(c, "mplane_tf_" + sq, (size_t)(2 * mwk::planes_tiles(len, W)), R.s, &v));
         fl[q] = static_cast<uint8_t*>(v);
-        for (uint8_t* b : {S[0][q], S[1][q], K[q]}) {   // halos outside the image stay 0
-            CUDA_OK(cudaMemsetAsync(b, 0, T * rb, R.s));
-            CUDA_OK(cudaMemsetAsync(b + (len + T) * rb, 0, T * rb, R.s));
-        }
         for (int a = 0; a < p; ++a) top[q] |= R.len[a] > 0;
         for (int a = p + 1; a < c->P; ++a) bot[q] |= R.len[a] > 0;
-        PartTimer t(c, R.s, p, MW_KC_U8);
-        MW_OK_OR_RETURN(kerr(mwk::planes_pack(pre[0], at_row<const uint8_t>(src, R.off[p]), W, len, W,
-                                              reinterpret_cast<uint32_t*>(S[0][q]),
-                                              reinterpret_cast<uint32_t*>(K[q]), launch_for(c, R.s, p), T),
+        // halo rows outside the image stay 0; the others are filled by the
+        // exchanges (K, S0 below; S1 by the first pass) before they are read
+        for (uint8_t* b : {S[0][q], S[1][q], K[q]}) {
+            if (!top[q]) CUDA_OK(cudaMemsetAsync(b, 0, T * rb, R.s));
+            if (!bot[q]) CUDA_OK(cudaMemsetAsync(b + (len + T) * rb, 0, T * rb, R.s));
+        }
+    }
+    std::vector<int> act;
+    bool slowed = false;
+    for (int q = 0; q < ppr; ++q) {
+        if (R.len[R.first + q] > 0) act.push_back(q);
+        slowed |= c->slow[R.first + q] > 1.0f;
+    }
+    // Without an injected slowdown the packs (unpacks) of all local partitions
+    // are one launch (blockIdx.y = partition); the launch is every active
+    // partition's compute time (they run concurrently inside it).
+    const bool batched = !slowed && !act.empty() && (int)act.size() <= mwk::kPlaneMaxParts;
+    auto timers_all = [&](int cls) {
+        std::vector<std::unique_ptr<PartTimer>> t;
+        for (int q : act) t.emplace_back(new PartTimer(c, R.s, R.first + q, cls, !t.empty()));
+        return t;
+    };
+    auto close_timers = [](std::vector<std::unique_ptr<PartTimer>>& t) {
+        while (!t.empty()) t.pop_back();   // closing events in reverse order
+    };
+    auto io_of = [&]() {
+        mwk::PlaneIO io{};
+        io.np = (int)act.size();
+        io.sp = W;
+        for (int i = 0; i < io.np; ++i) {
+            const int q = act[i], p = R.first + q;
+            io.src[i] = at_row<const uint8_t>(src, R.off[p]);
+            io.dst[i] = at_row<uint8_t>(dst, R.off[p]);
+            io.S0[i] = reinterpret_cast<uint32_t*>(S[0][q]);
+            io.S1[i] = reinterpret_cast<uint32_t*>(S[1][q]);
+            io.K[i] = reinterpret_cast<uint32_t*>(K[q]);
+            io.rows[i] = R.len[p];
+        }
+        return io;
+    };
+    if (batched) {
+        auto t = timers_all(MW_KC_U8);
+        MW_OK_OR_RETURN(kerr(mwk::planes_pack_io(pre[0], io_of(), W, launch_for(c, R.s, R.first), T),
                              "planes_pack"));
+        close_timers(t);
+    } else {
+        for (int q : act) {
+            const int p = R.first + q;
+            PartTimer t(c, R.s, p, MW_KC_U8);
+            MW_OK_OR_RETURN(kerr(mwk::planes_pack(pre[0], at_row<const uint8_t>(src, R.off[p]), W, R.len[p],
+                                                  W, reinterpret_cast<uint32_t*>(S[0][q]),
+                                                  reinterpret_cast<uint32_t*>(K[q]), launch_for(c, R.s, p), T),
+                                 "planes_pack"));
+        }
     }
     MW_OK_OR_RETURN(exchange_rows(R, K, T, rb));
     MW_OK_OR_RETURN(exchange_rows(R, S[0], T, rb));
+    // One rank, <= kPlaneMaxParts active partitions, no injected slowdown:
+    // the whole loop is one cooperative kernel over all partitions, halos
+    // exchanged inside it (stores into the neighbours' halo rows) and the loop
+    // condition decided on the device — no per-pass launches, copies or host
+    // reads.
+    if (c->nranks == 1 && batched && c->tune[mwk::TUNE_HYST_FUSED] != 0) {
+        mwk::PlaneMultiHost hm{};
+        hm.np = (int)act.size();
+        hm.wp = wp;
+        for (int i = 0; i < hm.np; ++i) {
+            const int q = act[i];
+            hm.S0[i] = reinterpret_cast<uint32_t*>(S[0][q]);
+            hm.S1[i] = reinterpret_cast<uint32_t*>(S[1][q]);
+            hm.K[i] = reinterpret_cast<const uint32_t*>(K[q]);
+            hm.fl[i] = fl[q];
+            hm.fl_bytes[i] = 2 * mwk::planes_tiles(R.len[R.first + q], W);
+            hm.rows[i] = R.len[R.first + q];
+        }
+        int* state = d_last + 4;   // {E, converged, final buffer}: read by the unpack
+        int* pflags = d_last + 8;
+        CUDA_OK(cudaMemsetAsync(pflags, 0xFF, 3 * sizeof(int), R.s));
+        {
+            auto t = timers_all(MW_KC_STENCIL);
+            MW_OK_OR_RETURN(kerr(mwk::planes_multi(hm, T, st.n, pflags, state, launch_for(c, R.s, R.first)),
+                                 "planes_multi"));
+            close_timers(t);
+        }
+        {
+            auto t = timers_all(MW_KC_U8);
+            MW_OK_OR_RETURN(kerr(mwk::planes_unpack_io(post, io_of(), state, W, W, launch_for(c, R.s, R.first), T),
+                                 "planes_unpack"));
+            close_timers(t);
+        }
+        if (is_while) {
+            CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 8, cudaMemcpyDeviceToHost, R.s));
+            f->plane_loop = true;
+        }
+        return MW_OK;
+    }
+    if (is_while && c->capturing)
+        return fail(MW_E_UNSUPPORTED,
+                    "this while-loop evaluates its condition on the host (several ranks or "
+                    "partitions) and cannot be captured in a graph");
     // The host reads the (running-max) last changing execution LAG passes
     // behind the device, so the GPU never waits for it; passes queued after
     // the fixed point change nothing, so they cost only their boundary tiles.
@@ -597,6 +686,15 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
     if (is_while) {
         f->executions += (double)E;
         if (!converged) f->converged = 0.0;
+    }
+    if (batched) {   // d_last[4..6] = 0: the unpack reads S0, here set to the final buffer
+        mwk::PlaneIO io = io_of();
+        for (int i = 0; i < io.np; ++i) io.S0[i] = reinterpret_cast<uint32_t*>(S[cur][act[i]]);
+        auto t = timers_all(MW_KC_U8);
+        MW_OK_OR_RETURN(kerr(mwk::planes_unpack_io(post, io, d_last + 4, W, W, launch_for(c, R.s, R.first), T),
+                             "planes_unpack"));
+        close_timers(t);
+        return MW_OK;
     }
     for (int q = 0; q < ppr; ++q) {
         const int p = R.first + q;

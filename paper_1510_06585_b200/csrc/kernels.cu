@@ -886,14 +886,18 @@ __device__ __forceinline__ uint32_t expand_nib(uint32_t n) {      // 4 bits -> 0
 
 // SEG >= 0: the chain is exactly one threshold with compile-time compare modes
 // (lo mode = SEG / 4, hi mode = SEG % 4); SEG < 0: any chain ending with it.
+// blockIdx.y = partition (PlaneIO table: several partitions in one launch)
 template <int SEG>
 __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8Prog p,
                                                      const __grid_constant__ U8Const c,
-                                                     const uint8_t* __restrict__ src, int64_t sp,
-                                                     int64_t rows, int64_t W, int64_t wp,
-                                                     uint32_t* __restrict__ S,
-                                                     uint32_t* __restrict__ K, FastDiv WP, int hd) {
-    const uint32_t total = (uint32_t)(rows * wp);
+                                                     const __grid_constant__ PlaneIO io, int64_t W,
+                                                     int64_t wp, FastDiv WP, int hd) {
+    const int q = blockIdx.y;
+    const uint8_t* __restrict__ src = io.src[q];
+    const int64_t sp = io.sp;
+    uint32_t* __restrict__ S = io.S0[q];
+    uint32_t* __restrict__ K = io.K[q];
+    const uint32_t total = (uint32_t)(io.rows[q] * wp);
     uint32_t one;
     asm volatile("mov.u32 %0, %%nsmid;" : "=r"(one));
     one = one > 0u ? 1u : 0u;
@@ -963,15 +967,15 @@ __global__ void __launch_bounds__(256) k_planes_pack(const __grid_constant__ U8P
 // covers 512 contiguous bytes, and the 8 plane-word loads per lane (2 lanes
 // share a word) are issued before any store.  (The per-word variant below
 // left every thread with one dependent L2 load per 32 bytes of output.)
-__global__ void __launch_bounds__(256) k_planes_unpack_fin_w(const uint32_t* __restrict__ S0,
-                                                             const uint32_t* __restrict__ S1,
+__global__ void __launch_bounds__(256) k_planes_unpack_fin_w(const __grid_constant__ PlaneIO io,
                                                              const int* __restrict__ state,
-                                                             uint8_t* __restrict__ dst, int64_t dp,
-                                                             int64_t rows, int64_t wp, FastDiv UPR,
+                                                             int64_t dp, int64_t wp, FastDiv UPR,
                                                              int hd) {
-    const uint32_t* S = state[2] ? S1 : S0;
+    const int q = blockIdx.y;
+    const uint32_t* S = state[2] ? io.S1[q] : io.S0[q];
+    uint8_t* __restrict__ dst = io.dst[q];
     const int lane = threadIdx.x & 31;
-    const uint32_t total = (uint32_t)(rows * (wp / 128));
+    const uint32_t total = (uint32_t)(io.rows[q] * (wp / 128));
     for (uint32_t u = blockIdx.x * 8u + (threadIdx.x >> 5); u < total; u += gridDim.x * 8u) {
         const uint32_t y = fdiv(u, UPR), q = u - y * UPR.d;
         const uint32_t* srow = S + ((int64_t)y + hd) * wp + 128ll * q;
@@ -996,15 +1000,14 @@ __global__ void __launch_bounds__(256) k_planes_unpack_fin_w(const uint32_t* __r
 template <bool FIN_ONLY>
 __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U8Prog p,
                                                        const __grid_constant__ U8Const c,
-                                                       const uint32_t* __restrict__ S0,
-                                                       const uint32_t* __restrict__ S1,
-                                                       const uint32_t* __restrict__ K,
-                                                       const int* __restrict__ state,
-                                                       uint8_t* __restrict__ dst, int64_t dp,
-                                                       int64_t rows, int64_t W, int64_t wp,
-                                                       FastDiv WP, int hd) {
-    const uint32_t* S = state[2] ? S1 : S0;
-    const uint32_t total = (uint32_t)(rows * wp);
+                                                       const __grid_constant__ PlaneIO io,
+                                                       const int* __restrict__ state, int64_t dp,
+                                                       int64_t W, int64_t wp, FastDiv WP, int hd) {
+    const int q = blockIdx.y;
+    const uint32_t* S = state[2] ? io.S1[q] : io.S0[q];
+    const uint32_t* __restrict__ K = io.K[q];
+    uint8_t* __restrict__ dst = io.dst[q];
+    const uint32_t total = (uint32_t)(io.rows[q] * wp);
     for (uint32_t n = blockIdx.x * 256u + threadIdx.x; n < total; n += gridDim.x * 256u) {
         const uint32_t y = fdiv(n, WP), w = n - y * WP.d;
         const uint32_t sb = S[(y + hd) * wp + w];
@@ -1360,6 +1363,165 @@ __global__ void __launch_bounds__(256) k_planes_pass(const __grid_constant__ CUt
     if (lane == 0 && my_last >= 0) atomicMax(last, (int)(k0 + my_last));
 }
 
+// Whole loop over SEVERAL partitions of one rank in one cooperative kernel.
+// The partitions keep their own plane buffers with T halo rows (the layout
+// of the per-pass protocol); the global tile list is the concatenation of the
+// partitions' tiles.  The halo exchange between neighbouring partitions is
+// folded into the store: a tile writing owned rows y < T (y >= rows - T) of
+// partition q also writes them into the bottom (top) halo rows of the previous
+// (next) active partition's output buffer — a pointer table, no extra pass
+// and no extra barrier; the next pass reads them through TMA after the grid
+// barrier.  Loop condition and exact E as in k_planes_loop.
+template <int T, int ROWS>
+__device__ __forceinline__ void plane_store_fwd(const uint32_t (&sv)[ROWS], const PlaneMultiArgs& a,
+                                                int q, int cur, int64_t strip, int64_t w, bool own_lane,
+                                                bool wv) {
+    constexpr int R = ROWS - 2 * T;
+    if (!own_lane || !wv) return;
+    const PlanePartDesc& d = a.p[q];
+    const int64_t y0 = strip * R;                      // owned row 0 of the tile
+    const int64_t wp = a.wp;
+    if (d.prev >= 0 && y0 < T) {                       // top rows -> prev's bottom halo
+        const PlanePartDesc& pd = a.p[d.prev];
+        uint32_t* o = pd.S[cur ^ 1] + (pd.rows + T + y0) * wp + w;
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (y0 + i < T && y0 + i < d.rows) o[i * wp] = sv[T + i];
+    }
+    if (d.next >= 0 && y0 + R > d.rows - T) {          // bottom rows -> next's top halo
+        uint32_t* o = a.p[d.next].S[cur ^ 1] + w;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int64_t y = y0 + i;
+            if (y >= d.rows - T && y < d.rows) o[(y - d.rows + T) * wp] = sv[T + i];
+        }
+    }
+}
+
+template <int T, int ROWS>
+__device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, int cur, int steps,
+                                                     bool first, int64_t gw, int64_t nwarps, int lane,
+                                                     uint32_t* sb, uint32_t* kb, uint64_t* bar,
+                                                     uint32_t& phase) {
+    constexpr int R = ROWS - 2 * T;
+    constexpr int OW = 30;
+    constexpr int BW = 36;
+    constexpr uint32_t kBox = ROWS * BW * 4;
+    const int64_t n_cb = a.n_cb;
+    const bool own_lane = lane >= 1 && lane <= OW;
+    auto locate = [&](int64_t t, int& q) {
+        q = 0;
+        while (q + 1 < a.np && t >= a.p[q + 1].tile0) ++q;
+        return t - a.p[q].tile0;
+    };
+    auto next_active = [&](int64_t t) {
+        for (; t < a.total; t += nwarps) {
+            int q;
+            const int64_t lt = locate(t, q);
+            const PlanePartDesc& d = a.p[q];
+            const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
+            if (plane_tile_active(d.fl + (cur ^ 1) * d.nt, strip, cb, d.n_strips, n_cb, first,
+                                  d.prev >= 0, d.next >= 0, lane))
+                break;
+            if (lane == 0) d.fl[cur * d.nt + lt] = 0;
+        }
+        return t;
+    };
+    auto issue = [&](int64_t t) {
+        if (lane == 0) {
+            int q;
+            const int64_t lt = locate(t, q);
+            const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
+            const int x = (int)(cb * OW - 1) & ~3, y = (int)(strip * R);   // buffer row (hd = T)
+            mbar_expect_tx(bar, 2 * kBox);
+            tma_load_2d(sb, &a.ts[q][cur], x, y, bar);
+            tma_load_2d(kb, &a.tk[q], x, y, bar);
+        }
+    };
+    int my_last = -1;
+    int64_t t = next_active(gw);
+    if (t < a.total) issue(t);
+    while (t < a.total) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        int q;
+        const int64_t lt = locate(t, q);
+        const int o = (int)((lt % n_cb) * OW - 1) & 3;
+        uint32_t sv[ROWS], kv[ROWS];
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+            sv[i] = sb[i * BW + o + lane];
+            kv[i] = kb[i * BW + o + lane];
+        }
+        __syncwarp();
+        const int64_t tn = next_active(t + nwarps);
+        if (tn < a.total) issue(tn);
+        const PlanePartDesc& d = a.p[q];
+        const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
+        const int64_t w = cb * OW - 1 + lane;
+        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
+        const uint8_t fl = tl < 0 ? 0 : (tl == steps - 1 ? 3 : 2);
+        my_last = max(my_last, tl);
+        const bool wv = w >= 0 && w < a.wp;
+        plane_store<T, ROWS>(sv, d.S[cur ^ 1], d.rows, a.wp, T, strip * R - T, w, own_lane, wv);
+        plane_store_fwd<T, ROWS>(sv, a, q, cur, strip, w, own_lane, wv);
+        if (lane == 0) d.fl[cur * d.nt + lt] = fl;
+        t = tn;
+    }
+    return my_last;
+}
+
+template <int T, int ROWS>
+__global__ void __launch_bounds__(256) k_planes_multi(const __grid_constant__ PlaneMultiArgs a,
+                                                      int64_t max_iters, int* __restrict__ flags,
+                                                      int* __restrict__ state) {
+    constexpr int BW = 36;
+    extern __shared__ __align__(128) uint32_t psm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * ROWS * BW);
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* sb = psm + wid * (2 * ROWS * BW);
+    uint32_t* kb = sb + ROWS * BW;
+    uint64_t* bar = &bars[wid];
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t gw = (int64_t)blockIdx.x * 8 + wid;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    uint32_t phase = 0;
+    int64_t k0 = 0;
+    int pass = 0;
+    while (k0 < max_iters) {
+        const int steps = (int)min((int64_t)T, max_iters - k0);
+        if (leader) flags[(pass + 1) % 3] = -1;
+        const int my_last = plane_multi_pass_warp<T, ROWS>(a, pass & 1, steps, pass == 0, gw, nwarps,
+                                                           lane, sb, kb, bar, phase);
+        if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        grid.sync();
+        const int last = *((volatile int*)&flags[pass % 3]);
+        if (last < k0 + steps - 1) {
+            if (leader) {
+                const int64_t last_global = last >= 0 ? last : k0 - 1;
+                state[0] = (int)(last_global + 2);
+                state[1] = 1;
+                state[2] = (pass & 1) ? 0 : 1;
+            }
+            return;
+        }
+        k0 += steps;
+        ++pass;
+    }
+    if (leader) {
+        state[0] = (int)max_iters;
+        state[1] = 0;
+        state[2] = pass == 0 ? 0 : (((pass - 1) & 1) ? 0 : 1);
+    }
+}
+
 // ------------------------------------------------------------ N-body
 // a_i = sum_j m_j d_ij (|d_ij|^2 + eps2)^-3/2 (R12): fp32 inside each
 // 256-source tile (global tile boundaries, so results do not depend on the
@@ -1698,9 +1860,10 @@ void tune_defaults(int* out) {
     out[TUNE_HYST_ROWS] = tuning_knob("MW_HYST_ROWS", 48);   // (8, 48): 0.407 vs 0.44 ms (8, 40)
     out[TUNE_NBODY_SPLIT] = tuning_knob("MW_NBODY_SPLIT", 0);
     out[TUNE_U8_TMA] = tuning_knob("MW_U8_TMA", 1);
+    out[TUNE_HYST_FUSED] = tuning_knob("MW_HYST_FUSED", 1);
     for (int k = 0; k < TUNE_COUNT; ++k)
         if (!tune_valid(k, out[k])) {   // ignore malformed overrides
-            const int d[TUNE_COUNT] = {1, 2, 1, 8, 40, 0, 1};
+            const int d[TUNE_COUNT] = {1, 2, 1, 8, 48, 0, 1, 1};
             out[k] = d[k];
         }
 }
@@ -1714,6 +1877,7 @@ bool tune_valid(int knob, int v) {
         case TUNE_HYST_ROWS: return v == 32 || v == 40 || v == 48;
         case TUNE_NBODY_SPLIT: return v == 0 || v == 1;
         case TUNE_U8_TMA: return v == 0 || v == 1;
+        case TUNE_HYST_FUSED: return v == 0 || v == 1;
     }
     return false;
 }
@@ -2086,20 +2250,27 @@ cudaError_t reduce_ranks(const void* const* srcs, int n, void* dst, size_t count
 // rounded up to 4 words: the row pitch of a TMA tensor map is a multiple of 16 B
 int64_t plane_words(int64_t W) { return (W + 127) / 128 * 4; }
 
-cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
-                        uint32_t* S, uint32_t* K, const Launch& L, int hd) {
+// grid: x = resident CTAs split over the partitions (y), at least one each
+static dim3 io_grid(const PlaneIO& io, int64_t per_row_items, int occ, const Launch& L) {
+    int64_t tot = 0;
+    for (int q = 0; q < io.np; ++q) tot += io.rows[q] * per_row_items;
+    const unsigned gx = grid_for(tot, occ, L);
+    return dim3(std::max(1u, gx / (unsigned)io.np), io.np);
+}
+
+cudaError_t planes_pack_io(const U8Prog& p, const PlaneIO& io, int64_t W, const Launch& L, int hd) {
     const int64_t wp = plane_words(W);
-    if (rows * wp >= (1ll << 31)) return cudaErrorInvalidValue;
-    if (rows <= 0) return cudaSuccess;
-    const int64_t tiles = (rows * wp + 255) / 256;
+    if (io.np < 1 || io.np > kPlaneMaxParts) return cudaErrorInvalidValue;
+    for (int q = 0; q < io.np; ++q)
+        if (io.rows[q] <= 0 || io.rows[q] * wp >= (1ll << 31)) return cudaErrorInvalidValue;
     const U8Const c = u8_consts(p);
     ++g_launches;
     const FastDiv WPd = make_fastdiv((uint32_t)wp);
 #define MW_PACK(SEGV)                                                                       \
     {                                                                                       \
         static int occ = resident_ctas(k_planes_pack<SEGV>, 256);                           \
-        k_planes_pack<SEGV><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(p, c, src, sp, rows, \
-                                                                          W, wp, S, K, WPd, hd); \
+        k_planes_pack<SEGV><<<io_grid(io, (wp + 255) / 256, occ, L), 256, 0, L.stream>>>(     \
+            p, c, io, W, wp, WPd, hd);                                                      \
         return cudaGetLastError();                                                          \
     }
     if (p.n == 1 && p.kind[0] == U8_SEGMENT) {
@@ -2121,30 +2292,64 @@ cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t
 #undef MW_PACK
 }
 
+cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
+                        uint32_t* S, uint32_t* K, const Launch& L, int hd) {
+    if (rows <= 0) return cudaSuccess;
+    PlaneIO io{};
+    io.np = 1;
+    io.sp = sp;
+    io.src[0] = src;
+    io.S0[0] = S;
+    io.K[0] = K;
+    io.rows[0] = rows;
+    return planes_pack_io(p, io, W, L, hd);
+}
+
+cudaError_t planes_unpack_io(const U8Prog& p, const PlaneIO& io, const int* state, int64_t dp,
+                             int64_t W, const Launch& L, int hd) {
+    const int64_t wp = plane_words(W);
+    if (io.np < 1 || io.np > kPlaneMaxParts) return cudaErrorInvalidValue;
+    bool dst_aligned = dp % 16 == 0, wide_ok = true;
+    for (int q = 0; q < io.np; ++q) {
+        if (io.rows[q] <= 0 || io.rows[q] * wp >= (1ll << 31)) return cudaErrorInvalidValue;
+        dst_aligned &= (reinterpret_cast<uintptr_t>(io.dst[q]) & 15) == 0;
+        wide_ok &= io.rows[q] * (wp / 128) < (1ll << 31);
+    }
+    const U8Const c = u8_consts(p);
+    ++g_launches;
+    if (p.n == 1 && p.kind[0] == U8_FINALIZE && wp % 128 == 0 && dst_aligned && wide_ok) {
+        static int occ = resident_ctas(k_planes_unpack_fin_w, 256);
+        // one warp per 128 plane words of a row
+        dim3 g = io_grid(io, 1, occ, L);
+        int64_t units = 0;
+        for (int q = 0; q < io.np; ++q) units = std::max(units, io.rows[q] * (wp / 128));
+        g.x = (unsigned)std::min<int64_t>(g.x, std::max<int64_t>(1, (units + 7) / 8));
+        k_planes_unpack_fin_w<<<g, 256, 0, L.stream>>>(io, state, dp, wp,
+                                                       make_fastdiv((uint32_t)(wp / 128)), hd);
+    } else if (p.n == 1 && p.kind[0] == U8_FINALIZE) {
+        static int occ = resident_ctas(k_planes_unpack<true>, 256);
+        k_planes_unpack<true><<<io_grid(io, (wp + 255) / 256, occ, L), 256, 0, L.stream>>>(
+            p, c, io, state, dp, W, wp, make_fastdiv((uint32_t)wp), hd);
+    } else {
+        static int occ = resident_ctas(k_planes_unpack<false>, 256);
+        k_planes_unpack<false><<<io_grid(io, (wp + 255) / 256, occ, L), 256, 0, L.stream>>>(
+            p, c, io, state, dp, W, wp, make_fastdiv((uint32_t)wp), hd);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S1,
                           const uint32_t* K, const int* state, uint8_t* dst, int64_t dp,
                           int64_t rows, int64_t W, const Launch& L, int hd) {
-    const int64_t wp = plane_words(W);
     if (rows <= 0) return cudaSuccess;
-    const int64_t tiles = (rows * wp + 255) / 256;
-    const U8Const c = u8_consts(p);
-    ++g_launches;
-    if (p.n == 1 && p.kind[0] == U8_FINALIZE && wp % 128 == 0 && dp % 16 == 0 &&
-        (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && rows * (wp / 128) < (1ll << 31)) {
-        static int occ = resident_ctas(k_planes_unpack_fin_w, 256);
-        const int64_t units = rows * (wp / 128);
-        k_planes_unpack_fin_w<<<grid_for((units + 7) / 8, occ, L), 256, 0, L.stream>>>(
-            S0, S1, state, dst, dp, rows, wp, make_fastdiv((uint32_t)(wp / 128)), hd);
-    } else if (p.n == 1 && p.kind[0] == U8_FINALIZE) {
-        static int occ = resident_ctas(k_planes_unpack<true>, 256);
-        k_planes_unpack<true><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp), hd);
-    } else {
-        static int occ = resident_ctas(k_planes_unpack<false>, 256);
-        k_planes_unpack<false><<<grid_for(tiles, occ, L), 256, 0, L.stream>>>(
-            p, c, S0, S1, K, state, dst, dp, rows, W, wp, make_fastdiv((uint32_t)wp), hd);
-    }
-    return cudaGetLastError();
+    PlaneIO io{};
+    io.np = 1;
+    io.S0[0] = const_cast<uint32_t*>(S0);
+    io.S1[0] = const_cast<uint32_t*>(S1);
+    io.K[0] = const_cast<uint32_t*>(K);
+    io.dst[0] = dst;
+    io.rows[0] = rows;
+    return planes_unpack_io(p, io, state, dp, W, L, hd);
 }
 
 int64_t planes_tiles(int64_t rows, int64_t W) {   // upper bound over the variants (R >= 8)
@@ -2310,6 +2515,64 @@ cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t r
     MW_PL(6, 48);
 #undef MW_PL
     return planes_loop_t<8, 48>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L);
+}
+
+template <int T, int ROWS>
+static cudaError_t planes_multi_t(const PlaneMultiHost& h, int64_t max_iters, int* flags, int* state,
+                                  const Launch& L) {
+    constexpr size_t smem = plane_smem_bytes<ROWS>();
+    static int occ = [] {
+        cudaFuncSetAttribute(k_planes_multi<T, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        return resident_ctas(k_planes_multi<T, ROWS>, 256, smem);
+    }();
+    constexpr int R = ROWS - 2 * T;
+    static PlaneMultiArgs a;   // host staging of the (large) parameter block
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    a = PlaneMultiArgs{};
+    a.np = h.np;
+    a.wp = h.wp;
+    a.n_cb = (h.wp + 29) / 30;
+    int64_t tiles = 0;
+    for (int q = 0; q < h.np; ++q) {
+        PlanePartDesc& d = a.p[q];
+        d.S[0] = h.S0[q];
+        d.S[1] = h.S1[q];
+        d.fl = h.fl[q];
+        d.rows = h.rows[q];
+        d.n_strips = (d.rows + R - 1) / R;
+        d.nt = d.n_strips * a.n_cb;
+        d.tile0 = tiles;
+        tiles += d.nt;
+        d.prev = q > 0 ? q - 1 : -1;
+        d.next = q + 1 < h.np ? q + 1 : -1;
+        if (d.rows < T || 2 * d.nt > h.fl_bytes[q]) return cudaErrorInvalidValue;
+        if (!plane_tmap(&a.ts[q][0], h.S0[q], d.rows, h.wp, ROWS, T) ||
+            !plane_tmap(&a.ts[q][1], h.S1[q], d.rows, h.wp, ROWS, T) ||
+            !plane_tmap(&a.tk[q], h.K[q], d.rows, h.wp, ROWS, T))
+            return cudaErrorInvalidValue;
+    }
+    a.total = tiles;
+    const unsigned grid = grid_for((tiles + 7) / 8, occ, L);
+    int64_t mi = max_iters;
+    void* args[] = {&a, &mi, &flags, &state};
+    ++g_launches;
+    return cudaLaunchCooperativeKernel((const void*)k_planes_multi<T, ROWS>, dim3(grid), dim3(256), args,
+                                       smem, L.stream);
+}
+
+cudaError_t planes_multi(const PlaneMultiHost& h, int T, int64_t max_iters, int* flags, int* state,
+                         const Launch& L) {
+    if (h.np < 1 || h.np > kPlaneMaxParts) return cudaErrorInvalidValue;
+    switch (T) {
+        case 12: return planes_multi_t<12, 40>(h, max_iters, flags, state, L);
+        case 8: return planes_multi_t<8, 48>(h, max_iters, flags, state, L);
+        case 6: return planes_multi_t<6, 32>(h, max_iters, flags, state, L);
+        case 4: return planes_multi_t<4, 32>(h, max_iters, flags, state, L);
+        case 2: return planes_multi_t<2, 32>(h, max_iters, flags, state, L);
+        default: return planes_multi_t<1, 32>(h, max_iters, flags, state, L);
+    }
 }
 
 int64_t nbody_part_doubles(int64_t count) { return (int64_t)kNbSeg * count * 3; }

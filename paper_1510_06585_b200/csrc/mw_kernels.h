@@ -2,6 +2,7 @@
 // (runtime.cpp) and the sm_100a kernels (kernels.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace mwk {
@@ -15,7 +16,8 @@ constexpr int kMaxOps = 16;
 // bit-identical results, only speed changes.
 enum TuneKnob : int {
     TUNE_RGBA_TMA = 0, TUNE_RGBA_UNROLL = 1, TUNE_HYST_PLANES = 2, TUNE_HYST_T = 3,
-    TUNE_HYST_ROWS = 4, TUNE_NBODY_SPLIT = 5, TUNE_U8_TMA = 6, TUNE_COUNT = 7
+    TUNE_HYST_ROWS = 4, TUNE_NBODY_SPLIT = 5, TUNE_U8_TMA = 6, TUNE_HYST_FUSED = 7,
+    TUNE_COUNT = 8
 };
 void tune_defaults(int* out);                 // measured best on B200 (+ MW_* env overrides)
 bool tune_valid(int knob, int value);
@@ -111,6 +113,56 @@ int planes_pass_depth(int T_pref, int64_t min_rows);   // largest built T <= bot
 cudaError_t planes_pass(const uint32_t* in, uint32_t* out, const uint32_t* K, int64_t rows,
                         int64_t W, int T, int steps, int64_t k0, const uint8_t* fprev,
                         uint8_t* fcur, int first, int top, int bot, int* last, const Launch& L);
+
+// The same over several partitions in ONE launch each (blockIdx.y = entry):
+// entry q packs rows src[q] (pitch sp) into S0[q] / K[q], resp. unpacks
+// (state[2] ? S1[q] : S0[q], K[q]) into dst[q] (pitch dp); rows[q] > 0.
+constexpr int kPlaneMaxParts = 8;
+struct PlaneIO {
+    int np;
+    int64_t sp;
+    const uint8_t* src[kPlaneMaxParts];
+    uint8_t* dst[kPlaneMaxParts];
+    uint32_t* S0[kPlaneMaxParts];
+    uint32_t* S1[kPlaneMaxParts];
+    uint32_t* K[kPlaneMaxParts];
+    int64_t rows[kPlaneMaxParts];
+};
+cudaError_t planes_pack_io(const U8Prog& p, const PlaneIO& io, int64_t W, const Launch& L, int hd);
+cudaError_t planes_unpack_io(const U8Prog& p, const PlaneIO& io, const int* state, int64_t dp,
+                             int64_t W, const Launch& L, int hd);
+// Several partitions of one rank, the whole loop in ONE cooperative kernel
+// (partitions in row order, every one with rows >= T; planes with T halo
+// rows as for planes_pass; pack + the initial K / S0 halo exchange done by the
+// caller).  Halos between consecutive partitions are exchanged inside the
+// kernel (stores into the neighbour's halo rows).  state[0..2] as
+// planes_loop (state[2]: index of the final buffer, S0 or S1, of every
+// partition); flags: 3 ints of scratch.
+struct PlanePartDesc {
+    uint32_t* S[2];
+    uint8_t* fl;                     // 2 x nt tile flags
+    int64_t rows, n_strips, nt, tile0;
+    int prev, next;                  // neighbouring partition in the table, -1 at the image edge
+};
+struct PlaneMultiArgs {
+    CUtensorMap ts[kPlaneMaxParts][2];
+    CUtensorMap tk[kPlaneMaxParts];
+    PlanePartDesc p[kPlaneMaxParts];
+    int np;
+    int64_t wp, n_cb, total;
+};
+struct PlaneMultiHost {
+    int np;
+    int64_t wp;
+    uint32_t* S0[kPlaneMaxParts];
+    uint32_t* S1[kPlaneMaxParts];
+    const uint32_t* K[kPlaneMaxParts];
+    uint8_t* fl[kPlaneMaxParts];
+    int64_t fl_bytes[kPlaneMaxParts];
+    int64_t rows[kPlaneMaxParts];
+};
+cudaError_t planes_multi(const PlaneMultiHost& h, int T, int64_t max_iters, int* flags, int* state,
+                         const Launch& L);
 
 // ------------------------------------------------------------ N-body
 // Bodies [first, first+count) of N: direct-sum acceleration (fp32 per

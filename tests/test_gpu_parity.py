@@ -1039,3 +1039,54 @@ def test_hysteresis_threshold_modes(lohi):
         r = run(pctx(k, d, 1), trees.hysteresis(*lohi), [M.arg(dev(gray)), M.arg(dst)])
         assert np.array_equal(dst.cpu().numpy(), want), (lohi, k)
         assert r["executions"] == D + 1, (lohi, k)
+
+
+# ----------------------------------------------------------------- hysteresis: fused multi-partition loop
+@pytest.mark.parametrize("fused", [1, 0])
+def test_hysteresis_partitions_fused_and_per_pass(fused):
+    """Several partitions of one rank: the whole loop in one cooperative kernel
+    (in-kernel halo stores into the neighbours' halo rows, device loop
+    condition) or one launch per partition and pass — identical output, E."""
+    rng = np.random.default_rng(11)
+    H, W = 777, 1300
+    gray = synth.np_u8_stream(8, 9, H * W).reshape(H, W)
+    want, D = oracle_hyst(gray)
+    L = K.segment(gray, 173, 250)
+    for k, d in [(8, None), (8, [0.3, 0.01, 0.0, 0.2, 0.09, 0.2, 0.0, 0.2]), (2, [0.999, 0.001])] + \
+            [(5, x) for x in dists(5, rng, 2)]:
+        c = pctx(k, d, 1)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_FUSED, fused)
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(c, trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want), d
+        assert r["executions"] == D + 1 and r["converged"]
+        for n in (D - 2, 3):
+            dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+            r = run(c, trees.hysteresis(max_iters=n), [M.arg(dev(gray)), M.arg(dst)])
+            assert np.array_equal(dst.cpu().numpy(), K.hyst_finalize(K.hyst_bfs(L, n)[0]))
+            assert r["executions"] == n and not r["converged"]
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        run(c, M.mw_loop_for(M.mw_kernel_hysteresis_step(), 13), [M.arg(dev(L)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, 13)[0])
+
+
+def test_hysteresis_fused_partitions_graph_capture():
+    """The fused multi-partition loop decides its condition on the device, so
+    the while-loop tree can be captured and replayed."""
+    H, W = 500, 640
+    gray = synth.np_u8_stream(8, 4, H * W).reshape(H, W)
+    want, D = oracle_hyst(gray)
+    c = pctx(4, [0.1, 0.4, 0.2, 0.3], 1)
+    s = torch.cuda.Stream()
+    src = dev(gray)
+    dst = torch.zeros_like(src)
+    torch.cuda.synchronize()
+    g = M.mw_graph_capture(c, trees.hysteresis(), [M.arg(src), M.arg(dst)], stream=s)
+    for _ in range(2):
+        dst.zero_()
+        torch.cuda.synchronize()
+        g.launch(s)
+        s.synchronize()
+        assert np.array_equal(dst.cpu().numpy(), want)
+        r = g.result()
+        assert r["executions"] == D + 1 and r["converged"]

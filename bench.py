@@ -296,6 +296,54 @@ class Saxpy(Workload):
         self.graphs = [self.graph]
         self.graph_kernels = self.graph.kernels // self.B
 
+    def warm_capture(self, stream):
+        """Warm-L2 auxiliary: the same graph shape on buffer set 0 only."""
+        self.warm_graph = self.M.mw_graph_capture_many(self.ctx, self.tree,
+                                                       [list(self.sets[0])] * self.B, stream)
+
+    def warm_timed(self, timed, k):
+        g0, self.graph = self.graph, self.warm_graph
+        timed(self.B)
+        t = timed(k)[0]
+        self.graph = g0
+        return t / k
+
+    def extra_aux(self, timed, start, stop, stream):
+        """n = 2^28 (3 GiB of traffic per run) shows the
+        kernel's own HBM efficiency; and the same rotating-buffer graph with
+        its runs strictly serialized (one lane) next to the default
+        dependency-aware graph (independent runs on parallel lanes)."""
+        torch, M = self.torch, self.M
+        out = {}
+        n = 1 << 28
+        x = torch.empty(n, dtype=torch.float32, device=self.dev)
+        y = torch.empty(n, dtype=torch.float32, device=self.dev)
+        self.synth.dev_fill_f32_um11(x, self.synth.SEED_SAXPY_X, 0)
+        self.synth.dev_fill_f32_um11(y, self.synth.SEED_SAXPY_Y, 0)
+        al = M.ArgList([M.arg(x), M.arg(y)])
+        ts = []
+        for r in range(6):
+            start.record(stream)
+            M.mw_run(self.ctx, self.tree, al, stream=stream)
+            stop.record(stream)
+            torch.cuda.synchronize()
+            if r:
+                ts.append(start.elapsed_time(stop))
+        ms = statistics.median(ts)
+        gbs = 12.0 * n / (ms / 1e3) / 1e9
+        out["n_2p28"] = {"ms_per_run": ms, "achieved_gbs": gbs, "frac": gbs / peaks()["hbm_gbs"]}
+        del x, y, al
+        lanes0 = M.mw_ctx_get_tuning(self.ctx, M.MW_TUNE_GRAPH_LANES)
+        M.mw_ctx_set_tuning(self.ctx, M.MW_TUNE_GRAPH_LANES, 1)
+        g1 = M.mw_graph_capture_many(self.ctx, self.tree, [list(st) for st in self.sets], stream)
+        M.mw_ctx_set_tuning(self.ctx, M.MW_TUNE_GRAPH_LANES, lanes0)
+        g0, self.graph = self.graph, g1
+        timed(self.B)
+        k = max(self.B, 2000 // self.B * self.B)
+        out["serialized_graph_ms_per_step"] = timed(k)[0] / k
+        self.graph = g0
+        return out
+
     def run_steps(self, k):
         assert k % self.B == 0, "steps must be a multiple of the buffer-set count"
         for _ in range(k // self.B):
@@ -633,6 +681,20 @@ def cpu_rate(name, budget_s):
 
 
 # ------------------------------------------------------------------ arms
+def host_info():
+    """nproc and the CPU model of the box the oracle ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "threads_used": 1}
+
+
 def run_reference(args, dist):
     """Reference arm: the CPU oracle as it stands, on host cores (rank 0 only)."""
     if dist.rank != 0:
@@ -666,7 +728,7 @@ def run_reference(args, dist):
                            arm=("CPU oracle (oracle/fft.py, numpy pocketfft fp64, 1 thread)"
                                 if wl == "fft" else "CPU oracle (oracle/, plain C, 1 thread)")),
             "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "oracle",
-                             "sample": f"per step: {sample}"},
+                             "sample": f"per step: {sample}", **host_info()},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -722,18 +784,31 @@ def run_marrow(args, dist, wl_name):
     # rebalancer, which is not part of a step.  Per-kernel times come from a
     # separate monitored pass below.
     M.mw_ctx_set_monitoring(ctx, False)
-    l0 = M.mw_ctx_launch_count(ctx)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dist.local) as clocks:
+
+    def timed(k):
+        """K steps between a barrier + synchronize on both sides: CUDA events
+        on the launch stream, max over ranks (ms for the K steps)."""
+        dist.barrier()
+        torch.cuda.synchronize()
         start.record(stream)
-        futs = w.run_steps(args.steps) if hasattr(w, "run_steps") else \
-            [w.step(i) for i in range(args.steps)]
+        fs = w.run_steps(k) if hasattr(w, "run_steps") else [w.step(i) for i in range(k)]
         stop.record(stream)
         torch.cuda.synchronize()
-    ms_local = start.elapsed_time(stop)
-    launches = M.mw_ctx_launch_count(ctx) - l0
+        return dist.max(start.elapsed_time(stop)), fs
+
+    # SURVEY §8(d) d.0: the median of `trials` timed trials of K steps (min and
+    # max reported); clocks sampled over all of them
+    trials = []
+    with ClockSampler(dist.local) as clocks:
+        for tr in range(args.trials):
+            l0 = M.mw_ctx_launch_count(ctx)
+            t_ms, futs = timed(args.steps)
+            launches = M.mw_ctx_launch_count(ctx) - l0
+            trials.append(t_ms)
+            if tr + 1 < args.trials:
+                del futs
+    ms_local = statistics.median(trials)
     if hasattr(w, "graphs"):
         launches = w.graph_kernels * args.steps
         res = w.graphs[0].result()
@@ -750,8 +825,40 @@ def run_marrow(args, dist, wl_name):
         del futs
     kstats = {cls: M.mw_kernel_stats(ctx, cls) for cls in range(M.MW_KC_COUNT)}
     M.mw_stats_enable(ctx, False)
-    ms = dist.max(ms_local)
+    ms = ms_local   # already the max over ranks, per trial
     value = w.units * args.steps / (ms / 1e3)
+    # auxiliaries: warm L2 (one buffer set, B = 1) and per-launch latency (one
+    # step, R = 1, then a synchronize; device events and host wall clock)
+    aux = {"trials_ms_per_step": [round(t / args.steps, 6) for t in trials],
+           "min_ms_per_step": min(trials) / args.steps, "max_ms_per_step": max(trials) / args.steps}
+    M.mw_ctx_set_monitoring(ctx, False)
+    if w.B > 1 and not hasattr(w, "graphs"):
+        b0, w.B = w.B, 1
+        kw = max(3, min(args.steps, 500))
+        timed(3)
+        aux["warm_l2_ms_per_step"] = timed(kw)[0] / kw
+        w.B = b0
+    elif w.B > 1 and hasattr(w, "warm_capture"):
+        w.warm_capture(stream)
+        aux["warm_l2_ms_per_step"] = w.warm_timed(timed, args.steps)
+    else:
+        aux["warm_l2_ms_per_step"] = None   # one set already exceeds L2: cold == warm
+    lat_dev, lat_wall = [], []
+    a0 = w.arglist(0)
+    for _ in range(3 if wl_name == "nbody" else 10):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        start.record(stream)
+        f1 = M.mw_run(ctx, w.tree, a0, stream=stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+        lat_wall.append(1e3 * (time.perf_counter() - t0))
+        lat_dev.append(start.elapsed_time(stop))
+        del f1
+    aux["single_step_ms"] = statistics.median(lat_dev)
+    aux["single_step_wall_ms"] = statistics.median(lat_wall)
+    if hasattr(w, "extra_aux"):
+        aux.update(w.extra_aux(timed, start, stop, stream))
     pk = peaks()
     # roofline of the dominant kernel class: algorithmic bytes (flops) of its
     # launches in the timed region / their CUDA-event-measured duration
@@ -810,7 +917,7 @@ def run_marrow(args, dist, wl_name):
             "config": dict(w.config(), parallelism=f"rows/slabs/bodies over {dist.world} GPU(s)",
                            partitions=dist.world * args.parts),
             "roofline": roof, "kernels": breakdown, "gpu_launches": launches,
-            "clocks": clocks.summary()}
+            "clocks": clocks.summary(), "trials": args.trials, "aux": aux}
     if comm is not None:
         line["comm"] = comm
     if wl_name == "hysteresis":
@@ -852,7 +959,7 @@ def run_marrow(args, dist, wl_name):
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
         rate, sample, spent = cpu_rate(w.name, args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": w.unit, "cores": 1, "kind": "oracle",
-                                "sample": sample, "seconds": round(spent, 2)}
+                                "sample": sample, "seconds": round(spent, 2), **host_info()}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
     ctx.destroy()
@@ -963,6 +1070,8 @@ def main():
     ap.add_argument("--workload", default="filter", choices=list(WORKLOADS) + ["all", "rebalance"])
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--trials", type=int, default=5,
+                    help="timed trials of K steps; the line reports the median (min/max in aux)")
     ap.add_argument("--parts", type=int, default=1,
                     help="virtual partitions per GPU (uniform distribution vector)")
     args = ap.parse_args()
@@ -984,8 +1093,11 @@ def main():
         run_rebalance_scenario(args, dist)
         return
     names = list(WORKLOADS) if args.workload == "all" else [args.workload]
-    default_steps = {"filter": 2000, "saxpy": 5000, "segmentation": 1000, "mapreduce_sum": 300,
-                     "mapreduce_dot": 200, "mapreduce_max": 200, "hysteresis": 20, "nbody": 3, "fft": 200}
+    # K per trial (x `--trials`): short enough that the default run stays
+    # below the ~0.2 s of continuous load after which the power cap lowers
+    # the SM clock (scripts/probe_power.py)
+    default_steps = {"filter": 200, "saxpy": 4992, "segmentation": 200, "mapreduce_sum": 60,
+                     "mapreduce_dot": 40, "mapreduce_max": 40, "hysteresis": 20, "nbody": 3, "fft": 100}
     user_steps = args.steps
     for n in names:
         args.steps = user_steps or default_steps[n]

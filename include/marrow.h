@@ -419,7 +419,11 @@ enum {
     MW_TUNE_HYST_FUSED = 7,   /* 1: several partitions of one rank run the whole plane loop in
                                  ONE cooperative kernel (in-kernel halo exchange, device loop
                                  condition); 0: one launch per partition and pass            */
-    MW_TUNE_COUNT = 8
+    MW_TUNE_GRAPH_LANES = 8,  /* mw_graph_capture_many: runs of a scratch-free fused chain whose
+                                 argument sets are pairwise independent (no write overlaps
+                                 another set's buffers) are captured on up to this many
+                                 parallel lanes (1, 2, 4); 1 = strictly serialized replays   */
+    MW_TUNE_COUNT = 9
 };
 mw_status mw_ctx_set_tuning(mw_ctx* ctx, int32_t knob, int32_t value);
 mw_status mw_ctx_get_tuning(const mw_ctx* ctx, int32_t knob, int32_t* value);

@@ -85,6 +85,8 @@ struct mw_ctx {
     cudaEvent_t last_run = nullptr;
     bool have_last_run = false;
     bool staging_overlap = false;   // mw_ctx_set_staging_overlap
+    cudaStream_t lane_s[3]{};       // extra capture lanes of mw_graph_capture_many
+    cudaEvent_t lane_ev[4]{};
     // pinned host memory
     int32_t* h_flag = nullptr;   // 16 ints: [0] byte-stencil flag, [4..7] plane-pass ring
     cudaEvent_t lag_ev[4]{};
@@ -1547,6 +1549,10 @@ static void ctx_teardown(mw_ctx* c) {
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);
     if (c->aux) cudaStreamDestroy(c->aux);
+    for (cudaStream_t q : c->lane_s)
+        if (q) cudaStreamDestroy(q);
+    for (cudaEvent_t e : c->lane_ev)
+        if (e) cudaEventDestroy(e);
     if (c->h_flag) cudaFreeHost(c->h_flag);
     for (cudaEvent_t e : c->lag_ev)
         if (e) cudaEventDestroy(e);
@@ -1922,7 +1928,47 @@ struct mw_graph {
     mw_future f;          // result slot of the captured run
     int64_t kernels = 0;  // library kernels per replay
     std::vector<void*> bufs;   // ctx scratch the graph writes (kept alive while it lives)
+    int lanes = 1;             // parallel capture lanes (independent runs)
 };
+
+// Runs of `root` on the nsets argument sets may execute concurrently when the
+// tree is one fused Map/Pipeline chain that touches no ctx scratch and no set
+// writes a byte another set reads or writes (data dependencies are the only
+// order a replay must keep).
+static bool sets_independent(const Node* root, const mw_arg* args, int nargs, int nsets) {
+    mw_status st;
+    const mw::NodeCache* nc = mw::plan_cached(root, &st);
+    if (!nc || nc->prog.size() != 1) return false;
+    const Step& s0 = nc->prog[0];
+    if (s0.kind == StepKind::Saxpy) {
+        if (saxpy_groups(s0.ops).size() != 1) return false;
+    } else if (s0.kind == StepKind::Rgba) {
+        if (rgba_groups(s0.ops).size() != 1) return false;
+    } else if (s0.kind == StepKind::U8) {
+        if (u8_groups(s0.ops).size() != 1) return false;
+    } else {
+        return false;
+    }
+    if (nargs != 2) return false;
+    struct Range {
+        uintptr_t a, b;
+        bool w;
+    };
+    std::vector<std::vector<Range>> rs(nsets);
+    for (int k = 0; k < nsets; ++k)
+        for (int i = 0; i < nargs; ++i) {
+            const mw_arg& x = args[(size_t)k * nargs + i];
+            if (x.location != MW_LOC_DEVICE) return false;
+            const uintptr_t a = reinterpret_cast<uintptr_t>(x.ptr);
+            rs[k].push_back({a, a + (uintptr_t)(x.local_rows * row_bytes(x)), i == 1});
+        }
+    for (int j = 0; j < nsets; ++j)
+        for (int k = j + 1; k < nsets; ++k)
+            for (const Range& u : rs[j])
+                for (const Range& v : rs[k])
+                    if ((u.w || v.w) && u.a < v.b && v.a < u.b) return false;
+    return true;
+}
 
 mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* args,
                                 int32_t nargs, int32_t nsets, void* stream, mw_graph** out) {
@@ -1946,11 +1992,36 @@ mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* ar
     c->capture_bufs = &used;
     mw_status st = MW_OK;
     try {
+        // independent runs: round-robin over `lanes` streams forked from and
+        // joined back into the capture stream
+        int lanes = std::min<int>(c->tune[mwk::TUNE_GRAPH_LANES], nsets);
+        if (lanes > 1 && !sets_independent(reinterpret_cast<const Node*>(root), args, nargs, nsets)) lanes = 1;
+        cudaStream_t ls[4] = {s, nullptr, nullptr, nullptr};
+        for (int l = 1; l < lanes && st == MW_OK; ++l) {
+            if (!c->lane_s[l - 1] &&
+                cudaStreamCreateWithFlags(&c->lane_s[l - 1], cudaStreamNonBlocking) != cudaSuccess)
+                st = fail(MW_E_CUDA, "lane stream");
+            ls[l] = c->lane_s[l - 1];
+        }
+        for (int l = 0; l < lanes && st == MW_OK; ++l)
+            if (!c->lane_ev[l] && cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming) != cudaSuccess)
+                st = fail(MW_E_CUDA, "lane event");
+        if (lanes > 1 && st == MW_OK) {
+            cudaEventRecord(c->lane_ev[0], s);
+            for (int l = 1; l < lanes; ++l) cudaStreamWaitEvent(ls[l], c->lane_ev[0], 0);
+        }
         for (int32_t k = 0; k < nsets && st == MW_OK; ++k) {
             g->f.has_reduce = false;
             g->f.plane_loop = false;
-            st = run(c, reinterpret_cast<const Node*>(root), args + (size_t)k * nargs, nargs, s, &g->f);
+            st = run(c, reinterpret_cast<const Node*>(root), args + (size_t)k * nargs, nargs, ls[k % lanes],
+                     &g->f);
         }
+        if (lanes > 1)
+            for (int l = 1; l < lanes; ++l) {
+                cudaEventRecord(c->lane_ev[l], ls[l]);
+                cudaStreamWaitEvent(s, c->lane_ev[l], 0);
+            }
+        g->lanes = lanes;
     } catch (...) {
         st = fail(MW_E_INVALID_SPEC, "internal error");
     }

@@ -90,3 +90,43 @@ def test_graph_scratch_survives_growth():
     assert np.array_equal(dst.cpu().numpy(), want)
     assert all(bool((p == 7).all()) for p in probes)
     del g
+
+
+@pytest.mark.parametrize("lanes", [1, 2, 4])
+def test_graph_lanes_keep_data_dependencies(lanes):
+    """mw_graph_capture_many puts runs on parallel lanes only when no set
+    writes what another set touches: disjoint sets give each set's own result;
+    sets sharing y (a chain of dependent runs) still replay in order."""
+    n = (1 << 16) + 3
+    c = M.mw_ctx_create(0, 0, 1, 2)
+    M.mw_ctx_set_tuning(c, M.MW_TUNE_GRAPH_LANES, lanes)
+    s = torch.cuda.Stream()
+    x = [torch.from_numpy(synth.np_f32_um11(1, k * n, n)).to(DEV) for k in range(6)]
+    y0 = [synth.np_f32_um11(2, k * n, n) for k in range(6)]
+    y = [torch.from_numpy(v).to(DEV) for v in y0]
+    torch.cuda.synchronize()
+    g = M.mw_graph_capture_many(c, trees.saxpy(0.75), [[M.arg(x[k]), M.arg(y[k])] for k in range(6)], stream=s)
+    g.launch(s)
+    s.synchronize()
+    for k in range(6):
+        assert np.array_equal(y[k].cpu().numpy(), K.saxpy(0.75, x[k].cpu().numpy(), y0[k]))
+    # dependent: every set updates the same y
+    yd = torch.from_numpy(y0[0]).to(DEV)
+    torch.cuda.synchronize()
+    g2 = M.mw_graph_capture_many(c, trees.saxpy(0.75), [[M.arg(x[k]), M.arg(yd)] for k in range(6)], stream=s)
+    g2.launch(s)
+    s.synchronize()
+    want = y0[0]
+    for k in range(6):
+        want = K.saxpy(0.75, x[k].cpu().numpy(), want)
+    assert np.array_equal(yd.cpu().numpy(), want)
+    # filter sets reading one source into distinct outputs are independent
+    img = synth.np_rgba(3, 0, 64 * 128).reshape(64, 128, 4)
+    src = torch.from_numpy(img).to(DEV)
+    outs = [torch.empty_like(src) for _ in range(4)]
+    torch.cuda.synchronize()
+    g3 = M.mw_graph_capture_many(c, trees.filter_pipeline(), [[M.arg(src), M.arg(o)] for o in outs], stream=s)
+    g3.launch(s)
+    s.synchronize()
+    want = K.mirror(K.solarize(K.gauss_noise(img, 4, 8), 128))
+    assert all(np.array_equal(o.cpu().numpy(), want) for o in outs)

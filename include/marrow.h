@@ -463,6 +463,74 @@ mw_status mw_kb_lookup(const mw_kb* kb, const mw_node* root, const int64_t* dims
 mw_status mw_autotune(mw_ctx* ctx, const mw_node* root, const mw_arg* args, int32_t nargs,
                       void* stream, int32_t reps, mw_kb* kb, int32_t* tune_out, double* best_ms);
 
+/* The exact (SCT, workload) record: *found = 0/1, its provenance and time.  */
+mw_status mw_kb_find(const mw_kb* kb, const mw_node* root, const int64_t* dims, int32_t ndims,
+                     int32_t* found, int32_t* provenance, double* best_ms);
+
+/* Heterogeneous devices (NEXT-4): partition `part` runs on a
+ * device of class `cls` (>= 0) whose relative performance is rel_perf (> 0).
+ * The distribution becomes proportional to the partitions' relative
+ * performances (P:388's static rule).  Classes are the device types of the
+ * profile builder's workload-distribution generator (Alg. 1).
+ * On one B200 a class is realised with the slowdown injector (or MIG).     */
+mw_status mw_ctx_set_device_class(mw_ctx* ctx, int32_t part, int32_t cls, double rel_perf);
+
+/* Profile building, Alg. 1 over the B200 configuration space:
+ * the knob dimensions that apply to the plan are iterated in nested loops,
+ * most likely values first, and a value that does not improve on the
+ * previous one discards the rest of its dimension; innermost, the
+ * workload-distribution generator binary-searches the share of
+ * device class A (partition 0's class) against the other classes, binding
+ * half of the transferable share to the faster type per iteration
+ * (transferableSize(n) = 1/2^n); every proposal runs warm-up + `executions`
+ * times (mean, step 13); a result better than the stored best is stored, and
+ * an improvement below precision_ms ends the search direction (steps 14-17).
+ * The best configuration is left in the ctx (tuning + distribution), stored
+ * in kb (provenance BUILT) when kb != NULL and returned.  Collective like
+ * mw_run; in-place arguments are restored afterwards.                      */
+typedef struct mw_profile_params {
+    int32_t executions;      /* runs per proposal (quality factor), default 3 */
+    double precision_ms;     /* step 17 stop, default 0                        */
+    int32_t max_dist_iters;  /* generator iterations (two device types), 10    */
+} mw_profile_params;
+void mw_profile_defaults(mw_profile_params* p);
+mw_status mw_profile_build(mw_ctx* ctx, const mw_node* root, const mw_arg* args, int32_t nargs,
+                           void* stream, const mw_profile_params* params, mw_kb* kb,
+                           int32_t* tune_out /* MW_TUNE_COUNT or NULL */,
+                           double* fractions_out /* n_parts or NULL */, int32_t nfrac,
+                           double* best_ms, int32_t* runs);
+
+/* Managed execution, the Fig. 5 decision process around mw_run:
+ * a new (SCT, workload) — different from the previous managed run's — gets
+ * its configuration (tuning + distribution) from the KB: the exact record or
+ * one derived by scope narrowing; a recurrent one first persists
+ * the previous run's attained time with the process that produced it
+ * (provenance DERIVED / BALANCED / BUILT), then runs the monitor
+ * (mw_rebalance with params->balance): when it triggers, the distribution is
+ * adjusted, or — with build_profiles set and no BUILT record yet — the
+ * profile is built from scratch (mw_profile_build, once per pair).
+ * *action says which branch ran.  Needs monitoring on; collective.          */
+enum {
+    MW_MANAGED_NO_KNOWLEDGE = 0, /* new pair, KB empty for it: current configuration */
+    MW_MANAGED_FROM_KB = 1,      /* new pair, exact KB record                         */
+    MW_MANAGED_DERIVED = 2,      /* new pair, configuration derived by scope narrowing */
+    MW_MANAGED_RECURRENT = 3,    /* recurrent pair, balanced: nothing changed          */
+    MW_MANAGED_ADJUSTED = 4,     /* recurrent, unbalanced: distribution adjusted        */
+    MW_MANAGED_BUILT = 5         /* recurrent, unbalanced: profile built from scratch   */
+};
+typedef struct mw_managed_params {
+    mw_balance_params balance;
+    int32_t build_profiles;      /* 0 (default): never build, only adjust */
+    mw_profile_params profile;
+} mw_managed_params;
+void mw_managed_defaults(mw_managed_params* p);
+mw_status mw_run_managed(mw_ctx* ctx, mw_kb* kb, const mw_managed_params* params,
+                         const mw_node* root, const mw_arg* args, int32_t nargs, void* stream,
+                         mw_future** out, int32_t* action);
+/* Persist the last managed run's result now (otherwise done by the next
+ * managed run).  Call after its future completed.                          */
+mw_status mw_managed_flush(mw_ctx* ctx);
+
 /* Number of kernels this library launched on the ctx since creation.        */
 mw_status mw_ctx_launch_count(const mw_ctx* ctx, int64_t* out);
 

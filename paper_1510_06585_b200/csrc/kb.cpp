@@ -168,6 +168,22 @@ mw_status mw_kb_store(mw_kb* kb, const mw_node* root, const int64_t* dims, int32
     return MW_OK;
 }
 
+mw_status mw_kb_find(const mw_kb* kb, const mw_node* root, const int64_t* dims, int32_t ndims,
+                     int32_t* found, int32_t* provenance, double* best_ms) {
+    if (!kb || !root || (ndims > 0 && !dims) || !found) return fail(MW_E_INVALID_SPEC, "NULL argument");
+    const std::string id = hex_id(root);
+    const std::vector<int64_t> w(dims, dims + ndims);
+    *found = 0;
+    for (const Record& r : kb->recs)
+        if (r.sct == id && r.dims == w) {
+            *found = 1;
+            if (provenance) *provenance = r.prov;
+            if (best_ms) *best_ms = r.ms;
+            break;
+        }
+    return MW_OK;
+}
+
 mw_status mw_kb_lookup(const mw_kb* kb, const mw_node* root, const int64_t* dims, int32_t ndims,
                        int32_t* tune_out, double* fractions_out, int32_t nparts, int32_t* scope) {
     if (!kb || !root || (ndims > 0 && !dims) || !tune_out || !scope)

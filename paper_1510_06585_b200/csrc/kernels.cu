@@ -1398,6 +1398,70 @@ __device__ __forceinline__ void plane_store_fwd(const uint32_t (&sv)[ROWS], cons
     }
 }
 
+// Tile activity across partition boundaries: the 3x3 rule of
+// plane_tile_active, where the strip above a partition's first strip is the
+// previous partition's last strip (and the one before it when that last strip
+// has fewer than T rows: a front crosses it within one pass), and the strip
+// below the last strip (or below the second-to-last one when the last is
+// short) is the next partition's first strip.  Neighbours' flags count with
+// bit 0 (changed in the last execution of the previous pass), as inside a
+// partition; no boundary strip is forced active.
+// PView caches what the check needs about the scan cursor's partition (it
+// changes a few times per warp and pass; the check runs for every candidate).
+struct PView {
+    const uint8_t* fp;        // previous-pass flags of the partition
+    uint8_t* fc;              // this pass's flags
+    int64_t n_strips, nt, t0, t1;
+    const uint8_t* fp_prev;   // previous partition: flags of its last strip (nullptr: none)
+    const uint8_t* fp_prev2;  // ... and of its second-to-last strip when the last is short
+    const uint8_t* fp_next;   // next partition: flags of its first strip
+    bool short_last;          // this partition's last strip has fewer than T rows
+};
+template <int T, int ROWS>
+__device__ __forceinline__ PView plane_view(const PlaneMultiArgs& a, int q, int cur, int64_t t0) {
+    constexpr int R = ROWS - 2 * T;
+    const PlanePartDesc& d = a.p[q];
+    PView v;
+    v.fp = d.fl + (cur ^ 1) * d.nt;
+    v.fc = d.fl + cur * d.nt;
+    v.n_strips = d.n_strips;
+    v.nt = d.nt;
+    v.t0 = t0;
+    v.t1 = t0 + d.nt;
+    v.short_last = d.rows - (d.n_strips - 1) * R < T;
+    v.fp_prev = v.fp_prev2 = v.fp_next = nullptr;
+    if (d.prev >= 0) {
+        const PlanePartDesc& pd = a.p[d.prev];
+        const uint8_t* f = pd.fl + (cur ^ 1) * pd.nt;
+        v.fp_prev = f + (pd.n_strips - 1) * a.n_cb;
+        if (pd.rows - (pd.n_strips - 1) * R < T && pd.n_strips >= 2) v.fp_prev2 = f + (pd.n_strips - 2) * a.n_cb;
+    }
+    if (d.next >= 0) {
+        const PlanePartDesc& nd = a.p[d.next];
+        v.fp_next = nd.fl + (cur ^ 1) * nd.nt;
+    }
+    return v;
+}
+__device__ __forceinline__ bool plane_tile_active_multi(const PView& v, int64_t n_cb, int64_t strip,
+                                                        int64_t cb, bool first, int lane) {
+    if (first) return true;
+    const int64_t c2 = cb + lane % 3 - 1;
+    bool x = false;
+    if (lane < 18 && c2 >= 0 && c2 < n_cb) {
+        if (lane < 9) {
+            const int64_t s2 = strip + lane / 3 - 1;
+            if (s2 >= 0 && s2 < v.n_strips) x = v.fp[s2 * n_cb + c2] & (lane == 4 ? 3 : 1);
+        } else if (lane < 12) {
+            if (strip == 0 && v.fp_prev) x = v.fp_prev[c2] & 1;
+        } else if (lane < 15) {
+            if (strip == 0 && v.fp_prev2) x = v.fp_prev2[c2] & 1;
+        } else if (v.fp_next && (strip == v.n_strips - 1 || (v.short_last && strip == v.n_strips - 2))) {
+            x = v.fp_next[c2] & 1;
+        }
+    }
+    return __any_sync(0xffffffffu, x);
+}
+
 template <int T, int ROWS>
 __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, int cur, int steps,
                                                      bool first, int64_t gw, int64_t nwarps, int lane,
@@ -1409,43 +1473,42 @@ __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, in
     constexpr uint32_t kBox = ROWS * BW * 4;
     const int64_t n_cb = a.n_cb;
     const bool own_lane = lane >= 1 && lane <= OW;
-    auto locate = [&](int64_t t, int& q) {
-        q = 0;
-        while (q + 1 < a.np && t >= a.p[q + 1].tile0) ++q;
-        return t - a.p[q].tile0;
-    };
+    // scan cursor over the concatenated tile list: a warp's tiles increase, so
+    // the partition of the next candidate is found by moving forward only
+    int sq = 0;
+    PView v = plane_view<T, ROWS>(a, 0, cur, 0);
     auto next_active = [&](int64_t t) {
         for (; t < a.total; t += nwarps) {
-            int q;
-            const int64_t lt = locate(t, q);
-            const PlanePartDesc& d = a.p[q];
+            while (t >= v.t1 && sq + 1 < a.np) {
+                ++sq;
+                v = plane_view<T, ROWS>(a, sq, cur, v.t1);
+            }
+            const int64_t lt = t - v.t0;
             const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
-            if (plane_tile_active(d.fl + (cur ^ 1) * d.nt, strip, cb, d.n_strips, n_cb, first,
-                                  d.prev >= 0, d.next >= 0, lane))
-                break;
-            if (lane == 0) d.fl[cur * d.nt + lt] = 0;
+            if (plane_tile_active_multi(v, n_cb, strip, cb, first, lane)) break;
+            if (lane == 0) v.fc[lt] = 0;
         }
         return t;
     };
-    auto issue = [&](int64_t t) {
+    auto issue = [&](int64_t t) {   // t was located by the scan cursor
         if (lane == 0) {
-            int q;
-            const int64_t lt = locate(t, q);
+            const int64_t lt = t - v.t0;
             const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
             const int x = (int)(cb * OW - 1) & ~3, y = (int)(strip * R);   // buffer row (hd = T)
             mbar_expect_tx(bar, 2 * kBox);
-            tma_load_2d(sb, &a.ts[q][cur], x, y, bar);
-            tma_load_2d(kb, &a.tk[q], x, y, bar);
+            tma_load_2d(sb, &a.ts[sq][cur], x, y, bar);
+            tma_load_2d(kb, &a.tk[sq], x, y, bar);
         }
     };
     int my_last = -1;
     int64_t t = next_active(gw);
+    int q = sq;
+    int64_t lt = t - v.t0;
+    uint8_t* fc = v.fc;
     if (t < a.total) issue(t);
     while (t < a.total) {
         mbar_wait(bar, phase);
         phase ^= 1u;
-        int q;
-        const int64_t lt = locate(t, q);
         const int o = (int)((lt % n_cb) * OW - 1) & 3;
         uint32_t sv[ROWS], kv[ROWS];
 #pragma unroll
@@ -1456,17 +1519,19 @@ __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, in
         __syncwarp();
         const int64_t tn = next_active(t + nwarps);
         if (tn < a.total) issue(tn);
-        const PlanePartDesc& d = a.p[q];
         const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
         const int64_t w = cb * OW - 1 + lane;
         const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
         const uint8_t fl = tl < 0 ? 0 : (tl == steps - 1 ? 3 : 2);
         my_last = max(my_last, tl);
         const bool wv = w >= 0 && w < a.wp;
-        plane_store<T, ROWS>(sv, d.S[cur ^ 1], d.rows, a.wp, T, strip * R - T, w, own_lane, wv);
+        plane_store<T, ROWS>(sv, a.p[q].S[cur ^ 1], a.p[q].rows, a.wp, T, strip * R - T, w, own_lane, wv);
         plane_store_fwd<T, ROWS>(sv, a, q, cur, strip, w, own_lane, wv);
-        if (lane == 0) d.fl[cur * d.nt + lt] = fl;
+        if (lane == 0) fc[lt] = fl;
         t = tn;
+        q = sq;
+        lt = t - v.t0;
+        fc = v.fc;
     }
     return my_last;
 }

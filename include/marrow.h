@@ -483,7 +483,10 @@ mw_status mw_ctx_set_device_class(mw_ctx* ctx, int32_t part, int32_t cls, double
  * device class A (partition 0's class) against the other classes, binding
  * half of the transferable share to the faster type per iteration
  * (transferableSize(n) = 1/2^n); every proposal runs warm-up + `executions`
- * times (mean, step 13); a result better than the stored best is stored, and
+ * times (mean, step 13; with several partitions per rank — virtual devices —
+ * the time is the makespan, the longest partition's compute time of the last
+ * execution, i.e. what concurrent devices would take); a result better than
+ * the stored best is stored, and
  * an improvement below precision_ms ends the search direction (steps 14-17).
  * The best configuration is left in the ctx (tuning + distribution), stored
  * in kb (provenance BUILT) when kb != NULL and returned.  Collective like

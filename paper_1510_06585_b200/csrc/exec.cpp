@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -2430,7 +2431,14 @@ mw_status mw_profile_build(mw_ctx* c, const mw_node* root, const mw_arg* args, i
         float ms = 0.f;
         CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
         *ms_out = (double)ms / prm.executions;
-        return part_times(c, parts);
+        MW_OK_OR_RETURN(part_times(c, parts));
+        // Partitions sharing a device (ppr > 1) stand in for devices of their
+        // own, which would run concurrently: the execution time of a
+        // configuration is then the makespan, the longest partition's compute
+        // time (the sum the shared stream takes is not what a multi-device
+        // run would see).
+        if (c->ppr > 1) *ms_out = (double)*std::max_element(parts.begin(), parts.end());
+        return MW_OK;
     };
     // steps 9-20 for the current platform configuration: returns the best
     // time this configuration reached
@@ -2446,6 +2454,15 @@ mw_status mw_profile_build(mw_ctx* c, const mw_node* root, const mw_arg* args, i
             st = exec(&t, parts);
             if (st != MW_OK) break;
             here = std::min(here, t);
+            if (getenv("MW_PROFILE_TRACE")) {
+                fprintf(stderr, "profile: tune");
+                for (int k = 0; k < mwk::TUNE_COUNT; ++k) fprintf(stderr, " %d", c->tune[k]);
+                fprintf(stderr, " dist");
+                for (double x : d) fprintf(stderr, " %.4f", x);
+                fprintf(stderr, " ms %.4f parts", t);
+                for (float x : parts) fprintf(stderr, " %.4f", x);
+                fprintf(stderr, "\n");
+            }
             gen.feed(parts);
             const double stored = best;
             if (t < stored) {   // store_profile (step 16)

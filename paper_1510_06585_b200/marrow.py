@@ -71,6 +71,20 @@ class mw_balance_state(ctypes.Structure):
                 ("abs_count", ctypes.c_int32), ("pad", ctypes.c_int32), ("runs", ctypes.c_int64)]
 
 
+class mw_profile_params(ctypes.Structure):
+    _fields_ = [("executions", ctypes.c_int32), ("precision_ms", ctypes.c_double),
+                ("max_dist_iters", ctypes.c_int32)]
+
+
+class mw_managed_params(ctypes.Structure):
+    _fields_ = [("balance", mw_balance_params), ("build_profiles", ctypes.c_int32),
+                ("profile", mw_profile_params)]
+
+
+(MW_MANAGED_NO_KNOWLEDGE, MW_MANAGED_FROM_KB, MW_MANAGED_DERIVED, MW_MANAGED_RECURRENT,
+ MW_MANAGED_ADJUSTED, MW_MANAGED_BUILT) = range(6)
+MANAGED_ACTIONS = ("no_knowledge", "from_kb", "derived", "recurrent", "adjusted", "built")
+
 _lib = None
 _P = ctypes.POINTER
 _vp, _i32, _i64, _f32, _f64, _u32 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
@@ -151,10 +165,19 @@ _SIG = {
     "mw_kb_lookup": [_vp, _vp, _P(_i64), _i32, _P(_i32), _P(_f64), _i32, _P(_i32)],
     "mw_autotune": [_vp, _vp, _P(mw_arg), _i32, _vp, _i32, _vp, _P(_i32), _P(_f64)],
     "mw_ctx_get_tuning": [_vp, _i32, _P(_i32)],
+    "mw_kb_find": [_vp, _vp, _P(_i64), _i32, _P(_i32), _P(_i32), _P(_f64)],
+    "mw_ctx_set_device_class": [_vp, _i32, _i32, _f64],
+    "mw_profile_defaults": [_P(mw_profile_params)],
+    "mw_profile_build": [_vp, _vp, _P(mw_arg), _i32, _vp, _P(mw_profile_params), _vp, _P(_i32), _P(_f64),
+                         _i32, _P(_f64), _P(_i32)],
+    "mw_managed_defaults": [_P(mw_managed_params)],
+    "mw_run_managed": [_vp, _vp, _P(mw_managed_params), _vp, _P(mw_arg), _i32, _vp, _P(_vp), _P(_i32)],
+    "mw_managed_flush": [_vp],
 }
 _RES = {"mw_status_string": ctypes.c_char_p, "mw_last_error": ctypes.c_char_p,
         "mw_abi_version": _i32, "mw_node_retain": None, "mw_node_release": None,
-        "mw_future_release": None, "mw_balance_defaults": None}
+        "mw_future_release": None, "mw_balance_defaults": None, "mw_profile_defaults": None,
+        "mw_managed_defaults": None}
 EXPORTS = tuple(_SIG)
 
 
@@ -843,3 +866,56 @@ def mw_autotune(ctx, node, args, stream=None, reps=3, kb=None):
     _call("mw_autotune", ctx.ptr, node.ptr, arr, len(args), _stream_arg(stream), reps,
           kb.ptr if kb is not None else None, tn, ctypes.byref(ms))
     return list(tn), ms.value
+
+
+# ---------------------------------------------------------------- NEXT-2 / NEXT-4
+def mw_kb_find(kb, node, dims):
+    """-> (found, provenance, best_ms) of the exact (SCT, workload) record."""
+    d = (_i64 * max(1, len(dims)))(*dims)
+    f, p, ms = _i32(), _i32(), _f64()
+    _call("mw_kb_find", kb.ptr, node.ptr, d, len(dims), ctypes.byref(f), ctypes.byref(p), ctypes.byref(ms))
+    return bool(f.value), p.value, ms.value
+
+
+def mw_ctx_set_device_class(ctx, part, cls, rel_perf=1.0):
+    """Partition `part` runs on device class `cls` with relative performance
+    rel_perf; the distribution becomes proportional to it."""
+    _call("mw_ctx_set_device_class", ctx.ptr, part, cls, _f64(rel_perf))
+
+
+def mw_profile_defaults():
+    p = mw_profile_params()
+    lib().mw_profile_defaults(ctypes.byref(p))
+    return p
+
+
+def mw_profile_build(ctx, node, args, params=None, kb=None, stream=None):
+    """Alg. 1 profile building; -> dict(tune, fractions, best_ms, runs)."""
+    arr = (mw_arg * len(args))(*args)
+    n = mw_ctx_info(ctx)["n_parts"]
+    tn, fr = (_i32 * MW_TUNE_COUNT)(), (_f64 * n)()
+    ms, runs = _f64(), _i32()
+    p = params or mw_profile_defaults()
+    _call("mw_profile_build", ctx.ptr, node.ptr, arr, len(args), _stream_arg(stream), ctypes.byref(p),
+          kb.ptr if kb is not None else None, tn, fr, n, ctypes.byref(ms), ctypes.byref(runs))
+    return {"tune": list(tn), "fractions": list(fr), "best_ms": ms.value, "runs": runs.value}
+
+
+def mw_managed_defaults():
+    p = mw_managed_params()
+    lib().mw_managed_defaults(ctypes.byref(p))
+    return p
+
+
+def mw_run_managed(ctx, kb, node, args, params=None, stream=None):
+    """Fig. 5 decision process around a run; -> (Future, action name)."""
+    al = args if isinstance(args, ArgList) else ArgList(args)
+    out, act = _vp(), _i32()
+    p = params or mw_managed_defaults()
+    _call("mw_run_managed", ctx.ptr, kb.ptr, ctypes.byref(p), node.ptr, al.arr, al.n, _stream_arg(stream),
+          ctypes.byref(out), ctypes.byref(act))
+    return Future(out, (al, node, ctx)), MANAGED_ACTIONS[act.value]
+
+
+def mw_managed_flush(ctx):
+    _call("mw_managed_flush", ctx.ptr)

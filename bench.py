@@ -1021,6 +1021,68 @@ def run_rebalance_scenario(args, dist):
     c1.destroy()
 
 
+def run_rebalance_nbody(args, dist):
+    """SURVEY §8(d) C5b rebalance scenario (the analogue of P:1101-1119): the
+    2^20-body N-body loop on P = 8 partitions (virtual devices on one GPU),
+    40 steps; partition 3 computes 2x slower (slowdown injector: its step is
+    repeated) during steps 10-29; after every step the monitor / rebalancer
+    runs (mw_rebalance: lbt trigger after three unbalanced runs, proportional
+    re-derivation).  A second context without rebalancing runs the same
+    trajectory in lockstep: positions and velocities must be bitwise equal at
+    every step (COPY state: the distribution never changes the result)."""
+    import torch
+
+    import synth
+    from paper_1510_06585_b200 import marrow as M
+    from paper_1510_06585_b200 import trees
+    if dist.world != 1:
+        if dist.rank == 0:
+            print(json.dumps({"workload": "rebalance_nbody", "skipped": "runs on one GPU (virtual partitions)"}))
+        return
+    N, P, steps = 1 << 20, 8, 40
+    ctx = M.mw_ctx_create(0, 0, 1, P)
+    ref = M.mw_ctx_create(0, 0, 1, 1)
+    M.mw_ctx_set_monitoring(ref, False)
+    pos = torch.empty((N, 4), dtype=torch.float32, device="cuda")
+    vel = torch.empty((N, 4), dtype=torch.float32, device="cuda")
+    synth.dev_fill_nbody(pos, vel, synth.SEED_NBODY, 0, 2.0 ** -20)
+    pr, vr = pos.clone(), vel.clone()
+    node = trees.nbody(1)
+    a = M.ArgList([M.arg(pos, M.MW_COPY), M.arg(vel, M.MW_COPY)])
+    ar = M.ArgList([M.arg(pr, M.MW_COPY), M.arg(vr, M.MW_COPY)])
+    trace, identical = [], True
+    for k in range(steps):
+        M.mw_ctx_set_slowdown(ctx, 3, 2.0 if 10 <= k < 30 else 1.0)
+        M.mw_run(ctx, node, a).wait()
+        M.mw_run(ref, node, ar).wait()
+        same = bool(torch.equal(pos, pr)) and bool(torch.equal(vel, vr))
+        identical &= same
+        ms, wall = M.mw_last_timings(ctx)
+        lens = M.mw_last_lengths(ctx)
+        act = [x for x, n in zip(ms, lens) if n > 0]
+        dev = min(act) / max(act)
+        trig = M.mw_rebalance(ctx)
+        st = M.mw_get_balance_state(ctx)
+        trace.append({"step": k, "slowed": 10 <= k < 30, "wall_ms": round(wall, 3),
+                      "part_ms": [round(x, 3) for x in ms], "bodies": lens, "dev": round(dev, 4),
+                      "lbt": round(st.lbt, 4), "triggered": trig, "bitwise_equal": same,
+                      "next_dist": [round(x, 5) for x in M.mw_get_distribution(ctx)]})
+    trig_steps = [t["step"] for t in trace if t["triggered"]]
+    line = {"workload": "nbody_rebalance_2^20_8parts",
+            "metric": "online rebalancing (lbt trigger, proportional re-derivation) under a 2x "
+                      "slowdown of partition 3 during steps 10-29 (SURVEY 8(d) C5b)",
+            "trigger_steps": trig_steps,
+            "positions_bitwise_identical_every_step": identical,
+            "dev_after_first_trigger_min": min((t["dev"] for t in trace
+                                                if trig_steps and trig_steps[0] < t["step"] < 30), default=None),
+            "share_of_partition_3_while_slowed": trace[25]["next_dist"][3],
+            "share_of_others_while_slowed": trace[25]["next_dist"][0],
+            "wall_ms": {"balanced": trace[9]["wall_ms"], "slowed_before_rebalance": trace[11]["wall_ms"],
+                        "slowed_after_rebalance": trace[25]["wall_ms"], "recovered": trace[39]["wall_ms"]},
+            "trace": trace}
+    print(json.dumps(line), flush=True)
+
+
 def traffic_from_profile(wl_name):
     """dram bytes (read + write) per launch of the dominant kernel, from the
     committed `ncu --set full` summary under profiles/ (null if absent)."""
@@ -1067,7 +1129,8 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="marrow", choices=["marrow", "reference"])
-    ap.add_argument("--workload", default="filter", choices=list(WORKLOADS) + ["all", "rebalance"])
+    ap.add_argument("--workload", default="filter",
+                    choices=list(WORKLOADS) + ["all", "rebalance", "rebalance_nbody"])
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--trials", type=int, default=5,
@@ -1088,6 +1151,9 @@ def main():
         if args.steps is None:
             args.steps = 10
         run_reference(args, dist)
+        return
+    if args.workload == "rebalance_nbody":
+        run_rebalance_nbody(args, dist)
         return
     if args.workload == "rebalance":
         run_rebalance_scenario(args, dist)

@@ -43,6 +43,30 @@ def peaks():
     return p
 
 
+def alu_peaks(pk):
+    """Peaks of the ALU-bound rows: measured by scripts/microbench_peaks.cu on
+    a B200 of this pool (profiles/r02_alu_peaks.jsonl: packed FFMA2 for the
+    FP32 pipe, LOP3 for the integer ALU pipe), else the guide's unit counts."""
+    sm_mhz = pk.get("sm_max_mhz") or 1965.0
+    out = {"nbody": (148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "TFLOP/s",
+                     "148 SM x 128 FP32 lanes x 2 flop x max SM clock (guide unit counts)"),
+           "hysteresis": (148 * 64 * sm_mhz * 1e6 / 1e12, "Tops/s",
+                          "148 SM x 64 integer-ALU lanes x max SM clock (guide unit counts)")}
+    path = os.path.join(ROOT, "profiles", "r02_alu_peaks.jsonl")
+    try:
+        with open(path) as f:
+            m = {d["kernel"]: d for d in map(json.loads, f) if d}
+        out["nbody"] = (m["ffma2"]["value"], "TFLOP/s",
+                        "measured: packed FFMA2 throughput (scripts/microbench_peaks.cu, "
+                        "profiles/r02_alu_peaks.jsonl)")
+        out["hysteresis"] = (m["lop3"]["value"], "Tops/s",
+                             "measured: LOP3 integer-ALU throughput (scripts/microbench_peaks.cu, "
+                             "profiles/r02_alu_peaks.jsonl)")
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
+
+
 # ------------------------------------------------------------------ clocks (NVML)
 class ClockSampler:
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -863,11 +887,7 @@ def run_marrow(args, dist, wl_name):
     # roofline of the dominant kernel class: algorithmic bytes (flops) of its
     # launches in the timed region / their CUDA-event-measured duration
     nlaunch = {cls: n for cls, (_, n) in kstats.items()}
-    sm_mhz = pk.get("sm_max_mhz") or 1965.0
-    alu_peak = {"nbody": (148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "TFLOP/s",
-                          "148 SM x 128 FP32 lanes x 2 flop x max SM clock (guide unit counts)"),
-                "hysteresis": (148 * 64 * sm_mhz * 1e6 / 1e12, "Tops/s",
-                               "148 SM x 64 integer-ALU lanes x max SM clock (guide unit counts)")}
+    alu_peak = alu_peaks(pk)
     breakdown = []
     for cls, (kms, kn) in kstats.items():
         if kn == 0:

@@ -273,6 +273,9 @@ class Filter(Workload):
                               M.arg(dst, local_offset=self.o, global_shape=(H, W, 4))))
         self.units = H * W                       # whole-job pixels per step
         self.launch_bytes = 8 * self.n * W       # algorithmic: read 4 B + write 4 B per pixel
+        # steps run over rotating buffer sets: a run reads nothing the previous
+        # one wrote, so its first loads may overlap the previous run's drain
+        M.mw_ctx_set_run_pipelining(self.ctx, True)
         self.l2_note = (f"inputs larger than L2 ({ws >> 20} MiB/rank working set)" if self.B == 1 else
                         f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)")
 
@@ -285,7 +288,9 @@ class Filter(Workload):
     def config(self):
         return {"workload": self.name, "image": [self.H, self.W, 4],
                 "tree": "pipeline(gauss_noise(seed=4,S=8), solarize(T=128), mirror)",
-                "rows_per_rank": self.n, "l2": self.l2_note}
+                "rows_per_rank": self.n, "l2": self.l2_note,
+                "runs": "pipelined (mw_ctx_set_run_pipelining): each run's first loads may precede the "
+                        "wait for the previous run, whose outputs it does not read; stores stay ordered"}
 
 
 class Saxpy(Workload):
@@ -409,6 +414,7 @@ class Segmentation(Workload):
         self.units, self.launch_bytes = shape[0] * slab, 2 * self.n * slab
         self.l2_note = (f"inputs larger than L2 ({ws >> 20} MiB/rank)" if self.B == 1 else
                         f"{self.B} rotating buffer sets")
+        M.mw_ctx_set_run_pipelining(self.ctx, True)   # a run never reads what the previous wrote
 
     def step(self, i):
         return self.M.mw_run(self.ctx, self.tree, self.arglist(i % self.B))
@@ -418,7 +424,8 @@ class Segmentation(Workload):
 
     def config(self):
         return {"workload": self.name, "shape_zyx": list(self.shape), "lo": 85, "hi": 170,
-                "slabs_per_rank": self.n, "l2": self.l2_note}
+                "slabs_per_rank": self.n, "l2": self.l2_note,
+                "runs": "pipelined (mw_ctx_set_run_pipelining), as the filter"}
 
 
 class MapReduce(Workload):

@@ -336,6 +336,15 @@ mw_status mw_graph_destroy(mw_graph* g);
  * the uploads of a run then overlap the previous run's downloads (no start
  * barrier).  Default off.                                                    */
 mw_status mw_ctx_set_staging_overlap(mw_ctx* ctx, int32_t on);
+/* Run pipelining.  on != 0 promises that between runs of this ctx on a
+ * stream no other work writes what a run reads (the runs' only data
+ * dependencies are through their arguments).  A fused Map/Pipeline chain run
+ * whose source the previous run did not write then issues its first loads
+ * before the programmatic-dependent-launch wait, overlapping the previous
+ * run's drain (consecutive runs over rotating buffers, e.g. a rank's small
+ * share); its stores still follow the wait, so the stream order of every
+ * write is kept.  Default off.                                              */
+mw_status mw_ctx_set_run_pipelining(mw_ctx* ctx, int32_t on);
 /* Monitoring (per-device execution times feed the load balancer)
  * is on by default: every run records CUDA events around each partition's
  * kernels (mw_last_timings, mw_kernel_stats, mw_rebalance).  Off: no events,

@@ -85,7 +85,16 @@ struct mw_ctx {
     // FIFO of runs across streams: every run waits for the previous run's end
     // (a no-op on one stream) and records it (ctx scratch is shared by runs).
     cudaEvent_t last_run = nullptr;
+    cudaStream_t last_stream = nullptr;
     bool have_last_run = false;
+    // run pipelining (mw_ctx_set_run_pipelining): the byte ranges the previous
+    // run read and wrote, to launch an independent next run without the
+    // programmatic-dependent-launch wait
+    bool pipelining = false;
+    struct Ranges {
+        std::vector<std::pair<uintptr_t, uintptr_t>> rd, wr;
+        bool valid = false;
+    } prev_io;
     bool staging_overlap = false;   // mw_ctx_set_staging_overlap
     cudaStream_t lane_s[3]{};       // extra capture lanes of mw_graph_capture_many
     cudaEvent_t lane_ev[4]{};
@@ -394,6 +403,7 @@ struct RunCtx {
     cudaStream_t s;
     std::vector<int64_t> off, len;  // all P partitions
     int first;                      // this rank's first partition
+    bool indep = false;             // the next launch may read ahead of the PDL wait (pipelining)
     int owner(int part) const { return part / c->ppr; }
     bool local(int part) const { return owner(part) == c->rank; }
 };
@@ -401,9 +411,10 @@ struct RunCtx {
 // Launch a chain of RGBA groups over rows [r0, r0+n): src -> ... -> dst.
 mw_status run_rgba(RunCtx& R, int part, const std::vector<mwk::RgbaProg>& progs,
                    const uint8_t* src, uint8_t* dst, int64_t rows, int64_t W, int64_t row0,
-                   uint8_t* tmp0, uint8_t* tmp1) {
+                   uint8_t* tmp0, uint8_t* tmp1, bool dep_wait = true) {
     mwk::Launch L = launch_for(R.c, R.s, part);
     L.slow = 1.0f;   // slowdown is applied by repetition (caller)
+    L.dep_wait = dep_wait || progs.size() != 1;
     const uint8_t* in = src;
     for (size_t g = 0; g < progs.size(); ++g) {
         uint8_t* out = (g + 1 == progs.size()) ? dst : ((g & 1) ? tmp1 : tmp0);
@@ -866,6 +877,10 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
                 }
                 PartTimer t(c, R.s, p, MW_KC_U8);
                 mwk::Launch L = launch_for(c, R.s, p);
+                // a one-step chain: the first launch may read ahead (pipelining), a
+                // later partition's follows one that wrote other rows of dst only
+                L.dep_wait = !(R.indep && prog.size() == 1 && groups.size() == 1 && !c->monitor);
+                R.indep = prog.size() == 1 && groups.size() == 1;
                 const uint8_t* in = cur[q].p;
                 int64_t ipitch = cur[q].pitch;
                 for (size_t g = 0; g < groups.size(); ++g) {
@@ -1165,6 +1180,40 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
     return MW_OK;
 }
 
+// ------------------------------------------------------------ run pipelining
+// Byte ranges of a run's device arguments: [0] read, [1] written for the
+// src -> dst chains; every argument counts as read and written otherwise.
+mw_ctx::Ranges run_ranges(const mw_arg* args, int nargs, bool chain) {
+    mw_ctx::Ranges r;
+    for (int i = 0; i < nargs; ++i) {
+        const mw_arg& a = args[i];
+        if (a.location != MW_LOC_DEVICE || !a.ptr) continue;
+        const int64_t n = a.mode == MW_COPY ? a.shape[0] : a.local_rows;
+        const uintptr_t b = reinterpret_cast<uintptr_t>(a.ptr);
+        const std::pair<uintptr_t, uintptr_t> rg{b, b + (uintptr_t)(n * row_bytes(a))};
+        if (!chain || i == 0) r.rd.push_back(rg);
+        if (!chain || i == 1) r.wr.push_back(rg);
+    }
+    r.valid = true;
+    return r;
+}
+bool overlaps(const std::vector<std::pair<uintptr_t, uintptr_t>>& a,
+              const std::vector<std::pair<uintptr_t, uintptr_t>>& b) {
+    for (auto& x : a)
+        for (auto& y : b)
+            if (x.first < y.second && y.first < x.second) return true;
+    return false;
+}
+// The run's first kernel may start reading before the previous run's last
+// kernel completed: the ctx promised pipelining, the previous run was on this
+// stream, and this run (a src -> dst chain) reads nothing that run wrote.
+// (Its stores still wait for the predecessor, so write hazards cannot arise.)
+bool run_independent(const mw_ctx* c, const mw_arg* args, int nargs) {
+    if (!c->pipelining || !c->prev_io.valid || c->capturing) return false;
+    const mw_ctx::Ranges cur = run_ranges(args, nargs, true);
+    return !overlaps(cur.rd, c->prev_io.wr);
+}
+
 // ------------------------------------------------------------ the run
 mw_status run_loop_host(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
                         mw_future* f);
@@ -1295,6 +1344,11 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
             t0 = static_cast<uint8_t*>(a);
             t1 = static_cast<uint8_t*>(b);
         }
+        // The first launch may read ahead of the dependent-launch wait when the
+        // previous run wrote nothing it reads (pipelining contract); a later
+        // partition's launch follows the previous partition's, which wrote
+        // other rows of dst only (src and dst never alias).
+        bool indep = run_independent(c, args, nargs);
         for (int q = 0; q < ppr; ++q) {
             int p = R.first + q;
             if (R.len[p] == 0) continue;
@@ -1302,12 +1356,15 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
             // src -> dst chains are idempotent: the slowdown injector repeats them
             // (time exactly proportional to the factor; results unchanged)
             const int reps = c->slow[p] > 1.0f ? (int)std::lround(c->slow[p]) : 1;
-            for (int rep = 0; rep < reps; ++rep)
+            for (int rep = 0; rep < reps; ++rep) {
                 MW_OK_OR_RETURN(run_rgba(R, p, groups, at_row<const uint8_t>(args[0], R.off[p]),
                                          at_row<uint8_t>(args[1], R.off[p]), R.len[p], W, R.off[p],
-                                         t0, t1));
+                                         t0, t1, !indep || rep > 0 || c->monitor));
+                indep = true;
+            }
         }
     } else if (ik == MW_VK_U8 || ik == MW_VK_U8_2D) {
+        R.indep = run_independent(c, args, nargs);
         MW_OK_OR_RETURN(run_u8(R, prog, args[0], args[1], f));
     } else if (ik == MW_VK_NBODY && ok == MW_VK_NBODY) {
         if (L > 0 && args[0].ptr == args[1].ptr) return fail(MW_E_SHAPE_MISMATCH, "pos and vel alias");
@@ -1416,6 +1473,8 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         if (c->monitor) CUDA_OK(cudaEventRecord(c->wall_b, s));
         c->last_len = R.len;
         c->have_run = c->monitor;
+        c->prev_io = run_ranges(args, nargs, ik == MW_VK_RGBA || ik == MW_VK_U8 || ik == MW_VK_U8_2D);
+        c->prev_io.valid = !host && prog.size() <= 1;
     }
     return MW_OK;
 }
@@ -1535,14 +1594,24 @@ static void reap_retired(mw_ctx* c, bool sync);
 // Runs of one ctx execute in call order even on different streams (they
 // share the ctx scratch): a run's stream first waits for the previous run's
 // end, which each run records.  On one stream the wait is a no-op.
+// The event is recorded lazily, only when the stream changes: consecutive
+// runs on one stream keep no event operations between their kernels (which
+// would stand between programmatically dependent launches).
 static mw_status fifo_enter(mw_ctx* c, cudaStream_t s) {
-    if (c->capturing || !c->have_last_run) return MW_OK;
-    CUDA_OK(cudaStreamWaitEvent(s, c->last_run, 0));
+    if (c->capturing || !c->have_last_run || s == c->last_stream) return MW_OK;
+    if (cudaEventRecord(c->last_run, c->last_stream) != cudaSuccess) {
+        (void)cudaGetLastError();   // the previous stream is gone: drain the device instead
+        CUDA_OK(cudaDeviceSynchronize());
+    } else {
+        CUDA_OK(cudaStreamWaitEvent(s, c->last_run, 0));
+    }
+    c->prev_io.valid = false;   // another stream: no programmatic overlap
     return MW_OK;
 }
 static void fifo_exit(mw_ctx* c, cudaStream_t s) {
     if (c->capturing) return;
-    if (cudaEventRecord(c->last_run, s) == cudaSuccess) c->have_last_run = true;
+    c->last_stream = s;
+    c->have_last_run = true;
 }
 
 static void ctx_teardown(mw_ctx* c) {
@@ -1889,6 +1958,13 @@ mw_status mw_ctx_set_slowdown(mw_ctx* c, int32_t part, float factor) {
     if (part < 0 || part >= c->P || !(factor >= 1.0f))
         return fail(MW_E_INVALID_SPEC, "bad partition or factor < 1");
     c->slow[part] = factor;
+    return MW_OK;
+}
+
+mw_status mw_ctx_set_run_pipelining(mw_ctx* c, int32_t on) {
+    if (!c) return fail(MW_E_STATE, "NULL ctx");
+    c->pipelining = on != 0;
+    c->prev_io.valid = false;
     return MW_OK;
 }
 

@@ -110,6 +110,7 @@ __device__ __forceinline__ void pdl_wait_and_release() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+
 // y_i <- fma(a_k, x_i, y_i), k = 0..n-1 (R8 single rounding).
 __global__ void __launch_bounds__(256) k_saxpy_vec(const __grid_constant__ SaxpyProg p, const float4* __restrict__ x,
                                                    float4* __restrict__ y, int64_t nvec) {
@@ -384,7 +385,7 @@ template <int kTmaChunk, int kTmaStages, bool MIRROR, bool KM, bool T128>
 __global__ void __launch_bounds__(256) k_rgba_ns_tma(const __grid_constant__ NsConst c,
                                                      const uint8_t* __restrict__ src,
                                                      uint8_t* __restrict__ dst, int64_t rows,
-                                                     uint32_t W, uint32_t row0) {
+                                                     uint32_t W, uint32_t row0, int dep) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint4* sin = reinterpret_cast<uint4*>(smem);                                   // NS x CH
     uint4* sout = reinterpret_cast<uint4*>(smem + kTmaStages * kTmaChunk);         // NS x CH
@@ -406,8 +407,12 @@ __global__ void __launch_bounds__(256) k_rgba_ns_tma(const __grid_constant__ NsC
         // launched with programmatic stream serialization: the CTA may start
         // while the previous kernel drains; thread 0 is the only thread that
         // touches global memory (bulk copies), so it waits here for the
-        // predecessor grid, then lets the next run's grid be scheduled
-        pdl_wait_and_release();
+        // predecessor grid, then lets the next run's grid be scheduled.
+        // dep == 0 (Launch::dep_wait false: the predecessor wrote nothing this
+        // run reads) issues the first loads BEFORE the wait, overlapping the
+        // predecessor's drain; every store still follows the wait, so each
+        // grid completes after its predecessor and the stream order holds.
+        if (dep) pdl_wait_and_release();
         for (int s = 0; s < kTmaStages; ++s) {
             const int64_t item = blockIdx.x + (int64_t)s * gridDim.x;
             if (item < n_items) {
@@ -415,6 +420,7 @@ __global__ void __launch_bounds__(256) k_rgba_ns_tma(const __grid_constant__ NsC
                 bulk_load(sin + s * VPC, src_of(item), kTmaChunk, &bar[s]);
             }
         }
+        if (!dep) pdl_wait_and_release();
     }
     __syncthreads();
     int it = 0;
@@ -680,7 +686,7 @@ template <int CH, int NS>
 __global__ void __launch_bounds__(256) k_u8_tma(const __grid_constant__ U8Prog p,
                                                 const __grid_constant__ U8Const c,
                                                 const uint8_t* __restrict__ src,
-                                                uint8_t* __restrict__ dst, int64_t nbytes) {
+                                                uint8_t* __restrict__ dst, int64_t nbytes, int dep) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint4* sin = reinterpret_cast<uint4*>(smem);
     uint4* sout = reinterpret_cast<uint4*>(smem + NS * CH);
@@ -691,6 +697,9 @@ __global__ void __launch_bounds__(256) k_u8_tma(const __grid_constant__ U8Prog p
     if (threadIdx.x == 0) {
         for (int st = 0; st < NS; ++st) mbar_init(&bar[st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // programmatic dependent launch, as k_rgba_ns_tma: thread 0 alone
+        // touches global memory; dep == 0 reads ahead of the wait
+        if (dep) pdl_wait_and_release();
         for (int st = 0; st < NS; ++st) {
             const int64_t item = blockIdx.x + (int64_t)st * gridDim.x;
             if (item < n_items) {
@@ -698,6 +707,7 @@ __global__ void __launch_bounds__(256) k_u8_tma(const __grid_constant__ U8Prog p
                 bulk_load(sin + st * VPC, src + item * CH, len_of(item), &bar[st]);
             }
         }
+        if (!dep) pdl_wait_and_release();
     }
     __syncthreads();
     int it = 0;
@@ -2092,7 +2102,7 @@ cudaError_t rgba_chain(const RgbaProg& p, const uint8_t* src, uint8_t* dst, int6
         cfg.attrs = at;                                                                        \
         cfg.numAttrs = 1;                                                                      \
         cudaLaunchKernelEx(&cfg, k_rgba_ns_tma<CH, NS, MI, KMI, TI>, nc, src, dst, rows,       \
-                           (uint32_t)W, (uint32_t)row0);                                       \
+                           (uint32_t)W, (uint32_t)row0, (int)L.dep_wait);                      \
     } while (0)
 #define MW_TMA_CFG(MI, KMI, TI)                                                                \
     do {                                                                                       \
@@ -2198,8 +2208,18 @@ cudaError_t u8_chain(const U8Prog& p, const uint8_t* src, int64_t sp, uint8_t* d
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
                 return resident_ctas(k_u8_tma<CH, NS>, 256, smem);                             \
             }();                                                                               \
-            k_u8_tma<CH, NS><<<grid_for(items, occ, L), 256, smem, L.stream>>>(p, c, src, dst,  \
-                                                                              rows * W);       \
+            cudaLaunchAttribute at[1];                                                         \
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                     \
+            at[0].val.programmaticStreamSerializationAllowed = 1;                              \
+            cudaLaunchConfig_t cfg = {};                                                       \
+            cfg.gridDim = dim3(grid_for(items, occ, L));                                       \
+            cfg.blockDim = dim3(256);                                                          \
+            cfg.dynamicSmemBytes = smem;                                                       \
+            cfg.stream = L.stream;                                                             \
+            cfg.attrs = at;                                                                    \
+            cfg.numAttrs = 1;                                                                  \
+            cudaLaunchKernelEx(&cfg, k_u8_tma<CH, NS>, p, c, src, dst, rows * W,               \
+                               (int)L.dep_wait);                                               \
         }
         if (items >= 8ll * sm_count() * 3) MW_U8_TMA_LAUNCH(2) else MW_U8_TMA_LAUNCH(3)
 #undef MW_U8_TMA_LAUNCH

@@ -25,6 +25,10 @@ struct Launch {
     cudaStream_t stream;
     float slow;        // 1 = full speed
     const int* tune;   // TUNE_COUNT values
+    // false: the launch reads nothing the stream's previous kernel wrote
+    // (mw_ctx_set_run_pipelining), so it may issue its first loads before the
+    // programmatic-dependent-launch wait (its stores still follow it)
+    bool dep_wait = true;
 };
 
 // ------------------------------------------------------------ fused Map chains

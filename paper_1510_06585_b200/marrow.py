@@ -120,6 +120,7 @@ _SIG = {
     "mw_map_reduce_sct": [_vp, _vp, _node_pp],
     "mw_ctx_set_monitoring": [_vp, _i32],
     "mw_ctx_set_staging_overlap": [_vp, _i32],
+    "mw_ctx_set_run_pipelining": [_vp, _i32],
     "mw_map_reduce_user": [_vp, _MERGE_FN, _vp, _node_pp],
     "mw_loop_host": [_vp, _i64, _COND_FN, _vp, _node_pp],
     "mw_loop_for": [_vp, _i64, _node_pp],
@@ -788,6 +789,12 @@ def mw_ctx_set_staging_overlap(ctx, on=True):
     """Host inputs are complete when mw_run is called: staged uploads overlap
     the previous run's downloads (no start barrier)."""
     _call("mw_ctx_set_staging_overlap", ctx.ptr, int(bool(on)))
+
+
+def mw_ctx_set_run_pipelining(ctx, on=True):
+    """Promise: no foreign work between this ctx's runs writes what they read;
+    independent fused-chain runs then overlap their predecessor's drain."""
+    _call("mw_ctx_set_run_pipelining", ctx.ptr, int(bool(on)))
 
 
 def mw_ctx_set_tuning(ctx, knob, value):

@@ -600,7 +600,10 @@ def test_graph_capture_replay():
         g3.launch(s)
     s.synchronize()
     assert np.array_equal(dst.cpu().numpy(), want_h) and g3.result()["executions"] == D + 1
-    # multi-partition byte stencil needs the host for its loop condition
+    # multi-partition per-pass protocol (HYST_FUSED = 0) needs the host for its
+    # loop condition (the fused multi-partition loop is capturable: see
+    # test_hysteresis_fused_partitions_graph_capture)
+    M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_FUSED, 0)
     with pytest.raises(M.MwError) as e:
         with torch.cuda.stream(s):
             M.mw_graph_capture(c, trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)], s)

@@ -130,3 +130,48 @@ def test_graph_lanes_keep_data_dependencies(lanes):
     s.synchronize()
     want = K.mirror(K.solarize(K.gauss_noise(img, 4, 8), 128))
     assert all(np.array_equal(o.cpu().numpy(), want) for o in outs)
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_run_pipelining_keeps_dependencies(parts):
+    """mw_ctx_set_run_pipelining: runs over rotating buffer sets read ahead of
+    the dependent-launch wait; a run reading what the previous run wrote
+    (filter applied twice through an intermediate) still waits for it."""
+    H, W = 1024, 4096   # W*4 a multiple of the TMA chunk: the TMA kernel runs
+    img = synth.np_rgba(3, 0, H * W).reshape(H, W, 4)
+    want = K.mirror(K.solarize(K.gauss_noise(img, 4, 8), 128))
+    want2 = K.mirror(K.solarize(K.gauss_noise(want, 4, 8), 128))
+    c = M.mw_ctx_create(0, 0, 1, parts)
+    M.mw_ctx_set_monitoring(c, False)
+    M.mw_ctx_set_run_pipelining(c, True)
+    s = torch.cuda.Stream()
+    srcs = [torch.from_numpy(img).to(DEV) for _ in range(3)]
+    dsts = [torch.empty_like(srcs[0]) for _ in range(3)]
+    mid, out = torch.empty_like(srcs[0]), torch.empty_like(srcs[0])
+    node = trees.filter_pipeline()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        for i in range(30):
+            M.mw_run(c, node, [M.arg(srcs[i % 3]), M.arg(dsts[i % 3])], stream=s)
+            if i % 7 == 3:   # a dependent pair
+                M.mw_run(c, node, [M.arg(srcs[0]), M.arg(mid)], stream=s)
+                M.mw_run(c, node, [M.arg(mid), M.arg(out)], stream=s)
+    s.synchronize()
+    assert all(np.array_equal(d.cpu().numpy(), want) for d in dsts)
+    assert np.array_equal(out.cpu().numpy(), want2)
+    # u8 chains (segmentation TMA ring) the same way
+    vol = synth.np_u8_stream(7, 0, 64 * 256 * 256).reshape(64, 256, 256)
+    vs = [torch.from_numpy(vol).to(DEV) for _ in range(2)]
+    vd = [torch.empty_like(vs[0]) for _ in range(2)]
+    v2 = torch.empty_like(vs[0])
+    seg = trees.segmentation()
+    seg2 = trees.segmentation(100, 200)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        for i in range(10):
+            M.mw_run(c, seg, [M.arg(vs[i % 2]), M.arg(vd[i % 2])], stream=s)
+        M.mw_run(c, seg2, [M.arg(vd[1]), M.arg(v2)], stream=s)   # reads the last run's output
+    s.synchronize()
+    ref = K.segment(vol, 85, 170)
+    assert all(np.array_equal(d.cpu().numpy(), ref) for d in vd)
+    assert np.array_equal(v2.cpu().numpy(), K.segment(ref, 100, 200))

@@ -121,7 +121,8 @@ class Result:
 
 
 def _compat(a, b):
-    return a == b or {a, b} == {U8, U8_2D}
+    # a saxpy value is the pair (x, y) of fp32 vectors: what map_product takes
+    return a == b or {a, b} == {U8, U8_2D} or {a, b} == {SAXPY, VEC2}
 
 
 def sig(node: Node):
@@ -217,20 +218,32 @@ def evaluate(node: Node, value, while_counts=None, lengths=None) -> Result:
         return evaluate(node.tree, value, lengths=lengths)
     if isinstance(node, Pipeline):
         r = Result(value)
-        any_changed = False
+        any_changed, execs, conv = False, 0, True
         for s in node.stages:
             r = evaluate(s, r.value)
             any_changed |= r.changed
+            execs += r.executions      # while-loop executions of the whole tree (marrow.h E)
+            conv &= r.converged
         r.changed = any_changed
+        r.executions, r.converged = execs, conv
         return r
     if isinstance(node, MapReduce):
         m = node.map_stage
         while isinstance(m, Map):
             m = m.tree
+        # a map stage that is a pipeline: its leading stages transform the
+        # value, the last one (a map leaf) forms the terms
+        pre = []
+        if isinstance(m, Pipeline):
+            pre, m = list(m.stages[:-1]), m.stages[-1]
+            while isinstance(m, Map):
+                m = m.tree
         if not isinstance(m, Leaf):
-            raise NotImplementedError("MapReduce map stage must be a map leaf")
+            raise NotImplementedError("MapReduce map stage must end with a map leaf")
         if m.kind not in ("map_identity", "map_product"):
             raise ValueError(m.kind)
+        for st in pre:
+            value = evaluate(st, value).value
         vals = value if isinstance(value, tuple) else (value,)
 
         def red(sl):
@@ -257,8 +270,13 @@ def evaluate(node: Node, value, while_counts=None, lengths=None) -> Result:
         return Result(None, reduced=_merge(node.op, parts))
     if isinstance(node, LoopFor):
         r = Result(value)
+        execs, conv, changed = 0, True, False
         for _ in range(node.n):
             r = evaluate(node.body, r.value)
+            execs += r.executions
+            conv &= r.converged
+            changed |= r.changed       # a loop body changed iff one of its executions did
+        r.executions, r.converged, r.changed = execs, conv, changed
         return r
     if isinstance(node, LoopWhileChanged):
         changed, e, v = True, 0, value

@@ -157,6 +157,7 @@ struct mw_future {
     double* res = nullptr;     // pinned slot (4 x 8 B): [0] reduced, [1] plane-loop {E, converged} int32
     bool has_reduce = false;
     bool plane_loop = false;
+    int64_t plane_m = 1, plane_nb = 0;   // steps per body execution, max body executions
     double executions = 0.0;
     double converged = 1.0;
     bool waited = false;
@@ -395,6 +396,29 @@ std::vector<mwk::SaxpyProg> saxpy_groups(const std::vector<mw::ChainOp>& ops) {
         out.back().a[out.back().n++] = o.fa;
     }
     return out;
+}
+
+// A while-loop runs in steps (m per body execution, at most nb bodies); the
+// body changed iff one of its steps did.  From the step count E_steps (the
+// last changing step + 2 when a step changed nothing, else m x nb): the body
+// executions the oracle's LoopWhileChanged reports, and whether it converged.
+void body_execs(int64_t e_steps, bool step_conv, int64_t m, int64_t nb, double* E, bool* conv) {
+    if (m <= 1) {
+        *E = (double)e_steps;
+        *conv = step_conv;
+        return;
+    }
+    if (step_conv) {
+        const int64_t last = e_steps - 2;   // -1: nothing ever changed
+        const int64_t eb = (last < 0 ? -1 : last / m) + 2;
+        if (eb <= nb) {
+            *E = (double)eb;
+            *conv = true;
+            return;
+        }
+    }
+    *E = (double)nb;
+    *conv = false;
 }
 
 // ------------------------------------------------------------ run state
@@ -639,6 +663,8 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
         if (is_while) {
             CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 8, cudaMemcpyDeviceToHost, R.s));
             f->plane_loop = true;
+            f->plane_m = st.m;
+            f->plane_nb = st.n / st.m;
         }
         return MW_OK;
     }
@@ -711,8 +737,11 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
         settled(x);
     }
     if (is_while) {
-        f->executions += (double)E;
-        if (!converged) f->converged = 0.0;
+        double eb;
+        bool cv;
+        body_execs(E, converged, st.m, st.n / st.m, &eb, &cv);
+        f->executions += eb;
+        if (!cv) f->converged = 0.0;
     }
     if (batched) {   // d_last[4..6] = 0: the unpack reads S0, here set to the final buffer
         mwk::PlaneIO io = io_of();
@@ -817,6 +846,8 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
             if (prog[1].kind == StepKind::StencilWhile) {
                 CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 8, cudaMemcpyDeviceToHost, R.s));
                 f->plane_loop = true;
+                f->plane_m = prog[1].m;
+                f->plane_nb = prog[1].n / prog[1].m;
             }
             return MW_OK;
         }
@@ -927,7 +958,7 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
             for (int a = p + 1; a < c->P; ++a) bot_nbr[q] |= R.len[a] > 0;
         }
         const int64_t max_it = st.n;
-        const int64_t ce = is_while ? std::max<int64_t>(1, st.check_every) : max_it;
+        const int64_t ce = is_while ? std::max<int64_t>(1, st.check_every) * st.m : max_it;
         int64_t it = 0;
         bool converged = !is_while;
         int64_t E = 0;
@@ -968,8 +999,11 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
         }
         if (is_while) {
             if (!converged) E = max_it;
-            f->executions += (double)E;
-            if (!converged) f->converged = 0.0;
+            double eb;
+            bool cv;
+            body_execs(E, converged, st.m, st.n / st.m, &eb, &cv);
+            f->executions += eb;
+            if (!cv) f->converged = 0.0;
         }
         for (int q = 0; q < ppr; ++q) {
             int p = R.first + q;
@@ -1319,7 +1353,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
                         "host-resident arguments are supported for single fused Map/Pipeline "
                         "chains (NEXT-1)");
         MW_OK_OR_RETURN(run_staged(R, prog[0], ik, args));
-    } else if (ik == MW_VK_SAXPY) {
+    } else if (ik == MW_VK_SAXPY && !(prog.size() == 1 && prog[0].kind == StepKind::Reduce)) {
         auto groups = prog.empty() ? std::vector<mwk::SaxpyProg>{} : saxpy_groups(prog[0].ops);
         for (int q = 0; q < ppr; ++q) {
             int p = R.first + q;
@@ -1368,7 +1402,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         MW_OK_OR_RETURN(run_u8(R, prog, args[0], args[1], f));
     } else if (ik == MW_VK_NBODY && ok == MW_VK_NBODY) {
         if (L > 0 && args[0].ptr == args[1].ptr) return fail(MW_E_SHAPE_MISMATCH, "pos and vel alias");
-        if (!prog.empty()) MW_OK_OR_RETURN(run_nbody(R, prog[0], args[0], args[1]));
+        for (const Step& stp : prog) MW_OK_OR_RETURN(run_nbody(R, stp, args[0], args[1]));
     } else if (ik == MW_VK_NBODY) {
         const Step& stp = prog[0];
         for (int q = 0; q < ppr; ++q) {
@@ -1383,7 +1417,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
                                             launch_for(c, s, p)),
                                  "nbody_accel"));
         }
-    } else if (ik == MW_VK_VEC1 || ik == MW_VK_VEC2) {
+    } else if (ik == MW_VK_VEC1 || ik == MW_VK_VEC2 || ik == MW_VK_SAXPY) {   // MapReduce
         const int64_t CH = 1ll << mwk::kChunkLog2;
         const int64_t nch = (L + CH - 1) / CH;
         void *pp, *rp;
@@ -1396,6 +1430,8 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
         MW_OK_OR_RETURN(kerr(mwk::reduce_fill_identity(partials, std::max<int64_t>(1, nch), s, rop),
                              "reduce_fill"));
         const bool dot = prog[0].dot;
+        mwk::SaxpyProg pre{};   // saxpy chain fused into the map stage (sct.cpp plan)
+        for (const mw::ChainOp& o : prog[0].pre) pre.a[pre.n++] = o.fa;
         for (int q = 0; q < ppr; ++q) {
             int p = R.first + q;
             if (R.len[p] == 0) continue;
@@ -1403,7 +1439,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
             MW_OK_OR_RETURN(kerr(mwk::reduce_chunks(at_row<const float>(args[0], R.off[p]),
                                                     dot ? at_row<const float>(args[1], R.off[p]) : nullptr,
                                                     R.off[p], R.off[p], R.len[p], L, partials,
-                                                    launch_for(c, s, p), rop),
+                                                    launch_for(c, s, p), rop, pre.n ? &pre : nullptr),
                                  "reduce_chunks"));
         }
         // merge "+" across ranks: each chunk partial has exactly
@@ -1796,8 +1832,11 @@ mw_status mw_future_result(mw_future* f, double* out, int32_t n) {
     double ex = f->executions, conv = f->converged;
     if (f->plane_loop) {
         const int32_t* st = reinterpret_cast<const int32_t*>(f->res + 1);
-        ex += (double)st[0];
-        if (!st[1]) conv = 0.0;
+        double eb;
+        bool cv;
+        body_execs(st[0], st[1] != 0, f->plane_m, f->plane_nb, &eb, &cv);
+        ex += eb;
+        if (!cv) conv = 0.0;
     }
     double red = f->has_reduce ? *f->res : 0.0;
     if (f->parts) {   // merging function over the partitions with work, in global order

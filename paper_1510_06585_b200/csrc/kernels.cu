@@ -1832,12 +1832,23 @@ __device__ __forceinline__ double red_term(double acc, float a, float b) {
     else return red_op<OP>(acc, DOT ? (double)a * (double)b : (double)a);
 }
 
-template <bool DOT, int OP>
+// PRE: the map stage is pipeline(saxpy chain, map_product) fused into the
+// reduction: the second operand is y' = fma(a_k, x, y) (k = 0..pre.n-1, fp32,
+// one rounding each, as the saxpy leaf) computed in registers, never stored.
+template <bool PRE>
+__device__ __forceinline__ float pre_y(const SaxpyProg& pre, float x, float y) {
+    if (PRE)
+        for (int k = 0; k < pre.n; ++k) y = __fmaf_rn(pre.a[k], x, y);
+    return y;
+}
+
+template <bool DOT, int OP, bool PRE = false>
 __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __restrict__ x,
                                                                const float* __restrict__ y,
                                                                int64_t x0, int64_t first_chunk,
                                                                int64_t n_chunks, int64_t total,
-                                                               double* __restrict__ partials) {
+                                                               double* __restrict__ partials,
+                                                               const __grid_constant__ SaxpyProg pre) {
     __shared__ double warp_part[kRedThreads / 32];
     const int64_t CH = 1ll << kChunkLog2;
     for (int64_t cc = blockIdx.x; cc < n_chunks; cc += gridDim.x) {
@@ -1860,17 +1871,21 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
                 uint4 a = ld_stream(xv + k * kRedThreads + threadIdx.x);
                 uint4 b = a;
                 if (DOT) b = ld_stream(yv + k * kRedThreads + threadIdx.x);
-                acc4[0] = red_term<OP, DOT>(acc4[0], __uint_as_float(a.x), __uint_as_float(b.x));
-                acc4[1] = red_term<OP, DOT>(acc4[1], __uint_as_float(a.y), __uint_as_float(b.y));
-                acc4[2] = red_term<OP, DOT>(acc4[2], __uint_as_float(a.z), __uint_as_float(b.z));
-                acc4[3] = red_term<OP, DOT>(acc4[3], __uint_as_float(a.w), __uint_as_float(b.w));
+                const float ax = __uint_as_float(a.x), ay = __uint_as_float(a.y);
+                const float az = __uint_as_float(a.z), aw = __uint_as_float(a.w);
+                acc4[0] = red_term<OP, DOT>(acc4[0], ax, pre_y<PRE>(pre, ax, __uint_as_float(b.x)));
+                acc4[1] = red_term<OP, DOT>(acc4[1], ay, pre_y<PRE>(pre, ay, __uint_as_float(b.y)));
+                acc4[2] = red_term<OP, DOT>(acc4[2], az, pre_y<PRE>(pre, az, __uint_as_float(b.z)));
+                acc4[3] = red_term<OP, DOT>(acc4[3], aw, pre_y<PRE>(pre, aw, __uint_as_float(b.w)));
             }
         } else {
             for (int k = 0; k < (int)(CH / 4 / kRedThreads); ++k) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     int64_t i = ((int64_t)k * kRedThreads + threadIdx.x) * 4 + e;
-                    if (i < len) acc4[e] = red_term<OP, DOT>(acc4[e], x[base + i], DOT ? y[base + i] : 0.f);
+                    if (i < len)
+                        acc4[e] = red_term<OP, DOT>(acc4[e], x[base + i],
+                                                    DOT ? pre_y<PRE>(pre, x[base + i], y[base + i]) : 0.f);
                 }
             }
         }
@@ -2692,19 +2707,35 @@ cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4*
 
 template <bool DOT, int OP>
 static void reduce_chunks_t(const float* x, const float* y, int64_t x0, int64_t c0, int64_t nc,
-                            int64_t total, double* partials, const Launch& L) {
-    static int occ = resident_ctas(k_reduce_chunks<DOT, OP>, kRedThreads);
+                            int64_t total, double* partials, const Launch& L,
+                            const SaxpyProg* pre = nullptr) {
     ++g_launches;
-    k_reduce_chunks<DOT, OP><<<grid_for(nc, occ, L), kRedThreads, 0, L.stream>>>(x, y, x0, c0, nc, total, partials);
+    if (DOT && pre && pre->n > 0) {
+        static int occp = resident_ctas(k_reduce_chunks<DOT, OP, true>, kRedThreads);
+        k_reduce_chunks<DOT, OP, true><<<grid_for(nc, occp, L), kRedThreads, 0, L.stream>>>(
+            x, y, x0, c0, nc, total, partials, *pre);
+        return;
+    }
+    static int occ = resident_ctas(k_reduce_chunks<DOT, OP>, kRedThreads);
+    k_reduce_chunks<DOT, OP><<<grid_for(nc, occ, L), kRedThreads, 0, L.stream>>>(x, y, x0, c0, nc, total, partials,
+                                                                                 SaxpyProg{});
 }
 
 cudaError_t reduce_chunks(const float* x, const float* y, int64_t x0, int64_t first,
                           int64_t count, int64_t total, double* partials, const Launch& L,
-                          int op) {
+                          int op, const SaxpyProg* pre) {
     if (count <= 0) return cudaSuccess;
     const int64_t CH = 1ll << kChunkLog2;
-    if (first % CH != 0 || op < 0 || op > 2) return cudaErrorInvalidValue;
+    if (first % CH != 0 || op < 0 || op > 2 || (pre && pre->n > 0 && !y)) return cudaErrorInvalidValue;
     int64_t c0 = first / CH, nc = (count + CH - 1) / CH;
+    if (pre && pre->n > 0) {
+        switch (op) {
+            case 0: reduce_chunks_t<true, 0>(x, y, x0, c0, nc, total, partials, L, pre); break;
+            case 1: reduce_chunks_t<true, 1>(x, y, x0, c0, nc, total, partials, L, pre); break;
+            default: reduce_chunks_t<true, 2>(x, y, x0, c0, nc, total, partials, L, pre); break;
+        }
+        return cudaGetLastError();
+    }
     switch (op * 2 + (y ? 1 : 0)) {
         case 0: reduce_chunks_t<false, 0>(x, y, x0, c0, nc, total, partials, L); break;
         case 1: reduce_chunks_t<true, 0>(x, y, x0, c0, nc, total, partials, L); break;

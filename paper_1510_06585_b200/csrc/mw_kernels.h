@@ -184,9 +184,11 @@ constexpr int kChunkLog2 = 16;      // canonical reduction chunk: 2^16 elements
 // (first % 2^16 == 0) into partials[chunk index]; y == nullptr: sum, else dot.
 // x[0] (and y[0]) hold global element x0.
 // op: MW_REDUCE_* (0 sum, 1 maxNum, 2 minNum).
+// pre (dot only): the map stage is pipeline(saxpy chain, map_product): the
+// terms are x * y' with y' = fma(pre.a[k], x, y) applied in order in fp32.
 cudaError_t reduce_chunks(const float* x, const float* y, int64_t x0, int64_t first,
                           int64_t count, int64_t total, double* partials, const Launch& L,
-                          int op = 0);
+                          int op = 0, const SaxpyProg* pre = nullptr);
 // Fixed-tree combine of nchunks partials into *result (one CTA).
 cudaError_t reduce_combine(const double* partials, int64_t nchunks, double* result,
                            cudaStream_t s, int op = 0);

@@ -113,7 +113,9 @@ std::vector<const Node*> leaves(const Node* n) {
 
 static bool compat(int a, int b) {
     auto u8 = [](int k) { return k == MW_VK_U8 || k == MW_VK_U8_2D; };
-    return a == b || (u8(a) && u8(b));
+    // a saxpy value is the pair (x, y): two fp32 vectors, what map_product takes
+    auto pair = [](int k) { return k == MW_VK_SAXPY || k == MW_VK_VEC2; };
+    return a == b || (u8(a) && u8(b)) || (pair(a) && pair(b));
 }
 static bool has_2d(const Node* n) {
     if (n->type == NodeType::Leaf) return n->leaf == LeafKind::HystStep;
@@ -201,12 +203,24 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
         case NodeType::MapReduce: {
             mw_status st = plan(n->kids[0], &a);
             if (st) return st;
+            // the map stage: map_identity / map_product, or a Map/Pipeline chain
+            // of saxpy stages followed by map_product (fused: the chain's output
+            // never leaves registers)
+            std::vector<ChainOp> pre;
+            if (a.size() == 2 && a[0].kind == StepKind::Saxpy && a[1].kind == StepKind::MapStage &&
+                a[1].dot) {
+                if ((int)a[0].ops.size() > 16)
+                    return fail(MW_E_UNSUPPORTED, "map stage: saxpy chain longer than 16 stages");
+                pre = a[0].ops;
+                a.erase(a.begin());
+            }
             if (a.size() != 1 || a[0].kind != StepKind::MapStage)
                 return fail(MW_E_UNSUPPORTED,
-                            "MapReduce map stage must be a single map_identity/map_product "
-                            "(device SCT reduction stages are NEXT-4)");
+                            "MapReduce map stage must be map_identity / map_product, or a saxpy "
+                            "chain followed by map_product");
             Step s;
             s.kind = StepKind::Reduce;
+            s.pre = pre;
             s.dot = a[0].dot;
             s.merge_op = n->merge_op;
             s.reduce_op = n->kids.size() > 1 ? (int32_t)n->kids[1]->ia : MW_REDUCE_SUM;
@@ -234,20 +248,33 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
                 out->push_back(s);
                 return MW_OK;
             }
-            return fail(MW_E_UNSUPPORTED,
-                        "LoopFor body must be a Map/Pipeline chain, a hysteresis step or an "
-                        "N-body step (mixed bodies are NEXT-4)");
+            // any other body (mixed chains and stencils, nested while-loops, ...):
+            // the loop is its body unrolled n times (P:376-378 with the state
+            // carried between executions), adjacent chains / stencil steps merged
+            if (n->n * (int64_t)a.size() > 4096)
+                return fail(MW_E_UNSUPPORTED, "loop over a mixed body unrolls to > 4096 steps");
+            for (int64_t i = 0; i < n->n; ++i) append_merged(*out, a);
+            int64_t ops = 0;
+            for (const Step& st : *out) ops += (int64_t)st.ops.size();
+            if (ops > kMaxChainOps) return fail(MW_E_UNSUPPORTED, "loop unrolls to > 65536 chain stages");
+            return MW_OK;
         }
         case NodeType::LoopWhile: {
             mw_status st = plan(n->kids[0], &a);
             if (st) return st;
-            if (a.size() != 1 || a[0].kind != StepKind::StencilFor || a[0].n != 1)
+            // the body is m >= 1 hysteresis steps (pipeline(step, step), loop_for(step, m),
+            // ...): the only built-in kernel that reports change; the loop runs in steps
+            // and reports body executions (a body changed iff one of its steps did)
+            if (a.size() != 1 || a[0].kind != StepKind::StencilFor || a[0].n < 1)
                 return fail(MW_E_UNSUPPORTED,
-                            "LoopWhileChanged body must be one hysteresis step (the only built-in "
+                            "LoopWhileChanged body must be hysteresis steps (the only built-in "
                             "kernel that reports change)");
+            if (n->n > (int64_t{1} << 40) / a[0].n)
+                return fail(MW_E_UNSUPPORTED, "while-loop step count overflows");
             Step s;
             s.kind = StepKind::StencilWhile;
-            s.n = n->n;
+            s.m = a[0].n;
+            s.n = n->n * s.m;
             s.check_every = n->check_every;
             out->push_back(s);
             return MW_OK;
@@ -293,7 +320,9 @@ const NodeCache* plan_cached(const Node* root, mw_status* st) {
 }
 
 int64_t granule_of(const Node* root, mw_status* st) {
-    int64_t g = align_of(root->in_kind);
+    // a MapReduce root partitions by canonical reduction chunks whatever its
+    // map stage's input kind (e.g. a saxpy chain fused into the map stage)
+    int64_t g = root->out_kind == MW_VK_SCALAR ? align_of(MW_VK_VEC2) : align_of(root->in_kind);
     for (const Node* l : leaves(root)) {
         int64_t epu, nu;
         leaf_epu_nu(l, &epu, &nu);

@@ -67,7 +67,8 @@ struct ChainOp {
 struct Step {
     StepKind kind;
     std::vector<ChainOp> ops;
-    int64_t n = 0;
+    int64_t n = 0;                     // StencilWhile: max STEPS (= max body executions x m)
+    int64_t m = 1;                     // StencilWhile: steps per body execution
     int32_t check_every = 1;
     float dt = 0.f, eps2 = 0.f;
     bool dot = false;
@@ -75,6 +76,7 @@ struct Step {
     bool strict = false;
     int32_t merge_op = 0;              // Reduce: MW_MERGE_*
     int32_t reduce_op = 0;             // Reduce: MW_REDUCE_* (device reduction stage)
+    std::vector<ChainOp> pre;          // Reduce: saxpy chain fused into the map stage (dot)
     void* fn = nullptr;
     void* user = nullptr;
 };

@@ -1093,3 +1093,101 @@ def test_hysteresis_fused_partitions_graph_capture():
         assert np.array_equal(dst.cpu().numpy(), want)
         r = g.result()
         assert r["executions"] == D + 1 and r["converged"]
+
+
+# ----------------------------------------------------------------- general SCT composition
+@pytest.mark.parametrize("m", [2, 3])
+def test_while_loop_with_multi_step_body(m):
+    """loop_while_changed(pipeline(step x m)): E counts BODY executions (a body
+    changed iff one of its steps did), as the oracle's LoopWhileChanged."""
+    H, W = 257, 300
+    gray = synth.np_u8_stream(8, 2, H * W).reshape(H, W)
+    body = sct.Pipeline([sct.Leaf("hysteresis_step")] * m)
+    otree = sct.Pipeline([sct.Leaf("segment", {"lo": 173, "hi": 250}),
+                          sct.LoopWhileChanged(body, 1000), sct.Leaf("hysteresis_finalize")])
+    want = sct.evaluate(otree, gray)
+    mb = M.mw_pipeline([M.mw_kernel_hysteresis_step() for _ in range(m)])
+    tree = M.mw_pipeline([M.mw_kernel_segment(173, 250), M.mw_loop_while_changed(mb, 1000, 1),
+                          M.mw_kernel_hysteresis_finalize()])
+    for k, d, planes in [(1, None, 1), (3, [0.3, 0.3, 0.4], 1), (3, [0.5, 0.0, 0.5], 0), (2, None, 0)]:
+        c = pctx(k, d, planes)
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(c, tree, [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want.value), (k, planes)
+        assert r["executions"] == want.executions and r["converged"], (r, want.executions)
+    # max body executions below the fixed point
+    n = max(1, want.executions - 3)
+    otree2 = sct.Pipeline([sct.Leaf("segment", {"lo": 173, "hi": 250}), sct.LoopWhileChanged(body, n)])
+    w2 = sct.evaluate(otree2, gray)
+    tree2 = M.mw_pipeline([M.mw_kernel_segment(173, 250), M.mw_loop_while_changed(mb, n, 1)])
+    for k, planes in ((1, 1), (3, 1), (2, 0)):
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(pctx(k, None, planes), tree2, [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), w2.value) and r["executions"] == n and not r["converged"]
+
+
+def test_loop_for_mixed_bodies():
+    """loop_for over bodies mixing kinds: the loop is its body unrolled (state
+    carried between executions), against the oracle's depth-first evaluation."""
+    H, W = 130, 170
+    gray = synth.np_u8_stream(8, 6, H * W).reshape(H, W)
+    lab = K.segment(gray, 173, 250)
+    cases = [
+        (sct.LoopFor(sct.Pipeline([sct.Leaf("segment", {"lo": 100, "hi": 200}),
+                                   sct.Leaf("hysteresis_step")]), 3),
+         M.mw_loop_for(M.mw_pipeline([M.mw_kernel_segment(100, 200), M.mw_kernel_hysteresis_step()]), 3),
+         gray),
+        (sct.LoopFor(sct.LoopWhileChanged(sct.Leaf("hysteresis_step"), 500), 2),
+         M.mw_loop_for(M.mw_loop_while_changed(M.mw_kernel_hysteresis_step(), 500), 2), lab),
+        (sct.LoopFor(sct.LoopFor(sct.Leaf("hysteresis_step"), 3), 4),
+         M.mw_loop_for(M.mw_loop_for(M.mw_kernel_hysteresis_step(), 3), 4), lab),
+    ]
+    for otree, tree, inp in cases:
+        want = sct.evaluate(otree, inp)
+        for k, d in ((1, None), (3, [0.2, 0.5, 0.3])):
+            dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+            r = run(ctx(k, d), tree, [M.arg(dev(inp)), M.arg(dst)])
+            assert np.array_equal(dst.cpu().numpy(), want.value)
+            assert r["executions"] == want.executions
+    # N-body loop over two steps of different dt (not merged: unrolled)
+    N = 700
+    pos, vel = synth.np_nbody(9, 0, N, 2.0 ** -9)
+    tree = M.mw_loop_for(M.mw_pipeline([M.mw_kernel_nbody_step(1e-3, 1e-4), M.mw_kernel_nbody_step(5e-4, 1e-4)]), 2)
+    p1, v1 = dev(pos), dev(vel)
+    run(ctx(2), tree, [M.arg(p1, M.MW_COPY), M.arg(v1, M.MW_COPY)])
+    p2, v2 = dev(pos), dev(vel)
+    c1 = ctx(1)
+    for _ in range(2):
+        run(c1, trees.nbody(1, dt=1e-3), [M.arg(p2, M.MW_COPY), M.arg(v2, M.MW_COPY)])
+        run(c1, trees.nbody(1, dt=5e-4), [M.arg(p2, M.MW_COPY), M.arg(v2, M.MW_COPY)])
+    assert torch.equal(p1, p2) and torch.equal(v1, v2)
+
+
+def test_mapreduce_fused_saxpy_map_stage():
+    """map_reduce(pipeline(saxpy chain, map_product)): the chain is fused into
+    the reduction kernel (y' never stored), against the oracle; the canonical
+    sum is bit-identical for every distribution and y is left untouched."""
+    n = 6 * (1 << 16) + 999
+    x = synth.np_f32_um11(5, 0, n)
+    y = synth.np_f32_um11(6, 0, n)
+    for chain in ([0.75], [2.5, -1.25, 0.5]):
+        otree = sct.MapReduce(sct.Pipeline([sct.Leaf("saxpy", {"a": a}) for a in chain] +
+                                           [sct.Leaf("map_product")]), "+")
+        want = sct.evaluate(otree, (x, y)).reduced
+        tree = M.mw_map_reduce(M.mw_pipeline([M.mw_kernel_saxpy(a) for a in chain] +
+                                             [M.mw_kernel_map_product()]))
+        got = []
+        for k, d in ((1, None), (3, [0.5, 0.1, 0.4]), (4, [0.0, 0.5, 0.25, 0.25])):
+            yd = dev(y)
+            got.append(run(ctx(k, d), tree, [M.arg(dev(x)), M.arg(yd)])["reduced"])
+            assert np.array_equal(yd.cpu().numpy(), y)
+        assert all(g == got[0] for g in got)
+        yp = y
+        for a in chain:
+            yp = K.saxpy(a, x, yp)
+        assert abs(got[0] - want) <= 1e-12 * K.abs_sum(x, yp)
+    # with the device reduction stage (max of the terms): bit-exact
+    tree = M.mw_map_reduce_sct(M.mw_pipeline([M.mw_kernel_saxpy(0.75), M.mw_kernel_map_product()]),
+                               M.mw_kernel_reduce(M.MW_REDUCE_MAX))
+    r = run(ctx(3, [0.3, 0.3, 0.4]), tree, [M.arg(dev(x)), M.arg(dev(y))])["reduced"]
+    assert r == (x.astype(np.float64) * K.saxpy(0.75, x, y).astype(np.float64)).max()

@@ -913,3 +913,49 @@ def test_loop_host_reduces_to_loop_for():
     r = sct.evaluate(sct.LoopHost(body, 2, lambda i: True), img)
     assert r.executions == 2 and not r.converged
     assert sct.kernel_execution_order(sct.LoopHost(body, 9, None), [2]) == [0, 1, 0, 1]
+
+
+# ----------------------------------------------------------------- composite map stage (general SCT composition)
+def test_mapreduce_composite_map_stage_closed_forms():
+    """map_reduce(pipeline(saxpy(a), map_product)): the map stage transforms
+    (x, y) -> (x, fma(a, x, y)) before the terms x * y' are formed (P:162,
+    P:191 map_reduce(SCT map_stage, ...)).  Pinned by closed forms that a
+    wrong composition (terms from y instead of y', the reduction before the
+    saxpy, a dropped fma) fails: a = 0 gives the pinned dot(x, y); y = 0 and
+    a = 1 give sum x^2 exactly (fractions); a = 2, y = -x give y' = x exactly."""
+    n = 3000
+    x = synth.np_f32_um11(31, 0, n)
+    y = synth.np_f32_um11(32, 0, n)
+    comp = lambda a: sct.MapReduce(sct.Pipeline([sct.Leaf("saxpy", {"a": a}),   # noqa: E731
+                                                 sct.Leaf("map_product")]), "+")
+    assert sct.sig(comp(1.0)) == (sct.SAXPY, "scalar")
+    assert sct.evaluate(comp(0.0), (x, y)).reduced == K.dot(x, y)
+    sq = sum(Fraction(float(v)) ** 2 for v in x)
+    z = np.zeros_like(x)
+    assert abs(Fraction(sct.evaluate(comp(1.0), (x, z)).reduced) - sq) <= sq * Fraction(1, 2 ** 52)
+    assert abs(Fraction(sct.evaluate(comp(2.0), (x, -x)).reduced) - sq) <= sq * Fraction(1, 2 ** 52)
+    # and the composition is not the plain dot when a != 0
+    assert sct.evaluate(comp(0.5), (x, y)).reduced != K.dot(x, y)
+
+
+def test_interpreter_reports_while_executions_through_composites():
+    """E (marrow.h out[2]) is the total of the while-loops' body executions
+    anywhere in the tree: through a pipeline (Fig. 1 shape) it is D + 1 of the
+    BFS depth (scipy-pinned hyst_bfs); a body of m steps changes iff one of its
+    steps does, so E_m = floor((D - 1) / m) + 2; loop_for(while, 2) adds one
+    more (an execution that changes nothing)."""
+    gray = synth.np_u8_stream(8, 2, 120 * 150).reshape(120, 150)
+    lab = K.segment(gray, 173, 250)
+    _, D = K.hyst_bfs(lab)
+    assert D >= 3
+    step = sct.Leaf("hysteresis_step")
+    fig1 = lambda body: sct.Pipeline([sct.Leaf("segment", {"lo": 173, "hi": 250}),   # noqa: E731
+                                      sct.LoopWhileChanged(body, 1000), sct.Leaf("hysteresis_finalize")])
+    assert sct.evaluate(fig1(step), gray).executions == D + 1
+    for m in (2, 3):
+        r = sct.evaluate(fig1(sct.Pipeline([step] * m)), gray)
+        assert r.executions == (D - 1) // m + 2 and r.converged
+        r2 = sct.evaluate(fig1(sct.LoopFor(step, m)), gray)
+        assert r2.executions == r.executions and np.array_equal(r2.value, r.value)
+    r = sct.evaluate(sct.LoopFor(sct.LoopWhileChanged(step, 1000), 2), lab)
+    assert r.executions == D + 2

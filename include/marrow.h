@@ -203,7 +203,9 @@ mw_status mw_loop_while_changed(mw_node* body, int64_t max_iters, int32_t check_
  * read or write host state (stage 3).  Iteration i reads the previous
  * iteration's output (ping-pong; src -> dst for i = 0), so a body of k
  * iterations equals loop_for(body, k).  Executions are reported like
- * LoopWhileChanged's.  Root-only (nested: MW_E_UNSUPPORTED); not capturable.
+ * LoopWhileChanged's.  The root, or one stage of a root pipeline (the stages
+ * before it run into an intermediate buffer, the ones after it from its
+ * output; deeper nesting: MW_E_UNSUPPORTED); not capturable.
  * mw_run returns after the last condition evaluation.                        */
 typedef int32_t (*mw_loop_cond_fn)(int64_t iteration, void* user);
 mw_status mw_loop_host(mw_node* body, int64_t max_iters, mw_loop_cond_fn cond, void* user,

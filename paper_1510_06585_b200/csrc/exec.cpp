@@ -1252,9 +1252,22 @@ bool run_independent(const mw_ctx* c, const mw_arg* args, int nargs) {
 mw_status run_loop_host(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
                         mw_future* f);
 
+mw_status run_split_host(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
+                         mw_future* f, int h);
+
+// index of the host-condition loop among a pipeline root's stages (-1: none)
+int host_stage(const Node* root) {
+    if (root->type != mw::NodeType::Pipeline) return -1;
+    for (size_t i = 0; i < root->kids.size(); ++i)
+        if (root->kids[i]->type == mw::NodeType::LoopHost) return (int)i;
+    return -1;
+}
+
 mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
               mw_future* f) {
+    while (root->type == mw::NodeType::Map) root = root->kids[0];   // Map(t) runs t
     if (root->type == mw::NodeType::LoopHost) return run_loop_host(c, root, args, nargs, s, f);
+    if (const int h = host_stage(root); h >= 0) return run_split_host(c, root, args, nargs, s, f, h);
     mw_status pst;
     const mw::NodeCache* nc = mw::plan_cached(root, &pst);
     if (!nc) return pst;
@@ -1561,6 +1574,85 @@ mw_status run_loop_host(mw_ctx* c, const Node* root, const mw_arg* args, int nar
                                 tbytes, cudaMemcpyDeviceToDevice, s));
     f->executions += (double)E;
     if (!stopped) f->converged = 0.0;
+    return MW_OK;
+}
+
+// A pipeline with a host-condition loop among its stages (NEXT-4, the Fig. 1
+// shape with the paper's host-side loop stages P:374-378): the stages before
+// the loop run as one fused sub-pipeline into an intermediate buffer, the
+// loop ping-pongs on the device with its condition on the host, the stages
+// after it run from its output into the destination.  In-place value kinds
+// (saxpy, N-body) run every part on the arguments themselves.
+mw_status run_split_host(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaStream_t s,
+                         mw_future* f, int h) {
+    if (c->capturing)
+        return fail(MW_E_UNSUPPORTED, "a host-condition loop evaluates its condition on the host "
+                                      "and cannot be captured in a graph");
+    const std::vector<Node*>& kids = root->kids;
+    for (size_t i = 0; i < kids.size(); ++i)
+        if ((int)i != h && host_stage(kids[i]) >= 0)
+            return fail(MW_E_UNSUPPORTED, "one host-condition loop per pipeline");
+    // the stages before / after the loop as nodes (a transient pipeline when
+    // there are several: the tree itself stays immutable)
+    auto part = [&](size_t b, size_t e, mw_node** out) -> mw_status {
+        *out = nullptr;
+        if (e <= b) return MW_OK;
+        if (e - b == 1) {
+            *out = reinterpret_cast<mw_node*>(kids[b]);
+            mw_node_retain(*out);
+            return MW_OK;
+        }
+        std::vector<mw_node*> st;
+        for (size_t i = b; i < e; ++i) st.push_back(reinterpret_cast<mw_node*>(kids[i]));
+        return mw_pipeline(st.data(), (int32_t)st.size(), out);
+    };
+    mw_node *pre = nullptr, *post = nullptr;
+    MW_OK_OR_RETURN(part(0, (size_t)h, &pre));
+    mw_status st = part((size_t)h + 1, kids.size(), &post);
+    if (st != MW_OK) {
+        if (pre) mw_node_release(pre);
+        return st;
+    }
+    struct Rel {
+        mw_node* n;
+        ~Rel() {
+            if (n) mw_node_release(n);
+        }
+    } rp{pre}, rq{post};
+    const Node* loop = kids[h];
+    const int ik = root->in_kind;
+    const bool two = nargs == 2 && (ik == MW_VK_RGBA || ik == MW_VK_U8 || ik == MW_VK_U8_2D || ik == MW_VK_CPLX);
+    if (!two) {   // in place: every part on the same arguments, in order
+        if (pre) MW_OK_OR_RETURN(run(c, reinterpret_cast<const Node*>(pre), args, nargs, s, f));
+        MW_OK_OR_RETURN(run_loop_host(c, loop, args, nargs, s, f));
+        if (post) MW_OK_OR_RETURN(run(c, reinterpret_cast<const Node*>(post), args, nargs, s, f));
+        return MW_OK;
+    }
+    // intermediates: this rank's rows, the destination's shape
+    const size_t bytes = (size_t)std::max<int64_t>(16, args[1].local_rows * row_bytes(args[1]));
+    auto tmp_arg = [&](const char* name, mw_arg* out) -> mw_status {
+        void* p;
+        MW_OK_OR_RETURN(scratch(c, name, bytes, s, &p));
+        *out = args[1];
+        out->ptr = p;
+        out->location = MW_LOC_DEVICE;
+        return MW_OK;
+    };
+    mw_arg a_in = args[0], a_mid, a_out;
+    if (pre) {
+        MW_OK_OR_RETURN(tmp_arg("split_pre", &a_mid));
+        const mw_arg pa[2] = {args[0], a_mid};
+        MW_OK_OR_RETURN(run(c, reinterpret_cast<const Node*>(pre), pa, 2, s, f));
+        a_in = a_mid;
+    }
+    if (post) MW_OK_OR_RETURN(tmp_arg("split_post", &a_out));
+    else a_out = args[1];
+    const mw_arg la[2] = {a_in, a_out};
+    MW_OK_OR_RETURN(run_loop_host(c, loop, la, 2, s, f));
+    if (post) {
+        const mw_arg qa[2] = {a_out, args[1]};
+        MW_OK_OR_RETURN(run(c, reinterpret_cast<const Node*>(post), qa, 2, s, f));
+    }
     return MW_OK;
 }
 

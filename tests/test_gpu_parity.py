@@ -961,9 +961,12 @@ def test_loop_host_condition():
     with torch.cuda.stream(s):
         with pytest.raises(M.MwError):
             M.mw_graph_capture(ctx(1), M.mw_loop_host(trees.saxpy(0.5), 3, lambda i: True), [M.arg(x), M.arg(y)], s)
-    with pytest.raises(M.MwError):
-        run(ctx(1), M.mw_pipeline([M.mw_loop_host(M.mw_kernel_mirror(), 2, lambda i: True), M.mw_kernel_mirror()]),
-            [M.arg(src), M.arg(torch.empty_like(src))])
+    # a host loop as a pipeline stage runs (test_host_condition_loop_inside_a_pipeline):
+    # mirror twice in the loop, once after it = one mirror
+    out = torch.empty_like(src)
+    r = run(ctx(1), M.mw_pipeline([M.mw_loop_host(M.mw_kernel_mirror(), 2, lambda i: True), M.mw_kernel_mirror()]),
+            [M.arg(src), M.arg(out)])
+    assert np.array_equal(out.cpu().numpy(), K.mirror(src.cpu().numpy())) and r["executions"] == 2
 
 
 def test_released_futures_and_arglist():
@@ -1191,3 +1194,58 @@ def test_mapreduce_fused_saxpy_map_stage():
                                M.mw_kernel_reduce(M.MW_REDUCE_MAX))
     r = run(ctx(3, [0.3, 0.3, 0.4]), tree, [M.arg(dev(x)), M.arg(dev(y))])["reduced"]
     assert r == (x.astype(np.float64) * K.saxpy(0.75, x, y).astype(np.float64)).max()
+
+
+def test_host_condition_loop_inside_a_pipeline():
+    """pipeline(..., loop_host(body, cond), ...): the Fig. 1 shape with the
+    paper's host-side loop condition as a stage, not the root."""
+    H, W = 140, 190
+    gray = synth.np_u8_stream(8, 11, H * W).reshape(H, W)
+    calls = []
+
+    def cond(i):
+        calls.append(i)
+        return i < 6
+
+    otree = sct.Pipeline([sct.Leaf("segment", {"lo": 173, "hi": 250}),
+                          sct.LoopHost(sct.Leaf("hysteresis_step"), 100, cond=lambda i: i < 6),
+                          sct.Leaf("hysteresis_finalize")])
+    want = sct.evaluate(otree, gray)
+    tree = M.mw_pipeline([M.mw_kernel_segment(173, 250),
+                          M.mw_loop_host(M.mw_kernel_hysteresis_step(), 100, cond),
+                          M.mw_kernel_hysteresis_finalize()])
+    for k, d in ((1, None), (3, [0.3, 0.0, 0.7])):
+        calls.clear()
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(ctx(k, d), tree, [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want.value)
+        assert r["executions"] == want.executions == 6 and r["converged"] and calls == list(range(7))
+    # RGBA: the loop between two fused chains; loop first / last
+    img = synth.np_rgba(3, 0, 33 * 64).reshape(33, 64, 4)
+    for pre, post in (([M.mw_kernel_gauss_noise(4, 8)], [M.mw_kernel_mirror()]), ([], [M.mw_kernel_mirror()]),
+                      ([M.mw_kernel_gauss_noise(4, 8), M.mw_kernel_mirror()], [])):
+        tree = M.mw_pipeline(pre + [M.mw_loop_host(M.mw_kernel_solarize(100), 10, lambda i: i < 3)] + post)
+        v = img
+        if pre:
+            v = K.gauss_noise(v, 4, 8)
+            if len(pre) == 2:
+                v = K.mirror(v)
+        for _ in range(3):
+            v = K.solarize(v, 100)
+        if post:
+            v = K.mirror(v)
+        dst = torch.empty_like(dev(img))
+        r = run(ctx(2, [0.6, 0.4]), tree, [M.arg(dev(img)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), v) and r["executions"] == 3
+    # in place (saxpy): every part on the same arguments
+    n = 4099
+    x = synth.np_f32_um11(1, 0, n)
+    y0 = synth.np_f32_um11(2, 0, n)
+    yd = dev(y0)
+    tree = M.mw_pipeline([M.mw_kernel_saxpy(0.5), M.mw_loop_host(M.mw_kernel_saxpy(0.25), 10, lambda i: i < 4),
+                          M.mw_kernel_saxpy(2.0)])
+    run(ctx(2), tree, [M.arg(dev(x)), M.arg(yd)])
+    want = K.saxpy(0.5, x, y0)
+    for _ in range(4):
+        want = K.saxpy(0.25, x, want)
+    assert np.array_equal(yd.cpu().numpy(), K.saxpy(2.0, x, want))

@@ -180,13 +180,26 @@ mw_status mw_map_reduce(mw_node* map_stage, int32_t merge_op, mw_node** out);   
 /* User-defined merging function (called on the host thread that waits on the
  * future; fn must not call back into libmarrow).                           */
 mw_status mw_map_reduce_user(mw_node* map_stage, mw_merge_fn fn, void* user, mw_node** out);
-/* MapReduce with a device reduction stage (an mw_kernel_reduce leaf; NEXT-4,
- * P:191): the map stage's terms are reduced on the device, partition
- * partials merged with the same operator across ranks (NCCL all-reduce).
- * Result as for mw_map_reduce (mw_future_result out[0] fp64, out[1] fp32).
- * reduction_stage not a reduce leaf, or map_stage not producing terms:
- * MW_E_INVALID_SPEC.                                                        */
+/* MapReduce with a device reduction stage (an mw_kernel_reduce leaf, or the
+ * reduction-stage SCT below; NEXT-4): the map stage's terms are
+ * reduced on the device, partition partials merged with the same operator
+ * across ranks (NCCL all-reduce).  Result as for mw_map_reduce
+ * (mw_future_result out[0] fp64, out[1] fp32).  A reduction stage that is
+ * not such a tree, or a map_stage not producing terms: MW_E_INVALID_SPEC.  */
 mw_status mw_map_reduce_sct(mw_node* map_stage, mw_node* reduction_stage, mw_node** out);
+/* Reduction-stage SCT leaves (NEXT-4, P:191 map_reduce(SCT, SCT) with the
+ * reduction placed on the device).  The reduction stage of
+ * mw_map_reduce_sct may be pipeline(term maps..., mw_kernel_reduce(op),
+ * scalar maps...): a term map applies to every fp64 term before the fold
+ * (ABS: |t|, SQUARE: t*t in fp64, exact for identity terms), a scalar map to
+ * the reduced fp64 value after the merge (SQRT, SCALE by c).  E.g. the L2
+ * norm = map_reduce_sct(map_identity, pipeline(term_map(SQUARE),
+ * reduce(SUM), scalar_map(SQRT))).  Fused into the reduction kernels (term
+ * maps) and its combine (scalar maps).  Unknown kind: MW_E_INVALID_SPEC.   */
+enum { MW_TERM_ABS = 0, MW_TERM_SQUARE = 1 };
+enum { MW_SCALAR_SQRT = 0, MW_SCALAR_SCALE = 1 };
+mw_status mw_kernel_term_map(int32_t kind, mw_node** out);
+mw_status mw_kernel_scalar_map(int32_t kind, double c, mw_node** out);
 mw_status mw_loop_for(mw_node* body, int64_t n, mw_node** out);           /* n >= 0 */
 /* while(changed && executions < max_iters) body.
  * The stop condition is evaluated on the device and reduced across ranks

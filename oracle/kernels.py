@@ -40,6 +40,7 @@ def lib():
             "orc_dot": (f64, [i64, vp, vp]),
             "orc_abs_sum": (f64, [i64, vp, vp]),
             "orc_fold_extreme": (f64, [i64, vp, vp, i32]),
+            "orc_sum_f64": (f64, [i64, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -193,3 +194,9 @@ def abs_sum(x, y=None):
     if y is not None:
         y = _c(y, np.float32)
     return float(lib().orc_abs_sum(x.size, _p(x), _p(y)))
+
+
+def sum_f64(t):
+    """Serial Neumaier fold of fp64 terms (reduction stage with term maps)."""
+    t = _c(t, np.float64)
+    return float(lib().orc_sum_f64(t.size, _p(t)))

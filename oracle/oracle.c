@@ -287,3 +287,12 @@ double orc_abs_sum(int64_t n, const float* x, const float* y) {
         neumaier_add(&s, &c, fabs(y ? (double)x[i] * (double)y[i] : (double)x[i]));
     return s + c;
 }
+
+/* Reduction-stage SCT with term maps (NEXT-4, R28): the
+ * serial Neumaier fp64 fold of already formed fp64 terms (the same fold as
+ * orc_sum / orc_dot, whose terms are formed from fp32 inputs).             */
+double orc_sum_f64(int64_t n, const double* t) {
+    double s = 0.0, c = 0.0;
+    for (int64_t i = 0; i < n; ++i) neumaier_add(&s, &c, t[i]);
+    return s + c;
+}

@@ -53,6 +53,8 @@ LEAF_SIG = {
     "debug_traits": (TRAITS, TRAITS),
     "fft": (CPLX, CPLX),
     "reduce": (TERMS, "scalar"),
+    "term_map": (TERMS, TERMS),        # reduction-stage SCT: |t| or t*t before the fold
+    "scalar_map": ("scalar", "scalar"),  # reduction-stage SCT: sqrt or scale of the result
 }
 
 
@@ -252,14 +254,34 @@ def evaluate(node: Node, value, while_counts=None, lengths=None) -> Result:
             return K.dot(vals[0][sl], vals[1][sl])
         if node.op == "+":
             return Result(None, reduced=red(slice(None)))
-        if isinstance(node.op, Leaf):          # device reduction stage
-            if node.op.kind != "reduce":
-                raise ValueError("the reduction stage must be a reduce leaf")
-            rop = node.op.params.get("op", "sum")
-            if rop == "sum":
-                return Result(None, reduced=red(slice(None)))
+        if isinstance(node.op, (Leaf, Pipeline)):   # device reduction stage SCT
+            stages = [node.op] if isinstance(node.op, Leaf) else list(node.op.stages)
+            kinds = [st.kind for st in stages]
+            if kinds.count("reduce") != 1:
+                raise ValueError("the reduction stage needs exactly one reduce leaf")
+            r = kinds.index("reduce")
+            rop = stages[r].params.get("op", "sum")
+            tmaps = [st.params["map"] for st in stages[:r]]
             y = vals[1] if m.kind == "map_product" else None
-            return Result(None, reduced=K.fold_extreme(vals[0], y, is_min=(rop == "min")))
+            if not tmaps:
+                if rop == "sum":
+                    acc = red(slice(None))
+                else:
+                    acc = K.fold_extreme(vals[0], y, is_min=(rop == "min"))
+            else:
+                # the terms in fp64 (x, or x*y exact), then the term maps in order
+                t = vals[0].astype(np.float64) * (y.astype(np.float64) if y is not None else 1.0)
+                for tm in tmaps:
+                    t = np.abs(t) if tm == "abs" else t * t
+                if rop == "sum":
+                    acc = K.sum_f64(t)
+                else:   # maxNum / minNum: NaN terms ignored, empty -> the identity
+                    t = t[~np.isnan(t)]
+                    acc = (float(t.min()) if t.size else np.inf) if rop == "min" else \
+                          (float(t.max()) if t.size else -np.inf)
+            for st in stages[r + 1:]:    # scalar maps of the reduced value, in order
+                acc = float(np.sqrt(acc)) if st.params["map"] == "sqrt" else acc * st.params["c"]
+            return Result(None, reduced=acc)
         if lengths is None:
             raise ValueError("merging functions other than + need the partition lengths")
         parts, o = [], 0
@@ -350,5 +372,5 @@ def _children(n):
     if isinstance(n, Map):
         return [n.tree]
     if isinstance(n, MapReduce):   # a reduction-stage SCT runs after the map stage
-        return [n.map_stage] + ([n.op] if isinstance(n.op, Leaf) else [])
+        return [n.map_stage] + ([n.op] if isinstance(n.op, (Leaf, Pipeline)) else [])
     return [n.body]

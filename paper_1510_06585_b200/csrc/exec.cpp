@@ -1452,7 +1452,8 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
             MW_OK_OR_RETURN(kerr(mwk::reduce_chunks(at_row<const float>(args[0], R.off[p]),
                                                     dot ? at_row<const float>(args[1], R.off[p]) : nullptr,
                                                     R.off[p], R.off[p], R.len[p], L, partials,
-                                                    launch_for(c, s, p), rop, pre.n ? &pre : nullptr),
+                                                    launch_for(c, s, p), rop, pre.n ? &pre : nullptr,
+                                                    prog[0].term_map),
                                  "reduce_chunks"));
         }
         // merge "+" across ranks: each chunk partial has exactly
@@ -1465,7 +1466,13 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
                                                                       : mwc::ROp::Sum,
                                                s));
         if (prog[0].merge_op == MW_MERGE_ADD) {
-            MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s, rop),
+            mwk::ScalarPost post{};
+            if (prog[0].post.size() > 8) return fail(MW_E_UNSUPPORTED, "more than 8 scalar maps");
+            for (const auto& pm : prog[0].post) {
+                post.kind[post.n] = pm.first;
+                post.c[post.n++] = pm.second;
+            }
+            MW_OK_OR_RETURN(kerr(mwk::reduce_combine(partials, nch, static_cast<double*>(rp), s, rop, &post),
                                  "reduce_combine"));
             CUDA_OK(cudaMemcpyAsync(f->res, rp, 8, cudaMemcpyDeviceToHost, s));
         } else {

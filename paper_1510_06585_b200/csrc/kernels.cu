@@ -1825,11 +1825,17 @@ template <int OP>
 __device__ __forceinline__ double red_id() {
     return OP == 0 ? 0.0 : (OP == 1 ? -CUDART_INF : CUDART_INF);
 }
-// one term into the accumulator: sum folds with an fma for products
-template <int OP, bool DOT>
+// one term into the accumulator: sum folds with an fma for products; TM
+// (reduction-stage term map): 0 none, 1 |t|, 2 t*t (fp64) before the fold
+template <int OP, bool DOT, int TM = 0>
 __device__ __forceinline__ double red_term(double acc, float a, float b) {
-    if constexpr (OP == 0) return DOT ? __fma_rn((double)a, (double)b, acc) : acc + (double)a;
-    else return red_op<OP>(acc, DOT ? (double)a * (double)b : (double)a);
+    if constexpr (TM == 0) {
+        if constexpr (OP == 0) return DOT ? __fma_rn((double)a, (double)b, acc) : acc + (double)a;
+        else return red_op<OP>(acc, DOT ? (double)a * (double)b : (double)a);
+    } else {
+        const double t = DOT ? (double)a * (double)b : (double)a;
+        return red_op<OP>(acc, TM == 1 ? fabs(t) : t * t);
+    }
 }
 
 // PRE: the map stage is pipeline(saxpy chain, map_product) fused into the
@@ -1842,7 +1848,7 @@ __device__ __forceinline__ float pre_y(const SaxpyProg& pre, float x, float y) {
     return y;
 }
 
-template <bool DOT, int OP, bool PRE = false>
+template <bool DOT, int OP, bool PRE = false, int TM = 0>
 __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __restrict__ x,
                                                                const float* __restrict__ y,
                                                                int64_t x0, int64_t first_chunk,
@@ -1873,10 +1879,10 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
                 if (DOT) b = ld_stream(yv + k * kRedThreads + threadIdx.x);
                 const float ax = __uint_as_float(a.x), ay = __uint_as_float(a.y);
                 const float az = __uint_as_float(a.z), aw = __uint_as_float(a.w);
-                acc4[0] = red_term<OP, DOT>(acc4[0], ax, pre_y<PRE>(pre, ax, __uint_as_float(b.x)));
-                acc4[1] = red_term<OP, DOT>(acc4[1], ay, pre_y<PRE>(pre, ay, __uint_as_float(b.y)));
-                acc4[2] = red_term<OP, DOT>(acc4[2], az, pre_y<PRE>(pre, az, __uint_as_float(b.z)));
-                acc4[3] = red_term<OP, DOT>(acc4[3], aw, pre_y<PRE>(pre, aw, __uint_as_float(b.w)));
+                acc4[0] = red_term<OP, DOT, TM>(acc4[0], ax, pre_y<PRE>(pre, ax, __uint_as_float(b.x)));
+                acc4[1] = red_term<OP, DOT, TM>(acc4[1], ay, pre_y<PRE>(pre, ay, __uint_as_float(b.y)));
+                acc4[2] = red_term<OP, DOT, TM>(acc4[2], az, pre_y<PRE>(pre, az, __uint_as_float(b.z)));
+                acc4[3] = red_term<OP, DOT, TM>(acc4[3], aw, pre_y<PRE>(pre, aw, __uint_as_float(b.w)));
             }
         } else {
             for (int k = 0; k < (int)(CH / 4 / kRedThreads); ++k) {
@@ -1884,8 +1890,8 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
                 for (int e = 0; e < 4; ++e) {
                     int64_t i = ((int64_t)k * kRedThreads + threadIdx.x) * 4 + e;
                     if (i < len)
-                        acc4[e] = red_term<OP, DOT>(acc4[e], x[base + i],
-                                                    DOT ? pre_y<PRE>(pre, x[base + i], y[base + i]) : 0.f);
+                        acc4[e] = red_term<OP, DOT, TM>(acc4[e], x[base + i],
+                                                        DOT ? pre_y<PRE>(pre, x[base + i], y[base + i]) : 0.f);
                 }
             }
         }
@@ -1906,7 +1912,8 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const float* __re
 
 template <int OP>
 __global__ void __launch_bounds__(1024) k_reduce_combine(const double* __restrict__ partials,
-                                                         int64_t n, double* __restrict__ result) {
+                                                         int64_t n, double* __restrict__ result,
+                                                         const __grid_constant__ ScalarPost post) {
     __shared__ double wp[32];
     double acc = red_id<OP>();
     for (int64_t i = threadIdx.x; i < n; i += 1024) acc = red_op<OP>(acc, partials[i]);
@@ -1918,6 +1925,8 @@ __global__ void __launch_bounds__(1024) k_reduce_combine(const double* __restric
         double s = wp[threadIdx.x];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s = red_op<OP>(s, __shfl_xor_sync(0xffffffffu, s, o));
+        // reduction-stage scalar maps of the reduced value, in order
+        for (int k = 0; k < post.n; ++k) s = post.kind[k] == 0 ? sqrt(s) : s * post.c[k];
         if (threadIdx.x == 0) *result = s;
     }
 }
@@ -2705,54 +2714,59 @@ cudaError_t nbody(const float4* pos, const float4* vel, float4* pos_out, float4*
     return cudaGetLastError();
 }
 
-template <bool DOT, int OP>
+template <bool DOT, int OP, bool PRE, int TM>
 static void reduce_chunks_t(const float* x, const float* y, int64_t x0, int64_t c0, int64_t nc,
-                            int64_t total, double* partials, const Launch& L,
-                            const SaxpyProg* pre = nullptr) {
+                            int64_t total, double* partials, const Launch& L, const SaxpyProg& pre) {
+    static int occ = resident_ctas(k_reduce_chunks<DOT, OP, PRE, TM>, kRedThreads);
     ++g_launches;
-    if (DOT && pre && pre->n > 0) {
-        static int occp = resident_ctas(k_reduce_chunks<DOT, OP, true>, kRedThreads);
-        k_reduce_chunks<DOT, OP, true><<<grid_for(nc, occp, L), kRedThreads, 0, L.stream>>>(
-            x, y, x0, c0, nc, total, partials, *pre);
+    k_reduce_chunks<DOT, OP, PRE, TM><<<grid_for(nc, occ, L), kRedThreads, 0, L.stream>>>(
+        x, y, x0, c0, nc, total, partials, pre);
+}
+template <bool DOT, int OP>
+static void reduce_chunks_tm(const float* x, const float* y, int64_t x0, int64_t c0, int64_t nc,
+                             int64_t total, double* partials, const Launch& L, const SaxpyProg* pre,
+                             int tm) {
+    if (DOT && pre && pre->n > 0) {   // fused saxpy map stage: no term map combination needed
+        if (tm == 0) reduce_chunks_t<DOT, OP, true, 0>(x, y, x0, c0, nc, total, partials, L, *pre);
+        else if (tm == 1) reduce_chunks_t<DOT, OP, true, 1>(x, y, x0, c0, nc, total, partials, L, *pre);
+        else reduce_chunks_t<DOT, OP, true, 2>(x, y, x0, c0, nc, total, partials, L, *pre);
         return;
     }
-    static int occ = resident_ctas(k_reduce_chunks<DOT, OP>, kRedThreads);
-    k_reduce_chunks<DOT, OP><<<grid_for(nc, occ, L), kRedThreads, 0, L.stream>>>(x, y, x0, c0, nc, total, partials,
-                                                                                 SaxpyProg{});
+    const SaxpyProg none{};
+    if (tm == 0) reduce_chunks_t<DOT, OP, false, 0>(x, y, x0, c0, nc, total, partials, L, none);
+    else if (tm == 1) reduce_chunks_t<DOT, OP, false, 1>(x, y, x0, c0, nc, total, partials, L, none);
+    else reduce_chunks_t<DOT, OP, false, 2>(x, y, x0, c0, nc, total, partials, L, none);
 }
 
 cudaError_t reduce_chunks(const float* x, const float* y, int64_t x0, int64_t first,
                           int64_t count, int64_t total, double* partials, const Launch& L,
-                          int op, const SaxpyProg* pre) {
+                          int op, const SaxpyProg* pre, int term_map) {
     if (count <= 0) return cudaSuccess;
     const int64_t CH = 1ll << kChunkLog2;
-    if (first % CH != 0 || op < 0 || op > 2 || (pre && pre->n > 0 && !y)) return cudaErrorInvalidValue;
+    if (first % CH != 0 || op < 0 || op > 2 || term_map < -1 || term_map > 1 ||
+        (pre && pre->n > 0 && !y))
+        return cudaErrorInvalidValue;
+    const int tm = term_map + 1;
     int64_t c0 = first / CH, nc = (count + CH - 1) / CH;
-    if (pre && pre->n > 0) {
-        switch (op) {
-            case 0: reduce_chunks_t<true, 0>(x, y, x0, c0, nc, total, partials, L, pre); break;
-            case 1: reduce_chunks_t<true, 1>(x, y, x0, c0, nc, total, partials, L, pre); break;
-            default: reduce_chunks_t<true, 2>(x, y, x0, c0, nc, total, partials, L, pre); break;
-        }
-        return cudaGetLastError();
-    }
     switch (op * 2 + (y ? 1 : 0)) {
-        case 0: reduce_chunks_t<false, 0>(x, y, x0, c0, nc, total, partials, L); break;
-        case 1: reduce_chunks_t<true, 0>(x, y, x0, c0, nc, total, partials, L); break;
-        case 2: reduce_chunks_t<false, 1>(x, y, x0, c0, nc, total, partials, L); break;
-        case 3: reduce_chunks_t<true, 1>(x, y, x0, c0, nc, total, partials, L); break;
-        case 4: reduce_chunks_t<false, 2>(x, y, x0, c0, nc, total, partials, L); break;
-        default: reduce_chunks_t<true, 2>(x, y, x0, c0, nc, total, partials, L); break;
+        case 0: reduce_chunks_tm<false, 0>(x, y, x0, c0, nc, total, partials, L, pre, tm); break;
+        case 1: reduce_chunks_tm<true, 0>(x, y, x0, c0, nc, total, partials, L, pre, tm); break;
+        case 2: reduce_chunks_tm<false, 1>(x, y, x0, c0, nc, total, partials, L, pre, tm); break;
+        case 3: reduce_chunks_tm<true, 1>(x, y, x0, c0, nc, total, partials, L, pre, tm); break;
+        case 4: reduce_chunks_tm<false, 2>(x, y, x0, c0, nc, total, partials, L, pre, tm); break;
+        default: reduce_chunks_tm<true, 2>(x, y, x0, c0, nc, total, partials, L, pre, tm); break;
     }
     return cudaGetLastError();
 }
 
 cudaError_t reduce_combine(const double* partials, int64_t nchunks, double* result,
-                           cudaStream_t s, int op) {
+                           cudaStream_t s, int op, const ScalarPost* post) {
     ++g_launches;
-    if (op == 1) k_reduce_combine<1><<<1, 1024, 0, s>>>(partials, nchunks, result);
-    else if (op == 2) k_reduce_combine<2><<<1, 1024, 0, s>>>(partials, nchunks, result);
-    else k_reduce_combine<0><<<1, 1024, 0, s>>>(partials, nchunks, result);
+    const ScalarPost none{};
+    const ScalarPost& ps = post ? *post : none;
+    if (op == 1) k_reduce_combine<1><<<1, 1024, 0, s>>>(partials, nchunks, result, ps);
+    else if (op == 2) k_reduce_combine<2><<<1, 1024, 0, s>>>(partials, nchunks, result, ps);
+    else k_reduce_combine<0><<<1, 1024, 0, s>>>(partials, nchunks, result, ps);
     return cudaGetLastError();
 }
 

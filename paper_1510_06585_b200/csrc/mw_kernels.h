@@ -186,12 +186,20 @@ constexpr int kChunkLog2 = 16;      // canonical reduction chunk: 2^16 elements
 // op: MW_REDUCE_* (0 sum, 1 maxNum, 2 minNum).
 // pre (dot only): the map stage is pipeline(saxpy chain, map_product): the
 // terms are x * y' with y' = fma(pre.a[k], x, y) applied in order in fp32.
+// term_map (reduction-stage term map, MW_TERM_*; -1 none) applies to every
+// fp64 term before the fold.
 cudaError_t reduce_chunks(const float* x, const float* y, int64_t x0, int64_t first,
                           int64_t count, int64_t total, double* partials, const Launch& L,
-                          int op = 0, const SaxpyProg* pre = nullptr);
-// Fixed-tree combine of nchunks partials into *result (one CTA).
+                          int op = 0, const SaxpyProg* pre = nullptr, int term_map = -1);
+// Fixed-tree combine of nchunks partials into *result (one CTA), then the
+// reduction-stage scalar maps (kind 0 sqrt, 1 scale by c) in order.
+struct ScalarPost {
+    int n;
+    int kind[8];
+    double c[8];
+};
 cudaError_t reduce_combine(const double* partials, int64_t nchunks, double* result,
-                           cudaStream_t s, int op = 0);
+                           cudaStream_t s, int op = 0, const ScalarPost* post = nullptr);
 // partials[0..n) = the operator's identity (0, -inf, +inf)
 cudaError_t reduce_fill_identity(double* partials, int64_t n, cudaStream_t s, int op);
 

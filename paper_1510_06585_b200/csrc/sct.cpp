@@ -54,6 +54,8 @@ static const char* leaf_name(LeafKind k) {
         case LeafKind::DebugTraits: return "debug_traits";
         case LeafKind::Fft: return "fft";
         case LeafKind::Reduce: return "reduce";
+        case LeafKind::TermMap: return "term_map";
+        case LeafKind::ScalarMap: return "scalar_map";
     }
     return "?";
 }
@@ -179,6 +181,8 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
             case LeafKind::MapProduct: s.kind = StepKind::MapStage; s.dot = true; break;
             case LeafKind::Fft: s.kind = StepKind::Fft; s.ops = {op}; break;
             case LeafKind::Reduce:
+            case LeafKind::TermMap:
+            case LeafKind::ScalarMap:
                 return fail(MW_E_INVALID_SPEC, "a reduction stage runs only inside mw_map_reduce_sct");
             case LeafKind::DebugTraits:
                 s.kind = StepKind::Traits;
@@ -223,7 +227,24 @@ mw_status plan(const Node* n, std::vector<Step>* out) {
             s.pre = pre;
             s.dot = a[0].dot;
             s.merge_op = n->merge_op;
-            s.reduce_op = n->kids.size() > 1 ? (int32_t)n->kids[1]->ia : MW_REDUCE_SUM;
+            s.reduce_op = MW_REDUCE_SUM;
+            if (n->kids.size() > 1) {
+                // the reduction stage SCT: term maps, one reduce, scalar maps
+                // (validated by mw_map_reduce_sct); composed term maps collapse
+                // (abs o square = square o abs = square, abs o abs = abs, ...)
+                for (const Node* l : leaves(n->kids[1])) {
+                    if (l->leaf == LeafKind::TermMap) {
+                        const int t = (int)l->ia;
+                        s.term_map = s.term_map == MW_TERM_SQUARE || t == MW_TERM_SQUARE ? MW_TERM_SQUARE : t;
+                    } else if (l->leaf == LeafKind::Reduce) {
+                        s.reduce_op = (int32_t)l->ia;
+                    } else if (l->leaf == LeafKind::ScalarMap) {
+                        double c;
+                        memcpy(&c, &l->ib, sizeof c);
+                        s.post.push_back({(int32_t)l->ia, c});
+                    }
+                }
+            }
             s.fn = n->fn;
             s.user = n->user;
             out->push_back(s);
@@ -692,11 +713,35 @@ mw_status mw_kernel_reduce(int32_t op, mw_node** out) {
     if (op < MW_REDUCE_SUM || op > MW_REDUCE_MIN) return fail(MW_E_INVALID_SPEC, "unknown reduction operator");
     return make_leaf(LeafKind::Reduce, MW_VK_TERMS, MW_VK_SCALAR, out, 0, 0, op);
 }
+mw_status mw_kernel_term_map(int32_t kind, mw_node** out) {
+    if (kind != MW_TERM_ABS && kind != MW_TERM_SQUARE) return fail(MW_E_INVALID_SPEC, "unknown term map");
+    return make_leaf(LeafKind::TermMap, MW_VK_TERMS, MW_VK_TERMS, out, 0, 0, kind);
+}
+mw_status mw_kernel_scalar_map(int32_t kind, double c, mw_node** out) {
+    if (kind != MW_SCALAR_SQRT && kind != MW_SCALAR_SCALE) return fail(MW_E_INVALID_SPEC, "unknown scalar map");
+    if (kind == MW_SCALAR_SCALE && !std::isfinite(c)) return fail(MW_E_INVALID_SPEC, "scale must be finite");
+    if (kind == MW_SCALAR_SQRT) c = 0.0;
+    int64_t bits;
+    memcpy(&bits, &c, sizeof bits);
+    return make_leaf(LeafKind::ScalarMap, MW_VK_SCALAR, MW_VK_SCALAR, out, 0, 0, kind, bits);
+}
 mw_status mw_map_reduce_sct(mw_node* map_stage, mw_node* reduction_stage, mw_node** out) {
     if (!reduction_stage) return fail(MW_E_INVALID_SPEC, "NULL reduction stage");
     const Node* r = reinterpret_cast<const Node*>(reduction_stage);
-    if (r->type != NodeType::Leaf || r->leaf != LeafKind::Reduce)
-        return fail(MW_E_INVALID_SPEC, "the reduction stage must be an mw_kernel_reduce leaf");
+    // the reduction stage SCT: a reduce leaf, or a pipeline of term maps, ONE
+    // reduce leaf and scalar maps (the kinds enforce the order)
+    int nred = 0;
+    bool ok = r->in_kind == MW_VK_TERMS && r->out_kind == MW_VK_SCALAR &&
+              (r->type == NodeType::Leaf || r->type == NodeType::Pipeline);
+    if (ok && r->type == NodeType::Pipeline)
+        for (const Node* k : r->kids) ok &= k->type == NodeType::Leaf;
+    for (const Node* l : leaves(r)) {
+        nred += l->leaf == LeafKind::Reduce;
+        ok &= l->leaf == LeafKind::Reduce || l->leaf == LeafKind::TermMap || l->leaf == LeafKind::ScalarMap;
+    }
+    if (!ok || nred != 1)
+        return fail(MW_E_INVALID_SPEC, "the reduction stage must be a reduce leaf or a pipeline of term "
+                                       "maps, one reduce leaf and scalar maps");
     mw_node* kids[2] = {map_stage, reduction_stage};
     return make_comp(NodeType::MapReduce, kids, 2, out, 0, 1, MW_MERGE_ADD);
 }

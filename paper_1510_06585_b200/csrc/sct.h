@@ -22,7 +22,9 @@ mw_status fail(mw_status code, const std::string& msg);
 enum class NodeType { Leaf, Pipeline, Map, MapReduce, LoopFor, LoopWhile, LoopHost };
 enum class LeafKind {
     Saxpy, GaussNoise, Solarize, Mirror, Segment, HystStep, HystFinalize,
-    NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits, Fft, Reduce
+    NbodyStep, NbodyAccel, MapIdentity, MapProduct, DebugTraits, Fft, Reduce,
+    TermMap,     // reduction-stage term map (ia: MW_TERM_*)
+    ScalarMap    // reduction-stage map of the reduced value (ia: MW_SCALAR_*, ib: bits of c)
 };
 
 struct Step;
@@ -77,6 +79,8 @@ struct Step {
     int32_t merge_op = 0;              // Reduce: MW_MERGE_*
     int32_t reduce_op = 0;             // Reduce: MW_REDUCE_* (device reduction stage)
     std::vector<ChainOp> pre;          // Reduce: saxpy chain fused into the map stage (dot)
+    int32_t term_map = -1;             // Reduce: -1 none, else MW_TERM_* applied to every term
+    std::vector<std::pair<int32_t, double>> post;   // Reduce: MW_SCALAR_* maps of the result
     void* fn = nullptr;
     void* user = nullptr;
 };

@@ -20,6 +20,8 @@ MW_OK = 0
  MW_E_OOM, MW_E_UNSUPPORTED) = range(1, 12)
 MW_MERGE_ADD, MW_MERGE_SUB, MW_MERGE_MUL, MW_MERGE_DIV, MW_MERGE_USER = range(5)
 MW_REDUCE_SUM, MW_REDUCE_MAX, MW_REDUCE_MIN = range(3)
+MW_TERM_ABS, MW_TERM_SQUARE = 0, 1
+MW_SCALAR_SQRT, MW_SCALAR_SCALE = 0, 1
 # host callbacks (NEXT-4): merging function and host-side loop condition
 _MERGE_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
 _COND_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p)
@@ -117,6 +119,8 @@ _SIG = {
     "mw_map": [_vp, _node_pp],
     "mw_map_reduce": [_vp, _i32, _node_pp],
     "mw_kernel_reduce": [_i32, _node_pp],
+    "mw_kernel_term_map": [_i32, _node_pp],
+    "mw_kernel_scalar_map": [_i32, _f64, _node_pp],
     "mw_map_reduce_sct": [_vp, _vp, _node_pp],
     "mw_ctx_set_monitoring": [_vp, _i32],
     "mw_ctx_set_staging_overlap": [_vp, _i32],
@@ -308,6 +312,16 @@ def mw_map_reduce(map_stage, merge_op=MW_MERGE_ADD):
 def mw_kernel_reduce(op=MW_REDUCE_SUM):
     """Device reduction-stage leaf (NEXT-4, P:191 map_reduce(SCT, SCT))."""
     return _new("mw_kernel_reduce", op)
+
+
+def mw_kernel_term_map(kind):
+    """Reduction-stage term map (MW_TERM_ABS / MW_TERM_SQUARE), NEXT-4."""
+    return _new("mw_kernel_term_map", kind)
+
+
+def mw_kernel_scalar_map(kind, c=0.0):
+    """Reduction-stage map of the reduced value (MW_SCALAR_SQRT / SCALE by c)."""
+    return _new("mw_kernel_scalar_map", kind, _f64(c))
 
 
 def mw_map_reduce_sct(map_stage, reduction_stage):

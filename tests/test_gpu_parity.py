@@ -1249,3 +1249,49 @@ def test_host_condition_loop_inside_a_pipeline():
     for _ in range(4):
         want = K.saxpy(0.25, x, want)
     assert np.array_equal(yd.cpu().numpy(), K.saxpy(2.0, x, want))
+
+
+def test_reduction_stage_sct():
+    """map_reduce_sct(map stage, pipeline(term maps, reduce(op), scalar maps)):
+    the L1 / L2 / L-inf norms, a mean and a sum of squared products, on the
+    device, against the oracle; every distribution gives the same bits."""
+    n = 5 * (1 << 16) + 4321
+    x = synth.np_f32_um11(5, 0, n)
+    y = synth.np_f32_um11(6, 0, n)
+
+    def both(tmaps, op, smaps, dot=False):
+        ot = [sct.Leaf("term_map", {"map": t}) for t in tmaps] + [sct.Leaf("reduce", {"op": op})] + \
+             [sct.Leaf("scalar_map", {"map": k, "c": c}) for k, c in smaps]
+        otree = sct.MapReduce(sct.Leaf("map_product" if dot else "map_identity"),
+                              ot[0] if len(ot) == 1 else sct.Pipeline(ot))
+        codes = {"abs": M.MW_TERM_ABS, "square": M.MW_TERM_SQUARE}
+        ops = {"sum": M.MW_REDUCE_SUM, "max": M.MW_REDUCE_MAX, "min": M.MW_REDUCE_MIN}
+        sk = {"sqrt": M.MW_SCALAR_SQRT, "scale": M.MW_SCALAR_SCALE}
+        st = [M.mw_kernel_term_map(codes[t]) for t in tmaps] + [M.mw_kernel_reduce(ops[op])] + \
+             [M.mw_kernel_scalar_map(sk[k], c) for k, c in smaps]
+        tree = M.mw_map_reduce_sct(M.mw_kernel_map_product() if dot else M.mw_kernel_map_identity(),
+                                   st[0] if len(st) == 1 else M.mw_pipeline(st))
+        return otree, tree
+
+    cases = [(["abs"], "sum", []), (["square"], "sum", [("sqrt", 0.0)]), (["abs"], "max", []),
+             ([], "sum", [("scale", 1.0 / n)]), (["square"], "sum", [], True), (["abs"], "min", [], True),
+             (["abs", "square"], "sum", [("sqrt", 0.0), ("scale", 0.5)])]
+    for case in cases:
+        tm, op, sm = case[:3]
+        dot = len(case) > 3
+        otree, tree = both(tm, op, sm, dot)
+        want = sct.evaluate(otree, (x, y) if dot else x).reduced
+        args = [M.arg(dev(x))] + ([M.arg(dev(y))] if dot else [])
+        got = [run(ctx(k, d), tree, args)["reduced"]
+               for k, d in ((1, None), (3, [0.2, 0.5, 0.3]), (4, [0.0, 0.25, 0.5, 0.25]))]
+        assert all(g == got[0] for g in got), case
+        if op == "sum":
+            assert abs(got[0] - want) <= 1e-12 * abs(want), (case, got[0], want)
+        else:
+            assert got[0] == want, case
+    # the map/reduce structure is validated
+    with pytest.raises(M.MwError):
+        M.mw_map_reduce_sct(M.mw_kernel_map_identity(),
+                            M.mw_pipeline([M.mw_kernel_term_map(0), M.mw_kernel_term_map(1)]))
+    with pytest.raises(M.MwError):
+        run(ctx(), M.mw_kernel_term_map(0), [M.arg(dev(x))])

@@ -128,11 +128,14 @@ def test_mapreduce_ranks_bit_identical(nranks, ppr, dist):
     y = synth.np_f32_um11(6, 0, n)
     trees_of = {"sum": lambda: trees.mapreduce(False), "dot": lambda: trees.mapreduce(True),
                 "max": lambda: trees.mapreduce_sct(M.MW_REDUCE_MAX, True),
-                "min": lambda: trees.mapreduce_sct(M.MW_REDUCE_MIN, True)}
+                "min": lambda: trees.mapreduce_sct(M.MW_REDUCE_MIN, True),
+                "l2": lambda: M.mw_map_reduce_sct(M.mw_kernel_map_identity(), M.mw_pipeline(
+                    [M.mw_kernel_term_map(M.MW_TERM_SQUARE), M.mw_kernel_reduce(M.MW_REDUCE_SUM),
+                     M.mw_kernel_scalar_map(M.MW_SCALAR_SQRT)]))}
     single = {}
     c1 = M.mw_ctx_create(0, 0, 1, 1)
     for key, t in trees_of.items():
-        args = [M.arg(dev(x))] + ([M.arg(dev(y))] if key != "sum" else [])
+        args = [M.arg(dev(x))] + ([M.arg(dev(y))] if key not in ("sum", "l2") else [])
         single[key] = M.mw_run(c1, t(), args).wait().result()["reduced"]
 
     def fn(r, c, s):
@@ -141,7 +144,7 @@ def test_mapreduce_ranks_bit_identical(nranks, ppr, dist):
             node = t()
             s0, s1, _ = local_rows(c, node, n, r)
             args = [M.arg(dev(x[s0:s1]), local_offset=s0, global_shape=(n,))]
-            if key != "sum":
+            if key not in ("sum", "l2"):
                 args.append(M.arg(dev(y[s0:s1]), local_offset=s0, global_shape=(n,)))
             res[key] = M.mw_run(c, node, args).wait().result()["reduced"]
         return res

@@ -959,3 +959,30 @@ def test_interpreter_reports_while_executions_through_composites():
         assert r2.executions == r.executions and np.array_equal(r2.value, r.value)
     r = sct.evaluate(sct.LoopFor(sct.LoopWhileChanged(step, 1000), 2), lab)
     assert r.executions == D + 2
+
+
+def test_reduction_stage_sct_closed_forms():
+    """Reduction-stage SCT (NEXT-4): term maps before the fold, scalar
+    maps after it.  Pins: the L2 norm of a +-1 vector is sqrt(n) exactly; the
+    L1 fold equals abs_sum (pinned above); sum of squares against exact
+    rational brute force; max |x| against a brute-force scan; mean = sum / n
+    with the scale applied after the fold (not per term); abs o square =
+    square."""
+    def red(ops, op="sum"):
+        tm = [sct.Leaf("term_map", {"map": t}) for t in ops[0]]
+        sm = [sct.Leaf("scalar_map", {"map": k, "c": c}) for k, c in ops[1]]
+        stages = tm + [sct.Leaf("reduce", {"op": op})] + sm
+        return sct.MapReduce(sct.Leaf("map_identity"), stages[0] if len(stages) == 1 else sct.Pipeline(stages))
+    rng = np.random.default_rng(5)
+    n = 4097
+    s = np.where(rng.integers(0, 2, n) == 1, 1.0, -1.0).astype(np.float32)
+    assert sct.evaluate(red((["square"], [("sqrt", 0.0)])), s).reduced == math.sqrt(n)
+    x = synth.np_f32_um11(33, 0, 2000)
+    assert sct.evaluate(red((["abs"], [])), x).reduced == K.abs_sum(x)
+    sq = sum(Fraction(float(v)) ** 2 for v in x)
+    got = Fraction(sct.evaluate(red((["square"], [])), x).reduced)
+    assert abs(got - sq) <= sq * Fraction(1, 2 ** 52)
+    assert sct.evaluate(red((["abs"], []), "max"), x).reduced == max(abs(float(v)) for v in x)
+    assert sct.evaluate(red(([], [("scale", 1.0 / 2000)])), x).reduced == K.sum_(x) * (1.0 / 2000)
+    assert sct.evaluate(red((["abs", "square"], [])), x).reduced == sct.evaluate(red((["square"], [])), x).reduced
+    assert sct.sig(red((["square"], [("sqrt", 0.0)]))) == (sct.VEC1, "scalar")

@@ -82,6 +82,8 @@ public:
         NCCL_CALL(ncclAllGather(send, recv, bytes, ncclUint8, comm, s));
         return MW_OK;
     }
+    bool same_process() const override { return false; }
+    mw_status launch_barrier() override { return MW_OK; }
     mw_status async_error() override {
         ncclResult_t r = ncclSuccess;
         ncclCommGetAsyncError(comm, &r);
@@ -161,9 +163,10 @@ public:
     cudaStream_t gstream = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
+    cudaStream_t tmp_stream = nullptr;
 
     ~Loopback() override {
-        if (tmp) cudaFree(tmp);
+        if (tmp) cudaFreeAsync(tmp, tmp_stream);
         if (h) {
             if (h->ready[me]) cudaEventDestroy(h->ready[me]);
             if (h->consumed[me]) cudaEventDestroy(h->consumed[me]);
@@ -210,6 +213,8 @@ public:
         return add({ALLGATHER, send, recv, bytes, -1, DType::I32, ROp::Sum}, s);
     }
     mw_status async_error() override { return MW_OK; }
+    bool same_process() const override { return true; }
+    mw_status launch_barrier() override { return h->barrier(); }
 
     // post stage `st` to every peer, then wait until every peer reached it
     mw_status stage(const std::vector<int>& peers, const std::vector<uint64_t>& seq, int st) {
@@ -275,13 +280,16 @@ public:
             if (o.kind == ALLREDUCE) need += (o.bytes * dsize(o.dt) + 255) / 256 * 256;
         mw_status err = MW_OK;
         if (need > tmp_bytes) {
-            if (tmp) cudaFree(tmp);
+            // stream-ordered: a device-wide synchronisation here could wait for
+            // another rank's kernel that is waiting for this rank
+            if (tmp) cudaFreeAsync(tmp, s);
             tmp = nullptr;
             tmp_bytes = 0;
-            if (cudaMalloc(&tmp, need) != cudaSuccess)
+            if (cudaMallocAsync(&tmp, need, s) != cudaSuccess)
                 err = fail(MW_E_OOM, "loopback: scratch allocation failed");
             else
                 tmp_bytes = need;
+            tmp_stream = s;
         }
         cudaEventRecord(h->ready[me], s);
         MW_OK_OR_RETURN_LB(stage(peers, seq, 1));

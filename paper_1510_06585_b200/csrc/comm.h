@@ -51,6 +51,15 @@ public:
     virtual mw_status allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
     // asynchronous transport faults (NCCL async errors); MW_OK if none
     virtual mw_status async_error() = 0;
+    // the ranks are threads of one process sharing a device (loopback):
+    // device pointers are valid on every rank as they are
+    virtual bool same_process() const = 0;
+    // host barrier among all ranks (loopback: after every rank launched its
+    // kernel of a cross-rank fused loop, so that no rank's first launch of
+    // another kernel — a lazy module load, which waits for the context's
+    // running kernels — can delay a peer's launch; NCCL ranks own their
+    // devices: no-op)
+    virtual mw_status launch_barrier() = 0;
 };
 
 // NCCL communicator from a 128-byte ncclUniqueId (collective over the group).

@@ -96,6 +96,11 @@ struct mw_ctx {
         bool valid = false;
     } prev_io;
     bool staging_overlap = false;   // mw_ctx_set_staging_overlap
+    // cross-rank fused hysteresis: this rank's barrier block (cudaMalloc:
+    // IPC-exportable), peers' buffers opened through CUDA IPC (NCCL ranks)
+    int* xblock = nullptr;
+    std::map<std::string, void*> ipc_open;
+    bool xr_broken = false;         // a cross-rank barrier timed out: per-pass path from now on
     cudaStream_t lane_s[3]{};       // extra capture lanes of mw_graph_capture_many
     cudaEvent_t lane_ev[4]{};
     // pinned host memory
@@ -158,6 +163,8 @@ struct mw_future {
     bool has_reduce = false;
     bool plane_loop = false;
     int64_t plane_m = 1, plane_nb = 0;   // steps per body execution, max body executions
+    bool plane_xr = false;               // cross-rank fused loop: state[3] < 0 = aborted
+    bool plane_count = true;             // the plane state counts executions (a while-loop)
     double executions = 0.0;
     double converged = 1.0;
     bool waited = false;
@@ -514,6 +521,149 @@ mw_status exchange_halos(RunCtx& R, std::vector<Halo>& H, int which, int64_t pit
     return exchange_rows(R, bufs, 1, pitch);
 }
 
+// ------------------------------------------------------------ cross-rank fused loop setup
+// A device pointer as another rank can open it: the raw address (ranks in
+// one process) and a CUDA IPC handle of its allocation + the offset in it.
+struct XPtr {
+    uint64_t raw, off;
+    uint8_t h[64];
+};
+struct XRec {   // what a rank publishes before a cross-rank fused loop
+    int32_t ok, nact;
+    int64_t first_rows, last_rows;
+    XPtr fs[2], ls[2], blk;   // first / last active partition's S0, S1; the barrier block
+};
+bool ipc_export(const void* p, XPtr* out) {
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<GetRange>(f);
+    }();
+    out->raw = reinterpret_cast<uint64_t>(p);
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    cudaIpcMemHandle_t h;
+    if (!fn || fn(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS ||
+        cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    memcpy(out->h, &h, 64);
+    out->off = reinterpret_cast<uint64_t>(p) - (uint64_t)base;
+    return true;
+}
+void* ipc_import(mw_ctx* c, const XPtr& x) {
+    const std::string key(reinterpret_cast<const char*>(x.h), 64);
+    auto it = c->ipc_open.find(key);
+    if (it == c->ipc_open.end()) {
+        cudaIpcMemHandle_t h;
+        memcpy(&h, x.h, 64);
+        void* base = nullptr;
+        if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return nullptr;
+        }
+        it = c->ipc_open.emplace(key, base).first;
+    }
+    return static_cast<uint8_t*>(it->second) + x.off;
+}
+
+// Every rank publishes its boundary partitions' planes and its barrier block;
+// the fused loop runs only when every rank can (no injected slowdown, <= 8
+// active partitions, pointers reachable): *xr tells.  Collective.
+mw_status xrank_setup(RunCtx& R, const std::vector<int>& act, const std::vector<uint8_t*> (&S)[2],
+                      bool slowed, mwk::PlaneMultiHost* hm, bool* xr) {
+    mw_ctx* c = R.c;
+    *xr = false;
+    const int n = c->nranks;
+    const bool same = c->comm->same_process();
+    if (!c->xblock) {   // nothing device-synchronising here: a peer's kernel may be spinning
+        if (cudaMalloc(&c->xblock, mwk::kXBlockInts * sizeof(int)) != cudaSuccess) {
+            (void)cudaGetLastError();
+            c->xblock = nullptr;
+        } else {
+            CUDA_OK(cudaMemsetAsync(c->xblock, 0, mwk::kXBlockInts * sizeof(int), R.s));
+        }
+    }
+    XRec me{};
+    me.ok = !slowed && (int)act.size() <= mwk::kPlaneMaxParts && n <= mwk::kXRanks && c->xblock != nullptr;
+    me.nact = (int)act.size();
+    auto exp = [&](const void* p, XPtr* o) {
+        if (same) {
+            o->raw = reinterpret_cast<uint64_t>(p);
+            return true;
+        }
+        return ipc_export(p, o);
+    };
+    if (me.ok && !act.empty()) {
+        const int qf = act.front(), ql = act.back();
+        me.first_rows = R.len[R.first + qf];
+        me.last_rows = R.len[R.first + ql];
+        for (int b = 0; b < 2; ++b) {
+            me.ok &= exp(S[b][qf], &me.fs[b]);
+            me.ok &= exp(S[b][ql], &me.ls[b]);
+        }
+    }
+    if (me.ok) me.ok &= exp(c->xblock, &me.blk);
+    void* d;
+    MW_OK_OR_RETURN(scratch(c, "xrank_recs", (size_t)n * sizeof(XRec) + sizeof(int), R.s, &d));
+    XRec* drec = static_cast<XRec*>(d);
+    std::vector<XRec> all(n);
+    CUDA_OK(cudaMemcpyAsync(drec + c->rank, &me, sizeof me, cudaMemcpyHostToDevice, R.s));
+    MW_OK_OR_RETURN(c->comm->allgather(drec + c->rank, drec, sizeof(XRec), R.s));
+    CUDA_OK(cudaMemcpyAsync(all.data(), drec, (size_t)n * sizeof(XRec), cudaMemcpyDeviceToHost, R.s));
+    CUDA_OK(cudaStreamSynchronize(R.s));
+    bool all_ok = true;
+    for (const XRec& r : all) all_ok &= r.ok != 0;
+    if (!all_ok) return MW_OK;
+    // open the peers' pointers; every rank must succeed (second agreement)
+    auto imp = [&](int r, const XPtr& x) -> void* {
+        if (same || r == c->rank) return reinterpret_cast<void*>(x.raw);
+        return ipc_import(c, x);
+    };
+    int ok2 = 1;
+    int prev = -1, next = -1;
+    for (int r = c->rank - 1; r >= 0 && prev < 0; --r)
+        if (all[r].nact > 0) prev = r;
+    for (int r = c->rank + 1; r < n && next < 0; ++r)
+        if (all[r].nact > 0) next = r;
+    for (int r = 0; r < n; ++r) {
+        hm->xbar[r] = static_cast<int*>(imp(r, all[r].blk));
+        ok2 &= hm->xbar[r] != nullptr;
+    }
+    if (!act.empty() && prev >= 0) {
+        hm->remote_prev = true;
+        hm->rprev_rows = all[prev].last_rows;
+        for (int b = 0; b < 2; ++b) {
+            hm->rprev_S[b] = static_cast<uint32_t*>(imp(prev, all[prev].ls[b]));
+            ok2 &= hm->rprev_S[b] != nullptr;
+        }
+    }
+    if (!act.empty() && next >= 0) {
+        hm->remote_next = true;
+        for (int b = 0; b < 2; ++b) {
+            hm->rnext_S[b] = static_cast<uint32_t*>(imp(next, all[next].fs[b]));
+            ok2 &= hm->rnext_S[b] != nullptr;
+        }
+    }
+    int* dok = reinterpret_cast<int*>(drec + n);
+    CUDA_OK(cudaMemcpyAsync(dok, &ok2, sizeof ok2, cudaMemcpyHostToDevice, R.s));
+    MW_OK_OR_RETURN(c->comm->allreduce(dok, 1, mwc::DType::I32, mwc::ROp::Min, R.s));
+    CUDA_OK(cudaMemcpyAsync(&ok2, dok, sizeof ok2, cudaMemcpyDeviceToHost, R.s));
+    CUDA_OK(cudaStreamSynchronize(R.s));
+    if (!ok2) return MW_OK;
+    hm->rank = c->rank;
+    hm->nranks = n;
+    hm->grid_div = same ? n : 1;   // loopback ranks share the GPU
+    *xr = true;
+    return MW_OK;
+}
+
 // ------------------------------------------------------------ bit planes, several partitions
 // [u8 chain ending with the threshold] -> stencil loop -> [u8 chain] over P
 // partitions (this rank's ppr of them).  Each partition's planes carry T halo
@@ -632,8 +782,16 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
     // exchanged inside it (stores into the neighbours' halo rows) and the loop
     // condition decided on the device — no per-pass launches, copies or host
     // reads.
-    if (c->nranks == 1 && batched && c->tune[mwk::TUNE_HYST_FUSED] != 0) {
-        mwk::PlaneMultiHost hm{};
+    // Several ranks: the same kernel on every rank, its halo stores going
+    // straight into the neighbouring ranks' planes (NVLink peer memory / the
+    // same device for loopback ranks) and a rank barrier per pass that also
+    // all-reduces the loop condition — one launch per rank for the whole
+    // loop, no per-pass transport calls or host reads.
+    mwk::PlaneMultiHost hm{};
+    bool xr = false;
+    if (c->nranks > 1 && c->comm && c->tune[mwk::TUNE_HYST_FUSED] != 0 && !c->xr_broken && !c->capturing)
+        MW_OK_OR_RETURN(xrank_setup(R, act, S, slowed, &hm, &xr));
+    if (xr || (c->nranks == 1 && batched && c->tune[mwk::TUNE_HYST_FUSED] != 0)) {
         hm.np = (int)act.size();
         hm.wp = wp;
         for (int i = 0; i < hm.np; ++i) {
@@ -645,26 +803,30 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
             hm.fl_bytes[i] = 2 * mwk::planes_tiles(R.len[R.first + q], W);
             hm.rows[i] = R.len[R.first + q];
         }
-        int* state = d_last + 4;   // {E, converged, final buffer}: read by the unpack
+        int* state = d_last + 4;   // {E, converged, final buffer, abort}: read by the unpack
         int* pflags = d_last + 8;
         CUDA_OK(cudaMemsetAsync(pflags, 0xFF, 3 * sizeof(int), R.s));
         {
             auto t = timers_all(MW_KC_STENCIL);
-            MW_OK_OR_RETURN(kerr(mwk::planes_multi(hm, T, st.n, pflags, state, launch_for(c, R.s, R.first)),
-                                 "planes_multi"));
+            mwk::Launch L = launch_for(c, R.s, R.first);
+            if (xr) L.slow = 1.0f;   // every rank's grid is sized for co-residency
+            MW_OK_OR_RETURN(kerr(mwk::planes_multi(hm, T, st.n, pflags, state, L), "planes_multi"));
             close_timers(t);
         }
-        {
+        if (xr) MW_OK_OR_RETURN(c->comm->launch_barrier());
+        if (!act.empty()) {
             auto t = timers_all(MW_KC_U8);
             MW_OK_OR_RETURN(kerr(mwk::planes_unpack_io(post, io_of(), state, W, W, launch_for(c, R.s, R.first), T),
                                  "planes_unpack"));
             close_timers(t);
         }
-        if (is_while) {
-            CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 8, cudaMemcpyDeviceToHost, R.s));
+        if (is_while || xr) {
+            CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 16, cudaMemcpyDeviceToHost, R.s));
             f->plane_loop = true;
+            f->plane_xr = xr;
             f->plane_m = st.m;
             f->plane_nb = st.n / st.m;
+            f->plane_count = is_while;
         }
         return MW_OK;
     }
@@ -846,6 +1008,8 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
             if (prog[1].kind == StepKind::StencilWhile) {
                 CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 8, cudaMemcpyDeviceToHost, R.s));
                 f->plane_loop = true;
+                f->plane_xr = false;
+                f->plane_count = true;
                 f->plane_m = prog[1].m;
                 f->plane_nb = prog[1].n / prog[1].m;
             }
@@ -1766,6 +1930,8 @@ static void ctx_teardown(mw_ctx* c) {
     if (c->st_start) cudaEventDestroy(c->st_start);
     if (c->last_run) cudaEventDestroy(c->last_run);
     for (void* p : c->orphans) ctx_free(c, p);
+    for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
+    if (c->xblock) cudaFree(c->xblock);
     if (c->m_root) mw_node_release(const_cast<mw_node*>(c->m_root));
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);
@@ -1931,11 +2097,18 @@ mw_status mw_future_result(mw_future* f, double* out, int32_t n) {
     double ex = f->executions, conv = f->converged;
     if (f->plane_loop) {
         const int32_t* st = reinterpret_cast<const int32_t*>(f->res + 1);
-        double eb;
-        bool cv;
-        body_execs(st[0], st[1] != 0, f->plane_m, f->plane_nb, &eb, &cv);
-        ex += eb;
-        if (!cv) conv = 0.0;
+        if (f->plane_xr && st[3] < 0) {
+            f->ctx->xr_broken = true;
+            return fail(MW_E_NCCL, "cross-rank hysteresis: a rank did not reach the pass barrier "
+                                   "within 10 s (the run aborted; later runs use the per-pass exchange)");
+        }
+        if (f->plane_count) {
+            double eb;
+            bool cv;
+            body_execs(st[0], st[1] != 0, f->plane_m, f->plane_nb, &eb, &cv);
+            ex += eb;
+            if (!cv) conv = 0.0;
+        }
     }
     double red = f->has_reduce ? *f->res : 0.0;
     if (f->parts) {   // merging function over the partitions with work, in global order

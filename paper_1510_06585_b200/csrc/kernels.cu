@@ -8,6 +8,7 @@
 // accesses, SWAR / DPX byte arithmetic), N-body is FP32-pipe bound.
 //
 // Definitions follow DESIGN.md §Readings (R1-R12), citing PAPER.md lines.
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -1391,15 +1392,17 @@ __device__ __forceinline__ void plane_store_fwd(const uint32_t (&sv)[ROWS], cons
     const PlanePartDesc& d = a.p[q];
     const int64_t y0 = strip * R;                      // owned row 0 of the tile
     const int64_t wp = a.wp;
-    if (d.prev >= 0 && y0 < T) {                       // top rows -> prev's bottom halo
-        const PlanePartDesc& pd = a.p[d.prev];
-        uint32_t* o = pd.S[cur ^ 1] + (pd.rows + T + y0) * wp + w;
+    if (d.prev != -1 && y0 < T) {                      // top rows -> prev's bottom halo
+        // prev == -2: the previous active rank's last partition (peer memory)
+        uint32_t* base = d.prev >= 0 ? a.p[d.prev].S[cur ^ 1] : a.rprev_S[cur ^ 1];
+        const int64_t prows = d.prev >= 0 ? a.p[d.prev].rows : a.rprev_rows;
+        uint32_t* o = base + (prows + T + y0) * wp + w;
 #pragma unroll
         for (int i = 0; i < R; ++i)
             if (y0 + i < T && y0 + i < d.rows) o[i * wp] = sv[T + i];
     }
-    if (d.next >= 0 && y0 + R > d.rows - T) {          // bottom rows -> next's top halo
-        uint32_t* o = a.p[d.next].S[cur ^ 1] + w;
+    if (d.next != -1 && y0 + R > d.rows - T) {         // bottom rows -> next's top halo
+        uint32_t* o = (d.next >= 0 ? a.p[d.next].S[cur ^ 1] : a.rnext_S[cur ^ 1]) + w;
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const int64_t y = y0 + i;
@@ -1426,6 +1429,7 @@ struct PView {
     const uint8_t* fp_prev2;  // ... and of its second-to-last strip when the last is short
     const uint8_t* fp_next;   // next partition: flags of its first strip
     bool short_last;          // this partition's last strip has fewer than T rows
+    bool force_top, force_bot;   // neighbour on another rank: boundary strips always run
 };
 template <int T, int ROWS>
 __device__ __forceinline__ PView plane_view(const PlaneMultiArgs& a, int q, int cur, int64_t t0) {
@@ -1440,6 +1444,8 @@ __device__ __forceinline__ PView plane_view(const PlaneMultiArgs& a, int q, int 
     v.t1 = t0 + d.nt;
     v.short_last = d.rows - (d.n_strips - 1) * R < T;
     v.fp_prev = v.fp_prev2 = v.fp_next = nullptr;
+    v.force_top = d.prev == -2;
+    v.force_bot = d.next == -2;
     if (d.prev >= 0) {
         const PlanePartDesc& pd = a.p[d.prev];
         const uint8_t* f = pd.fl + (cur ^ 1) * pd.nt;
@@ -1455,6 +1461,10 @@ __device__ __forceinline__ PView plane_view(const PlaneMultiArgs& a, int q, int 
 __device__ __forceinline__ bool plane_tile_active_multi(const PView& v, int64_t n_cb, int64_t strip,
                                                         int64_t cb, bool first, int lane) {
     if (first) return true;
+    // a neighbour on another rank: its flags are not read, its halo may change
+    if ((v.force_top && strip == 0) ||
+        (v.force_bot && (strip == v.n_strips - 1 || (v.short_last && strip == v.n_strips - 2))))
+        return true;
     const int64_t c2 = cb + lane % 3 - 1;
     bool x = false;
     if (lane < 18 && c2 >= 0 && c2 < n_cb) {
@@ -1485,6 +1495,7 @@ __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, in
     const bool own_lane = lane >= 1 && lane <= OW;
     // scan cursor over the concatenated tile list: a warp's tiles increase, so
     // the partition of the next candidate is found by moving forward only
+    if (a.total == 0) return -1;   // a rank without active partitions only joins the barriers
     int sq = 0;
     PView v = plane_view<T, ROWS>(a, 0, cur, 0);
     auto next_active = [&](int64_t t) {
@@ -1566,6 +1577,10 @@ __global__ void __launch_bounds__(256) k_planes_multi(const __grid_constant__ Pl
     const int64_t gw = (int64_t)blockIdx.x * 8 + wid;
     const int64_t nwarps = (int64_t)gridDim.x * 8;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool xr = a.nranks > 1;
+    int* own = xr ? a.xbar[a.rank] : nullptr;
+    // arrivals of earlier runs (every rank ran the same passes: equal on all)
+    const int epoch0 = xr && leader ? *((volatile int*)&own[1]) : 0;
     uint32_t phase = 0;
     int64_t k0 = 0;
     int pass = 0;
@@ -1576,14 +1591,63 @@ __global__ void __launch_bounds__(256) k_planes_multi(const __grid_constant__ Pl
                                                            lane, sb, kb, bar, phase);
         if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (xr) __threadfence_system();   // halo stores into peers before the rank barrier
         grid.sync();
+        if (xr) {
+            // rank barrier + all-reduce (max) of the last changing execution:
+            // each leader publishes its value into every rank's slot, then
+            // arrives on every rank's counter (release at system scope) and
+            // waits for all arrivals of this pass on its own (acquire)
+            if (leader) {
+                const int slot = 4 + (pass % 3) * kXRanks;
+                const int lv = *((volatile int*)&flags[pass % 3]);
+                for (int r = 0; r < a.nranks; ++r)
+                    asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(a.xbar[r] + slot + a.rank), "r"(lv)
+                                 : "memory");
+                __threadfence_system();
+                for (int r = 0; r < a.nranks; ++r)
+                    asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(a.xbar[r]) : "memory");
+                const int target = epoch0 + (pass + 1) * a.nranks;
+                unsigned long long t0;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                bool ok = true;
+                for (;;) {
+                    int cnt;
+                    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(cnt) : "l"(own) : "memory");
+                    if (cnt >= target) break;
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if (t - t0 > 10000000000ull) {   // 10 s: a rank is not running; abort
+                        ok = false;
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+                int g = -1;
+                for (int r = 0; r < a.nranks && ok; ++r) g = max(g, *((volatile int*)&own[slot + r]));
+                flags[pass % 3] = ok ? g : INT_MIN;
+            }
+            grid.sync();
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // peers' halo rows, read by TMA
+        }
         const int last = *((volatile int*)&flags[pass % 3]);
+        if (last == INT_MIN) {   // cross-rank barrier timed out
+            if (leader) {
+                state[0] = (int)k0;
+                state[1] = 0;
+                state[2] = (pass & 1) ? 0 : 1;
+                state[3] = -1;
+            }
+            return;
+        }
         if (last < k0 + steps - 1) {
             if (leader) {
                 const int64_t last_global = last >= 0 ? last : k0 - 1;
                 state[0] = (int)(last_global + 2);
                 state[1] = 1;
                 state[2] = (pass & 1) ? 0 : 1;
+                state[3] = 0;
+                if (xr) own[1] = epoch0 + (pass + 1) * a.nranks;
             }
             return;
         }
@@ -1594,6 +1658,8 @@ __global__ void __launch_bounds__(256) k_planes_multi(const __grid_constant__ Pl
         state[0] = (int)max_iters;
         state[1] = 0;
         state[2] = pass == 0 ? 0 : (((pass - 1) & 1) ? 0 : 1);
+        state[3] = 0;
+        if (xr) own[1] = epoch0 + pass * a.nranks;
     }
 }
 
@@ -2645,6 +2711,18 @@ static cudaError_t planes_multi_t(const PlaneMultiHost& h, int64_t max_iters, in
     a.np = h.np;
     a.wp = h.wp;
     a.n_cb = (h.wp + 29) / 30;
+    a.rank = h.rank;
+    a.nranks = h.nranks;
+    if (h.nranks < 1 || h.nranks > kXRanks) return cudaErrorInvalidValue;
+    for (int r = 0; r < h.nranks && h.nranks > 1; ++r) {
+        if (!h.xbar[r]) return cudaErrorInvalidValue;
+        a.xbar[r] = h.xbar[r];
+    }
+    a.rprev_S[0] = h.rprev_S[0];
+    a.rprev_S[1] = h.rprev_S[1];
+    a.rprev_rows = h.rprev_rows;
+    a.rnext_S[0] = h.rnext_S[0];
+    a.rnext_S[1] = h.rnext_S[1];
     int64_t tiles = 0;
     for (int q = 0; q < h.np; ++q) {
         PlanePartDesc& d = a.p[q];
@@ -2656,8 +2734,8 @@ static cudaError_t planes_multi_t(const PlaneMultiHost& h, int64_t max_iters, in
         d.nt = d.n_strips * a.n_cb;
         d.tile0 = tiles;
         tiles += d.nt;
-        d.prev = q > 0 ? q - 1 : -1;
-        d.next = q + 1 < h.np ? q + 1 : -1;
+        d.prev = q > 0 ? q - 1 : (h.remote_prev ? -2 : -1);
+        d.next = q + 1 < h.np ? q + 1 : (h.remote_next ? -2 : -1);
         if (d.rows < T || 2 * d.nt > h.fl_bytes[q]) return cudaErrorInvalidValue;
         if (!plane_tmap(&a.ts[q][0], h.S0[q], d.rows, h.wp, ROWS, T) ||
             !plane_tmap(&a.ts[q][1], h.S1[q], d.rows, h.wp, ROWS, T) ||
@@ -2665,7 +2743,10 @@ static cudaError_t planes_multi_t(const PlaneMultiHost& h, int64_t max_iters, in
             return cudaErrorInvalidValue;
     }
     a.total = tiles;
-    const unsigned grid = grid_for((tiles + 7) / 8, occ, L);
+    // loopback ranks share the GPU: each rank's cooperative grid takes its
+    // share of the SMs so every rank's kernel is resident at the barriers
+    const unsigned grid = std::max(1u, std::min(grid_for(std::max<int64_t>(1, (tiles + 7) / 8), occ, L),
+                                                (unsigned)(sm_count() * occ / std::max(1, h.grid_div))));
     int64_t mi = max_iters;
     void* args[] = {&a, &mi, &flags, &state};
     ++g_launches;
@@ -2675,7 +2756,7 @@ static cudaError_t planes_multi_t(const PlaneMultiHost& h, int64_t max_iters, in
 
 cudaError_t planes_multi(const PlaneMultiHost& h, int T, int64_t max_iters, int* flags, int* state,
                          const Launch& L) {
-    if (h.np < 1 || h.np > kPlaneMaxParts) return cudaErrorInvalidValue;
+    if (h.np < (h.nranks > 1 ? 0 : 1) || h.np > kPlaneMaxParts) return cudaErrorInvalidValue;
     switch (T) {
         case 12: return planes_multi_t<12, 40>(h, max_iters, flags, state, L);
         case 8: return planes_multi_t<8, 48>(h, max_iters, flags, state, L);

@@ -148,15 +148,29 @@ struct PlanePartDesc {
     int64_t rows, n_strips, nt, tile0;
     int prev, next;                  // neighbouring partition in the table, -1 at the image edge
 };
+// Several RANKS (the cross-rank fused loop): prev / next == -2 marks a
+// neighbour on another rank, whose plane buffers the kernel stores into
+// directly (peer memory over NVLink; the same device for loopback ranks);
+// after every pass the ranks meet in a barrier on the xbar blocks (one per
+// rank: [0] arrival counter, [1] epoch = arrivals of earlier runs, [2]
+// spare, [4 + 3 * kXRanks) the ranks' last-changed executions per pass
+// slot), which also all-reduces the loop condition.
+constexpr int kXRanks = 16;
+constexpr int kXBlockInts = 4 + 3 * kXRanks;
 struct PlaneMultiArgs {
     CUtensorMap ts[kPlaneMaxParts][2];
     CUtensorMap tk[kPlaneMaxParts];
     PlanePartDesc p[kPlaneMaxParts];
     int np;
     int64_t wp, n_cb, total;
+    uint32_t* rprev_S[2];   // previous active rank's last partition (prev == -2)
+    int64_t rprev_rows;
+    uint32_t* rnext_S[2];   // next active rank's first partition (next == -2)
+    int* xbar[kXRanks];     // every rank's barrier block
+    int rank, nranks;       // nranks == 1: no cross-rank barrier
 };
 struct PlaneMultiHost {
-    int np;
+    int np;                 // 0 allowed with nranks > 1 (the rank only joins the barriers)
     int64_t wp;
     uint32_t* S0[kPlaneMaxParts];
     uint32_t* S1[kPlaneMaxParts];
@@ -164,7 +178,15 @@ struct PlaneMultiHost {
     uint8_t* fl[kPlaneMaxParts];
     int64_t fl_bytes[kPlaneMaxParts];
     int64_t rows[kPlaneMaxParts];
+    bool remote_prev = false, remote_next = false;
+    uint32_t* rprev_S[2]{};
+    int64_t rprev_rows = 0;
+    uint32_t* rnext_S[2]{};
+    int* xbar[kXRanks]{};
+    int rank = 0, nranks = 1;
+    int grid_div = 1;       // loopback ranks share one GPU: each gets 1/grid_div of it
 };
+// state[3] = -1 when a cross-rank barrier timed out (10 s; the run aborted).
 cudaError_t planes_multi(const PlaneMultiHost& h, int T, int64_t max_iters, int* flags, int* state,
                          const Launch& L);
 

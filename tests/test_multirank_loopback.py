@@ -188,9 +188,13 @@ def oracle_hyst(gray, lo=173, hi=250):
     return K.hyst_finalize(fixed), D
 
 
-@pytest.mark.parametrize("planes", [1, 0])
+@pytest.mark.parametrize("planes,fused", [(1, 1), (1, 0), (0, 0)])
 @pytest.mark.parametrize("nranks,ppr,dist", CASES)
-def test_hysteresis_ranks_bitwise_and_E(planes, nranks, ppr, dist):
+def test_hysteresis_ranks_bitwise_and_E(planes, fused, nranks, ppr, dist):
+    """planes + fused: one cooperative kernel per rank for the whole loop, halo
+    rows stored into the neighbouring ranks' planes, a rank barrier per pass;
+    planes alone: per-pass kernels + transport halos + lagged all-reduce;
+    bytes: the byte stencil."""
     H, W = 333, 515
     gray = synth.np_u8_stream(8, 0, H * W).reshape(H, W)
     want, D = oracle_hyst(gray)
@@ -201,17 +205,22 @@ def test_hysteresis_ranks_bitwise_and_E(planes, nranks, ppr, dist):
             node = trees.hysteresis(check_every=ce)
             s0, s1, _ = local_rows(c, node, H, r)
             dst = torch.empty((s1 - s0, W), dtype=torch.uint8, device=DEV)
-            res = M.mw_run(c, node, [M.arg(dev(gray[s0:s1]), local_offset=s0, global_shape=(H, W)),
+            src = dev(gray[s0:s1])
+            l0 = M.mw_ctx_launch_count(c)
+            res = M.mw_run(c, node, [M.arg(src, local_offset=s0, global_shape=(H, W)),
                                      M.arg(dst, local_offset=s0, global_shape=(H, W))]).wait().result()
-            got.append((s0, dst.cpu().numpy(), res["executions"], res["converged"]))
+            got.append((s0, dst.cpu().numpy(), res["executions"], res["converged"],
+                        M.mw_ctx_launch_count(c) - l0))
         return got
 
-    res = run_ranks(nranks, ppr, dist, fn, tune=[(M.MW_TUNE_HYST_PLANES, planes)])
+    res = run_ranks(nranks, ppr, dist, fn, tune=[(M.MW_TUNE_HYST_PLANES, planes), (M.MW_TUNE_HYST_FUSED, fused)])
     for i in range(2):
         out = assemble([(g[i][0], g[i][1]) for g in res], (H, W), np.uint8)
         assert np.array_equal(out, want)
         for g in res:
             assert g[i][2] == D + 1 and g[i][3]
+            if planes and fused:   # the whole loop is one launch per rank (+ pack/unpack/setup)
+                assert g[i][4] <= 8, g[i][4]
 
 
 def test_hysteresis_ranks_max_iters():

@@ -1558,7 +1558,7 @@ __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, in
 }
 
 template <int T, int ROWS>
-__global__ void __launch_bounds__(256) k_planes_multi(const __grid_constant__ PlaneMultiArgs a,
+__global__ void __launch_bounds__(256, 1) k_planes_multi(const __grid_constant__ PlaneMultiArgs a,
                                                       int64_t max_iters, int* __restrict__ flags,
                                                       int* __restrict__ state) {
     constexpr int BW = 36;

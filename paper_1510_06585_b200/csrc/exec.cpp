@@ -25,159 +25,19 @@
 #include <string>
 #include <vector>
 
-#include "comm.h"
-#include "marrow.h"
-#include "mw_kernels.h"
-#include "sct.h"
 
-namespace mw {
-const char* last_error_cstr();
-}
+#include "ctx.h"
 
-using mw::fail;
-using mw::Node;
-using mw::Step;
-using mw::StepKind;
+using namespace mwx;
 
-#define CUDA_OK(expr)                                                                   \
-    do {                                                                                \
-        cudaError_t e_ = (expr);                                                        \
-        if (e_ != cudaSuccess)                                                          \
-            return fail(e_ == cudaErrorMemoryAllocation ? MW_E_OOM : MW_E_CUDA,         \
-                        std::string(#expr) + ": " + cudaGetErrorString(e_));            \
-    } while (0)
 #define NCCL_OK(expr)                                                                   \
     do {                                                                                \
         ncclResult_t r_ = (expr);                                                       \
         if (r_ != ncclSuccess)                                                          \
             return fail(MW_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
     } while (0)
-#define MW_OK_OR_RETURN(expr)          \
-    do {                               \
-        mw_status s_ = (expr);         \
-        if (s_ != MW_OK) return s_;    \
-    } while (0)
 
-namespace {
-
-struct Buf {
-    void* p = nullptr;
-    size_t bytes = 0;
-};
-
-constexpr int kStageSlots = 3;
-
-}  // namespace
-
-struct mw_ctx {
-    int device = 0, rank = 0, nranks = 1, ppr = 1, P = 1;
-    std::unique_ptr<mwc::Comm> comm;   // NCCL, or the test-only loopback (comm.h)
-    mw_alloc_fns alloc{};
-    bool has_alloc = false;
-    std::vector<double> dist;
-    std::map<std::string, Buf> scratch;
-    // Scratch pointers baked into live CUDA graphs (refcount per pointer): a
-    // buffer replaced by a larger one while a graph references it is parked in
-    // `orphans` and freed with the last such graph (or at teardown).
-    std::map<void*, int> graph_refs;
-    std::vector<void*> orphans;
-    std::vector<void*>* capture_bufs = nullptr;   // collects scratch used while capturing
-    // FIFO of runs across streams: every run waits for the previous run's end
-    // (a no-op on one stream) and records it (ctx scratch is shared by runs).
-    cudaEvent_t last_run = nullptr;
-    cudaStream_t last_stream = nullptr;
-    bool have_last_run = false;
-    // run pipelining (mw_ctx_set_run_pipelining): the byte ranges the previous
-    // run read and wrote, to launch an independent next run without the
-    // programmatic-dependent-launch wait
-    bool pipelining = false;
-    struct Ranges {
-        std::vector<std::pair<uintptr_t, uintptr_t>> rd, wr;
-        bool valid = false;
-    } prev_io;
-    bool staging_overlap = false;   // mw_ctx_set_staging_overlap
-    // cross-rank fused hysteresis: this rank's barrier block (cudaMalloc:
-    // IPC-exportable), peers' buffers opened through CUDA IPC (NCCL ranks)
-    int* xblock = nullptr;
-    std::map<std::string, void*> ipc_open;
-    bool xr_broken = false;         // a cross-rank barrier timed out: per-pass path from now on
-    cudaStream_t lane_s[3]{};       // extra capture lanes of mw_graph_capture_many
-    cudaEvent_t lane_ev[4]{};
-    // pinned host memory
-    int32_t* h_flag = nullptr;   // 16 ints: [0] byte-stencil flag, [4..7] plane-pass ring
-    cudaEvent_t lag_ev[4]{};
-    std::vector<double*> res_free;
-    std::vector<double*> res_pages;
-    // monitoring
-    std::vector<cudaEvent_t> ev_pool;
-    size_t ev_used = 0;
-    struct Rec {
-        int part;
-        int cls;
-        cudaEvent_t a, b;
-        int64_t launches;
-    };
-    std::vector<Rec> recs;      // last run (mw_last_timings)
-    bool stats_on = false;
-    std::vector<Rec> stats;     // every run since mw_stats_enable (mw_kernel_stats)
-    cudaEvent_t wall_a = nullptr, wall_b = nullptr;
-    std::vector<int64_t> last_len;
-    bool have_run = false;
-    mw_balance_state bstate{};
-    std::vector<float> slow;
-    // device classes (NEXT-4 heterogeneous devices): class id and
-    // relative performance per partition
-    std::vector<int> cls;
-    std::vector<double> relperf;
-    // managed runs (Fig. 5): the (SCT, workload) of the previous
-    // managed run, and its result still to be persisted in the KB
-    std::string mkey;
-    bool m_pending = false;
-    const mw_node* m_root = nullptr;
-    std::vector<int64_t> m_dims;
-    int m_prov = MW_PROV_DERIVED;
-    mw_kb* m_kb = nullptr;
-    unsigned long long launches0 = 0;
-    // host staging (NEXT-1 overlap)
-    cudaStream_t copy_in = nullptr, copy_out = nullptr, aux = nullptr;
-    cudaEvent_t st_in[kStageSlots]{}, st_comp[kStageSlots]{}, st_out[kStageSlots]{};
-    cudaEvent_t st_start = nullptr;
-    bool st_valid[kStageSlots]{};   // slot has a recorded st_out (possibly from an earlier run)
-    bool capturing = false;     // inside mw_graph_capture: no timing events, no host syncs
-    bool monitor = true;        // per-partition timing events (mw_ctx_set_monitoring)
-    int refs = 1;               // the user's handle + outstanding futures and graphs
-    bool destroyed = false;     // mw_ctx_destroy called; teardown at the last release
-    // futures released while their run was still in flight: reclaimed once
-    // their event completed (next mw_run) or at mw_ctx_destroy — releasing a
-    // future never blocks the host, so a loop that drops each future keeps
-    // the device fed
-    std::deque<mw_future*> retired;    // in release order
-    std::vector<cudaEvent_t> fut_ev;   // completion events of released futures, reused
-    int tune[mwk::TUNE_COUNT];  // tuning knobs (mw_ctx_set_tuning)
-};
-
-struct mw_future {
-    mw_ctx* ctx = nullptr;
-    cudaEvent_t done = nullptr;
-    double* res = nullptr;     // pinned slot (4 x 8 B): [0] reduced, [1] plane-loop {E, converged} int32
-    bool has_reduce = false;
-    bool plane_loop = false;
-    int64_t plane_m = 1, plane_nb = 0;   // steps per body execution, max body executions
-    bool plane_xr = false;               // cross-rank fused loop: state[3] < 0 = aborted
-    bool plane_count = true;             // the plane state counts executions (a while-loop)
-    double executions = 0.0;
-    double converged = 1.0;
-    bool waited = false;
-    bool completed = false;    // a query or wait saw the run complete
-    // MapReduce with a non-ADD merging function: per-partition partials (pinned)
-    double* parts = nullptr;
-    std::vector<char> part_active;
-    int32_t merge_op = 0;
-    mw_merge_fn merge_fn = nullptr;
-    void* merge_user = nullptr;
-};
-
-namespace {
+namespace mwx {
 
 // ------------------------------------------------------------ memory
 mw_status ctx_alloc(mw_ctx* c, size_t bytes, cudaStream_t s, void** out) {
@@ -1827,7 +1687,69 @@ mw_status run_split_host(mw_ctx* c, const Node* root, const mw_arg* args, int na
     return MW_OK;
 }
 
-}  // namespace
+// Runs of one ctx execute in call order even on different streams (they
+// share the ctx scratch): a run's stream first waits for the previous run's
+// end, which each run records.  On one stream the wait is a no-op.
+// The event is recorded lazily, only when the stream changes: consecutive
+// runs on one stream keep no event operations between their kernels (which
+// would stand between programmatically dependent launches).
+mw_status fifo_enter(mw_ctx* c, cudaStream_t s) {
+    if (c->capturing || !c->have_last_run || s == c->last_stream) return MW_OK;
+    if (cudaEventRecord(c->last_run, c->last_stream) != cudaSuccess) {
+        (void)cudaGetLastError();   // the previous stream is gone: drain the device instead
+        CUDA_OK(cudaDeviceSynchronize());
+    } else {
+        CUDA_OK(cudaStreamWaitEvent(s, c->last_run, 0));
+    }
+    c->prev_io.valid = false;   // another stream: no programmatic overlap
+    return MW_OK;
+}
+void fifo_exit(mw_ctx* c, cudaStream_t s) {
+    if (c->capturing) return;
+    c->last_stream = s;
+    c->have_last_run = true;
+}
+
+static void ctx_teardown(mw_ctx* c) {
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : c->scratch) ctx_free(c, kv.second.p);
+    c->comm.reset();
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->fut_ev) cudaEventDestroy(e);
+    if (c->wall_a) cudaEventDestroy(c->wall_a);
+    if (c->wall_b) cudaEventDestroy(c->wall_b);
+    for (int i = 0; i < kStageSlots; ++i) {
+        if (c->st_in[i]) cudaEventDestroy(c->st_in[i]);
+        if (c->st_comp[i]) cudaEventDestroy(c->st_comp[i]);
+        if (c->st_out[i]) cudaEventDestroy(c->st_out[i]);
+    }
+    if (c->st_start) cudaEventDestroy(c->st_start);
+    if (c->last_run) cudaEventDestroy(c->last_run);
+    for (void* p : c->orphans) ctx_free(c, p);
+    for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
+    if (c->xblock) cudaFree(c->xblock);
+    if (c->m_root) mw_node_release(const_cast<mw_node*>(c->m_root));
+    if (c->copy_in) cudaStreamDestroy(c->copy_in);
+    if (c->copy_out) cudaStreamDestroy(c->copy_out);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    for (cudaStream_t q : c->lane_s)
+        if (q) cudaStreamDestroy(q);
+    for (cudaEvent_t e : c->lane_ev)
+        if (e) cudaEventDestroy(e);
+    if (c->h_flag) cudaFreeHost(c->h_flag);
+    for (cudaEvent_t e : c->lag_ev)
+        if (e) cudaEventDestroy(e);
+    for (double* p : c->res_pages) cudaFreeHost(p);
+    (void)cudaGetLastError();   // leave no stale error behind for the host application
+    delete c;
+}
+void ctx_retain(mw_ctx* c) { ++c->refs; }
+void ctx_release(mw_ctx* c) {
+    if (--c->refs == 0) ctx_teardown(c);
+}
+
+}  // namespace mwx
 
 // ============================================================ C-ABI
 extern "C" {
@@ -1889,68 +1811,6 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
 }
 
 static void reap_retired(mw_ctx* c, bool sync);
-
-// Runs of one ctx execute in call order even on different streams (they
-// share the ctx scratch): a run's stream first waits for the previous run's
-// end, which each run records.  On one stream the wait is a no-op.
-// The event is recorded lazily, only when the stream changes: consecutive
-// runs on one stream keep no event operations between their kernels (which
-// would stand between programmatically dependent launches).
-static mw_status fifo_enter(mw_ctx* c, cudaStream_t s) {
-    if (c->capturing || !c->have_last_run || s == c->last_stream) return MW_OK;
-    if (cudaEventRecord(c->last_run, c->last_stream) != cudaSuccess) {
-        (void)cudaGetLastError();   // the previous stream is gone: drain the device instead
-        CUDA_OK(cudaDeviceSynchronize());
-    } else {
-        CUDA_OK(cudaStreamWaitEvent(s, c->last_run, 0));
-    }
-    c->prev_io.valid = false;   // another stream: no programmatic overlap
-    return MW_OK;
-}
-static void fifo_exit(mw_ctx* c, cudaStream_t s) {
-    if (c->capturing) return;
-    c->last_stream = s;
-    c->have_last_run = true;
-}
-
-static void ctx_teardown(mw_ctx* c) {
-    cudaSetDevice(c->device);
-    cudaDeviceSynchronize();
-    for (auto& kv : c->scratch) ctx_free(c, kv.second.p);
-    c->comm.reset();
-    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-    for (cudaEvent_t e : c->fut_ev) cudaEventDestroy(e);
-    if (c->wall_a) cudaEventDestroy(c->wall_a);
-    if (c->wall_b) cudaEventDestroy(c->wall_b);
-    for (int i = 0; i < kStageSlots; ++i) {
-        if (c->st_in[i]) cudaEventDestroy(c->st_in[i]);
-        if (c->st_comp[i]) cudaEventDestroy(c->st_comp[i]);
-        if (c->st_out[i]) cudaEventDestroy(c->st_out[i]);
-    }
-    if (c->st_start) cudaEventDestroy(c->st_start);
-    if (c->last_run) cudaEventDestroy(c->last_run);
-    for (void* p : c->orphans) ctx_free(c, p);
-    for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
-    if (c->xblock) cudaFree(c->xblock);
-    if (c->m_root) mw_node_release(const_cast<mw_node*>(c->m_root));
-    if (c->copy_in) cudaStreamDestroy(c->copy_in);
-    if (c->copy_out) cudaStreamDestroy(c->copy_out);
-    if (c->aux) cudaStreamDestroy(c->aux);
-    for (cudaStream_t q : c->lane_s)
-        if (q) cudaStreamDestroy(q);
-    for (cudaEvent_t e : c->lane_ev)
-        if (e) cudaEventDestroy(e);
-    if (c->h_flag) cudaFreeHost(c->h_flag);
-    for (cudaEvent_t e : c->lag_ev)
-        if (e) cudaEventDestroy(e);
-    for (double* p : c->res_pages) cudaFreeHost(p);
-    (void)cudaGetLastError();   // leave no stale error behind for the host application
-    delete c;
-}
-static void ctx_retain(mw_ctx* c) { ++c->refs; }
-static void ctx_release(mw_ctx* c) {
-    if (--c->refs == 0) ctx_teardown(c);
-}
 
 // Futures and graphs hold a reference: a ctx destroyed while they are alive
 // is torn down when the last of them is released.
@@ -2323,672 +2183,5 @@ mw_status mw_ctx_launch_count(const mw_ctx* c, int64_t* out) {
     return MW_OK;
 }
 
-
-// ------------------------------------------------------------ graphs
-struct mw_graph {
-    mw_ctx* ctx = nullptr;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    mw_future f;          // result slot of the captured run
-    int64_t kernels = 0;  // library kernels per replay
-    std::vector<void*> bufs;   // ctx scratch the graph writes (kept alive while it lives)
-    int lanes = 1;             // parallel capture lanes (independent runs)
-};
-
-// Runs of `root` on the nsets argument sets may execute concurrently when the
-// tree is one fused Map/Pipeline chain that touches no ctx scratch and no set
-// writes a byte another set reads or writes (data dependencies are the only
-// order a replay must keep).
-static bool sets_independent(const Node* root, const mw_arg* args, int nargs, int nsets) {
-    mw_status st;
-    const mw::NodeCache* nc = mw::plan_cached(root, &st);
-    if (!nc || nc->prog.size() != 1) return false;
-    const Step& s0 = nc->prog[0];
-    if (s0.kind == StepKind::Saxpy) {
-        if (saxpy_groups(s0.ops).size() != 1) return false;
-    } else if (s0.kind == StepKind::Rgba) {
-        if (rgba_groups(s0.ops).size() != 1) return false;
-    } else if (s0.kind == StepKind::U8) {
-        if (u8_groups(s0.ops).size() != 1) return false;
-    } else {
-        return false;
-    }
-    if (nargs != 2) return false;
-    struct Range {
-        uintptr_t a, b;
-        bool w;
-    };
-    std::vector<std::vector<Range>> rs(nsets);
-    for (int k = 0; k < nsets; ++k)
-        for (int i = 0; i < nargs; ++i) {
-            const mw_arg& x = args[(size_t)k * nargs + i];
-            if (x.location != MW_LOC_DEVICE) return false;
-            const uintptr_t a = reinterpret_cast<uintptr_t>(x.ptr);
-            rs[k].push_back({a, a + (uintptr_t)(x.local_rows * row_bytes(x)), i == 1});
-        }
-    for (int j = 0; j < nsets; ++j)
-        for (int k = j + 1; k < nsets; ++k)
-            for (const Range& u : rs[j])
-                for (const Range& v : rs[k])
-                    if ((u.w || v.w) && u.a < v.b && v.a < u.b) return false;
-    return true;
-}
-
-mw_status mw_graph_capture_many(mw_ctx* c, const mw_node* root, const mw_arg* args,
-                                int32_t nargs, int32_t nsets, void* stream, mw_graph** out) {
-    if (!c || !root || !out || (nargs > 0 && !args) || nsets < 1)
-        return fail(MW_E_INVALID_SPEC, "NULL argument or nsets < 1");
-    if (!stream) return fail(MW_E_INVALID_SPEC, "graph capture needs a non-default stream");
-    if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
-    CUDA_OK(cudaSetDevice(c->device));
-    (void)cudaGetLastError();   // see mw_run
-    std::unique_ptr<mw_graph> g(new mw_graph);
-    g->ctx = c;
-    g->f.ctx = c;
-    MW_OK_OR_RETURN(fifo_enter(c, static_cast<cudaStream_t>(stream)));   // before capture begins
-    CUDA_OK(cudaHostAlloc(&g->f.res, 32, cudaHostAllocDefault));
-    memset(g->f.res, 0, 32);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const unsigned long long l0 = mwk::launch_count();
-    CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-    c->capturing = true;
-    std::vector<void*> used;
-    c->capture_bufs = &used;
-    mw_status st = MW_OK;
-    try {
-        // independent runs: round-robin over `lanes` streams forked from and
-        // joined back into the capture stream
-        int lanes = std::min<int>(c->tune[mwk::TUNE_GRAPH_LANES], nsets);
-        if (lanes > 1 && !sets_independent(reinterpret_cast<const Node*>(root), args, nargs, nsets)) lanes = 1;
-        cudaStream_t ls[4] = {s, nullptr, nullptr, nullptr};
-        for (int l = 1; l < lanes && st == MW_OK; ++l) {
-            if (!c->lane_s[l - 1] &&
-                cudaStreamCreateWithFlags(&c->lane_s[l - 1], cudaStreamNonBlocking) != cudaSuccess)
-                st = fail(MW_E_CUDA, "lane stream");
-            ls[l] = c->lane_s[l - 1];
-        }
-        for (int l = 0; l < lanes && st == MW_OK; ++l)
-            if (!c->lane_ev[l] && cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming) != cudaSuccess)
-                st = fail(MW_E_CUDA, "lane event");
-        if (lanes > 1 && st == MW_OK) {
-            cudaEventRecord(c->lane_ev[0], s);
-            for (int l = 1; l < lanes; ++l) cudaStreamWaitEvent(ls[l], c->lane_ev[0], 0);
-        }
-        for (int32_t k = 0; k < nsets && st == MW_OK; ++k) {
-            g->f.has_reduce = false;
-            g->f.plane_loop = false;
-            st = run(c, reinterpret_cast<const Node*>(root), args + (size_t)k * nargs, nargs, ls[k % lanes],
-                     &g->f);
-        }
-        if (lanes > 1)
-            for (int l = 1; l < lanes; ++l) {
-                cudaEventRecord(c->lane_ev[l], ls[l]);
-                cudaStreamWaitEvent(s, c->lane_ev[l], 0);
-            }
-        g->lanes = lanes;
-    } catch (...) {
-        st = fail(MW_E_INVALID_SPEC, "internal error");
-    }
-    c->capturing = false;
-    c->capture_bufs = nullptr;
-    cudaGraph_t graph = nullptr;
-    cudaError_t e = cudaStreamEndCapture(s, &graph);
-    if (st != MW_OK || e != cudaSuccess) {
-        if (graph) cudaGraphDestroy(graph);
-        cudaFreeHost(g->f.res);
-        if (st != MW_OK) return st;
-        return fail(MW_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    }
-    g->graph = graph;
-    e = cudaGraphInstantiate(&g->exec, graph, 0);
-    if (e != cudaSuccess) {
-        cudaGraphDestroy(graph);
-        cudaFreeHost(g->f.res);
-        return fail(MW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    }
-    g->kernels = (int64_t)(mwk::launch_count() - l0);
-    std::sort(used.begin(), used.end());
-    used.erase(std::unique(used.begin(), used.end()), used.end());
-    for (void* p : used) ++c->graph_refs[p];
-    g->bufs = std::move(used);
-    ctx_retain(c);
-    *out = g.release();
-    return MW_OK;
-}
-
-mw_status mw_graph_capture(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
-                           void* stream, mw_graph** out) {
-    return mw_graph_capture_many(c, root, args, nargs, 1, stream, out);
-}
-
-mw_status mw_graph_launch(mw_graph* g, void* stream) {
-    if (!g || !g->exec) return fail(MW_E_STATE, "invalid graph");
-    CUDA_OK(cudaSetDevice(g->ctx->device));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    MW_OK_OR_RETURN(fifo_enter(g->ctx, s));
-    CUDA_OK(cudaGraphLaunch(g->exec, s));
-    fifo_exit(g->ctx, s);
-    return MW_OK;
-}
-
-mw_status mw_graph_result(mw_graph* g, double* out, int32_t n) {
-    if (!g || !out) return fail(MW_E_STATE, "invalid graph");
-    g->f.waited = true;   // the caller synchronised the launch stream
-    return mw_future_result(&g->f, out, n);
-}
-
-mw_status mw_graph_kernels(const mw_graph* g, int64_t* out) {
-    if (!g || !out) return fail(MW_E_STATE, "invalid graph");
-    *out = g->kernels;
-    return MW_OK;
-}
-
-mw_status mw_graph_destroy(mw_graph* g) {
-    if (!g) return fail(MW_E_STATE, "NULL graph");
-    cudaSetDevice(g->ctx->device);
-    cudaDeviceSynchronize();
-    if (g->exec) cudaGraphExecDestroy(g->exec);
-    if (g->graph) cudaGraphDestroy(g->graph);
-    if (g->f.res) cudaFreeHost(g->f.res);
-    mw_ctx* c = g->ctx;
-    for (void* p : g->bufs) {
-        auto it = c->graph_refs.find(p);
-        if (it == c->graph_refs.end() || --it->second > 0) continue;
-        c->graph_refs.erase(it);
-        auto o = std::find(c->orphans.begin(), c->orphans.end(), p);
-        if (o != c->orphans.end()) {   // replaced while the graph lived: free it now
-            c->orphans.erase(o);
-            ctx_free(c, p);
-        }
-    }
-    delete g;
-    ctx_release(c);
-    return MW_OK;
-}
-
-
-// ------------------------------------------------------------ profile building
-// Arguments a run updates in place (Saxpy y, N-body state): profile
-// building runs the tree many times and restores them afterwards.
-struct Snapshots {
-    mw_ctx* c;
-    cudaStream_t s;
-    std::vector<std::pair<const mw_arg*, void*>> snaps;
-    static size_t bytes_of(const mw_arg& a) {
-        int64_t n = a.mode == MW_COPY ? a.shape[0] : a.local_rows;
-        return (size_t)(n * row_bytes(a));
-    }
-    mw_status take(const Node* r, const mw_arg* args, int nargs) {
-        std::vector<int> inplace;
-        const int ik = r->in_kind, ok = r->out_kind;
-        if (ik == MW_VK_SAXPY && nargs == 2) inplace = {1};
-        if (ik == MW_VK_NBODY && ok == MW_VK_NBODY && nargs == 2) inplace = {0, 1};
-        for (int i : inplace) {
-            void* p;
-            MW_OK_OR_RETURN(scratch(c, "autotune_snap" + std::to_string(i), bytes_of(args[i]) + 16, s, &p));
-            CUDA_OK(cudaMemcpyAsync(p, args[i].ptr, bytes_of(args[i]), cudaMemcpyDefault, s));
-            snaps.push_back({&args[i], p});
-        }
-        return MW_OK;
-    }
-    mw_status restore() {
-        for (auto& sn : snaps)
-            CUDA_OK(cudaMemcpyAsync(sn.first->ptr, sn.second, bytes_of(*sn.first), cudaMemcpyDefault, s));
-        return MW_OK;
-    }
-};
-
-mw_status mw_autotune(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
-                      void* stream, int32_t reps, mw_kb* kb, int32_t* tune_out, double* best_ms) {
-    if (!c || !root || (nargs > 0 && !args) || reps < 1) return fail(MW_E_INVALID_SPEC, "bad argument");
-    if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
-    CUDA_OK(cudaSetDevice(c->device));
-    (void)cudaGetLastError();   // see mw_run
-    const Node* r = reinterpret_cast<const Node*>(root);
-    std::vector<Step> prog;
-    MW_OK_OR_RETURN(mw::plan(r, &prog));
-    bool has_rgba = false, has_stencil = false, has_nbody = false, has_u8 = false;
-    for (const Step& st : prog) {
-        has_u8 |= st.kind == StepKind::U8;
-        has_rgba |= st.kind == StepKind::Rgba;
-        has_stencil |= st.kind == StepKind::StencilFor || st.kind == StepKind::StencilWhile;
-        has_nbody |= st.kind == StepKind::NbodyLoop || st.kind == StepKind::NbodyAccel;
-    }
-    using Tune = std::vector<int>;
-    const Tune base(c->tune, c->tune + mwk::TUNE_COUNT);
-    std::vector<Tune> cands{base};
-    if (has_rgba) {
-        for (int tma = 0; tma <= 9; ++tma)
-            for (int un : {2, 4, 8}) {
-                if (tma > 0 && un != base[mwk::TUNE_RGBA_UNROLL]) continue;
-                Tune t = base;
-                t[mwk::TUNE_RGBA_TMA] = tma;
-                t[mwk::TUNE_RGBA_UNROLL] = un;
-                cands.push_back(t);
-            }
-    }
-    if (has_stencil) {
-        const int pairs[7][2] = {{4, 32}, {6, 32}, {8, 32}, {8, 40}, {12, 40}, {6, 48}, {8, 48}};
-        Tune t = base;
-        t[mwk::TUNE_HYST_PLANES] = 0;
-        cands.push_back(t);
-        for (auto& pr : pairs) {
-            Tune u = base;
-            u[mwk::TUNE_HYST_PLANES] = 1;
-            u[mwk::TUNE_HYST_T] = pr[0];
-            u[mwk::TUNE_HYST_ROWS] = pr[1];
-            cands.push_back(u);
-        }
-    }
-    if (has_u8)
-        for (int v : {0, 1}) {
-            Tune t = base;
-            t[mwk::TUNE_U8_TMA] = v;
-            cands.push_back(t);
-        }
-    if (has_nbody)
-        for (int sp : {0, 1}) {
-            Tune t = base;
-            t[mwk::TUNE_NBODY_SPLIT] = sp;
-            cands.push_back(t);
-        }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    MW_OK_OR_RETURN(fifo_enter(c, s));
-    Snapshots snap{c, s, {}};
-    MW_OK_OR_RETURN(snap.take(r, args, nargs));
-    auto restore = [&]() -> mw_status { return snap.restore(); };
-    cudaEvent_t e0, e1;
-    CUDA_OK(cudaEventCreate(&e0));
-    CUDA_OK(cudaEventCreate(&e1));
-    mw_future f;
-    f.ctx = c;
-    double tmp[4] = {0, 0, 0, 0};
-    f.res = tmp;   // host memory is fine: results are only written by D2H copies we sync on
-    double best = 1e300;
-    Tune best_t = base;
-    mw_status st = MW_OK;
-    for (const Tune& t : cands) {
-        for (int k = 0; k < mwk::TUNE_COUNT; ++k) c->tune[k] = t[k];
-        st = run(c, r, args, nargs, s, &f);   // warm-up (allocates scratch)
-        if (st != MW_OK) break;
-        CUDA_OK(cudaEventRecord(e0, s));
-        for (int i = 0; i < reps && st == MW_OK; ++i) st = run(c, r, args, nargs, s, &f);
-        if (st != MW_OK) break;
-        CUDA_OK(cudaEventRecord(e1, s));
-        CUDA_OK(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
-        const double per = (double)ms / reps;
-        if (per < best) {
-            best = per;
-            best_t = t;
-        }
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    for (int k = 0; k < mwk::TUNE_COUNT; ++k) c->tune[k] = best_t[k];
-    MW_OK_OR_RETURN(restore());
-    fifo_exit(c, s);
-    CUDA_OK(cudaStreamSynchronize(s));
-    if (st != MW_OK) return st;
-    if (kb) {
-        std::vector<int64_t> dims(args[0].shape, args[0].shape + args[0].ndim);
-        MW_OK_OR_RETURN(mw_kb_store(kb, root, dims.data(), (int32_t)dims.size(), best_t.data(),
-                                    c->dist.data(), c->P, best, MW_PROV_BUILT));
-    }
-    if (tune_out)
-        for (int k = 0; k < mwk::TUNE_COUNT; ++k) tune_out[k] = best_t[k];
-    if (best_ms) *best_ms = best;
-    return MW_OK;
-}
-
-
-// ------------------------------------------------------------ device classes (NEXT-4)
-mw_status mw_ctx_set_device_class(mw_ctx* c, int32_t part, int32_t cls, double rel_perf) {
-    if (!c) return fail(MW_E_STATE, "NULL ctx");
-    if (part < 0 || part >= c->P || cls < 0 || !(rel_perf > 0.0) || !std::isfinite(rel_perf))
-        return fail(MW_E_INVALID_SPEC, "bad partition, class or relative performance");
-    c->cls[part] = cls;
-    c->relperf[part] = rel_perf;
-    // the static distribution is proportional to relative performance
-    double tot = 0.0;
-    for (double x : c->relperf) tot += x;
-    for (int i = 0; i < c->P; ++i) c->dist[i] = c->relperf[i] / tot;
-    return MW_OK;
-}
-
-void mw_profile_defaults(mw_profile_params* p) {
-    if (!p) return;
-    p->executions = 3;
-    p->precision_ms = 0.0;
-    p->max_dist_iters = 10;
-}
-
-}  // extern "C"
-
-namespace {
-
-// Per-partition compute times of the last run (this rank's view after the
-// collective all-gather), for the workload distribution generator.
-mw_status part_times(mw_ctx* c, std::vector<float>& ms) {
-    ms.assign(c->P, 0.f);
-    return mw_last_timings(c, ms.data(), c->P, nullptr);
-}
-
-// Workload distribution generator of Alg. 1: a binary search
-// that moves load between two device types — class A (the class of the
-// first partition) and the others.  The transferable share starts at 1,
-// each iteration splits it evenly, binds one half to the type that
-// performed better and keeps the other half transferable
-// (transferableSize(n) = 1/2^n).  Inside a type the share follows the
-// partitions' relative performance.  With one type it yields the
-// relative-performance distribution once.
-struct DistGen {
-    const mw_ctx* c;
-    int clsA = 0;
-    bool two = false;
-    double boundA = 0.0, boundB = 0.0, T = 1.0;
-    int iter = 0;
-    double lastA = 0.0;
-    explicit DistGen(const mw_ctx* c_) : c(c_) {
-        clsA = c->cls[0];
-        for (int p = 0; p < c->P; ++p) two |= c->cls[p] != clsA;
-    }
-    bool done(int max_iters) const { return two ? iter >= max_iters : iter >= 1; }
-    std::vector<double> next() {
-        const double shareA = two ? boundA + T / 2 : 0.0;
-        lastA = shareA;
-        ++iter;
-        std::vector<double> d(c->P, 0.0);
-        double ra = 0.0, rb = 0.0;
-        for (int p = 0; p < c->P; ++p) (c->cls[p] == clsA ? ra : rb) += c->relperf[p];
-        for (int p = 0; p < c->P; ++p) {
-            if (!two) d[p] = c->relperf[p] / ra;
-            else if (c->cls[p] == clsA) d[p] = shareA * c->relperf[p] / ra;
-            else d[p] = (1.0 - shareA) * c->relperf[p] / rb;
-        }
-        return d;
-    }
-    // per-type compute time of the proposal: the half goes to the faster type
-    void feed(const std::vector<float>& ms) {
-        if (!two) return;
-        double ta = 0.0, tb = 0.0;
-        for (int p = 0; p < c->P; ++p) (c->cls[p] == clsA ? ta : tb) = std::max(c->cls[p] == clsA ? ta : tb, (double)ms[p]);
-        if (ta <= tb) boundA += T / 2;
-        else boundB += T / 2;
-        T /= 2;
-    }
-};
-
-// One knob dimension of the configuration space: candidate settings, most
-// likely first (P:555-565 ordering).
-using Setting = std::vector<std::pair<int, int>>;
-std::vector<std::vector<Setting>> config_dims(const mw_ctx* c, const std::vector<Step>& prog) {
-    bool rgba = false, u8 = false, stencil = false, nbody = false;
-    for (const Step& st : prog) {
-        rgba |= st.kind == StepKind::Rgba;
-        u8 |= st.kind == StepKind::U8;
-        stencil |= st.kind == StepKind::StencilFor || st.kind == StepKind::StencilWhile;
-        nbody |= st.kind == StepKind::NbodyLoop || st.kind == StepKind::NbodyAccel;
-    }
-    std::vector<std::vector<Setting>> dims;
-    auto ordered = [&](int knob, std::vector<int> vals) {
-        std::vector<Setting> d{{{knob, c->tune[knob]}}};
-        for (int v : vals)
-            if (v != c->tune[knob]) d.push_back({{knob, v}});
-        dims.push_back(d);
-    };
-    if (rgba) ordered(mwk::TUNE_RGBA_TMA, {1, 9, 5, 6, 3, 2, 4, 8, 7, 0});
-    if (u8 && !stencil) ordered(mwk::TUNE_U8_TMA, {1, 0});
-    if (stencil) {
-        std::vector<Setting> d;
-        d.push_back({{mwk::TUNE_HYST_PLANES, 1}, {mwk::TUNE_HYST_T, c->tune[mwk::TUNE_HYST_T]},
-                     {mwk::TUNE_HYST_ROWS, c->tune[mwk::TUNE_HYST_ROWS]}});
-        const int pairs[7][2] = {{8, 48}, {8, 40}, {6, 48}, {12, 40}, {6, 32}, {8, 32}, {4, 32}};
-        for (auto& pr : pairs)
-            if (pr[0] != c->tune[mwk::TUNE_HYST_T] || pr[1] != c->tune[mwk::TUNE_HYST_ROWS])
-                d.push_back({{mwk::TUNE_HYST_PLANES, 1}, {mwk::TUNE_HYST_T, pr[0]}, {mwk::TUNE_HYST_ROWS, pr[1]}});
-        d.push_back({{mwk::TUNE_HYST_PLANES, 0}});
-        dims.push_back(d);
-        if (c->ppr > 1) ordered(mwk::TUNE_HYST_FUSED, {1, 0});
-    }
-    if (nbody) ordered(mwk::TUNE_NBODY_SPLIT, {0, 1});
-    return dims;
-}
-
-std::string wl_key(const mw_node* root, const mw_arg* args) {
-    uint8_t id[32];
-    mw_node_id(root, id);
-    std::string k(reinterpret_cast<const char*>(id), 32);
-    for (int d = 0; d < args[0].ndim; ++d) k += ":" + std::to_string(args[0].shape[d]);
-    return k;
-}
-
-}  // namespace
-
-extern "C" {
-
-// Alg. 1 over the B200 configuration space: nested knob
-// dimensions with the discard rule, the binary-search distribution
-// generator innermost, store-if-better with the precision stop.
-mw_status mw_profile_build(mw_ctx* c, const mw_node* root, const mw_arg* args, int32_t nargs,
-                           void* stream, const mw_profile_params* pp, mw_kb* kb, int32_t* tune_out,
-                           double* fractions_out, int32_t nfrac, double* best_ms, int32_t* runs_out) {
-    if (!c || !root || (nargs > 0 && !args) || nargs < 1) return fail(MW_E_INVALID_SPEC, "bad argument");
-    if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
-    if (fractions_out && nfrac < c->P) return fail(MW_E_INVALID_SPEC, "fractions_out too small");
-    mw_profile_params prm;
-    mw_profile_defaults(&prm);
-    if (pp) prm = *pp;
-    if (prm.executions < 1 || prm.max_dist_iters < 1 || !(prm.precision_ms >= 0.0))
-        return fail(MW_E_INVALID_SPEC, "bad profile parameters");
-    CUDA_OK(cudaSetDevice(c->device));
-    (void)cudaGetLastError();
-    const Node* r = reinterpret_cast<const Node*>(root);
-    std::vector<Step> prog;
-    MW_OK_OR_RETURN(mw::plan(r, &prog));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    MW_OK_OR_RETURN(fifo_enter(c, s));
-    Snapshots snap{c, s, {}};
-    MW_OK_OR_RETURN(snap.take(r, args, nargs));
-    const bool mon0 = c->monitor;
-    c->monitor = true;   // the generator needs per-partition times
-    const std::vector<int> tune0(c->tune, c->tune + mwk::TUNE_COUNT);
-    const std::vector<double> dist0 = c->dist;
-    cudaEvent_t e0, e1;
-    CUDA_OK(cudaEventCreate(&e0));
-    CUDA_OK(cudaEventCreate(&e1));
-    mw_future f;
-    f.ctx = c;
-    double tmp[4] = {0, 0, 0, 0};
-    f.res = tmp;
-    double best = 1e300;
-    std::vector<int> best_t = tune0;
-    std::vector<double> best_d = dist0;
-    int runs = 0;
-    mw_status st = MW_OK;
-    // exec_for_profile (step 13): warm-up + `executions` runs, mean time
-    auto exec = [&](double* ms_out, std::vector<float>& parts) -> mw_status {
-        MW_OK_OR_RETURN(run(c, r, args, nargs, s, &f));
-        CUDA_OK(cudaEventRecord(e0, s));
-        for (int i = 0; i < prm.executions; ++i) MW_OK_OR_RETURN(run(c, r, args, nargs, s, &f));
-        CUDA_OK(cudaEventRecord(e1, s));
-        CUDA_OK(cudaEventSynchronize(e1));
-        runs += 1 + prm.executions;
-        float ms = 0.f;
-        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
-        *ms_out = (double)ms / prm.executions;
-        MW_OK_OR_RETURN(part_times(c, parts));
-        // Partitions sharing a device (ppr > 1) stand in for devices of their
-        // own, which would run concurrently: the execution time of a
-        // configuration is then the makespan, the longest partition's compute
-        // time (the sum the shared stream takes is not what a multi-device
-        // run would see).
-        if (c->ppr > 1) *ms_out = (double)*std::max_element(parts.begin(), parts.end());
-        return MW_OK;
-    };
-    // steps 9-20 for the current platform configuration: returns the best
-    // time this configuration reached
-    auto dist_search = [&]() -> double {
-        DistGen gen(c);
-        double here = 1e300;
-        std::vector<float> parts;
-        while (st == MW_OK && !gen.done(prm.max_dist_iters)) {
-            const std::vector<double> d = gen.next();
-            if (mw::check_distribution(d.data(), c->P) != MW_OK) break;
-            c->dist = d;
-            double t = 0.0;
-            st = exec(&t, parts);
-            if (st != MW_OK) break;
-            here = std::min(here, t);
-            if (getenv("MW_PROFILE_TRACE")) {
-                fprintf(stderr, "profile: tune");
-                for (int k = 0; k < mwk::TUNE_COUNT; ++k) fprintf(stderr, " %d", c->tune[k]);
-                fprintf(stderr, " dist");
-                for (double x : d) fprintf(stderr, " %.4f", x);
-                fprintf(stderr, " ms %.4f parts", t);
-                for (float x : parts) fprintf(stderr, " %.4f", x);
-                fprintf(stderr, "\n");
-            }
-            gen.feed(parts);
-            const double stored = best;
-            if (t < stored) {   // store_profile (step 16)
-                best = t;
-                best_t.assign(c->tune, c->tune + mwk::TUNE_COUNT);
-                best_d = d;
-                if (stored - t < prm.precision_ms) break;   // step 17
-            } else {
-                break;
-            }
-        }
-        return here;
-    };
-    const std::vector<std::vector<Setting>> dims = config_dims(c, prog);
-    // nested configuration loops with the discard rule (steps 21, 23, 25):
-    // a value that does not improve on the previous one discards the rest
-    std::function<double(size_t)> search = [&](size_t level) -> double {
-        if (level == dims.size()) return dist_search();
-        double prev = 1e300, here = 1e300;
-        for (const Setting& v : dims[level]) {
-            if (st != MW_OK) break;
-            for (auto& kv : v) c->tune[kv.first] = kv.second;
-            const double t = search(level + 1);
-            here = std::min(here, t);
-            if (!(t < prev)) break;
-            prev = t;
-        }
-        return here;
-    };
-    search(0);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    for (int k = 0; k < mwk::TUNE_COUNT; ++k) c->tune[k] = best < 1e300 ? best_t[k] : tune0[k];
-    c->dist = best < 1e300 ? best_d : dist0;
-    c->monitor = mon0;
-    MW_OK_OR_RETURN(snap.restore());
-    fifo_exit(c, s);
-    CUDA_OK(cudaStreamSynchronize(s));
-    if (st != MW_OK) return st;
-    if (kb) {
-        std::vector<int64_t> dimsv(args[0].shape, args[0].shape + args[0].ndim);
-        MW_OK_OR_RETURN(mw_kb_store(kb, root, dimsv.data(), (int32_t)dimsv.size(), c->tune, c->dist.data(), c->P,
-                                    best, MW_PROV_BUILT));
-    }
-    if (tune_out)
-        for (int k = 0; k < mwk::TUNE_COUNT; ++k) tune_out[k] = c->tune[k];
-    if (fractions_out)
-        for (int i = 0; i < c->P; ++i) fractions_out[i] = c->dist[i];
-    if (best_ms) *best_ms = best;
-    if (runs_out) *runs_out = runs;
-    return MW_OK;
-}
-
-void mw_managed_defaults(mw_managed_params* p) {
-    if (!p) return;
-    mw_balance_defaults(&p->balance);
-    p->build_profiles = 0;
-    mw_profile_defaults(&p->profile);
-}
-
-// Persist the previous managed run's attained result (its wall time with
-// the configuration it ran) with the process that produced it.
-static mw_status managed_persist(mw_ctx* c) {
-    if (!c->m_pending || !c->m_kb) return MW_OK;
-    c->m_pending = false;
-    float wall = 0.f;
-    MW_OK_OR_RETURN(mw_last_timings(c, nullptr, 0, &wall));
-    return mw_kb_store(c->m_kb, c->m_root, c->m_dims.data(), (int32_t)c->m_dims.size(), c->tune, c->dist.data(),
-                       c->P, (double)wall, c->m_prov);
-}
-
-// Fig. 5: the decision process around a run request.
-mw_status mw_run_managed(mw_ctx* c, mw_kb* kb, const mw_managed_params* mp, const mw_node* root,
-                         const mw_arg* args, int32_t nargs, void* stream, mw_future** out,
-                         int32_t* action) {
-    if (!c || !kb || !root || !out || nargs < 1 || !args) return fail(MW_E_INVALID_SPEC, "NULL argument");
-    if (c->destroyed) return fail(MW_E_STATE, "ctx was destroyed");
-    mw_managed_params prm;
-    mw_managed_defaults(&prm);
-    if (mp) prm = *mp;
-    if (!c->monitor) return fail(MW_E_STATE, "managed runs need monitoring (mw_ctx_set_monitoring)");
-    const std::string key = wl_key(root, args);
-    const std::vector<int64_t> dims(args[0].shape, args[0].shape + args[0].ndim);
-    int act = MW_MANAGED_RECURRENT;
-    if (c->m_pending && c->m_kb == kb && key == c->mkey) {
-        // recurrent (SCT, workload): persist the last result, assess balance
-        MW_OK_OR_RETURN(managed_persist(c));
-        int32_t trig = 0;
-        MW_OK_OR_RETURN(mw_rebalance(c, &prm.balance, &trig));
-        int32_t found = 0, prov = 0;
-        double ms = 0.0;
-        MW_OK_OR_RETURN(mw_kb_find(kb, root, dims.data(), (int32_t)dims.size(), &found, &prov, &ms));
-        if (prm.build_profiles && trig && !(found && prov == MW_PROV_BUILT)) {
-            // "Build SCT profile": only once per (SCT, workload), when asked for
-            MW_OK_OR_RETURN(mw_profile_build(c, root, args, nargs, stream, &prm.profile, kb, nullptr, nullptr, 0,
-                                             nullptr, nullptr));
-            c->bstate = mw_balance_state{};
-            act = MW_MANAGED_BUILT;
-            c->m_prov = MW_PROV_BUILT;
-        } else if (trig) {
-            act = MW_MANAGED_ADJUSTED;   // "Adjust workload distribution"
-            c->m_prov = MW_PROV_BALANCED;
-        }
-    } else {
-        // new (SCT, workload): "Derive work distribution" from the KB
-        if (c->m_kb) MW_OK_OR_RETURN(managed_persist(c));
-        int32_t scope = MW_KB_NONE;
-        std::vector<int32_t> tune(c->tune, c->tune + mwk::TUNE_COUNT);
-        std::vector<double> fr(c->P);
-        MW_OK_OR_RETURN(mw_kb_lookup(kb, root, dims.data(), (int32_t)dims.size(), tune.data(), fr.data(), c->P,
-                                     &scope));
-        if (scope != MW_KB_NONE) {
-            for (int k = 0; k < mwk::TUNE_COUNT; ++k)
-                if (mwk::tune_valid(k, tune[k])) c->tune[k] = tune[k];
-            if (mw::check_distribution(fr.data(), c->P) == MW_OK) c->dist = fr;
-            act = scope == MW_KB_EXACT ? MW_MANAGED_FROM_KB : MW_MANAGED_DERIVED;
-        } else {
-            act = MW_MANAGED_NO_KNOWLEDGE;
-        }
-        c->m_prov = MW_PROV_DERIVED;
-        c->bstate = mw_balance_state{};
-        c->mkey = key;
-        c->m_kb = kb;
-        if (c->m_root != root) {   // keep the tree alive for the deferred KB store
-            mw_node_retain(const_cast<mw_node*>(root));
-            if (c->m_root) mw_node_release(const_cast<mw_node*>(c->m_root));
-            c->m_root = root;
-        }
-        c->m_dims = dims;
-    }
-    MW_OK_OR_RETURN(mw_run(c, root, args, nargs, stream, out));
-    c->m_pending = true;
-    if (action) *action = act;
-    return MW_OK;
-}
-
-mw_status mw_managed_flush(mw_ctx* c) {
-    if (!c) return fail(MW_E_STATE, "NULL ctx");
-    return managed_persist(c);
-}
 
 }  // extern "C"

@@ -379,9 +379,6 @@ class Saxpy(Workload):
             self.graph.launch(self.stream)
         return []
 
-    def step(self, i):
-        raise NotImplementedError
-
     def config(self):
         return {"workload": self.name, "n": self.L, "a": 2.5, "l2": self.l2_note,
                 "launch": "one CUDA graph replaying the rotating-buffer runs back to back "

@@ -1073,14 +1073,13 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // and a rolled execution loop beats smem-resident K and a fully unrolled
 // shrinking-window loop, whose code no longer fits the instruction cache.)
 // One execution on register rows [LO, HI] (rows outside keep their values
-// and only serve as neighbours); returns whether an owned row [T, ROWS - T)
-// of an owned lane changed.
-// One execution on register rows [LO, HI] (rows outside keep their values
-// and only serve as neighbours); returns whether an owned row [T, ROWS - T)
-// of an owned lane changed.
+// and only serve as neighbours).  Returns bit 0: an owned row [T, ROWS - T)
+// of an owned lane changed; bit 1: a bit of the window inside `vm` changed.
+// vm masks off the bits of lanes 0/31 whose value is no longer exact (their
+// missing outer neighbour: one bit per execution from the far end).
 template <int T, int ROWS, int LO, int HI>
-__device__ __forceinline__ bool plane_exec(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
-                                           bool own_lane) {
+__device__ __forceinline__ int plane_exec(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
+                                          bool own_lane, uint32_t vm) {
     auto hrow = [&](uint32_t sx) {
         // lanes 0/31 take their own word as the outer neighbour: the error
         // enters at their far bits and moves one bit per execution, never
@@ -1090,17 +1089,19 @@ __device__ __forceinline__ bool plane_exec(uint32_t (&sv)[ROWS], const uint32_t 
         return sx | __funnelshift_l(l, sx, 1) | __funnelshift_r(sx, r, 1);
     };
     uint32_t hp = hrow(sv[LO - 1]), hc = hrow(sv[LO]);
-    uint32_t ch = 0;
+    uint32_t ch = 0, ca = 0;
 #pragma unroll
     for (int i = LO; i <= HI; ++i) {
         const uint32_t hn = hrow(sv[i + 1]);     // old row i+1 (not yet updated)
         const uint32_t s2 = sv[i] | (kv[i] & (hp | hc | hn));
         if (i >= T && i < ROWS - T) ch |= s2 ^ sv[i];
+        else ca |= s2 ^ sv[i];
         sv[i] = s2;
         hp = hc;
         hc = hn;
     }
-    return __any_sync(0xffffffffu, own_lane && ch != 0);
+    const bool any = ((ch | ca) & vm) != 0;
+    return (__any_sync(0xffffffffu, own_lane && ch != 0) ? 1 : 0) | (__any_sync(0xffffffffu, any) ? 2 : 0);
 }
 
 // T executions on a register tile (rows [ybase, ybase + ROWS) x lanes).
@@ -1110,28 +1111,55 @@ __device__ __forceinline__ bool plane_exec(uint32_t (&sv)[ROWS], const uint32_t 
 // in the rest (a superset of what each later execution needs); executions
 // run in pairs so the updated rows alternate between two register sets
 // instead of being moved back every execution.
+// Early stop: the positions still exact after execution j+1 shrink by the
+// stencil radius per execution (V_{j+1} within V_j), and their values depend
+// only on V_j.  When execution j+1 changes nothing on (a superset of) V_{j+1},
+// the true iterates j and j+1 agree there, hence by induction every later
+// iterate agrees with iterate j on the smaller V_m, which contains the owned
+// region: the remaining executions of the pass cannot change an owned bit,
+// and the registers already hold the pass's result there.
 // Returns the last execution (0-based) that changed an owned bit.
 template <int T, int ROWS>
 __device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
-                                           int steps, bool own_lane) {
+                                           int steps, bool own_lane, int lane) {
     int tile_last = -1;
+    // exact bits of this lane after the next execution (lanes 0/31 lose one
+    // bit per execution at their far end)
+    const int shl = lane == 0, shr = lane == 31;
+    uint32_t vm = ~0u;
     if (T % 4 == 0 && steps == T) {
         constexpr int H = T / 2;
 #pragma unroll 1
         for (int st = 0; st < H; st += 2) {
-            if (plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane)) tile_last = st;
-            if (plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane)) tile_last = st + 1;
+            vm = (vm << shl) >> shr;
+            int r = plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane, vm);
+            if (r & 1) tile_last = st;
+            if (!(r & 2)) return tile_last;
+            vm = (vm << shl) >> shr;
+            r = plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane, vm);
+            if (r & 1) tile_last = st + 1;
+            if (!(r & 2)) return tile_last;
         }
 #pragma unroll 1
         for (int st = H; st < T; st += 2) {
-            if (plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane)) tile_last = st;
-            if (plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane)) tile_last = st + 1;
+            vm = (vm << shl) >> shr;
+            int r = plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane, vm);
+            if (r & 1) tile_last = st;
+            if (!(r & 2)) return tile_last;
+            vm = (vm << shl) >> shr;
+            r = plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane, vm);
+            if (r & 1) tile_last = st + 1;
+            if (!(r & 2)) return tile_last;
         }
         return tile_last;
     }
 #pragma unroll 1
-    for (int st = 0; st < steps; ++st)
-        if (plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane)) tile_last = st;
+    for (int st = 0; st < steps; ++st) {
+        vm = (vm << shl) >> shr;
+        const int r = plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane, vm);
+        if (r & 1) tile_last = st;
+        if (!(r & 2)) break;
+    }
     return tile_last;
 }
 
@@ -1255,7 +1283,7 @@ __device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUt
         if (tn < n_tiles) issue(tn);
         const int64_t strip = t / n_cb, cb = t - strip * n_cb;
         const int64_t w = cb * OW - 1 + lane;
-        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
+        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane, lane);
         // bit 0: changed in the last execution of the pass (fronts still alive);
         // bit 1: changed at all.  last_bit = false: bit 0 = bit 1 (the looser
         // any-change rule; both kernels use the tight one — boundary strips of
@@ -1542,7 +1570,7 @@ __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, in
         if (tn < a.total) issue(tn);
         const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
         const int64_t w = cb * OW - 1 + lane;
-        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane);
+        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane, lane);
         const uint8_t fl = tl < 0 ? 0 : (tl == steps - 1 ? 3 : 2);
         my_last = max(my_last, tl);
         const bool wv = w >= 0 && w < a.wp;

@@ -828,7 +828,7 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
             MW_OK_OR_RETURN(scratch(c, "plane_k", pb, R.s, &kk));
             MW_OK_OR_RETURN(scratch(c, "plane_flags", 64, R.s, &fl));
             void* tf;
-            MW_OK_OR_RETURN(scratch(c, "plane_tflags", (size_t)(2 * mwk::planes_tiles(rows, W)), R.s, &tf));
+            MW_OK_OR_RETURN(scratch(c, "plane_act", (size_t)(4 * (mwk::planes_tiles(rows, W) + 1)), R.s, &tf));
             uint32_t* S0 = static_cast<uint32_t*>(s0);
             uint32_t* S1 = static_cast<uint32_t*>(s1);
             uint32_t* K = static_cast<uint32_t*>(kk);
@@ -856,7 +856,7 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
             {
                 PartTimer t(c, R.s, p0, MW_KC_STENCIL);
                 MW_OK_OR_RETURN(kerr(mwk::planes_loop(S0, S1, K, rows, W, prog[1].n, flags, state,
-                                                      static_cast<uint8_t*>(tf), L),
+                                                      static_cast<uint32_t*>(tf), L),
                                      "planes_loop"));
             }
             {

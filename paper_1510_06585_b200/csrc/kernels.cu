@@ -1121,8 +1121,13 @@ __device__ __forceinline__ int plane_exec(uint32_t (&sv)[ROWS], const uint32_t (
 // Returns the last execution (0-based) that changed an owned bit.
 template <int T, int ROWS>
 __device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t (&kv)[ROWS],
-                                           int steps, bool own_lane, int lane) {
+                                           int steps, bool own_lane, int lane, int* nexec = nullptr) {
     int tile_last = -1;
+    int ne = 0;
+    struct Cnt {   // executions run (diagnostics: MW_HYST_PROF)
+        int* p; int& n;
+        __device__ ~Cnt() { if (p) *p = n; }
+    } cnt{nexec, ne};
     // exact bits of this lane after the next execution (lanes 0/31 lose one
     // bit per execution at their far end)
     const int shl = lane == 0, shr = lane == 31;
@@ -1132,10 +1137,12 @@ __device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t 
 #pragma unroll 1
         for (int st = 0; st < H; st += 2) {
             vm = (vm << shl) >> shr;
+            ++ne;
             int r = plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane, vm);
             if (r & 1) tile_last = st;
             if (!(r & 2)) return tile_last;
             vm = (vm << shl) >> shr;
+            ++ne;
             r = plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane, vm);
             if (r & 1) tile_last = st + 1;
             if (!(r & 2)) return tile_last;
@@ -1143,10 +1150,12 @@ __device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t 
 #pragma unroll 1
         for (int st = H; st < T; st += 2) {
             vm = (vm << shl) >> shr;
+            ++ne;
             int r = plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane, vm);
             if (r & 1) tile_last = st;
             if (!(r & 2)) return tile_last;
             vm = (vm << shl) >> shr;
+            ++ne;
             r = plane_exec<T, ROWS, H + 1, ROWS - 2 - H>(sv, kv, own_lane, vm);
             if (r & 1) tile_last = st + 1;
             if (!(r & 2)) return tile_last;
@@ -1156,6 +1165,7 @@ __device__ __forceinline__ int plane_steps(uint32_t (&sv)[ROWS], const uint32_t 
 #pragma unroll 1
     for (int st = 0; st < steps; ++st) {
         vm = (vm << shl) >> shr;
+        ++ne;
         const int r = plane_exec<T, ROWS, 1, ROWS - 2>(sv, kv, own_lane, vm);
         if (r & 1) tile_last = st;
         if (!(r & 2)) break;
@@ -1236,7 +1246,8 @@ __device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUt
                                                int top_nbr, int bot_nbr, int64_t gw,
                                                int64_t nwarps, int lane, uint32_t* sb,
                                                uint32_t* kb, uint64_t* bar, uint32_t& phase,
-                                               bool last_bit = false) {
+                                               bool last_bit = false,
+                                               unsigned long long* pstat = nullptr) {
     constexpr int R = ROWS - 2 * T;
     constexpr int OW = 30;
     constexpr int BW = 36;                          // box width (words)
@@ -1283,7 +1294,12 @@ __device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUt
         if (tn < n_tiles) issue(tn);
         const int64_t strip = t / n_cb, cb = t - strip * n_cb;
         const int64_t w = cb * OW - 1 + lane;
-        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane, lane);
+        int ne = 0;
+        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane, lane, pstat ? &ne : nullptr);
+        if (pstat && lane == 0) {
+            atomicAdd(pstat, (unsigned long long)ne);
+            atomicAdd(pstat + 32, 1ull);
+        }
         // bit 0: changed in the last execution of the pass (fronts still alive);
         // bit 1: changed at all.  last_bit = false: bit 0 = bit 1 (the looser
         // any-change rule; both kernels use the tight one — boundary strips of
@@ -1300,6 +1316,110 @@ __device__ __forceinline__ int plane_pass_warp(const CUtensorMap* tin, const CUt
 // The per-warp slots of shared memory: [8][2][ROWS][36] words, then 8 mbarriers.
 template <int ROWS>
 constexpr size_t plane_smem_bytes() { return 8 * 2 * ROWS * 36 * 4 + 8 * 8; }
+// The one-partition loop keeps TWO slots per warp: [8][2 slots][2][ROWS][36]
+// words, then 16 mbarriers (221 KiB at ROWS = 48).
+template <int ROWS>
+constexpr size_t plane_loop_smem_bytes() { return 8 * 2 * 2 * ROWS * 36 * 4 + 16 * 8; }
+
+// One pass of the one-partition loop for one warp.  Activity is PUSHED: a
+// tile that changed an owned bit stamps itself for the next pass (its newest
+// state must reach the other buffer), and one still changing in the last
+// execution (a live front, which moves at most T <= R rows / 30 words in the
+// next pass) stamps its 3x3 tile neighbourhood.  act[t] == stamp: t is
+// active in this pass (stamps are unique per pass and run, so nothing is ever
+// cleared; a stale equal value could only add work, never change a result:
+// a processed tile computes the same iterates from the buffer).  The warp
+// reads the stamps of its tiles (gw + i nwarps) 32 at a time, so the active
+// list is known up front (no per-tile flag scan on the critical path), and
+// keeps two tiles in flight in its two slots — in the sparse late passes a
+// tile runs 1-2 executions, too few to hide a tile load behind.  (Measured:
+// a global queue of the pass's active tiles claimed with atomics — dynamic
+// balance — made every pass ~2x slower: one hot counter for ~10^4 claims.)
+template <int T, int ROWS>
+__device__ __forceinline__ int plane_loop_pass_warp(const CUtensorMap* tin, const CUtensorMap* tk,
+                                                    uint32_t* __restrict__ out, int64_t rows,
+                                                    int64_t wp, int steps, uint32_t* __restrict__ act,
+                                                    uint32_t stamp, bool all_active, int64_t gw,
+                                                    int64_t nwarps, int lane, uint32_t* slots,
+                                                    uint64_t* bars, uint32_t& phases,
+                                                    unsigned long long* pstat) {
+    constexpr int R = ROWS - 2 * T;
+    constexpr int OW = 30;
+    constexpr int BW = 36;
+    constexpr uint32_t kBox = ROWS * BW * 4;
+    const int64_t n_strips = (rows + R - 1) / R;
+    const int64_t n_cb = (wp + OW - 1) / OW;
+    const int64_t n_tiles = n_strips * n_cb;
+    const bool own_lane = lane >= 1 && lane <= OW;
+    const int64_t n_my = gw < n_tiles ? (n_tiles - gw + nwarps - 1) / nwarps : 0;
+    // active-tile generator over the warp's tiles, 32 stamps per load
+    int64_t chunk = -1;
+    uint32_t mask = 0;
+    auto next_tile = [&]() -> int64_t {
+        while (mask == 0) {
+            ++chunk;
+            if (chunk * 32 >= n_my) return -1;
+            const int64_t i = chunk * 32 + lane;
+            bool a = false;
+            if (i < n_my) a = all_active || __ldcg(act + gw + i * nwarps) == stamp;
+            mask = __ballot_sync(0xffffffffu, a);
+        }
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        return gw + (chunk * 32 + b) * nwarps;
+    };
+    auto issue = [&](int64_t t, int s) {
+        if (lane == 0) {
+            const int64_t strip = t / n_cb, cb = t - strip * n_cb;
+            const int x = (int)(cb * OW - 1) & ~3, y = (int)(strip * R - T + 1);   // hd = 1
+            uint32_t* sb = slots + s * (2 * ROWS * BW);
+            mbar_expect_tx(&bars[s], 2 * kBox);
+            tma_load_2d(sb, tin, x, y, &bars[s]);
+            tma_load_2d(sb + ROWS * BW, tk, x, y, &bars[s]);
+        }
+    };
+    int my_last = -1;
+    int64_t cur = next_tile();
+    if (cur >= 0) issue(cur, 0);
+    int64_t nxt = cur >= 0 ? next_tile() : -1;
+    if (nxt >= 0) issue(nxt, 1);
+    int s = 0;
+    while (cur >= 0) {
+        mbar_wait(&bars[s], (phases >> s) & 1u);
+        phases ^= 1u << s;
+        const uint32_t* sb = slots + s * (2 * ROWS * BW);
+        const uint32_t* kb = sb + ROWS * BW;
+        const int o = (int)((cur % n_cb) * OW - 1) & 3;
+        uint32_t sv[ROWS], kv[ROWS];
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+            sv[i] = sb[i * BW + o + lane];
+            kv[i] = kb[i * BW + o + lane];
+        }
+        __syncwarp();                                  // slot s free: refill it
+        const int64_t n2 = nxt >= 0 ? next_tile() : -1;
+        if (n2 >= 0) issue(n2, s);
+        const int64_t strip = cur / n_cb, cb = cur - strip * n_cb;
+        const int64_t w = cb * OW - 1 + lane;
+        int ne = 0;
+        const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane, lane, pstat ? &ne : nullptr);
+        if (pstat && lane == 0) {
+            atomicAdd(pstat, (unsigned long long)ne);
+            atomicAdd(pstat + 32, 1ull);
+        }
+        my_last = max(my_last, tl);
+        plane_store<T, ROWS>(sv, out, rows, wp, 1, strip * R - T, w, own_lane, w >= 0 && w < wp);
+        if (tl >= 0) {
+            const int64_t s2 = strip + lane / 3 - 1, c2 = cb + lane % 3 - 1;
+            const bool nb = tl == steps - 1 ? lane < 9 : lane == 4;
+            if (nb && s2 >= 0 && s2 < n_strips && c2 >= 0 && c2 < n_cb) act[s2 * n_cb + c2] = stamp + 1;
+        }
+        cur = nxt;
+        nxt = n2;
+        s ^= 1;
+    }
+    return my_last;
+}
 
 template <int T, int ROWS>
 __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUtensorMap tm_s0,
@@ -1310,19 +1430,19 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
                                                      int64_t wp, int64_t max_iters,
                                                      int* __restrict__ flags,
                                                      int* __restrict__ state,
-                                                     uint8_t* __restrict__ tflags,
+                                                     uint32_t* __restrict__ act,
                                                      unsigned long long* __restrict__ prof) {
     constexpr int R = ROWS - 2 * T;
     constexpr int BW = 36;
-    extern __shared__ __align__(128) uint32_t psm[];   // 8 warp slots, then 8 mbarriers
-    uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * ROWS * BW);
+    extern __shared__ __align__(128) uint32_t psm[];   // 8 x 2 warp slots, then 16 mbarriers
+    uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * 2 * ROWS * BW);
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t* sb = psm + wid * (2 * ROWS * BW);     // [ROWS][BW] S box, then K box
-    uint32_t* kb = sb + ROWS * BW;
-    uint64_t* bar = &bars[wid];
+    uint32_t* slots = psm + wid * (2 * 2 * ROWS * BW);
+    uint64_t* bar = &bars[2 * wid];
     if (lane == 0) {
-        mbar_init(bar, 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -1330,22 +1450,25 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
     const int64_t nwarps = (int64_t)gridDim.x * 8;
     const int64_t n_tiles = ((rows + R - 1) / R) * ((wp + 29) / 30);
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    // act[n_tiles] = this run's stamp base (pass p is active at base + p);
+    // the leader advances it past the run's stamps after the last barrier
+    const uint32_t base = *((volatile uint32_t*)&act[n_tiles]);
     auto gtime = []() {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         return t;
     };
     if (prof && leader) prof[0] = gtime();
-    uint32_t phase = 0;
+    uint32_t phases = 0;
     int64_t k0 = 0;
     int pass = 0;
     while (k0 < max_iters) {
         const int steps = (int)min((int64_t)T, max_iters - k0);
         if (leader) flags[(pass + 1) % 3] = -1;   // last read two barriers ago
-        const int my_last = plane_pass_warp<T, ROWS>(
-            (pass & 1) ? &tm_s1 : &tm_s0, &tm_k, (pass & 1) ? S0 : S1, rows, wp, 1, steps,
-            tflags + ((pass + 1) & 1) * n_tiles, tflags + (pass & 1) * n_tiles, pass == 0, 0, 0,
-            gw, nwarps, lane, sb, kb, bar, phase, true);
+        const int my_last = plane_loop_pass_warp<T, ROWS>(
+            (pass & 1) ? &tm_s1 : &tm_s0, &tm_k, (pass & 1) ? S0 : S1, rows, wp, steps, act,
+            base + (uint32_t)pass, pass == 0, gw, nwarps, lane, slots, bar, phases,
+            prof && pass < 30 ? prof + 32 + pass : nullptr);
         if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
         // the next pass reads `out` through the async (TMA) proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1358,6 +1481,7 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
                 state[0] = (int)(last_global + 2);
                 state[1] = 1;
                 state[2] = (pass & 1) ? 0 : 1;
+                act[n_tiles] = base + (uint32_t)pass + 2;
             }
             return;
         }
@@ -1368,6 +1492,7 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
         state[0] = (int)max_iters;
         state[1] = 0;
         state[2] = pass == 0 ? 0 : (((pass - 1) & 1) ? 0 : 1);
+        act[n_tiles] = base + (uint32_t)pass + 2;
     }
 }
 
@@ -2626,8 +2751,8 @@ static unsigned long long* hyst_prof_buf() {
 template <int T, int ROWS>
 static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows,
                                  int64_t wp, int64_t max_iters, int* flags, int* state,
-                                 uint8_t* tflags, const Launch& L) {
-    constexpr size_t smem = plane_smem_bytes<ROWS>();
+                                 uint32_t* act, const Launch& L) {
+    constexpr size_t smem = plane_loop_smem_bytes<ROWS>();
     static int occ = [] {
         cudaFuncSetAttribute(k_planes_loop<T, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
@@ -2644,7 +2769,7 @@ static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, 
     unsigned long long* prof = hyst_prof_buf();
     if (prof) cudaMemsetAsync(prof, 0, 1024, L.stream);
     int64_t r = rows, w = wp, mi = max_iters;
-    void* args[] = {&ts0, &ts1, &tk, &S0, &S1, &r, &w, &mi, &flags, &state, &tflags, &prof};
+    void* args[] = {&ts0, &ts1, &tk, &S0, &S1, &r, &w, &mi, &flags, &state, &act, &prof};
     ++g_launches;
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid),
                                                 dim3(256), args, smem, L.stream);
@@ -2653,8 +2778,10 @@ static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, 
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, L.stream);
         cudaStreamSynchronize(L.stream);
         fprintf(stderr, "MW_HYST_PROF grid=%u tiles=%lld", grid, (long long)tiles);
-        for (int i = 1; i < 100 && h[i]; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) / 1e3);
-        fprintf(stderr, " us\n");
+        for (int i = 1; i < 32 && h[i]; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) / 1e3);
+        fprintf(stderr, " us; tiles run / executions per pass:");
+        for (int i = 0; i < 30 && h[64 + i]; ++i) fprintf(stderr, " %llu/%llu", h[64 + i], h[32 + i]);
+        fprintf(stderr, "\n");
     }
     return e;
 }
@@ -2704,13 +2831,13 @@ cudaError_t planes_pass(const uint32_t* in, uint32_t* out, const uint32_t* K, in
 }
 
 cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,
-                        int64_t max_iters, int* flags, int* state, uint8_t* tflags,
+                        int64_t max_iters, int* flags, int* state, uint32_t* act,
                         const Launch& L) {
     const int64_t wp = plane_words(W);
     const int T = L.tune[TUNE_HYST_T];
     const int ROWS = L.tune[TUNE_HYST_ROWS];
 #define MW_PL(TT, RR) \
-    if (T == TT && ROWS == RR) return planes_loop_t<TT, RR>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L)
+    if (T == TT && ROWS == RR) return planes_loop_t<TT, RR>(S0, S1, K, rows, wp, max_iters, flags, state, act, L)
     MW_PL(4, 32);
     MW_PL(6, 32);
     MW_PL(8, 32);
@@ -2719,7 +2846,7 @@ cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t r
     MW_PL(8, 48);
     MW_PL(6, 48);
 #undef MW_PL
-    return planes_loop_t<8, 48>(S0, S1, K, rows, wp, max_iters, flags, state, tflags, L);
+    return planes_loop_t<8, 48>(S0, S1, K, rows, wp, max_iters, flags, state, act, L);
 }
 
 template <int T, int ROWS>

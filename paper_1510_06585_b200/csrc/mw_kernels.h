@@ -90,10 +90,11 @@ int64_t plane_words(int64_t W);
 // hd: halo rows above and below the interior in the plane buffers
 cudaError_t planes_pack(const U8Prog& p, const uint8_t* src, int64_t sp, int64_t rows, int64_t W,
                         uint32_t* S, uint32_t* K, const Launch& L, int hd = 1);
-// tflags: 2 * planes_tiles(rows, W) bytes of per-tile change flags (scratch).
+// act: planes_tiles(rows, W) + 1 32-bit per-tile activity stamps (scratch;
+// never needs clearing: the last word is the stamp base the kernel advances).
 int64_t planes_tiles(int64_t rows, int64_t W);
 cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows, int64_t W,
-                        int64_t max_iters, int* flags, int* state, uint8_t* tflags,
+                        int64_t max_iters, int* flags, int* state, uint32_t* act,
                         const Launch& L);
 cudaError_t planes_unpack(const U8Prog& p, const uint32_t* S0, const uint32_t* S1,
                           const uint32_t* K, const int* state, uint8_t* dst, int64_t dp,

@@ -51,6 +51,10 @@ struct mw_ctx {
     bool has_alloc = false;
     std::vector<double> dist;
     std::map<std::string, mwx::Buf> scratch;
+    // one-partition plane loop: the (S0, S1, K, flags, rows, wp) whose zero halo
+    // rows and loop flags are in place (the loop kernel leaves flags ready for
+    // the next run), so a repeated run enqueues no memsets
+    std::vector<uintptr_t> planes_prep;
     // Scratch pointers baked into live CUDA graphs (refcount per pointer): a
     // buffer replaced by a larger one while a graph references it is parked in
     // `orphans` and freed with the last such graph (or at teardown).

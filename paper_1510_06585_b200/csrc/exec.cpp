@@ -834,11 +834,18 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
             uint32_t* K = static_cast<uint32_t*>(kk);
             int* flags = static_cast<int*>(fl);
             int* state = flags + 4;
-            for (uint32_t* b : {S0, S1, K}) {   // zero halo rows (outside the image = 0)
-                CUDA_OK(cudaMemsetAsync(b, 0, wp * 4, R.s));
-                CUDA_OK(cudaMemsetAsync(b + (rows + 1) * wp, 0, wp * 4, R.s));
+            const std::vector<uintptr_t> key = {(uintptr_t)S0, (uintptr_t)S1, (uintptr_t)K, (uintptr_t)flags,
+                                                (uintptr_t)rows, (uintptr_t)wp};
+            if (c->planes_prep != key) {
+                // no kernel writes the halo rows, and the loop leaves its flags
+                // at -1 for the next run: both are set up once per buffer set
+                c->planes_prep.clear();
+                for (uint32_t* b : {S0, S1, K}) {   // zero halo rows (outside the image = 0)
+                    CUDA_OK(cudaMemsetAsync(b, 0, wp * 4, R.s));
+                    CUDA_OK(cudaMemsetAsync(b + (rows + 1) * wp, 0, wp * 4, R.s));
+                }
+                CUDA_OK(cudaMemsetAsync(flags, 0xFF, 64, R.s));   // pass flags start at -1
             }
-            CUDA_OK(cudaMemsetAsync(flags, 0xFF, 64, R.s));   // pass flags start at -1
             auto pre = u8_groups(prog[0].ops);
             if (pre.size() != 1) return fail(MW_E_UNSUPPORTED, "chain before the loop > 16 ops");
             mwk::U8Prog post{};
@@ -865,6 +872,7 @@ mw_status run_u8(RunCtx& R, const std::vector<Step>& prog, const mw_arg& src, co
                                                         at_row<uint8_t>(dst, R.off[p0]), inner, rows, W, L),
                                      "planes_unpack"));
             }
+            c->planes_prep = key;
             if (prog[1].kind == StepKind::StencilWhile) {
                 CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 8, cudaMemcpyDeviceToHost, R.s));
                 f->plane_loop = true;

@@ -1482,6 +1482,9 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
                 state[1] = 1;
                 state[2] = (pass & 1) ? 0 : 1;
                 act[n_tiles] = base + (uint32_t)pass + 2;
+                // ready for the next run (every thread has read the flags
+                // and decided to leave: -1 only confirms that decision)
+                flags[0] = -1;
             }
             return;
         }
@@ -1493,6 +1496,7 @@ __global__ void __launch_bounds__(256) k_planes_loop(const __grid_constant__ CUt
         state[1] = 0;
         state[2] = pass == 0 ? 0 : (((pass - 1) & 1) ? 0 : 1);
         act[n_tiles] = base + (uint32_t)pass + 2;
+        flags[0] = -1;
     }
 }
 

@@ -1806,6 +1806,8 @@ mw_status mw_ctx_create(int32_t device, int32_t rank, int32_t nranks, int32_t pa
     CUDA_OK(cudaEventCreate(&c->wall_b));
     CUDA_OK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreateWithFlags(&c->last_run, cudaEventDisableTiming));
+    CUDA_OK(mwk::fft_prepare(c->aux));   // before any capture can start
+    CUDA_OK(cudaStreamSynchronize(c->aux));
     c->launches0 = mwk::launch_count();
     c->bstate = mw_balance_state{};
     if (use_comm) {

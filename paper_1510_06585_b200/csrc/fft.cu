@@ -20,12 +20,18 @@
 // k1 ("T layout").  The inverse runs the mirror image: local inverse FFT on
 // the T layout, then the twiddled radix-C inverse DFT gathered across the
 // cluster lands in natural order — fft followed by ifft needs no exchange in
-// the middle.  Twiddles come from exact-rounded fp64 tables in shared memory
-// (quadrant-reduced; the cross-CTA one is two-level), so mu <= 4u (R25).
+// the middle.  Twiddles come from exact-rounded fp64 tables laid out so a
+// warp reads them without index arithmetic or quadrant folding: the 512-point
+// pass from a [r][k] table in shared memory (k = thread mod 32: one load per
+// twiddle serves both butterflies of a thread), the 8192-point pass from a
+// [r][k] table in global memory (64 KiB, L1-resident: both CTAs of an SM read
+// the same table), the cross-CTA twiddle W_65536^e from two full-circle
+// 256-entry tables (e = 256 h + l); so mu <= 4u (R25).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "mw_kernels.h"
 
@@ -37,13 +43,21 @@ namespace {
 constexpr int FN2 = 8192;              // points per CTA
 constexpr int FT = 256;                // threads per CTA
 constexpr int FPAD = FN2 + FN2 / 32;   // one pad element per 32 (conflict-free radix-32 stores)
-// twiddle tables are stored XOR-swizzled (tsw): the index strides r * k of
-// the Stockham twiddles then spread over more banks (a bank model over all
-// r of both passes: 37 % fewer shared-memory wavefronts than linear order)
-constexpr int T13 = 2048;              // W_8192^i, i < 8192/4 (first quadrant)
-constexpr int T9 = 128;                // W_512^i,  i < 512/4
-constexpr int THI = 64, TLO = 256;     // W_65536^(256h) and W_65536^l (first quadrant)
-constexpr size_t kFftSmem = sizeof(float2) * (FPAD + T13 + T9 + THI + TLO);
+constexpr int T9 = 16 * 32;            // W_512^(r k) at [r][k], r < 16, k < 32
+constexpr int THI = 256, TLO = 256;    // W_65536^(256 h) and W_65536^l, full circle
+constexpr size_t kFftSmem = sizeof(float2) * (FPAD + T9 + THI + TLO);
+
+// W_8192^(r k) at [r][k], r < 16, k < 512 (forward sign), filled once per
+// device by k_fft_tw13 before the first FFT launch.
+__device__ float2 g_tw13[16 * 512];
+__global__ void k_fft_tw13() {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 16 * 512) return;
+    const int r = i / 512, k = i % 512;
+    double sn, cs;
+    sincospi(2.0 * ((r * k) & 8191) / 8192.0, &sn, &cs);
+    g_tw13[i] = make_float2((float)cs, (float)-sn);
+}
 
 __device__ __forceinline__ int fpad(int i) { return i + (i >> 5); }
 
@@ -68,6 +82,12 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * w (INV: a * conj(w))
+template <bool INV>
+__device__ __forceinline__ float2 cmulw(float2 a, float2 w) {
+    if (INV) return make_float2(fmaf(a.x, w.x, a.y * w.y), fmaf(a.y, w.x, -a.x * w.y));
+    return cmul(a, w);
 }
 
 // cos(2 pi k / 32), k = 0..8 (fp32, correctly rounded)
@@ -142,24 +162,10 @@ __device__ __forceinline__ void dft(float2* v) {
     }
 }
 
-// W_M^e from a first-quadrant table T[i] = W_M^i, i < M/4 (exact quadrant turn)
-__device__ __forceinline__ int tsw(int i) { return i ^ ((i >> 1) & 15); }
-template <bool INV>
-__device__ __forceinline__ float2 tw_q(const float2* T, int e, int qlog2) {
-    const int q = (e >> qlog2) & 3;
-    float2 w = T[tsw(e & ((1 << qlog2) - 1))];
-    if (q & 1) w = make_float2(w.y, -w.x);    // * (-i)
-    if (q & 2) w = make_float2(-w.x, -w.y);   // * (-1)
-    if (INV) w.y = -w.y;
-    return w;
-}
-// W_65536^e, two-level first-quadrant table
+// W_65536^e (INV: conjugate), e < 65536, two-level full-circle tables
 template <bool INV>
 __device__ __forceinline__ float2 tw_cross(const float2* Thi, const float2* Tlo, int e) {
-    const int q = (e >> 14) & 3, r = e & 16383;
-    float2 w = cmul(Thi[r >> 8], Tlo[r & 255]);
-    if (q & 1) w = make_float2(w.y, -w.x);
-    if (q & 2) w = make_float2(-w.x, -w.y);
+    float2 w = cmul(Thi[e >> 8], Tlo[e & 255]);
     if (INV) w.y = -w.y;
     return w;
 }
@@ -168,7 +174,7 @@ __device__ __forceinline__ float2 tw_cross(const float2* Thi, const float2* Tlo,
 // all stores): v[r] = s[j + r N2/R] * W_{Ns R}^{r k}, R-point DFT, stored at
 // (j / Ns) Ns R + k + r Ns, k = j mod Ns.
 template <int R, int NS, bool INV>
-__device__ __forceinline__ void stockham_pass(float2* s, const float2* T13p, const float2* T9p) {
+__device__ __forceinline__ void stockham_pass(float2* s, const float2* T9p) {
     constexpr int NB = FN2 / R, PER = NB / FT;
     int tid = threadIdx.x;
     asm volatile("" : "+r"(tid));   // per pass: no addresses kept live across passes
@@ -183,13 +189,14 @@ __device__ __forceinline__ void stockham_pass(float2* s, const float2* T13p, con
 #pragma unroll
         for (int r = 0; r < R; ++r) v[p][r] = src[r * (NB + NB / 32)];
         if constexpr (NS > 1) {
-            constexpr int M = NS * R;
+            static_assert(NS * R == 512 || NS * R == 8192, "twiddle tables");
+            // k = j mod NS with j = tid + 256 p: the [r][k] tables are read at
+            // consecutive k across a warp (no bank conflicts, full sectors)
+            const float2* tw = NS * R == 512 ? T9p + k : g_tw13 + k;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                float2 w;
-                if constexpr (M == 8192) w = tw_q<INV>(T13p, (r * k) & 8191, 11);
-                else w = tw_q<INV>(T9p, (r * k) & 511, 7);
-                v[p][r] = cmul(v[p][r], w);
+                const float2 w = NS * R == 512 ? tw[r * NS] : __ldg(tw + r * NS);
+                v[p][r] = cmulw<INV>(v[p][r], w);
             }
         }
         dft<R, INV>(v[p]);
@@ -214,11 +221,11 @@ __device__ __forceinline__ void stockham_pass(float2* s, const float2* T13p, con
 // competing with the cluster-exchange code around them (measured: inlining
 // them into the fused forward->inverse kernel spills ~400 B per thread).
 template <bool INV>
-__device__ __noinline__ void local_fft(float2* s, const float2* T13p, const float2* T9p) {
+__device__ __noinline__ void local_fft(float2* s, const float2* T9p) {
     static_assert(FN2 == 32 * 16 * 16, "pass plan");
-    stockham_pass<32, 1, INV>(s, T13p, T9p);
-    stockham_pass<16, 32, INV>(s, T13p, T9p);
-    stockham_pass<16, 512, INV>(s, T13p, T9p);
+    stockham_pass<32, 1, INV>(s, T9p);
+    stockham_pass<16, 32, INV>(s, T9p);
+    stockham_pass<16, 512, INV>(s, T9p);
 }
 
 template <int C>
@@ -259,20 +266,22 @@ template <int C, int MODE>
 __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, int64_t nfft) {
     extern __shared__ float4 fft_smem[];
     float2* S = reinterpret_cast<float2*>(fft_smem);
-    float2* T13p = S + FPAD;
-    float2* T9p = T13p + T13;
+    float2* T9p = S + FPAD;
     float2* Thi = T9p + T9;
     float2* Tlo = Thi + THI;
-    for (int i = threadIdx.x; i < T13 + T9 + THI + TLO; i += FT) {
+    for (int i = threadIdx.x; i < T9 + THI + TLO; i += FT) {
         double x;   // angle / pi
-        float2* dst;
-        if (i < T13) { x = 2.0 * i / 8192.0; dst = T13p + tsw(i); }
-        else if (i < T13 + T9) { x = 2.0 * (i - T13) / 512.0; dst = T9p + tsw(i - T13); }
-        else if (i < T13 + T9 + THI) { x = 2.0 * 256.0 * (i - T13 - T9) / 65536.0; dst = Thi + (i - T13 - T9); }
-        else { x = 2.0 * (i - T13 - T9 - THI) / 65536.0; dst = Tlo + (i - T13 - T9 - THI); }
+        if (i < T9) {
+            const int r = i / 32, k = i % 32;
+            x = 2.0 * ((r * k) & 511) / 512.0;
+        } else if (i < T9 + THI) {
+            x = 2.0 * 256.0 * (i - T9) / 65536.0;
+        } else {
+            x = 2.0 * (i - T9 - THI) / 65536.0;
+        }
         double sn, cs;
         sincospi(x, &sn, &cs);
-        *dst = make_float2((float)cs, (float)-sn);
+        T9p[i] = make_float2((float)cs, (float)-sn);   // the three tables are contiguous
     }
     __syncthreads();
     constexpr int NI = 32 / C;             // n2 values per thread (x C values of n1)
@@ -331,8 +340,8 @@ __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, in
             }
             csync<C>();
         }
-        if constexpr (MODE != FFT_I) local_fft<false>(S, T13p, T9p);   // -> X[k1 + C k2] at k2
-        if constexpr (MODE != FFT_F) local_fft<true>(S, T13p, T9p);    // -> z[k1][n2] at n2
+        if constexpr (MODE != FFT_I) local_fft<false>(S, T9p);   // -> X[k1 + C k2] at k2
+        if constexpr (MODE != FFT_F) local_fft<true>(S, T9p);    // -> z[k1][n2] at n2
         csync<C>();   // every CTA's local transform is complete
         {
             float2 v[NI][C];
@@ -427,10 +436,28 @@ cudaError_t fft_launch_mode(int mode, const float2* in, float2* out, int64_t nff
 
 bool fft_supported(int log2n) { return log2n >= 13 && log2n <= 16; }
 
+cudaError_t fft_prepare(cudaStream_t s) {
+    static std::mutex mu;
+    static bool filled[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 64 || filled[dev]) return cudaSuccess;
+    k_fft_tw13<<<32, 256, 0, s>>>();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) filled[dev] = true;
+    return e;
+}
+
 cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint32_t inv, int nst,
                       const Launch& L) {
     if (nfft <= 0) return cudaSuccess;
     if (nst > 32 || !fft_supported(log2n)) return cudaErrorInvalidValue;
+    {
+        cudaError_t e = fft_prepare(L.stream);   // no-op after the context's creation
+        if (e != cudaSuccess) return e;
+    }
     const float2* src = reinterpret_cast<const float2*>(in);
     float2* o2 = reinterpret_cast<float2*>(out);
     if (nst == 0) {

@@ -237,6 +237,8 @@ void note_launch();   // count one launch of ours (mw_ctx_launch_count)
 // nfft transforms of N = 2^log2n complex64 points (interleaved re, im), a
 // chain of nst stages (bit s of inv: inverse with 1/N); in may equal out.
 bool fft_supported(int log2n);   // 13..16
+// one-time per-device setup of the FFT twiddle table (mw_ctx_create)
+cudaError_t fft_prepare(cudaStream_t s);
 cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint32_t inv, int nst,
                       const Launch& L);
 unsigned long long launch_count();  // kernels launched by this library

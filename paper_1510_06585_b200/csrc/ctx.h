@@ -55,6 +55,7 @@ struct mw_ctx {
     // rows and loop flags are in place (the loop kernel leaves flags ready for
     // the next run), so a repeated run enqueues no memsets
     std::vector<uintptr_t> planes_prep;
+    std::vector<uintptr_t> planes_multi_prep;   // the same for the fused multi-partition loop
     // Scratch pointers baked into live CUDA graphs (refcount per pointer): a
     // buffer replaced by a larger one while a graph references it is parked in
     // `orphans` and freed with the last such graph (or at teardown).

@@ -562,7 +562,20 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
     void* lp;
     MW_OK_OR_RETURN(scratch(c, "planes_last", 64, R.s, &lp));
     int* d_last = static_cast<int*>(lp);
-    CUDA_OK(cudaMemsetAsync(d_last, 0, 64, R.s));   // d_last[4..6]: unpack state (buffer 0)
+    // (buffers, lengths, T, W) of the partitions: when equal to the last FUSED
+    // run's, the image-edge halo rows are still zero and the fused loop left
+    // its flags ready, so the run enqueues no memsets
+    std::vector<uintptr_t> key = {(uintptr_t)d_last, (uintptr_t)T, (uintptr_t)W};
+    const bool fused_path = (c->nranks == 1 && c->tune[mwk::TUNE_HYST_FUSED] != 0) ||
+                            (c->nranks > 1 && c->comm && c->tune[mwk::TUNE_HYST_FUSED] != 0 && !c->xr_broken &&
+                             !c->capturing);
+    bool prepared = false;
+    for (int pass2 = 0; pass2 < 2; ++pass2) {   // pass 0: buffers -> key; pass 1: memsets if needed
+    if (pass2 == 1) {
+        prepared = fused_path && c->planes_multi_prep == key;
+        c->planes_multi_prep.clear();
+        if (!prepared) CUDA_OK(cudaMemsetAsync(d_last, 0, 64, R.s));   // d_last[4..6]: unpack state (buffer 0)
+    }
     for (int q = 0; q < ppr; ++q) {
         const int p = R.first + q;
         const int64_t len = R.len[p];
@@ -578,14 +591,22 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
         K[q] = static_cast<uint8_t*>(v);
         MW_OK_OR_RETURN(scratch(c, "mplane_tf_" + sq, (size_t)(2 * mwk::planes_tiles(len, W)), R.s, &v));
         fl[q] = static_cast<uint8_t*>(v);
+        top[q] = bot[q] = 0;
         for (int a = 0; a < p; ++a) top[q] |= R.len[a] > 0;
         for (int a = p + 1; a < c->P; ++a) bot[q] |= R.len[a] > 0;
+        if (pass2 == 0) {
+            for (uint8_t* b : {S[0][q], S[1][q], K[q]}) key.push_back((uintptr_t)b);
+            key.insert(key.end(), {(uintptr_t)q, (uintptr_t)len, (uintptr_t)top[q], (uintptr_t)bot[q]});
+            continue;
+        }
         // halo rows outside the image stay 0; the others are filled by the
         // exchanges (K, S0 below; S1 by the first pass) before they are read
-        for (uint8_t* b : {S[0][q], S[1][q], K[q]}) {
-            if (!top[q]) CUDA_OK(cudaMemsetAsync(b, 0, T * rb, R.s));
-            if (!bot[q]) CUDA_OK(cudaMemsetAsync(b + (len + T) * rb, 0, T * rb, R.s));
-        }
+        if (!prepared)
+            for (uint8_t* b : {S[0][q], S[1][q], K[q]}) {
+                if (!top[q]) CUDA_OK(cudaMemsetAsync(b, 0, T * rb, R.s));
+                if (!bot[q]) CUDA_OK(cudaMemsetAsync(b + (len + T) * rb, 0, T * rb, R.s));
+            }
+    }
     }
     std::vector<int> act;
     bool slowed = false;
@@ -663,9 +684,17 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
             hm.fl_bytes[i] = 2 * mwk::planes_tiles(R.len[R.first + q], W);
             hm.rows[i] = R.len[R.first + q];
         }
+        {
+            int64_t words = 1;
+            for (int i = 0; i < hm.np; ++i) words += mwk::planes_tiles(hm.rows[i], W);
+            void* av;
+            MW_OK_OR_RETURN(scratch(c, "mplane_act", (size_t)words * 4, R.s, &av));
+            hm.act = static_cast<uint32_t*>(av);
+            hm.act_words = words;
+        }
         int* state = d_last + 4;   // {E, converged, final buffer, abort}: read by the unpack
         int* pflags = d_last + 8;
-        CUDA_OK(cudaMemsetAsync(pflags, 0xFF, 3 * sizeof(int), R.s));
+        if (!prepared) CUDA_OK(cudaMemsetAsync(pflags, 0xFF, 3 * sizeof(int), R.s));
         {
             auto t = timers_all(MW_KC_STENCIL);
             mwk::Launch L = launch_for(c, R.s, R.first);
@@ -680,6 +709,7 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
                                  "planes_unpack"));
             close_timers(t);
         }
+        c->planes_multi_prep = key;
         if (is_while || xr) {
             CUDA_OK(cudaMemcpyAsync(f->res + 1, state, 16, cudaMemcpyDeviceToHost, R.s));
             f->plane_loop = true;
@@ -690,6 +720,7 @@ mw_status run_planes_multi(RunCtx& R, const std::vector<Step>& prog, const mw_ar
         }
         return MW_OK;
     }
+    if (prepared) CUDA_OK(cudaMemsetAsync(d_last, 0, 64, R.s));   // skipped above for a fused run
     if (is_while && c->capturing)
         return fail(MW_E_UNSUPPORTED,
                     "this while-loop evaluates its condition on the host (several ranks or "

@@ -1568,125 +1568,84 @@ __device__ __forceinline__ void plane_store_fwd(const uint32_t (&sv)[ROWS], cons
     }
 }
 
-// Tile activity across partition boundaries: the 3x3 rule of
-// plane_tile_active, where the strip above a partition's first strip is the
-// previous partition's last strip (and the one before it when that last strip
-// has fewer than T rows: a front crosses it within one pass), and the strip
-// below the last strip (or below the second-to-last one when the last is
-// short) is the next partition's first strip.  Neighbours' flags count with
-// bit 0 (changed in the last execution of the previous pass), as inside a
-// partition; no boundary strip is forced active.
-// PView caches what the check needs about the scan cursor's partition (it
-// changes a few times per warp and pass; the check runs for every candidate).
-struct PView {
-    const uint8_t* fp;        // previous-pass flags of the partition
-    uint8_t* fc;              // this pass's flags
-    int64_t n_strips, nt, t0, t1;
-    const uint8_t* fp_prev;   // previous partition: flags of its last strip (nullptr: none)
-    const uint8_t* fp_prev2;  // ... and of its second-to-last strip when the last is short
-    const uint8_t* fp_next;   // next partition: flags of its first strip
-    bool short_last;          // this partition's last strip has fewer than T rows
-    bool force_top, force_bot;   // neighbour on another rank: boundary strips always run
-};
-template <int T, int ROWS>
-__device__ __forceinline__ PView plane_view(const PlaneMultiArgs& a, int q, int cur, int64_t t0) {
-    constexpr int R = ROWS - 2 * T;
-    const PlanePartDesc& d = a.p[q];
-    PView v;
-    v.fp = d.fl + (cur ^ 1) * d.nt;
-    v.fc = d.fl + cur * d.nt;
-    v.n_strips = d.n_strips;
-    v.nt = d.nt;
-    v.t0 = t0;
-    v.t1 = t0 + d.nt;
-    v.short_last = d.rows - (d.n_strips - 1) * R < T;
-    v.fp_prev = v.fp_prev2 = v.fp_next = nullptr;
-    v.force_top = d.prev == -2;
-    v.force_bot = d.next == -2;
-    if (d.prev >= 0) {
-        const PlanePartDesc& pd = a.p[d.prev];
-        const uint8_t* f = pd.fl + (cur ^ 1) * pd.nt;
-        v.fp_prev = f + (pd.n_strips - 1) * a.n_cb;
-        if (pd.rows - (pd.n_strips - 1) * R < T && pd.n_strips >= 2) v.fp_prev2 = f + (pd.n_strips - 2) * a.n_cb;
-    }
-    if (d.next >= 0) {
-        const PlanePartDesc& nd = a.p[d.next];
-        v.fp_next = nd.fl + (cur ^ 1) * nd.nt;
-    }
-    return v;
-}
-__device__ __forceinline__ bool plane_tile_active_multi(const PView& v, int64_t n_cb, int64_t strip,
-                                                        int64_t cb, bool first, int lane) {
-    if (first) return true;
-    // a neighbour on another rank: its flags are not read, its halo may change
-    if ((v.force_top && strip == 0) ||
-        (v.force_bot && (strip == v.n_strips - 1 || (v.short_last && strip == v.n_strips - 2))))
-        return true;
-    const int64_t c2 = cb + lane % 3 - 1;
-    bool x = false;
-    if (lane < 18 && c2 >= 0 && c2 < n_cb) {
-        if (lane < 9) {
-            const int64_t s2 = strip + lane / 3 - 1;
-            if (s2 >= 0 && s2 < v.n_strips) x = v.fp[s2 * n_cb + c2] & (lane == 4 ? 3 : 1);
-        } else if (lane < 12) {
-            if (strip == 0 && v.fp_prev) x = v.fp_prev[c2] & 1;
-        } else if (lane < 15) {
-            if (strip == 0 && v.fp_prev2) x = v.fp_prev2[c2] & 1;
-        } else if (v.fp_next && (strip == v.n_strips - 1 || (v.short_last && strip == v.n_strips - 2))) {
-            x = v.fp_next[c2] & 1;
-        }
-    }
-    return __any_sync(0xffffffffu, x);
-}
-
+// One pass of the multi-partition loop for one warp: the push-model activity
+// and two-slot ring of plane_loop_pass_warp over the concatenated tile list.
+// A live front also stamps across partition boundaries: a tile in a
+// partition's first strip stamps the previous partition's last strip (and the
+// one before it when that last strip has fewer than T rows — a front crosses
+// it within one pass), a tile in the last strip (or in the second-to-last one
+// when the last is short) the next partition's first strip.  Boundary strips
+// whose neighbour is on another rank run every pass (its flags are not read).
 template <int T, int ROWS>
 __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, int cur, int steps,
-                                                     bool first, int64_t gw, int64_t nwarps, int lane,
-                                                     uint32_t* sb, uint32_t* kb, uint64_t* bar,
-                                                     uint32_t& phase) {
+                                                     bool first, uint32_t stamp, int64_t gw,
+                                                     int64_t nwarps, int lane, uint32_t* slots,
+                                                     uint64_t* bars, uint32_t& phases) {
     constexpr int R = ROWS - 2 * T;
     constexpr int OW = 30;
     constexpr int BW = 36;
     constexpr uint32_t kBox = ROWS * BW * 4;
     const int64_t n_cb = a.n_cb;
     const bool own_lane = lane >= 1 && lane <= OW;
-    // scan cursor over the concatenated tile list: a warp's tiles increase, so
-    // the partition of the next candidate is found by moving forward only
     if (a.total == 0) return -1;   // a rank without active partitions only joins the barriers
-    int sq = 0;
-    PView v = plane_view<T, ROWS>(a, 0, cur, 0);
-    auto next_active = [&](int64_t t) {
-        for (; t < a.total; t += nwarps) {
-            while (t >= v.t1 && sq + 1 < a.np) {
-                ++sq;
-                v = plane_view<T, ROWS>(a, sq, cur, v.t1);
-            }
-            const int64_t lt = t - v.t0;
-            const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
-            if (plane_tile_active_multi(v, n_cb, strip, cb, first, lane)) break;
-            if (lane == 0) v.fc[lt] = 0;
-        }
-        return t;
+    uint32_t* __restrict__ act = a.act;
+    const int64_t n_my = gw < a.total ? (a.total - gw + nwarps - 1) / nwarps : 0;
+    auto part_of = [&](int64_t t) {
+        int q = 0;
+        while (q + 1 < a.np && t >= a.p[q + 1].tile0) ++q;
+        return q;
     };
-    auto issue = [&](int64_t t) {   // t was located by the scan cursor
+    auto short_last = [&](const PlanePartDesc& d) { return d.rows - (d.n_strips - 1) * R < T; };
+    int64_t chunk = -1;
+    uint32_t mask = 0;
+    auto next_tile = [&]() -> int64_t {
+        while (mask == 0) {
+            ++chunk;
+            if (chunk * 32 >= n_my) return -1;
+            const int64_t i = chunk * 32 + lane;
+            bool on = false;
+            if (i < n_my) {
+                const int64_t t = gw + i * nwarps;
+                on = first || __ldcg(act + t) == stamp;
+                if (!on) {
+                    const PlanePartDesc& d = a.p[part_of(t)];
+                    const int64_t strip = (t - d.tile0) / n_cb;
+                    on = (d.prev == -2 && strip == 0) ||
+                         (d.next == -2 && (strip == d.n_strips - 1 || (short_last(d) && strip == d.n_strips - 2)));
+                }
+            }
+            mask = __ballot_sync(0xffffffffu, on);
+        }
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        return gw + (chunk * 32 + b) * nwarps;
+    };
+    auto issue = [&](int64_t t, int s) {
         if (lane == 0) {
-            const int64_t lt = t - v.t0;
+            const int q = part_of(t);
+            const int64_t lt = t - a.p[q].tile0;
             const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
             const int x = (int)(cb * OW - 1) & ~3, y = (int)(strip * R);   // buffer row (hd = T)
-            mbar_expect_tx(bar, 2 * kBox);
-            tma_load_2d(sb, &a.ts[sq][cur], x, y, bar);
-            tma_load_2d(kb, &a.tk[sq], x, y, bar);
+            uint32_t* sb = slots + s * (2 * ROWS * BW);
+            mbar_expect_tx(&bars[s], 2 * kBox);
+            tma_load_2d(sb, &a.ts[q][cur], x, y, &bars[s]);
+            tma_load_2d(sb + ROWS * BW, &a.tk[q], x, y, &bars[s]);
         }
     };
     int my_last = -1;
-    int64_t t = next_active(gw);
-    int q = sq;
-    int64_t lt = t - v.t0;
-    uint8_t* fc = v.fc;
-    if (t < a.total) issue(t);
-    while (t < a.total) {
-        mbar_wait(bar, phase);
-        phase ^= 1u;
+    int64_t t = next_tile();
+    if (t >= 0) issue(t, 0);
+    int64_t nxt = t >= 0 ? next_tile() : -1;
+    if (nxt >= 0) issue(nxt, 1);
+    int s = 0;
+    while (t >= 0) {
+        mbar_wait(&bars[s], (phases >> s) & 1u);
+        phases ^= 1u << s;
+        const int q = part_of(t);
+        const PlanePartDesc& d = a.p[q];
+        const int64_t lt = t - d.tile0;
+        const uint32_t* sb = slots + s * (2 * ROWS * BW);
+        const uint32_t* kb = sb + ROWS * BW;
         const int o = (int)((lt % n_cb) * OW - 1) & 3;
         uint32_t sv[ROWS], kv[ROWS];
 #pragma unroll
@@ -1694,22 +1653,40 @@ __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, in
             sv[i] = sb[i * BW + o + lane];
             kv[i] = kb[i * BW + o + lane];
         }
-        __syncwarp();
-        const int64_t tn = next_active(t + nwarps);
-        if (tn < a.total) issue(tn);
+        __syncwarp();                                  // slot s free: refill it
+        const int64_t n2 = nxt >= 0 ? next_tile() : -1;
+        if (n2 >= 0) issue(n2, s);
         const int64_t strip = lt / n_cb, cb = lt - strip * n_cb;
         const int64_t w = cb * OW - 1 + lane;
         const int tl = plane_steps<T, ROWS>(sv, kv, steps, own_lane, lane);
-        const uint8_t fl = tl < 0 ? 0 : (tl == steps - 1 ? 3 : 2);
         my_last = max(my_last, tl);
         const bool wv = w >= 0 && w < a.wp;
-        plane_store<T, ROWS>(sv, a.p[q].S[cur ^ 1], a.p[q].rows, a.wp, T, strip * R - T, w, own_lane, wv);
+        plane_store<T, ROWS>(sv, d.S[cur ^ 1], d.rows, a.wp, T, strip * R - T, w, own_lane, wv);
         plane_store_fwd<T, ROWS>(sv, a, q, cur, strip, w, own_lane, wv);
-        if (lane == 0) fc[lt] = fl;
-        t = tn;
-        q = sq;
-        lt = t - v.t0;
-        fc = v.fc;
+        if (tl >= 0) {
+            const bool live = tl == steps - 1;
+            int64_t target = -1;
+            const int64_t c2 = cb + lane % 3 - 1;
+            if (lane < 9) {   // the partition's own 3x3 neighbourhood (lane 4: the tile)
+                const int64_t s2 = strip + lane / 3 - 1;
+                if ((live || lane == 4) && s2 >= 0 && s2 < d.n_strips && c2 >= 0 && c2 < n_cb)
+                    target = d.tile0 + s2 * n_cb + c2;
+            } else if (live && lane < 18 && c2 >= 0 && c2 < n_cb) {
+                if (lane < 15) {   // previous partition: last strip, and the one before a short one
+                    if (strip == 0 && d.prev >= 0) {
+                        const PlanePartDesc& pd = a.p[d.prev];
+                        if (lane < 12) target = pd.tile0 + (pd.n_strips - 1) * n_cb + c2;
+                        else if (short_last(pd) && pd.n_strips >= 2) target = pd.tile0 + (pd.n_strips - 2) * n_cb + c2;
+                    }
+                } else if (d.next >= 0 && (strip == d.n_strips - 1 || (short_last(d) && strip == d.n_strips - 2))) {
+                    target = a.p[d.next].tile0 + c2;   // next partition: first strip
+                }
+            }
+            if (target >= 0) act[target] = stamp + 1;
+        }
+        t = nxt;
+        nxt = n2;
+        s ^= 1;
     }
     return my_last;
 }
@@ -1717,17 +1694,18 @@ __device__ __forceinline__ int plane_multi_pass_warp(const PlaneMultiArgs& a, in
 template <int T, int ROWS>
 __global__ void __launch_bounds__(256, 1) k_planes_multi(const __grid_constant__ PlaneMultiArgs a,
                                                       int64_t max_iters, int* __restrict__ flags,
-                                                      int* __restrict__ state) {
+                                                      int* __restrict__ state,
+                                                      unsigned long long* __restrict__ prof) {
     constexpr int BW = 36;
-    extern __shared__ __align__(128) uint32_t psm[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * ROWS * BW);
+    extern __shared__ __align__(128) uint32_t psm[];   // 8 x 2 warp slots, then 16 mbarriers
+    uint64_t* bars = reinterpret_cast<uint64_t*>(psm + 8 * 2 * 2 * ROWS * BW);
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t* sb = psm + wid * (2 * ROWS * BW);
-    uint32_t* kb = sb + ROWS * BW;
-    uint64_t* bar = &bars[wid];
+    uint32_t* slots = psm + wid * (2 * 2 * ROWS * BW);
+    uint64_t* bar = &bars[2 * wid];
     if (lane == 0) {
-        mbar_init(bar, 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -1738,18 +1716,30 @@ __global__ void __launch_bounds__(256, 1) k_planes_multi(const __grid_constant__
     int* own = xr ? a.xbar[a.rank] : nullptr;
     // arrivals of earlier runs (every rank ran the same passes: equal on all)
     const int epoch0 = xr && leader ? *((volatile int*)&own[1]) : 0;
-    uint32_t phase = 0;
+    // act[total] = this run's stamp base (as in k_planes_loop)
+    const uint32_t base = *((volatile uint32_t*)&a.act[a.total]);
+    if (prof && leader) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        prof[0] = t;
+    }
+    uint32_t phases = 0;
     int64_t k0 = 0;
     int pass = 0;
     while (k0 < max_iters) {
         const int steps = (int)min((int64_t)T, max_iters - k0);
         if (leader) flags[(pass + 1) % 3] = -1;
-        const int my_last = plane_multi_pass_warp<T, ROWS>(a, pass & 1, steps, pass == 0, gw, nwarps,
-                                                           lane, sb, kb, bar, phase);
+        const int my_last = plane_multi_pass_warp<T, ROWS>(a, pass & 1, steps, pass == 0, base + (uint32_t)pass,
+                                                           gw, nwarps, lane, slots, bar, phases);
         if (lane == 0 && my_last >= 0) atomicMax(&flags[pass % 3], (int)(k0 + my_last));
         asm volatile("fence.proxy.async.global;" ::: "memory");
         if (xr) __threadfence_system();   // halo stores into peers before the rank barrier
         grid.sync();
+        if (prof && leader && pass < 30) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            prof[1 + pass] = t;
+        }
         if (xr) {
             // rank barrier + all-reduce (max) of the last changing execution:
             // each leader publishes its value into every rank's slot, then
@@ -1794,6 +1784,8 @@ __global__ void __launch_bounds__(256, 1) k_planes_multi(const __grid_constant__
                 state[1] = 0;
                 state[2] = (pass & 1) ? 0 : 1;
                 state[3] = -1;
+                a.act[a.total] = base + (uint32_t)pass + 2;
+                flags[0] = -1;   // ready for the next run (see k_planes_loop)
             }
             return;
         }
@@ -1805,6 +1797,8 @@ __global__ void __launch_bounds__(256, 1) k_planes_multi(const __grid_constant__
                 state[2] = (pass & 1) ? 0 : 1;
                 state[3] = 0;
                 if (xr) own[1] = epoch0 + (pass + 1) * a.nranks;
+                a.act[a.total] = base + (uint32_t)pass + 2;
+                flags[0] = -1;
             }
             return;
         }
@@ -1817,6 +1811,8 @@ __global__ void __launch_bounds__(256, 1) k_planes_multi(const __grid_constant__
         state[2] = pass == 0 ? 0 : (((pass - 1) & 1) ? 0 : 1);
         state[3] = 0;
         if (xr) own[1] = epoch0 + pass * a.nranks;
+        a.act[a.total] = base + (uint32_t)pass + 2;
+        flags[0] = -1;
     }
 }
 
@@ -2751,6 +2747,16 @@ static unsigned long long* hyst_prof_buf() {
     }();
     return p;
 }
+static void hyst_prof_print(const unsigned long long* prof, unsigned grid, int64_t tiles, cudaStream_t st) {
+    unsigned long long h[128];
+    cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "MW_HYST_PROF grid=%u tiles=%lld", grid, (long long)tiles);
+    for (int i = 1; i < 32 && h[i]; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) / 1e3);
+    fprintf(stderr, " us; tiles run / executions per pass:");
+    for (int i = 0; i < 30 && h[64 + i]; ++i) fprintf(stderr, " %llu/%llu", h[64 + i], h[32 + i]);
+    fprintf(stderr, "\n");
+}
 
 template <int T, int ROWS>
 static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t rows,
@@ -2777,16 +2783,7 @@ static cudaError_t planes_loop_t(uint32_t* S0, uint32_t* S1, const uint32_t* K, 
     ++g_launches;
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_planes_loop<T, ROWS>, dim3(grid),
                                                 dim3(256), args, smem, L.stream);
-    if (prof && e == cudaSuccess) {
-        unsigned long long h[128];
-        cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, L.stream);
-        cudaStreamSynchronize(L.stream);
-        fprintf(stderr, "MW_HYST_PROF grid=%u tiles=%lld", grid, (long long)tiles);
-        for (int i = 1; i < 32 && h[i]; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) / 1e3);
-        fprintf(stderr, " us; tiles run / executions per pass:");
-        for (int i = 0; i < 30 && h[64 + i]; ++i) fprintf(stderr, " %llu/%llu", h[64 + i], h[32 + i]);
-        fprintf(stderr, "\n");
-    }
+    if (prof && e == cudaSuccess) hyst_prof_print(prof, grid, tiles, L.stream);
     return e;
 }
 
@@ -2856,7 +2853,7 @@ cudaError_t planes_loop(uint32_t* S0, uint32_t* S1, const uint32_t* K, int64_t r
 template <int T, int ROWS>
 static cudaError_t planes_multi_t(const PlaneMultiHost& h, int64_t max_iters, int* flags, int* state,
                                   const Launch& L) {
-    constexpr size_t smem = plane_smem_bytes<ROWS>();
+    constexpr size_t smem = plane_loop_smem_bytes<ROWS>();
     static int occ = [] {
         cudaFuncSetAttribute(k_planes_multi<T, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
@@ -2902,15 +2899,21 @@ static cudaError_t planes_multi_t(const PlaneMultiHost& h, int64_t max_iters, in
             return cudaErrorInvalidValue;
     }
     a.total = tiles;
+    if (!h.act || h.act_words < tiles + 1) return cudaErrorInvalidValue;
+    a.act = h.act;
     // loopback ranks share the GPU: each rank's cooperative grid takes its
     // share of the SMs so every rank's kernel is resident at the barriers
     const unsigned grid = std::max(1u, std::min(grid_for(std::max<int64_t>(1, (tiles + 7) / 8), occ, L),
                                                 (unsigned)(sm_count() * occ / std::max(1, h.grid_div))));
     int64_t mi = max_iters;
-    void* args[] = {&a, &mi, &flags, &state};
+    unsigned long long* prof = hyst_prof_buf();
+    if (prof) cudaMemsetAsync(prof, 0, 1024, L.stream);
+    void* args[] = {&a, &mi, &flags, &state, &prof};
     ++g_launches;
-    return cudaLaunchCooperativeKernel((const void*)k_planes_multi<T, ROWS>, dim3(grid), dim3(256), args,
-                                       smem, L.stream);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_planes_multi<T, ROWS>, dim3(grid), dim3(256),
+                                                args, smem, L.stream);
+    if (prof && e == cudaSuccess) hyst_prof_print(prof, grid, tiles, L.stream);
+    return e;
 }
 
 cudaError_t planes_multi(const PlaneMultiHost& h, int T, int64_t max_iters, int* flags, int* state,

@@ -169,6 +169,7 @@ struct PlaneMultiArgs {
     uint32_t* rnext_S[2];   // next active rank's first partition (next == -2)
     int* xbar[kXRanks];     // every rank's barrier block
     int rank, nranks;       // nranks == 1: no cross-rank barrier
+    uint32_t* act;          // total + 1 activity stamps (the last: the stamp base)
 };
 struct PlaneMultiHost {
     int np;                 // 0 allowed with nranks > 1 (the rank only joins the barriers)
@@ -186,6 +187,8 @@ struct PlaneMultiHost {
     int* xbar[kXRanks]{};
     int rank = 0, nranks = 1;
     int grid_div = 1;       // loopback ranks share one GPU: each gets 1/grid_div of it
+    uint32_t* act = nullptr;   // activity stamps over the concatenated tiles (scratch, never cleared)
+    int64_t act_words = 0;     // >= tiles + 1
 };
 // state[3] = -1 when a cross-rank barrier timed out (10 s; the run aborted).
 cudaError_t planes_multi(const PlaneMultiHost& h, int T, int64_t max_iters, int* flags, int* state,

@@ -1076,6 +1076,40 @@ def test_hysteresis_partitions_fused_and_per_pass(fused):
         assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, 13)[0])
 
 
+@pytest.mark.parametrize("ppr", [1, 4])
+def test_hysteresis_repeated_runs_one_ctx(ppr):
+    """Runs of one ctx reuse the plane buffers: the image-edge halo rows and
+    the loop flags are set up once per buffer set (the loop kernels leave their
+    flags ready) and the per-tile activity stamps are never cleared.  A
+    sequence of different inputs, trees (while / max_iters / loop_for) and
+    paths (fused, per-pass, slowed partition) on the same buffers must match
+    the oracle at every run."""
+    H, W = 391, 700
+    c = pctx(ppr, None, 1)
+    L0 = None
+    seq = [(1, 0, None), (1, 0, 5), (0, 0, None), (1, 0, None), (1, 2.0, None), (1, 0, 7), (1, 0, None)]
+    for i, (fused, slow, n) in enumerate(seq):
+        gray = synth.np_u8_stream(8, 100 + i, H * W).reshape(H, W)
+        L = K.segment(gray, 173, 250)
+        M.mw_ctx_set_tuning(c, M.MW_TUNE_HYST_FUSED, fused)
+        if ppr > 1:
+            M.mw_ctx_set_slowdown(c, 1, slow if slow else 1.0)
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        if n is None:
+            want, D = oracle_hyst(gray)
+            r = run(c, trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)])
+            assert r["executions"] == D + 1 and r["converged"], (i, r, D)
+        else:
+            want = K.hyst_finalize(K.hyst_bfs(L, n)[0])
+            r = run(c, trees.hysteresis(max_iters=n), [M.arg(dev(gray)), M.arg(dst)])
+            assert r["executions"] == n, (i, r)
+        assert np.array_equal(dst.cpu().numpy(), want), i
+        # a loop_for over the labels on the same buffers in between
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        run(c, M.mw_loop_for(M.mw_kernel_hysteresis_step(), 9), [M.arg(dev(L)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, 9)[0]), i
+
+
 def test_hysteresis_fused_partitions_graph_capture():
     """The fused multi-partition loop decides its condition on the device, so
     the while-loop tree can be captured and replayed."""

@@ -1076,6 +1076,65 @@ def test_hysteresis_partitions_fused_and_per_pass(fused):
         assert np.array_equal(dst.cpu().numpy(), K.hyst_bfs(L, 13)[0])
 
 
+def _path_image(H, W, pts):
+    """Gray image: 0 everywhere (below lo), weak (200) on the path, strong
+    (255) at its first point: the fronts run along the path one pixel per
+    execution, so the last change lands at a chosen execution."""
+    g = np.zeros((H, W), dtype=np.uint8)
+    for (y, x) in pts:
+        g[y, x] = 200
+    g[pts[0]] = 255
+    return g
+
+
+def _serpentine(H, W, legs, run, drop):
+    """Right `run` px, down `drop` rows, left `run` px, ... `legs` legs, then
+    the total length is known exactly (8-connected, no shortcuts: legs are
+    `drop` >= 2 rows apart)."""
+    pts, y, x, d = [], 1, 1, 1
+    for leg in range(legs):
+        for _ in range(run):
+            pts.append((y, x))
+            x += d
+        for _ in range(drop):
+            pts.append((y, x))
+            y += 1
+        d = -d
+    return pts
+
+
+@pytest.mark.parametrize("ppr", [1, 3])
+def test_hysteresis_fronts_across_tiles_and_passes(ppr):
+    """Fronts crossing warp-tile boundaries (32-row strips, 960-pixel column
+    blocks) and ending at every position of a pass (the first, a middle and
+    the last of the T = 8 executions): exercises the per-tile early stop,
+    the push-model activity stamps (self and 3x3, across partitions at ppr = 3)
+    and the exact E at pass boundaries."""
+    H, W = 300, 2100
+    cases = []
+    for L in (7, 8, 9, 15, 16, 17, 40):   # horizontal across the 960-px block edge
+        cases.append([(150, 955 - L // 2 + i) for i in range(L + 1)])
+    for L in (8, 9, 31, 33):               # vertical across strip edges
+        cases.append([(20 + i, 500) for i in range(L + 1)])
+    cases.append([(5 + i, 940 + i) for i in range(70)])   # diagonal through a tile corner
+    cases.append(_serpentine(H, W, 5, 1500, 3))           # long snake, E in the thousands
+    c = pctx(ppr, None, 1)
+    for k, pts in enumerate(cases):
+        gray = _path_image(H, W, pts)
+        want, D = oracle_hyst(gray)
+        dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+        r = run(c, trees.hysteresis(), [M.arg(dev(gray)), M.arg(dst)])
+        assert np.array_equal(dst.cpu().numpy(), want), k
+        assert r["executions"] == D + 1 and r["converged"], (k, r, D)
+        L = K.segment(gray, 173, 250)
+        for n in (D - 1, D, 8 * (D // 8)):
+            if n < 1:
+                continue
+            dst = torch.empty((H, W), dtype=torch.uint8, device=DEV)
+            r = run(c, trees.hysteresis(max_iters=n), [M.arg(dev(gray)), M.arg(dst)])
+            assert np.array_equal(dst.cpu().numpy(), K.hyst_finalize(K.hyst_bfs(L, n)[0])), (k, n)
+
+
 @pytest.mark.parametrize("ppr", [1, 4])
 def test_hysteresis_repeated_runs_one_ctx(ppr):
     """Runs of one ctx reuse the plane buffers: the image-edge halo rows and

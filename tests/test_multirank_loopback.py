@@ -244,6 +244,50 @@ def test_hysteresis_ranks_max_iters():
     assert all(x["executions"] == n and not x["converged"] for _, _, x in res)
 
 
+@pytest.mark.parametrize("nranks,ppr", [(2, 1), (3, 2)])
+def test_hysteresis_ranks_fronts_across_rank_boundaries(nranks, ppr):
+    """Fronts running along constructed paths across the rank boundaries
+    (vertical lines through the row split, a serpentine through every
+    partition): the fused cross-rank loop's forced boundary strips, the push
+    stamps of the partitions and the device barrier's loop condition must
+    give the oracle's iterates and E."""
+    H, W = 240, 1100
+    paths = [[(10 + i, 300) for i in range(200)],                      # vertical, crosses every split
+             [(5 + i, 900 + (i % 2)) for i in range(223)]]              # zig-zag column
+    # serpentine, legs 3 rows apart, through every rank (E = 8611 < max_iters)
+    pts, y, x, d = [], 1, 1, 1
+    for leg in range(70):
+        for _ in range(120):
+            pts.append((y, x))
+            x += d
+        for _ in range(3):
+            pts.append((y, x))
+            y += 1
+        d = -d
+        if y + 4 >= H:
+            break
+    paths.append(pts)
+    for k, p in enumerate(paths):
+        gray = np.zeros((H, W), dtype=np.uint8)
+        for (yy, xx) in p:
+            gray[yy, xx] = 200
+        gray[p[0]] = 255
+        want, D = oracle_hyst(gray)
+
+        def fn(r, c, s):
+            node = trees.hysteresis()
+            s0, s1, _ = local_rows(c, node, H, r)
+            dst = torch.empty((s1 - s0, W), dtype=torch.uint8, device=DEV)
+            res = M.mw_run(c, node, [M.arg(dev(gray[s0:s1]), local_offset=s0, global_shape=(H, W)),
+                                     M.arg(dst, local_offset=s0, global_shape=(H, W))]).wait().result()
+            return s0, dst.cpu().numpy(), res
+
+        res = run_ranks(nranks, ppr, None, fn)
+        out = assemble([(a, b) for a, b, _ in res], (H, W), np.uint8)
+        assert np.array_equal(out, want), k
+        assert all(x["executions"] == D + 1 and x["converged"] for _, _, x in res), (k, D)
+
+
 # ----------------------------------------------------------------- N-body (COPY re-replication)
 @pytest.mark.parametrize("nranks,ppr,dist", CASES)
 def test_nbody_ranks_replicated_bitwise(nranks, ppr, dist):

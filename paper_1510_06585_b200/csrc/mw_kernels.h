@@ -1,5 +1,6 @@
 // mw_kernels.h — internal launcher interface between the host runtime
-// (runtime.cpp) and the sm_100a kernels (kernels.cu).  Not part of the ABI.
+// (exec.cpp, graph.cpp, profile.cpp) and the sm_100a kernels (chains.cu,
+// planes.cu, nbody.cu, reduce.cu, fft.cu, kernels.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
 #include <cuda.h>

@@ -32,6 +32,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <set>
 
 #include "mw_kernels.h"
 
@@ -438,15 +439,15 @@ bool fft_supported(int log2n) { return log2n >= 13 && log2n <= 16; }
 
 cudaError_t fft_prepare(cudaStream_t s) {
     static std::mutex mu;
-    static bool filled[64] = {};
+    static std::set<int> filled;   // devices whose g_tw13 is written (one module copy per device)
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
-    if (dev >= 64 || filled[dev]) return cudaSuccess;
+    if (filled.count(dev)) return cudaSuccess;
     k_fft_tw13<<<32, 256, 0, s>>>();
     e = cudaGetLastError();
-    if (e == cudaSuccess) filled[dev] = true;
+    if (e == cudaSuccess) filled.insert(dev);
     return e;
 }
 

@@ -312,9 +312,12 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // Every execution inside a pass is one global Jacobi step; the device keeps
 // the last execution index that changed an owned pixel, so E is exact and a
 // pass that ends without change has reached the fixed point (extra in-pass
-// executions past it are no-ops).  Tiles whose 3x3 tile neighbourhood did not
-// change in the previous pass are skipped.  One cooperative kernel runs all
-// passes; flags[pass % 3] = last changed execution of the pass (-1: none).
+// executions past it are no-ops).  Tiles are skipped when provably unchanged
+// (no live front in their 3x3 tile neighbourhood and no change of their own in
+// the previous pass; DESIGN R35), and a tile stops its pass early once an
+// execution changes nothing on its exact positions (R34).  One cooperative
+// kernel runs all passes; flags[pass % 3] = last changed execution of the
+// pass (-1: none).
 
 // One warp tile: T Jacobi executions (steps <= T) on register rows
 // [strip*R - T, strip*R + R + T) x lanes, owned rows/lanes written to `out`.
@@ -324,6 +327,7 @@ __global__ void __launch_bounds__(256) k_planes_unpack(const __grid_constant__ U
 // (Measured on B200: keeping the weak plane in registers with 256-thread CTAs
 // and a rolled execution loop beats smem-resident K and a fully unrolled
 // shrinking-window loop, whose code no longer fits the instruction cache.)
+
 // One execution on register rows [LO, HI] (rows outside keep their values
 // and only serve as neighbours).  Returns bit 0: an owned row [T, ROWS - T)
 // of an owned lane changed; bit 1: a bit of the window inside `vm` changed.
@@ -472,9 +476,9 @@ __device__ __forceinline__ bool plane_tile_active(const uint8_t* fprev, int64_t 
 // words from the 16-byte-aligned column at or left of the tile's first word
 // — TMA box origins are 16-byte aligned; lane l reads word o + l of a box
 // row — 2-D TMA with out-of-bounds zero fill = the image-boundary rule)
-// into its shared-memory slot while it computes the current one; the L2
-// latency of the tile load (~2.4 us per tile measured with plain loads,
-// 28 % of the loop) is hidden behind the T executions.
+// into one of its two shared-memory slots while it computes the current one;
+// the L2 latency of the tile load (~2.4 us per tile measured with plain
+// loads, 28 % of the loop in round 1) is hidden behind the executions.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
                                             uint64_t* bar) {
     asm volatile(

@@ -447,7 +447,11 @@ enum {
                                  argument sets are pairwise independent (no write overlaps
                                  another set's buffers) are captured on up to this many
                                  parallel lanes (1, 2, 4); 1 = strictly serialized replays   */
-    MW_TUNE_COUNT = 9
+    MW_TUNE_FFT_4STEP = 9,    /* pipeline(fft, ifft) at N = 65536: 1 = 4-step 256 x 256 path
+                                 (three launches per chunk of transforms, L2-resident
+                                 intermediate in the output buffer); 0 = one thread-block
+                                 cluster per transform (distributed shared memory)           */
+    MW_TUNE_COUNT = 10
 };
 mw_status mw_ctx_set_tuning(mw_ctx* ctx, int32_t knob, int32_t value);
 mw_status mw_ctx_get_tuning(const mw_ctx* ctx, int32_t knob, int32_t* value);

@@ -30,7 +30,9 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 
@@ -51,13 +53,25 @@ constexpr size_t kFftSmem = sizeof(float2) * (FPAD + T9 + THI + TLO);
 // W_8192^(r k) at [r][k], r < 16, k < 512 (forward sign), filled once per
 // device by k_fft_tw13 before the first FFT launch.
 __device__ float2 g_tw13[16 * 512];
+// The 4-step path's tables: W_256^(l k) at [l][k] (l, k < 16) and the
+// full-circle two-level W_65536^e = hi[e >> 8] * lo[e & 255].
+__device__ float2 g_w256[256];
+__device__ float2 g_w16hi[256];
+__device__ float2 g_w16lo[256];
 __global__ void k_fft_tw13() {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 16 * 512) return;
-    const int r = i / 512, k = i % 512;
     double sn, cs;
-    sincospi(2.0 * ((r * k) & 8191) / 8192.0, &sn, &cs);
-    g_tw13[i] = make_float2((float)cs, (float)-sn);
+    if (i < 16 * 512) {
+        const int r = i / 512, k = i % 512;
+        sincospi(2.0 * ((r * k) & 8191) / 8192.0, &sn, &cs);
+        g_tw13[i] = make_float2((float)cs, (float)-sn);
+    } else if (i < 16 * 512 + 3 * 256) {
+        const int j = i - 16 * 512, t = j / 256, e = j % 256;
+        const double x = t == 0 ? 2.0 * ((e / 16) * (e % 16)) / 256.0
+                       : t == 1 ? 2.0 * 256.0 * e / 65536.0 : 2.0 * e / 65536.0;
+        sincospi(x, &sn, &cs);
+        (t == 0 ? g_w256 : t == 1 ? g_w16hi : g_w16lo)[e] = make_float2((float)cs, (float)-sn);
+    }
 }
 
 __device__ __forceinline__ int fpad(int i) { return i + (i >> 5); }
@@ -249,6 +263,9 @@ __device__ __forceinline__ void war_wait() {
     else __syncthreads();
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
 __device__ __forceinline__ float2 ld_nc(const float2* p) {
     float2 v;
     asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
@@ -388,6 +405,241 @@ __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, in
     war_wait<C>();   // no CTA leaves while a peer may still read its shared memory
 }
 
+// ---- 4-step path for the fused pipeline(fft, ifft) at N = 65536 = 256 x 256.
+// n = c + 256 r (c: column, r: row), k = k2 + 256 k1:
+//   A (columns):  Y[k2][c] = sum_r x[c + 256 r] W_256^{r k2}, then x W_N^{c k2}
+//   B (rows):     X[k2 + 256 k1] = sum_c Y'[k2][c] W_256^{c k1}
+// and the inverse mirrored: B^-1 over k1 -> Z'[k2][c], x W_N^{-c k2}, A^-1
+// over k2 -> x[c + 256 r] (1/N).  Three launches per chunk of transforms —
+// A, then B with B^-1 fused (the spectrum never leaves the registers), then
+// A^-1 — each in place on the output buffer, which holds the intermediate:
+// a chunk (64 transforms = 32 MiB) stays in L2 between the launches, so HBM
+// sees one read of the input and one write of the output.  No clusters, no
+// distributed shared memory: every 256-point DFT belongs to one half-warp
+// (16 points per lane, two radix-16 register DFTs and one shared-memory
+// transpose), so each SM keeps many independent DFTs in flight.
+
+// DFT-256 of TWO independent rows by a half-warp (interleaved for ILP): lane
+// l holds x[l + 16 j], j < 16, of each and ends with X[l + 16 j] (the same
+// layout).  16 x 16: DFT-16 over j, twiddle W_256^{l k1} (the table is
+// symmetric, read as [k1][l]: consecutive across the lanes), transpose
+// through sc ([16][17] per row: conflict-free both ways), DFT-16 over l.
+template <bool INV>
+__device__ __forceinline__ void dft256_hw2(float2 (&a)[16], float2 (&b)[16], int l, float2* sa, float2* sb,
+                                           const float2* w256) {
+    dft<16, INV>(a);
+    dft<16, INV>(b);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+        const float2 w = w256[k * 16 + l];
+        a[k] = cmulw<INV>(a[k], w);
+        b[k] = cmulw<INV>(b[k], w);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        sa[k * 17 + l] = a[k];
+        sb[k * 17 + l] = b[k];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        a[j] = sa[l * 17 + j];
+        b[j] = sb[l * 17 + j];
+    }
+    __syncwarp();
+    dft<16, INV>(a);
+    dft<16, INV>(b);
+}
+// The same two DFT-256s with the transpose done inside the columns' own
+// tile storage (column c at tile[r * pitch + c]): y[l][k1] goes to row
+// 16 k1 + ((l + k1) & 15), read back by lane L at rows 16 L + ((j + L) & 15)
+// — with an odd pitch both directions are bank-conflict-free, and no scratch
+// is needed (more CTAs per SM).
+template <bool INV, int PITCH>
+__device__ __forceinline__ void dft256_col2(float2 (&a)[16], float2 (&b)[16], int l, float2* tile, int ca,
+                                            int cb, const float2* w256) {
+    dft<16, INV>(a);
+    dft<16, INV>(b);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+        const float2 w = w256[k * 16 + l];
+        a[k] = cmulw<INV>(a[k], w);
+        b[k] = cmulw<INV>(b[k], w);
+    }
+    __syncwarp();   // every lane has read its column values
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int r = 16 * k + ((l + k) & 15);
+        tile[r * PITCH + ca] = a[k];
+        tile[r * PITCH + cb] = b[k];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int r = 16 * l + ((j + l) & 15);
+        a[j] = tile[r * PITCH + ca];
+        b[j] = tile[r * PITCH + cb];
+    }
+    __syncwarp();
+    dft<16, INV>(a);
+    dft<16, INV>(b);
+}
+__device__ __forceinline__ float2 tw65536(const float2* tb, int e, bool inv) {
+    float2 w = cmul(tb[256 + (e >> 8)], tb[512 + (e & 255)]);
+    if (inv) w.y = -w.y;
+    return w;
+}
+// the three 256-entry tables (W_256 [l][k], W_65536 hi, lo) into shared memory
+__device__ __forceinline__ void f4_tables(float2* tb) {
+    for (int i = threadIdx.x; i < 768; i += blockDim.x)
+        tb[i] = __ldg(i < 256 ? &g_w256[i] : i < 512 ? &g_w16hi[i - 256] : &g_w16lo[i - 512]);
+}
+
+
+
+// Column pass over one 256 x 32 tile (columns c0 .. c0 + 31) of transform f:
+// INV = false: A + W_N^{c k2}; INV = true: A^-1 and 1/N.  In place on `out`
+// (the input `in` on the forward pass).
+constexpr int kF4Cols = 16;                 // columns per tile (8 half-warps x 2)
+constexpr int kF4Pitch = kF4Cols + 1;       // odd pitch: conflict-free column access
+constexpr size_t kF4ColSmem = sizeof(float2) * (256 * kF4Pitch + 768);
+
+// Column pass over one 256 x 16 tile (columns c0 .. c0 + 15) of transform f:
+// INV = false: A + W_N^{c k2}; INV = true: A^-1 and 1/N.  In place on `out`
+// (the input `in` on the forward pass).  128 threads, ~41 KiB: four CTAs per
+// SM overlap one another's load, compute and store phases.  (Measured: a
+// persistent version with two tile buffers per CTA — the next tile's copies
+// landing during the current one — 0.405 vs 0.335 ms per batch: fewer CTAs
+// per SM hide less.)
+template <bool INV>
+__global__ void __launch_bounds__(128) k_fft4_cols(const float2* in, float2* out, int64_t f0) {
+    extern __shared__ float4 f4_smem[];
+    float2* tile = reinterpret_cast<float2*>(f4_smem);
+    float2* tb = tile + 256 * kF4Pitch;
+    f4_tables(tb);
+    const int tid = threadIdx.x;
+    constexpr int kTiles = 256 / kF4Cols;
+    const int64_t f = f0 + blockIdx.x / kTiles;
+    const int c0 = (blockIdx.x % kTiles) * kF4Cols;
+    const float2* src = in + f * 65536 + c0;
+    float2* dst = out + f * 65536 + c0;
+    const int cc = tid & (kF4Cols - 1), r0 = tid / kF4Cols;
+    constexpr int kRowStep = 128 / kF4Cols;
+    // all of this thread's elements in flight at once (asynchronous copies
+    // straight into the padded tile: no registers held across the latency)
+#pragma unroll
+    for (int i = 0; i < 256 / kRowStep; ++i) {
+        const int r = r0 + kRowStep * i;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(tile + r * kF4Pitch + cc)),
+                     "l"(src + r * 256 + cc)
+                     : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const int hw = tid >> 4, l = tid & 15;
+    const int ca = 2 * hw, cb = 2 * hw + 1;   // this half-warp's two columns
+    float2 a[16], b[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        a[j] = tile[(l + 16 * j) * kF4Pitch + ca];
+        b[j] = tile[(l + 16 * j) * kF4Pitch + cb];
+    }
+    dft256_col2<INV, kF4Pitch>(a, b, l, tile, ca, cb, tb);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int k = l + 16 * j;
+        if (!INV) {
+            a[j] = cmul(a[j], tw65536(tb, ((c0 + ca) * k) & 65535, false));
+            b[j] = cmul(b[j], tw65536(tb, ((c0 + cb) * k) & 65535, false));
+        } else {
+            a[j] = make_float2(a[j].x * (1.0f / 65536.0f), a[j].y * (1.0f / 65536.0f));
+            b[j] = make_float2(b[j].x * (1.0f / 65536.0f), b[j].y * (1.0f / 65536.0f));
+        }
+    }
+    __syncwarp();   // the transposed values were read by every lane
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int k = l + 16 * j;
+        tile[k * kF4Pitch + ca] = a[j];
+        tile[k * kF4Pitch + cb] = b[j];
+    }
+    __syncthreads();
+    // the forward pass leaves the intermediate for the row pass (no
+    // streaming hint); the inverse pass writes the result (streaming)
+#pragma unroll 8
+    for (int i = 0; i < 256 / kRowStep; ++i) {
+        const int r = r0 + kRowStep * i;
+        if (INV) st_cs(dst + r * 256 + cc, tile[r * kF4Pitch + cc]);
+        else dst[r * 256 + cc] = tile[r * kF4Pitch + cc];
+    }
+}
+
+// Row pass, fused B then B^-1 (then W_N^{-c k2}) on 32 rows per CTA (two
+// per half-warp, interleaved), in place; rows go straight to registers
+// (coalesced), the transposes through a [16][17] scratch per row.  (Staging
+// the rows through shared memory with in-place transposes, as the column
+// pass does, measured slower: 0.347 vs 0.335 ms per batch.)
+constexpr size_t kF4RowSmem = sizeof(float2) * (32 * 16 * 17 + 768);
+__global__ void __launch_bounds__(256) k_fft4_rows_fi(float2* out, int64_t f0) {
+    extern __shared__ float4 f4r_smem[];
+    float2* scr = reinterpret_cast<float2*>(f4r_smem);
+    float2* tb = scr + 32 * 16 * 17;
+    f4_tables(tb);
+    __syncthreads();
+    const int tid = threadIdx.x;
+    const int hw = tid >> 4, l = tid & 15;
+    const int64_t f = f0 + blockIdx.x / 8;
+    const int ka = (blockIdx.x % 8) * 32 + 2 * hw, kb = ka + 1;
+    float2* ra = out + f * 65536 + (int64_t)ka * 256;
+    float2* rb = ra + 256;
+    float2 a[16], b[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        a[j] = ra[l + 16 * j];
+        b[j] = rb[l + 16 * j];
+    }
+    float2* sa = scr + (2 * hw) * (16 * 17);
+    float2* sb = sa + 16 * 17;
+    dft256_hw2<false>(a, b, l, sa, sb, tb);   // X[k2 + 256 k1], k1 = l + 16 j
+    dft256_hw2<true>(a, b, l, sa, sb, tb);    // Z'[k2][c], c = l + 16 j
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int c = l + 16 * j;
+        ra[c] = cmul(a[j], tw65536(tb, (ka * c) & 65535, true));
+        rb[c] = cmul(b[j], tw65536(tb, (kb * c) & 65535, true));
+    }
+}
+
+static int64_t tuning_chunk() {
+    static const int64_t c = [] {
+        const char* v = getenv("MW_FFT4_CHUNK");
+        return v ? (int64_t)atoi(v) : (int64_t)512;
+    }();
+    return c;
+}
+
+cudaError_t fft4_fi(const float2* in, float2* out, int64_t nfft, const Launch& L) {
+    static bool attr = [] {
+        cudaFuncSetAttribute(k_fft4_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);
+        cudaFuncSetAttribute(k_fft4_cols<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);
+        cudaFuncSetAttribute(k_fft4_rows_fi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4RowSmem);
+        return true;
+    }();
+    (void)attr;
+    const int64_t chunk = tuning_chunk();   // transforms per launch triple
+    for (int64_t f0 = 0; f0 < nfft; f0 += chunk) {
+        const int64_t nf = nfft - f0 < chunk ? nfft - f0 : chunk;
+        const unsigned cgrid = (unsigned)(nf * (256 / kF4Cols));
+        note_launch();
+        k_fft4_cols<false><<<cgrid, 128, kF4ColSmem, L.stream>>>(in, out, f0);
+        note_launch();
+        k_fft4_rows_fi<<<(unsigned)(nf * 8), 256, kF4RowSmem, L.stream>>>(out, f0);
+        note_launch();
+        k_fft4_cols<true><<<cgrid, 128, kF4ColSmem, L.stream>>>(out, out, f0);
+    }
+    return cudaGetLastError();
+}
+
 template <int C, int MODE>
 cudaError_t fft_launch(const float2* in, float2* out, int64_t nfft, const Launch& L) {
     static int max_clusters = -1;
@@ -445,7 +697,7 @@ cudaError_t fft_prepare(cudaStream_t s) {
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
     if (filled.count(dev)) return cudaSuccess;
-    k_fft_tw13<<<32, 256, 0, s>>>();
+    k_fft_tw13<<<35, 256, 0, s>>>();
     e = cudaGetLastError();
     if (e == cudaSuccess) filled.insert(dev);
     return e;
@@ -475,6 +727,15 @@ cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint
             used = 2;
         }
         cudaError_t e;
+        // the 4-step path for the fused pair at 2^16 (the slowdown injector's
+        // clamped grids stay on the cluster path, whose clusters are persistent)
+        if (mode == FFT_FI && log2n == 16 && L.tune[TUNE_FFT_4STEP] && !(L.slow > 1.0f)) {
+            e = fft4_fi(src, o2, nfft, L);
+            if (e != cudaSuccess) return e;
+            src = o2;
+            s += used;
+            continue;
+        }
         switch (log2n) {
             case 13: e = fft_launch_mode<1>(mode, src, o2, nfft, L); break;
             case 14: e = fft_launch_mode<2>(mode, src, o2, nfft, L); break;

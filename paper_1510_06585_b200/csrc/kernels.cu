@@ -36,6 +36,7 @@ void tune_defaults(int* out) {
     out[TUNE_U8_TMA] = tuning_knob("MW_U8_TMA", 1);
     out[TUNE_HYST_FUSED] = tuning_knob("MW_HYST_FUSED", 1);
     out[TUNE_GRAPH_LANES] = tuning_knob("MW_GRAPH_LANES", 4);
+    out[TUNE_FFT_4STEP] = tuning_knob("MW_FFT_4STEP", 1);
     for (int k = 0; k < TUNE_COUNT; ++k)
         if (!tune_valid(k, out[k])) {   // ignore malformed overrides
             const int d[TUNE_COUNT] = {1, 2, 1, 8, 48, 0, 1, 1, 4};
@@ -54,6 +55,7 @@ bool tune_valid(int knob, int v) {
         case TUNE_U8_TMA: return v == 0 || v == 1;
         case TUNE_HYST_FUSED: return v == 0 || v == 1;
         case TUNE_GRAPH_LANES: return v == 1 || v == 2 || v == 4;
+        case TUNE_FFT_4STEP: return v == 0 || v == 1;
     }
     return false;
 }

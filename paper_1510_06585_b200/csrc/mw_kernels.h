@@ -18,7 +18,7 @@ constexpr int kMaxOps = 16;
 enum TuneKnob : int {
     TUNE_RGBA_TMA = 0, TUNE_RGBA_UNROLL = 1, TUNE_HYST_PLANES = 2, TUNE_HYST_T = 3,
     TUNE_HYST_ROWS = 4, TUNE_NBODY_SPLIT = 5, TUNE_U8_TMA = 6, TUNE_HYST_FUSED = 7,
-    TUNE_GRAPH_LANES = 8, TUNE_COUNT = 9
+    TUNE_GRAPH_LANES = 8, TUNE_FFT_4STEP = 9, TUNE_COUNT = 10
 };
 void tune_defaults(int* out);                 // measured best on B200 (+ MW_* env overrides)
 bool tune_valid(int knob, int value);

@@ -35,8 +35,8 @@ MW_BALANCE_PROPORTIONAL, MW_BALANCE_ABS = 0, 1
 MW_PROV_BUILT, MW_PROV_DERIVED, MW_PROV_BALANCED = 0, 1, 2
 MW_KB_NONE, MW_KB_EXACT, MW_KB_SCT, MW_KB_WORKLOAD, MW_KB_DIMENSIONALITY = range(5)
 (MW_TUNE_RGBA_TMA, MW_TUNE_RGBA_UNROLL, MW_TUNE_HYST_PLANES, MW_TUNE_HYST_T, MW_TUNE_HYST_ROWS,
- MW_TUNE_NBODY_SPLIT, MW_TUNE_U8_TMA, MW_TUNE_HYST_FUSED, MW_TUNE_GRAPH_LANES,
- MW_TUNE_COUNT) = range(10)
+ MW_TUNE_NBODY_SPLIT, MW_TUNE_U8_TMA, MW_TUNE_HYST_FUSED, MW_TUNE_GRAPH_LANES, MW_TUNE_FFT_4STEP,
+ MW_TUNE_COUNT) = range(11)
 (MW_KC_SAXPY, MW_KC_RGBA, MW_KC_U8, MW_KC_STENCIL, MW_KC_NBODY, MW_KC_REDUCE,
  MW_KC_TRAITS, MW_KC_FFT, MW_KC_COUNT) = range(9)
 

@@ -790,6 +790,24 @@ def test_fft_chain_parity(log2n, dirs):
     assert torch.equal(src, dev(x))   # input untouched
 
 
+@pytest.mark.parametrize("four", [0, 1])
+@pytest.mark.parametrize("dirs", ["FI", "FIFI", "IFI"])
+def test_fft_fused_pair_paths(four, dirs):
+    """The fused pipeline(fft, ifft) at 2^16 on both implementations — the
+    4-step 256 x 256 path (MW_TUNE_FFT_4STEP = 1, default) and one
+    thread-block cluster per transform (0) — within the bound of the oracle,
+    also inside longer chains and after an inverse leaf."""
+    N, B = 1 << 16, 5
+    x = _fft_in(B, N, 123)
+    src = dev(x)
+    dst = torch.empty_like(src)
+    c = ctx()
+    M.mw_ctx_set_tuning(c, M.MW_TUNE_FFT_4STEP, four)
+    run(c, _fft_tree(16, dirs), [M.arg(src), M.arg(dst)])
+    _fft_check(dst.cpu().numpy(), x, dirs)
+    assert torch.equal(src, dev(x))
+
+
 def test_fft_pipeline_partitions_bitwise_and_batch():
     """The benchmark tree over a batch split into partitions (whole FFTs per
     partition, zero shares, ragged splits): every FFT is computed the same way

@@ -6,9 +6,9 @@ import os
 from paper_1510_06585_b200 import marrow as M
 from paper_1510_06585_b200 import trees
 
-T0 = [1, 2, 1, 8, 40, 0, 1, 1, 4]
-T1 = [0, 4, 1, 8, 40, 0, 0, 0, 1]
-T2 = [3, 2, 0, 4, 32, 1, 1, 1, 2]
+T0 = [1, 2, 1, 8, 40, 0, 1, 1, 4, 1]
+T1 = [0, 4, 1, 8, 40, 0, 0, 0, 1, 0]
+T2 = [3, 2, 0, 4, 32, 1, 1, 1, 2, 1]
 
 
 def test_store_lookup_exact_and_refinement(tmp_path):

@@ -237,12 +237,13 @@ struct DistGen {
 // likely first (P:555-565 ordering).
 using Setting = std::vector<std::pair<int, int>>;
 std::vector<std::vector<Setting>> config_dims(const mw_ctx* c, const std::vector<Step>& prog) {
-    bool rgba = false, u8 = false, stencil = false, nbody = false;
+    bool rgba = false, u8 = false, stencil = false, nbody = false, fft = false;
     for (const Step& st : prog) {
         rgba |= st.kind == StepKind::Rgba;
         u8 |= st.kind == StepKind::U8;
         stencil |= st.kind == StepKind::StencilFor || st.kind == StepKind::StencilWhile;
         nbody |= st.kind == StepKind::NbodyLoop || st.kind == StepKind::NbodyAccel;
+        fft |= st.kind == StepKind::Fft;
     }
     std::vector<std::vector<Setting>> dims;
     auto ordered = [&](int knob, std::vector<int> vals) {
@@ -266,6 +267,7 @@ std::vector<std::vector<Setting>> config_dims(const mw_ctx* c, const std::vector
         if (c->ppr > 1) ordered(mwk::TUNE_HYST_FUSED, {1, 0});
     }
     if (nbody) ordered(mwk::TUNE_NBODY_SPLIT, {0, 1});
+    if (fft) ordered(mwk::TUNE_FFT_4STEP, {1, 0});
     return dims;
 }
 

@@ -426,7 +426,8 @@ mw_status mw_ctx_set_slowdown(mw_ctx* ctx, int32_t part, float factor);
 
 /* Tuning knobs: the B200 platform configuration of a profile (P:446-456
  * item (d)) — block/element shapes the profile builder (mw_autotune)
- * searches.  Every value gives bit-identical results.  Defaults are the
+ * searches.  Every value gives bit-identical results (MW_TUNE_FFT_4STEP:
+ * two FFT algorithms, both within the oracle's bound).  Defaults are the
  * measured best on B200 (MW_* environment variables override them).       */
 enum {
     MW_TUNE_RGBA_TMA = 0,     /* fused RGBA chain: 0 LSU path, 1 = 16 KiB TMA ring, 2 stages

@@ -484,17 +484,23 @@ class Hysteresis(Workload):
         self.kclass = M.MW_KC_STENCIL
         self.H, self.W = H, W
         self.o, self.n = self.slice(H)
-        src = t.empty((self.n, W), dtype=t.uint8, device=self.dev)
-        self.synth.dev_fill_u8_stream(src, self.synth.SEED_HYST, self.o * W)
-        dst = t.empty_like(src)
-        self.sets = [(M.arg(src, local_offset=self.o, global_shape=(H, W)),
-                      M.arg(dst, local_offset=self.o, global_shape=(H, W)))]
-        self.B = 1
+        # a rank's share below 2x L2 (N >= 4) rotates over buffer sets (the
+        # bit planes themselves are ctx scratch, L2-resident by design)
+        ws = 2 * self.n * W
+        self.B = self.sets_for(ws)
+        self.sets = []
+        for _ in range(self.B):
+            src = t.empty((self.n, W), dtype=t.uint8, device=self.dev)
+            self.synth.dev_fill_u8_stream(src, self.synth.SEED_HYST, self.o * W)
+            dst = t.empty_like(src)
+            self.sets.append((M.arg(src, local_offset=self.o, global_shape=(H, W)),
+                              M.arg(dst, local_offset=self.o, global_shape=(H, W))))
         self.units, self.launch_bytes = H * W, 2 * self.n * W   # per stencil execution
-        self.l2_note = f"ping-pong labels {2 * (self.n + 2) * W >> 20} MiB/rank"
+        self.l2_note = (f"inputs larger than L2 ({ws >> 20} MiB/rank)" if self.B == 1 else
+                        f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)")
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, self.arglist(0))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(i % self.B))
 
     def plane(self, launches, steps):
         # bit planes unless disabled (one partition: one cooperative launch per
@@ -588,19 +594,23 @@ class Fft(Workload):
         self.kclass = M.MW_KC_FFT
         self.Bt, self.N = B, 1 << log2n
         self.o, self.n = self.slice(B)
-        src = t.empty((self.n, self.N, 2), dtype=t.float32, device=self.dev)
-        self.synth.dev_fill_f32_um11(src, 11, self.o * self.N * 2)
-        dst = t.empty_like(src)
         g = (B, self.N, 2)
-        self.sets = [(M.arg(src, local_offset=self.o, global_shape=g),
-                      M.arg(dst, local_offset=self.o, global_shape=g))]
-        self.B = 1
-        self.units = B
         ws = 2 * self.n * self.N * 8
-        self.l2_note = f"inputs larger than L2 ({ws >> 20} MiB/rank)"
+        # a rank's share below 2x L2 (N >= 4) rotates over buffer sets, as the filter
+        self.B = self.sets_for(ws)
+        self.sets = []
+        for _ in range(self.B):
+            src = t.empty((self.n, self.N, 2), dtype=t.float32, device=self.dev)
+            self.synth.dev_fill_f32_um11(src, 11, self.o * self.N * 2)
+            dst = t.empty_like(src)
+            self.sets.append((M.arg(src, local_offset=self.o, global_shape=g),
+                              M.arg(dst, local_offset=self.o, global_shape=g)))
+        self.units = B
+        self.l2_note = (f"inputs larger than L2 ({ws >> 20} MiB/rank)" if self.B == 1 else
+                        f"{self.B} rotating buffer sets ({self.B * ws >> 20} MiB >= 2x L2)")
 
     def step(self, i):
-        return self.M.mw_run(self.ctx, self.tree, self.arglist(0))
+        return self.M.mw_run(self.ctx, self.tree, self.arglist(i % self.B))
 
     def roof_bytes(self, cls, launches, steps, res):
         # the fused FFT -> IFFT reads and writes each transform once: 2 x 512 KiB

@@ -15,13 +15,16 @@ namespace {
 constexpr int kNbTile = 256;
 constexpr int kNbPairs = 3;               // body pairs per thread (6 bodies; 2 and 4 measured slower)
 constexpr int kNbPer = 2 * kNbPairs;
-// The source range is cut into kNbSeg fixed segments (tile-aligned thirds):
-// work items are (body block, segment), so 2^20 bodies make 3072 items for
-// 444 resident CTAs (6.9 waves, 99 % busy) instead of 1024 (2.3 waves, 77 %).
-// Each item writes its fp64 partial; k_nbody_fin sums the segments in order.
-// The split depends only on N, so results stay identical for every
-// distribution of the bodies.
-constexpr int kNbSeg = 3;
+// The source range is cut into kNbSeg fixed tile-aligned segments: work
+// items are (body block, segment), so the items of a partition fill the
+// resident CTAs in many waves whatever its share — 2^20 bodies make 32784
+// items for 296 resident CTAs (2 per SM: 111 waves), a 1/8 share 4128 (14
+// waves, 99.6 % of the last one busy); with 3 segments a 1/2 share left its
+// 4th wave half empty (1.75x instead of 2x the whole step's rate).  Each item
+// writes its fp64 partial; k_nbody_fin sums the segments in order.  The split
+// depends only on N, so results stay identical for every distribution of the
+// bodies.
+constexpr int kNbSeg = 48;
 
 // Packed FP32x2 arithmetic (sm_100a FADD2/FMUL2/FFMA2): one instruction
 // updates a pair of bodies; scalar operands are broadcast by ptxas.

@@ -1153,8 +1153,12 @@ mw_status run_nbody(RunCtx& R, const Step& st, const mw_arg& pos, const mw_arg& 
 
 // FFT chains (NEXT-3): groups of <= 32 stages per fft_chain call, the first
 // reading src, later ones in place on dst.
-mw_status run_fft_chain(const std::vector<mw::ChainOp>& ops, const float* src, float* dst,
-                        int64_t nfft, int log2n, const mwk::Launch& L) {
+mw_status run_fft_chain(mw_ctx* c, const std::vector<mw::ChainOp>& ops, const float* src, float* dst,
+                        int64_t nfft, int log2n, mwk::Launch L) {
+    if (const size_t wb = mwk::fft_work_bytes(nfft, log2n)) {
+        MW_OK_OR_RETURN(scratch(c, "fft_work", wb, L.stream, &L.work));
+        L.work_bytes = wb;
+    }
     for (size_t g = 0; g < ops.size(); g += 32) {
         const int n = (int)std::min<size_t>(32, ops.size() - g);
         uint32_t inv = 0;
@@ -1246,7 +1250,7 @@ mw_status run_staged(RunCtx& R, const Step& st, int in_kind, const mw_arg* args)
                                                        : MW_KC_SAXPY);
                 mwk::Launch L = launch_for(c, R.s, p);
                 if (st.kind == StepKind::Fft) {
-                    MW_OK_OR_RETURN(run_fft_chain(st.ops, reinterpret_cast<const float*>(d0),
+                    MW_OK_OR_RETURN(run_fft_chain(c, st.ops, reinterpret_cast<const float*>(d0),
                                                   reinterpret_cast<float*>(d1), n, (int)st.ops[0].ia, L));
                 } else if (st.kind == StepKind::Rgba) {
                     MW_OK_OR_RETURN(kerr(mwk::rgba_chain(rgba[0], d0, d1, n, a0.shape[1], r0, L), "rgba_chain"));
@@ -1574,7 +1578,7 @@ mw_status run(mw_ctx* c, const Node* root, const mw_arg* args, int nargs, cudaSt
                 continue;
             }
             PartTimer t(c, s, p, MW_KC_FFT);
-            MW_OK_OR_RETURN(run_fft_chain(ops, at_row<const float>(args[0], R.off[p]),
+            MW_OK_OR_RETURN(run_fft_chain(c, ops, at_row<const float>(args[0], R.off[p]),
                                           at_row<float>(args[1], R.off[p]), R.len[p], (int)ops[0].ia,
                                           launch_for(c, s, p)));
         }

@@ -511,16 +511,14 @@ constexpr size_t kF4ColSmem = sizeof(float2) * (256 * kF4Pitch + 768);
 // persistent version with two tile buffers per CTA — the next tile's copies
 // landing during the current one — 0.405 vs 0.335 ms per batch: fewer CTAs
 // per SM hide less.)
+// One column tile (256 x kF4Cols, columns c0 ..) of transform f by 128
+// threads: INV = false: A + W_N^{c k2}; INV = true: A^-1 and 1/N.  Reads
+// in + f N, writes out + f N (in place when they alias).  Ends with the
+// tile's stores issued; the caller synchronises before reusing `tile`.
 template <bool INV>
-__global__ void __launch_bounds__(128) k_fft4_cols(const float2* in, float2* out, int64_t f0) {
-    extern __shared__ float4 f4_smem[];
-    float2* tile = reinterpret_cast<float2*>(f4_smem);
-    float2* tb = tile + 256 * kF4Pitch;
-    f4_tables(tb);
+__device__ __forceinline__ void f4_col_tile(const float2* in, float2* out, int64_t f, int c0, float2* tile,
+                                            const float2* tb) {
     const int tid = threadIdx.x;
-    constexpr int kTiles = 256 / kF4Cols;
-    const int64_t f = f0 + blockIdx.x / kTiles;
-    const int c0 = (blockIdx.x % kTiles) * kF4Cols;
     const float2* src = in + f * 65536 + c0;
     float2* dst = out + f * 65536 + c0;
     const int cc = tid & (kF4Cols - 1), r0 = tid / kF4Cols;
@@ -574,22 +572,31 @@ __global__ void __launch_bounds__(128) k_fft4_cols(const float2* in, float2* out
     }
 }
 
-// Row pass, fused B then B^-1 (then W_N^{-c k2}) on 32 rows per CTA (two
-// per half-warp, interleaved), in place; rows go straight to registers
-// (coalesced), the transposes through a [16][17] scratch per row.  (Staging
-// the rows through shared memory with in-place transposes, as the column
-// pass does, measured slower: 0.347 vs 0.335 ms per batch.)
-constexpr size_t kF4RowSmem = sizeof(float2) * (32 * 16 * 17 + 768);
-__global__ void __launch_bounds__(256) k_fft4_rows_fi(float2* out, int64_t f0) {
-    extern __shared__ float4 f4r_smem[];
-    float2* scr = reinterpret_cast<float2*>(f4r_smem);
-    float2* tb = scr + 32 * 16 * 17;
+// Column pass over one 256 x 16 tile (columns c0 .. c0 + 15) of transform f:
+// INV = false: A + W_N^{c k2}; INV = true: A^-1 and 1/N.  In place on `out`
+// (the input `in` on the forward pass).  128 threads, ~41 KiB: four CTAs per
+// SM overlap one another's load, compute and store phases.  (Measured: a
+// persistent version with two tile buffers per CTA — the next tile's copies
+// landing during the current one — 0.405 vs 0.335 ms per batch: fewer CTAs
+// per SM hide less; five CTAs per SM at 96 registers: 0.389 ms.)
+template <bool INV>
+__global__ void __launch_bounds__(128) k_fft4_cols(const float2* in, float2* out, int64_t f0) {
+    extern __shared__ float4 f4_smem[];
+    float2* tile = reinterpret_cast<float2*>(f4_smem);
+    float2* tb = tile + 256 * kF4Pitch;
     f4_tables(tb);
-    __syncthreads();
+    constexpr int kTiles = 256 / kF4Cols;
+    f4_col_tile<INV>(in, out, f0 + blockIdx.x / kTiles, (blockIdx.x % kTiles) * kF4Cols, tile, tb);
+}
+
+// Rows k0 .. k0 + blockDim / 8 - 1 of transform f, fused B then B^-1 (then
+// W_N^{-c k2}), two rows per half-warp (interleaved), in place; rows go
+// straight to registers (coalesced), the transposes through a [16][17]
+// scratch per row (scr: 2 * 16 * 17 float2 per half-warp).
+__device__ __forceinline__ void f4_row_block(float2* out, int64_t f, int k0, float2* scr, const float2* tb) {
     const int tid = threadIdx.x;
     const int hw = tid >> 4, l = tid & 15;
-    const int64_t f = f0 + blockIdx.x / 8;
-    const int ka = (blockIdx.x % 8) * 32 + 2 * hw, kb = ka + 1;
+    const int ka = k0 + 2 * hw, kb = ka + 1;
     float2* ra = out + f * 65536 + (int64_t)ka * 256;
     float2* rb = ra + 256;
     float2 a[16], b[16];
@@ -610,6 +617,109 @@ __global__ void __launch_bounds__(256) k_fft4_rows_fi(float2* out, int64_t f0) {
     }
 }
 
+// Row pass, 32 rows per CTA of 256 threads.  (Staging the rows through
+// shared memory with in-place transposes, as the column pass does, measured
+// slower: 0.347 vs 0.335 ms per batch; three CTAs per SM at 80 registers:
+// 0.354 ms.)
+constexpr size_t kF4RowSmem = sizeof(float2) * (32 * 16 * 17 + 768);
+__global__ void __launch_bounds__(256) k_fft4_rows_fi(float2* out, int64_t f0) {
+    extern __shared__ float4 f4r_smem[];
+    float2* scr = reinterpret_cast<float2*>(f4r_smem);
+    float2* tb = scr + 32 * 16 * 17;
+    f4_tables(tb);
+    __syncthreads();
+    f4_row_block(out, f0 + blockIdx.x / 8, (blockIdx.x % 8) * 32, scr, tb);
+}
+
+// ---- Dataflow form of the same three passes: ONE persistent launch whose
+// CTAs claim work items from an atomic ticket in an order that pipelines the
+// transforms through the passes — slot group g holds the 16 column tiles of
+// transform g, the 16 row blocks (16 rows each) of transform g - L and the
+// 16 inverse column tiles of transform g - 2L.  Without launch boundaries
+// the passes of different transforms overlap, so a batch too small to fill
+// the SMs in whole waves of each pass (a rank's share of a strong-scaled
+// batch) loses no partial-wave tails; a transform's intermediate is consumed
+// from L2.  Readiness: ctr[1 + f] counts the finished column tiles (16) then
+// row blocks (32) of transform f, released after the item's stores
+// (bar.sync, then fence + atomic by one thread), acquired by the consumer's
+// first thread before its loads.  An item waits only on items with smaller
+// tickets, all claimed by running CTAs, so the kernel cannot deadlock,
+// whatever the residency.  Same arithmetic per element as the three
+// launches: bit-identical results.
+constexpr int kF4FlowTpf = 48;   // items per transform (16 + 16 + 16)
+constexpr size_t kF4FlowSmem = sizeof(float2) * (256 * kF4Pitch + 768);   // the row scratch fits the tile
+static_assert(16 * 16 * 17 <= 256 * kF4Pitch, "row scratch of 16 rows inside the column tile");
+
+__device__ __forceinline__ int64_t f4_slots_before(int64_t g, int64_t nf, int64_t L) {
+    auto cl = [nf](int64_t v) { return v < 0 ? (int64_t)0 : v > nf ? nf : v; };
+    return cl(g) + cl(g - L) + cl(g - 2 * L);
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(128, 4) k_fft4_flow(const float2* in, float2* out, int64_t nf, int64_t L,
+                                                      unsigned* ctr) {
+    extern __shared__ float4 f4f_smem[];
+    float2* tile = reinterpret_cast<float2*>(f4f_smem);
+    float2* tb = tile + 256 * kF4Pitch;
+    __shared__ long long s_item[2];
+    f4_tables(tb);
+    const int64_t total = nf * kF4FlowTpf;
+    long long next = 0;
+    if (threadIdx.x == 0) next = (long long)atomicAdd(ctr, 1u);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const long long t = next;
+            long long kind = -1, f = 0, sub = 0;
+            if (t < total) {
+                next = (long long)atomicAdd(ctr, 1u);   // claim the next item early
+                const int64_t s = t >> 4;
+                sub = t & 15;
+                // the slot group: the largest g with slots_before(g) <= s
+                int64_t lo = 0, hi = nf + 2 * L - 1;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) >> 1;
+                    if (f4_slots_before(mid, nf, L) <= s) lo = mid;
+                    else hi = mid - 1;
+                }
+                int64_t j = s - f4_slots_before(lo, nf, L);
+                for (int q = 0; q < 3; ++q) {
+                    const int64_t g = lo - q * L;
+                    if (g < 0 || g >= nf) continue;
+                    if (j-- == 0) {
+                        kind = q;
+                        f = g;
+                        break;
+                    }
+                }
+                if (kind > 0) {   // wait for the producing pass of transform f
+                    const unsigned need = kind == 1 ? 16u : 32u;
+                    const unsigned* p = ctr + 1 + f;
+                    while (ld_acquire_u32(p) < need) __nanosleep(256);
+                }
+            }
+            s_item[0] = kind;
+            s_item[1] = (f << 4) | sub;
+        }
+        __syncthreads();
+        const long long kind = s_item[0], fs = s_item[1];
+        if (kind < 0) break;
+        const int64_t f = fs >> 4;
+        const int sub = (int)(fs & 15);
+        if (kind == 0) f4_col_tile<false>(in, out, f, sub * kF4Cols, tile, tb);
+        else if (kind == 1) f4_row_block(out, f, sub * 16, tile, tb);
+        else f4_col_tile<true>(out, out, f, sub * kF4Cols, tile, tb);
+        __syncthreads();   // every store of the item issued; the tile is free
+        if (kind < 2 && threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(ctr + 1 + f, 1u);
+        }
+    }
+}
+
 static int64_t tuning_chunk() {
     static const int64_t c = [] {
         const char* v = getenv("MW_FFT4_CHUNK");
@@ -618,7 +728,48 @@ static int64_t tuning_chunk() {
     return c;
 }
 
+static int64_t tuning_lag() {
+    static const int64_t c = [] {
+        const char* v = getenv("MW_FFT4_LAG");
+        return v ? (int64_t)atoi(v) : (int64_t)64;
+    }();
+    return c;
+}
+// largest batch the automatic form (knob value 1) runs as one dataflow launch
+static int64_t tuning_flow_max() {
+    static const int64_t c = [] {
+        const char* v = getenv("MW_FFT4_FLOW_MAX");
+        return v ? (int64_t)atoll(v) : (int64_t)256;
+    }();
+    return c;
+}
+
+// the dataflow launch: L.work holds (1 + nfft) counters, zeroed here
+cudaError_t fft4_flow(const float2* in, float2* out, int64_t nfft, const Launch& L) {
+    static int per_sm = [] {
+        cudaFuncSetAttribute(k_fft4_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4FlowSmem);
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fft4_flow, 128, kF4FlowSmem) != cudaSuccess || n < 1)
+            n = 1;
+        return n;
+    }();
+    const size_t need = (size_t)(nfft + 1) * sizeof(unsigned);
+    if (!L.work || L.work_bytes < need || nfft * kF4FlowTpf >= (int64_t)UINT32_MAX) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(L.work, 0, need, L.stream);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > nfft * kF4FlowTpf) grid = nfft * kF4FlowTpf;
+    note_launch();
+    k_fft4_flow<<<(unsigned)grid, 128, kF4FlowSmem, L.stream>>>(in, out, nfft, tuning_lag(),
+                                                                 static_cast<unsigned*>(L.work));
+    return cudaGetLastError();
+}
+
 cudaError_t fft4_fi(const float2* in, float2* out, int64_t nfft, const Launch& L) {
+    // 1: the form by batch size (one dataflow launch for batches that leave
+    // partial waves in the three launches; 2 / 3 forced)
+    const int form = L.tune[TUNE_FFT_4STEP];
+    if (form == 2 || (form == 1 && nfft <= tuning_flow_max())) return fft4_flow(in, out, nfft, L);
     static bool attr = [] {
         cudaFuncSetAttribute(k_fft4_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);
         cudaFuncSetAttribute(k_fft4_cols<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);
@@ -701,6 +852,10 @@ cudaError_t fft_prepare(cudaStream_t s) {
     e = cudaGetLastError();
     if (e == cudaSuccess) filled.insert(dev);
     return e;
+}
+
+size_t fft_work_bytes(int64_t nfft, int log2n) {
+    return log2n == 16 ? (size_t)(nfft + 1) * sizeof(unsigned) : 0;
 }
 
 cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint32_t inv, int nst,

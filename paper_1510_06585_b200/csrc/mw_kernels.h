@@ -30,6 +30,10 @@ struct Launch {
     // (mw_ctx_set_run_pipelining), so it may issue its first loads before the
     // programmatic-dependent-launch wait (its stores still follow it)
     bool dep_wait = true;
+    // per-ctx device scratch for launches that need one (the FFT dataflow
+    // path's readiness counters: fft_work_bytes)
+    void* work = nullptr;
+    size_t work_bytes = 0;
 };
 
 // ------------------------------------------------------------ fused Map chains
@@ -245,6 +249,8 @@ bool fft_supported(int log2n);   // 13..16
 cudaError_t fft_prepare(cudaStream_t s);
 cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint32_t inv, int nst,
                       const Launch& L);
+// device scratch fft_chain needs in L.work for nfft transforms of 2^log2n
+size_t fft_work_bytes(int64_t nfft, int log2n);
 unsigned long long launch_count();  // kernels launched by this library
 
 }  // namespace mwk

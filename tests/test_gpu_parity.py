@@ -790,11 +790,12 @@ def test_fft_chain_parity(log2n, dirs):
     assert torch.equal(src, dev(x))   # input untouched
 
 
-@pytest.mark.parametrize("four", [0, 1])
+@pytest.mark.parametrize("four", [0, 1, 2, 3])
 @pytest.mark.parametrize("dirs", ["FI", "FIFI", "IFI"])
 def test_fft_fused_pair_paths(four, dirs):
-    """The fused pipeline(fft, ifft) at 2^16 on both implementations — the
-    4-step 256 x 256 path (MW_TUNE_FFT_4STEP = 1, default) and one
+    """The fused pipeline(fft, ifft) at 2^16 on every implementation — the
+    4-step 256 x 256 path as three launches (MW_TUNE_FFT_4STEP = 3), as one
+    persistent dataflow launch (2), chosen by batch size (1, default) and one
     thread-block cluster per transform (0) — within the bound of the oracle,
     also inside longer chains and after an inverse leaf."""
     N, B = 1 << 16, 5
@@ -806,6 +807,32 @@ def test_fft_fused_pair_paths(four, dirs):
     run(c, _fft_tree(16, dirs), [M.arg(src), M.arg(dst)])
     _fft_check(dst.cpu().numpy(), x, dirs)
     assert torch.equal(src, dev(x))
+
+
+@pytest.mark.parametrize("B", [1, 2, 17, 40, 300])
+def test_fft_4step_dataflow_bitwise(B):
+    """The dataflow launch (MW_TUNE_FFT_4STEP = 2: work items claimed from an
+    atomic ticket, passes of a transform ordered by readiness counters) runs
+    the same arithmetic per element as the three launches (3): bit-identical
+    outputs for batches shorter and longer than the pipelining lag (64), within
+    the oracle's bound, and on a repeated run of the same ctx (the counters are
+    re-zeroed per launch)."""
+    N = 1 << 16
+    x = _fft_in(B, N, 900 + B)
+    src = dev(x)
+    ref = torch.empty_like(src)
+    c1 = ctx()
+    M.mw_ctx_set_tuning(c1, M.MW_TUNE_FFT_4STEP, 3)
+    run(c1, trees.fft_pipeline(16), [M.arg(src), M.arg(ref)])
+    c2 = ctx()
+    M.mw_ctx_set_tuning(c2, M.MW_TUNE_FFT_4STEP, 2)
+    for _ in range(2):
+        dst = torch.full_like(src, float("nan"))
+        run(c2, trees.fft_pipeline(16), [M.arg(src), M.arg(dst)])
+        assert torch.equal(dst, ref)
+    if B <= 40:
+        _fft_check(dst.cpu().numpy(), x, "FI")
+    assert torch.equal(src, dev(x))   # input untouched
 
 
 def test_fft_pipeline_partitions_bitwise_and_batch():

@@ -58,6 +58,10 @@ __device__ float2 g_tw13[16 * 512];
 __device__ float2 g_w256[256];
 __device__ float2 g_w16hi[256];
 __device__ float2 g_w16lo[256];
+// The 16 x 4096 path's tables, laid out [m][t] so a warp reads consecutive
+// entries: W_4096^(m t) and W_65536^(m t), m < 16, t < 256.
+__device__ float2 g_w4096t[16 * 256];
+__device__ float2 g_w65536t[16 * 256];
 __global__ void k_fft_tw13() {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double sn, cs;
@@ -71,6 +75,12 @@ __global__ void k_fft_tw13() {
                        : t == 1 ? 2.0 * 256.0 * e / 65536.0 : 2.0 * e / 65536.0;
         sincospi(x, &sn, &cs);
         (t == 0 ? g_w256 : t == 1 ? g_w16hi : g_w16lo)[e] = make_float2((float)cs, (float)-sn);
+    } else if (i < 16 * 512 + 3 * 256 + 2 * 4096) {
+        const int j = i - (16 * 512 + 3 * 256), q = j / 4096, mt = j % 4096;
+        const int m = mt / 256, t = mt % 256;
+        const double x = q == 0 ? 2.0 * ((m * t) % 4096) / 4096.0 : 2.0 * (m * t) / 65536.0;
+        sincospi(x, &sn, &cs);
+        (q == 0 ? g_w4096t : g_w65536t)[mt] = make_float2((float)cs, (float)-sn);
     }
 }
 
@@ -720,6 +730,132 @@ __global__ void __launch_bounds__(128, 4) k_fft4_flow(const float2* in, float2* 
     }
 }
 
+// ---- 16 x 4096 four-step path (MW_TUNE_FFT_4STEP = 4) for the fused
+// pipeline(fft, ifft) at N = 65536: n = c + 4096 r (c < 4096, r < 16),
+// k = k1 + 16 k2:
+//   A:     Y[k1][c] = sum_r x[c + 4096 r] W_16^{r k1}, times W_N^{c k1}
+//   B:     X[k1 + 16 k2] = sum_c Y'[k1][c] W_4096^{c k2}; B^-1 over k2, then
+//          times W_N^{-c k1}
+//   A^-1:  x[c + 4096 r] = (1/N) sum_k1 Z'[k1][c] W_16^{-r k1}
+// The column passes are one register DFT-16 per thread over 16 loads that
+// are coalesced across the warp (consecutive c): no shared memory at all.
+// The row pass holds one contiguous 4096-point row per CTA: DFT-4096 =
+// 16 x 256 (c = t + 256 j, k2 = m + 16 k'): a DFT-16 over j per thread t,
+// twiddle W_4096^{t m}, a transpose through shared memory, a DFT-256 over t
+// per half-warp (m = half-warp), then the inverse mirrored (spectrum never
+// leaves the registers).  Against the 256 x 256 path this halves the
+// shared-memory traffic (the 256-point column DFTs needed staged tiles).
+__device__ __forceinline__ float2 tw65536g(int e, bool inv) {
+    float2 w = cmul(__ldg(&g_w16hi[e >> 8]), __ldg(&g_w16lo[e & 255]));
+    if (inv) w.y = -w.y;
+    return w;
+}
+
+// pass A (INV = false: DFT-16 over r, times W_N^{c k1}) and pass A^-1
+// (INV = true: inverse DFT-16 over k1, times 1/N), one column per thread,
+// in place on `out` (reading `in` on the forward pass)
+template <bool INV>
+__global__ void __launch_bounds__(256) k_fft16_cols(const float2* in, float2* out, int64_t f0) {
+    const int64_t f = f0 + blockIdx.x / 16;
+    const int c = (blockIdx.x % 16) * 256 + threadIdx.x;
+    const float2* src = in + f * 65536 + c;
+    float2* dst = out + f * 65536 + c;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = src[r * 4096];
+    dft<16, INV>(v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (!INV) {
+            if (k > 0) v[k] = cmul(v[k], tw65536g((c * k) & 65535, false));
+            dst[k * 4096] = v[k];
+        } else {
+            st_cs(dst + k * 4096, make_float2(v[k].x * (1.0f / 65536.0f), v[k].y * (1.0f / 65536.0f)));
+        }
+    }
+}
+
+// DFT-256 by a half-warp: lane l holds x[l + 16 j] (j < 16) and ends with
+// X[l + 16 j]; sc is the half-warp's [16][17] scratch (dft256_hw2 for one row)
+template <bool INV>
+__device__ __forceinline__ void dft256_hw1(float2 (&a)[16], int l, float2* sc, const float2* w256) {
+    dft<16, INV>(a);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) a[k] = cmulw<INV>(a[k], w256[k * 16 + l]);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sc[k * 17 + l] = a[k];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = sc[l * 17 + j];
+    __syncwarp();
+    dft<16, INV>(a);
+}
+
+// pass B, B^-1 and W_N^{-c k1} on row k1 of transform f (one row per CTA of
+// 256 threads), in place
+constexpr int kF16Pitch = 272;   // >= 256 points of a row, and >= 16 x 17 scratch
+constexpr size_t kF16RowSmem = sizeof(float2) * (16 * kF16Pitch + 768);
+__global__ void __launch_bounds__(256) k_fft16_rows_fi(float2* out, int64_t f0) {
+    extern __shared__ float4 f16_smem[];
+    float2* S = reinterpret_cast<float2*>(f16_smem);
+    float2* tb = S + 16 * kF16Pitch;
+    const int64_t f = f0 + blockIdx.x / 16;
+    const int k1 = blockIdx.x % 16;
+    float2* row = out + f * 65536 + (int64_t)k1 * 4096;
+    const int t = threadIdx.x;
+    float2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = row[t + 256 * j];
+    f4_tables(tb);
+    __syncthreads();
+    dft<16, false>(v);   // U[t][m]
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        if (m > 0) v[m] = cmul(v[m], __ldg(&g_w4096t[m * 256 + t]));
+        S[m * kF16Pitch + t] = v[m];
+    }
+    __syncthreads();
+    const int h = t >> 4, l = t & 15;   // half-warp h: m = h
+    float2* Sh = S + h * kF16Pitch;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = Sh[l + 16 * i];
+    __syncwarp();   // the row is in registers: its storage is the scratch now
+    dft256_hw1<false>(v, l, Sh, tb);   // X[m + 16 k'], k' = l + 16 i
+    dft256_hw1<true>(v, l, Sh, tb);    // 256 U'[t][m], t = l + 16 i
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Sh[l + 16 * i] = v[i];
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        v[m] = S[m * kF16Pitch + t];
+        if (m > 0) v[m] = cmulw<true>(v[m], __ldg(&g_w4096t[m * 256 + t]));
+    }
+    dft<16, true>(v);   // 4096 Y'[t + 256 j]
+    // W_N^{-c k1}, c = t + 256 j: W_N^{t k1} (table [k1][t]) W_256^{j k1}
+    const float2 wt = __ldg(&g_w65536t[k1 * 256 + t]);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float2 w = j == 0 ? wt : cmul(wt, tb[j * 16 + k1]);   // tb[0..255]: W_256^(a b) at [a][b]
+        row[t + 256 * j] = k1 == 0 ? v[j] : cmulw<true>(v[j], w);
+    }
+}
+
+cudaError_t fft16_fi(const float2* in, float2* out, int64_t nfft, const Launch& L) {
+    static bool attr = [] {
+        cudaFuncSetAttribute(k_fft16_rows_fi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF16RowSmem);
+        return true;
+    }();
+    (void)attr;
+    const unsigned grid = (unsigned)(nfft * 16);
+    note_launch();
+    k_fft16_cols<false><<<grid, 256, 0, L.stream>>>(in, out, 0);
+    note_launch();
+    k_fft16_rows_fi<<<grid, 256, kF16RowSmem, L.stream>>>(out, 0);
+    note_launch();
+    k_fft16_cols<true><<<grid, 256, 0, L.stream>>>(out, out, 0);
+    return cudaGetLastError();
+}
+
 static int64_t tuning_chunk() {
     static const int64_t c = [] {
         const char* v = getenv("MW_FFT4_CHUNK");
@@ -769,6 +905,7 @@ cudaError_t fft4_fi(const float2* in, float2* out, int64_t nfft, const Launch& L
     // 1: the form by batch size (one dataflow launch for batches that leave
     // partial waves in the three launches; 2 / 3 forced)
     const int form = L.tune[TUNE_FFT_4STEP];
+    if (form == 4) return fft16_fi(in, out, nfft, L);
     if (form == 2 || (form == 1 && nfft <= tuning_flow_max())) return fft4_flow(in, out, nfft, L);
     static bool attr = [] {
         cudaFuncSetAttribute(k_fft4_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);
@@ -848,7 +985,7 @@ cudaError_t fft_prepare(cudaStream_t s) {
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
     if (filled.count(dev)) return cudaSuccess;
-    k_fft_tw13<<<35, 256, 0, s>>>();
+    k_fft_tw13<<<(16 * 512 + 3 * 256 + 2 * 4096 + 255) / 256, 256, 0, s>>>();
     e = cudaGetLastError();
     if (e == cudaSuccess) filled.insert(dev);
     return e;

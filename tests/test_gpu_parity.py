@@ -790,7 +790,7 @@ def test_fft_chain_parity(log2n, dirs):
     assert torch.equal(src, dev(x))   # input untouched
 
 
-@pytest.mark.parametrize("four", [0, 1, 2, 3])
+@pytest.mark.parametrize("four", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("dirs", ["FI", "FIFI", "IFI"])
 def test_fft_fused_pair_paths(four, dirs):
     """The fused pipeline(fft, ifft) at 2^16 on every implementation — the

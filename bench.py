@@ -579,7 +579,7 @@ REF_CONFIG = {
 
 KCLASS = {0: "saxpy_chain", 1: "rgba_chain (k_rgba_ns)", 2: "u8_chain / plane pack+unpack",
           3: "hysteresis stencil loop", 4: "k_nbody", 5: "k_reduce_chunks", 6: "traits",
-          7: "k_fft4 cols / rows (4-step FFT)"}
+          7: "k_fft16 cols / rows (16 x 4096 four-step FFT)"}
 
 class Fft(Workload):
     """NEXT-3: the paper's FFT benchmark: a batch of 512 KiB

@@ -448,15 +448,14 @@ enum {
                                  argument sets are pairwise independent (no write overlaps
                                  another set's buffers) are captured on up to this many
                                  parallel lanes (1, 2, 4); 1 = strictly serialized replays   */
-    MW_TUNE_FFT_4STEP = 9,    /* pipeline(fft, ifft) at N = 65536: the 4-step 256 x 256 path
-                                 as 3 = three launches (column, row, inverse column pass)
-                                 or 2 = ONE persistent dataflow launch (work items from an
-                                 atomic ticket, the passes of a transform ordered by device
-                                 readiness counters: no partial-wave tails per pass);
-                                 1 = the 4-step path, dataflow up to MW_FFT4_FLOW_MAX = 256
-                                 transforms per partition, three launches above (default);
-                                 0 = one thread-block cluster per transform (distributed
-                                 shared memory).  1, 2 and 3 are bit-identical              */
+    MW_TUNE_FFT_4STEP = 9,    /* pipeline(fft, ifft) at N = 65536 as a four-step FFT:
+                                 1 = 16 x 4096 (column DFT-16s in registers, one 4096-point
+                                 row per CTA; default), 256 x 256 as 3 = three launches
+                                 (column, row, inverse column pass) or 2 = ONE persistent
+                                 dataflow launch (work items from an atomic ticket, the
+                                 passes of a transform ordered by device readiness
+                                 counters); 0 = one thread-block cluster per transform
+                                 (distributed shared memory).  2 and 3 are bit-identical  */
     MW_TUNE_COUNT = 10
 };
 mw_status mw_ctx_set_tuning(mw_ctx* ctx, int32_t knob, int32_t value);

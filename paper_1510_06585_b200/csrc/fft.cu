@@ -6,7 +6,13 @@
 // is 512 KBytes."  Readings R23-R25: N = 65536 complex64 points
 // per FFT (2^13..2^16 accepted), forward e^{-2 pi i nk/N}, inverse with 1/N.
 //
-// B200 design.  One FFT is held on chip by a thread-block CLUSTER of
+// B200 design.  The fused pipeline(fft, ifft) at N = 65536 (the benchmark)
+// runs as a 16 x 4096 four-step FFT by default (k_fft16_*, below: three
+// launches, the column passes HBM-bound register DFT-16s, the row pass one
+// 4096-point row per CTA with forward and inverse fused); a 256 x 256
+// four-step form (k_fft4_*, three launches or one dataflow launch) and the
+// cluster kernel are kept as tuning alternatives.  Every other chain:
+// one FFT is held on chip by a thread-block CLUSTER of
 // C = N / 8192 CTAs (C in {1,2,4,8}); each CTA keeps 8192 points (64 KiB,
 // padded) in shared memory and the CTAs exchange data through distributed
 // shared memory, so one FFT moves through HBM exactly once per launch — and a
@@ -871,15 +877,6 @@ static int64_t tuning_lag() {
     }();
     return c;
 }
-// largest batch the automatic form (knob value 1) runs as one dataflow launch
-static int64_t tuning_flow_max() {
-    static const int64_t c = [] {
-        const char* v = getenv("MW_FFT4_FLOW_MAX");
-        return v ? (int64_t)atoll(v) : (int64_t)256;
-    }();
-    return c;
-}
-
 // the dataflow launch: L.work holds (1 + nfft) counters, zeroed here
 cudaError_t fft4_flow(const float2* in, float2* out, int64_t nfft, const Launch& L) {
     static int per_sm = [] {
@@ -902,11 +899,11 @@ cudaError_t fft4_flow(const float2* in, float2* out, int64_t nfft, const Launch&
 }
 
 cudaError_t fft4_fi(const float2* in, float2* out, int64_t nfft, const Launch& L) {
-    // 1: the form by batch size (one dataflow launch for batches that leave
-    // partial waves in the three launches; 2 / 3 forced)
+    // 1: 16 x 4096 (default: faster at every batch size measured, 64 .. 512
+    // transforms); 256 x 256 as 2: one dataflow launch, 3: three launches
     const int form = L.tune[TUNE_FFT_4STEP];
-    if (form == 4) return fft16_fi(in, out, nfft, L);
-    if (form == 2 || (form == 1 && nfft <= tuning_flow_max())) return fft4_flow(in, out, nfft, L);
+    if (form == 1) return fft16_fi(in, out, nfft, L);
+    if (form == 2) return fft4_flow(in, out, nfft, L);
     static bool attr = [] {
         cudaFuncSetAttribute(k_fft4_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);
         cudaFuncSetAttribute(k_fft4_cols<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);
@@ -1019,7 +1016,7 @@ cudaError_t fft_chain(const float* in, float* out, int64_t nfft, int log2n, uint
             used = 2;
         }
         cudaError_t e;
-        // the 4-step path for the fused pair at 2^16 (the slowdown injector's
+        // a four-step path for the fused pair at 2^16 (the slowdown injector's
         // clamped grids stay on the cluster path, whose clusters are persistent)
         if (mode == FFT_FI && log2n == 16 && L.tune[TUNE_FFT_4STEP] && !(L.slow > 1.0f)) {
             e = fft4_fi(src, o2, nfft, L);

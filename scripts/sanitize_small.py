@@ -1,7 +1,8 @@
 """Small runs of every kernel family for compute-sanitizer:
 memcheck / racecheck / synccheck over the TMA rings (filter, u8 chains), the
 bit-plane hysteresis kernels (one-partition cooperative loop, per-partition
-pass, fused multi-partition loop, pack/unpack), the cluster FFT, N-body and
+pass, fused multi-partition loop, pack/unpack), the cluster FFT, the
+four-step FFTs at 2^16 (16 x 4096; 256 x 256 three launches and dataflow), N-body and
 the MapReduce reduction — each checked against the oracle, so a sanitizer
 pass is also a parity pass.  Sizes are small (sanitizers are ~100x slower)."""
 import sys
@@ -70,6 +71,22 @@ dst = torch.empty_like(dev(x))
 run(c, trees.fft_pipeline(log2n), [M.arg(dev(x)), M.arg(dst)])
 err = FF.rel_l2(FF.as_complex(dst.cpu().numpy()), FF.fft_chain(FF.as_complex(x), "FI"))
 check("fft", bool(np.all(err <= FF.tolerance(N, 2))))
+# FFT at N = 65536: the 16 x 4096 four-step path (default), the 256 x 256
+# one as three launches and as the dataflow launch (ticket + readiness
+# counters; bit-identical to the three launches)
+B, N = 3, 1 << 16
+x = synth.np_f32_um11(12, 0, B * N * 2).reshape(B, N, 2)
+want = FF.fft_chain(FF.as_complex(x), "FI")
+outs = {}
+for four in (1, 3, 2):
+    c = M.mw_ctx_create(0, 0, 1, 1)
+    M.mw_ctx_set_tuning(c, M.MW_TUNE_FFT_4STEP, four)
+    dst = torch.empty_like(dev(x))
+    run(c, trees.fft_pipeline(16), [M.arg(dev(x)), M.arg(dst)])
+    outs[four] = dst.cpu().numpy()
+    err = FF.rel_l2(FF.as_complex(outs[four]), want)
+    check(f"fft 2^16 form {four}", bool(np.all(err <= FF.tolerance(N, 2))))
+check("fft 2^16 dataflow == three launches", np.array_equal(outs[2], outs[3]))
 # N-body
 pos, vel = synth.np_nbody(9, 0, 700, 2.0 ** -9)
 po, vo, _ = K.nbody_step(pos, vel, 1e-4, 1e-3)

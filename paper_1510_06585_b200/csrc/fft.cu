@@ -761,9 +761,8 @@ __device__ __forceinline__ float2 tw65536g(int e, bool inv) {
 // (INV = true: inverse DFT-16 over k1, times 1/N), one column per thread,
 // in place on `out` (reading `in` on the forward pass)
 template <bool INV>
-__global__ void __launch_bounds__(256) k_fft16_cols(const float2* in, float2* out, int64_t f0) {
-    const int64_t f = f0 + blockIdx.x / 16;
-    const int c = (blockIdx.x % 16) * 256 + threadIdx.x;
+__device__ __forceinline__ void f16_col(const float2* in, float2* out, int64_t f, int b) {
+    const int c = b * 256 + threadIdx.x;
     const float2* src = in + f * 65536 + c;
     float2* dst = out + f * 65536 + c;
     float2 v[16];
@@ -779,6 +778,10 @@ __global__ void __launch_bounds__(256) k_fft16_cols(const float2* in, float2* ou
             st_cs(dst + k * 4096, make_float2(v[k].x * (1.0f / 65536.0f), v[k].y * (1.0f / 65536.0f)));
         }
     }
+}
+template <bool INV>
+__global__ void __launch_bounds__(256) k_fft16_cols(const float2* in, float2* out, int64_t f0) {
+    f16_col<INV>(in, out, f0 + blockIdx.x / 16, blockIdx.x % 16);
 }
 
 // DFT-256 by a half-warp: lane l holds x[l + 16 j] (j < 16) and ends with
@@ -801,19 +804,13 @@ __device__ __forceinline__ void dft256_hw1(float2 (&a)[16], int l, float2* sc, c
 // 256 threads), in place
 constexpr int kF16Pitch = 272;   // >= 256 points of a row, and >= 16 x 17 scratch
 constexpr size_t kF16RowSmem = sizeof(float2) * (16 * kF16Pitch + 768);
-__global__ void __launch_bounds__(256) k_fft16_rows_fi(float2* out, int64_t f0) {
-    extern __shared__ float4 f16_smem[];
-    float2* S = reinterpret_cast<float2*>(f16_smem);
-    float2* tb = S + 16 * kF16Pitch;
-    const int64_t f = f0 + blockIdx.x / 16;
-    const int k1 = blockIdx.x % 16;
+// (S: 16 x kF16Pitch float2; tb: the W_256 table, filled and synchronised)
+__device__ __forceinline__ void f16_row(float2* out, int64_t f, int k1, float2* S, const float2* tb) {
     float2* row = out + f * 65536 + (int64_t)k1 * 4096;
     const int t = threadIdx.x;
     float2 v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = row[t + 256 * j];
-    f4_tables(tb);
-    __syncthreads();
     dft<16, false>(v);   // U[t][m]
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
@@ -843,6 +840,80 @@ __global__ void __launch_bounds__(256) k_fft16_rows_fi(float2* out, int64_t f0) 
     for (int j = 0; j < 16; ++j) {
         const float2 w = j == 0 ? wt : cmul(wt, tb[j * 16 + k1]);   // tb[0..255]: W_256^(a b) at [a][b]
         row[t + 256 * j] = k1 == 0 ? v[j] : cmulw<true>(v[j], w);
+    }
+}
+__global__ void __launch_bounds__(256) k_fft16_rows_fi(float2* out, int64_t f0) {
+    extern __shared__ float4 f16_smem[];
+    float2* S = reinterpret_cast<float2*>(f16_smem);
+    float2* tb = S + 16 * kF16Pitch;
+    f4_tables(tb);
+    __syncthreads();
+    f16_row(out, f0 + blockIdx.x / 16, blockIdx.x % 16, S, tb);
+}
+
+// The 16 x 4096 passes as ONE persistent dataflow launch (the scheme of
+// k_fft4_flow: tickets, slot groups g = A of g, B of g - L, A^-1 of g - 2L,
+// readiness counters per transform; 16 column blocks of 256 columns, 16
+// rows, 16 inverse column blocks per transform): the intermediate is
+// consumed from L2, so HBM sees the input once and the output once and the
+// HBM-bound column passes overlap the SM-bound row pass.  Same arithmetic
+// per element as k_fft16_*: bit-identical results.
+__global__ void __launch_bounds__(256, 3) k_fft16_flow(const float2* in, float2* out, int64_t nf, int64_t L,
+                                                       unsigned* ctr) {
+    extern __shared__ float4 f16f_smem[];
+    float2* S = reinterpret_cast<float2*>(f16f_smem);
+    float2* tb = S + 16 * kF16Pitch;
+    __shared__ long long s_item[2];
+    f4_tables(tb);
+    const int64_t total = nf * kF4FlowTpf;
+    long long next = 0;
+    if (threadIdx.x == 0) next = (long long)atomicAdd(ctr, 1u);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const long long t = next;
+            long long kind = -1, f = 0, sub = 0;
+            if (t < total) {
+                next = (long long)atomicAdd(ctr, 1u);   // claim the next item early
+                const int64_t s = t >> 4;
+                sub = t & 15;
+                int64_t lo = 0, hi = nf + 2 * L - 1;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) >> 1;
+                    if (f4_slots_before(mid, nf, L) <= s) lo = mid;
+                    else hi = mid - 1;
+                }
+                int64_t j = s - f4_slots_before(lo, nf, L);
+                for (int q = 0; q < 3; ++q) {
+                    const int64_t g = lo - q * L;
+                    if (g < 0 || g >= nf) continue;
+                    if (j-- == 0) {
+                        kind = q;
+                        f = g;
+                        break;
+                    }
+                }
+                if (kind > 0) {   // wait for the producing pass of transform f
+                    const unsigned need = kind == 1 ? 16u : 32u;
+                    const unsigned* p = ctr + 1 + f;
+                    while (ld_acquire_u32(p) < need) __nanosleep(256);
+                }
+            }
+            s_item[0] = kind;
+            s_item[1] = (f << 4) | sub;
+        }
+        __syncthreads();
+        const long long kind = s_item[0], fs = s_item[1];
+        if (kind < 0) break;
+        const int64_t f = fs >> 4;
+        const int sub = (int)(fs & 15);
+        if (kind == 0) f16_col<false>(in, out, f, sub);
+        else if (kind == 1) f16_row(out, f, sub, S, tb);
+        else f16_col<true>(out, out, f, sub);
+        __syncthreads();   // every store of the item issued; S is free
+        if (kind < 2 && threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(ctr + 1 + f, 1u);
+        }
     }
 }
 
@@ -898,11 +969,47 @@ cudaError_t fft4_flow(const float2* in, float2* out, int64_t nfft, const Launch&
     return cudaGetLastError();
 }
 
+// The 16 x 4096 dataflow launch: L.work holds (1 + nfft) counters, zeroed
+// here.  Measured on the 512-transform batch: 0.291 ms at lag 32-48 against
+// 0.316 ms for the three launches on the same box (lag 24: 0.296, 64: 0.300);
+// below ~256 transforms the three launches are as fast or faster (128: 78
+// vs 83 us), hence kF16FlowMin for the default form.
+constexpr int64_t kF16FlowMin = 256;
+static int64_t tuning_lag16() {
+    static const int64_t c = [] {
+        const char* v = getenv("MW_FFT4_LAG");
+        return v ? (int64_t)atoi(v) : (int64_t)32;
+    }();
+    return c;
+}
+cudaError_t fft16_flow(const float2* in, float2* out, int64_t nfft, const Launch& L) {
+    static int per_sm = [] {
+        cudaFuncSetAttribute(k_fft16_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF16RowSmem);
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fft16_flow, 256, kF16RowSmem) != cudaSuccess || n < 1)
+            n = 1;
+        return n;
+    }();
+    const size_t need = (size_t)(nfft + 1) * sizeof(unsigned);
+    if (!L.work || L.work_bytes < need || nfft * kF4FlowTpf >= (int64_t)UINT32_MAX) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(L.work, 0, need, L.stream);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > nfft * kF4FlowTpf) grid = nfft * kF4FlowTpf;
+    note_launch();
+    k_fft16_flow<<<(unsigned)grid, 256, kF16RowSmem, L.stream>>>(in, out, nfft, tuning_lag16(),
+                                                                  static_cast<unsigned*>(L.work));
+    return cudaGetLastError();
+}
+
 cudaError_t fft4_fi(const float2* in, float2* out, int64_t nfft, const Launch& L) {
-    // 1: 16 x 4096 (default: faster at every batch size measured, 64 .. 512
-    // transforms); 256 x 256 as 2: one dataflow launch, 3: three launches
+    // 16 x 4096 as 1 (default: the dataflow launch from kF16FlowMin
+    // transforms per partition, three launches below), 4 (dataflow launch)
+    // or 5 (three launches); 256 x 256 as 2 (dataflow launch) or 3 (three
+    // launches) — the 16 x 4096 forms are faster at every batch size measured
     const int form = L.tune[TUNE_FFT_4STEP];
-    if (form == 1) return fft16_fi(in, out, nfft, L);
+    if (form == 5 || (form == 1 && nfft < kF16FlowMin)) return fft16_fi(in, out, nfft, L);
+    if (form == 1 || form == 4) return fft16_flow(in, out, nfft, L);
     if (form == 2) return fft4_flow(in, out, nfft, L);
     static bool attr = [] {
         cudaFuncSetAttribute(k_fft4_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);

@@ -790,12 +790,13 @@ def test_fft_chain_parity(log2n, dirs):
     assert torch.equal(src, dev(x))   # input untouched
 
 
-@pytest.mark.parametrize("four", [0, 1, 2, 3])
+@pytest.mark.parametrize("four", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("dirs", ["FI", "FIFI", "IFI"])
 def test_fft_fused_pair_paths(four, dirs):
     """The fused pipeline(fft, ifft) at 2^16 on every implementation — the
-    16 x 4096 four-step path (MW_TUNE_FFT_4STEP = 1, default), the 256 x 256
-    one as three launches (3) and as one persistent dataflow launch (2), and
+    16 x 4096 four-step path as one persistent dataflow launch (4), as three
+    launches (5) and chosen by batch size (MW_TUNE_FFT_4STEP = 1, default),
+    the 256 x 256 one as three launches (3) and as a dataflow launch (2), and
     one thread-block cluster per transform (0) — within the bound of the
     oracle, also inside longer chains and after an inverse leaf."""
     N, B = 1 << 16, 5
@@ -809,23 +810,25 @@ def test_fft_fused_pair_paths(four, dirs):
     assert torch.equal(src, dev(x))
 
 
+@pytest.mark.parametrize("launches,flow", [(3, 2), (5, 4)])
 @pytest.mark.parametrize("B", [1, 2, 17, 40, 300])
-def test_fft_4step_dataflow_bitwise(B):
-    """The dataflow launch (MW_TUNE_FFT_4STEP = 2: work items claimed from an
-    atomic ticket, passes of a transform ordered by readiness counters) runs
-    the same arithmetic per element as the three launches (3): bit-identical
-    outputs for batches shorter and longer than the pipelining lag (64), within
-    the oracle's bound, and on a repeated run of the same ctx (the counters are
-    re-zeroed per launch)."""
+def test_fft_4step_dataflow_bitwise(B, launches, flow):
+    """The dataflow launches (MW_TUNE_FFT_4STEP = 2 for 256 x 256, 4 for
+    16 x 4096: work items claimed from an atomic ticket, passes of a
+    transform ordered by readiness counters) run the same arithmetic per
+    element as the three launches of the same decomposition (3, 5):
+    bit-identical outputs for batches shorter and longer than the pipelining
+    lag (64), within the oracle's bound, and on a repeated run of the same
+    ctx (the counters are re-zeroed per launch)."""
     N = 1 << 16
     x = _fft_in(B, N, 900 + B)
     src = dev(x)
     ref = torch.empty_like(src)
     c1 = ctx()
-    M.mw_ctx_set_tuning(c1, M.MW_TUNE_FFT_4STEP, 3)
+    M.mw_ctx_set_tuning(c1, M.MW_TUNE_FFT_4STEP, launches)
     run(c1, trees.fft_pipeline(16), [M.arg(src), M.arg(ref)])
     c2 = ctx()
-    M.mw_ctx_set_tuning(c2, M.MW_TUNE_FFT_4STEP, 2)
+    M.mw_ctx_set_tuning(c2, M.MW_TUNE_FFT_4STEP, flow)
     for _ in range(2):
         dst = torch.full_like(src, float("nan"))
         run(c2, trees.fft_pipeline(16), [M.arg(src), M.arg(dst)])

@@ -426,11 +426,12 @@ __global__ void __launch_bounds__(FT, 2) k_fft(const float2* in, float2* out, in
 //   A (columns):  Y[k2][c] = sum_r x[c + 256 r] W_256^{r k2}, then x W_N^{c k2}
 //   B (rows):     X[k2 + 256 k1] = sum_c Y'[k2][c] W_256^{c k1}
 // and the inverse mirrored: B^-1 over k1 -> Z'[k2][c], x W_N^{-c k2}, A^-1
-// over k2 -> x[c + 256 r] (1/N).  Three launches per chunk of transforms —
-// A, then B with B^-1 fused (the spectrum never leaves the registers), then
-// A^-1 — each in place on the output buffer, which holds the intermediate:
-// a chunk (64 transforms = 32 MiB) stays in L2 between the launches, so HBM
-// sees one read of the input and one write of the output.  No clusters, no
+// over k2 -> x[c + 256 r] (1/N).  Three launches per chunk of transforms
+// (MW_FFT4_CHUNK, default the whole batch) — A, then B with B^-1 fused (the
+// spectrum never leaves the registers), then A^-1 — each in place on the
+// output buffer, which holds the intermediate (a batch larger than L2
+// round-trips it through HBM once per pass; k_fft4_flow keeps it in L2
+// instead).  No clusters, no
 // distributed shared memory: every 256-point DFT belongs to one half-warp
 // (16 points per lane, two radix-16 register DFTs and one shared-memory
 // transpose), so each SM keeps many independent DFTs in flight.

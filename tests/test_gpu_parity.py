@@ -891,8 +891,13 @@ def test_fft_edge_cases():
         run(c, trees.fft_pipeline(14), [M.arg(src), M.arg(dst)])
 
 
-def test_fft_host_staged_and_graph():
-    log2n, B = 16, 40
+@pytest.mark.parametrize("B", [40, 300])
+def test_fft_host_staged_and_graph(B):
+    """Host-staged runs and a captured graph (replayed twice: the dataflow
+    launch's readiness counters are re-zeroed by the captured memset) equal
+    the device run — B = 300 takes the 16 x 4096 dataflow launch on the
+    device and in the graph, three launches per staged chunk."""
+    log2n = 16
     x = _fft_in(B, 1 << log2n, 3)
     src = dev(x)
     ref = torch.empty_like(src)
@@ -906,9 +911,11 @@ def test_fft_host_staged_and_graph():
     with torch.cuda.stream(s):
         out = torch.empty_like(src)
         g = M.mw_graph_capture(c, trees.fft_pipeline(log2n), [M.arg(src), M.arg(out)], s)
-        g.launch(s)
-        s.synchronize()
-    assert torch.equal(out, ref)
+        for _ in range(2):
+            out.fill_(float("nan"))
+            g.launch(s)
+            s.synchronize()
+            assert torch.equal(out, ref)
 
 
 # ----------------------------------------------------------------- NEXT-4 variants

@@ -911,8 +911,10 @@ __global__ void __launch_bounds__(256, 3) k_fft16_flow(const float2* in, float2*
         else if (kind == 1) f16_row(out, f, sub, S, tb);
         else f16_col<true>(out, out, f, sub);
         __syncthreads();   // every store of the item issued; S is free
-        if (kind < 2 && threadIdx.x == 0) {
-            __threadfence();
+        // release by the last warp while thread 0 claims and waits for the
+        // next item: the fence no longer sits on the CTA's critical path
+        if (kind < 2 && threadIdx.x == blockDim.x - 32) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
             atomicAdd(ctr + 1 + f, 1u);
         }
     }

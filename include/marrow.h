@@ -450,15 +450,13 @@ enum {
                                  parallel lanes (1, 2, 4); 1 = strictly serialized replays   */
     MW_TUNE_FFT_4STEP = 9,    /* pipeline(fft, ifft) at N = 65536 as a four-step FFT,
                                  16 x 4096 (column DFT-16s in registers, one 4096-point
-                                 row per CTA) as 4 = ONE persistent dataflow launch (work
+                                 row per CTA) as 1 = ONE persistent dataflow launch (work
                                  items from an atomic ticket, the passes of a transform
                                  ordered by device readiness counters, the intermediate
-                                 consumed from L2) or 5 = three launches; 1 = 16 x 4096,
-                                 the dataflow launch from 256 transforms per partition,
-                                 three launches below (default); 256 x 256 as 2 (dataflow
-                                 launch) or 3 (three launches); 0 = one thread-block
-                                 cluster per transform (distributed shared memory).  4 and
-                                 5 are bit-identical, so are 2 and 3                        */
+                                 consumed from L2; default) or 4 = three launches;
+                                 256 x 256 as 2 (dataflow launch) or 3 (three launches);
+                                 0 = one thread-block cluster per transform (distributed
+                                 shared memory).  1 and 4 are bit-identical, so are 2 and 3 */
     MW_TUNE_COUNT = 10
 };
 mw_status mw_ctx_set_tuning(mw_ctx* ctx, int32_t knob, int32_t value);

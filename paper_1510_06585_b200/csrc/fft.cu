@@ -730,8 +730,9 @@ __global__ void __launch_bounds__(128, 4) k_fft4_flow(const float2* in, float2* 
         else if (kind == 1) f4_row_block(out, f, sub * 16, tile, tb);
         else f4_col_tile<true>(out, out, f, sub * kF4Cols, tile, tb);
         __syncthreads();   // every store of the item issued; the tile is free
-        if (kind < 2 && threadIdx.x == 0) {
-            __threadfence();
+        // release by the last warp, overlapping thread 0's claim and wait
+        if (kind < 2 && threadIdx.x == blockDim.x - 32) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
             atomicAdd(ctr + 1 + f, 1u);
         }
     }
@@ -973,11 +974,9 @@ cudaError_t fft4_flow(const float2* in, float2* out, int64_t nfft, const Launch&
 }
 
 // The 16 x 4096 dataflow launch: L.work holds (1 + nfft) counters, zeroed
-// here.  Measured on the 512-transform batch: 0.291 ms at lag 32-48 against
-// 0.316 ms for the three launches on the same box (lag 24: 0.296, 64: 0.300);
-// below ~256 transforms the three launches are as fast or faster (128: 78
-// vs 83 us), hence kF16FlowMin for the default form.
-constexpr int64_t kF16FlowMin = 256;
+// here.  Measured on the 512-transform batch: 0.273 ms at lag 32 against
+// 0.315 ms for the three launches on the same box (lag 24 and 64 slower);
+// 256 / 128 / 64 transforms: 146 / 82 / 47 us against 163 / 83 / 48 us.
 static int64_t tuning_lag16() {
     static const int64_t c = [] {
         const char* v = getenv("MW_FFT4_LAG");
@@ -1006,13 +1005,13 @@ cudaError_t fft16_flow(const float2* in, float2* out, int64_t nfft, const Launch
 }
 
 cudaError_t fft4_fi(const float2* in, float2* out, int64_t nfft, const Launch& L) {
-    // 16 x 4096 as 1 (default: the dataflow launch from kF16FlowMin
-    // transforms per partition, three launches below), 4 (dataflow launch)
-    // or 5 (three launches); 256 x 256 as 2 (dataflow launch) or 3 (three
-    // launches) — the 16 x 4096 forms are faster at every batch size measured
+    // 16 x 4096 as 1 (one dataflow launch, default) or 4 (three launches);
+    // 256 x 256 as 2 (dataflow launch) or 3 (three launches) — the 16 x 4096
+    // forms are faster at every batch size measured, its dataflow launch as
+    // fast as its three launches from 64 transforms and faster from 256
     const int form = L.tune[TUNE_FFT_4STEP];
-    if (form == 5 || (form == 1 && nfft < kF16FlowMin)) return fft16_fi(in, out, nfft, L);
-    if (form == 1 || form == 4) return fft16_flow(in, out, nfft, L);
+    if (form == 1) return fft16_flow(in, out, nfft, L);
+    if (form == 4) return fft16_fi(in, out, nfft, L);
     if (form == 2) return fft4_flow(in, out, nfft, L);
     static bool attr = [] {
         cudaFuncSetAttribute(k_fft4_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4ColSmem);

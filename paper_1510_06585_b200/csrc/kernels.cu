@@ -55,7 +55,7 @@ bool tune_valid(int knob, int v) {
         case TUNE_U8_TMA: return v == 0 || v == 1;
         case TUNE_HYST_FUSED: return v == 0 || v == 1;
         case TUNE_GRAPH_LANES: return v == 1 || v == 2 || v == 4;
-        case TUNE_FFT_4STEP: return v >= 0 && v <= 5;
+        case TUNE_FFT_4STEP: return v >= 0 && v <= 4;
     }
     return false;
 }

@@ -267,7 +267,7 @@ std::vector<std::vector<Setting>> config_dims(const mw_ctx* c, const std::vector
         if (c->ppr > 1) ordered(mwk::TUNE_HYST_FUSED, {1, 0});
     }
     if (nbody) ordered(mwk::TUNE_NBODY_SPLIT, {0, 1});
-    if (fft) ordered(mwk::TUNE_FFT_4STEP, {1, 4, 5, 3, 2, 0});
+    if (fft) ordered(mwk::TUNE_FFT_4STEP, {1, 4, 2, 3, 0});
     return dims;
 }
 

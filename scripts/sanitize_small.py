@@ -71,14 +71,15 @@ dst = torch.empty_like(dev(x))
 run(c, trees.fft_pipeline(log2n), [M.arg(dev(x)), M.arg(dst)])
 err = FF.rel_l2(FF.as_complex(dst.cpu().numpy()), FF.fft_chain(FF.as_complex(x), "FI"))
 check("fft", bool(np.all(err <= FF.tolerance(N, 2))))
-# FFT at N = 65536: the 16 x 4096 four-step path (default), the 256 x 256
-# one as three launches and as the dataflow launch (ticket + readiness
-# counters; bit-identical to the three launches)
+# FFT at N = 65536: the 16 x 4096 four-step path as its dataflow launch
+# (default) and as three launches, the 256 x 256 one as three launches and
+# as the dataflow launch (ticket + readiness counters; each dataflow launch
+# bit-identical to the three launches of its decomposition)
 B, N = 3, 1 << 16
 x = synth.np_f32_um11(12, 0, B * N * 2).reshape(B, N, 2)
 want = FF.fft_chain(FF.as_complex(x), "FI")
 outs = {}
-for four in (1, 3, 2):
+for four in (1, 4, 3, 2):
     c = M.mw_ctx_create(0, 0, 1, 1)
     M.mw_ctx_set_tuning(c, M.MW_TUNE_FFT_4STEP, four)
     dst = torch.empty_like(dev(x))
@@ -86,7 +87,7 @@ for four in (1, 3, 2):
     outs[four] = dst.cpu().numpy()
     err = FF.rel_l2(FF.as_complex(outs[four]), want)
     check(f"fft 2^16 form {four}", bool(np.all(err <= FF.tolerance(N, 2))))
-check("fft 2^16 dataflow == three launches", np.array_equal(outs[2], outs[3]))
+check("fft 2^16 dataflow == three launches", np.array_equal(outs[2], outs[3]) and np.array_equal(outs[1], outs[4]))
 # N-body
 pos, vel = synth.np_nbody(9, 0, 700, 2.0 ** -9)
 po, vo, _ = K.nbody_step(pos, vel, 1e-4, 1e-3)

@@ -891,6 +891,25 @@ def test_fft_edge_cases():
         run(c, trees.fft_pipeline(14), [M.arg(src), M.arg(dst)])
 
 
+@pytest.mark.parametrize("four", [1, 2, 3, 4])
+def test_fft_2p16_edge_cases(four):
+    """The four-step forms at 2^16: an empty batch, one FFT on three
+    partitions (two of them empty), loop_for(pipeline(fft, ifft), 3) (three
+    fused pairs, each a dataflow launch or three launches in place on the
+    output)."""
+    c = ctx(3, [0.0, 1.0, 0.0])
+    M.mw_ctx_set_tuning(c, M.MW_TUNE_FFT_4STEP, four)
+    e = torch.empty((0, 1 << 16, 2), dtype=torch.float32, device=DEV)
+    run(c, trees.fft_pipeline(16), [M.arg(e), M.arg(torch.empty_like(e))])
+    x = _fft_in(1, 1 << 16, 21)
+    src = dev(x)
+    dst = torch.empty_like(src)
+    run(c, trees.fft_pipeline(16), [M.arg(src), M.arg(dst)])
+    _fft_check(dst.cpu().numpy(), x, "FI")
+    run(c, M.mw_loop_for(trees.fft_pipeline(16), 3), [M.arg(src), M.arg(dst)])
+    _fft_check(dst.cpu().numpy(), x, "FIFIFI")
+
+
 @pytest.mark.parametrize("B", [40, 300])
 def test_fft_host_staged_and_graph(B):
     """Host-staged runs (chunks of the batch) and a captured graph (replayed

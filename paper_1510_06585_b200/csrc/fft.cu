@@ -730,11 +730,10 @@ __global__ void __launch_bounds__(128, 4) k_fft4_flow(const float2* in, float2* 
         else if (kind == 1) f4_row_block(out, f, sub * 16, tile, tb);
         else f4_col_tile<true>(out, out, f, sub * kF4Cols, tile, tb);
         __syncthreads();   // every store of the item issued; the tile is free
-        // release by the last warp, overlapping thread 0's claim and wait
-        if (kind < 2 && threadIdx.x == blockDim.x - 32) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            atomicAdd(ctr + 1 + f, 1u);
-        }
+        // release by the last warp, overlapping thread 0's claim and wait (a
+        // release RMW: unlike a fence it does not invalidate the SM's L1)
+        if (kind < 2 && threadIdx.x == blockDim.x - 32)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + 1 + f) : "memory");
     }
 }
 
@@ -913,11 +912,10 @@ __global__ void __launch_bounds__(256, 3) k_fft16_flow(const float2* in, float2*
         else f16_col<true>(out, out, f, sub);
         __syncthreads();   // every store of the item issued; S is free
         // release by the last warp while thread 0 claims and waits for the
-        // next item: the fence no longer sits on the CTA's critical path
-        if (kind < 2 && threadIdx.x == blockDim.x - 32) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            atomicAdd(ctr + 1 + f, 1u);
-        }
+        // next item (off the CTA's critical path), as a release RMW: unlike a
+        // fence it does not invalidate the SM's L1
+        if (kind < 2 && threadIdx.x == blockDim.x - 32)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + 1 + f) : "memory");
     }
 }
 

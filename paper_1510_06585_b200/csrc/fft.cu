@@ -977,7 +977,7 @@ cudaError_t fft4_flow(const float2* in, float2* out, int64_t nfft, const Launch&
 // 256 / 128 / 64 transforms: 146 / 82 / 47 us against 163 / 83 / 48 us.
 static int64_t tuning_lag16() {
     static const int64_t c = [] {
-        const char* v = getenv("MW_FFT4_LAG");
+        const char* v = getenv("MW_FFT16_LAG");
         return v ? (int64_t)atoi(v) : (int64_t)32;
     }();
     return c;

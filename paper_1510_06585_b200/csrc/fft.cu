@@ -671,6 +671,27 @@ __device__ __forceinline__ int64_t f4_slots_before(int64_t g, int64_t nf, int64_
     auto cl = [nf](int64_t v) { return v < 0 ? (int64_t)0 : v > nf ? nf : v; };
     return cl(g) + cl(g - L) + cl(g - 2 * L);
 }
+// the slot group of slot s: the largest g with slots_before(g) <= s.  For
+// nf >= 2L, slots_before is linear on [0, L), [L, 2L), [2L, nf), [nf, nf + L)
+// and [nf + L, nf + 2L) with slopes 1, 2, 3, 2, 1 — solved directly (checked
+// against the binary search for every slot of nf < 1000, L <= 64); a binary
+// search otherwise
+__device__ __forceinline__ int64_t f4_slot_group(int64_t s, int64_t nf, int64_t L) {
+    if (nf >= 2 * L) {
+        if (s < L) return s;
+        if (s < 3 * L) return (s + L) >> 1;
+        if (s < 3 * nf - 3 * L) return (s + 3 * L) / 3;
+        if (s < 3 * nf - L) return (s - nf + 3 * L) >> 1;
+        return s - 2 * nf + 2 * L;
+    }
+    int64_t lo = 0, hi = nf + 2 * L - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (f4_slots_before(mid, nf, L) <= s) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -695,13 +716,7 @@ __global__ void __launch_bounds__(128, 4) k_fft4_flow(const float2* in, float2* 
                 next = (long long)atomicAdd(ctr, 1u);   // claim the next item early
                 const int64_t s = t >> 4;
                 sub = t & 15;
-                // the slot group: the largest g with slots_before(g) <= s
-                int64_t lo = 0, hi = nf + 2 * L - 1;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi + 1) >> 1;
-                    if (f4_slots_before(mid, nf, L) <= s) lo = mid;
-                    else hi = mid - 1;
-                }
+                const int64_t lo = f4_slot_group(s, nf, L);
                 int64_t j = s - f4_slots_before(lo, nf, L);
                 for (int q = 0; q < 3; ++q) {
                     const int64_t g = lo - q * L;
@@ -877,12 +892,7 @@ __global__ void __launch_bounds__(256, 3) k_fft16_flow(const float2* in, float2*
                 next = (long long)atomicAdd(ctr, 1u);   // claim the next item early
                 const int64_t s = t >> 4;
                 sub = t & 15;
-                int64_t lo = 0, hi = nf + 2 * L - 1;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi + 1) >> 1;
-                    if (f4_slots_before(mid, nf, L) <= s) lo = mid;
-                    else hi = mid - 1;
-                }
+                const int64_t lo = f4_slot_group(s, nf, L);
                 int64_t j = s - f4_slots_before(lo, nf, L);
                 for (int q = 0; q < 3; ++q) {
                     const int64_t g = lo - q * L;

@@ -982,13 +982,14 @@ cudaError_t fft4_flow(const float2* in, float2* out, int64_t nfft, const Launch&
 }
 
 // The 16 x 4096 dataflow launch: L.work holds (1 + nfft) counters, zeroed
-// here.  Measured on the 512-transform batch: 0.273 ms at lag 32 against
-// 0.315 ms for the three launches on the same box (lag 24 and 64 slower);
+// here.  Measured on the 512-transform batch: 0.258 ms at lag 40 against
+// 0.315 ms for the three launches on the same box (lag 24 / 32 / 48: 0.274 /
+// 0.262 / 0.2585);
 // 256 / 128 / 64 transforms: 146 / 82 / 47 us against 163 / 83 / 48 us.
 static int64_t tuning_lag16() {
     static const int64_t c = [] {
         const char* v = getenv("MW_FFT16_LAG");
-        return v ? (int64_t)atoi(v) : (int64_t)32;
+        return v ? (int64_t)atoi(v) : (int64_t)40;
     }();
     return c;
 }
